@@ -1,0 +1,547 @@
+// ref_tool — TEST INFRASTRUCTURE (oracle).  Drives the UNMODIFIED reference
+// library (oracle/_ref/libadc.a, built from /root/reference/proj/src by
+// oracle/Makefile) through its own public API to
+//   * print the generated gradients the B200 kernels transcribe,
+//   * produce golden input/output vectors for the parity tests,
+//   * time the reference CPU path on the host cores (bench.py --impl reference
+//     and the cpu_baseline leg).
+// Only tests/, __graft_entry__.smoke() and bench.py's reference legs run it.
+//
+// Binary I/O: raw little-endian float64 arrays, concatenated, sizes given on
+// the command line.  Timing and summaries are printed as one JSON line.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <iostream>
+#include <random>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "adc/eval.hpp"
+#include "adc/fit.hpp"
+#include "adc/launch.hpp"
+#include "adc/parser.hpp"
+#include "adc/printer.hpp"
+#include "adc/tooling.hpp"
+#include "adc/transform.hpp"
+
+#include "corpus_embed.inc"
+
+using namespace adc;
+using clk = std::chrono::steady_clock;
+
+namespace {
+
+[[noreturn]] void die(const std::string& m) {
+  std::fprintf(stderr, "ref_tool: %s\n", m.c_str());
+  std::exit(2);
+}
+
+std::vector<double> read_f64(const std::string& path, size_t count) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) die("cannot open " + path);
+  std::vector<double> v(count);
+  in.read(reinterpret_cast<char*>(v.data()), static_cast<std::streamsize>(count * 8));
+  if (static_cast<size_t>(in.gcount()) != count * 8) die("short read from " + path);
+  return v;
+}
+
+void write_f64(std::ofstream& out, const std::vector<double>& v) {
+  out.write(reinterpret_cast<const char*>(v.data()), static_cast<std::streamsize>(v.size() * 8));
+}
+
+double secs(clk::time_point a, clk::time_point b) {
+  return std::chrono::duration<double>(b - a).count();
+}
+
+// Module holding the named DSL plus every derivative its calls reference
+// (tooling.cpp:103-119), exactly as the CLI's load_and_derive does.
+Module load_named(const std::string& name) {
+  const char* src = nullptr;
+  if (name == "kernels") src = kKernelsDsl;
+  else if (name == "gsum") src = kGsumDsl;
+  else if (name == "gaussnd") src = kGaussndDsl;
+  else if (name == "gpoly") src = kGpolyDsl;
+  else die("unknown module " + name);
+  Module m = parse_or_throw(src);
+  ensure_called_derivatives(m);
+  return m;
+}
+
+// Adds `<fn>_grad...` for the requested parameters (reverse.cpp:703-725).
+std::string add_gradient(Module& m, const std::string& fn, const std::vector<std::string>& wrt) {
+  const FunctionDef* f = m.find(fn);
+  if (f == nullptr) die("no function " + fn);
+  std::string name = gradient_name(*f, wrt);
+  if (m.find(name) == nullptr) {
+    AdjointProgram g = differentiate_gradient(*f, wrt);
+    m.functions.push_back(std::move(g.derived));
+  }
+  return name;
+}
+
+unsigned default_workers() {
+  unsigned w = std::thread::hardware_concurrency();
+  return w == 0 ? 1 : w;
+}
+
+// ---------------------------------------------------------------------------
+// print <module> <fn> <wrt...>   — the generated gradient text.
+int cmd_print(int argc, char** argv) {
+  if (argc < 4) die("print <module> <fn> <wrt...>");
+  Module m = load_named(argv[1]);
+  std::vector<std::string> wrt(argv + 3, argv + argc);
+  std::string name = add_gradient(m, argv[2], wrt);
+  std::cout << print(*m.find(name));
+  return 0;
+}
+
+// golden-check — the printed gauss_grad_0_1 must equal the reference's frozen
+// golden text (proj/tests/golden/gauss_grad_0_1.golden, compared byte-for-byte
+// as test_reverse.cpp:62-67 does).
+int cmd_golden_check(int, char**) {
+  Module m = load_named("kernels");
+  const FunctionDef* g = m.find("gauss_grad_0_1");
+  if (g == nullptr) die("gauss_grad_0_1 not derived");
+  std::string text = print(*g);
+  bool ok = text == std::string(kGaussGradGolden);
+  std::printf("{\"golden_match\": %s}\n", ok ? "true" : "false");
+  return ok ? 0 : 1;
+}
+
+
+// ---------------------------------------------------------------------------
+// gauss1d <n> <seed> <sigma> <block> <out.bin> [workers]
+//   Criterion-5 style fixture (acceptance.cpp:160-211): x~U(-3,3), p~U(-2,2)
+//   drawn from mt19937_64(seed) through uniform_real_distribution in the same
+//   order as PointSampler (support.hpp:36-43); runs adc::launch(prog,"compute",
+//   {n/block+1, block, n}) and the plain sequential Program::eval loop.
+//   Writes x, p, dx, dp.
+int cmd_gauss1d(int argc, char** argv) {
+  if (argc < 6) die("gauss1d <n> <seed> <sigma> <block> <out> [workers]");
+  const int64_t n = std::atoll(argv[1]);
+  const uint64_t seed = std::strtoull(argv[2], nullptr, 0);
+  const double sigma = std::atof(argv[3]);
+  const int64_t block = std::atoll(argv[4]);
+  const unsigned workers = argc > 6 ? static_cast<unsigned>(std::atoi(argv[6])) : 0;
+  std::mt19937_64 rng(seed);
+  std::vector<double> x(n), px(n);
+  for (int64_t i = 0; i < n; ++i) {
+    x[i] = std::uniform_real_distribution<double>(-3, 3)(rng);
+    px[i] = std::uniform_real_distribution<double>(-2, 2)(rng);
+  }
+  Program prog(load_named("kernels"));
+  LaunchConfig cfg{n / block + 1, block, n};
+  std::vector<double> dx_seq(n, 0.0), dp_seq(n, 0.0);
+  {
+    ArgPack args;
+    args.add_array(x).add_array(px).add_real(sigma).add_array(dx_seq).add_array(dp_seq);
+    for (int64_t g = 0; g < cfg.grid_dim * cfg.block_dim; ++g) {
+      EvalOptions o;
+      o.has_thread_ctx = true;
+      o.block_idx = g / cfg.block_dim;
+      o.block_dim = cfg.block_dim;
+      o.thread_idx = g % cfg.block_dim;
+      o.problem_n = n;
+      prog.eval("compute", args, o);
+    }
+  }
+  BufferSet b;
+  b.arrays["x"] = x;
+  b.arrays["p"] = px;
+  b.scalars["sigma"] = sigma;
+  b.arrays["dx"] = std::vector<double>(n, 0.0);
+  b.arrays["dp"] = std::vector<double>(n, 0.0);
+  LaunchOptions lo;
+  lo.workers = workers;
+  auto t0 = clk::now();
+  LaunchStats st = launch(prog, "compute", cfg, b, lo);
+  double sec = secs(t0, clk::now());
+  int64_t active = 0, idle = 0;
+  for (uint32_t c : st.thread_statements) (c == 3 ? active : idle) += 1;
+  bool same = b.arrays["dx"] == dx_seq && b.arrays["dp"] == dp_seq;
+  std::ofstream out(argv[5], std::ios::binary);
+  write_f64(out, x);
+  write_f64(out, px);
+  write_f64(out, b.arrays["dx"]);
+  write_f64(out, b.arrays["dp"]);
+  std::printf("{\"n\": %lld, \"grid\": %lld, \"block\": %lld, \"active\": %lld, \"idle\": %lld, "
+              "\"launch_equals_sequential\": %s, \"seconds\": %.6f, \"workers\": %u}\n",
+              (long long)n, (long long)cfg.grid_dim, (long long)block, (long long)active,
+              (long long)idle, same ? "true" : "false", sec,
+              workers ? workers : default_workers());
+  return same ? 0 : 1;
+}
+
+// gauss1d-in <n> <sigma> <block> <in.bin> <out.bin> [workers] [repeats]
+//   in = x, p, dx0, dp0 (n each); out = dx, dp after one adc::launch.
+//   Used for parity at arbitrary sizes and as the timed reference arm.
+int cmd_gauss1d_in(int argc, char** argv) {
+  if (argc < 6) die("gauss1d-in <n> <sigma> <block> <in> <out> [workers] [repeats]");
+  const int64_t n = std::atoll(argv[1]);
+  const double sigma = std::atof(argv[2]);
+  const int64_t block = std::atoll(argv[3]);
+  const unsigned workers = argc > 6 ? static_cast<unsigned>(std::atoi(argv[6])) : 0;
+  const int repeats = argc > 7 ? std::max(1, std::atoi(argv[7])) : 1;
+  std::vector<double> all = read_f64(argv[4], static_cast<size_t>(4 * n));
+  Program prog(load_named("kernels"));
+  LaunchConfig cfg{n / block + 1, block, n};
+  BufferSet b;
+  b.arrays["x"].assign(all.begin(), all.begin() + n);
+  b.arrays["p"].assign(all.begin() + n, all.begin() + 2 * n);
+  b.scalars["sigma"] = sigma;
+  LaunchOptions lo;
+  lo.workers = workers;
+  std::vector<double> times;
+  for (int r = 0; r < repeats; ++r) {
+    b.arrays["dx"].assign(all.begin() + 2 * n, all.begin() + 3 * n);
+    b.arrays["dp"].assign(all.begin() + 3 * n, all.begin() + 4 * n);
+    auto t0 = clk::now();
+    launch(prog, "compute", cfg, b, lo);
+    times.push_back(secs(t0, clk::now()));
+  }
+  std::ofstream out(argv[5], std::ios::binary);
+  write_f64(out, b.arrays["dx"]);
+  write_f64(out, b.arrays["dp"]);
+  std::sort(times.begin(), times.end());
+  std::printf("{\"n\": %lld, \"seconds_median\": %.6f, \"seconds_min\": %.6f, \"workers\": %u}\n",
+              (long long)n, times[times.size() / 2], times[0], workers ? workers : default_workers());
+  return 0;
+}
+
+// gaussnd-in <dim> <n> <sigma> <in.bin> <out.bin> [workers]
+//   in = x, p, dx0, dp0 in structure-of-arrays layout ([d*n + i]); each point
+//   is gathered into contiguous rows and run through
+//   Program::eval("gaussnd_grad_0_1") on an nproc thread pool (Program is
+//   immutable and safe for concurrent eval, eval.hpp:86-88).  out = dx, dp (SoA).
+int cmd_gaussnd_in(int argc, char** argv) {
+  if (argc < 6) die("gaussnd-in <dim> <n> <sigma> <in> <out> [workers]");
+  const int64_t dim = std::atoll(argv[1]);
+  const int64_t n = std::atoll(argv[2]);
+  const double sigma = std::atof(argv[3]);
+  unsigned workers = argc > 6 ? static_cast<unsigned>(std::atoi(argv[6])) : 0;
+  if (workers == 0) workers = default_workers();
+  const size_t tot = static_cast<size_t>(dim * n);
+  std::vector<double> all = read_f64(argv[4], 4 * tot);
+  const double* X = all.data();
+  const double* P = X + tot;
+  std::vector<double> DX(all.begin() + 2 * tot, all.begin() + 3 * tot);
+  std::vector<double> DP(all.begin() + 3 * tot, all.begin() + 4 * tot);
+  Module m = load_named("gaussnd");
+  add_gradient(m, "gaussnd", {"x", "p"});
+  Program prog(std::move(m));
+  std::atomic<int64_t> next{0};
+  auto body = [&]() {
+    std::vector<double> x(dim), p(dim), dx(dim), dp(dim);
+    for (;;) {
+      int64_t i = next.fetch_add(1);
+      if (i >= n) break;
+      for (int64_t d = 0; d < dim; ++d) {
+        x[d] = X[d * n + i];
+        p[d] = P[d * n + i];
+        dx[d] = DX[d * n + i];
+        dp[d] = DP[d * n + i];
+      }
+      ArgPack a;
+      a.add_array(x).add_array(p).add_real(sigma).add_int(dim).add_array(dx).add_array(dp);
+      prog.eval("gaussnd_grad_0_1", a);
+      for (int64_t d = 0; d < dim; ++d) {
+        DX[d * n + i] = dx[d];
+        DP[d * n + i] = dp[d];
+      }
+    }
+  };
+  auto t0 = clk::now();
+  std::vector<std::thread> pool;
+  for (unsigned w = 0; w < workers; ++w) pool.emplace_back(body);
+  for (auto& t : pool) t.join();
+  double sec = secs(t0, clk::now());
+  std::ofstream out(argv[5], std::ios::binary);
+  write_f64(out, DX);
+  write_f64(out, DP);
+  std::printf("{\"dim\": %lld, \"n\": %lld, \"seconds\": %.6f, \"workers\": %u}\n",
+              (long long)dim, (long long)n, sec, workers);
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// χ² over a model-parameterised engine.  For gsum this is the unmodified
+// FitEngine (fit.cpp); for any other model the same formulas
+// (fit.cpp:206-259, 268-278, 315-425) are evaluated over the reference
+// Program running that model and its generated gradient.  `clamp` lists the
+// parameter indices the σ clamp applies to (fit.cpp:268-278 hard-codes every
+// third index, which is right for gsum only).
+struct ModelEngine {
+  std::string model;
+  std::string grad;
+  Program prog;
+  std::vector<int> clamp_idx;
+
+  ModelEngine(const std::string& name, Module m, std::string g, std::vector<int> clamp)
+      : model(name), grad(std::move(g)), prog(std::move(m)), clamp_idx(std::move(clamp)) {}
+
+  ArgPack pack(double x, const std::vector<double>& q) const {
+    ArgPack a;
+    a.add_real(x);
+    a.add_array(const_cast<double*>(q.data()), static_cast<int64_t>(q.size()));
+    a.add_int(static_cast<int64_t>(q.size()) / 3);
+    return a;
+  }
+  double eval_model(double x, const std::vector<double>& q) const {
+    ArgPack a = pack(x, q);
+    return *prog.eval(model, a).value;
+  }
+  void eval_grad(double x, const std::vector<double>& q, std::vector<double>& out) const {
+    out.assign(q.size(), 0.0);
+    ArgPack a = pack(x, q);
+    a.add_array(out.data(), static_cast<int64_t>(out.size()));
+    prog.eval(grad, a);
+  }
+  double chi2(const Histogram& h, const std::vector<double>& q) const {
+    double s = 0.0;
+    std::vector<double> m(static_cast<size_t>(h.bins));
+    for (int j = 0; j < h.bins; ++j) {
+      m[j] = eval_model(h.center(j), q);
+      s += m[j];
+    }
+    double sum = 0.0;
+    const double scale = static_cast<double>(h.events) / s;
+    for (int j = 0; j < h.bins; ++j) {
+      double c = h.counts[j];
+      if (c <= 0.0) continue;
+      double r = c - scale * m[j];
+      sum += r * r / c;
+    }
+    return sum;
+  }
+  void chi2_gradient(const Histogram& h, const std::vector<double>& q,
+                     std::vector<double>& out) const {
+    const size_t np = q.size();
+    out.assign(np, 0.0);
+    const double events = static_cast<double>(h.events);
+    std::vector<double> m(static_cast<size_t>(h.bins));
+    double s = 0.0;
+    for (int j = 0; j < h.bins; ++j) {
+      m[j] = eval_model(h.center(j), q);
+      s += m[j];
+    }
+    double t_sum = 0.0;
+    for (int j = 0; j < h.bins; ++j) {
+      double c = h.counts[j];
+      if (c <= 0.0) continue;
+      double r = c - events * m[j] / s;
+      t_sum += 2.0 * r * m[j] / c;
+    }
+    const double s_coef = events / (s * s) * t_sum;
+    std::vector<double> bg(np);
+    for (int j = 0; j < h.bins; ++j) {
+      double c = h.counts[j];
+      double w = s_coef;
+      if (c > 0.0) {
+        double r = c - events * m[j] / s;
+        w += -2.0 * r / c * events / s;
+      }
+      if (w == 0.0) continue;
+      eval_grad(h.center(j), q, bg);
+      for (size_t i = 0; i < np; ++i) out[i] += w * bg[i];
+    }
+  }
+  int clamp(std::vector<double>& q, double sigma_min) const {
+    int n = 0;
+    for (int i : clamp_idx)
+      if (static_cast<size_t>(i) < q.size() && q[i] < sigma_min) {
+        q[i] = sigma_min;
+        ++n;
+      }
+    return n;
+  }
+  // Steepest descent + Armijo backtracking, fit.cpp:315-425 (use_hessian off).
+  FitResult fit(const Histogram& h, std::vector<double> q, const FitOptions& o) const {
+    FitResult res;
+    res.sigma_clamps += clamp(q, o.sigma_min);
+    const size_t np = q.size();
+    double cur = chi2(h, q);
+    if (o.trace_iterates > 0) res.iterates.push_back(q);
+    std::vector<double> g(np);
+    for (int iter = 0; iter < o.budget; ++iter) {
+      chi2_gradient(h, q, g);
+      ++res.gradient_evals;
+      double gmax = 0.0;
+      for (double v : g) gmax = std::max(gmax, std::fabs(v));
+      if (gmax <= o.grad_tol) {
+        res.converged = true;
+        break;
+      }
+      double gd = 0.0;
+      for (size_t i = 0; i < np; ++i) gd += g[i] * g[i];
+      double t = 1.0, next = 0.0;
+      bool accepted = false;
+      std::vector<double> cand;
+      while (t >= 1e-18) {
+        std::vector<double> trial = q;
+        for (size_t i = 0; i < np; ++i) trial[i] -= t * g[i];
+        int cl = clamp(trial, o.sigma_min);
+        double c2 = chi2(h, trial);
+        if (c2 <= cur - o.armijo_c1 * t * gd) {
+          accepted = true;
+          next = c2;
+          cand = std::move(trial);
+          res.sigma_clamps += cl;
+          break;
+        }
+        t *= 0.5;
+      }
+      if (!accepted) {
+        res.converged = true;
+        break;
+      }
+      double rel_dec = (cur - next) / std::max(1.0, std::fabs(cur));
+      q = std::move(cand);
+      cur = next;
+      ++res.iterations;
+      if (o.trace_iterates > res.iterations) res.iterates.push_back(q);
+      if (rel_dec <= o.chi2_rel_tol) {
+        res.converged = true;
+        break;
+      }
+    }
+    res.params = std::move(q);
+    res.chi2 = cur;
+    return res;
+  }
+};
+
+ModelEngine make_engine(const std::string& model) {
+  Module m = load_named(model);
+  std::string g = add_gradient(m, model, {"q"});
+  std::vector<int> clamp;
+  if (model == "gsum") {
+    for (int i = 2; i < 64; i += 3) clamp.push_back(i);
+  } else {
+    clamp = {2};  // gpoly: only q[2] is a width
+  }
+  return ModelEngine(model, std::move(m), g, clamp);
+}
+
+Histogram read_hist(int64_t bins, double lo, double hi, const std::string& path) {
+  Histogram h;
+  h.bins = static_cast<int>(bins);
+  h.lo = lo;
+  h.hi = hi;
+  h.counts = read_f64(path, static_cast<size_t>(bins));
+  double tot = 0;
+  for (double c : h.counts) tot += c;
+  h.events = static_cast<uint64_t>(tot);
+  return h;
+}
+
+// chi2-in <model> <bins> <lo> <hi> <counts.bin> <out.bin> <repeats> q...
+//   out = [chi2, grad[np]].  events = Σ counts (the reference sampler
+//   guarantees this, fit.cpp:88,94-102).  For gsum the result also comes from
+//   the unmodified adc::FitEngine and both must agree bitwise.
+int cmd_chi2_in(int argc, char** argv) {
+  if (argc < 8) die("chi2-in <model> <bins> <lo> <hi> <counts> <out> <repeats> q...");
+  std::string model = argv[1];
+  Histogram h = read_hist(std::atoll(argv[2]), std::atof(argv[3]), std::atof(argv[4]), argv[5]);
+  const int repeats = std::max(1, std::atoi(argv[7]));
+  std::vector<double> q;
+  for (int i = 8; i < argc; ++i) q.push_back(std::atof(argv[i]));
+  ModelEngine eng = make_engine(model);
+  std::vector<double> g;
+  double c2 = 0;
+  std::vector<double> tg, tc;
+  for (int r = 0; r < repeats; ++r) {
+    auto t0 = clk::now();
+    eng.chi2_gradient(h, q, g);
+    auto t1 = clk::now();
+    c2 = eng.chi2(h, q);
+    auto t2 = clk::now();
+    tg.push_back(secs(t0, t1));
+    tc.push_back(secs(t1, t2));
+  }
+  bool engine_match = true;
+  if (model == "gsum") {
+    FitEngine fe;
+    std::vector<double> g2;
+    fe.chi2_gradient(h, q, GradientProvider::AdReverse, g2);
+    engine_match = g2 == g && fe.chi2(h, q) == c2;
+  }
+  std::ofstream out(argv[6], std::ios::binary);
+  std::vector<double> res{c2};
+  res.insert(res.end(), g.begin(), g.end());
+  write_f64(out, res);
+  std::sort(tg.begin(), tg.end());
+  std::sort(tc.begin(), tc.end());
+  std::printf("{\"bins\": %d, \"events\": %llu, \"grad_seconds\": %.6f, \"chi2_seconds\": %.6f, "
+              "\"fitengine_match\": %s}\n",
+              h.bins, (unsigned long long)h.events, tg[tg.size() / 2], tc[tc.size() / 2],
+              engine_match ? "true" : "false");
+  return engine_match ? 0 : 1;
+}
+
+// fit-in <model> <bins> <lo> <hi> <counts.bin> <out.bin> <trace> <budget> q...
+//   out = [chi2, iterations, gradient_evals, converged, sigma_clamps,
+//          params[np], iterates[trace x np] (zero padded)].
+int cmd_fit_in(int argc, char** argv) {
+  if (argc < 9) die("fit-in <model> <bins> <lo> <hi> <counts> <out> <trace> <budget> q...");
+  std::string model = argv[1];
+  Histogram h = read_hist(std::atoll(argv[2]), std::atof(argv[3]), std::atof(argv[4]), argv[5]);
+  FitOptions o;
+  o.trace_iterates = std::atoi(argv[7]);
+  o.budget = std::atoi(argv[8]);
+  std::vector<double> q;
+  for (int i = 9; i < argc; ++i) q.push_back(std::atof(argv[i]));
+  ModelEngine eng = make_engine(model);
+  auto t0 = clk::now();
+  FitResult r = eng.fit(h, q, o);
+  double sec = secs(t0, clk::now());
+  bool engine_match = true;
+  if (model == "gsum") {
+    FitEngine fe;
+    FitResult r2 = fe.fit(h, GradientProvider::AdReverse, q, o);
+    engine_match = r2.params == r.params && r2.iterates == r.iterates && r2.chi2 == r.chi2 &&
+                   r2.iterations == r.iterations;
+  }
+  std::vector<double> res{r.chi2, double(r.iterations), double(r.gradient_evals),
+                          r.converged ? 1.0 : 0.0, double(r.sigma_clamps)};
+  res.insert(res.end(), r.params.begin(), r.params.end());
+  for (int k = 0; k < o.trace_iterates; ++k) {
+    if (static_cast<size_t>(k) < r.iterates.size())
+      res.insert(res.end(), r.iterates[k].begin(), r.iterates[k].end());
+    else
+      res.insert(res.end(), q.size(), 0.0);
+  }
+  std::ofstream out(argv[6], std::ios::binary);
+  write_f64(out, res);
+  std::printf("{\"iterations\": %d, \"converged\": %s, \"seconds\": %.6f, "
+              "\"fitengine_match\": %s}\n",
+              r.iterations, r.converged ? "true" : "false", sec, engine_match ? "true" : "false");
+  return engine_match ? 0 : 1;
+}
+}  // namespace
+
+int main(int argc, char** argv) {
+  if (argc < 2) die("usage: ref_tool <command> ...");
+  std::string cmd = argv[1];
+  try {
+    if (cmd == "print") return cmd_print(argc - 1, argv + 1);
+    if (cmd == "golden-check") return cmd_golden_check(argc - 1, argv + 1);
+    if (cmd == "gauss1d") return cmd_gauss1d(argc - 1, argv + 1);
+    if (cmd == "gauss1d-in") return cmd_gauss1d_in(argc - 1, argv + 1);
+    if (cmd == "gaussnd-in") return cmd_gaussnd_in(argc - 1, argv + 1);
+    if (cmd == "chi2-in") return cmd_chi2_in(argc - 1, argv + 1);
+    if (cmd == "fit-in") return cmd_fit_in(argc - 1, argv + 1);
+  } catch (const Error& e) {
+    std::fprintf(stderr, "ref_tool: adc::Error(kind=%d): %s\n", static_cast<int>(e.kind()),
+                 e.what());
+    return 3;
+  }
+  die("unknown command " + cmd);
+}

@@ -1,0 +1,61 @@
+/* restate.h — TEST INFRASTRUCTURE (oracle).  Plain-C restatement of the
+ * reference's arithmetic on the hot path, used only by tests/, smoke() and
+ * bench.py's cpu_baseline leg as the CHECKER.  Never linked into the product.
+ *
+ * Every function transcribes the code the reference generates or runs, one
+ * IEEE operation per source operation, compiled with -ffp-contract=off:
+ *   rs_gauss_grad_0_1   <- proj/tests/golden/gauss_grad_0_1.golden:1-42
+ *   rs_gaussnd_grad_0_1 <- differentiate_gradient(gaussnd,{x,p}) output
+ *                          (oracle/dsl/gaussnd.dsl; reverse.cpp:703-725)
+ *   rs_gsum / rs_gsum_grad_1   <- fit.cpp:125-138 model + its generated gradient
+ *   rs_gpoly / rs_gpoly_grad_1 <- oracle/dsl/gpoly.dsl + its generated gradient
+ *   rs_chi2 / rs_chi2_gradient <- FitEngine::chi2 / chi2_gradient,
+ *                                 proj/src/fit.cpp:206-222 / 224-259
+ * Pinned against the reference itself: tests/test_oracle.py compares every
+ * function with golden vectors written by oracle/_ref/ref_tool (the
+ * unmodified reference library) — see tests/golden/README.md.
+ */
+#ifndef ADC_ORACLE_RESTATE_H
+#define ADC_ORACLE_RESTATE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { RS_MODEL_GSUM = 0, RS_MODEL_GPOLY = 1 };
+
+/* Listing-1 batch: for g in [0,n): gauss_grad_0_1(x[g],p[g],sigma,&dx[g],&dp[g]) */
+void rs_gauss_grad_batch(const double* x, const double* p, double sigma, double* dx, double* dp,
+                         int64_t n);
+
+/* N-dim batch over structure-of-arrays rows: element (d, i) at [d*ld + i]. */
+void rs_gaussnd_grad_batch(const double* x, const double* p, double sigma, int64_t dim, int64_t n,
+                           int64_t ld, double* dx, double* dp);
+
+/* One point, contiguous row of length dim (the layout Program::eval sees). */
+void rs_gaussnd_grad_0_1(const double* x, const double* p, double sigma, int64_t dim, double* dx,
+                         double* dp);
+
+double rs_model(int model, double x, const double* q, int64_t np);
+void rs_model_grad(int model, double x, const double* q, int64_t np, double* slot);
+
+/* Sequential, verbatim fit.cpp:206-222. */
+double rs_chi2(int model, const double* counts, int64_t bins, double lo, double hi, double events,
+               const double* q, int64_t np);
+/* Sequential, verbatim fit.cpp:224-259. */
+void rs_chi2_gradient(int model, const double* counts, int64_t bins, double lo, double hi,
+                      double events, const double* q, int64_t np, double* out);
+/* Same formula with Neumaier-compensated sums (the accuracy reference for
+ * order-changed GPU reductions).  abs_out[i] = sum_j |w_j dm_j/dq_i|, the
+ * scale the reduction tolerance is stated against. */
+void rs_chi2_gradient_compensated(int model, const double* counts, int64_t bins, double lo,
+                                  double hi, double events, const double* q, int64_t np,
+                                  double* out, double* abs_out);
+double rs_chi2_compensated(int model, const double* counts, int64_t bins, double lo, double hi,
+                           double events, const double* q, int64_t np, double* abs_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,99 @@
+"""ctypes binding of oracle/restate.c (TEST INFRASTRUCTURE — the checker).
+
+Built by `make -C oracle restate` (also run by __graft_entry__.build()); if the
+.so is missing this builds it with gcc (present on the GPU box too).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(HERE, "_ref", "librestate.so")
+MODELS = {"gsum": 0, "gpoly": 1}
+
+_D = ctypes.POINTER(ctypes.c_double)
+_lib = None
+
+
+def _p(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_D)
+
+
+class Restate:
+    def __init__(self, lib):
+        self.lib = lib
+        i64, d, i = ctypes.c_int64, ctypes.c_double, ctypes.c_int
+        lib.rs_gauss_grad_batch.argtypes = [_D, _D, d, _D, _D, i64]
+        lib.rs_gaussnd_grad_batch.argtypes = [_D, _D, d, i64, i64, i64, _D, _D]
+        lib.rs_model.argtypes = [i, d, _D, i64]
+        lib.rs_model.restype = d
+        lib.rs_model_grad.argtypes = [i, d, _D, i64, _D]
+        lib.rs_chi2.argtypes = [i, _D, i64, d, d, d, _D, i64]
+        lib.rs_chi2.restype = d
+        lib.rs_chi2_gradient.argtypes = [i, _D, i64, d, d, d, _D, i64, _D]
+        lib.rs_chi2_gradient_compensated.argtypes = [i, _D, i64, d, d, d, _D, i64, _D, _D]
+        lib.rs_chi2_compensated.argtypes = [i, _D, i64, d, d, d, _D, i64, _D]
+        lib.rs_chi2_compensated.restype = d
+
+    def gauss_grad(self, x, p, sigma, dx, dp):
+        """In-place accumulate, like the reference slots."""
+        self.lib.rs_gauss_grad_batch(_p(x), _p(p), sigma, _p(dx), _p(dp), x.size)
+
+    def gaussnd_grad(self, x, p, sigma, dx, dp):
+        dim, n = x.shape
+        self.lib.rs_gaussnd_grad_batch(_p(x), _p(p), sigma, dim, n, n, _p(dx), _p(dp))
+
+    def model(self, model, x, q):
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        return self.lib.rs_model(MODELS[model], x, _p(q), q.size)
+
+    def model_grad(self, model, x, q):
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        out = np.zeros(q.size)
+        self.lib.rs_model_grad(MODELS[model], x, _p(q), q.size, _p(out))
+        return out
+
+    def chi2(self, model, counts, lo, hi, events, q):
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        return self.lib.rs_chi2(MODELS[model], _p(counts), counts.size, lo, hi, events, _p(q), q.size)
+
+    def chi2_gradient(self, model, counts, lo, hi, events, q):
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        out = np.zeros(q.size)
+        self.lib.rs_chi2_gradient(MODELS[model], _p(counts), counts.size, lo, hi, events, _p(q),
+                                  q.size, _p(out))
+        return out
+
+    def chi2_gradient_compensated(self, model, counts, lo, hi, events, q):
+        """Returns (gradient, scale) with scale_i = sum_j |w_j dm_j/dq_i|."""
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        out = np.zeros(q.size)
+        scale = np.zeros(q.size)
+        self.lib.rs_chi2_gradient_compensated(MODELS[model], _p(counts), counts.size, lo, hi,
+                                              events, _p(q), q.size, _p(out), _p(scale))
+        return out, scale
+
+    def chi2_compensated(self, model, counts, lo, hi, events, q):
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        scale = np.zeros(1)
+        v = self.lib.rs_chi2_compensated(MODELS[model], _p(counts), counts.size, lo, hi, events,
+                                         _p(q), q.size, _p(scale))
+        return v, float(scale[0])
+
+
+def build():
+    subprocess.run(["make", "-s", "-C", HERE, "restate"], check=True)
+
+
+def load() -> Restate:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(SO):
+            build()
+        _lib = Restate(ctypes.CDLL(SO))
+    return _lib

@@ -1,0 +1,145 @@
+"""Generates tests/golden/*.npz from the UNMODIFIED reference (oracle/_ref/ref_tool,
+built by `make -C oracle` from /root/reference/proj/src).  Run here, in the
+container that has /root/reference; the committed .npz files are what the
+tests read (the GPU box has no /root/reference).
+
+    python tests/golden/make_golden.py
+
+Every fixture stores the inputs and the reference outputs side by side.
+"""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+import tempfile
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+from paper_2203_06139_b200 import synth  # noqa: E402
+
+TOOL = os.path.join(ROOT, "oracle", "_ref", "ref_tool")
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def run(*args):
+    r = subprocess.run([TOOL, *map(str, args)], check=True, capture_output=True, text=True)
+    return json.loads(r.stdout.strip().splitlines()[-1]) if r.stdout.strip().startswith("{") else r.stdout
+
+
+def f64(path, count):
+    a = np.fromfile(path, dtype="<f8")
+    assert a.size == count, (path, a.size, count)
+    return a
+
+
+def fnv1a64(data: bytes) -> int:
+    h = 0xCBF29CE484222325
+    for b in data:
+        h ^= b
+        h = (h * 0x100000001B3) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def main():
+    tmp = tempfile.mkdtemp()
+    ti, to = os.path.join(tmp, "in.bin"), os.path.join(tmp, "out.bin")
+    # Fingerprints (FNV-1a 64) of the printed generated gradients: the B200
+    # kernel registry is keyed by them (include/adc_cuda.h).  Only the hashes
+    # are committed, not the generated text.
+    assert run("golden-check")["golden_match"]
+    fps = {}
+    for mod, fn, wrt in (("kernels", "gauss", ("x", "p")), ("gaussnd", "gaussnd", ("x", "p")),
+                         ("gpoly", "gpoly", ("q",)), ("gsum", "gsum", ("q",))):
+        text = run("print", mod, fn, *wrt)
+        name = text.split("(")[0].split()[-1]
+        fps[name] = f"0x{fnv1a64(text.encode()):016x}"
+    with open(os.path.join(OUT, "gradient_fingerprints.json"), "w") as fh:
+        json.dump(fps, fh, indent=1, sort_keys=True)
+        fh.write("\n")
+
+    # Listing 1 / criterion 5: N=512, seed 0x5EED, sigma 1.3, grid 3 x 256.
+    meta = run("gauss1d", 512, "0x5EED", 1.3, 256, to)
+    a = f64(to, 4 * 512).reshape(4, 512)
+    np.savez(os.path.join(OUT, "gauss1d_n512.npz"), x=a[0], p=a[1], dx=a[2], dp=a[3], sigma=1.3,
+             grid=meta["grid"], block=256, active=meta["active"], idle=meta["idle"])
+
+    # KAT gauss(1,0,1) (test_reverse.cpp:69-82) + ragged accumulate case.
+    cases = {}
+    rng = np.random.Generator(np.random.PCG64(7))
+    for name, n, sigma, block, x, p, dx0, dp0 in (
+        ("kat", 1, 1.0, 1, np.array([1.0]), np.array([0.0]), np.zeros(1), np.zeros(1)),
+        ("accum300", 300, 0.7, 128, rng.uniform(-3, 3, 300), rng.uniform(-2, 2, 300),
+         rng.standard_normal(300), rng.standard_normal(300)),
+        ("edges", 6, 1.3, 32, np.array([0.0, -0.0, 1e-300, 5.0, -40.0, 2.0]),
+         np.array([0.0, 0.0, 0.0, -5.0, 40.0, 2.0]), np.array([-0.0, 0.0, 1.0, 0.0, 0.0, -0.0]),
+         np.zeros(6)),
+    ):
+        np.concatenate([x, p, dx0, dp0]).astype("<f8").tofile(ti)
+        run("gauss1d-in", n, sigma, block, ti, to)
+        o = f64(to, 2 * n).reshape(2, n)
+        cases[name] = dict(x=x, p=p, dx0=dx0, dp0=dp0, dx=o[0], dp=o[1], sigma=sigma, block=block)
+    np.savez(os.path.join(OUT, "gauss1d_cases.npz"),
+             **{f"{k}_{f}": v for k, d in cases.items() for f, v in d.items()})
+
+    # N-dim Gaussian, SoA layout, nonzero initial slots (accumulate semantics).
+    nd = {}
+    for dim, n, seed in ((100, 64, 11), (1000, 8, 12), (1, 33, 13), (37, 70, 14), (128, 40, 15),
+                         (129, 5, 16)):
+        x, p = synth.points_nd(dim, n, seed=seed)
+        r = np.random.Generator(np.random.PCG64(seed + 100))
+        dx0 = r.standard_normal((dim, n)) * 1e-3
+        dp0 = r.standard_normal((dim, n)) * 1e-3
+        sigma = 1.3
+        np.concatenate([x.ravel(), p.ravel(), dx0.ravel(), dp0.ravel()]).astype("<f8").tofile(ti)
+        run("gaussnd-in", dim, n, sigma, ti, to)
+        o = f64(to, 2 * dim * n).reshape(2, dim, n)
+        key = f"d{dim}_n{n}"
+        nd.update({f"{key}_x": x, f"{key}_p": p, f"{key}_dx0": dx0, f"{key}_dp0": dp0,
+                   f"{key}_dx": o[0], f"{key}_dp": o[1], f"{key}_sigma": sigma})
+    np.savez(os.path.join(OUT, "gaussnd_cases.npz"), **nd)
+
+    # chi2 value + gradient (fit.cpp:206-259) for gpoly and gsum K=1,2.
+    ch = {}
+    for key, model, bins, events, qtrue, q in (
+        ("gpoly_b2000", "gpoly", 2000, 1e6, synth.GPOLY_TRUTH, synth.GPOLY_INIT),
+        ("gsum1_b1000", "gsum", 1000, 1e5, (1.0, 0.0, 1.5), (0.8, 0.3, 1.2)),
+        ("gsum2_b1500", "gsum", 1500, 2e5, (1.0, -5 / 3, 1.5, 1.0, 5 / 3, 1.0),
+         (0.8, -1.3666666666666667, 1.2, 0.8, 1.9666666666666668, 0.8)),
+    ):
+        counts, ev = synth.histogram(bins, -5.0, 5.0, events, model, qtrue, seed=bins)
+        counts.astype("<f8").tofile(ti)
+        meta = run("chi2-in", model, bins, -5.0, 5.0, ti, to, 1, *[repr(float(v)) for v in q])
+        assert meta["fitengine_match"]
+        o = f64(to, 1 + len(q))
+        ch.update({f"{key}_counts": counts, f"{key}_q": np.array(q, dtype=np.float64),
+                   f"{key}_chi2": o[0], f"{key}_grad": o[1:], f"{key}_events": ev,
+                   f"{key}_model": model})
+    np.savez(os.path.join(OUT, "chi2_cases.npz"), **ch)
+
+    # Fit loop iterates (fit.cpp:315-425), trace 10, budget 12.
+    fi = {}
+    for key, model, bins, events, qtrue, q in (
+        ("gpoly_b400", "gpoly", 400, 2e5, synth.GPOLY_TRUTH, synth.GPOLY_INIT),
+        ("gsum1_b300", "gsum", 300, 1e5, (1.0, 0.0, 1.5), (0.8, 0.3, 1.2)),
+    ):
+        counts, ev = synth.histogram(bins, -5.0, 5.0, events, model, qtrue, seed=bins + 1)
+        counts.astype("<f8").tofile(ti)
+        meta = run("fit-in", model, bins, -5.0, 5.0, ti, to, 10, 12, *[repr(float(v)) for v in q])
+        assert meta["fitengine_match"]
+        np_ = len(q)
+        o = f64(to, 5 + np_ + 10 * np_)
+        fi.update({f"{key}_counts": counts, f"{key}_init": np.array(q, dtype=np.float64),
+                   f"{key}_chi2": o[0], f"{key}_iterations": o[1], f"{key}_gradient_evals": o[2],
+                   f"{key}_converged": o[3], f"{key}_sigma_clamps": o[4],
+                   f"{key}_params": o[5:5 + np_], f"{key}_iterates": o[5 + np_:].reshape(10, np_),
+                   f"{key}_model": model})
+    np.savez(os.path.join(OUT, "fit_cases.npz"), **fi)
+    print("golden fixtures written to", OUT)
+
+
+if __name__ == "__main__":
+    main()
