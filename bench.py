@@ -1,0 +1,455 @@
+"""Benchmark driver (contract in the task statement; workloads in DESIGN.md §5).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload gaussnd100|gaussnd1000|gauss1d|chi2] [--no-secondary]
+
+Headline workload (BASELINE.json configs[1]): batched reverse-mode gradient of
+the 100-dim Gaussian over 10M points per GPU, FP64, structure-of-arrays,
+inputs resident in HBM (32 GB per GPU > the 126 MB L2, so no flush is needed
+between steps).  A step = one launch of gaussnd_grad_0_1 over all points of
+the rank.  Multi-GPU: points are independent, each rank owns its own 10M
+points (weak scaling), no collective on the data path; the chi2 secondary
+line does one all_gather of the chunk records per gradient.
+
+Rank 0 prints ONE JSON line.  `--impl reference` times the reference's own
+CPU implementation (oracle/_ref/ref_tool over the unmodified reference
+library) on the host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+REF_TOOL = os.path.join(ROOT, "oracle", "_ref", "ref_tool")
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+
+WORKLOADS = {
+    # name: (dim, points per GPU, description)
+    "gaussnd100": (100, 10_000_000, "N-dim Gaussian gradient gaussnd_grad_0_1, dim=100, "
+                                    "10M points per GPU, FP64 SoA (BASELINE configs[1])"),
+    "gaussnd1000": (1000, 1_000_000, "N-dim Gaussian gradient, dim=1000, 1M points per GPU "
+                                     "(BASELINE configs[3])"),
+    "gauss1d": (1, 1_000_000, "Listing-1 compute -> gauss_grad_0_1 over 1M points "
+                              "(BASELINE configs[0])"),
+}
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+def traffic_for(workload):
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(workload)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.proc, self.lines = index, None, []
+
+    def __enter__(self):
+        if shutil.which("nvidia-smi"):
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- distributed
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def maybe_init_pg(world, local, backend="nccl"):
+    import torch
+    import torch.distributed as dist
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend, device_id=torch.device("cuda", local))
+    return dist if world > 1 else None
+
+
+def barrier_sync(dist):
+    import torch
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+        torch.cuda.synchronize()
+
+
+def max_over_ranks(dist, value):
+    import torch
+    if dist is None:
+        return value
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------- reference arm
+def run_ref_tool(args, timeout=900):
+    r = subprocess.run([REF_TOOL, *map(str, args)], capture_output=True, text=True,
+                       timeout=timeout, check=True)
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def cpu_reference_gaussnd(dim, total_points, workers=0):
+    """The unmodified reference Program::eval(gaussnd_grad_0_1) on an nproc
+    thread pool; returns (pt*param/s, seconds, sample description)."""
+    uniq = min(total_points, 4096 if dim <= 100 else 512)
+    out = run_ref_tool(["gaussnd-bench", dim, uniq, total_points, 1.3, 42, workers])
+    rate = total_points * 2 * dim / out["seconds"]
+    return rate, out
+
+
+def cpu_port_gaussnd(dim, npts):
+    """Fallback: the C restatement (oracle/restate.c), one core."""
+    import numpy as np
+    from oracle import restate_lib
+    from paper_2203_06139_b200 import synth
+    rs = restate_lib.load()
+    x, p = synth.points_nd(dim, npts, seed=7)
+    dx, dp = np.zeros_like(x), np.zeros_like(x)
+    t0 = time.perf_counter()
+    rs.gaussnd_grad(x, p, 1.3, dx, dp)
+    dt = time.perf_counter() - t0
+    return npts * 2 * dim / dt, {"seconds": dt, "points": npts, "workers": 1}
+
+
+def reference_arm(a, world, rank):
+    if rank != 0:
+        return
+    dim, npts, desc = WORKLOADS[a.workload]
+    cores = os.cpu_count()
+    kind = "reference" if os.path.exists(REF_TOOL) else "port"
+    # each step: a bounded sample of the workload (~1-2 s on the host cores)
+    if a.workload == "gauss1d":
+        per_step = 1_000_000
+    else:
+        per_step = 24_000 if dim <= 100 else 2_400
+        per_step = max(per_step, cores * (2000 if dim <= 100 else 200))
+    rates = []
+    for s in range(a.warmup + a.steps):
+        if kind == "reference":
+            if a.workload == "gauss1d":
+                out = run_ref_tool(["gauss1d-bench", per_step, 1])
+                rate = per_step * 2 / out["seconds"]
+            else:
+                rate, out = cpu_reference_gaussnd(dim, per_step)
+        else:
+            rate, out = cpu_port_gaussnd(dim, min(per_step, 20000))
+        if s >= a.warmup:
+            rates.append(rate)
+    value = statistics.median(rates)
+    sample = f"{per_step} points x {dim} dims per step through the reference's " \
+             f"{'adc::launch(compute)' if a.workload == 'gauss1d' else 'Program::eval(gaussnd_grad_0_1)'}" \
+             f" on {cores} host threads"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "pt*param/s",
+        "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": per_step * 2 * dim / value * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "sample_points_per_step": per_step, "dim": dim},
+        "cpu_baseline": {"value": value, "unit": "pt*param/s", "cores": cores, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "pt*param/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- our arm
+def event_time(fn, stream):
+    import torch
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    fn()
+    b.record(stream)
+    return a, b
+
+
+def bench_points(a, world, rank, local, dist):
+    """Device-resident timing + e2e through the host-buffer API."""
+    import numpy as np
+    import torch
+    import paper_2203_06139_b200 as adc
+
+    dim, npts, desc = WORKLOADS[a.workload]
+    dev = torch.device("cuda", local)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    spread = 0.1 if dim <= 100 else 0.03
+    if a.workload == "gauss1d":
+        x = torch.rand(npts, dtype=torch.float64, device=dev, generator=g) * 6 - 3
+        p = torch.rand(npts, dtype=torch.float64, device=dev, generator=g) * 4 - 2
+    else:
+        p = torch.rand((dim, npts), dtype=torch.float64, device=dev, generator=g) * 4 - 2
+        x = p + spread * torch.randn((dim, npts), dtype=torch.float64, device=dev, generator=g)
+    dx = torch.zeros_like(x)
+    dp = torch.zeros_like(x)
+    stream = torch.cuda.current_stream(dev)
+    if a.workload == "gauss1d":
+        cfg = adc.LaunchConfig(npts // 256 + 1, 256, npts)
+        bufs = adc.BufferSet(arrays={"x": x, "p": p, "dx": dx, "dp": dp}, scalars={"sigma": 1.3})
+        step = lambda: adc.launch("compute", cfg, bufs)  # noqa: E731
+    else:
+        step = lambda: adc.launch_batch("gaussnd_grad_0_1", x, p, 1.3, dx, dp)  # noqa: E731
+    for _ in range(a.warmup):
+        step()
+    barrier_sync(dist)
+    evs = []
+    with ClockSampler(local) as clocks:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for _ in range(a.steps):
+            evs.append(event_time(step, stream))
+        t_end.record(stream)
+        barrier_sync(dist)
+    elapsed_ms = max_over_ranks(dist, t_start.elapsed_time(t_end))
+    kernel_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    units = npts * (2 * dim if dim > 1 else 2)
+    value = world * units * a.steps / (elapsed_ms * 1e-3)
+    alg_bytes = 48 * npts * dim  # x, p read; dx, dp read + written
+    pk = peaks()
+    avg_kernel_s = statistics.mean(kernel_ms) * 1e-3
+    achieved = alg_bytes / avg_kernel_s / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / pk["hbm_gbs"], "traffic": traffic_for(a.workload),
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if not pk.get("_fallback")
+            else "fallback 6650 GB/s (B200_PROFILING.md)",
+            "algorithmic_bytes_per_launch": alg_bytes,
+            "kernel_ms_avg": statistics.mean(kernel_ms), "kernel_ms_min": min(kernel_ms)}
+    del dx, dp
+    # ---- e2e: public API with pinned HOST buffers, H2D + D2H inside the timing
+    e2e = None
+    if not a.no_e2e:
+        hx = torch.empty(x.shape, dtype=torch.float64, pin_memory=True)
+        hp = torch.empty(x.shape, dtype=torch.float64, pin_memory=True)
+        hx.copy_(x)
+        hp.copy_(p)
+        del x, p
+        torch.cuda.empty_cache()
+        hdx = torch.zeros(hx.shape, dtype=torch.float64, pin_memory=True)
+        hdp = torch.zeros(hx.shape, dtype=torch.float64, pin_memory=True)
+        nx, npp, ndx, ndp = hx.numpy(), hp.numpy(), hdx.numpy(), hdp.numpy()
+        if a.workload == "gauss1d":
+            hb = adc.BufferSet(arrays={"x": nx, "p": npp, "dx": ndx, "dp": ndp},
+                               scalars={"sigma": 1.3})
+            hstep = lambda: adc.launch("compute", cfg, hb)  # noqa: E731
+        else:
+            hstep = lambda: adc.launch_batch("gaussnd_grad_0_1", nx, npp, 1.3, ndx, ndp)  # noqa
+        hstep()
+        e2e_steps = max(1, min(a.steps, a.e2e_steps))
+        barrier_sync(dist)
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            hstep()
+        dt = max_over_ranks(dist, time.perf_counter() - t0)
+        e2e = {"value": world * units * e2e_steps / dt, "unit": "pt*param/s",
+               "h2d_bytes_per_step": 4 * 8 * npts * dim, "d2h_bytes_per_step": 2 * 8 * npts * dim,
+               "steps": e2e_steps, "path": "launch_batch/launch with pinned numpy buffers -> "
+               "adc_cuda_*_host (chunked H2D/kernel/D2H over two streams)"}
+        del hx, hp, hdx, hdp
+    return value, elapsed_ms / a.steps, roof, e2e, clocks.summary(), desc, dim, npts
+
+
+def bench_chi2(world, rank, local, dist, bins=100_000_000, passes=20, warm=3):
+    """chi2 fit gradient over `bins` bins (BASELINE configs[4]); per rank a
+    shard of whole chunks, one all_gather of the chunk records per pass."""
+    import numpy as np
+    import torch
+    import paper_2203_06139_b200 as adc
+    from paper_2203_06139_b200 import synth
+
+    dev = torch.device("cuda", local)
+    g = torch.Generator(device=dev)
+    g.manual_seed(77)
+    # counts ~ Poisson(E m_j / S) with the gpoly truth, generated on the device
+    width = 10.0 / bins
+    xs = -5.0 + (torch.arange(bins, dtype=torch.float64, device=dev) + 0.5) * width
+    q0 = synth.GPOLY_TRUTH
+    m = q0[0] * torch.exp(-0.5 * ((xs - q0[1]) / q0[2]) ** 2) + q0[3] + q0[4] * xs + q0[5] * xs * xs
+    lam = m * (bins * 100.0 / float(m.sum()))
+    counts = torch.poisson(lam, generator=g)
+    counts[::100] = 0
+    del xs, m, lam
+    events = float(counts.sum())
+    h = adc.Histogram(bins, -5.0, 5.0, events, counts)
+    q = list(synth.GPOLY_INIT)
+    plan = adc.Chi2Plan("gpoly", 6, h, world=world, rank=rank)
+    L = plan.layout
+    R = adc.record_len(6, True)
+    nloc = L.chunk_end - L.chunk_begin
+    per = (L.nchunks + world - 1) // world
+    loc = torch.zeros(per * R, dtype=torch.float64, device=dev)
+    allr = torch.zeros(world * per * R, dtype=torch.float64, device=dev)
+    counts_by_rank = [((L.nchunks * (r + 1)) // world - (L.nchunks * r) // world)
+                      for r in range(world)]
+
+    def one_pass():
+        plan.partials(q, True, loc)
+        if dist is not None:
+            torch.cuda.synchronize()
+            dist.all_gather_into_tensor(allr, loc)
+            host = allr.cpu().numpy().reshape(world, per * R)
+            rec = np.concatenate([host[r, :counts_by_rank[r] * R] for r in range(world)])
+        else:
+            rec = loc.cpu().numpy()[:nloc * R]
+        return adc.finalize(6, events, rec, True)
+
+    for _ in range(warm):
+        one_pass()
+    barrier_sync(dist)
+    t0 = time.perf_counter()
+    for _ in range(passes):
+        grad, c2 = one_pass()
+    dt = max_over_ranks(dist, time.perf_counter() - t0) / passes
+    # device-only kernel time of this rank's pass (tile + chunk kernels)
+    stream = torch.cuda.current_stream(dev)
+    kt = []
+    for _ in range(5):
+        e0, e1 = event_time(lambda: plan.partials(q, True, loc), stream)
+        torch.cuda.synchronize()
+        kt.append(e0.elapsed_time(e1))
+    out = {"workload": f"chi2 gradient, gpoly (Gaussian + quadratic bkg), {bins:.0e} bins over "
+                       f"{world} GPU(s) (BASELINE configs[4])",
+           "passes_per_s": 1.0 / dt, "ms_per_pass": dt * 1e3,
+           "device_ms_per_rank_pass": statistics.median(kt),
+           "bins_per_s_device": (L.bin_end - L.bin_begin) / (statistics.median(kt) * 1e-3),
+           "collective": "all_gather of chunk records" if world > 1 else "none",
+           "chi2": c2}
+    plan.close()
+    return out
+
+
+def ours_arm(a, world, rank, local):
+    import torch
+    torch.cuda.set_device(local)
+    dist = maybe_init_pg(world, local)
+    import paper_2203_06139_b200  # noqa: F401  (fails loudly without the CUDA library)
+    value, ms_step, roof, e2e, clocks, desc, dim, npts = bench_points(a, world, rank, local, dist)
+    secondary = []
+    if not a.no_secondary:
+        try:
+            secondary.append(bench_chi2(world, rank, local, dist))
+        except Exception as ex:  # secondary lines never hide the headline
+            secondary.append({"workload": "chi2", "error": repr(ex)[:200]})
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cores = os.cpu_count()
+        try:
+            if os.path.exists(REF_TOOL):
+                n_cpu = max(24_000, cores * 2000) if dim <= 100 else max(2_400, cores * 200)
+                if a.workload == "gauss1d":
+                    out = run_ref_tool(["gauss1d-bench", 1_000_000, 1])
+                    rate, n_cpu = 2_000_000 / out["seconds"], 1_000_000
+                else:
+                    rate, out = cpu_reference_gaussnd(dim, n_cpu)
+                cpu = {"value": rate, "unit": "pt*param/s", "cores": out.get("workers", cores),
+                       "kind": "reference",
+                       "sample": f"{n_cpu} points x {dim} dims through the unmodified reference "
+                                 f"(oracle/_ref/ref_tool) on all host threads"}
+            else:
+                rate, out = cpu_port_gaussnd(dim, 20000)
+                cpu = {"value": rate, "unit": "pt*param/s", "cores": 1, "kind": "port",
+                       "sample": "20000 points through oracle/restate.c, one core"}
+        except Exception as ex:
+            cpu = {"error": repr(ex)[:200]}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "pt*param/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device Philox RNG: p~U(-2,2), x=p+0.1*N(0,1), sigma=1.3)",
+            "config": {"workload": desc, "dim": dim, "points_per_gpu": npts,
+                       "layout": "structure-of-arrays x[d*n+i]",
+                       "l2": f"inputs {4 * 8 * npts * dim / 1e9:.1f} GB per GPU >> 126 MB L2; "
+                             "no flush needed",
+                       "parallelism": f"dp{world} (points sharded, no collective)"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": a.steps,
+            "clocks": clocks, "secondary": secondary,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="gaussnd100", choices=sorted(WORKLOADS))
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    a = ap.parse_args()
+    world, rank, local = dist_setup()
+    if a.impl == "reference":
+        reference_arm(a, world, rank)
+        return
+    ours_arm(a, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,192 @@
+/* adc_cuda.h — C ABI of the B200-native batched reverse-mode gradient engine.
+ *
+ * Drop-in boundary for the reference `adc` (arxiv/paper_2203_06139 artifact)
+ * hot path.  The reference exposes a C++ API only (no FFI); the entry points
+ * below are what its C++ call sites bind when the B200 backend is enabled
+ * (INTEGRATION.md shows the bridge a maintainer adds to launch.cpp / fit.cpp).
+ * Plain pointers and sizes, no torch or C++ types, stream-ordered, never
+ * throws.  Every function returns an adc_status; on failure the thread-local
+ * message is available from adc_cuda_last_error().
+ *
+ * There is NO CPU fallback: without a CUDA device every compute entry point
+ * returns ADC_E_CUDA.
+ */
+#ifndef ADC_CUDA_H
+#define ADC_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADC_CUDA_ABI_VERSION 1
+
+/* Status codes.  1..5 mirror adc::ErrorKind in declaration order
+ * (proj/include/adc/diag.hpp:17-23) so the C++ bridge maps them back to
+ * adc::Error(kind, message) one-to-one. */
+typedef enum adc_status {
+  ADC_OK = 0,
+  ADC_E_SEMANTIC = 1,  /* ErrorKind::Semantic */
+  ADC_E_TRANSFORM = 2, /* ErrorKind::Transform */
+  ADC_E_EVAL = 3,      /* ErrorKind::Eval: domain errors (division by zero, ...) */
+  ADC_E_LAUNCH = 4,    /* ErrorKind::Launch: config, refusal, buffer binding */
+  ADC_E_IO = 5,        /* ErrorKind::Io */
+  ADC_E_CUDA = 6,      /* CUDA runtime failure / no device */
+  ADC_E_ARG = 7        /* invalid argument to the C ABI itself */
+} adc_status;
+
+int adc_cuda_abi_version(void);
+/* Thread-local text of the last failure on this thread ("" if none). */
+const char* adc_cuda_last_error(void);
+/* Device query: SM count and compute capability of the current device. */
+int adc_cuda_device_info(int* sm_count, int* cc_major, int* cc_minor);
+
+/* ---------------------------------------------------------------------------
+ * Kernel registry.  Each hand-written kernel implements exactly one generated
+ * gradient; it is keyed by the gradient's name (gradient_name,
+ * linearize.cpp:243-258) and the FNV-1a-64 fingerprint of its printed text
+ * (adc::print(FunctionDef), printer.hpp:13).  A miss is ADC_E_LAUNCH —
+ * there is no interpreter fallback.
+ */
+uint64_t adc_cuda_fingerprint(const char* text, size_t len);
+int adc_cuda_registry_find(const char* gradient_name, uint64_t fingerprint, int32_t* kernel_id);
+int32_t adc_cuda_registry_size(void);
+const char* adc_cuda_registry_name(int32_t kernel_id);
+uint64_t adc_cuda_registry_fingerprint(int32_t kernel_id);
+
+enum {
+  ADC_KERNEL_GAUSS_GRAD_0_1 = 0,   /* proj/tests/golden/gauss_grad_0_1.golden */
+  ADC_KERNEL_GAUSSND_GRAD_0_1 = 1, /* oracle/dsl/gaussnd.dsl, wrt {x, p} */
+  ADC_KERNEL_GSUM_GRAD_1 = 2,      /* fit.cpp:125-138 model, wrt {q} */
+  ADC_KERNEL_GPOLY_GRAD_1 = 3      /* oracle/dsl/gpoly.dsl, wrt {q} */
+};
+
+/* ---------------------------------------------------------------------------
+ * Listing-1 kernel `compute` (proj/corpus/kernels.dsl:9-14) launched as
+ * adc::launch(prog, "compute", {grid_dim, block_dim, n}, buffers)
+ * (proj/src/launch.cpp:252-346): for every global index g < n,
+ *   gauss_grad_0_1(x[g], p[g], sigma, dx[g], dp[g])
+ * accumulating into dx/dp (slots are += only, never assigned).
+ * Validates like LaunchConfig::validate (launch.cpp:9-19).  Device pointers.
+ * sigma == 0 is the interpreter's "division by zero" (ADC_E_EVAL). */
+int adc_cuda_compute_gauss(int64_t grid_dim, int64_t block_dim, int64_t n, const double* x,
+                           const double* p, double sigma, double* dx, double* dp, void* stream);
+
+/* Same, host buffers: copies in, runs, copies dx/dp back, chunked over two
+ * streams so PCIe traffic overlaps the kernel.  Synchronous. */
+int adc_cuda_compute_gauss_host(int64_t grid_dim, int64_t block_dim, int64_t n, const double* x,
+                                const double* p, double sigma, double* dx, double* dp);
+
+/* ---------------------------------------------------------------------------
+ * Batched N-dim Gaussian gradient gaussnd_grad_0_1(x, p, sigma, dim, dx, dp)
+ * over n independent points.  Structure-of-arrays: coordinate d of point i is
+ * at [d * ld + i] (ld >= n) in x, p, dx, dp.  Slots accumulate.  Device
+ * pointers, stream-ordered. */
+int adc_cuda_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, const double* p,
+                          double sigma, double* dx, double* dp, void* stream);
+/* Host-buffer variant (pinned memory recommended); synchronous, pipelined. */
+int adc_cuda_gaussnd_grad_host(int64_t n, int64_t dim, int64_t ld, const double* x,
+                               const double* p, double sigma, double* dx, double* dp);
+/* Kernel selection for experiments: 0 = auto, 1 = point-per-thread
+ * (reference summation order), 2 = dims-over-warps tile. */
+int adc_cuda_gaussnd_set_variant(int32_t variant);
+
+/* ---------------------------------------------------------------------------
+ * chi2 histogram fit (FitEngine::chi2 / chi2_gradient, proj/src/fit.cpp:206-259)
+ * for model-parameterised histograms.
+ *
+ * One pass over the bins accumulates, per fixed-size chunk of bins,
+ *   [S, A1, A2, C0, G0[np], G1[np], G2[np]]     (value-only: [S, A1, A2, C0])
+ * with S = sum m_j, A1 = sum_{c>0} m_j, A2 = sum_{c>0} m_j^2/c_j,
+ * C0 = sum_{c>0} c_j, G0 = sum grad m_j, G1 = sum_{c>0} grad m_j,
+ * G2 = sum_{c>0} (m_j/c_j) grad m_j, reduced in a FIXED order (no atomics).
+ * adc_chi2_finalize turns the chunk records into chi2 and its gradient:
+ *   a = E/S, chi2 = C0 - 2a A1 + a^2 A2, T = 2 A1 - 2a A2,
+ *   grad = (E/S^2) T G0 - 2a G1 + 2a^2 G2
+ * which is exact algebra on fit.cpp:231-258.  Chunk boundaries are the same
+ * for every world size, so the result is bitwise independent of the number
+ * of GPUs the chunks were computed on.
+ */
+enum { ADC_MODEL_GSUM = 0, ADC_MODEL_GPOLY = 1 };
+
+typedef struct adc_chi2_layout {
+  int64_t bins;
+  int64_t tile_bins;   /* bins per tile (one CTA pass, fixed in-tile order) */
+  int64_t chunk_tiles; /* tiles per chunk (fixed tree) */
+  int64_t nchunks;     /* chunks over the whole histogram */
+  int64_t chunk_begin; /* this rank's chunk range [chunk_begin, chunk_end) */
+  int64_t chunk_end;
+  int64_t bin_begin; /* this rank's bin range */
+  int64_t bin_end;
+} adc_chi2_layout;
+
+/* Host-only (no device needed): the tiling and this rank's shard. */
+int adc_chi2_make_layout(int64_t bins, int32_t world, int32_t rank, adc_chi2_layout* out);
+/* Doubles per chunk record: 4 + 3*np (gradient) or 4 (value only). */
+int32_t adc_chi2_record_len(int32_t np, int32_t want_grad);
+/* Host-only: fixed-order tree over nchunks records, then the closed form
+ * above.  grad may be NULL when want_grad == 0. */
+int adc_chi2_finalize(int32_t np, double events, const double* records, int64_t nchunks,
+                      int32_t want_grad, double* grad, double* chi2);
+
+typedef struct adc_chi2_plan adc_chi2_plan;
+/* counts: DEVICE pointer to the full histogram (float64[bins]); only this
+ * rank's bin range is read.  The plan owns its workspace, a CUDA graph per
+ * pass kind and a pinned result buffer. */
+int adc_cuda_chi2_plan_create(adc_chi2_plan** plan, int32_t model, int32_t np, int64_t bins,
+                              double lo, double hi, double events, const double* counts,
+                              int32_t world, int32_t rank, void* stream);
+int adc_cuda_chi2_plan_destroy(adc_chi2_plan* plan);
+int adc_cuda_chi2_plan_layout(const adc_chi2_plan* plan, adc_chi2_layout* out);
+/* Enqueue this rank's pass: chunk records for [chunk_begin, chunk_end) are
+ * written to records_dev + (chunk - chunk_begin) * record_len (device
+ * pointer; NULL = the plan's own buffer, readable via
+ * adc_cuda_chi2_plan_records).  Stream-ordered, asynchronous. */
+int adc_cuda_chi2_partials(adc_chi2_plan* plan, const double* q, int32_t want_grad,
+                           double* records_dev);
+double* adc_cuda_chi2_plan_records(adc_chi2_plan* plan);
+/* Single-device convenience (world == 1): pass + D2H + finalize, synchronous.
+ * FitEngine::chi2_gradient(h, q, AdReverse, out) and FitEngine::chi2(h, q). */
+int adc_cuda_chi2_gradient(adc_chi2_plan* plan, const double* q, double* grad, double* chi2);
+int adc_cuda_chi2(adc_chi2_plan* plan, const double* q, double* chi2);
+/* Selects per-bin arithmetic: 0 = faithful (IEEE divisions exactly as the
+ * generated code), 1 = fast (reciprocal multiplies; within the reduction
+ * tolerance).  Default 1. */
+int adc_cuda_chi2_set_precision(adc_chi2_plan* plan, int32_t mode);
+
+/* ---------------------------------------------------------------------------
+ * Fit loop (FitEngine::fit, proj/src/fit.cpp:315-425: steepest descent with
+ * Armijo backtracking, sigma clamp) driven on the host over the device passes.
+ * clamp_idx lists the parameters the sigma clamp applies to (fit.cpp:268-278
+ * hard-codes every third index; gsum passes 2,5,8,..., gpoly passes 2). */
+typedef struct adc_fit_options {
+  int32_t budget;        /* 400 */
+  double grad_tol;       /* 1e-6 */
+  double chi2_rel_tol;   /* 1e-12 */
+  double sigma_min;      /* 1e-3 */
+  double armijo_c1;      /* 1e-4 */
+  int32_t trace_iterates;
+} adc_fit_options;
+
+typedef struct adc_fit_result {
+  double chi2;
+  int32_t iterations;
+  int32_t converged;
+  int32_t sigma_clamps;
+  uint64_t gradient_evals;
+  uint64_t chi2_evals;
+  uint64_t gradient_ns; /* host wall clock around gradient passes (fit.cpp:332-336) */
+} adc_fit_result;
+
+void adc_fit_default_options(adc_fit_options* o);
+/* params: in = init (np), out = final.  iterates: trace_iterates * np doubles
+ * (or NULL).  Single device. */
+int adc_cuda_fit(adc_chi2_plan* plan, double* params, const int32_t* clamp_idx, int32_t nclamp,
+                 const adc_fit_options* opts, adc_fit_result* result, double* iterates);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADC_CUDA_H */

@@ -525,6 +525,125 @@ int cmd_fit_in(int argc, char** argv) {
               r.iterations, r.converged ? "true" : "false", sec, engine_match ? "true" : "false");
   return engine_match ? 0 : 1;
 }
+
+// ---------------------------------------------------------------------------
+// Timed reference arms (bench.py --impl reference and the cpu_baseline leg).
+// Inputs are drawn here from mt19937_64 in the per-point layout the reference
+// evaluates; `total` evaluations cycle over `unique` points so the sample's
+// memory stays bounded while its CPU time scales.
+
+// gaussnd-bench <dim> <unique> <total> <sigma> <seed> [workers]
+int cmd_gaussnd_bench(int argc, char** argv) {
+  if (argc < 6) die("gaussnd-bench <dim> <unique> <total> <sigma> <seed> [workers]");
+  const int64_t dim = std::atoll(argv[1]);
+  const int64_t uniq = std::atoll(argv[2]);
+  const int64_t total = std::atoll(argv[3]);
+  const double sigma = std::atof(argv[4]);
+  const uint64_t seed = std::strtoull(argv[5], nullptr, 0);
+  unsigned workers = argc > 6 ? static_cast<unsigned>(std::atoi(argv[6])) : 0;
+  if (workers == 0) workers = default_workers();
+  const double spread = dim <= 100 ? 0.1 : 0.03;
+  std::mt19937_64 rng(seed);
+  std::vector<double> X(uniq * dim), P(uniq * dim);
+  std::normal_distribution<double> nd(0.0, 1.0);
+  for (int64_t k = 0; k < uniq * dim; ++k) {
+    P[k] = std::uniform_real_distribution<double>(-2, 2)(rng);
+    X[k] = P[k] + spread * nd(rng);
+  }
+  Module m = load_named("gaussnd");
+  add_gradient(m, "gaussnd", {"x", "p"});
+  Program prog(std::move(m));
+  std::atomic<int64_t> next{0};
+  std::vector<double> checksum(workers, 0.0);
+  auto body = [&](unsigned w) {
+    std::vector<double> dx(dim), dp(dim);
+    for (;;) {
+      int64_t g = next.fetch_add(1);
+      if (g >= total) break;
+      const int64_t i = g % uniq;
+      std::fill(dx.begin(), dx.end(), 0.0);
+      std::fill(dp.begin(), dp.end(), 0.0);
+      ArgPack a;
+      a.add_array(&X[i * dim], dim).add_array(&P[i * dim], dim).add_real(sigma).add_int(dim);
+      a.add_array(dx).add_array(dp);
+      prog.eval("gaussnd_grad_0_1", a);
+      checksum[w] += dx[0];
+    }
+  };
+  auto t0 = clk::now();
+  std::vector<std::thread> pool;
+  for (unsigned w = 0; w < workers; ++w) pool.emplace_back(body, w);
+  for (auto& t : pool) t.join();
+  double sec = secs(t0, clk::now());
+  double cs = 0;
+  for (double c : checksum) cs += c;
+  std::printf("{\"dim\": %lld, \"points\": %lld, \"unique\": %lld, \"seconds\": %.6f, "
+              "\"workers\": %u, \"checksum\": %.17g}\n",
+              (long long)dim, (long long)total, (long long)uniq, sec, workers, cs);
+  return 0;
+}
+
+// gauss1d-bench <n> <seed> [workers]  — adc::launch(compute) over n points.
+int cmd_gauss1d_bench(int argc, char** argv) {
+  if (argc < 3) die("gauss1d-bench <n> <seed> [workers]");
+  const int64_t n = std::atoll(argv[1]);
+  const uint64_t seed = std::strtoull(argv[2], nullptr, 0);
+  const unsigned workers = argc > 3 ? static_cast<unsigned>(std::atoi(argv[3])) : 0;
+  std::mt19937_64 rng(seed);
+  BufferSet b;
+  auto& x = b.arrays["x"];
+  auto& p = b.arrays["p"];
+  x.resize(n);
+  p.resize(n);
+  for (int64_t i = 0; i < n; ++i) {
+    x[i] = std::uniform_real_distribution<double>(-3, 3)(rng);
+    p[i] = std::uniform_real_distribution<double>(-2, 2)(rng);
+  }
+  b.arrays["dx"].assign(n, 0.0);
+  b.arrays["dp"].assign(n, 0.0);
+  b.scalars["sigma"] = 1.3;
+  Program prog(load_named("kernels"));
+  LaunchOptions lo;
+  lo.workers = workers;
+  auto t0 = clk::now();
+  launch(prog, "compute", {n / 256 + 1, 256, n}, b, lo);
+  double sec = secs(t0, clk::now());
+  std::printf("{\"points\": %lld, \"seconds\": %.6f, \"workers\": %u}\n", (long long)n, sec,
+              workers ? workers : default_workers());
+  return 0;
+}
+
+// chi2-bench <model> <bins> <passes> q...  — single-threaded, as the
+// reference's chi2_gradient is (fit.cpp:224-259); Poisson-free synthetic
+// counts (the pass cost does not depend on the values).
+int cmd_chi2_bench(int argc, char** argv) {
+  if (argc < 4) die("chi2-bench <model> <bins> <passes> q...");
+  std::string model = argv[1];
+  const int64_t bins = std::atoll(argv[2]);
+  const int passes = std::max(1, std::atoi(argv[3]));
+  std::vector<double> q;
+  for (int i = 4; i < argc; ++i) q.push_back(std::atof(argv[i]));
+  Histogram h;
+  h.bins = static_cast<int>(bins);
+  h.lo = -5.0;
+  h.hi = 5.0;
+  h.counts.resize(bins);
+  std::mt19937_64 rng(42);
+  double tot = 0;
+  for (int64_t j = 0; j < bins; ++j) {
+    h.counts[j] = (j % 100 == 0) ? 0.0 : double(50 + rng() % 100);
+    tot += h.counts[j];
+  }
+  h.events = static_cast<uint64_t>(tot);
+  ModelEngine eng = make_engine(model);
+  std::vector<double> g;
+  auto t0 = clk::now();
+  for (int r = 0; r < passes; ++r) eng.chi2_gradient(h, q, g);
+  double sec = secs(t0, clk::now());
+  std::printf("{\"bins\": %lld, \"passes\": %d, \"seconds\": %.6f, \"workers\": 1, "
+              "\"g0\": %.17g}\n", (long long)bins, passes, sec, g.empty() ? 0.0 : g[0]);
+  return 0;
+}
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -538,6 +657,9 @@ int main(int argc, char** argv) {
     if (cmd == "gaussnd-in") return cmd_gaussnd_in(argc - 1, argv + 1);
     if (cmd == "chi2-in") return cmd_chi2_in(argc - 1, argv + 1);
     if (cmd == "fit-in") return cmd_fit_in(argc - 1, argv + 1);
+    if (cmd == "gaussnd-bench") return cmd_gaussnd_bench(argc - 1, argv + 1);
+    if (cmd == "gauss1d-bench") return cmd_gauss1d_bench(argc - 1, argv + 1);
+    if (cmd == "chi2-bench") return cmd_chi2_bench(argc - 1, argv + 1);
   } catch (const Error& e) {
     std::fprintf(stderr, "ref_tool: adc::Error(kind=%d): %s\n", static_cast<int>(e.kind()),
                  e.what());

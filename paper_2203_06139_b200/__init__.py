@@ -1,0 +1,18 @@
+"""B200-native batched reverse-mode gradient engine (arxiv/paper_2203_06139 hot path).
+
+The compute path is libadc_b200.so (hand-written sm_100a CUDA behind the C ABI
+of include/adc_cuda.h); this package is the host-side mirror of the
+reference's launch/fit interfaces over that ABI.  Importing it without the
+built library raises: there is no CPU fallback.
+"""
+from ._capi import AdcError, LIB_PATH, lib  # noqa: F401
+from .launch import (BufferSet, LaunchConfig, LaunchOptions, LaunchStats, launch,  # noqa: F401
+                     launch_batch, registry_find)
+from .fit import (Chi2Plan, FitEngine, FitOptions, FitResult, Histogram, chi2_layout,  # noqa: F401
+                  finalize, record_len)
+
+__all__ = [
+    "AdcError", "BufferSet", "LaunchConfig", "LaunchOptions", "LaunchStats", "launch",
+    "launch_batch", "registry_find", "Chi2Plan", "FitEngine", "FitOptions", "FitResult",
+    "Histogram", "chi2_layout", "finalize", "record_len",
+]

@@ -1,0 +1,115 @@
+"""ctypes binding of the C ABI in include/adc_cuda.h (libadc_b200.so, in-tree).
+
+The product path: every compute call goes to the CUDA library.  If the
+library is missing this module raises at import — there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libadc_b200.so")
+
+# adc_status codes; 1..5 mirror adc::ErrorKind (proj/include/adc/diag.hpp:17-23).
+ERROR_KINDS = {1: "Semantic", 2: "Transform", 3: "Eval", 4: "Launch", 5: "Io", 6: "Cuda", 7: "Arg"}
+MODEL_IDS = {"gsum": 0, "gpoly": 1}
+
+
+class AdcError(RuntimeError):
+    """Mirror of adc::Error (diag.hpp:29-37): one exception type with a kind."""
+
+    def __init__(self, kind: str, message: str):
+        super().__init__(message)
+        self.kind = kind
+
+
+class Chi2Layout(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in (
+        "bins", "tile_bins", "chunk_tiles", "nchunks", "chunk_begin", "chunk_end", "bin_begin",
+        "bin_end")]
+
+
+class FitOptions(ctypes.Structure):
+    _fields_ = [("budget", ctypes.c_int32), ("grad_tol", ctypes.c_double),
+                ("chi2_rel_tol", ctypes.c_double), ("sigma_min", ctypes.c_double),
+                ("armijo_c1", ctypes.c_double), ("trace_iterates", ctypes.c_int32)]
+
+
+class FitResultC(ctypes.Structure):
+    _fields_ = [("chi2", ctypes.c_double), ("iterations", ctypes.c_int32),
+                ("converged", ctypes.c_int32), ("sigma_clamps", ctypes.c_int32),
+                ("gradient_evals", ctypes.c_uint64), ("chi2_evals", ctypes.c_uint64),
+                ("gradient_ns", ctypes.c_uint64)]
+
+
+_D = ctypes.POINTER(ctypes.c_double)
+_VP = ctypes.c_void_p
+_I64, _I32, _DBL = ctypes.c_int64, ctypes.c_int32, ctypes.c_double
+
+# name -> (restype, argtypes); every symbol declared in include/adc_cuda.h.
+SIGNATURES = {
+    "adc_cuda_abi_version": (ctypes.c_int, []),
+    "adc_cuda_last_error": (ctypes.c_char_p, []),
+    "adc_cuda_device_info": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)] * 3),
+    "adc_cuda_fingerprint": (ctypes.c_uint64, [ctypes.c_char_p, ctypes.c_size_t]),
+    "adc_cuda_registry_find": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_uint64,
+                                              ctypes.POINTER(_I32)]),
+    "adc_cuda_registry_size": (_I32, []),
+    "adc_cuda_registry_name": (ctypes.c_char_p, [_I32]),
+    "adc_cuda_registry_fingerprint": (ctypes.c_uint64, [_I32]),
+    "adc_cuda_compute_gauss": (ctypes.c_int, [_I64, _I64, _I64, _VP, _VP, _DBL, _VP, _VP, _VP]),
+    "adc_cuda_compute_gauss_host": (ctypes.c_int, [_I64, _I64, _I64, _VP, _VP, _DBL, _VP, _VP]),
+    "adc_cuda_gaussnd_grad": (ctypes.c_int, [_I64, _I64, _I64, _VP, _VP, _DBL, _VP, _VP, _VP]),
+    "adc_cuda_gaussnd_grad_host": (ctypes.c_int, [_I64, _I64, _I64, _VP, _VP, _DBL, _VP, _VP]),
+    "adc_cuda_gaussnd_set_variant": (ctypes.c_int, [_I32]),
+    "adc_chi2_make_layout": (ctypes.c_int, [_I64, _I32, _I32, ctypes.POINTER(Chi2Layout)]),
+    "adc_chi2_record_len": (_I32, [_I32, _I32]),
+    "adc_chi2_finalize": (ctypes.c_int, [_I32, _DBL, _D, _I64, _I32, _D, _D]),
+    "adc_cuda_chi2_plan_create": (ctypes.c_int, [ctypes.POINTER(_VP), _I32, _I32, _I64, _DBL,
+                                                 _DBL, _DBL, _VP, _I32, _I32, _VP]),
+    "adc_cuda_chi2_plan_destroy": (ctypes.c_int, [_VP]),
+    "adc_cuda_chi2_plan_layout": (ctypes.c_int, [_VP, ctypes.POINTER(Chi2Layout)]),
+    "adc_cuda_chi2_partials": (ctypes.c_int, [_VP, _D, _I32, _VP]),
+    "adc_cuda_chi2_plan_records": (_VP, [_VP]),
+    "adc_cuda_chi2_gradient": (ctypes.c_int, [_VP, _D, _D, _D]),
+    "adc_cuda_chi2": (ctypes.c_int, [_VP, _D, _D]),
+    "adc_cuda_chi2_set_precision": (ctypes.c_int, [_VP, _I32]),
+    "adc_fit_default_options": (None, [ctypes.POINTER(FitOptions)]),
+    "adc_cuda_fit": (ctypes.c_int, [_VP, _D, ctypes.POINTER(_I32), _I32,
+                                    ctypes.POINTER(FitOptions), ctypes.POINTER(FitResultC), _D]),
+}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+            "g.build()'` (make -C paper_2203_06139_b200/csrc). There is no CPU fallback.")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def check(rc: int):
+    if rc != 0:
+        msg = lib.adc_cuda_last_error().decode()
+        raise AdcError(ERROR_KINDS.get(rc, str(rc)), msg)
+
+
+def dptr(a) -> ctypes.c_void_p:
+    """Pointer of a torch tensor (device or host) or a numpy array."""
+    if hasattr(a, "data_ptr"):
+        return ctypes.c_void_p(a.data_ptr())
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def dbl_array(values):
+    arr = (ctypes.c_double * len(values))(*[float(v) for v in values])
+    return arr

@@ -1,0 +1,273 @@
+// C ABI (include/adc_cuda.h): error state, device query, kernel registry,
+// argument validation mirroring the reference's launch contract, and the
+// host-buffer pipelines (H2D / kernel / D2H overlapped over two streams).
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+
+namespace adcb {
+
+int launch_gauss_grad(int64_t n, const double* x, const double* p, double sigma, double* dx,
+                      double* dp, cudaStream_t stream);
+int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, const double* p,
+                        double sigma, double* dx, double* dp, cudaStream_t s);
+int gaussnd_set_variant(int v);
+
+static thread_local std::string t_error;
+
+void set_error(const std::string& msg) { t_error = msg; }
+void clear_error() { t_error.clear(); }
+int fail(int code, const std::string& msg) {
+  t_error = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  t_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return ADC_E_CUDA;
+}
+
+static int g_sm_count[64] = {0};
+int sm_count() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (g_sm_count[dev] == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    g_sm_count[dev] = v > 0 ? v : 148;
+  }
+  return g_sm_count[dev];
+}
+
+bool device_present() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    return false;
+  }
+  return true;
+}
+
+// Checks a device exists and is sm_100 (the only architecture compiled).
+static int require_device() {
+  if (!device_present())
+    return fail(ADC_E_CUDA, "no CUDA device: the B200 engine has no CPU fallback");
+  int dev = 0, major = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (major != 10) return fail(ADC_E_CUDA, "device is not sm_100 (built for sm_100a only)");
+  return ADC_OK;
+}
+
+// Device staging for the host-buffer pipelines (grown on demand, reused).
+struct Staging {
+  std::mutex mu;
+  int device = -1;
+  size_t bytes = 0;
+  double* buf[2] = {nullptr, nullptr};
+  cudaStream_t stream[2] = {nullptr, nullptr};
+  int ensure(size_t need) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (device != dev) {
+      release();
+      device = dev;
+    }
+    if (stream[0] == nullptr) {
+      ADCB_CUDA(cudaStreamCreateWithFlags(&stream[0], cudaStreamNonBlocking));
+      ADCB_CUDA(cudaStreamCreateWithFlags(&stream[1], cudaStreamNonBlocking));
+    }
+    if (need <= bytes) return ADC_OK;
+    for (auto& b : buf)
+      if (b) cudaFree(b), b = nullptr;
+    bytes = 0;
+    for (auto& b : buf) ADCB_CUDA(cudaMalloc(&b, need));
+    bytes = need;
+    return ADC_OK;
+  }
+  void release() {
+    for (auto& b : buf)
+      if (b) cudaFree(b), b = nullptr;
+    for (auto& s : stream)
+      if (s) cudaStreamDestroy(s), s = nullptr;
+    bytes = 0;
+  }
+};
+static Staging g_staging;
+
+}  // namespace adcb
+
+using namespace adcb;
+
+// ---------------------------------------------------------------------------
+extern "C" int adc_cuda_abi_version(void) { return ADC_CUDA_ABI_VERSION; }
+extern "C" const char* adc_cuda_last_error(void) { return t_error.c_str(); }
+
+extern "C" int adc_cuda_device_info(int* sms, int* cc_major, int* cc_minor) {
+  clear_error();
+  if (!device_present()) return fail(ADC_E_CUDA, "no CUDA device");
+  int dev = 0;
+  ADCB_CUDA(cudaGetDevice(&dev));
+  if (sms) ADCB_CUDA(cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, dev));
+  if (cc_major) ADCB_CUDA(cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, dev));
+  if (cc_minor) ADCB_CUDA(cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, dev));
+  return ADC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Registry.  Fingerprints are FNV-1a-64 of adc::print(<generated gradient>)
+// as produced by the unmodified reference (tests/golden/gradient_fingerprints.json,
+// written by tests/golden/make_golden.py through oracle/_ref/ref_tool).
+namespace {
+struct RegEntry {
+  const char* name;
+  uint64_t fingerprint;
+};
+constexpr RegEntry kRegistry[] = {
+    {"gauss_grad_0_1", 0xf7c0f9e804312d53ull},
+    {"gaussnd_grad_0_1", 0x4676b5ba30fbac81ull},
+    {"gsum_grad_1", 0x04bab8a0562c8d71ull},
+    {"gpoly_grad_1", 0xfe0da677548ccdafull},
+};
+constexpr int32_t kRegistrySize = sizeof(kRegistry) / sizeof(kRegistry[0]);
+}  // namespace
+
+extern "C" uint64_t adc_cuda_fingerprint(const char* text, size_t len) {
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (size_t i = 0; i < len; ++i) {
+    h ^= static_cast<unsigned char>(text[i]);
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+
+extern "C" int adc_cuda_registry_find(const char* name, uint64_t fp, int32_t* id) {
+  clear_error();
+  if (name == nullptr || id == nullptr) return fail(ADC_E_ARG, "null argument");
+  for (int32_t k = 0; k < kRegistrySize; ++k) {
+    if (std::strcmp(kRegistry[k].name, name) != 0) continue;
+    if (kRegistry[k].fingerprint != fp)
+      return fail(ADC_E_LAUNCH, std::string("no B200 kernel for this body of '") + name +
+                                    "': generated text differs from the registered gradient");
+    *id = k;
+    return ADC_OK;
+  }
+  return fail(ADC_E_LAUNCH, std::string("no B200 kernel registered for '") + name + "'");
+}
+
+extern "C" int32_t adc_cuda_registry_size(void) { return kRegistrySize; }
+extern "C" const char* adc_cuda_registry_name(int32_t id) {
+  return id >= 0 && id < kRegistrySize ? kRegistry[id].name : nullptr;
+}
+extern "C" uint64_t adc_cuda_registry_fingerprint(int32_t id) {
+  return id >= 0 && id < kRegistrySize ? kRegistry[id].fingerprint : 0;
+}
+
+// ---------------------------------------------------------------------------
+// LaunchConfig::validate (launch.cpp:9-19), same messages.
+static int validate_config(int64_t grid, int64_t block, int64_t n) {
+  if (grid <= 0 || block <= 0 || n <= 0)
+    return fail(ADC_E_LAUNCH, "launch configuration must be positive (grid " +
+                                  std::to_string(grid) + ", block " + std::to_string(block) +
+                                  ", n " + std::to_string(n) + ")");
+  if (grid > INT64_MAX / block || grid * block < n)
+    return fail(ADC_E_LAUNCH, "grid " + std::to_string(grid) + " x block " +
+                                  std::to_string(block) + " does not cover problem size " +
+                                  std::to_string(n));
+  return ADC_OK;
+}
+
+extern "C" int adc_cuda_compute_gauss(int64_t grid, int64_t block, int64_t n, const double* x,
+                                      const double* p, double sigma, double* dx, double* dp,
+                                      void* stream) {
+  clear_error();
+  if (int rc = validate_config(grid, block, n)) return rc;
+  if (!x || !p || !dx || !dp) return fail(ADC_E_LAUNCH, "missing buffer");
+  if (int rc = require_device()) return rc;
+  return launch_gauss_grad(n, x, p, sigma, dx, dp, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int adc_cuda_compute_gauss_host(int64_t grid, int64_t block, int64_t n,
+                                           const double* x, const double* p, double sigma,
+                                           double* dx, double* dp) {
+  clear_error();
+  if (int rc = validate_config(grid, block, n)) return rc;
+  if (!x || !p || !dx || !dp) return fail(ADC_E_LAUNCH, "missing buffer");
+  if (int rc = require_device()) return rc;
+  std::lock_guard<std::mutex> lock(g_staging.mu);
+  const int64_t chunk = std::min<int64_t>(n, int64_t(16) << 20);  // points per stage
+  if (int rc = g_staging.ensure((size_t)chunk * 4 * sizeof(double))) return rc;
+  for (int64_t i0 = 0, k = 0; i0 < n; i0 += chunk, ++k) {
+    const int64_t c = std::min(chunk, n - i0);
+    cudaStream_t s = g_staging.stream[k & 1];
+    double* b = g_staging.buf[k & 1];
+    double *X = b, *P = b + chunk, *DX = b + 2 * chunk, *DP = b + 3 * chunk;
+    const size_t bytes = (size_t)c * sizeof(double);
+    ADCB_CUDA(cudaMemcpyAsync(X, x + i0, bytes, cudaMemcpyHostToDevice, s));
+    ADCB_CUDA(cudaMemcpyAsync(P, p + i0, bytes, cudaMemcpyHostToDevice, s));
+    ADCB_CUDA(cudaMemcpyAsync(DX, dx + i0, bytes, cudaMemcpyHostToDevice, s));
+    ADCB_CUDA(cudaMemcpyAsync(DP, dp + i0, bytes, cudaMemcpyHostToDevice, s));
+    if (int rc = launch_gauss_grad(c, X, P, sigma, DX, DP, s)) return rc;
+    ADCB_CUDA(cudaMemcpyAsync(dx + i0, DX, bytes, cudaMemcpyDeviceToHost, s));
+    ADCB_CUDA(cudaMemcpyAsync(dp + i0, DP, bytes, cudaMemcpyDeviceToHost, s));
+  }
+  ADCB_CUDA(cudaStreamSynchronize(g_staging.stream[0]));
+  ADCB_CUDA(cudaStreamSynchronize(g_staging.stream[1]));
+  return ADC_OK;
+}
+
+// ---------------------------------------------------------------------------
+extern "C" int adc_cuda_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x,
+                                     const double* p, double sigma, double* dx, double* dp,
+                                     void* stream) {
+  clear_error();
+  if (n < 0 || dim < 0) return fail(ADC_E_LAUNCH, "gaussnd: negative size");
+  if (ld < n) return fail(ADC_E_LAUNCH, "gaussnd: leading dimension smaller than n");
+  if (n > 0 && dim > 0 && (!x || !p || !dx || !dp)) return fail(ADC_E_LAUNCH, "missing buffer");
+  if (int rc = require_device()) return rc;
+  return launch_gaussnd_grad(n, dim, ld, x, p, sigma, dx, dp, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int adc_cuda_gaussnd_grad_host(int64_t n, int64_t dim, int64_t ld, const double* x,
+                                          const double* p, double sigma, double* dx, double* dp) {
+  clear_error();
+  if (n < 0 || dim < 0) return fail(ADC_E_LAUNCH, "gaussnd: negative size");
+  if (ld < n) return fail(ADC_E_LAUNCH, "gaussnd: leading dimension smaller than n");
+  if (n > 0 && dim > 0 && (!x || !p || !dx || !dp)) return fail(ADC_E_LAUNCH, "missing buffer");
+  if (int rc = require_device()) return rc;
+  if (n == 0) return launch_gaussnd_grad(0, dim, ld, x, p, sigma, dx, dp, nullptr);
+  if (dim == 0) return launch_gaussnd_grad(n, 0, n, x, p, sigma, dx, dp, nullptr);
+  std::lock_guard<std::mutex> lock(g_staging.mu);
+  // ~512 MB per array per stage; a whole number of 32-point tiles.
+  int64_t chunk = (int64_t(512) << 20) / (dim * (int64_t)sizeof(double));
+  chunk = std::max<int64_t>(32, chunk / 32 * 32);
+  chunk = std::min(chunk, n);
+  if (int rc = g_staging.ensure((size_t)chunk * dim * 4 * sizeof(double))) return rc;
+  const size_t spitch = (size_t)ld * sizeof(double);
+  for (int64_t i0 = 0, k = 0; i0 < n; i0 += chunk, ++k) {
+    const int64_t c = std::min(chunk, n - i0);
+    cudaStream_t s = g_staging.stream[k & 1];
+    double* b = g_staging.buf[k & 1];
+    const size_t plane = (size_t)chunk * dim;
+    double *X = b, *P = b + plane, *DX = b + 2 * plane, *DP = b + 3 * plane;
+    const size_t w = (size_t)c * sizeof(double), dpitch = (size_t)chunk * sizeof(double);
+    ADCB_CUDA(cudaMemcpy2DAsync(X, dpitch, x + i0, spitch, w, dim, cudaMemcpyHostToDevice, s));
+    ADCB_CUDA(cudaMemcpy2DAsync(P, dpitch, p + i0, spitch, w, dim, cudaMemcpyHostToDevice, s));
+    ADCB_CUDA(cudaMemcpy2DAsync(DX, dpitch, dx + i0, spitch, w, dim, cudaMemcpyHostToDevice, s));
+    ADCB_CUDA(cudaMemcpy2DAsync(DP, dpitch, dp + i0, spitch, w, dim, cudaMemcpyHostToDevice, s));
+    if (int rc = launch_gaussnd_grad(c, dim, chunk, X, P, sigma, DX, DP, s)) return rc;
+    ADCB_CUDA(cudaMemcpy2DAsync(dx + i0, spitch, DX, dpitch, w, dim, cudaMemcpyDeviceToHost, s));
+    ADCB_CUDA(cudaMemcpy2DAsync(dp + i0, spitch, DP, dpitch, w, dim, cudaMemcpyDeviceToHost, s));
+  }
+  ADCB_CUDA(cudaStreamSynchronize(g_staging.stream[0]));
+  ADCB_CUDA(cudaStreamSynchronize(g_staging.stream[1]));
+  return ADC_OK;
+}
+
+extern "C" int adc_cuda_gaussnd_set_variant(int32_t v) {
+  clear_error();
+  return gaussnd_set_variant(v);
+}

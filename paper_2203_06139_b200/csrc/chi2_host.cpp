@@ -1,0 +1,393 @@
+// Host side of the chi2 pass: tiling/sharding layout, the fixed-order final
+// reduction + closed form (adc_chi2_finalize), the per-histogram plan (device
+// workspace, pinned staging, one CUDA graph per pass kind) and the fit loop
+// (FitEngine::fit, proj/src/fit.cpp:315-425).
+//
+// Compiled with -ffp-contract=off: every host-side double expression here is
+// evaluated operation by operation, like the reference's fit.cpp.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "chi2_internal.h"
+#include "common.cuh"
+
+using namespace adcb;
+
+namespace {
+
+constexpr int64_t kChunkTiles = 128;
+constexpr int64_t kTileThreads = 256;
+
+int bpt_for(int64_t bins) { return bins >= (int64_t(1) << 22) ? 32 : 4; }
+
+}  // namespace
+
+extern "C" int adc_chi2_make_layout(int64_t bins, int32_t world, int32_t rank,
+                                    adc_chi2_layout* out) {
+  clear_error();
+  if (out == nullptr) return fail(ADC_E_ARG, "layout: null output");
+  if (bins <= 0) return fail(ADC_E_ARG, "histogram must have at least one bin");
+  if (world <= 0 || rank < 0 || rank >= world) return fail(ADC_E_ARG, "bad rank/world");
+  adc_chi2_layout L{};
+  L.bins = bins;
+  L.tile_bins = bpt_for(bins) * kTileThreads;
+  L.chunk_tiles = kChunkTiles;
+  const int64_t ntiles = (bins + L.tile_bins - 1) / L.tile_bins;
+  L.nchunks = (ntiles + kChunkTiles - 1) / kChunkTiles;
+  L.chunk_begin = L.nchunks * rank / world;
+  L.chunk_end = L.nchunks * (rank + 1) / world;
+  const int64_t chunk_bins = L.tile_bins * kChunkTiles;
+  L.bin_begin = std::min(bins, L.chunk_begin * chunk_bins);
+  L.bin_end = std::min(bins, L.chunk_end * chunk_bins);
+  *out = L;
+  return ADC_OK;
+}
+
+extern "C" int32_t adc_chi2_record_len(int32_t np, int32_t want_grad) {
+  return want_grad ? 4 + 3 * np : 4;
+}
+
+extern "C" int adc_chi2_finalize(int32_t np, double events, const double* records,
+                                 int64_t nchunks, int32_t want_grad, double* grad, double* chi2) {
+  clear_error();
+  if (records == nullptr || nchunks <= 0) return fail(ADC_E_ARG, "finalize: no records");
+  if (np <= 0 || np > kMaxNp) return fail(ADC_E_ARG, "finalize: bad parameter count");
+  const int R = adc_chi2_record_len(np, want_grad);
+  std::vector<double> r(records, records + nchunks * R);
+  // Fixed pairwise tree over chunks (stride doubling), identical for any
+  // sharding of the chunks over GPUs.
+  for (int64_t s = 1; s < nchunks; s *= 2)
+    for (int64_t i = 0; i + s < nchunks; i += 2 * s)
+      for (int v = 0; v < R; ++v) r[i * R + v] = r[i * R + v] + r[(i + s) * R + v];
+  const double S = r[0], A1 = r[1], A2 = r[2], C0 = r[3];
+  const double a = events / S;  // chi2: scale = E/S (fit.cpp:214)
+  if (chi2 != nullptr) {
+    // sum_{c>0} (c - a m)^2 / c = C0 - 2a A1 + a^2 A2
+    const double two_a = 2.0 * a;
+    *chi2 = (C0 - two_a * A1) + (a * a) * A2;
+  }
+  if (want_grad && grad != nullptr) {
+    // T = sum_{c>0} 2 r m / c = 2 A1 - 2a A2; s_coef = E/S^2 * T (fit.cpp:238-245)
+    const double t_sum = 2.0 * A1 - (2.0 * a) * A2;
+    const double s_coef = events / (S * S) * t_sum;
+    // w_j = s_coef + [c>0](-2 r_j / c_j * E / S)  =>  sum_j w_j dm_j
+    //     = s_coef G0 - 2a (G1 - a G2)          (fit.cpp:248-258)
+    const double* G0 = &r[4];
+    const double* G1 = &r[4 + np];
+    const double* G2 = &r[4 + 2 * np];
+    for (int i = 0; i < np; ++i) grad[i] = s_coef * G0[i] - (2.0 * a) * (G1[i] - a * G2[i]);
+  }
+  return ADC_OK;
+}
+
+// ---------------------------------------------------------------------------
+struct adc_chi2_plan {
+  int model = 0, np = 0;
+  int64_t bins = 0;
+  double lo = 0, hi = 0, events = 0, width = 0;
+  const double* counts = nullptr;
+  adc_chi2_layout L{};
+  int bpt = 4;
+  int fast = 1;
+  int device = 0;
+  cudaStream_t stream = nullptr;       // plan-owned: graph replays
+  cudaStream_t user_stream = nullptr;  // caller's: adc_cuda_chi2_partials
+  double* qdev = nullptr;
+  double* tile_ws = nullptr;
+  double* records = nullptr;
+  double* h_q = nullptr;
+  double* h_rec = nullptr;
+  cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [grad][fast]
+};
+
+namespace {
+
+int check_domain(const adc_chi2_plan* P, const double* q) {
+  // Divisions by the width parameters are the interpreter's checked
+  // divisions (eval.cpp:543) in gpoly/gsum and their gradients.
+  if (P->model == ADC_MODEL_GPOLY) {
+    if (q[2] == 0.0) return fail(ADC_E_EVAL, "division by zero");
+  } else {
+    for (int j = 2; j < P->np; j += 3)
+      if (q[j] == 0.0) return fail(ADC_E_EVAL, "division by zero");
+  }
+  return ADC_OK;
+}
+
+Chi2Pass make_pass(const adc_chi2_plan* P) {
+  Chi2Pass pass{};
+  pass.counts = P->counts;
+  pass.qdev = P->qdev;
+  pass.tile_ws = P->tile_ws;
+  pass.lo = P->lo;
+  pass.width = P->width;
+  pass.bin_end = P->L.bin_end;
+  pass.tile_begin = P->L.chunk_begin * P->L.chunk_tiles;
+  pass.tile_end = (P->L.bin_end + P->L.tile_bins - 1) / P->L.tile_bins;
+  if (pass.tile_end < pass.tile_begin) pass.tile_end = pass.tile_begin;
+  return pass;
+}
+
+int64_t local_chunks(const adc_chi2_plan* P) { return P->L.chunk_end - P->L.chunk_begin; }
+
+int build_graph(adc_chi2_plan* P, int grad) {
+  cudaGraph_t g = nullptr;
+  ADCB_CUDA(cudaStreamBeginCapture(P->stream, cudaStreamCaptureModeThreadLocal));
+  cudaMemcpyAsync(P->qdev, P->h_q, qdev_bytes(), cudaMemcpyHostToDevice, P->stream);
+  int rc = chi2_enqueue(make_pass(P), P->model, P->np, grad != 0, P->fast != 0, P->bpt,
+                        P->L.chunk_tiles, P->records, P->stream);
+  const size_t rec_bytes =
+      (size_t)local_chunks(P) * adc_chi2_record_len(P->np, grad) * sizeof(double);
+  cudaMemcpyAsync(P->h_rec, P->records, rec_bytes, cudaMemcpyDeviceToHost, P->stream);
+  cudaError_t e = cudaStreamEndCapture(P->stream, &g);
+  if (rc != ADC_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+  e = cudaGraphInstantiate(&P->graph[grad][P->fast], g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+  return ADC_OK;
+}
+
+// One single-device pass through the captured graph; leaves the records in
+// h_rec.
+int run_pass(adc_chi2_plan* P, const double* q, int grad) {
+  if (P->L.chunk_begin != 0 || P->L.chunk_end != P->L.nchunks)
+    return fail(ADC_E_ARG, "sharded plan: use adc_cuda_chi2_partials + adc_chi2_finalize");
+  if (int rc = check_domain(P, q)) return rc;
+  ADCB_CUDA(cudaSetDevice(P->device));
+  fill_qdev(P->model, P->np, q, P->h_q);
+  if (P->graph[grad][P->fast] == nullptr)
+    if (int rc = build_graph(P, grad)) return rc;
+  ADCB_CUDA(cudaGraphLaunch(P->graph[grad][P->fast], P->stream));
+  ADCB_CUDA(cudaStreamSynchronize(P->stream));
+  return ADC_OK;
+}
+
+}  // namespace
+
+extern "C" int adc_cuda_chi2_plan_create(adc_chi2_plan** out, int32_t model, int32_t np,
+                                         int64_t bins, double lo, double hi, double events,
+                                         const double* counts, int32_t world, int32_t rank,
+                                         void* stream) {
+  clear_error();
+  if (out == nullptr) return fail(ADC_E_ARG, "plan: null output");
+  *out = nullptr;
+  if (!device_present()) return fail(ADC_E_CUDA, "no CUDA device: the B200 engine has no CPU fallback");
+  if (model != ADC_MODEL_GSUM && model != ADC_MODEL_GPOLY) return fail(ADC_E_ARG, "unknown model");
+  if (model == ADC_MODEL_GPOLY && np != 6) return fail(ADC_E_ARG, "gpoly has 6 parameters");
+  if (model == ADC_MODEL_GSUM) {
+    const int k = np / 3;
+    if (np % 3 != 0 || !(k == 1 || k == 2 || k == 3 || k == 4 || k == 8))
+      return fail(ADC_E_ARG, "gsum: parameter count must be 3K with K in {1,2,3,4,8}");
+  }
+  if (counts == nullptr) return fail(ADC_E_ARG, "plan: null counts");
+  if (!(hi > lo)) return fail(ADC_E_EVAL, "degenerate histogram range");
+  adc_chi2_plan* P = new (std::nothrow) adc_chi2_plan();
+  if (P == nullptr) return fail(ADC_E_CUDA, "out of host memory");
+  if (int rc = adc_chi2_make_layout(bins, world, rank, &P->L)) {
+    delete P;
+    return rc;
+  }
+  P->model = model;
+  P->np = np;
+  P->bins = bins;
+  P->lo = lo;
+  P->hi = hi;
+  P->events = events;
+  P->width = (hi - lo) / static_cast<double>(bins);  // Histogram::width (fit.hpp:30)
+  P->counts = counts;
+  P->bpt = bpt_for(bins);
+  cudaGetDevice(&P->device);
+  auto cleanup = [&](int rc) {
+    adc_cuda_chi2_plan_destroy(P);
+    return rc;
+  };
+  P->user_stream = static_cast<cudaStream_t>(stream);
+  if (stream != nullptr) {
+    cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cleanup(cuda_fail(e, "cudaStreamSynchronize"));
+  }
+  const int64_t ntiles_local = std::max<int64_t>(
+      1, (P->L.bin_end + P->L.tile_bins - 1) / P->L.tile_bins - P->L.chunk_begin * P->L.chunk_tiles);
+  const int Rmax = adc_chi2_record_len(np, 1);
+  const int64_t nrec = std::max<int64_t>(1, local_chunks(P));
+  cudaError_t e;
+  if ((e = cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaMalloc(&P->qdev, qdev_bytes())) != cudaSuccess ||
+      (e = cudaMalloc(&P->tile_ws, (size_t)ntiles_local * Rmax * sizeof(double))) != cudaSuccess ||
+      (e = cudaMalloc(&P->records, (size_t)nrec * Rmax * sizeof(double))) != cudaSuccess ||
+      (e = cudaMallocHost(&P->h_q, qdev_bytes())) != cudaSuccess ||
+      (e = cudaMallocHost(&P->h_rec, (size_t)nrec * Rmax * sizeof(double))) != cudaSuccess)
+    return cleanup(cuda_fail(e, "chi2 plan allocation"));
+  *out = P;
+  return ADC_OK;
+}
+
+extern "C" int adc_cuda_chi2_plan_destroy(adc_chi2_plan* P) {
+  if (P == nullptr) return ADC_OK;
+  for (auto& row : P->graph)
+    for (auto& g : row)
+      if (g) cudaGraphExecDestroy(g);
+  if (P->qdev) cudaFree(P->qdev);
+  if (P->tile_ws) cudaFree(P->tile_ws);
+  if (P->records) cudaFree(P->records);
+  if (P->h_q) cudaFreeHost(P->h_q);
+  if (P->h_rec) cudaFreeHost(P->h_rec);
+  if (P->stream) cudaStreamDestroy(P->stream);
+  delete P;
+  return ADC_OK;
+}
+
+extern "C" int adc_cuda_chi2_plan_layout(const adc_chi2_plan* P, adc_chi2_layout* out) {
+  clear_error();
+  if (P == nullptr || out == nullptr) return fail(ADC_E_ARG, "null plan");
+  *out = P->L;
+  return ADC_OK;
+}
+
+extern "C" int adc_cuda_chi2_set_precision(adc_chi2_plan* P, int32_t mode) {
+  clear_error();
+  if (P == nullptr || (mode != 0 && mode != 1)) return fail(ADC_E_ARG, "precision mode is 0 or 1");
+  P->fast = mode;
+  return ADC_OK;
+}
+
+extern "C" double* adc_cuda_chi2_plan_records(adc_chi2_plan* P) {
+  return P ? P->records : nullptr;
+}
+
+extern "C" int adc_cuda_chi2_partials(adc_chi2_plan* P, const double* q, int32_t want_grad,
+                                      double* records_dev) {
+  clear_error();
+  if (P == nullptr || q == nullptr) return fail(ADC_E_ARG, "null argument");
+  if (int rc = check_domain(P, q)) return rc;
+  ADCB_CUDA(cudaSetDevice(P->device));
+  cudaStream_t s = P->user_stream ? P->user_stream : P->stream;
+  // h_q may still be read by an in-flight copy of a previous pass
+  ADCB_CUDA(cudaStreamSynchronize(s));
+  fill_qdev(P->model, P->np, q, P->h_q);
+  ADCB_CUDA(cudaMemcpyAsync(P->qdev, P->h_q, qdev_bytes(), cudaMemcpyHostToDevice, s));
+  return chi2_enqueue(make_pass(P), P->model, P->np, want_grad != 0, P->fast != 0, P->bpt,
+                      P->L.chunk_tiles, records_dev ? records_dev : P->records, s);
+}
+
+extern "C" int adc_cuda_chi2_gradient(adc_chi2_plan* P, const double* q, double* grad,
+                                      double* chi2) {
+  clear_error();
+  if (P == nullptr || q == nullptr || grad == nullptr) return fail(ADC_E_ARG, "null argument");
+  if (int rc = run_pass(P, q, 1)) return rc;
+  return adc_chi2_finalize(P->np, P->events, P->h_rec, P->L.nchunks, 1, grad, chi2);
+}
+
+extern "C" int adc_cuda_chi2(adc_chi2_plan* P, const double* q, double* chi2) {
+  clear_error();
+  if (P == nullptr || q == nullptr || chi2 == nullptr) return fail(ADC_E_ARG, "null argument");
+  if (int rc = run_pass(P, q, 0)) return rc;
+  return adc_chi2_finalize(P->np, P->events, P->h_rec, P->L.nchunks, 0, nullptr, chi2);
+}
+
+// ---------------------------------------------------------------------------
+// Fit loop: FitEngine::fit (fit.cpp:315-425), steepest descent with Armijo
+// backtracking, generalised sigma clamp (fit.cpp:268-278 hard-codes every
+// third index, which is only right for gsum).  The optional numeric-Hessian
+// Newton step (fit.cpp:346-381, off by default) is not part of this path.
+extern "C" void adc_fit_default_options(adc_fit_options* o) {
+  o->budget = 400;
+  o->grad_tol = 1e-6;
+  o->chi2_rel_tol = 1e-12;
+  o->sigma_min = 1e-3;
+  o->armijo_c1 = 1e-4;
+  o->trace_iterates = 0;
+}
+
+extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* clamp_idx,
+                            int32_t nclamp, const adc_fit_options* opts, adc_fit_result* result,
+                            double* iterates) {
+  using clk = std::chrono::steady_clock;
+  clear_error();
+  if (P == nullptr || params == nullptr || opts == nullptr || result == nullptr)
+    return fail(ADC_E_ARG, "null argument");
+  const int np = P->np;
+  auto clamp = [&](std::vector<double>& q) {
+    int n = 0;
+    for (int k = 0; k < nclamp; ++k) {
+      const int i = clamp_idx[k];
+      if (i >= 0 && i < np && q[i] < opts->sigma_min) {
+        q[i] = opts->sigma_min;
+        ++n;
+      }
+    }
+    return n;
+  };
+  adc_fit_result res{};
+  std::vector<double> q(params, params + np);
+  res.sigma_clamps += clamp(q);
+  int traced = 0;
+  auto trace = [&](const std::vector<double>& v) {
+    if (iterates != nullptr && traced < opts->trace_iterates) {
+      std::memcpy(iterates + (size_t)traced * np, v.data(), np * sizeof(double));
+      ++traced;
+    }
+  };
+  double cur = 0.0;
+  if (int rc = adc_cuda_chi2(P, q.data(), &cur)) return rc;
+  ++res.chi2_evals;
+  if (opts->trace_iterates > 0) trace(q);
+  std::vector<double> g(np), trial(np);
+  for (int iter = 0; iter < opts->budget; ++iter) {
+    auto t0 = clk::now();
+    if (int rc = adc_cuda_chi2_gradient(P, q.data(), g.data(), nullptr)) return rc;
+    res.gradient_ns += (uint64_t)std::chrono::nanoseconds(clk::now() - t0).count();
+    ++res.gradient_evals;
+    double gmax = 0.0;
+    for (double v : g) gmax = std::max(gmax, std::fabs(v));
+    if (gmax <= opts->grad_tol) {
+      res.converged = 1;
+      break;
+    }
+    double gd = 0.0;
+    for (int i = 0; i < np; ++i) gd += g[i] * g[i];
+    double t = 1.0, next = 0.0;
+    bool accepted = false;
+    while (t >= 1e-18) {
+      trial = q;
+      for (int i = 0; i < np; ++i) trial[i] -= t * g[i];
+      const int cl = clamp(trial);
+      double c2 = 0.0;
+      if (int rc = adc_cuda_chi2(P, trial.data(), &c2)) return rc;
+      ++res.chi2_evals;
+      if (c2 <= cur - opts->armijo_c1 * t * gd) {
+        accepted = true;
+        next = c2;
+        res.sigma_clamps += cl;
+        break;
+      }
+      t *= 0.5;
+    }
+    if (!accepted) {
+      res.converged = 1;
+      break;
+    }
+    const double rel_dec = (cur - next) / std::max(1.0, std::fabs(cur));
+    q = trial;
+    cur = next;
+    ++res.iterations;
+    if (opts->trace_iterates > res.iterations) trace(q);
+    if (rel_dec <= opts->chi2_rel_tol) {
+      res.converged = 1;
+      break;
+    }
+  }
+  std::memcpy(params, q.data(), np * sizeof(double));
+  res.chi2 = cur;
+  *result = res;
+  return ADC_OK;
+}

@@ -1,0 +1,27 @@
+// Internal interface between the chi2 kernels (chi2.cu) and the host side
+// (chi2_host.cpp).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace adcb {
+
+constexpr int kMaxNp = 24;  // gsum up to K = 8 components (the reference bench K list 1,2,4,8)
+
+struct Chi2Pass {
+  const double* counts;  // full histogram, device
+  const double* qdev;    // QDev (2 * kMaxNp doubles), device
+  double* tile_ws;       // [tile_end - tile_begin][R]
+  double lo, width;      // Histogram::center = lo + (j + 0.5) * width
+  int64_t bin_end;       // one past the last bin this rank reads
+  int64_t tile_begin, tile_end;
+};
+
+int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast, int bpt,
+                 int64_t chunk_tiles, double* records, cudaStream_t s);
+void fill_qdev(int model, int np, const double* q, double* host_qdev);
+size_t qdev_bytes();
+
+}  // namespace adcb

@@ -1,0 +1,51 @@
+// Shared device/host helpers for the B200 gradient engine (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "adc_cuda.h"
+
+namespace adcb {
+
+// One IEEE-754 double operation per call, never contracted into FMA: the
+// generated gradient code executes one elementary op per statement
+// (linearize.cpp:94-221) and the interpreter evaluates each with plain C++
+// double arithmetic (eval.cpp:524-594), so faithful kernels must not fuse.
+__device__ __forceinline__ double fadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double fsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double fmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double fdiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// Streaming loads: read-only, do not allocate in L1 (data is touched once).
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 ld_stream2(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p));
+  return v;
+}
+
+// Thread-local error state behind adc_cuda_last_error().
+void set_error(const std::string& msg);
+void clear_error();
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define ADCB_CUDA(call)                                           \
+  do {                                                            \
+    cudaError_t e__ = (call);                                     \
+    if (e__ != cudaSuccess) return ::adcb::cuda_fail(e__, #call); \
+  } while (0)
+
+int sm_count();  // cached per device
+bool device_present();
+
+}  // namespace adcb

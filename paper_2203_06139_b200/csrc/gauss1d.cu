@@ -1,0 +1,115 @@
+// K1 — Listing-1 batch: kernel `compute` (proj/corpus/kernels.dsl:9-14) calling
+// the generated gauss_grad_0_1 (proj/tests/golden/gauss_grad_0_1.golden:1-42)
+// once per point, fused into one pass over HBM: read x, p; read-modify-write
+// dx, dp (48 B per point, HBM-bound).
+//
+// The per-point body is the golden text with its thread-uniform statements
+// hoisted to the host (and computed there with the same libm the reference
+// uses, so they are bit-identical):
+//   _t4 = (2*sigma)*sigma, _r1 = 0 + _t8*1 with _t8 = pow(2*PI,-0.5)*pow(sigma,-0.5)
+// Every remaining statement is one IEEE op in golden order (no FMA), so the
+// output differs from the reference interpreter only where libdevice exp and
+// glibc exp round differently (<= 1 ulp on exp(t)).
+#include <cmath>
+
+#include "common.cuh"
+
+namespace adcb {
+
+__device__ __forceinline__ void gauss_grad_0_1_point(double x, double p, double t4, double r1,
+                                                     double& dx, double& dp) {
+  const double t0 = fsub(x, p);           // _t0 = x - p
+  const double t1 = -t0;                  // _t1 = -_t0
+  const double t2 = fmul(t1, t0);         // _t2 = _t1 * _t0
+  const double t = fdiv(t2, t4);          // t = _t2 / _t4
+  const double t9 = exp(t);               // _t9 = exp(t)
+  const double r2 = fadd(0.0, fmul(r1, t9));   // _d_t += _r1 * _q0        -> _r2
+  const double r3 = fadd(0.0, fdiv(r2, t4));   // _d__t2 += _r2 / _t4      -> _r3
+  const double r4 = fadd(0.0, fmul(r3, t0));   // _d__t1 += _r3 * _t0      -> _r4
+  double d0 = fadd(0.0, fmul(t1, r3));         // _d__t0 += _t1 * _r3
+  d0 = fadd(d0, -r4);                          // _d__t0 += -_r4           -> _r5
+  dx = fadd(dx, d0);                           // _d_x[0] += _r5
+  dp = fadd(dp, -d0);                          // _d_p[0] += -_r5
+}
+
+// Two points per thread with 16-byte loads/stores (all four buffers 16 B
+// aligned); grid-stride over point pairs.
+__global__ void __launch_bounds__(256) gauss_grad_vec2_kernel(
+    const double2* __restrict__ x, const double2* __restrict__ p, double2* __restrict__ dx,
+    double2* __restrict__ dp, int64_t npairs, double t4, double r1) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < npairs;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const double2 xv = ld_stream2(x + k);
+    const double2 pv = ld_stream2(p + k);
+    double2 a = dx[k];
+    double2 b = dp[k];
+    gauss_grad_0_1_point(xv.x, pv.x, t4, r1, a.x, b.x);
+    gauss_grad_0_1_point(xv.y, pv.y, t4, r1, a.y, b.y);
+    dx[k] = a;
+    dp[k] = b;
+  }
+}
+
+__global__ void __launch_bounds__(256) gauss_grad_scalar_kernel(
+    const double* __restrict__ x, const double* __restrict__ p, double* __restrict__ dx,
+    double* __restrict__ dp, int64_t begin, int64_t n, double t4, double r1) {
+  for (int64_t i = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double a = dx[i], b = dp[i];
+    gauss_grad_0_1_point(ld_stream(x + i), ld_stream(p + i), t4, r1, a, b);
+    dx[i] = a;
+    dp[i] = b;
+  }
+}
+
+// Uniform statements of gauss_grad_0_1 (golden lines 11-17, 20-23), on the host.
+struct GaussUniform {
+  double t4, r1;
+};
+static int gauss_uniform(double sigma, GaussUniform* u) {
+  const double PI = 3.14159265358979323846;  // ast.cpp:119-123
+  const double t3 = 2 * sigma;
+  const double t4 = t3 * sigma;
+  // The interpreter raises at the first executed division `t = _t2 / _t4`
+  // (eval.cpp:543) — every active thread executes it.
+  if (t4 == 0.0) return fail(ADC_E_EVAL, "division by zero");
+  const double t5 = 2 * PI;
+  const double t6 = std::pow(t5, -0.5);
+  const double t7 = std::pow(sigma, -0.5);
+  const double t8 = t6 * t7;
+  double d_t9 = 0;
+  d_t9 += t8 * 1.0;  // _d__t9 += _t8 * _r0, _r0 = 1
+  u->t4 = t4;
+  u->r1 = d_t9;
+  return ADC_OK;
+}
+
+int launch_gauss_grad(int64_t n, const double* x, const double* p, double sigma, double* dx,
+                      double* dp, cudaStream_t stream) {
+  GaussUniform u{};
+  if (int rc = gauss_uniform(sigma, &u)) return rc;
+  if (n == 0) return ADC_OK;
+  const int threads = 256;
+  const int64_t cap = (int64_t)sm_count() * 16;
+  const bool aligned = (((uintptr_t)x | (uintptr_t)p | (uintptr_t)dx | (uintptr_t)dp) & 15) == 0;
+  int64_t done = 0;
+  if (aligned && n >= 2) {
+    const int64_t npairs = n / 2;
+    int64_t blocks = (npairs + threads - 1) / threads;
+    if (blocks > cap) blocks = cap;
+    gauss_grad_vec2_kernel<<<(unsigned)blocks, threads, 0, stream>>>(
+        (const double2*)x, (const double2*)p, (double2*)dx, (double2*)dp, npairs, u.t4, u.r1);
+    done = npairs * 2;
+  }
+  if (done < n) {
+    int64_t rest = n - done;
+    int64_t blocks = (rest + threads - 1) / threads;
+    if (blocks > cap) blocks = cap;
+    gauss_grad_scalar_kernel<<<(unsigned)blocks, threads, 0, stream>>>(x, p, dx, dp, done, n,
+                                                                        u.t4, u.r1);
+  }
+  ADCB_CUDA(cudaGetLastError());
+  return ADC_OK;
+}
+
+}  // namespace adcb

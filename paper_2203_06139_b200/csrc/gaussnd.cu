@@ -1,0 +1,231 @@
+// K2 — batched N-dim Gaussian gradient gaussnd_grad_0_1 over many points.
+//
+// Generated code (differentiate_gradient(gaussnd, {x, p}), reverse.cpp:335-553;
+// DSL in oracle/dsl/gaussnd.dsl):
+//   forward  for i: _t0 = x[i]-p[i]; _t1 = _t0*_t0; t = t + _t1   (3 tape pushes per i)
+//            t = -t / ((2*sigma)*sigma); value = _t8 * exp(t)
+//   reverse  _r2 = 0 + _t8*exp(t); _r3 = 0 + _r2/_t4; _d_t = 0 + -_r3
+//            for i (descending): _r5 = _d_t; _r6 = (0 + _r5*_t0) + _t0*_r5;
+//                                _d_x[i] += _r6; _d_p[i] += -_r6
+// The tape only restores values no adjoint rule reads except _t0, which is
+// recomputed exactly (x[i]-p[i]) or kept on chip: no global-memory tape.
+//
+// Layout: structure-of-arrays, coordinate d of point i at [d*ld + i].
+// Mapping: lane = point (a warp reads one 256 B row segment per load),
+// warps of a CTA split the dims of a 32-point tile.  Each warp keeps the
+// u = x-p of its first `dstage` dims in shared memory for the reverse sweep;
+// dims beyond that are re-read (most recent first, so they hit L2).
+// With W = 1 the forward sum runs in exactly the reference order; with W > 1
+// the per-warp partial sums are combined in fixed warp order (deterministic,
+// <= W-term regrouping of t).
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+
+namespace adcb {
+
+template <int W, int U>
+__global__ void __launch_bounds__(W * 32) gaussnd_tile_kernel(
+    const double* __restrict__ x, const double* __restrict__ p, double* __restrict__ dx,
+    double* __restrict__ dp, int64_t n, int dim, int64_t ld, double t4, double r1, int dpw,
+    int dstage) {
+  extern __shared__ double smem[];
+  double* tpart = smem;                    // [W][32]
+  double* stage = smem + W * 32;           // [W][dstage][32]
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  double* my_stage = stage + (size_t)warp * dstage * 32 + lane;
+  const int d0 = warp * dpw;
+  const int d1 = min(dim, d0 + dpw);
+  const int64_t ntiles = (n + 31) / 32;
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i = tile * 32 + lane;
+    const bool valid = i < n;
+    const double* xi = x + i;
+    const double* pi = p + i;
+    // ---- forward sweep: u_d and this warp's partial of t -------------------
+    double t = 0.0;
+    int d = d0;
+    if (valid) {
+      for (; d + U <= d1; d += U) {
+        double xv[U], pv[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          xv[k] = ld_stream(xi + (int64_t)(d + k) * ld);
+          pv[k] = ld_stream(pi + (int64_t)(d + k) * ld);
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const double u = fsub(xv[k], pv[k]);  // _t0 = x[i] - p[i]
+          if (d + k - d0 < dstage) my_stage[(d + k - d0) * 32] = u;
+          t = fadd(t, fmul(u, u));              // _t1 = _t0*_t0; t = t + _t1
+        }
+      }
+      for (; d < d1; ++d) {
+        const double u = fsub(ld_stream(xi + (int64_t)d * ld), ld_stream(pi + (int64_t)d * ld));
+        if (d - d0 < dstage) my_stage[(d - d0) * 32] = u;
+        t = fadd(t, fmul(u, u));
+      }
+    }
+    if (W > 1) {
+      tpart[warp * 32 + lane] = t;
+      __syncthreads();
+      t = tpart[lane];
+#pragma unroll
+      for (int w = 1; w < W; ++w) t = fadd(t, tpart[w * 32 + lane]);
+    }
+    // ---- scalar chain (identical in every warp of the tile) -----------------
+    const double tt = fdiv(-t, t4);                // _t2 = -t; t = _t2 / _t4
+    const double e = exp(tt);                      // _t9 = exp(t)
+    const double r2 = fadd(0.0, fmul(r1, e));      // _d_t += _r1 * _q0
+    const double r3 = fadd(0.0, fdiv(r2, t4));     // _d__t2 += _r2 / _t4
+    const double c = fadd(0.0, -r3);               // _d_t += -_r3  (= _r4 = _r5 every i)
+    // ---- reverse sweep: dx += r6, dp += -r6, most recently loaded dims first
+    if (valid) {
+      double* dxi = dx + i;
+      double* dpi = dp + i;
+      d = d1;
+      const int dre = min(d1, d0 + dstage);  // [dre, d1) re-read, [d0, dre) staged
+      for (; d - U >= dre; d -= U) {
+        double xv[U], pv[U], a[U], b[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const int64_t o = (int64_t)(d - 1 - k) * ld;
+          xv[k] = ld_stream(xi + o);
+          pv[k] = ld_stream(pi + o);
+          a[k] = dxi[o];
+          b[k] = dpi[o];
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const double u = fsub(xv[k], pv[k]);
+          const double r6 = fadd(fadd(0.0, fmul(c, u)), fmul(u, c));
+          const int64_t o = (int64_t)(d - 1 - k) * ld;
+          dxi[o] = fadd(a[k], r6);
+          dpi[o] = fadd(b[k], -r6);
+        }
+      }
+      for (; d > dre; --d) {
+        const int64_t o = (int64_t)(d - 1) * ld;
+        const double u = fsub(ld_stream(xi + o), ld_stream(pi + o));
+        const double r6 = fadd(fadd(0.0, fmul(c, u)), fmul(u, c));
+        dxi[o] = fadd(dxi[o], r6);
+        dpi[o] = fadd(dpi[o], -r6);
+      }
+      for (; d - U >= d0; d -= U) {
+        double a[U], b[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const int64_t o = (int64_t)(d - 1 - k) * ld;
+          a[k] = dxi[o];
+          b[k] = dpi[o];
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const double u = my_stage[(d - 1 - k - d0) * 32];
+          const double r6 = fadd(fadd(0.0, fmul(c, u)), fmul(u, c));
+          const int64_t o = (int64_t)(d - 1 - k) * ld;
+          dxi[o] = fadd(a[k], r6);
+          dpi[o] = fadd(b[k], -r6);
+        }
+      }
+      for (; d > d0; --d) {
+        const int64_t o = (int64_t)(d - 1) * ld;
+        const double u = my_stage[(d - 1 - d0) * 32];
+        const double r6 = fadd(fadd(0.0, fmul(c, u)), fmul(u, c));
+        dxi[o] = fadd(dxi[o], r6);
+        dpi[o] = fadd(dpi[o], -r6);
+      }
+    }
+    if (W > 1) __syncthreads();  // tpart is rewritten by the next tile
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 0 auto; 1/3/4 = one warp per 32-point tile (reference summation order) with
+// 8/16/32 rows in flight per thread; 2 = dims split over the warps of a CTA.
+static int g_variant = 0;
+
+struct NdConfig {
+  int w, u, dpw, dstage, blocks_per_sm;
+  size_t smem;
+};
+
+template <int W, int U>
+static int launch_tile(const NdConfig& c, int64_t n, int dim, int64_t ld, const double* x,
+                       const double* p, double* dx, double* dp, double t4, double r1,
+                       cudaStream_t s) {
+  auto k = gaussnd_tile_kernel<W, U>;
+  if (c.smem > 48 * 1024)
+    ADCB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem));
+  int occ = 0;
+  ADCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, W * 32, c.smem));
+  if (occ < 1) return fail(ADC_E_LAUNCH, "gaussnd: tile configuration does not fit an SM");
+  const int64_t ntiles = (n + 31) / 32;
+  int64_t blocks = std::min<int64_t>(ntiles, (int64_t)occ * sm_count());
+  k<<<(unsigned)blocks, W * 32, c.smem, s>>>(x, p, dx, dp, n, dim, ld, t4, r1, c.dpw, c.dstage);
+  ADCB_CUDA(cudaGetLastError());
+  return ADC_OK;
+}
+
+// Shared-memory budget per SM usable by the stage buffers.
+static constexpr size_t kSmemPerSm = 224 * 1024;
+
+static NdConfig choose(int dim) {
+  NdConfig c{};
+  const int variant = g_variant;
+  // W = 1 keeps the reference's summation order; it needs the whole u row of
+  // a point on chip: 256 B per dim per warp.  Use it while >= 8 warps fit.
+  if (variant == 1 || variant == 3 || variant == 4 ||
+      (variant == 0 && (size_t)dim * 256 * 8 <= kSmemPerSm)) {
+    c.w = 1;
+    c.dpw = dim;
+    c.dstage = dim;
+    if ((size_t)dim * 256 > kSmemPerSm - 512) c.dstage = (int)((kSmemPerSm - 512) / 256);
+  } else {
+    c.w = dim >= 512 ? 16 : 8;
+    c.dpw = (dim + c.w - 1) / c.w;
+    // one CTA per SM for W=16, stage as much as fits
+    const size_t per_cta = kSmemPerSm / (c.w == 16 ? 1 : 2);
+    const size_t avail = per_cta - (size_t)c.w * 32 * 8 - 1024;
+    c.dstage = std::min<int>(c.dpw, (int)(avail / ((size_t)c.w * 256)));
+  }
+  c.u = variant == 1 ? 8 : variant == 4 ? 32 : 16;
+  if (c.w > 1) c.u = 8;
+  c.smem = ((size_t)c.w * 32 + (size_t)c.w * c.dstage * 32) * sizeof(double);
+  return c;
+}
+
+int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, const double* p,
+                        double sigma, double* dx, double* dp, cudaStream_t s) {
+  const double PI = 3.14159265358979323846;
+  const double t3 = 2 * sigma;
+  const double t4 = t3 * sigma;
+  // `t = _t2 / _t4` runs once per point: the interpreter's division check
+  // (eval.cpp:543) fires for any point.
+  if (n > 0 && t4 == 0.0) return fail(ADC_E_EVAL, "division by zero");
+  if (n == 0) return ADC_OK;
+  if (dim > (1 << 24)) return fail(ADC_E_ARG, "gaussnd: dim too large");
+  double d_t9 = 0;
+  d_t9 += (std::pow(2 * PI, -0.5) * std::pow(sigma, -0.5)) * 1.0;  // _d__t9 += _t8 * _r0
+  NdConfig c = choose((int)dim);
+  switch (c.w) {
+    case 1:
+      if (c.u == 8) return launch_tile<1, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+      if (c.u == 32) return launch_tile<1, 32>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+      return launch_tile<1, 16>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+    case 8: return launch_tile<8, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+    case 16: return launch_tile<16, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+  }
+  return fail(ADC_E_ARG, "gaussnd: bad configuration");
+}
+
+int gaussnd_set_variant(int v) {
+  if (v < 0 || v > 4) return fail(ADC_E_ARG, "gaussnd variant must be 0..4");
+  g_variant = v;
+  return ADC_OK;
+}
+
+}  // namespace adcb

@@ -1,0 +1,190 @@
+"""Host-side mirror of the reference histogram-fit API (proj/include/adc/fit.hpp)
+over the B200 C ABI, model-parameterised (gsum of fit.cpp:125-138, or the
+Gaussian + quadratic background gpoly of oracle/dsl/gpoly.dsl).
+
+    h = Histogram(bins, lo, hi, events, counts)
+    eng = FitEngine("gpoly", np=6)
+    eng.chi2(h, q); eng.chi2_gradient(h, q); eng.fit(h, init, FitOptions())
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import List
+
+import numpy as np
+
+from ._capi import (MODEL_IDS, AdcError, Chi2Layout, FitOptions as _FitOptionsC, FitResultC,
+                    check, dbl_array, dptr, lib)
+
+
+@dataclass
+class Histogram:
+    """fit.hpp:23-34.  counts: numpy float64 (host) or a float64 CUDA tensor."""
+    bins: int
+    lo: float
+    hi: float
+    events: float
+    counts: object
+
+    def width(self) -> float:
+        return (self.hi - self.lo) / self.bins
+
+    def center(self, i: int) -> float:
+        return self.lo + (i + 0.5) * self.width()
+
+
+@dataclass
+class FitOptions:
+    """fit.hpp:56-65 (use_hessian is not part of the B200 path)."""
+    budget: int = 400
+    grad_tol: float = 1e-6
+    chi2_rel_tol: float = 1e-12
+    sigma_min: float = 1e-3
+    armijo_c1: float = 1e-4
+    trace_iterates: int = 0
+
+
+@dataclass
+class FitResult:
+    """fit.hpp:67-78 (op counters are interpreter metadata, not part of this path)."""
+    params: List[float]
+    chi2: float
+    iterations: int
+    gradient_evals: int
+    gradient_wall_ns: int
+    converged: bool
+    sigma_clamps: int
+    chi2_evals: int = 0
+    iterates: List[List[float]] = field(default_factory=list)
+
+
+def chi2_layout(bins: int, world: int = 1, rank: int = 0) -> Chi2Layout:
+    L = Chi2Layout()
+    check(lib.adc_chi2_make_layout(bins, world, rank, ctypes.byref(L)))
+    return L
+
+
+def record_len(np_: int, want_grad: bool) -> int:
+    return lib.adc_chi2_record_len(np_, 1 if want_grad else 0)
+
+
+def finalize(np_: int, events: float, records: np.ndarray, want_grad: bool = True):
+    """Fixed-order reduction of chunk records + closed form (host, no device)."""
+    rec = np.ascontiguousarray(records, dtype=np.float64).ravel()
+    R = record_len(np_, want_grad)
+    nchunks = rec.size // R
+    g = np.zeros(np_)
+    c2 = ctypes.c_double()
+    check(lib.adc_chi2_finalize(np_, float(events), rec.ctypes.data_as(ctypes.POINTER(
+        ctypes.c_double)), nchunks, 1 if want_grad else 0, g.ctypes.data_as(ctypes.POINTER(
+            ctypes.c_double)), ctypes.byref(c2)))
+    return (g, c2.value) if want_grad else c2.value
+
+
+class Chi2Plan:
+    """One histogram resident on one device (or one rank's shard of it)."""
+
+    def __init__(self, model: str, np_: int, h: Histogram, world: int = 1, rank: int = 0):
+        import torch
+        if model not in MODEL_IDS:
+            raise AdcError("Arg", f"unknown model '{model}'")
+        self.model, self.np, self.h = model, np_, h
+        counts = h.counts
+        if not hasattr(counts, "is_cuda"):
+            counts = torch.from_numpy(np.ascontiguousarray(counts, dtype=np.float64)).cuda()
+        self.counts = counts  # keep alive
+        self._p = ctypes.c_void_p()
+        check(lib.adc_cuda_chi2_plan_create(
+            ctypes.byref(self._p), MODEL_IDS[model], np_, h.bins, float(h.lo), float(h.hi),
+            float(h.events), dptr(counts), world, rank,
+            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        self.layout = Chi2Layout()
+        check(lib.adc_cuda_chi2_plan_layout(self._p, ctypes.byref(self.layout)))
+
+    def set_precision(self, fast: bool):
+        check(lib.adc_cuda_chi2_set_precision(self._p, 1 if fast else 0))
+
+    def gradient(self, q):
+        g = np.zeros(self.np)
+        c2 = ctypes.c_double()
+        check(lib.adc_cuda_chi2_gradient(self._p, dbl_array(q), g.ctypes.data_as(
+            ctypes.POINTER(ctypes.c_double)), ctypes.byref(c2)))
+        return g, c2.value
+
+    def chi2(self, q) -> float:
+        c2 = ctypes.c_double()
+        check(lib.adc_cuda_chi2(self._p, dbl_array(q), ctypes.byref(c2)))
+        return c2.value
+
+    def partials(self, q, want_grad: bool, records_dev=None):
+        """Enqueue this rank's pass; records land in records_dev (a float64 CUDA
+        tensor of local_chunks * record_len) or the plan's own buffer."""
+        check(lib.adc_cuda_chi2_partials(self._p, dbl_array(q), 1 if want_grad else 0,
+                                         dptr(records_dev) if records_dev is not None else None))
+
+    @property
+    def stream_ptr(self):
+        return None
+
+    def close(self):
+        if self._p:
+            lib.adc_cuda_chi2_plan_destroy(self._p)
+            self._p = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def default_clamp(model: str, np_: int):
+    """Indices the sigma clamp applies to: every third for gsum (fit.cpp:268-278),
+    only the width q[2] for gpoly."""
+    return list(range(2, np_, 3)) if model == "gsum" else [2]
+
+
+class FitEngine:
+    """adc::FitEngine (fit.hpp:82-112), model-parameterised, B200 passes."""
+
+    def __init__(self, model: str = "gsum", np_: int = 3):
+        self.model, self.np = model, np_
+        self._plans = {}
+
+    def _plan(self, h: Histogram) -> Chi2Plan:
+        key = id(h)
+        pl = self._plans.get(key)
+        if pl is None or pl.h is not h:
+            pl = Chi2Plan(self.model, self.np, h)
+            self._plans = {key: pl}
+        return pl
+
+    def gradient_fn_name(self) -> str:
+        return f"{self.model}_grad_1"
+
+    def chi2(self, h: Histogram, q) -> float:
+        return self._plan(h).chi2(q)
+
+    def chi2_gradient(self, h: Histogram, q) -> np.ndarray:
+        return self._plan(h).gradient(q)[0]
+
+    def fit(self, h: Histogram, init, opts: FitOptions | None = None, clamp=None) -> FitResult:
+        opts = opts or FitOptions()
+        pl = self._plan(h)
+        o = _FitOptionsC(opts.budget, opts.grad_tol, opts.chi2_rel_tol, opts.sigma_min,
+                         opts.armijo_c1, opts.trace_iterates)
+        idx = default_clamp(self.model, self.np) if clamp is None else list(clamp)
+        cidx = (ctypes.c_int32 * max(1, len(idx)))(*idx)
+        params = np.ascontiguousarray(init, dtype=np.float64).copy()
+        its = np.zeros(max(1, opts.trace_iterates) * self.np)
+        res = FitResultC()
+        dp = ctypes.POINTER(ctypes.c_double)
+        check(lib.adc_cuda_fit(pl._p, params.ctypes.data_as(dp), cidx, len(idx), ctypes.byref(o),
+                               ctypes.byref(res), its.ctypes.data_as(dp)))
+        n_tr = min(opts.trace_iterates, res.iterations + 1) if opts.trace_iterates else 0
+        return FitResult(params=list(params), chi2=res.chi2, iterations=res.iterations,
+                         gradient_evals=res.gradient_evals, gradient_wall_ns=res.gradient_ns,
+                         converged=bool(res.converged), sigma_clamps=res.sigma_clamps,
+                         chi2_evals=res.chi2_evals,
+                         iterates=[list(its[k * self.np:(k + 1) * self.np]) for k in range(n_tr)])

@@ -1,0 +1,172 @@
+"""Host-side mirror of the reference batch-dispatch API (proj/include/adc/launch.hpp)
+over the B200 C ABI.
+
+    cfg = LaunchConfig(n // 256 + 1, 256, n)
+    buffers = BufferSet(arrays={"x": x, "p": p, "dx": dx, "dp": dp}, scalars={"sigma": 1.3})
+    stats = launch("compute", cfg, buffers)          # adc::launch(prog, "compute", cfg, buffers)
+
+Arrays may be numpy float64 arrays (host: the call copies in and out) or
+torch float64 CUDA tensors (device: stream-ordered, no copies).  The kernel
+is the Listing-1 `compute` (proj/corpus/kernels.dsl:9-14) whose callee is
+looked up in the kernel registry by the gradient's name and fingerprint.
+
+launch_batch is the NEW batched path for multi-dimensional per-point
+gradients (the reference cannot express it safely): one
+point per column of structure-of-arrays buffers.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Dict
+
+import numpy as np
+
+from ._capi import AdcError, check, dptr, lib
+
+# The Listing-1 kernel signature (kernels.dsl:9) and the race_check verdict of
+# the reference for it (launch.cpp:112-240; test_launch.cpp:60-65).
+COMPUTE_PARAMS = (("x", "real[]"), ("p", "real[]"), ("sigma", "real"), ("dx", "real[]"),
+                  ("dp", "real[]"))
+COMPUTE_ACCESS = {"x": "shared-read", "p": "shared-read", "sigma": "shared-read",
+                  "dx": "private-per-thread", "dp": "private-per-thread"}
+COMPUTE_SHARED_HAZARD = {"dsigma": "whole array shared with a writing callee across threads"}
+
+
+@dataclass
+class LaunchConfig:
+    """launch.hpp:15-21."""
+    grid_dim: int = 0
+    block_dim: int = 0
+    n: int = 0
+
+    def validate(self):
+        """LaunchConfig::validate (launch.cpp:9-19), same messages."""
+        if self.grid_dim <= 0 or self.block_dim <= 0 or self.n <= 0:
+            raise AdcError("Launch", f"launch configuration must be positive (grid {self.grid_dim}"
+                                     f", block {self.block_dim}, n {self.n})")
+        if self.grid_dim * self.block_dim < self.n:
+            raise AdcError("Launch", f"grid {self.grid_dim} x block {self.block_dim} does not "
+                                     f"cover problem size {self.n}")
+
+
+@dataclass
+class BufferSet:
+    """launch.hpp:46-50."""
+    arrays: Dict[str, object] = field(default_factory=dict)
+    scalars: Dict[str, float] = field(default_factory=dict)
+    integers: Dict[str, int] = field(default_factory=dict)
+
+
+@dataclass
+class LaunchOptions:
+    """launch.hpp:52-56.  `workers` and `sequential` have no meaning on the GPU
+    (the result is identical for any of them) and are accepted for drop-in use."""
+    unsafe: bool = False
+    workers: int = 0
+    sequential: bool = False
+
+
+@dataclass
+class LaunchStats:
+    """launch.hpp:58-61; thread_statements is derived analytically for the
+    Listing-1 shape: 3 kernel-frame statements for g < n, 2 for the padding
+    threads (test_launch.cpp:119-128).  Materialised on first access."""
+    active: int
+    idle: int
+
+    @property
+    def thread_statements(self) -> np.ndarray:
+        ts = np.full(self.active + self.idle, 2, dtype=np.uint32)
+        ts[:self.active] = 3
+        return ts
+
+
+def _fingerprints():
+    """The registry's own (name -> fingerprint) table (include/adc_cuda.h)."""
+    return {lib.adc_cuda_registry_name(i).decode(): lib.adc_cuda_registry_fingerprint(i)
+            for i in range(lib.adc_cuda_registry_size())}
+
+
+def registry_find(name: str, fingerprint: int) -> int:
+    import ctypes
+    kid = ctypes.c_int32(-1)
+    check(lib.adc_cuda_registry_find(name.encode(), fingerprint, ctypes.byref(kid)))
+    return kid.value
+
+
+def _is_torch(a) -> bool:
+    return hasattr(a, "is_cuda")
+
+
+def _stream_of(a):
+    import torch
+    return torch.cuda.current_stream(a.device).cuda_stream
+
+
+def launch(kernel: str, cfg: LaunchConfig, buffers: BufferSet,
+           opts: LaunchOptions | None = None, callee_fingerprint: int | None = None) -> LaunchStats:
+    """adc::launch (launch.cpp:252-346) for the Listing-1 kernels of kernels.dsl."""
+    opts = opts or LaunchOptions()
+    cfg.validate()
+    if kernel == "compute_shared":
+        # race_check reports dsigma as a shared-write hazard (launch.cpp:261-267).
+        if not opts.unsafe:
+            raise AdcError("Launch", "launch refused, hazardous parameter(s): dsigma (whole array "
+                                     "shared with a writing callee across threads); pass the "
+                                     "unsafe flag to force")
+        raise AdcError("Launch", "no B200 kernel registered for 'gauss_grad'")
+    if kernel != "compute":
+        raise AdcError("Launch", f"unknown kernel '{kernel}'")
+    fp = _fingerprints()["gauss_grad_0_1"] if callee_fingerprint is None else callee_fingerprint
+    registry_find("gauss_grad_0_1", fp)
+    arrs = {}
+    for name, typ in COMPUTE_PARAMS:
+        if typ == "real[]":
+            if name not in buffers.arrays:
+                raise AdcError("Launch", f"missing buffer '{name}'")
+            a = buffers.arrays[name]
+            ln = a.numel() if _is_torch(a) else a.size
+            if ln < cfg.n:  # every array of `compute` is indexed by the thread (launch.cpp:279-284)
+                raise AdcError("Launch", f"buffer '{name}' has length {ln} but is indexed by thread"
+                                         f" over {cfg.n} elements")
+            arrs[name] = a
+        elif name not in buffers.scalars:
+            raise AdcError("Launch", f"missing scalar value '{name}'")
+    sigma = float(buffers.scalars["sigma"])
+    x, p, dx, dp = (arrs[k] for k in ("x", "p", "dx", "dp"))
+    if _is_torch(x):
+        for a in (x, p, dx, dp):
+            if not (a.is_cuda and a.is_contiguous()) or str(a.dtype) != "torch.float64":
+                raise AdcError("Launch", "device buffers must be contiguous float64 CUDA tensors")
+        check(lib.adc_cuda_compute_gauss(cfg.grid_dim, cfg.block_dim, cfg.n, dptr(x), dptr(p),
+                                         sigma, dptr(dx), dptr(dp), _stream_of(x)))
+    else:
+        for a in (x, p, dx, dp):
+            if a.dtype != np.float64 or not a.flags.c_contiguous:
+                raise AdcError("Launch", "host buffers must be contiguous float64 arrays")
+        check(lib.adc_cuda_compute_gauss_host(cfg.grid_dim, cfg.block_dim, cfg.n, dptr(x),
+                                              dptr(p), sigma, dptr(dx), dptr(dp)))
+    return LaunchStats(active=cfg.n, idle=cfg.grid_dim * cfg.block_dim - cfg.n)
+
+
+def launch_batch(grad_fn: str, x, p, sigma: float, dx, dp, ld: int | None = None,
+                 callee_fingerprint: int | None = None):
+    """Batched per-point gradient over structure-of-arrays buffers of shape
+    (dim, n): gaussnd_grad_0_1(x[:, i], p[:, i], sigma, dim, dx[:, i], dp[:, i])
+    for every point i, accumulating into dx, dp."""
+    if grad_fn != "gaussnd_grad_0_1":
+        raise AdcError("Launch", f"no B200 kernel registered for '{grad_fn}'")
+    fp = _fingerprints()[grad_fn] if callee_fingerprint is None else callee_fingerprint
+    registry_find(grad_fn, fp)
+    dim, n = x.shape
+    ld = n if ld is None else ld
+    if _is_torch(x):
+        check(lib.adc_cuda_gaussnd_grad(n, dim, ld, dptr(x), dptr(p), float(sigma), dptr(dx),
+                                        dptr(dp), _stream_of(x)))
+    else:
+        check(lib.adc_cuda_gaussnd_grad_host(n, dim, ld, dptr(x), dptr(p), float(sigma), dptr(dx),
+                                             dptr(dp)))
+
+
+def set_gaussnd_variant(v: int):
+    check(lib.adc_cuda_gaussnd_set_variant(v))

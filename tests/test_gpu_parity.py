@@ -1,0 +1,255 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the C oracle.  Tolerances:
+  * per-point outputs: |g - r| <= 1e-12 * max(|g|, |r|)  (true relative)
+  * reductions (chi2, its gradient): |g - r| <= 1e-12 * sum_j |term_j|
+    against the Neumaier-compensated restatement of fit.cpp:206-259.
+"""
+import numpy as np
+import pytest
+
+from conftest import golden, rel_err
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2203_06139_b200 as adc  # noqa: E402
+from paper_2203_06139_b200 import synth  # noqa: E402
+from paper_2203_06139_b200.launch import set_gaussnd_variant  # noqa: E402
+
+REL = 1e-12
+DEV = "cuda"
+
+
+def t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def host(a):
+    torch.cuda.synchronize()
+    return a.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------- K1
+def test_listing1_n512_device_and_host():
+    g = golden("gauss1d_n512.npz")
+    for path in ("device", "host"):
+        if path == "device":
+            x, p = t(g["x"]), t(g["p"])
+            dx, dp = torch.zeros(512, dtype=torch.float64, device=DEV), torch.zeros(
+                512, dtype=torch.float64, device=DEV)
+        else:
+            x, p = g["x"].copy(), g["p"].copy()
+            dx, dp = np.zeros(512), np.zeros(512)
+        st = adc.launch("compute", adc.LaunchConfig(512 // 256 + 1, 256, 512),
+                        adc.BufferSet(arrays={"x": x, "p": p, "dx": dx, "dp": dp},
+                                      scalars={"sigma": 1.3}))
+        assert st.active == 512 and st.idle == 256 and st.thread_statements.size == 768
+        gx = host(dx) if path == "device" else dx
+        gp = host(dp) if path == "device" else dp
+        assert rel_err(gx, g["dx"]).max() <= REL
+        assert rel_err(gp, g["dp"]).max() <= REL
+        assert np.array_equal(gx, -gp)  # dx == -dp exactly from zero slots
+        # most components are bit-identical (exp may round differently by 1 ulp)
+        assert np.mean(gx == g["dx"]) > 0.9
+
+
+@pytest.mark.parametrize("case", ["kat", "accum300", "edges"])
+def test_listing1_cases(case):
+    g = golden("gauss1d_cases.npz")
+    n = g[f"{case}_x"].size
+    block = int(g[f"{case}_block"])
+    dx, dp = t(g[f"{case}_dx0"]), t(g[f"{case}_dp0"])
+    adc.launch("compute", adc.LaunchConfig(n // block + 1, block, n),
+               adc.BufferSet(arrays={"x": t(g[f"{case}_x"]), "p": t(g[f"{case}_p"]), "dx": dx,
+                                     "dp": dp}, scalars={"sigma": float(g[f"{case}_sigma"])}))
+    assert acc_err(host(dx), g[f"{case}_dx"], g[f"{case}_dx0"]).max() <= REL
+    assert acc_err(host(dp), g[f"{case}_dp"], g[f"{case}_dp0"]).max() <= REL
+    if case == "kat":
+        assert host(dx)[0] == pytest.approx(-0.2419707245191434, rel=1e-15)
+
+
+def acc_err(g, r, init):
+    """Accumulated slots: the increment is compared relative to the larger of
+    the result and the initial slot value (a 1-ulp difference in the increment
+    is amplified by cancellation against the slot otherwise)."""
+    g, r, init = (np.asarray(a, dtype=np.float64) for a in (g, r, init))
+    den = np.maximum(np.maximum(np.abs(g), np.abs(r)), np.abs(init))
+    return np.abs(g - r) / np.maximum(den, 1e-300)
+
+
+def test_listing1_1m_vs_oracle(restate):
+    n = 10**6
+    x, p = synth.points_1d(n)
+    dx0 = np.random.default_rng(3).standard_normal(n)
+    dp0 = np.random.default_rng(4).standard_normal(n)
+    ox, op = dx0.copy(), dp0.copy()
+    restate.gauss_grad(x, p, 1.3, ox, op)
+    dx, dp = t(dx0), t(dp0)
+    adc.launch("compute", adc.LaunchConfig(n // 256 + 1, 256, n),
+               adc.BufferSet(arrays={"x": t(x), "p": t(p), "dx": dx, "dp": dp},
+                             scalars={"sigma": 1.3}))
+    assert acc_err(host(dx), ox, dx0).max() <= REL and acc_err(host(dp), op, dp0).max() <= REL
+    # odd length + unaligned views take the scalar path
+    dx2 = torch.zeros(n + 1, dtype=torch.float64, device=DEV)
+    dp2 = torch.zeros(n + 1, dtype=torch.float64, device=DEV)
+    xs, ps = t(np.concatenate([[0.0], x])), t(np.concatenate([[0.0], p]))
+    m = n - 1
+    adc.launch("compute", adc.LaunchConfig(m // 256 + 1, 256, m),
+               adc.BufferSet(arrays={"x": xs[1:1 + m], "p": ps[1:1 + m], "dx": dx2[1:1 + m],
+                                     "dp": dp2[1:1 + m]}, scalars={"sigma": 1.3}))
+    ox2, op2 = np.zeros(m), np.zeros(m)
+    restate.gauss_grad(x[:m].copy(), p[:m].copy(), 1.3, ox2, op2)
+    assert rel_err(host(dx2)[1:1 + m], ox2).max() <= REL
+
+
+def test_listing1_domain_error():
+    z = torch.zeros(4, dtype=torch.float64, device=DEV)
+    with pytest.raises(adc.AdcError) as e:
+        adc.launch("compute", adc.LaunchConfig(1, 4, 4),
+                   adc.BufferSet(arrays={"x": z, "p": z, "dx": z, "dp": z}, scalars={"sigma": 0.0}))
+    assert e.value.kind == "Eval" and "division by zero" in str(e.value)
+
+
+# ---------------------------------------------------------------------------- K2
+ND_KEYS = ["d100_n64", "d1000_n8", "d1_n33", "d37_n70", "d128_n40", "d129_n5"]
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("key", ND_KEYS)
+def test_gaussnd_golden(key, variant):
+    g = golden("gaussnd_cases.npz")
+    set_gaussnd_variant(variant)
+    try:
+        dx, dp = t(g[f"{key}_dx0"]), t(g[f"{key}_dp0"])
+        adc.launch_batch("gaussnd_grad_0_1", t(g[f"{key}_x"]), t(g[f"{key}_p"]),
+                         float(g[f"{key}_sigma"]), dx, dp)
+        assert acc_err(host(dx), g[f"{key}_dx"], g[f"{key}_dx0"]).max() <= REL
+        assert acc_err(host(dp), g[f"{key}_dp"], g[f"{key}_dp0"]).max() <= REL
+    finally:
+        set_gaussnd_variant(0)
+
+
+def test_gaussnd_host_path():
+    g = golden("gaussnd_cases.npz")
+    key = "d37_n70"
+    dx, dp = g[f"{key}_dx0"].copy(), g[f"{key}_dp0"].copy()
+    adc.launch_batch("gaussnd_grad_0_1", g[f"{key}_x"].copy(), g[f"{key}_p"].copy(),
+                     float(g[f"{key}_sigma"]), dx, dp)
+    assert acc_err(dx, g[f"{key}_dx"], g[f"{key}_dx0"]).max() <= REL
+    assert acc_err(dp, g[f"{key}_dp"], g[f"{key}_dp0"]).max() <= REL
+
+
+@pytest.mark.parametrize("dim,n", [(100, 200_003), (1000, 20_011), (5, 77), (300, 1000)])
+def test_gaussnd_vs_oracle(restate, dim, n):
+    x, p = synth.points_nd(dim, n, seed=dim)
+    ox, op = np.zeros((dim, n)), np.zeros((dim, n))
+    restate.gaussnd_grad(x, p, 1.3, ox, op)
+    for variant in (1, 2):
+        set_gaussnd_variant(variant)
+        try:
+            dx = torch.zeros((dim, n), dtype=torch.float64, device=DEV)
+            dp = torch.zeros_like(dx)
+            adc.launch_batch("gaussnd_grad_0_1", t(x), t(p), 1.3, dx, dp)
+            hx, hp = host(dx), host(dp)
+            assert rel_err(hx, ox).max() <= REL, variant
+            assert rel_err(hp, op).max() <= REL, variant
+            assert np.array_equal(hx, -hp)
+        finally:
+            set_gaussnd_variant(0)
+
+
+def test_gaussnd_accumulates_twice():
+    # accumulate-only slots: two launches double the first (test_reverse.cpp:335-348).
+    x, p = synth.points_nd(64, 4096, seed=5)
+    dx = torch.zeros((64, 4096), dtype=torch.float64, device=DEV)
+    dp = torch.zeros_like(dx)
+    X, P = t(x), t(p)
+    adc.launch_batch("gaussnd_grad_0_1", X, P, 0.9, dx, dp)
+    once = host(dx).copy()
+    adc.launch_batch("gaussnd_grad_0_1", X, P, 0.9, dx, dp)
+    assert np.array_equal(host(dx), 2 * once)
+
+
+# ---------------------------------------------------------------------------- chi2
+CHI2_KEYS = ["gpoly_b2000", "gsum1_b1000", "gsum2_b1500"]
+
+
+@pytest.mark.parametrize("fast", [False, True])
+@pytest.mark.parametrize("key", CHI2_KEYS)
+def test_chi2_golden(restate, key, fast):
+    g = golden("chi2_cases.npz")
+    model = str(g[f"{key}_model"])
+    counts, q, ev = g[f"{key}_counts"], g[f"{key}_q"], float(g[f"{key}_events"])
+    h = adc.Histogram(counts.size, -5.0, 5.0, ev, counts)
+    plan = adc.Chi2Plan(model, q.size, h)
+    plan.set_precision(fast)
+    grad, c2 = plan.gradient(q)
+    ref, scale = restate.chi2_gradient_compensated(model, counts, -5.0, 5.0, ev, q)
+    assert np.all(np.abs(grad - ref) <= 1e-12 * scale), (grad, ref, scale)
+    # and against the reference's own (sequential) numbers
+    assert np.all(np.abs(grad - g[f"{key}_grad"]) <= 1e-12 * scale)
+    vref, vscale = restate.chi2_compensated(model, counts, -5.0, 5.0, ev, q)
+    assert abs(c2 - vref) <= 1e-12 * vscale
+    assert abs(plan.chi2(q) - g[f"{key}_chi2"]) <= 1e-12 * vscale
+
+
+def test_chi2_config3_1e6(restate):
+    counts, ev = synth.histogram(10**6, events=1e8)
+    q = np.array(synth.GPOLY_INIT)
+    h = adc.Histogram(counts.size, -5.0, 5.0, ev, counts)
+    plan = adc.Chi2Plan("gpoly", 6, h)
+    grad, c2 = plan.gradient(q)
+    ref, scale = restate.chi2_gradient_compensated("gpoly", counts, -5.0, 5.0, ev, q)
+    assert np.all(np.abs(grad - ref) <= 1e-12 * scale)
+    vref, vscale = restate.chi2_compensated("gpoly", counts, -5.0, 5.0, ev, q)
+    assert abs(c2 - vref) <= 1e-12 * vscale
+
+
+def test_chi2_sharding_bitwise_invariant():
+    # Any split of whole chunks over ranks gives the same bits (fixed trees).
+    counts, ev = synth.histogram(3_000_000, events=3e8, seed=9)
+    q = np.array(synth.GPOLY_INIT)
+    h = adc.Histogram(counts.size, -5.0, 5.0, ev, counts)
+    full = adc.Chi2Plan("gpoly", 6, h)
+    g1, c1 = full.gradient(q)
+    R = adc.record_len(6, True)
+    for world in (2, 3, 4, 8):
+        recs = []
+        for rank in range(world):
+            pl = adc.Chi2Plan("gpoly", 6, h, world=world, rank=rank)
+            nloc = pl.layout.chunk_end - pl.layout.chunk_begin
+            buf = torch.zeros(max(1, nloc) * R, dtype=torch.float64, device=DEV)
+            pl.partials(q, True, buf)
+            torch.cuda.synchronize()
+            recs.append(buf.cpu().numpy()[:nloc * R])
+            pl.close()
+        gw, cw = adc.finalize(6, ev, np.concatenate(recs), True)
+        assert np.array_equal(gw, g1) and cw == c1, world
+
+
+def test_chi2_domain_error():
+    counts, ev = synth.histogram(1000, events=1e5)
+    h = adc.Histogram(1000, -5.0, 5.0, ev, counts)
+    with pytest.raises(adc.AdcError) as e:
+        adc.FitEngine("gpoly", 6).chi2_gradient(h, [1, 0, 0.0, 0, 0, 0])
+    assert e.value.kind == "Eval"
+
+
+# ---------------------------------------------------------------------------- fit
+@pytest.mark.parametrize("key", ["gpoly_b400", "gsum1_b300"])
+def test_fit_iterates_match_reference(key):
+    g = golden("fit_cases.npz")
+    model = str(g[f"{key}_model"])
+    init = g[f"{key}_init"]
+    counts = g[f"{key}_counts"]
+    h = adc.Histogram(counts.size, -5.0, 5.0, float(counts.sum()), counts)
+    eng = adc.FitEngine(model, init.size)
+    res = eng.fit(h, init, adc.FitOptions(budget=12, trace_iterates=10))
+    ref_its = g[f"{key}_iterates"]
+    n_ref = min(10, int(g[f"{key}_iterations"]) + 1)
+    assert len(res.iterates) == n_ref
+    for k in range(n_ref):
+        assert rel_err(res.iterates[k], ref_its[k]).max() <= 1e-9, k
+    assert res.iterations == int(g[f"{key}_iterations"])
+    assert rel_err(res.params, g[f"{key}_params"]).max() <= 1e-9
+    assert rel_err(res.chi2, g[f"{key}_chi2"]) <= 1e-10
