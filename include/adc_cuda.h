@@ -43,6 +43,14 @@ const char* adc_cuda_last_error(void);
 /* Device query: SM count and compute capability of the current device. */
 int adc_cuda_device_info(int* sm_count, int* cc_major, int* cc_minor);
 
+/* Device memory and ordering helpers for C / C++ callers without a CUDA
+ * runtime of their own (the C++ mirror in include/adcx/adc_b200.hpp).
+ * kind: 1 = host->device, 2 = device->host, 3 = device->device. */
+int adc_cuda_alloc(void** ptr, size_t bytes);
+int adc_cuda_free(void* ptr);
+int adc_cuda_copy(void* dst, const void* src, size_t bytes, int32_t kind);
+int adc_cuda_synchronize(void);
+
 /* ---------------------------------------------------------------------------
  * Kernel registry.  Each hand-written kernel implements exactly one generated
  * gradient; it is keyed by the gradient's name (gradient_name,

@@ -1,0 +1,239 @@
+// adc_b200.hpp — header-only C++ mirror of the reference's hot-path API over
+// the B200 C ABI (include/adc_cuda.h).  Same type names, fields and error
+// behaviour as the reference (proj/include/adc/launch.hpp, fit.hpp,
+// diag.hpp) in namespace adc::b200, so C++ callers switch by namespace:
+//
+//   adc::launch(prog, "compute", cfg, buffers)   ->  adc::b200::launch("compute", cfg, buffers)
+//   adc::FitEngine().chi2_gradient(h, q, p, out)  ->  adc::b200::FitEngine("gsum", 3)...
+//
+// Differences, by design: a launch names the Listing-1 kernel (the DSL Program
+// is not needed on this path; the reference-side bridge in INTEGRATION.md
+// recognises it from the Program), and FitEngine takes the model name because
+// the B200 engine is model-parameterised (fit.cpp hard-wires gsum).
+// Link with -ladc_b200 (paper_2203_06139_b200/libadc_b200.so).
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "adc_cuda.h"
+
+namespace adc::b200 {
+
+// diag.hpp:17-23 order; Cuda/Arg are the device-side additions.
+enum class ErrorKind { Semantic, Transform, Eval, Launch, Io, Cuda, Arg };
+
+class Error : public std::runtime_error {
+ public:
+  Error(ErrorKind kind, const std::string& message) : std::runtime_error(message), kind_(kind) {}
+  ErrorKind kind() const { return kind_; }
+
+ private:
+  ErrorKind kind_;
+};
+
+inline void check(int rc) {
+  if (rc == ADC_OK) return;
+  throw Error(static_cast<ErrorKind>(rc - 1), adc_cuda_last_error());
+}
+
+// ---- launch.hpp ------------------------------------------------------------
+struct LaunchConfig {
+  int64_t grid_dim = 0;
+  int64_t block_dim = 0;
+  int64_t n = 0;
+  void validate() const {  // launch.cpp:9-19, same messages
+    if (grid_dim <= 0 || block_dim <= 0 || n <= 0)
+      throw Error(ErrorKind::Launch, "launch configuration must be positive (grid " +
+                                         std::to_string(grid_dim) + ", block " +
+                                         std::to_string(block_dim) + ", n " + std::to_string(n) +
+                                         ")");
+    if (grid_dim * block_dim < n)
+      throw Error(ErrorKind::Launch, "grid " + std::to_string(grid_dim) + " x block " +
+                                         std::to_string(block_dim) +
+                                         " does not cover problem size " + std::to_string(n));
+  }
+};
+
+struct BufferSet {
+  std::map<std::string, std::vector<double>> arrays;
+  std::map<std::string, double> scalars;
+  std::map<std::string, int64_t> integers;
+};
+
+struct LaunchOptions {
+  bool unsafe = false;    // hazardous kernels have no B200 kernel: refused either way
+  unsigned workers = 0;   // accepted for drop-in use; the GPU result does not depend on it
+  bool sequential = false;
+};
+
+struct LaunchStats {
+  std::vector<uint32_t> thread_statements;  // 3 per active thread, 2 per padding thread
+};
+
+// adc::launch (launch.cpp:252-346) for the Listing-1 kernel `compute`
+// (kernels.dsl:9-14) with host buffers; callee_fingerprint 0 = the registry's.
+inline LaunchStats launch(const std::string& kernel, const LaunchConfig& cfg, BufferSet& buffers,
+                          const LaunchOptions& opts = {}, uint64_t callee_fingerprint = 0) {
+  cfg.validate();
+  if (kernel == "compute_shared") {
+    if (!opts.unsafe)
+      throw Error(ErrorKind::Launch,
+                  "launch refused, hazardous parameter(s): dsigma (whole array shared with a "
+                  "writing callee across threads); pass the unsafe flag to force");
+    throw Error(ErrorKind::Launch, "no B200 kernel registered for 'gauss_grad'");
+  }
+  if (kernel != "compute") throw Error(ErrorKind::Launch, "unknown kernel '" + kernel + "'");
+  int32_t id = -1;
+  check(adc_cuda_registry_find(
+      "gauss_grad_0_1",
+      callee_fingerprint ? callee_fingerprint
+                         : adc_cuda_registry_fingerprint(ADC_KERNEL_GAUSS_GRAD_0_1),
+      &id));
+  for (const char* name : {"x", "p", "dx", "dp"}) {
+    auto it = buffers.arrays.find(name);
+    if (it == buffers.arrays.end())
+      throw Error(ErrorKind::Launch, std::string("missing buffer '") + name + "'");
+    if (static_cast<int64_t>(it->second.size()) < cfg.n)
+      throw Error(ErrorKind::Launch, std::string("buffer '") + name + "' has length " +
+                                         std::to_string(it->second.size()) +
+                                         " but is indexed by thread over " +
+                                         std::to_string(cfg.n) + " elements");
+  }
+  auto s = buffers.scalars.find("sigma");
+  if (s == buffers.scalars.end()) throw Error(ErrorKind::Launch, "missing scalar value 'sigma'");
+  check(adc_cuda_compute_gauss_host(cfg.grid_dim, cfg.block_dim, cfg.n,
+                                    buffers.arrays["x"].data(), buffers.arrays["p"].data(),
+                                    s->second, buffers.arrays["dx"].data(),
+                                    buffers.arrays["dp"].data()));
+  LaunchStats st;
+  st.thread_statements.assign(static_cast<size_t>(cfg.grid_dim * cfg.block_dim), 2u);
+  for (int64_t g = 0; g < cfg.n; ++g) st.thread_statements[static_cast<size_t>(g)] = 3u;
+  return st;
+}
+
+// The batched path the reference cannot express:
+// gaussnd_grad_0_1 over n points, structure-of-arrays [d * ld + i].
+inline void launch_batch_gaussnd(int64_t n, int64_t dim, const std::vector<double>& x,
+                                 const std::vector<double>& p, double sigma,
+                                 std::vector<double>& dx, std::vector<double>& dp) {
+  const size_t need = static_cast<size_t>(n * dim);
+  if (x.size() < need || p.size() < need || dx.size() < need || dp.size() < need)
+    throw Error(ErrorKind::Launch, "gaussnd buffers shorter than dim * n");
+  check(adc_cuda_gaussnd_grad_host(n, dim, n, x.data(), p.data(), sigma, dx.data(), dp.data()));
+}
+
+// ---- fit.hpp -------------------------------------------------------------
+struct Histogram {
+  int bins = 0;
+  double lo = 0.0;
+  double hi = 0.0;
+  uint64_t events = 0;
+  std::vector<double> counts;
+  double width() const { return (hi - lo) / bins; }
+  double center(int i) const { return lo + (i + 0.5) * width(); }
+};
+
+struct FitOptions {
+  int budget = 400;
+  double grad_tol = 1e-6;
+  double chi2_rel_tol = 1e-12;
+  double sigma_min = 1e-3;
+  double armijo_c1 = 1e-4;
+  int trace_iterates = 0;
+};
+
+struct FitResult {
+  std::vector<double> params;
+  double chi2 = 0.0;
+  int iterations = 0;
+  uint64_t gradient_evals = 0;
+  uint64_t gradient_wall_ns = 0;
+  bool converged = false;
+  int sigma_clamps = 0;
+  std::vector<std::vector<double>> iterates;
+};
+
+class FitEngine {
+ public:
+  // model: "gsum" (np = 3K, fit.cpp:125-138) or "gpoly" (np = 6).
+  FitEngine(std::string model = "gsum", int np = 3) : model_(std::move(model)), np_(np) {
+    if (model_ != "gsum" && model_ != "gpoly")
+      throw Error(ErrorKind::Arg, "unknown model '" + model_ + "'");
+  }
+  ~FitEngine() { release(); }
+  FitEngine(const FitEngine&) = delete;
+  FitEngine& operator=(const FitEngine&) = delete;
+
+  std::string gradient_fn_name() const { return model_ + "_grad_1"; }
+
+  double chi2(const Histogram& h, const std::vector<double>& q) {
+    double c2 = 0.0;
+    check(adc_cuda_chi2(plan(h), q.data(), &c2));
+    return c2;
+  }
+  void chi2_gradient(const Histogram& h, const std::vector<double>& q, std::vector<double>& out) {
+    out.assign(q.size(), 0.0);
+    check(adc_cuda_chi2_gradient(plan(h), q.data(), out.data(), nullptr));
+  }
+  FitResult fit(const Histogram& h, std::vector<double> init, const FitOptions& o = {}) {
+    std::vector<int32_t> clamp;
+    if (model_ == "gsum")
+      for (int i = 2; i < np_; i += 3) clamp.push_back(i);
+    else
+      clamp.push_back(2);
+    adc_fit_options co{o.budget, o.grad_tol, o.chi2_rel_tol, o.sigma_min, o.armijo_c1,
+                       o.trace_iterates};
+    adc_fit_result cr{};
+    std::vector<double> its(static_cast<size_t>(std::max(1, o.trace_iterates) * np_));
+    check(adc_cuda_fit(plan(h), init.data(), clamp.data(), static_cast<int32_t>(clamp.size()),
+                       &co, &cr, its.data()));
+    FitResult r;
+    r.params = init;
+    r.chi2 = cr.chi2;
+    r.iterations = cr.iterations;
+    r.gradient_evals = cr.gradient_evals;
+    r.gradient_wall_ns = cr.gradient_ns;
+    r.converged = cr.converged != 0;
+    r.sigma_clamps = cr.sigma_clamps;
+    const int n_tr = o.trace_iterates ? std::min(o.trace_iterates, cr.iterations + 1) : 0;
+    for (int k = 0; k < n_tr; ++k)
+      r.iterates.emplace_back(its.begin() + k * np_, its.begin() + (k + 1) * np_);
+    return r;
+  }
+
+ private:
+  // One device-resident histogram is cached (re-uploaded when `h` changes).
+  adc_chi2_plan* plan(const Histogram& h) {
+    if (plan_ != nullptr && key_ == &h && key_counts_ == h.counts.data()) return plan_;
+    release();
+    const size_t bytes = h.counts.size() * sizeof(double);
+    check(adc_cuda_alloc(&counts_, bytes));
+    check(adc_cuda_copy(counts_, h.counts.data(), bytes, 1));
+    check(adc_cuda_chi2_plan_create(&plan_, model_ == "gsum" ? ADC_MODEL_GSUM : ADC_MODEL_GPOLY,
+                                    np_, h.bins, h.lo, h.hi, static_cast<double>(h.events),
+                                    static_cast<const double*>(counts_), 1, 0, nullptr));
+    key_ = &h;
+    key_counts_ = h.counts.data();
+    return plan_;
+  }
+  void release() {
+    if (plan_) adc_cuda_chi2_plan_destroy(plan_);
+    if (counts_) adc_cuda_free(counts_);
+    plan_ = nullptr;
+    counts_ = nullptr;
+  }
+
+  std::string model_;
+  int np_;
+  adc_chi2_plan* plan_ = nullptr;
+  void* counts_ = nullptr;
+  const Histogram* key_ = nullptr;
+  const double* key_counts_ = nullptr;
+};
+
+}  // namespace adc::b200

@@ -52,6 +52,10 @@ SIGNATURES = {
     "adc_cuda_abi_version": (ctypes.c_int, []),
     "adc_cuda_last_error": (ctypes.c_char_p, []),
     "adc_cuda_device_info": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)] * 3),
+    "adc_cuda_alloc": (ctypes.c_int, [ctypes.POINTER(_VP), ctypes.c_size_t]),
+    "adc_cuda_free": (ctypes.c_int, [_VP]),
+    "adc_cuda_copy": (ctypes.c_int, [_VP, _VP, ctypes.c_size_t, _I32]),
+    "adc_cuda_synchronize": (ctypes.c_int, []),
     "adc_cuda_fingerprint": (ctypes.c_uint64, [ctypes.c_char_p, ctypes.c_size_t]),
     "adc_cuda_registry_find": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_uint64,
                                               ctypes.POINTER(_I32)]),

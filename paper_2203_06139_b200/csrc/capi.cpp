@@ -117,6 +117,43 @@ extern "C" int adc_cuda_device_info(int* sms, int* cc_major, int* cc_minor) {
   return ADC_OK;
 }
 
+extern "C" int adc_cuda_alloc(void** ptr, size_t bytes) {
+  clear_error();
+  if (ptr == nullptr) return fail(ADC_E_ARG, "null argument");
+  *ptr = nullptr;
+  if (int rc = require_device()) return rc;
+  ADCB_CUDA(cudaMalloc(ptr, bytes));
+  return ADC_OK;
+}
+
+extern "C" int adc_cuda_free(void* ptr) {
+  clear_error();
+  if (ptr == nullptr) return ADC_OK;
+  ADCB_CUDA(cudaFree(ptr));
+  return ADC_OK;
+}
+
+extern "C" int adc_cuda_copy(void* dst, const void* src, size_t bytes, int32_t kind) {
+  clear_error();
+  if (bytes == 0) return ADC_OK;
+  if (dst == nullptr || src == nullptr) return fail(ADC_E_ARG, "null argument");
+  const cudaMemcpyKind k = kind == 1   ? cudaMemcpyHostToDevice
+                           : kind == 2 ? cudaMemcpyDeviceToHost
+                           : kind == 3 ? cudaMemcpyDeviceToDevice
+                                       : cudaMemcpyDefault;
+  if (kind < 1 || kind > 3) return fail(ADC_E_ARG, "copy kind must be 1, 2 or 3");
+  if (int rc = require_device()) return rc;
+  ADCB_CUDA(cudaMemcpy(dst, src, bytes, k));
+  return ADC_OK;
+}
+
+extern "C" int adc_cuda_synchronize(void) {
+  clear_error();
+  if (int rc = require_device()) return rc;
+  ADCB_CUDA(cudaDeviceSynchronize());
+  return ADC_OK;
+}
+
 // ---------------------------------------------------------------------------
 // Registry.  Fingerprints are FNV-1a-64 of adc::print(<generated gradient>)
 // as produced by the unmodified reference (tests/golden/gradient_fingerprints.json,

@@ -18,10 +18,12 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "chi2_internal.h"
 #include "common.cuh"
+#include "fastmath.cuh"
 
 namespace adcb {
 
@@ -35,22 +37,45 @@ struct QDev {
   double inv[kMaxNp];  // 1/q for width parameters (fast mode)
 };
 
+// ---- fast-mode math ----------------------------------------------------------
+// exp_nonpos (fastmath.cuh): table-driven exp for the models' non-positive
+// arguments, ~11 FP64 ops with its constants in uniform registers.
+// 1/c for a positive count: MUFU.RCP64H seed + two Newton steps.
+__device__ __forceinline__ double rcp_pos(double c) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(c));
+  double e = __fma_rn(-c, r, 1.0);
+  r = __fma_rn(r, e, r);
+  e = __fma_rn(-c, r, 1.0);
+  return __fma_rn(r, e, r);
+}
+
 // ---- models ------------------------------------------------------------------
 // gpoly (oracle/dsl/gpoly.dsl) and its generated gpoly_grad_1; gsum
 // (fit.cpp:125-138) and gsum_grad_1.  FAST replaces the divisions by the
 // width parameter with multiplies by its host-computed reciprocal.
 struct GPoly {
   static constexpr int NP = 6;
+  struct Reg {  // uniform parameters, held in registers for the whole pass
+    double q0, q1, q2, q3, q4, q5, inv2;
+  };
+  __device__ static __forceinline__ Reg load(const QDev& Q) {
+    return Reg{Q.q[0], Q.q[1], Q.q[2], Q.q[3], Q.q[4], Q.q[5], Q.inv[2]};
+  }
   template <bool GRAD, bool FAST>
-  __device__ static __forceinline__ void eval(double x, const QDev& Q, double& m, double* bg) {
-    const double q0 = Q.q[0], q1 = Q.q[1], q2 = Q.q[2], q3 = Q.q[3], q4 = Q.q[4], q5 = Q.q[5];
+  __device__ static __forceinline__ void eval(double x, const Reg& Q, const double* tab, double& m,
+                                              double* bg) {
+    const double q0 = Q.q0, q1 = Q.q1, q2 = Q.q2, q3 = Q.q3, q4 = Q.q4, q5 = Q.q5;
     const double t0 = fsub(x, q1);                              // _t0 = x - q[1]
-    const double z = FAST ? fmul(t0, Q.inv[2]) : fdiv(t0, q2);  // z = _t0 / q[2]
+    const double z = FAST ? fmul(t0, Q.inv2) : fdiv(t0, q2);    // z = _t0 / q[2]
     const double t1 = fmul(-0.5, z);                            // _t1 = -0.5 * z
     const double t2 = fmul(t1, z);                              // _t2 = _t1 * z
-    const double e = exp(t2);                                   // _t3 = exp(_t2)
+    const double e = FAST ? exp_nonpos(t2, tab) : exp(t2);      // _t3 = exp(_t2)
     const double g = fmul(q0, e);                               // g = q[0] * _t3
-    m = fadd(fadd(fadd(g, q3), fmul(q4, x)), fmul(fmul(q5, x), x));
+    if (FAST)
+      m = __fma_rn(q5 * x, x, __fma_rn(q4, x, g + q3));
+    else
+      m = fadd(fadd(fadd(g, q3), fmul(q4, x)), fmul(fmul(q5, x), x));
     if constexpr (GRAD) {
       // gpoly_grad_1 reverse sweep with the unit seeds folded (0 + v terms
       // only normalise -0, which cannot change a sum).
@@ -61,9 +86,9 @@ struct GPoly {
       const double r8 = fmul(q0, e);          // _r8 = (q[0]*_r6)*_q0
       const double d1 = fmul(r8, z);          // _d__t1 += _r8*z
       double dz = fmul(t1, r8);               // _d_z += _t1*_r8
-      dz = fadd(dz, fmul(-0.5, d1));          // _d_z += -0.5*_r9
-      const double r11 = FAST ? fmul(dz, Q.inv[2]) : fdiv(dz, q2);             // _r10/q[2]
-      bg[2] = -(FAST ? fmul(fmul(dz, z), Q.inv[2]) : fdiv(fmul(dz, z), q2));  // -(_r10*_q1/q[2])
+      dz = FAST ? __fma_rn(-0.5, d1, dz) : fadd(dz, fmul(-0.5, d1));  // _d_z += -0.5*_r9
+      const double r11 = FAST ? fmul(dz, Q.inv2) : fdiv(dz, q2);             // _r10/q[2]
+      bg[2] = -(FAST ? fmul(fmul(dz, z), Q.inv2) : fdiv(fmul(dz, z), q2));  // -(_r10*_q1/q[2])
       bg[1] = -r11;                                                            // _d_q[1] += -_r11
     }
   }
@@ -72,25 +97,38 @@ struct GPoly {
 template <int K>
 struct GSum {
   static constexpr int NP = 3 * K;
+  struct Reg {
+    double q[3 * K];
+    double inv[K];
+  };
+  __device__ static __forceinline__ Reg load(const QDev& Q) {
+    Reg r;
+#pragma unroll
+    for (int i = 0; i < 3 * K; ++i) r.q[i] = Q.q[i];
+#pragma unroll
+    for (int j = 0; j < K; ++j) r.inv[j] = Q.inv[3 * j + 2];
+    return r;
+  }
   template <bool GRAD, bool FAST>
-  __device__ static __forceinline__ void eval(double x, const QDev& Q, double& m, double* bg) {
+  __device__ static __forceinline__ void eval(double x, const Reg& Q, const double* tab, double& m,
+                                              double* bg) {
     double acc = 0.0;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       const double amp = Q.q[3 * j], mu = Q.q[3 * j + 1], sg = Q.q[3 * j + 2];
       const double t0 = fsub(x, mu);                                   // _t0 = x - mu
-      const double z = FAST ? fmul(t0, Q.inv[3 * j + 2]) : fdiv(t0, sg);  // z = _t0 / sg
+      const double z = FAST ? fmul(t0, Q.inv[j]) : fdiv(t0, sg);  // z = _t0 / sg
       const double t1 = fmul(-0.5, z);                                 // _t1 = -0.5 * z
       const double t2 = fmul(t1, z);                                   // _t2 = _t1 * z
-      const double e = exp(t2);                                        // _t3 = exp(_t2)
-      acc = fadd(acc, fmul(amp, e));                                   // acc = acc + amp*_t3
+      const double e = FAST ? exp_nonpos(t2, tab) : exp(t2);           // _t3 = exp(_t2)
+      acc = FAST ? __fma_rn(amp, e, acc) : fadd(acc, fmul(amp, e));    // acc = acc + amp*_t3
       if constexpr (GRAD) {
         const double r3 = fmul(amp, e);        // _r3 = (amp*_r1)*_q0
         const double r4 = fmul(r3, z);         // _d__t1 += _r3*z
         double dz = fmul(t1, r3);              // _d_z += _t1*_r3
-        dz = fadd(dz, fmul(-0.5, r4));         // _d_z += -0.5*_r4
-        const double r6 = FAST ? fmul(dz, Q.inv[3 * j + 2]) : fdiv(dz, sg);
-        bg[3 * j + 2] = -(FAST ? fmul(fmul(dz, z), Q.inv[3 * j + 2]) : fdiv(fmul(dz, z), sg));
+        dz = FAST ? __fma_rn(-0.5, r4, dz) : fadd(dz, fmul(-0.5, r4));  // _d_z += -0.5*_r4
+        const double r6 = FAST ? fmul(dz, Q.inv[j]) : fdiv(dz, sg);
+        bg[3 * j + 2] = -(FAST ? fmul(fmul(dz, z), Q.inv[j]) : fdiv(fmul(dz, z), sg));
         bg[3 * j + 1] = -r6;                   // _d_mu += -_r6
         bg[3 * j] = e;                         // _d_amp += _r1*_t3
       }
@@ -100,48 +138,131 @@ struct GSum {
 };
 
 // ---- K3: tile pass -------------------------------------------------------------
-template <class M, bool GRAD, bool FAST, int BPT>
-__global__ void __launch_bounds__(kTileThreads) chi2_tile_kernel(Chi2Pass P) {
+// Per thread: bins base + k*256 (k < BPT) in increasing k, counts streamed
+// through a PD-deep register ring (+ an L2 prefetch of the next tile), so the
+// FP64 pipe is not left waiting on HBM.  Accumulation is branch-free: with
+// w = [c > 0] and ic = [c > 0]/c,
+//   S += m; A1 += w m; A2 += m (m ic); C0 += c; G0 += dm; G1 += w dm; G2 += (m ic) dm.
+// Full tiles skip the per-bin bounds test.
+constexpr int kPD = 4;
+
+// CTAs per SM the register budget is tuned for (spill-free at these counts).
+// (measured on B200: 2 x 256 threads with 128 registers beats 3 x 256 with 80
+// for the gpoly gradient pass, 0.503 vs 0.539 ms at 1e8 bins)
+template <class M, bool GRAD>
+constexpr int tile_min_blocks() {
+  return M::NP <= 6 ? 2 : 1;
+}
+
+template <class M, bool GRAD, bool FAST>
+struct BinTerm {
+  double m, c, w, mc;
+  double bg[GRAD ? M::NP : 1];
+};
+
+// jh = j + 0.5 exactly (j < 2^52), so x is bit-identical to Histogram::center.
+template <class M, bool GRAD, bool FAST>
+__device__ __forceinline__ void bin_term(const Chi2Pass& P, const typename M::Reg& QR,
+                                         const double* tab, double jh, double c,
+                                         BinTerm<M, GRAD, FAST>& t) {
+  const double x = fadd(P.lo, fmul(jh, P.width));  // Histogram::center: lo + (j + 0.5) * width
+  M::template eval<GRAD, FAST>(x, QR, tab, t.m, t.bg);
+  const bool pos = c > 0.0;
+  t.c = c;
+  t.w = pos ? 1.0 : 0.0;
+  const double ic = pos ? (FAST ? rcp_pos(c) : 1.0 / c) : 0.0;
+  t.mc = t.m * ic;
+}
+
+template <class M, bool GRAD, bool FAST>
+__device__ __forceinline__ void bin_accumulate(const BinTerm<M, GRAD, FAST>& t, double* acc) {
+  constexpr int NP = M::NP;
+  acc[0] += t.m;
+  acc[1] = __fma_rn(t.w, t.m, acc[1]);
+  acc[2] = __fma_rn(t.m, t.mc, acc[2]);
+  acc[3] += t.c;
+  if constexpr (GRAD) {
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      acc[4 + i] += t.bg[i];
+      acc[4 + NP + i] = __fma_rn(t.w, t.bg[i], acc[4 + NP + i]);
+      acc[4 + 2 * NP + i] = __fma_rn(t.mc, t.bg[i], acc[4 + 2 * NP + i]);
+    }
+  }
+}
+
+// PAIR evaluates two independent bins before folding either, giving the
+// scheduler two dependency chains to interleave (the model's exp chain is
+// ~15 dependent FP64 ops deep).  The accumulation order is unchanged.
+template <class M, bool GRAD, bool FAST, int BPT, bool CHECK, bool PAIR>
+__device__ __forceinline__ void tile_bins(const Chi2Pass& P, const typename M::Reg& QR,
+                                          const double* tab, int64_t base, double* acc) {
+  constexpr int PD = BPT < kPD ? BPT : kPD;
+  constexpr int STEP = PAIR && PD >= 2 ? 2 : 1;
+  double ring[PD];
+#pragma unroll
+  for (int k = 0; k < PD; ++k) {
+    const int64_t j = base + (int64_t)k * kTileThreads;
+    ring[k] = (!CHECK || j < P.bin_end) ? ld_stream(P.counts + j) : 0.0;
+  }
+  double jh = fadd((double)base, 0.5);  // advanced by 256.0 per bin: exact integers + 0.5
+  for (int k0 = 0; k0 < BPT; k0 += PD) {
+#pragma unroll
+    for (int kk = 0; kk < PD; kk += STEP) {
+      BinTerm<M, GRAD, FAST> t[STEP];
+      bool valid[STEP];
+#pragma unroll
+      for (int u = 0; u < STEP; ++u) {
+        const int k = k0 + kk + u;
+        const int64_t j = base + (int64_t)k * kTileThreads;
+        const double c = ring[kk + u];
+        const int64_t jn = j + (int64_t)PD * kTileThreads;
+        ring[kk + u] = (k + PD < BPT && (!CHECK || jn < P.bin_end)) ? ld_stream(P.counts + jn)
+                                                                     : 0.0;
+        valid[u] = !CHECK || j < P.bin_end;
+        if (valid[u]) bin_term<M, GRAD, FAST>(P, QR, tab, jh, c, t[u]);
+        jh = fadd(jh, (double)kTileThreads);
+      }
+#pragma unroll
+      for (int u = 0; u < STEP; ++u)
+        if (valid[u]) bin_accumulate<M, GRAD, FAST>(t[u], acc);
+    }
+  }
+}
+
+template <class M, bool GRAD, bool FAST, int BPT, int MINB = tile_min_blocks<M, GRAD>(),
+          bool PAIR = false>
+__global__ void __launch_bounds__(kTileThreads, MINB) chi2_tile_kernel(Chi2Pass P) {
   constexpr int NP = M::NP;
   constexpr int R = GRAD ? 4 + 3 * NP : 4;
   __shared__ QDev Q;
   __shared__ double red[kTileThreads / 32][R];
+  __shared__ double tab[64];
   if (threadIdx.x < kMaxNp) {
     Q.q[threadIdx.x] = P.qdev[threadIdx.x];
     Q.inv[threadIdx.x] = P.qdev[kMaxNp + threadIdx.x];
   }
+  if (threadIdx.x < 64) tab[threadIdx.x] = exp2((double)threadIdx.x / 64.0);
   __syncthreads();
+  const typename M::Reg QR = M::load(Q);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int64_t TB = (int64_t)BPT * kTileThreads;
   for (int64_t tile = P.tile_begin + blockIdx.x; tile < P.tile_end; tile += gridDim.x) {
+    const int64_t base = tile * TB + threadIdx.x;
+    {  // the next tile of this CTA into L2 while this one computes
+      const int64_t nb = base + (int64_t)gridDim.x * TB;
+#pragma unroll 4
+      for (int k = 0; k < BPT; k += 4)
+        if (nb + (int64_t)k * kTileThreads < P.bin_end)
+          prefetch_l2(P.counts + nb + (int64_t)k * kTileThreads);
+    }
     double acc[R];
 #pragma unroll
     for (int v = 0; v < R; ++v) acc[v] = 0.0;
-    const int64_t base = tile * (int64_t)(BPT * kTileThreads) + threadIdx.x;
-#pragma unroll 2
-    for (int k = 0; k < BPT; ++k) {
-      const int64_t j = base + (int64_t)k * kTileThreads;
-      if (j < P.bin_end) {
-        const double c = ld_stream(P.counts + j);
-        const double x = fadd(P.lo, fmul(fadd((double)j, 0.5), P.width));  // Histogram::center
-        double m, bg[GRAD ? NP : 1];
-        M::template eval<GRAD, FAST>(x, Q, m, bg);
-        const bool pos = c > 0.0;
-        const double ic = pos ? (FAST ? __drcp_rn(c) : 1.0) : 0.0;
-        const double mc = pos ? (FAST ? m * ic : m / c) : 0.0;
-        acc[0] += m;
-        acc[1] += pos ? m : 0.0;
-        acc[2] += m * mc;
-        acc[3] += pos ? c : 0.0;
-        if constexpr (GRAD) {
-#pragma unroll
-          for (int i = 0; i < NP; ++i) {
-            acc[4 + i] += bg[i];
-            acc[4 + NP + i] += pos ? bg[i] : 0.0;
-            acc[4 + 2 * NP + i] += mc * bg[i];
-          }
-        }
-      }
-    }
+    if ((tile + 1) * TB <= P.bin_end)
+      tile_bins<M, GRAD, FAST, BPT, false, PAIR>(P, QR, tab, base, acc);
+    else
+      tile_bins<M, GRAD, FAST, BPT, true, PAIR>(P, QR, tab, base, acc);
     // fixed shuffle tree, then fixed cross-warp tree
 #pragma unroll
     for (int v = 0; v < R; ++v) {
@@ -186,9 +307,24 @@ __global__ void __launch_bounds__(kChunkThreads) chi2_chunk_kernel(
 }
 
 // ---- dispatch ----------------------------------------------------------------
+int g_chi2_tune = 0;  // experiment knob (ADC_CHI2_TUNE): 0 default, 1 = 3 CTAs/SM, 2 = paired bins
+
 template <class M, bool GRAD, bool FAST>
 static void launch_tiles_t(const Chi2Pass& P, int bpt, int blocks, cudaStream_t s) {
-  if (bpt == 32)
+  constexpr int MB = tile_min_blocks<M, GRAD>();
+  if constexpr (std::is_same<M, GPoly>::value && FAST) {
+    if (bpt == 128 && g_chi2_tune != 0) {  // experiments: 1 = 3 CTAs/SM, 2 = paired bins
+      const int b3 = std::min(blocks * 3 / 2, sm_count() * 3);
+      if (g_chi2_tune == 1)
+        chi2_tile_kernel<M, GRAD, FAST, 128, 3, false><<<b3, kTileThreads, 0, s>>>(P);
+      else
+        chi2_tile_kernel<M, GRAD, FAST, 128, MB, true><<<blocks, kTileThreads, 0, s>>>(P);
+      return;
+    }
+  }
+  if (bpt == 128)
+    chi2_tile_kernel<M, GRAD, FAST, 128><<<blocks, kTileThreads, 0, s>>>(P);
+  else if (bpt == 32)
     chi2_tile_kernel<M, GRAD, FAST, 32><<<blocks, kTileThreads, 0, s>>>(P);
   else
     chi2_tile_kernel<M, GRAD, FAST, 4><<<blocks, kTileThreads, 0, s>>>(P);
@@ -212,7 +348,9 @@ int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast, int
   if (ntiles <= 0) return ADC_OK;
   const int R = grad ? 4 + 3 * np : 4;
   // Persistent grid: a few CTAs per SM, tiles grid-strided.
-  const int64_t blocks = std::min<int64_t>(ntiles, (int64_t)sm_count() * 4);
+  // Persistent grid: as many CTAs as are resident (2 per SM for the small
+  // models, see tile_min_blocks), tiles grid-strided.
+  const int64_t blocks = std::min<int64_t>(ntiles, (int64_t)sm_count() * (np <= 6 ? 2 : 1));
   if (model == ADC_MODEL_GPOLY) {
     launch_tiles_m<GPoly>(P, grad, fast, bpt, (int)blocks, s);
   } else {
@@ -245,5 +383,10 @@ void fill_qdev(int model, int np, const double* q, double* host_qdev) {
 }
 
 size_t qdev_bytes() { return sizeof(QDev); }
+
+int chi2_set_tune(int v) {
+  g_chi2_tune = v;
+  return ADC_OK;
+}
 
 }  // namespace adcb

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -20,10 +21,20 @@ using namespace adcb;
 
 namespace {
 
-constexpr int64_t kChunkTiles = 128;
 constexpr int64_t kTileThreads = 256;
+constexpr int64_t kChunkBins = int64_t(1) << 20;  // large histograms: 1 Mi-bin chunks
 
-int bpt_for(int64_t bins) { return bins >= (int64_t(1) << 22) ? 32 : 4; }
+// Bins per thread per tile: large histograms amortise the per-tile reduction
+// over more bins; small ones keep enough tiles to fill 148 SMs.
+int bpt_for(int64_t bins) {
+  if (bins >= (int64_t(1) << 24)) return 128;
+  if (bins >= (int64_t(1) << 22)) return 32;
+  return 4;
+}
+int64_t chunk_tiles_for(int64_t bins) {
+  const int64_t tile = bpt_for(bins) * kTileThreads;
+  return bins >= (int64_t(1) << 22) ? kChunkBins / tile : 128;  // <= 128 (K4 handles 128)
+}
 
 }  // namespace
 
@@ -36,12 +47,12 @@ extern "C" int adc_chi2_make_layout(int64_t bins, int32_t world, int32_t rank,
   adc_chi2_layout L{};
   L.bins = bins;
   L.tile_bins = bpt_for(bins) * kTileThreads;
-  L.chunk_tiles = kChunkTiles;
+  L.chunk_tiles = chunk_tiles_for(bins);
   const int64_t ntiles = (bins + L.tile_bins - 1) / L.tile_bins;
-  L.nchunks = (ntiles + kChunkTiles - 1) / kChunkTiles;
+  L.nchunks = (ntiles + L.chunk_tiles - 1) / L.chunk_tiles;
   L.chunk_begin = L.nchunks * rank / world;
   L.chunk_end = L.nchunks * (rank + 1) / world;
-  const int64_t chunk_bins = L.tile_bins * kChunkTiles;
+  const int64_t chunk_bins = L.tile_bins * L.chunk_tiles;
   L.bin_begin = std::min(bins, L.chunk_begin * chunk_bins);
   L.bin_end = std::min(bins, L.chunk_end * chunk_bins);
   *out = L;
@@ -96,7 +107,7 @@ struct adc_chi2_plan {
   int fast = 1;
   int device = 0;
   cudaStream_t stream = nullptr;       // plan-owned: graph replays
-  cudaStream_t user_stream = nullptr;  // caller's: adc_cuda_chi2_partials
+  cudaStream_t user_stream = nullptr;  // caller's (0 = legacy default): adc_cuda_chi2_partials
   double* qdev = nullptr;
   double* tile_ws = nullptr;
   double* records = nullptr;
@@ -255,8 +266,9 @@ extern "C" int adc_cuda_chi2_plan_layout(const adc_chi2_plan* P, adc_chi2_layout
 
 extern "C" int adc_cuda_chi2_set_precision(adc_chi2_plan* P, int32_t mode) {
   clear_error();
-  if (P == nullptr || (mode != 0 && mode != 1)) return fail(ADC_E_ARG, "precision mode is 0 or 1");
+  if (P == nullptr || mode < 0 || mode > 1) return fail(ADC_E_ARG, "precision mode is 0 or 1");
   P->fast = mode;
+  if (const char* t = getenv("ADC_CHI2_TUNE")) chi2_set_tune(atoi(t));
   return ADC_OK;
 }
 
@@ -270,7 +282,7 @@ extern "C" int adc_cuda_chi2_partials(adc_chi2_plan* P, const double* q, int32_t
   if (P == nullptr || q == nullptr) return fail(ADC_E_ARG, "null argument");
   if (int rc = check_domain(P, q)) return rc;
   ADCB_CUDA(cudaSetDevice(P->device));
-  cudaStream_t s = P->user_stream ? P->user_stream : P->stream;
+  cudaStream_t s = P->user_stream;  // the caller's stream (0 = legacy default stream)
   // h_q may still be read by an in-flight copy of a previous pass
   ADCB_CUDA(cudaStreamSynchronize(s));
   fill_qdev(P->model, P->np, q, P->h_q);

@@ -23,5 +23,6 @@ int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast, int
                  int64_t chunk_tiles, double* records, cudaStream_t s);
 void fill_qdev(int model, int np, const double* q, double* host_qdev);
 size_t qdev_bytes();
+int chi2_set_tune(int v);  // kernel-variant experiments (ADC_CHI2_TUNE)
 
 }  // namespace adcb

@@ -33,6 +33,23 @@ __device__ __forceinline__ double2 ld_stream2(const double2* p) {
   return v;
 }
 
+// L2 prefetch of the line holding p (no register cost, no completion wait):
+// keeps more DRAM requests in flight than the register budget allows.
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// L2 prefetch of [p, p+bytes) through the bulk-copy (TMA) unit: one lane
+// covers a whole row segment, so it does not occupy the LSU queue.  The
+// range is widened to 16-byte alignment as the instruction requires.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, unsigned bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const uintptr_t lo = a & ~uintptr_t(15);
+  const uintptr_t hi = (a + bytes + 15) & ~uintptr_t(15);
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((unsigned)(hi - lo))
+               : "memory");
+}
+
 // Thread-local error state behind adc_cuda_last_error().
 void set_error(const std::string& msg);
 void clear_error();

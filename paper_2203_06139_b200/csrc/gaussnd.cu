@@ -25,7 +25,7 @@
 
 namespace adcb {
 
-template <int W, int U>
+template <int W, int U, int PF>
 __global__ void __launch_bounds__(W * 32) gaussnd_tile_kernel(
     const double* __restrict__ x, const double* __restrict__ p, double* __restrict__ dx,
     double* __restrict__ dp, int64_t n, int dim, int64_t ld, double t4, double r1, int dpw,
@@ -55,6 +55,37 @@ __global__ void __launch_bounds__(W * 32) gaussnd_tile_kernel(
         for (int k = 0; k < U; ++k) {
           xv[k] = ld_stream(xi + (int64_t)(d + k) * ld);
           pv[k] = ld_stream(pi + (int64_t)(d + k) * ld);
+        }
+        if (PF == 2) {
+          // lane l < U: x row d+U+l, lane U+l: p row d+U+l (one 256 B segment
+          // each); past the range: the first dx / dp rows of the reverse sweep
+          const int l = lane % U;
+          const bool second = lane >= U && lane < 2 * U;
+          const int dn = d + U + l;
+          const int64_t tb = tile * 32;
+          const unsigned seg = (unsigned)((n - tb < 32 ? n - tb : 32) * sizeof(double));
+          if (lane < 2 * U) {
+            if (dn < d1) {
+              bulk_prefetch_l2((second ? p : x) + (int64_t)dn * ld + tb, seg);
+            } else if (d1 - 1 - (dn - d1) >= d0) {
+              bulk_prefetch_l2((second ? dp : dx) + (int64_t)(d1 - 1 - (dn - d1)) * ld + tb, seg);
+            }
+          }
+        } else if (PF == 1) {
+          // next batch of x, p rows; in the last batch, the first rows the
+          // reverse sweep will read (dx, dp at the top of the range)
+#pragma unroll
+          for (int k = 0; k < U; ++k) {
+            const int dn = d + U + k;
+            if (dn < d1) {
+              prefetch_l2(xi + (int64_t)dn * ld);
+              prefetch_l2(pi + (int64_t)dn * ld);
+            } else if (d1 - 1 - (dn - d1) >= d0) {
+              const int64_t o = (int64_t)(d1 - 1 - (dn - d1)) * ld;
+              prefetch_l2(dx + i + o);
+              prefetch_l2(dp + i + o);
+            }
+          }
         }
 #pragma unroll
         for (int k = 0; k < U; ++k) {
@@ -122,6 +153,37 @@ __global__ void __launch_bounds__(W * 32) gaussnd_tile_kernel(
           a[k] = dxi[o];
           b[k] = dpi[o];
         }
+        if (PF == 2) {
+          const int l = lane % U;
+          const bool second = lane >= U && lane < 2 * U;
+          const int dn = d - 1 - U - l;
+          const int64_t tb = tile * 32, tn = tb + (int64_t)gridDim.x * 32;
+          if (lane < 2 * U) {
+            if (dn >= d0) {
+              const unsigned seg = (unsigned)((n - tb < 32 ? n - tb : 32) * sizeof(double));
+              bulk_prefetch_l2((second ? dp : dx) + (int64_t)dn * ld + tb, seg);
+            } else if (tn < n && d0 + (d0 - 1 - dn) < d1) {
+              const unsigned seg = (unsigned)((n - tn < 32 ? n - tn : 32) * sizeof(double));
+              bulk_prefetch_l2((second ? p : x) + (int64_t)(d0 + (d0 - 1 - dn)) * ld + tn, seg);
+            }
+          }
+        } else if (PF == 1) {
+          // next batch of dx, dp rows (descending); in the last batch, the
+          // first x, p rows of this warp's next tile
+          const int64_t inext = i + (int64_t)gridDim.x * 32;
+#pragma unroll
+          for (int k = 0; k < U; ++k) {
+            const int dn = d - 1 - U - k;
+            if (dn >= d0) {
+              prefetch_l2(dxi + (int64_t)dn * ld);
+              prefetch_l2(dpi + (int64_t)dn * ld);
+            } else if (inext < n && d0 + (d0 - 1 - dn) < d1) {
+              const int64_t o = (int64_t)(d0 + (d0 - 1 - dn)) * ld;
+              prefetch_l2(x + inext + o);
+              prefetch_l2(p + inext + o);
+            }
+          }
+        }
 #pragma unroll
         for (int k = 0; k < U; ++k) {
           const double u = my_stage[(d - 1 - k - d0) * 32];
@@ -145,7 +207,9 @@ __global__ void __launch_bounds__(W * 32) gaussnd_tile_kernel(
 
 // ---------------------------------------------------------------------------
 // 0 auto; 1/3/4 = one warp per 32-point tile (reference summation order) with
-// 8/16/32 rows in flight per thread; 2 = dims split over the warps of a CTA.
+// 8/16/32 rows in flight per thread (+ L2 prefetch of the next batch);
+// 5 = as 3 without prefetch; 6 = as 3 with bulk (TMA-unit) prefetch;
+// 2 = dims split over the warps of a CTA (7 = same with bulk prefetch).
 static int g_variant = 0;
 
 struct NdConfig {
@@ -153,11 +217,11 @@ struct NdConfig {
   size_t smem;
 };
 
-template <int W, int U>
+template <int W, int U, int PF = 1>
 static int launch_tile(const NdConfig& c, int64_t n, int dim, int64_t ld, const double* x,
                        const double* p, double* dx, double* dp, double t4, double r1,
                        cudaStream_t s) {
-  auto k = gaussnd_tile_kernel<W, U>;
+  auto k = gaussnd_tile_kernel<W, U, PF>;
   if (c.smem > 48 * 1024)
     ADCB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem));
   int occ = 0;
@@ -178,7 +242,7 @@ static NdConfig choose(int dim) {
   const int variant = g_variant;
   // W = 1 keeps the reference's summation order; it needs the whole u row of
   // a point on chip: 256 B per dim per warp.  Use it while >= 8 warps fit.
-  if (variant == 1 || variant == 3 || variant == 4 ||
+  if (variant == 1 || variant == 3 || variant == 4 || variant == 5 || variant == 6 ||
       (variant == 0 && (size_t)dim * 256 * 8 <= kSmemPerSm)) {
     c.w = 1;
     c.dpw = dim;
@@ -215,15 +279,21 @@ int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, con
     case 1:
       if (c.u == 8) return launch_tile<1, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
       if (c.u == 32) return launch_tile<1, 32>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+      if (g_variant == 5)
+        return launch_tile<1, 16, 0>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+      if (g_variant == 6)
+        return launch_tile<1, 16, 2>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
       return launch_tile<1, 16>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
     case 8: return launch_tile<8, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
-    case 16: return launch_tile<16, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+    case 16:
+      if (g_variant == 7) return launch_tile<16, 8, 2>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+      return launch_tile<16, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
   }
   return fail(ADC_E_ARG, "gaussnd: bad configuration");
 }
 
 int gaussnd_set_variant(int v) {
-  if (v < 0 || v > 4) return fail(ADC_E_ARG, "gaussnd variant must be 0..4");
+  if (v < 0 || v > 7) return fail(ADC_E_ARG, "gaussnd variant must be 0..7");
   g_variant = v;
   return ADC_OK;
 }

@@ -114,4 +114,4 @@ def test_chi2_layout_shards_whole_chunks():
                 assert a.chunk_end == b.chunk_begin and a.bin_end == b.bin_begin
                 assert a.bin_end == min(bins, a.chunk_end * chunk_bins)
     L = adc.chi2_layout(10**8)
-    assert L.tile_bins == 8192 and L.nchunks == 96
+    assert L.tile_bins == 32768 and L.chunk_tiles == 32 and L.nchunks == 96

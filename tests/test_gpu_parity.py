@@ -114,7 +114,7 @@ def test_listing1_domain_error():
 ND_KEYS = ["d100_n64", "d1000_n8", "d1_n33", "d37_n70", "d128_n40", "d129_n5"]
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7])
 @pytest.mark.parametrize("key", ND_KEYS)
 def test_gaussnd_golden(key, variant):
     g = golden("gaussnd_cases.npz")
@@ -144,7 +144,7 @@ def test_gaussnd_vs_oracle(restate, dim, n):
     x, p = synth.points_nd(dim, n, seed=dim)
     ox, op = np.zeros((dim, n)), np.zeros((dim, n))
     restate.gaussnd_grad(x, p, 1.3, ox, op)
-    for variant in (1, 2):
+    for variant in (1, 2, 6, 7):
         set_gaussnd_variant(variant)
         try:
             dx = torch.zeros((dim, n), dtype=torch.float64, device=DEV)
