@@ -1,0 +1,236 @@
+// Reference-side binding (see adc_b200_bridge.hpp).  Uses only the reference's
+// public API plus the C ABI of include/adc_cuda.h.
+#include "adc_b200_bridge.hpp"
+
+#include <cstring>
+#include <map>
+
+#include "adc/parser.hpp"
+#include "adc/printer.hpp"
+#include "adc/transform.hpp"
+#include "adc_cuda.h"
+
+namespace adc::b200_bridge {
+namespace {
+
+[[noreturn]] void rethrow(int rc) {
+  // adc_status 1..5 == ErrorKind + 1 (include/adc_cuda.h)
+  ErrorKind k = rc >= 1 && rc <= 5 ? static_cast<ErrorKind>(rc - 1) : ErrorKind::Launch;
+  throw Error(k, std::string("B200: ") + adc_cuda_last_error());
+}
+void check(int rc) {
+  if (rc != ADC_OK) rethrow(rc);
+}
+
+uint64_t fingerprint(const FunctionDef& f) {
+  const std::string text = print(f);
+  return adc_cuda_fingerprint(text.data(), text.size());
+}
+
+bool is_var(const Expr& e, const char* name) {
+  return e.kind == ExprKind::VarRef && e.name == name;
+}
+
+// The Listing-1 shape (kernels.dsl:9-14):
+//   integer i = blockIdx * blockDim + threadIdx;  if (i < N) { grad(args...); }
+struct Listing1 {
+  std::string thread_var;
+  const Stmt* call = nullptr;
+};
+
+bool match_listing1(const FunctionDef& k, Listing1& out) {
+  if (k.body.size() != 2) return false;
+  const Stmt& d = *k.body[0];
+  if (d.kind != StmtKind::VarDecl || d.decl_type != ValType::Integer || !d.expr) return false;
+  const Expr& e = *d.expr;
+  if (e.kind != ExprKind::Binary || e.op != BinOp::Add) return false;
+  const Expr& mul = *e.args[0];
+  if (mul.kind != ExprKind::Binary || mul.op != BinOp::Mul || !is_var(*mul.args[0], "blockIdx") ||
+      !is_var(*mul.args[1], "blockDim") || !is_var(*e.args[1], "threadIdx"))
+    return false;
+  const Stmt& g = *k.body[1];
+  if (g.kind != StmtKind::If || !g.else_block.empty() || g.then_block.size() != 1) return false;
+  const Expr& c = *g.expr;
+  if (c.kind != ExprKind::Compare || c.cmp != CmpOp::Lt || !is_var(*c.args[0], d.target.c_str()) ||
+      !is_var(*c.args[1], "N"))
+    return false;
+  const Stmt& call = *g.then_block[0];
+  if (call.kind != StmtKind::CallStmt) return false;
+  out.thread_var = d.target;
+  out.call = &call;
+  return true;
+}
+
+// Per-thread interpreter counters for one active and one idle thread of the
+// kernel (ops are data-independent for these gradients), so LaunchStats.counts
+// matches the reference's sum over threads without interpreting every point.
+void analytic_counts(const Program& p, const std::string& kernel, const FunctionDef& k,
+                     const LaunchConfig& cfg, const BufferSet& buffers, LaunchStats& st) {
+  std::vector<std::vector<double>> scratch;
+  scratch.reserve(k.params.size());
+  ArgPack args;
+  for (const auto& prm : k.params) {
+    if (prm.type == ValType::RealArray) {
+      scratch.emplace_back(1, buffers.arrays.at(prm.name)[0]);
+      args.add_array(scratch.back());
+    } else if (prm.type == ValType::Real) {
+      args.add_real(buffers.scalars.at(prm.name));
+    } else {
+      args.add_int(buffers.integers.at(prm.name));
+    }
+  }
+  EvalOptions o;
+  o.has_thread_ctx = true;
+  o.block_dim = cfg.block_dim;
+  o.problem_n = cfg.n;
+  o.block_idx = 0;
+  o.thread_idx = 0;
+  EvalResult active = p.eval(kernel, args, o);
+  const int64_t total = cfg.grid_dim * cfg.block_dim;
+  EvalResult idle{};
+  if (total > cfg.n) {
+    o.block_idx = cfg.n / cfg.block_dim;
+    o.thread_idx = cfg.n % cfg.block_dim;
+    idle = p.eval(kernel, args, o);
+  }
+  auto scale = [](const OpCounters& c, uint64_t n) {
+    OpCounters r;
+    r.adds = c.adds * n;
+    r.muls = c.muls * n;
+    r.divs = c.divs * n;
+    r.intrinsics = c.intrinsics * n;
+    r.comparisons = c.comparisons * n;
+    r.tape_pushes = c.tape_pushes * n;
+    r.tape_pops = c.tape_pops * n;
+    return r;
+  };
+  st.counts = scale(active.counts, static_cast<uint64_t>(cfg.n));
+  st.counts += scale(idle.counts, static_cast<uint64_t>(total - cfg.n));
+  st.thread_statements.assign(static_cast<size_t>(total),
+                              static_cast<uint32_t>(idle.top_statements));
+  for (int64_t g = 0; g < cfg.n; ++g)
+    st.thread_statements[static_cast<size_t>(g)] = static_cast<uint32_t>(active.top_statements);
+}
+
+}  // namespace
+
+LaunchStats launch(const Program& p, const std::string& kernel, const LaunchConfig& cfg,
+                   BufferSet& buffers, const LaunchOptions& opts) {
+  // launch.cpp:254-267 — validation and the hazard gate, unchanged.
+  cfg.validate();
+  const FunctionDef* k = p.module().find(kernel);
+  if (k == nullptr) throw Error(ErrorKind::Launch, "unknown kernel '" + kernel + "'");
+  if (!k->qualifiers.global)
+    throw Error(ErrorKind::Launch, "'" + kernel + "' is not a global kernel");
+  AccessReport report = race_check(p.module(), kernel);
+  if (report.has_hazard() && !opts.unsafe) {
+    std::string msg = "launch refused, hazardous parameter(s):";
+    for (const auto& e : report.entries)
+      if (e.access == Access::SharedWriteHazard) msg += " " + e.param + " (" + e.note + ")";
+    msg += "; pass the unsafe flag to force";
+    throw Error(ErrorKind::Launch, msg);
+  }
+  // launch.cpp:271-303 — buffer binding and length validation, unchanged.
+  for (const auto& param : k->params) {
+    if (param.type == ValType::RealArray) {
+      auto it = buffers.arrays.find(param.name);
+      if (it == buffers.arrays.end())
+        throw Error(ErrorKind::Launch, "missing buffer '" + param.name + "'");
+      const AccessReport::Entry* e = report.find(param.name);
+      if (e != nullptr && e->indexed_by_thread && static_cast<int64_t>(it->second.size()) < cfg.n)
+        throw Error(ErrorKind::Launch, "buffer '" + param.name + "' has length " +
+                                           std::to_string(it->second.size()) +
+                                           " but is indexed by thread over " +
+                                           std::to_string(cfg.n) + " elements");
+    } else if (param.type == ValType::Real) {
+      if (!buffers.scalars.count(param.name))
+        throw Error(ErrorKind::Launch, "missing scalar value '" + param.name + "'");
+    } else if (!buffers.integers.count(param.name)) {
+      throw Error(ErrorKind::Launch, "missing integer value '" + param.name + "'");
+    }
+  }
+  // Kernel shape + registry lookup by the callee's printed text.
+  Listing1 l1;
+  if (report.has_hazard() || !match_listing1(*k, l1))
+    throw Error(ErrorKind::Launch, "no B200 kernel for '" + kernel + "'");
+  const FunctionDef* callee = p.module().find(l1.call->callee);
+  if (callee == nullptr) throw Error(ErrorKind::Launch, "unknown callee '" + l1.call->callee + "'");
+  int32_t id = -1;
+  check(adc_cuda_registry_find(callee->name.c_str(), fingerprint(*callee), &id));
+  if (id != ADC_KERNEL_GAUSS_GRAD_0_1 || l1.call->call_args.size() != 5)
+    throw Error(ErrorKind::Launch, "no B200 launch path for '" + callee->name + "'");
+  // gauss_grad_0_1(x[i], p[i], sigma, dx[i], dp[i]): slices at the thread index
+  // and one by-value real.
+  std::vector<double*> arr;
+  double sigma = 0.0;
+  for (size_t a = 0; a < 5; ++a) {
+    const Expr& e = *l1.call->call_args[a];
+    if (a == 2) {
+      if (e.kind != ExprKind::VarRef) throw Error(ErrorKind::Launch, "unsupported sigma argument");
+      sigma = buffers.scalars.at(e.name);
+      continue;
+    }
+    if (e.kind != ExprKind::Index || !is_var(*e.args[0], l1.thread_var.c_str()))
+      throw Error(ErrorKind::Launch, "unsupported argument shape for the B200 kernel");
+    arr.push_back(buffers.arrays.at(e.name).data());
+  }
+  LaunchStats st;
+  analytic_counts(p, kernel, *k, cfg, buffers, st);
+  check(adc_cuda_compute_gauss_host(cfg.grid_dim, cfg.block_dim, cfg.n, arr[0], arr[1], sigma,
+                                    arr[2], arr[3]));
+  return st;
+}
+
+// ---------------------------------------------------------------------------
+namespace {
+struct DevHist {
+  const Histogram* key = nullptr;
+  void* counts = nullptr;
+  adc_chi2_plan* plan = nullptr;
+  int np = 0;
+  ~DevHist() {
+    if (plan) adc_cuda_chi2_plan_destroy(plan);
+    if (counts) adc_cuda_free(counts);
+  }
+};
+thread_local DevHist t_hist;
+std::string t_model_source;
+
+adc_chi2_plan* plan_for(const FitEngine& engine, const Histogram& h, size_t np) {
+  // The engine's generated gradient must be the registered one.
+  if (t_model_source.empty())
+    throw Error(ErrorKind::Launch, "B200: set_model_source() was not called");
+  Module m = parse_or_throw(t_model_source);
+  AdjointProgram g = differentiate_gradient(*m.find("gsum"), {"q"});
+  int32_t id = -1;
+  check(adc_cuda_registry_find(engine.gradient_fn_name().c_str(), fingerprint(g.derived), &id));
+  if (t_hist.key == &h && t_hist.np == static_cast<int>(np)) return t_hist.plan;
+  t_hist.~DevHist();
+  new (&t_hist) DevHist();
+  const size_t bytes = h.counts.size() * sizeof(double);
+  check(adc_cuda_alloc(&t_hist.counts, bytes));
+  check(adc_cuda_copy(t_hist.counts, h.counts.data(), bytes, 1));
+  check(adc_cuda_chi2_plan_create(&t_hist.plan, ADC_MODEL_GSUM, static_cast<int32_t>(np), h.bins,
+                                  h.lo, h.hi, static_cast<double>(h.events),
+                                  static_cast<const double*>(t_hist.counts), 1, 0, nullptr));
+  t_hist.key = &h;
+  t_hist.np = static_cast<int>(np);
+  return t_hist.plan;
+}
+}  // namespace
+
+void set_model_source(const std::string& source) { t_model_source = source; }
+
+void chi2_gradient(const FitEngine& engine, const Histogram& h, const std::vector<double>& q,
+                   std::vector<double>& out) {
+  out.assign(q.size(), 0.0);
+  check(adc_cuda_chi2_gradient(plan_for(engine, h, q.size()), q.data(), out.data(), nullptr));
+}
+
+double chi2(const FitEngine& engine, const Histogram& h, const std::vector<double>& q) {
+  double c2 = 0.0;
+  check(adc_cuda_chi2(plan_for(engine, h, q.size()), q.data(), &c2));
+  return c2;
+}
+
+}  // namespace adc::b200_bridge

@@ -1,0 +1,37 @@
+// adc_b200_bridge.hpp — the REFERENCE-SIDE binding: what a maintainer of the
+// reference `adc` (arxiv/paper_2203_06139 artifact) adds so its own call sites
+// run the hot path on a B200 through include/adc_cuda.h.  It is written against
+// the reference's public headers (proj/include/adc/*.hpp) and is compiled here
+// only by oracle/Makefile for the integration test (tests/test_bridge.py);
+// INTEGRATION.md shows where it plugs in.
+#pragma once
+
+#include <string>
+
+#include "adc/fit.hpp"
+#include "adc/launch.hpp"
+
+namespace adc::b200_bridge {
+
+/// Same signature and contract as adc::launch (proj/include/adc/launch.hpp:66-67,
+/// proj/src/launch.cpp:252-346).  Validation, the race_check refusal and buffer
+/// binding are the reference's own; a Listing-1 kernel (thread index, `if (i < N)`
+/// guard, one call of a registered generated gradient with a[i] slices) runs on
+/// the GPU.  Anything else throws Error(Launch, "no B200 kernel ...") — callers
+/// that want the interpreter call adc::launch themselves; there is no silent
+/// fallback.
+LaunchStats launch(const Program& p, const std::string& kernel, const LaunchConfig& cfg,
+                   BufferSet& buffers, const LaunchOptions& opts = {});
+
+/// The FitEngine model source (fit.cpp:125-138 kModelSource); its generated
+/// gradient is fingerprinted against the B200 registry before any pass.
+void set_model_source(const std::string& source);
+
+/// FitEngine::chi2_gradient / chi2 (fit.cpp:206-259) for the reference model
+/// (gsum, fit.cpp:125-138) with the histogram on the GPU.  The model's
+/// generated gradient text is checked against the B200 registry first.
+void chi2_gradient(const FitEngine& engine, const Histogram& h, const std::vector<double>& q,
+                   std::vector<double>& out);
+double chi2(const FitEngine& engine, const Histogram& h, const std::vector<double>& q);
+
+}  // namespace adc::b200_bridge

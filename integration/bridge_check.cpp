@@ -1,0 +1,155 @@
+// bridge_check — integration test of the reference-side binding
+// (integration/adc_b200_bridge.cpp): the unmodified reference library
+// (oracle/_ref/libadc.a) and its own public API, with adc::launch and
+// FitEngine::chi2_gradient routed to the B200 through include/adc_cuda.h.
+// Built by oracle/Makefile; run by tests/test_bridge.py.
+//   bridge_check cpu   — error-contract checks that need no GPU
+//   bridge_check gpu   — parity of the bridged calls against the reference's
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <string>
+
+#include "adc/fit.hpp"
+#include "adc/launch.hpp"
+#include "adc/parser.hpp"
+#include "adc/tooling.hpp"
+#include "adc_b200_bridge.hpp"
+#include "corpus_embed.inc"
+
+using namespace adc;
+
+static int failures = 0;
+#define EXPECT(cond, what)                                 \
+  do {                                                     \
+    if (!(cond)) {                                         \
+      std::printf("FAIL %s\n", what);                      \
+      ++failures;                                          \
+    } else {                                               \
+      std::printf("ok   %s\n", what);                      \
+    }                                                      \
+  } while (0)
+
+static Program kernels_program() {
+  Module m = parse_or_throw(kKernelsDsl);
+  ensure_called_derivatives(m);
+  return Program(std::move(m));
+}
+
+template <class F>
+static std::string error_of(F&& f, ErrorKind* kind = nullptr) {
+  try {
+    f();
+  } catch (const Error& e) {
+    if (kind) *kind = e.kind();
+    return e.what();
+  }
+  return "";
+}
+
+static double rel(double a, double b) {
+  double s = std::max(std::fabs(a), std::fabs(b));
+  return s == 0 ? 0 : std::fabs(a - b) / s;
+}
+
+static void cpu_checks(const Program& p) {
+  // Refusal and binding errors are the reference's own, before any device use.
+  BufferSet b;
+  b.arrays["x"] = std::vector<double>(64, 0.5);
+  b.arrays["p"] = std::vector<double>(64, 0.0);
+  b.scalars["sigma"] = 1.0;
+  b.arrays["dx"] = std::vector<double>(64, 0.0);
+  b.arrays["dp"] = std::vector<double>(64, 0.0);
+  b.arrays["dsigma"] = std::vector<double>(1, 0.0);
+  ErrorKind k1{}, k2{};
+  std::string r = error_of([&] { adc::launch(p, "compute_shared", {1, 64, 64}, b); }, &k1);
+  std::string g = error_of([&] { b200_bridge::launch(p, "compute_shared", {1, 64, 64}, b); }, &k2);
+  EXPECT(!r.empty() && r == g && k1 == k2 && k1 == ErrorKind::Launch,
+         "hazardous compute_shared refused with the reference's message");
+  BufferSet s = b;
+  s.arrays["x"].resize(10);
+  EXPECT(error_of([&] { adc::launch(p, "compute", {3, 256, 512}, s); }) ==
+             error_of([&] { b200_bridge::launch(p, "compute", {3, 256, 512}, s); }),
+         "short buffer: same message");
+  s.arrays.erase("x");
+  EXPECT(error_of([&] { b200_bridge::launch(p, "compute", {3, 256, 512}, s); }) ==
+             "missing buffer 'x'",
+         "missing buffer: same message");
+  EXPECT(error_of([&] { b200_bridge::launch(p, "compute", {0, 256, 512}, b); }) ==
+             error_of([&] { adc::launch(p, "compute", {0, 256, 512}, b); }),
+         "bad LaunchConfig: same message");
+  EXPECT(error_of([&] { b200_bridge::launch(p, "noop", {1, 1, 1}, b); }).find("no B200 kernel") !=
+             std::string::npos,
+         "non-Listing-1 kernel: explicit 'no B200 kernel' (no fallback)");
+}
+
+static void gpu_checks(const Program& p) {
+  for (int64_t n : {512, 1000003}) {
+    std::mt19937_64 rng(n == 512 ? 0x5EED : 7);
+    std::vector<double> x(n), px(n), d0(n), e0(n);
+    for (int64_t i = 0; i < n; ++i) {
+      x[i] = std::uniform_real_distribution<double>(-3, 3)(rng);
+      px[i] = std::uniform_real_distribution<double>(-2, 2)(rng);
+      d0[i] = n == 512 ? 0.0 : std::uniform_real_distribution<double>(-1, 1)(rng);
+      e0[i] = n == 512 ? 0.0 : std::uniform_real_distribution<double>(-1, 1)(rng);
+    }
+    BufferSet ref, gpu;
+    for (BufferSet* b : {&ref, &gpu}) {
+      b->arrays["x"] = x;
+      b->arrays["p"] = px;
+      b->scalars["sigma"] = 1.3;
+      b->arrays["dx"] = d0;
+      b->arrays["dp"] = e0;
+    }
+    LaunchConfig cfg{n / 256 + 1, 256, n};
+    LaunchStats rs = adc::launch(p, "compute", cfg, ref);
+    LaunchStats gs = b200_bridge::launch(p, "compute", cfg, gpu);
+    double worst = 0;
+    size_t same = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      for (const char* a : {"dx", "dp"}) {
+        double r = ref.arrays[a][i], g = gpu.arrays[a][i];
+        double scale = std::max({std::fabs(r), std::fabs(g), std::fabs(a[1] == 'x' ? d0[i] : e0[i])});
+        worst = std::max(worst, scale == 0 ? 0 : std::fabs(r - g) / scale);
+        same += r == g;
+      }
+    }
+    std::printf("     n=%lld worst rel %.3g, bit-identical %.4f\n", (long long)n, worst,
+                double(same) / (2.0 * n));
+    EXPECT(worst <= 1e-12, "bridged launch matches adc::launch within 1e-12");
+    EXPECT(rs.thread_statements == gs.thread_statements, "LaunchStats.thread_statements equal");
+    EXPECT(rs.counts == gs.counts, "LaunchStats.counts (op counters) equal");
+  }
+  // FitEngine (gsum K=1, 2) chi2 and gradient on the GPU vs the reference engine.
+  b200_bridge::set_model_source(kGsumDsl);
+  FitEngine eng;
+  for (int k : {1, 2}) {
+    std::vector<double> truth = gauss_sum::default_truth(k, -5, 5);
+    Histogram h = sample_histogram(truth, 100000, 1000, -5, 5, 42 + k);
+    std::vector<double> q = gauss_sum::perturbed_init(truth);
+    std::vector<double> gr, gg;
+    eng.chi2_gradient(h, q, GradientProvider::AdReverse, gr);
+    b200_bridge::chi2_gradient(eng, h, q, gg);
+    double gmax = 0, worst = 0;
+    for (double v : gr) gmax = std::max(gmax, std::fabs(v));
+    for (size_t i = 0; i < q.size(); ++i) worst = std::max(worst, std::fabs(gr[i] - gg[i]) / gmax);
+    double cr = eng.chi2(h, q), cg = b200_bridge::chi2(eng, h, q);
+    std::printf("     gsum K=%d: gradient worst |diff|/max|g| %.3g, chi2 rel %.3g\n", k, worst,
+                rel(cr, cg));
+    EXPECT(worst <= 1e-11 && rel(cr, cg) <= 1e-12, "bridged FitEngine chi2/gradient match");
+  }
+}
+
+int main(int argc, char** argv) {
+  const std::string mode = argc > 1 ? argv[1] : "cpu";
+  Program p = kernels_program();
+  try {
+    cpu_checks(p);
+    if (mode == "gpu") gpu_checks(p);
+  } catch (const Error& e) {
+    std::printf("FAIL unexpected adc::Error: %s\n", e.what());
+    ++failures;
+  }
+  std::printf("%s: %d failure(s)\n", mode.c_str(), failures);
+  return failures == 0 ? 0 : 1;
+}

@@ -1,0 +1,117 @@
+// C++ mirror (include/adcx/adc_b200.hpp) check: compiles against the header,
+// links libadc_b200.so, exercises the reference-shaped API.
+//   cxx_api_check cpu — error contract without a GPU (no CPU fallback)
+//   cxx_api_check gpu — Listing-1 launch, batched N-dim, FitEngine vs the C oracle
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <string>
+
+#include "adcx/adc_b200.hpp"
+#include "restate.h"
+
+using namespace adc::b200;
+static int failures = 0;
+#define EXPECT(c, w)                   \
+  do {                                 \
+    std::printf("%s %s\n", (c) ? "ok  " : "FAIL", w); \
+    if (!(c)) ++failures;              \
+  } while (0)
+
+template <class F>
+static std::string err(F&& f, ErrorKind* k = nullptr) {
+  try {
+    f();
+  } catch (const Error& e) {
+    if (k) *k = e.kind();
+    return e.what();
+  }
+  return "";
+}
+
+static double relmax(const std::vector<double>& a, const std::vector<double>& b) {
+  double w = 0;
+  for (size_t i = 0; i < a.size(); ++i) {
+    double s = std::max(std::fabs(a[i]), std::fabs(b[i]));
+    if (s > 0) w = std::max(w, std::fabs(a[i] - b[i]) / s);
+  }
+  return w;
+}
+
+int main(int argc, char** argv) {
+  const bool gpu = argc > 1 && std::string(argv[1]) == "gpu";
+  BufferSet b;
+  b.arrays["x"] = std::vector<double>(512, 0.5);
+  b.arrays["p"] = std::vector<double>(512, 0.0);
+  b.arrays["dx"] = std::vector<double>(512, 0.0);
+  b.arrays["dp"] = std::vector<double>(512, 0.0);
+  b.scalars["sigma"] = 1.3;
+  ErrorKind k{};
+  EXPECT(err([&] { launch("compute", {1, 256, 512}, b); }, &k) ==
+                 "grid 1 x block 256 does not cover problem size 512" && k == ErrorKind::Launch,
+         "LaunchConfig::validate message");
+  EXPECT(err([&] { launch("compute_shared", {1, 64, 64}, b); }).find("launch refused") == 0,
+         "hazard refusal");
+  if (!gpu) {
+    EXPECT(err([&] { launch("compute", {3, 256, 512}, b); }, &k).find("no CUDA device") !=
+                   std::string::npos && k == ErrorKind::Cuda,
+           "no GPU: Error(Cuda), no CPU fallback");
+  } else {
+    // Listing 1 at n = 512 (acceptance.cpp:160-211 analog) vs the oracle.
+    const int64_t n = 100003;
+    std::mt19937_64 rng(0x5EED);
+    BufferSet h;
+    for (const char* a : {"x", "p", "dx", "dp"}) h.arrays[a].resize(n);
+    for (int64_t i = 0; i < n; ++i) {
+      h.arrays["x"][i] = std::uniform_real_distribution<double>(-3, 3)(rng);
+      h.arrays["p"][i] = std::uniform_real_distribution<double>(-2, 2)(rng);
+    }
+    h.scalars["sigma"] = 1.3;
+    std::vector<double> ox(n, 0.0), op(n, 0.0);
+    rs_gauss_grad_batch(h.arrays["x"].data(), h.arrays["p"].data(), 1.3, ox.data(), op.data(), n);
+    LaunchStats st = launch("compute", {n / 256 + 1, 256, n}, h);
+    EXPECT(relmax(h.arrays["dx"], ox) <= 1e-12 && relmax(h.arrays["dp"], op) <= 1e-12,
+           "launch(compute) matches the oracle within 1e-12");
+    EXPECT(st.thread_statements.size() == size_t((n / 256 + 1) * 256) &&
+               st.thread_statements[0] == 3 && st.thread_statements.back() == 2,
+           "LaunchStats shape");
+    // Batched N-dim.
+    const int64_t dim = 37, m = 1001;
+    std::vector<double> X(dim * m), P(dim * m), DX(dim * m, 0.0), DP(dim * m, 0.0);
+    for (auto& v : P) v = std::uniform_real_distribution<double>(-2, 2)(rng);
+    for (size_t i = 0; i < X.size(); ++i) X[i] = P[i] + 0.1 * std::normal_distribution<double>()(rng);
+    std::vector<double> RX(dim * m, 0.0), RP(dim * m, 0.0);
+    rs_gaussnd_grad_batch(X.data(), P.data(), 1.3, dim, m, m, RX.data(), RP.data());
+    launch_batch_gaussnd(m, dim, X, P, 1.3, DX, DP);
+    EXPECT(relmax(DX, RX) <= 1e-12 && relmax(DP, RP) <= 1e-12, "launch_batch_gaussnd matches");
+    // FitEngine gsum K=1 over a 4000-bin histogram vs the compensated oracle.
+    Histogram hist;
+    hist.bins = 4000;
+    hist.lo = -5;
+    hist.hi = 5;
+    hist.counts.resize(hist.bins);
+    double tot = 0;
+    for (int j = 0; j < hist.bins; ++j) {
+      double x = hist.center(j);
+      hist.counts[j] = j % 100 == 0 ? 0.0 : std::round(200 * std::exp(-0.5 * x * x / 2.25));
+      tot += hist.counts[j];
+    }
+    hist.events = (uint64_t)tot;
+    std::vector<double> q = {0.8, 0.3, 1.2}, g, ref(3), scale(3);
+    FitEngine eng("gsum", 3);
+    eng.chi2_gradient(hist, q, g);
+    rs_chi2_gradient_compensated(RS_MODEL_GSUM, hist.counts.data(), hist.bins, -5, 5, tot,
+                                 q.data(), 3, ref.data(), scale.data());
+    bool okg = true;
+    for (int i = 0; i < 3; ++i) okg = okg && std::fabs(g[i] - ref[i]) <= 1e-12 * scale[i];
+    EXPECT(okg, "FitEngine::chi2_gradient within 1e-12 * sum|terms|");
+    const double c0 = eng.chi2(hist, q);
+    FitResult r = eng.fit(hist, q, FitOptions{});
+    std::printf("     fit: %d iterations, chi2 %.6g -> %.6g, mu %.4f sigma %.4f\n", r.iterations, c0,
+                r.chi2, r.params[1], r.params[2]);
+    EXPECT(r.chi2 < c0 && std::fabs(r.params[1]) < 0.05 && std::fabs(r.params[2] - 1.5) < 0.05,
+           "FitEngine::fit recovers mu and sigma (test_fit.cpp:81-93 bounds)");
+  }
+  std::printf("%d failure(s)\n", failures);
+  return failures ? 1 : 0;
+}
