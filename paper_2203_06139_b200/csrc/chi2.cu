@@ -307,18 +307,14 @@ __global__ void __launch_bounds__(kChunkThreads) chi2_chunk_kernel(
 }
 
 // ---- dispatch ----------------------------------------------------------------
-int g_chi2_tune = 0;  // experiment knob (ADC_CHI2_TUNE): 0 default, 1 = 3 CTAs/SM, 2 = paired bins
+int g_chi2_tune = 0;  // experiment knob (ADC_CHI2_TUNE): 0 default, != 0 = paired bins
 
 template <class M, bool GRAD, bool FAST>
 static void launch_tiles_t(const Chi2Pass& P, int bpt, int blocks, cudaStream_t s) {
   constexpr int MB = tile_min_blocks<M, GRAD>();
   if constexpr (std::is_same<M, GPoly>::value && FAST) {
-    if (bpt == 128 && g_chi2_tune != 0) {  // experiments: 1 = 3 CTAs/SM, 2 = paired bins
-      const int b3 = std::min(blocks * 3 / 2, sm_count() * 3);
-      if (g_chi2_tune == 1)
-        chi2_tile_kernel<M, GRAD, FAST, 128, 3, false><<<b3, kTileThreads, 0, s>>>(P);
-      else
-        chi2_tile_kernel<M, GRAD, FAST, 128, MB, true><<<blocks, kTileThreads, 0, s>>>(P);
+    if (bpt == 128 && g_chi2_tune != 0) {  // experiments: 2 = paired bins
+      chi2_tile_kernel<M, GRAD, FAST, 128, MB, true><<<blocks, kTileThreads, 0, s>>>(P);
       return;
     }
   }

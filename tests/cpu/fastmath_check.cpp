@@ -17,5 +17,5 @@ int main() {
     if (ulp > maxulp) { maxulp = ulp; worst = x; }
   }
   printf("max ulp %.3f at %.17g\n", maxulp, worst);
-  return maxulp < 3 ? 0 : 1;
+  return maxulp < 1.5 ? 0 : 1;
 }

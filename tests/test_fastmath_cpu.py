@@ -1,5 +1,5 @@
 """The chi2 fast-mode exp (csrc/fastmath.cuh is __host__ __device__) compiled
-for the host and checked against glibc exp: <= 2 ulp over [-745, 0],
+for the host and checked against glibc exp: <= 1 ulp (measured; bound checked at 1.5) over [-745, 0],
 correct subnormals.  CPU only."""
 import os
 import subprocess
