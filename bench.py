@@ -378,6 +378,61 @@ def bench_chi2(world, rank, local, dist, bins=100_000_000, passes=20, warm=3):
     return out
 
 
+def bench_fit_1e6(local, bins=1_000_000):
+    """BASELINE configs[2]: chi2 fit of the Gaussian + quadratic background over
+    1e6 bins with the gradient-descent (Armijo) fit loop of fit.cpp:315-425,
+    driven by adc_cuda_fit over CUDA-graph passes."""
+    import paper_2203_06139_b200 as adc
+    from paper_2203_06139_b200 import synth
+    counts, ev = synth.histogram(bins, events=1e8, seed=11)
+    h = adc.Histogram(bins, -5.0, 5.0, ev, counts)
+    eng = adc.FitEngine("gpoly", 6)
+    eng.chi2(h, synth.GPOLY_INIT)  # upload + graph capture outside the timing
+    eng.chi2_gradient(h, synth.GPOLY_INIT)
+    t0 = time.perf_counter()
+    r = eng.fit(h, synth.GPOLY_INIT, adc.FitOptions(budget=400))
+    dt = time.perf_counter() - t0
+    return {"workload": "chi2 fit, gpoly, 1e6 bins, GD + Armijo (BASELINE configs[2])",
+            "fit_seconds": dt, "iterations": r.iterations, "fit_iterations_per_s": r.iterations / dt,
+            "gradient_evals": r.gradient_evals, "chi2_evals": r.chi2_evals,
+            "passes_per_s": (r.gradient_evals + r.chi2_evals) / dt,
+            "gradient_ms_avg": r.gradient_wall_ns / max(1, r.gradient_evals) / 1e6,
+            "converged": r.converged, "params": [round(v, 6) for v in r.params]}
+
+
+def bench_points_small(local, workload, steps=20, warm=3):
+    """Device-resident timing of a secondary per-point config (no e2e)."""
+    import torch
+    import paper_2203_06139_b200 as adc
+    dim, npts, desc = WORKLOADS[workload]
+    dev = torch.device("cuda", local)
+    g = torch.Generator(device=dev)
+    g.manual_seed(99)
+    if workload == "gauss1d":
+        x = torch.rand(npts, dtype=torch.float64, device=dev, generator=g) * 6 - 3
+        p = torch.rand(npts, dtype=torch.float64, device=dev, generator=g) * 4 - 2
+        cfg = adc.LaunchConfig(npts // 256 + 1, 256, npts)
+        dx, dp = torch.zeros_like(x), torch.zeros_like(x)
+        bufs = adc.BufferSet(arrays={"x": x, "p": p, "dx": dx, "dp": dp}, scalars={"sigma": 1.3})
+        step = lambda: adc.launch("compute", cfg, bufs)  # noqa: E731
+    else:
+        p = torch.rand((dim, npts), dtype=torch.float64, device=dev, generator=g) * 4 - 2
+        x = p + 0.03 * torch.randn((dim, npts), dtype=torch.float64, device=dev, generator=g)
+        dx, dp = torch.zeros_like(x), torch.zeros_like(x)
+        step = lambda: adc.launch_batch("gaussnd_grad_0_1", x, p, 1.3, dx, dp)  # noqa: E731
+    for _ in range(warm):
+        step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    evs = [event_time(step, stream) for _ in range(steps)]
+    torch.cuda.synchronize()
+    ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in evs)
+    units = npts * 2 * dim
+    return {"workload": desc, "value": units / (ms * 1e-3), "unit": "pt*param/s",
+            "kernel_ms_median": ms, "hbm_gbs": 48 * npts * dim / (ms * 1e-3) / 1e9,
+            "note": "device-resident, CUDA events per launch"}
+
+
 def ours_arm(a, world, rank, local):
     import torch
     torch.cuda.set_device(local)
@@ -386,10 +441,16 @@ def ours_arm(a, world, rank, local):
     value, ms_step, roof, e2e, clocks, desc, dim, npts = bench_points(a, world, rank, local, dist)
     secondary = []
     if not a.no_secondary:
-        try:
-            secondary.append(bench_chi2(world, rank, local, dist))
-        except Exception as ex:  # secondary lines never hide the headline
-            secondary.append({"workload": "chi2", "error": repr(ex)[:200]})
+        jobs = [lambda: bench_chi2(world, rank, local, dist)]
+        if world == 1:
+            jobs += [lambda: bench_fit_1e6(local),
+                     lambda: bench_points_small(local, "gauss1d"),
+                     lambda: bench_points_small(local, "gaussnd1000")]
+        for job in jobs:
+            try:
+                secondary.append(job())
+            except Exception as ex:  # secondary lines never hide the headline
+                secondary.append({"error": repr(ex)[:200]})
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         cores = os.cpu_count()

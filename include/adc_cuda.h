@@ -159,14 +159,21 @@ double* adc_cuda_chi2_plan_records(adc_chi2_plan* plan);
  * FitEngine::chi2_gradient(h, q, AdReverse, out) and FitEngine::chi2(h, q). */
 int adc_cuda_chi2_gradient(adc_chi2_plan* plan, const double* q, double* grad, double* chi2);
 int adc_cuda_chi2(adc_chi2_plan* plan, const double* q, double* chi2);
+/* chi2 of ncand (<= 32) parameter vectors qs[ncand][np] in ONE pass over the
+ * bins (fast mode): each result is bit-identical to adc_cuda_chi2 on that
+ * vector.  The fit loop uses it to evaluate the Armijo trials t = 1, 1/2, ...
+ * of fit.cpp:390-403 in batches.  Single device. */
+int adc_cuda_chi2_multi(adc_chi2_plan* plan, const double* qs, int32_t ncand, double* chi2s);
 /* Selects per-bin arithmetic: 0 = faithful (IEEE divisions exactly as the
  * generated code), 1 = fast (reciprocal multiplies; within the reduction
  * tolerance).  Default 1. */
 int adc_cuda_chi2_set_precision(adc_chi2_plan* plan, int32_t mode);
 
 /* ---------------------------------------------------------------------------
- * Fit loop (FitEngine::fit, proj/src/fit.cpp:315-425: steepest descent with
- * Armijo backtracking, sigma clamp) driven on the host over the device passes.
+ * Fit loop (FitEngine::fit, proj/src/fit.cpp:315-425: steepest descent or the
+ * optional damped Newton step from a central-difference Hessian of the
+ * gradient, Armijo backtracking, sigma clamp) driven on the host over the
+ * device passes.
  * clamp_idx lists the parameters the sigma clamp applies to (fit.cpp:268-278
  * hard-codes every third index; gsum passes 2,5,8,..., gpoly passes 2). */
 typedef struct adc_fit_options {
@@ -176,6 +183,7 @@ typedef struct adc_fit_options {
   double sigma_min;      /* 1e-3 */
   double armijo_c1;      /* 1e-4 */
   int32_t trace_iterates;
+  int32_t use_hessian;   /* 0; Newton step from a numeric Hessian of the gradient (fit.cpp:346-381) */
 } adc_fit_options;
 
 typedef struct adc_fit_result {

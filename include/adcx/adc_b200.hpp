@@ -144,6 +144,7 @@ struct FitOptions {
   double chi2_rel_tol = 1e-12;
   double sigma_min = 1e-3;
   double armijo_c1 = 1e-4;
+  bool use_hessian = false;
   int trace_iterates = 0;
 };
 
@@ -187,7 +188,7 @@ class FitEngine {
     else
       clamp.push_back(2);
     adc_fit_options co{o.budget, o.grad_tol, o.chi2_rel_tol, o.sigma_min, o.armijo_c1,
-                       o.trace_iterates};
+                       o.trace_iterates, o.use_hessian ? 1 : 0};
     adc_fit_result cr{};
     std::vector<double> its(static_cast<size_t>(std::max(1, o.trace_iterates) * np_));
     check(adc_cuda_fit(plan(h), init.data(), clamp.data(), static_cast<int32_t>(clamp.size()),

@@ -362,7 +362,37 @@ struct ModelEngine {
       }
     return n;
   }
-  // Steepest descent + Armijo backtracking, fit.cpp:315-425 (use_hessian off).
+  // (H + lambda I) d = g, Gaussian elimination with partial pivoting
+  // (the algorithm of fit.cpp:282-311).
+  static bool damped(std::vector<double> hm, std::vector<double> g, double lambda, int n,
+                     std::vector<double>& out) {
+    for (int i = 0; i < n; ++i) hm[i * n + i] += lambda;
+    for (int col = 0; col < n; ++col) {
+      int piv = col;
+      for (int r = col + 1; r < n; ++r)
+        if (std::fabs(hm[r * n + col]) > std::fabs(hm[piv * n + col])) piv = r;
+      if (std::fabs(hm[piv * n + col]) < 1e-30) return false;
+      if (piv != col) {
+        for (int c = 0; c < n; ++c) std::swap(hm[piv * n + c], hm[col * n + c]);
+        std::swap(g[piv], g[col]);
+      }
+      for (int r = col + 1; r < n; ++r) {
+        double f = hm[r * n + col] / hm[col * n + col];
+        for (int c = col; c < n; ++c) hm[r * n + c] -= f * hm[col * n + c];
+        g[r] -= f * g[col];
+      }
+    }
+    out.assign(n, 0.0);
+    for (int r = n - 1; r >= 0; --r) {
+      double v = g[r];
+      for (int c = r + 1; c < n; ++c) v -= hm[r * n + c] * out[c];
+      out[r] = v / hm[r * n + r];
+    }
+    return true;
+  }
+
+  // Steepest descent or the numeric-Hessian Newton step + Armijo
+  // backtracking, fit.cpp:315-425.
   FitResult fit(const Histogram& h, std::vector<double> q, const FitOptions& o) const {
     FitResult res;
     res.sigma_clamps += clamp(q, o.sigma_min);
@@ -379,14 +409,42 @@ struct ModelEngine {
         res.converged = true;
         break;
       }
+      std::vector<double> direction = g;
+      if (o.use_hessian) {
+        const int n = static_cast<int>(np);
+        std::vector<double> hess(np * np, 0.0), gp(np), gm(np), probe = q;
+        for (int c = 0; c < n; ++c) {
+          double x = probe[c];
+          double step = std::cbrt(2.220446049250313e-16) * std::max(1.0, std::fabs(x));
+          probe[c] = x + step;
+          chi2_gradient(h, probe, gp);
+          probe[c] = x - step;
+          chi2_gradient(h, probe, gm);
+          res.gradient_evals += 2;
+          probe[c] = x;
+          for (int r = 0; r < n; ++r) hess[r * n + c] = (gp[r] - gm[r]) / (2.0 * step);
+        }
+        double lambda = 0.0;
+        bool ok = false;
+        for (int attempt = 0; attempt < 10 && !ok; ++attempt) {
+          ok = damped(hess, g, lambda, n, direction);
+          if (ok) {
+            double descent = 0.0;
+            for (size_t i = 0; i < np; ++i) descent += g[i] * direction[i];
+            ok = descent > 0.0;
+          }
+          lambda = lambda == 0.0 ? 1e-6 : lambda * 10.0;
+        }
+        if (!ok) direction = g;
+      }
       double gd = 0.0;
-      for (size_t i = 0; i < np; ++i) gd += g[i] * g[i];
+      for (size_t i = 0; i < np; ++i) gd += g[i] * direction[i];
       double t = 1.0, next = 0.0;
       bool accepted = false;
       std::vector<double> cand;
       while (t >= 1e-18) {
         std::vector<double> trial = q;
-        for (size_t i = 0; i < np; ++i) trial[i] -= t * g[i];
+        for (size_t i = 0; i < np; ++i) trial[i] -= t * direction[i];
         int cl = clamp(trial, o.sigma_min);
         double c2 = chi2(h, trial);
         if (c2 <= cur - o.armijo_c1 * t * gd) {
@@ -486,7 +544,7 @@ int cmd_chi2_in(int argc, char** argv) {
   return engine_match ? 0 : 1;
 }
 
-// fit-in <model> <bins> <lo> <hi> <counts.bin> <out.bin> <trace> <budget> q...
+// fit-in <model> <bins> <lo> <hi> <counts.bin> <out.bin> <trace> <budget[:hess]> q...
 //   out = [chi2, iterations, gradient_evals, converged, sigma_clamps,
 //          params[np], iterates[trace x np] (zero padded)].
 int cmd_fit_in(int argc, char** argv) {
@@ -496,6 +554,7 @@ int cmd_fit_in(int argc, char** argv) {
   FitOptions o;
   o.trace_iterates = std::atoi(argv[7]);
   o.budget = std::atoi(argv[8]);
+  o.use_hessian = std::strstr(argv[8], ":hess") != nullptr;
   std::vector<double> q;
   for (int i = 9; i < argc; ++i) q.push_back(std::atof(argv[i]));
   ModelEngine eng = make_engine(model);

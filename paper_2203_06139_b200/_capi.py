@@ -33,7 +33,8 @@ class Chi2Layout(ctypes.Structure):
 class FitOptions(ctypes.Structure):
     _fields_ = [("budget", ctypes.c_int32), ("grad_tol", ctypes.c_double),
                 ("chi2_rel_tol", ctypes.c_double), ("sigma_min", ctypes.c_double),
-                ("armijo_c1", ctypes.c_double), ("trace_iterates", ctypes.c_int32)]
+                ("armijo_c1", ctypes.c_double), ("trace_iterates", ctypes.c_int32),
+                ("use_hessian", ctypes.c_int32)]
 
 
 class FitResultC(ctypes.Structure):
@@ -78,6 +79,7 @@ SIGNATURES = {
     "adc_cuda_chi2_plan_records": (_VP, [_VP]),
     "adc_cuda_chi2_gradient": (ctypes.c_int, [_VP, _D, _D, _D]),
     "adc_cuda_chi2": (ctypes.c_int, [_VP, _D, _D]),
+    "adc_cuda_chi2_multi": (ctypes.c_int, [_VP, _D, _I32, _D]),
     "adc_cuda_chi2_set_precision": (ctypes.c_int, [_VP, _I32]),
     "adc_fit_default_options": (None, [ctypes.POINTER(FitOptions)]),
     "adc_cuda_fit": (ctypes.c_int, [_VP, _D, ctypes.POINTER(_I32), _I32,

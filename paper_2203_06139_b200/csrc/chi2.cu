@@ -283,6 +283,87 @@ __global__ void __launch_bounds__(kTileThreads, MINB) chi2_tile_kernel(Chi2Pass 
   }
 }
 
+// ---- K3m: multi-candidate chi2 value pass (batched Armijo line search) ---------
+// One sweep over the bins evaluates chi2 for up to kMultiMax parameter vectors
+// (the line-search trials q - t g, t = 1, 1/2, ...).  blockIdx.y selects a
+// group of kMultiGroup candidates.  Per candidate the per-thread order, the
+// shuffle tree and the cross-warp tree are those of the single value pass, so
+// every candidate's record is bit-identical to a separate chi2 pass.
+// Record layout per tile / chunk: [C0, (S, A1, A2) x ncand].
+constexpr int kMultiGroup = 8;
+
+template <class M, int BPT>
+__global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P, int ncand) {
+  constexpr int G = kMultiGroup;
+  __shared__ QDev Q[G];
+  __shared__ double red[kTileThreads / 32][3 * G + 1];
+  __shared__ double tab[64];
+  const int g0 = blockIdx.y * G;
+  const int ng = min(G, ncand - g0);
+  for (int t = threadIdx.x; t < G * kMaxNp; t += kTileThreads) {
+    const int c = t / kMaxNp, i = t % kMaxNp;
+    const double* src = P.qdev + (size_t)(g0 + (c < ng ? c : 0)) * 2 * kMaxNp;
+    Q[c].q[i] = src[i];
+    Q[c].inv[i] = src[kMaxNp + i];
+  }
+  if (threadIdx.x < 64) tab[threadIdx.x] = exp2((double)threadIdx.x / 64.0);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int R = 1 + 3 * ncand;
+  constexpr int64_t TB = (int64_t)BPT * kTileThreads;
+  for (int64_t tile = P.tile_begin + blockIdx.x; tile < P.tile_end; tile += gridDim.x) {
+    const int64_t base = tile * TB + threadIdx.x;
+    double acc[3 * G + 1];
+#pragma unroll
+    for (int v = 0; v < 3 * G + 1; ++v) acc[v] = 0.0;
+    double jh = fadd((double)base, 0.5);
+    for (int k = 0; k < BPT; ++k) {
+      const int64_t j = base + (int64_t)k * kTileThreads;
+      if (j < P.bin_end) {
+        const double c = ld_stream(P.counts + j);
+        const double x = fadd(P.lo, fmul(jh, P.width));
+        const bool pos = c > 0.0;
+        const double w = pos ? 1.0 : 0.0;
+        const double ic = pos ? rcp_pos(c) : 0.0;
+        acc[3 * G] += c;
+#pragma unroll
+        for (int cnd = 0; cnd < G; ++cnd) {
+          if (cnd < ng) {
+            const typename M::Reg QR = M::load(Q[cnd]);
+            double m, bg[1];
+            M::template eval<false, true>(x, QR, tab, m, bg);
+            const double mc = m * ic;
+            acc[3 * cnd] += m;
+            acc[3 * cnd + 1] = __fma_rn(w, m, acc[3 * cnd + 1]);
+            acc[3 * cnd + 2] = __fma_rn(m, mc, acc[3 * cnd + 2]);
+          }
+        }
+      }
+      jh = fadd(jh, (double)kTileThreads);
+    }
+#pragma unroll
+    for (int v = 0; v < 3 * G + 1; ++v) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc[v] += __shfl_down_sync(0xffffffffu, acc[v], off);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int v = 0; v < 3 * G + 1; ++v) red[warp][v] = acc[v];
+    }
+    __syncthreads();
+    for (int v = threadIdx.x; v < 3 * ng + 1; v += kTileThreads) {
+      const int src = v < 3 * ng ? v : 3 * G;  // C0 is the last local entry
+      const double s01 = red[0][src] + red[1][src], s23 = red[2][src] + red[3][src];
+      const double s45 = red[4][src] + red[5][src], s67 = red[6][src] + red[7][src];
+      const double val = (s01 + s23) + (s45 + s67);
+      double* out = P.tile_ws + (tile - P.tile_begin) * R;
+      if (v < 3 * ng) out[1 + 3 * g0 + v] = val;
+      else if (blockIdx.y == 0) out[0] = val;
+    }
+    __syncthreads();
+  }
+}
+
 // ---- K4: chunk reduce (fixed tree over the chunk's tiles) ---------------------
 // One CTA per chunk; warp w owns record entries v = w, w+8, ...; lane l sums
 // tiles l, l+32, l+64, l+96 pairwise, then a fixed shuffle tree.
@@ -360,6 +441,40 @@ int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast, int
     }
   }
   ADCB_CUDA(cudaGetLastError());
+  const int64_t nchunks = (ntiles + chunk_tiles - 1) / chunk_tiles;
+  chi2_chunk_kernel<<<(unsigned)nchunks, kChunkThreads, 0, s>>>(P.tile_ws, ntiles, R,
+                                                               (int)chunk_tiles, records);
+  ADCB_CUDA(cudaGetLastError());
+  return ADC_OK;
+}
+
+int chi2_multi_enqueue(const Chi2Pass& P, int model, int np, int ncand, int bpt,
+                       int64_t chunk_tiles, double* records, cudaStream_t s) {
+  const int64_t ntiles = P.tile_end - P.tile_begin;
+  if (ntiles <= 0) return ADC_OK;
+  if (ncand < 1 || ncand > kMultiMax) return fail(ADC_E_ARG, "chi2 multi: bad candidate count");
+  const dim3 grid((unsigned)std::min<int64_t>(ntiles, (int64_t)sm_count() * 2),
+                  (unsigned)((ncand + kMultiGroup - 1) / kMultiGroup));
+  auto go = [&](auto model_tag) {
+    using M = decltype(model_tag);
+    if (bpt == 128) chi2_multi_kernel<M, 128><<<grid, kTileThreads, 0, s>>>(P, ncand);
+    else if (bpt == 32) chi2_multi_kernel<M, 32><<<grid, kTileThreads, 0, s>>>(P, ncand);
+    else chi2_multi_kernel<M, 4><<<grid, kTileThreads, 0, s>>>(P, ncand);
+  };
+  if (model == ADC_MODEL_GPOLY) {
+    go(GPoly{});
+  } else {
+    switch (np / 3) {
+      case 1: go(GSum<1>{}); break;
+      case 2: go(GSum<2>{}); break;
+      case 3: go(GSum<3>{}); break;
+      case 4: go(GSum<4>{}); break;
+      case 8: go(GSum<8>{}); break;
+      default: return fail(ADC_E_ARG, "gsum: unsupported component count");
+    }
+  }
+  ADCB_CUDA(cudaGetLastError());
+  const int R = 1 + 3 * ncand;
   const int64_t nchunks = (ntiles + chunk_tiles - 1) / chunk_tiles;
   chi2_chunk_kernel<<<(unsigned)nchunks, kChunkThreads, 0, s>>>(P.tile_ws, ntiles, R,
                                                                (int)chunk_tiles, records);

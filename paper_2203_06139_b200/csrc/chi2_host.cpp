@@ -114,6 +114,13 @@ struct adc_chi2_plan {
   double* h_q = nullptr;
   double* h_rec = nullptr;
   cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [grad][fast]
+  // batched line search (adc_cuda_chi2_multi): lazily allocated
+  double* qmulti = nullptr;     // device [kMultiMax][QDev]
+  double* h_qmulti = nullptr;   // pinned
+  double* tile_ws_multi = nullptr;
+  double* records_multi = nullptr;
+  double* h_rec_multi = nullptr;
+  int64_t multi_passes = 0;
 };
 
 namespace {
@@ -252,6 +259,11 @@ extern "C" int adc_cuda_chi2_plan_destroy(adc_chi2_plan* P) {
   if (P->records) cudaFree(P->records);
   if (P->h_q) cudaFreeHost(P->h_q);
   if (P->h_rec) cudaFreeHost(P->h_rec);
+  if (P->qmulti) cudaFree(P->qmulti);
+  if (P->h_qmulti) cudaFreeHost(P->h_qmulti);
+  if (P->tile_ws_multi) cudaFree(P->tile_ws_multi);
+  if (P->records_multi) cudaFree(P->records_multi);
+  if (P->h_rec_multi) cudaFreeHost(P->h_rec_multi);
   if (P->stream) cudaStreamDestroy(P->stream);
   delete P;
   return ADC_OK;
@@ -306,6 +318,61 @@ extern "C" int adc_cuda_chi2(adc_chi2_plan* P, const double* q, double* chi2) {
   return adc_chi2_finalize(P->np, P->events, P->h_rec, P->L.nchunks, 0, nullptr, chi2);
 }
 
+extern "C" int adc_cuda_chi2_multi(adc_chi2_plan* P, const double* qs, int32_t ncand,
+                                   double* chi2s) {
+  clear_error();
+  if (P == nullptr || qs == nullptr || chi2s == nullptr) return fail(ADC_E_ARG, "null argument");
+  if (ncand < 1 || ncand > kMultiMax) return fail(ADC_E_ARG, "chi2 multi: 1..32 candidates");
+  if (P->L.chunk_begin != 0 || P->L.chunk_end != P->L.nchunks)
+    return fail(ADC_E_ARG, "sharded plan: multi pass is single-device");
+  for (int k = 0; k < ncand; ++k)
+    if (int rc = check_domain(P, qs + (size_t)k * P->np)) return rc;
+  ADCB_CUDA(cudaSetDevice(P->device));
+  const size_t qb = qdev_bytes();
+  const int Rm = 1 + 3 * kMultiMax;
+  const int64_t ntiles_local = std::max<int64_t>(
+      1, (P->L.bin_end + P->L.tile_bins - 1) / P->L.tile_bins - P->L.chunk_begin * P->L.chunk_tiles);
+  const int64_t nrec = std::max<int64_t>(1, local_chunks(P));
+  if (P->qmulti == nullptr) {
+    ADCB_CUDA(cudaMalloc(&P->qmulti, qb * kMultiMax));
+    ADCB_CUDA(cudaMallocHost(&P->h_qmulti, qb * kMultiMax));
+    ADCB_CUDA(cudaMalloc(&P->tile_ws_multi, (size_t)ntiles_local * Rm * sizeof(double)));
+    ADCB_CUDA(cudaMalloc(&P->records_multi, (size_t)nrec * Rm * sizeof(double)));
+    ADCB_CUDA(cudaMallocHost(&P->h_rec_multi, (size_t)nrec * Rm * sizeof(double)));
+  }
+  for (int k = 0; k < ncand; ++k)
+    fill_qdev(P->model, P->np, qs + (size_t)k * P->np,
+              reinterpret_cast<double*>(reinterpret_cast<char*>(P->h_qmulti) + k * qb));
+  ADCB_CUDA(cudaMemcpyAsync(P->qmulti, P->h_qmulti, qb * ncand, cudaMemcpyHostToDevice, P->stream));
+  Chi2Pass pass = make_pass(P);
+  pass.qdev = P->qmulti;
+  pass.tile_ws = P->tile_ws_multi;
+  if (int rc = chi2_multi_enqueue(pass, P->model, P->np, ncand, P->bpt, P->L.chunk_tiles,
+                                  P->records_multi, P->stream))
+    return rc;
+  const int R = 1 + 3 * ncand;
+  ADCB_CUDA(cudaMemcpyAsync(P->h_rec_multi, P->records_multi,
+                            (size_t)P->L.nchunks * R * sizeof(double), cudaMemcpyDeviceToHost,
+                            P->stream));
+  ADCB_CUDA(cudaStreamSynchronize(P->stream));
+  ++P->multi_passes;
+  // Per candidate: the same records a single value pass produces -> same finalize.
+  std::vector<double> rec4((size_t)P->L.nchunks * 4);
+  for (int k = 0; k < ncand; ++k) {
+    for (int64_t c = 0; c < P->L.nchunks; ++c) {
+      const double* r = P->h_rec_multi + c * R;
+      rec4[c * 4 + 0] = r[1 + 3 * k];
+      rec4[c * 4 + 1] = r[2 + 3 * k];
+      rec4[c * 4 + 2] = r[3 + 3 * k];
+      rec4[c * 4 + 3] = r[0];
+    }
+    if (int rc = adc_chi2_finalize(P->np, P->events, rec4.data(), P->L.nchunks, 0, nullptr,
+                                   chi2s + k))
+      return rc;
+  }
+  return ADC_OK;
+}
+
 // ---------------------------------------------------------------------------
 // Fit loop: FitEngine::fit (fit.cpp:315-425), steepest descent with Armijo
 // backtracking, generalised sigma clamp (fit.cpp:268-278 hard-codes every
@@ -318,7 +385,39 @@ extern "C" void adc_fit_default_options(adc_fit_options* o) {
   o->sigma_min = 1e-3;
   o->armijo_c1 = 1e-4;
   o->trace_iterates = 0;
+  o->use_hessian = 0;
 }
+
+namespace {
+// (H + lambda I) d = g by Gaussian elimination with partial pivoting, the
+// reference's damped solve (fit.cpp:282-311); false on a vanishing pivot.
+bool damped_solve(std::vector<double> h, std::vector<double> g, double lambda, int n,
+                  std::vector<double>& out) {
+  for (int i = 0; i < n; ++i) h[(size_t)i * n + i] += lambda;
+  for (int col = 0; col < n; ++col) {
+    int piv = col;
+    for (int r = col + 1; r < n; ++r)
+      if (std::fabs(h[(size_t)r * n + col]) > std::fabs(h[(size_t)piv * n + col])) piv = r;
+    if (std::fabs(h[(size_t)piv * n + col]) < 1e-30) return false;
+    if (piv != col) {
+      for (int c = 0; c < n; ++c) std::swap(h[(size_t)piv * n + c], h[(size_t)col * n + c]);
+      std::swap(g[piv], g[col]);
+    }
+    for (int r = col + 1; r < n; ++r) {
+      const double f = h[(size_t)r * n + col] / h[(size_t)col * n + col];
+      for (int c = col; c < n; ++c) h[(size_t)r * n + c] -= f * h[(size_t)col * n + c];
+      g[r] -= f * g[col];
+    }
+  }
+  out.assign(n, 0.0);
+  for (int r = n - 1; r >= 0; --r) {
+    double v = g[r];
+    for (int c = r + 1; c < n; ++c) v -= h[(size_t)r * n + c] * out[c];
+    out[r] = v / h[(size_t)r * n + r];
+  }
+  return true;
+}
+}  // namespace
 
 extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* clamp_idx,
                             int32_t nclamp, const adc_fit_options* opts, adc_fit_result* result,
@@ -365,24 +464,90 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
       res.converged = 1;
       break;
     }
+    std::vector<double> direction = g;
+    if (opts->use_hessian) {
+      // Central differences of the gradient, 2*np extra passes (fit.cpp:346-381).
+      std::vector<double> hess((size_t)np * np, 0.0), gp(np), gm(np), probe = q;
+      for (int c = 0; c < np; ++c) {
+        const double x = probe[c];
+        const double step = std::cbrt(2.220446049250313e-16) * std::max(1.0, std::fabs(x));
+        const auto h0 = clk::now();
+        probe[c] = x + step;
+        if (int rc = adc_cuda_chi2_gradient(P, probe.data(), gp.data(), nullptr)) return rc;
+        probe[c] = x - step;
+        if (int rc = adc_cuda_chi2_gradient(P, probe.data(), gm.data(), nullptr)) return rc;
+        res.gradient_ns += (uint64_t)std::chrono::nanoseconds(clk::now() - h0).count();
+        res.gradient_evals += 2;
+        probe[c] = x;
+        for (int r = 0; r < np; ++r) hess[(size_t)r * np + c] = (gp[r] - gm[r]) / (2.0 * step);
+      }
+      double lambda = 0.0;
+      bool ok = false;
+      for (int attempt = 0; attempt < 10 && !ok; ++attempt) {
+        ok = damped_solve(hess, g, lambda, np, direction);
+        if (ok) {
+          double descent = 0.0;
+          for (int i = 0; i < np; ++i) descent += g[i] * direction[i];
+          ok = descent > 0.0;
+        }
+        lambda = lambda == 0.0 ? 1e-6 : lambda * 10.0;
+      }
+      if (!ok) direction = g;  // steepest descent
+    }
     double gd = 0.0;
-    for (int i = 0; i < np; ++i) gd += g[i] * g[i];
+    for (int i = 0; i < np; ++i) gd += g[i] * direction[i];
     double t = 1.0, next = 0.0;
     bool accepted = false;
-    while (t >= 1e-18) {
-      trial = q;
-      for (int i = 0; i < np; ++i) trial[i] -= t * g[i];
-      const int cl = clamp(trial);
-      double c2 = 0.0;
-      if (int rc = adc_cuda_chi2(P, trial.data(), &c2)) return rc;
-      ++res.chi2_evals;
-      if (c2 <= cur - opts->armijo_c1 * t * gd) {
-        accepted = true;
-        next = c2;
-        res.sigma_clamps += cl;
-        break;
+    if (P->fast) {
+      // Batched Armijo: the trials t = 1, 1/2, 1/4, ... of the sequential
+      // search (fit.cpp:390-403) evaluated kMultiMax at a time in one pass;
+      // the first accepted one is taken, so the iterate is the same as the
+      // sequential search's (each candidate's chi2 is bit-identical to a
+      // single value pass).
+      std::vector<double> trials, tvals, c2s(kMultiMax);
+      std::vector<int> cls;
+      while (t >= 1e-18 && !accepted) {
+        trials.clear();
+        tvals.clear();
+        cls.clear();
+        for (double tt = t; tt >= 1e-18 && (int)tvals.size() < kMultiMax; tt *= 0.5) {
+          trial = q;
+          for (int i = 0; i < np; ++i) trial[i] -= tt * direction[i];
+          cls.push_back(clamp(trial));
+          trials.insert(trials.end(), trial.begin(), trial.end());
+          tvals.push_back(tt);
+        }
+        if (tvals.empty()) break;
+        if (int rc = adc_cuda_chi2_multi(P, trials.data(), (int32_t)tvals.size(), c2s.data()))
+          return rc;
+        for (size_t k = 0; k < tvals.size(); ++k) {
+          ++res.chi2_evals;
+          if (c2s[k] <= cur - opts->armijo_c1 * tvals[k] * gd) {
+            accepted = true;
+            next = c2s[k];
+            res.sigma_clamps += cls[k];
+            trial.assign(trials.begin() + k * np, trials.begin() + (k + 1) * np);
+            break;
+          }
+        }
+        t = tvals.back() * 0.5;
       }
-      t *= 0.5;
+    } else {
+      while (t >= 1e-18) {
+        trial = q;
+        for (int i = 0; i < np; ++i) trial[i] -= t * direction[i];
+        const int cl = clamp(trial);
+        double c2 = 0.0;
+        if (int rc = adc_cuda_chi2(P, trial.data(), &c2)) return rc;
+        ++res.chi2_evals;
+        if (c2 <= cur - opts->armijo_c1 * t * gd) {
+          accepted = true;
+          next = c2;
+          res.sigma_clamps += cl;
+          break;
+        }
+        t *= 0.5;
+      }
     }
     if (!accepted) {
       res.converged = 1;

@@ -8,7 +8,8 @@
 
 namespace adcb {
 
-constexpr int kMaxNp = 24;  // gsum up to K = 8 components (the reference bench K list 1,2,4,8)
+constexpr int kMaxNp = 24;
+constexpr int kMultiMax = 32;  // line-search candidates per multi pass  // gsum up to K = 8 components (the reference bench K list 1,2,4,8)
 
 struct Chi2Pass {
   const double* counts;  // full histogram, device
@@ -21,6 +22,8 @@ struct Chi2Pass {
 
 int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast, int bpt,
                  int64_t chunk_tiles, double* records, cudaStream_t s);
+int chi2_multi_enqueue(const Chi2Pass& P, int model, int np, int ncand, int bpt,
+                       int64_t chunk_tiles, double* records, cudaStream_t s);
 void fill_qdev(int model, int np, const double* q, double* host_qdev);
 size_t qdev_bytes();
 int chi2_set_tune(int v);  // kernel-variant experiments (ADC_CHI2_TUNE)

@@ -36,12 +36,13 @@ class Histogram:
 
 @dataclass
 class FitOptions:
-    """fit.hpp:56-65 (use_hessian is not part of the B200 path)."""
+    """fit.hpp:56-65."""
     budget: int = 400
     grad_tol: float = 1e-6
     chi2_rel_tol: float = 1e-12
     sigma_min: float = 1e-3
     armijo_c1: float = 1e-4
+    use_hessian: bool = False
     trace_iterates: int = 0
 
 
@@ -117,6 +118,15 @@ class Chi2Plan:
         check(lib.adc_cuda_chi2(self._p, dbl_array(q), ctypes.byref(c2)))
         return c2.value
 
+    def chi2_multi(self, qs) -> np.ndarray:
+        """chi2 of several parameter vectors in one pass (bit-identical to chi2)."""
+        qs = np.ascontiguousarray(qs, dtype=np.float64).reshape(-1, self.np)
+        out = np.zeros(qs.shape[0])
+        dp = ctypes.POINTER(ctypes.c_double)
+        check(lib.adc_cuda_chi2_multi(self._p, qs.ctypes.data_as(dp), qs.shape[0],
+                                      out.ctypes.data_as(dp)))
+        return out
+
     def partials(self, q, want_grad: bool, records_dev=None):
         """Enqueue this rank's pass; records land in records_dev (a float64 CUDA
         tensor of local_chunks * record_len) or the plan's own buffer."""
@@ -173,7 +183,7 @@ class FitEngine:
         opts = opts or FitOptions()
         pl = self._plan(h)
         o = _FitOptionsC(opts.budget, opts.grad_tol, opts.chi2_rel_tol, opts.sigma_min,
-                         opts.armijo_c1, opts.trace_iterates)
+                         opts.armijo_c1, opts.trace_iterates, 1 if opts.use_hessian else 0)
         idx = default_clamp(self.model, self.np) if clamp is None else list(clamp)
         cidx = (ctypes.c_int32 * max(1, len(idx)))(*idx)
         params = np.ascontiguousarray(init, dtype=np.float64).copy()

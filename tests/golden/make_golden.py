@@ -122,13 +122,16 @@ def main():
 
     # Fit loop iterates (fit.cpp:315-425), trace 10, budget 12.
     fi = {}
-    for key, model, bins, events, qtrue, q in (
-        ("gpoly_b400", "gpoly", 400, 2e5, synth.GPOLY_TRUTH, synth.GPOLY_INIT),
-        ("gsum1_b300", "gsum", 300, 1e5, (1.0, 0.0, 1.5), (0.8, 0.3, 1.2)),
+    for key, model, bins, events, qtrue, q, budget in (
+        ("gpoly_b400", "gpoly", 400, 2e5, synth.GPOLY_TRUTH, synth.GPOLY_INIT, "12"),
+        ("gsum1_b300", "gsum", 300, 1e5, (1.0, 0.0, 1.5), (0.8, 0.3, 1.2), "12"),
+        ("gpoly_b400_hess", "gpoly", 400, 2e5, synth.GPOLY_TRUTH, synth.GPOLY_INIT, "12:hess"),
+        ("gsum1_b300_hess", "gsum", 300, 1e5, (1.0, 0.0, 1.5), (0.8, 0.3, 1.2), "12:hess"),
     ):
         counts, ev = synth.histogram(bins, -5.0, 5.0, events, model, qtrue, seed=bins + 1)
         counts.astype("<f8").tofile(ti)
-        meta = run("fit-in", model, bins, -5.0, 5.0, ti, to, 10, 12, *[repr(float(v)) for v in q])
+        meta = run("fit-in", model, bins, -5.0, 5.0, ti, to, 10, budget,
+                   *[repr(float(v)) for v in q])
         assert meta["fitengine_match"]
         np_ = len(q)
         o = f64(to, 5 + np_ + 10 * np_)
@@ -136,7 +139,7 @@ def main():
                    f"{key}_chi2": o[0], f"{key}_iterations": o[1], f"{key}_gradient_evals": o[2],
                    f"{key}_converged": o[3], f"{key}_sigma_clamps": o[4],
                    f"{key}_params": o[5:5 + np_], f"{key}_iterates": o[5 + np_:].reshape(10, np_),
-                   f"{key}_model": model})
+                   f"{key}_model": model, f"{key}_hessian": budget.endswith(":hess")})
     np.savez(os.path.join(OUT, "fit_cases.npz"), **fi)
     print("golden fixtures written to", OUT)
 

@@ -236,20 +236,63 @@ def test_chi2_domain_error():
 
 
 # ---------------------------------------------------------------------------- fit
-@pytest.mark.parametrize("key", ["gpoly_b400", "gsum1_b300"])
+@pytest.mark.parametrize("key", ["gpoly_b400", "gsum1_b300", "gpoly_b400_hess",
+                                 "gsum1_b300_hess"])
 def test_fit_iterates_match_reference(key):
+    """Fit iterates against the reference's FitEngine::fit (fit.cpp:315-425).
+
+    Steepest descent: every traced iterate within 1e-9.  Numeric-Hessian Newton
+    steps difference the gradient over ~6e-6 and solve a nearly singular system
+    (chi2 normalises by S, so the overall amplitude scale is unidentified and
+    the Hessian is singular along it): the reference's own iterate-sequence
+    precedent, 1e-5 (test_fit.cpp:95-109), applies to the identified shape
+    parameters; the final chi2 must agree to 1e-6."""
     g = golden("fit_cases.npz")
     model = str(g[f"{key}_model"])
     init = g[f"{key}_init"]
     counts = g[f"{key}_counts"]
+    hess = bool(g[f"{key}_hessian"])
     h = adc.Histogram(counts.size, -5.0, 5.0, float(counts.sum()), counts)
     eng = adc.FitEngine(model, init.size)
-    res = eng.fit(h, init, adc.FitOptions(budget=12, trace_iterates=10))
+    res = eng.fit(h, init, adc.FitOptions(budget=12, trace_iterates=10, use_hessian=hess))
     ref_its = g[f"{key}_iterates"]
     n_ref = min(10, int(g[f"{key}_iterations"]) + 1)
     assert len(res.iterates) == n_ref
-    for k in range(n_ref):
-        assert rel_err(res.iterates[k], ref_its[k]).max() <= 1e-9, k
     assert res.iterations == int(g[f"{key}_iterations"])
-    assert rel_err(res.params, g[f"{key}_params"]).max() <= 1e-9
-    assert rel_err(res.chi2, g[f"{key}_chi2"]) <= 1e-10
+    assert rel_err(res.chi2, g[f"{key}_chi2"]) <= (1e-6 if hess else 1e-10)
+    if not hess:
+        cols, tol = slice(None), 1e-9
+    else:
+        cols, tol = ([1, 2] if model == "gsum" else slice(None)), 1e-5
+    for k in range(n_ref):
+        assert rel_err(np.asarray(res.iterates[k])[cols], ref_its[k][cols]).max() <= tol, k
+    assert rel_err(np.asarray(res.params)[cols], g[f"{key}_params"][cols]).max() <= tol
+
+
+def test_chi2_multi_bitwise_equals_single():
+    # The batched line-search pass gives each candidate exactly the single pass's bits.
+    for bins in (2000, 1_000_000, 5_000_000):
+        counts, ev = synth.histogram(bins, events=100.0 * bins, seed=bins)
+        h = adc.Histogram(bins, -5.0, 5.0, ev, counts)
+        pl = adc.Chi2Plan("gpoly", 6, h)
+        q = np.array(synth.GPOLY_INIT)
+        g = np.array([1e3, -2e3, 5e2, 10.0, -3.0, 1.0])
+        qs = np.stack([q - 2.0 ** -k * g for k in range(32)])
+        multi = pl.chi2_multi(qs)
+        single = np.array([pl.chi2(qk) for qk in qs])
+        assert np.array_equal(multi, single), bins
+        assert np.array_equal(pl.chi2_multi(qs[:5]), single[:5])
+
+
+def test_fit_1e6_newton_converges_to_truth():
+    # Plain steepest descent (the reference default) crawls on this badly scaled
+    # 6-parameter problem; the reference's numeric-Hessian Newton option converges.
+    counts, ev = synth.histogram(10**6, events=1e8, seed=11)
+    h = adc.Histogram(10**6, -5.0, 5.0, ev, counts)
+    r = adc.FitEngine("gpoly", 6).fit(h, synth.GPOLY_INIT,
+                                      adc.FitOptions(budget=400, use_hessian=True))
+    # the Gaussian's position and width are identified (the overall scale is
+    # not: chi2 normalises by S, fit.cpp:231-245)
+    # Gaussian parameters recovered to the reference's bounds (test_fit.cpp:81-93)
+    assert abs(r.params[1] - synth.GPOLY_TRUTH[1]) < 0.05
+    assert abs(r.params[2] - synth.GPOLY_TRUTH[2]) < 0.05
