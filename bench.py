@@ -114,13 +114,33 @@ def dist_setup():
     return world, rank, local
 
 
+BACKEND = "nccl"
+
+
+def device_index(local):
+    """One process per GPU; with --dist-backend gloo on a box with fewer GPUs
+    than ranks (path testing only) ranks share devices round-robin."""
+    import torch
+    return local % max(1, torch.cuda.device_count())
+
+
 def maybe_init_pg(world, local, backend="nccl"):
     import torch
     import torch.distributed as dist
+    global BACKEND
+    BACKEND = backend
     if world > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group(backend, device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group(backend, device_id=torch.device("cuda", device_index(local)))
+        else:
+            dist.init_process_group(backend)
     return dist if world > 1 else None
+
+
+def coll_device():
+    """Collectives run on the GPU with NCCL, on host copies with gloo."""
+    return "cuda" if BACKEND == "nccl" else "cpu"
 
 
 def barrier_sync(dist):
@@ -135,7 +155,7 @@ def max_over_ranks(dist, value):
     import torch
     if dist is None:
         return value
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    t = torch.tensor([value], dtype=torch.float64, device=coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -346,8 +366,13 @@ def bench_chi2(world, rank, local, dist, bins=100_000_000, passes=20, warm=3):
         plan.partials(q, True, loc)
         if dist is not None:
             torch.cuda.synchronize()
-            dist.all_gather_into_tensor(allr, loc)
-            host = allr.cpu().numpy().reshape(world, per * R)
+            if BACKEND == "nccl":
+                dist.all_gather_into_tensor(allr, loc)   # the one exchange step (NVLink)
+                host = allr.cpu().numpy().reshape(world, per * R)
+            else:
+                parts = [torch.zeros(per * R, dtype=torch.float64) for _ in range(world)]
+                dist.all_gather(parts, loc.cpu())
+                host = torch.stack(parts).numpy()
             rec = np.concatenate([host[r, :counts_by_rank[r] * R] for r in range(world)])
         else:
             rec = loc.cpu().numpy()[:nloc * R]
@@ -435,8 +460,9 @@ def bench_points_small(local, workload, steps=20, warm=3):
 
 def ours_arm(a, world, rank, local):
     import torch
+    local = device_index(local)
     torch.cuda.set_device(local)
-    dist = maybe_init_pg(world, local)
+    dist = maybe_init_pg(world, local, a.dist_backend)
     import paper_2203_06139_b200  # noqa: F401  (fails loudly without the CUDA library)
     value, ms_step, roof, e2e, clocks, desc, dim, npts = bench_points(a, world, rank, local, dist)
     secondary = []
@@ -504,6 +530,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: collectives on host copies (multi-rank path test on 1 GPU)")
     a = ap.parse_args()
     world, rank, local = dist_setup()
     if a.impl == "reference":
