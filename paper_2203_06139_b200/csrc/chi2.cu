@@ -56,6 +56,14 @@ __device__ __forceinline__ double rcp_pos(double c) {
 // width parameter with multiplies by its host-computed reciprocal.
 struct GPoly {
   static constexpr int NP = 6;
+  // q[3..5] enter linearly: dm/dq = (1, x, x^2) does not depend on q, so their
+  // G0 and G1 sums are the same for every pass of a fit (precomputed once).
+  static constexpr int LIN0 = 3;
+  __device__ static __forceinline__ void lin_basis(double x, double* phi) {
+    phi[0] = 1.0;
+    phi[1] = x;
+    phi[2] = fmul(x, x);
+  }
   struct Reg {  // uniform parameters, held in registers for the whole pass
     double q0, q1, q2, q3, q4, q5, inv2;
   };
@@ -97,6 +105,8 @@ struct GPoly {
 template <int K>
 struct GSum {
   static constexpr int NP = 3 * K;
+  static constexpr int LIN0 = NP;  // no q-independent gradient components
+  __device__ static __forceinline__ void lin_basis(double, double*) {}
   struct Reg {
     double q[3 * K];
     double inv[K];
@@ -184,8 +194,10 @@ __device__ __forceinline__ void bin_accumulate(const BinTerm<M, GRAD, FAST>& t, 
   if constexpr (GRAD) {
 #pragma unroll
     for (int i = 0; i < NP; ++i) {
-      acc[4 + i] += t.bg[i];
-      acc[4 + NP + i] = __fma_rn(t.w, t.bg[i], acc[4 + NP + i]);
+      if (i < M::LIN0) {  // q-independent G0 / G1 entries come from the lin pre-pass
+        acc[4 + i] += t.bg[i];
+        acc[4 + NP + i] = __fma_rn(t.w, t.bg[i], acc[4 + NP + i]);
+      }
       acc[4 + 2 * NP + i] = __fma_rn(t.mc, t.bg[i], acc[4 + 2 * NP + i]);
     }
   }
@@ -194,10 +206,11 @@ __device__ __forceinline__ void bin_accumulate(const BinTerm<M, GRAD, FAST>& t, 
 // PAIR evaluates two independent bins before folding either, giving the
 // scheduler two dependency chains to interleave (the model's exp chain is
 // ~15 dependent FP64 ops deep).  The accumulation order is unchanged.
-template <class M, bool GRAD, bool FAST, int BPT, bool CHECK, bool PAIR>
+template <class M, bool GRAD, bool FAST, bool CHECK, bool PAIR>
 __device__ __forceinline__ void tile_bins(const Chi2Pass& P, const typename M::Reg& QR,
                                           const double* tab, int64_t base, double* acc) {
-  constexpr int PD = BPT < kPD ? BPT : kPD;
+  constexpr int PD = kPD;  // P.bpt is a multiple of kPD (adc_chi2_make_layout)
+  const int BPT = P.bpt;
   constexpr int STEP = PAIR && PD >= 2 ? 2 : 1;
   double ring[PD];
 #pragma unroll
@@ -230,7 +243,7 @@ __device__ __forceinline__ void tile_bins(const Chi2Pass& P, const typename M::R
   }
 }
 
-template <class M, bool GRAD, bool FAST, int BPT, int MINB = tile_min_blocks<M, GRAD>(),
+template <class M, bool GRAD, bool FAST, int MINB = tile_min_blocks<M, GRAD>(),
           bool PAIR = false>
 __global__ void __launch_bounds__(kTileThreads, MINB) chi2_tile_kernel(Chi2Pass P) {
   constexpr int NP = M::NP;
@@ -246,7 +259,8 @@ __global__ void __launch_bounds__(kTileThreads, MINB) chi2_tile_kernel(Chi2Pass 
   __syncthreads();
   const typename M::Reg QR = M::load(Q);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int64_t TB = (int64_t)BPT * kTileThreads;
+  const int BPT = P.bpt;
+  const int64_t TB = (int64_t)BPT * kTileThreads;
   for (int64_t tile = P.tile_begin + blockIdx.x; tile < P.tile_end; tile += gridDim.x) {
     const int64_t base = tile * TB + threadIdx.x;
     {  // the next tile of this CTA into L2 while this one computes
@@ -260,9 +274,9 @@ __global__ void __launch_bounds__(kTileThreads, MINB) chi2_tile_kernel(Chi2Pass 
 #pragma unroll
     for (int v = 0; v < R; ++v) acc[v] = 0.0;
     if ((tile + 1) * TB <= P.bin_end)
-      tile_bins<M, GRAD, FAST, BPT, false, PAIR>(P, QR, tab, base, acc);
+      tile_bins<M, GRAD, FAST, false, PAIR>(P, QR, tab, base, acc);
     else
-      tile_bins<M, GRAD, FAST, BPT, true, PAIR>(P, QR, tab, base, acc);
+      tile_bins<M, GRAD, FAST, true, PAIR>(P, QR, tab, base, acc);
     // fixed shuffle tree, then fixed cross-warp tree
 #pragma unroll
     for (int v = 0; v < R; ++v) {
@@ -292,7 +306,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) chi2_tile_kernel(Chi2Pass 
 // Record layout per tile / chunk: [C0, (S, A1, A2) x ncand].
 constexpr int kMultiGroup = 8;
 
-template <class M, int BPT>
+template <class M>
 __global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P, int ncand) {
   constexpr int G = kMultiGroup;
   __shared__ QDev Q[G];
@@ -310,7 +324,8 @@ __global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P,
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int R = 1 + 3 * ncand;
-  constexpr int64_t TB = (int64_t)BPT * kTileThreads;
+  const int BPT = P.bpt;
+  const int64_t TB = (int64_t)BPT * kTileThreads;
   for (int64_t tile = P.tile_begin + blockIdx.x; tile < P.tile_end; tile += gridDim.x) {
     const int64_t base = tile * TB + threadIdx.x;
     double acc[3 * G + 1];
@@ -364,12 +379,69 @@ __global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P,
   }
 }
 
+// ---- K3l: q-independent basis sums (once per plan) ------------------------------
+// For the linear parameters: G0_i = sum phi_i(x_j), G1_i = sum [c_j > 0] phi_i(x_j),
+// accumulated with exactly the per-thread order and trees of the gradient
+// pass, so merging them (chunk kernel) gives the same bits as accumulating
+// them in every pass.  Record per tile / chunk: [G0_lin..., G1_lin...].
+template <class M>
+__global__ void __launch_bounds__(kTileThreads) chi2_lin_kernel(Chi2Pass P) {
+  constexpr int L = M::NP - M::LIN0;
+  constexpr int RL = 2 * (L > 0 ? L : 1);
+  __shared__ double red[kTileThreads / 32][RL];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int BPT = P.bpt;
+  const int64_t TB = (int64_t)BPT * kTileThreads;
+  for (int64_t tile = P.tile_begin + blockIdx.x; tile < P.tile_end; tile += gridDim.x) {
+    const int64_t base = tile * TB + threadIdx.x;
+    double acc[RL];
+#pragma unroll
+    for (int v = 0; v < RL; ++v) acc[v] = 0.0;
+    double jh = fadd((double)base, 0.5);
+    for (int k = 0; k < BPT; ++k) {
+      const int64_t j = base + (int64_t)k * kTileThreads;
+      if (j < P.bin_end) {
+        const double c = ld_stream(P.counts + j);
+        const double x = fadd(P.lo, fmul(jh, P.width));
+        const double w = c > 0.0 ? 1.0 : 0.0;
+        double phi[L > 0 ? L : 1];
+        M::lin_basis(x, phi);
+#pragma unroll
+        for (int i = 0; i < L; ++i) {
+          acc[i] += phi[i];
+          acc[L + i] = __fma_rn(w, phi[i], acc[L + i]);
+        }
+      }
+      jh = fadd(jh, (double)kTileThreads);
+    }
+#pragma unroll
+    for (int v = 0; v < RL; ++v) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc[v] += __shfl_down_sync(0xffffffffu, acc[v], off);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int v = 0; v < RL; ++v) red[warp][v] = acc[v];
+    }
+    __syncthreads();
+    for (int v = threadIdx.x; v < RL; v += kTileThreads) {
+      const double s01 = red[0][v] + red[1][v], s23 = red[2][v] + red[3][v];
+      const double s45 = red[4][v] + red[5][v], s67 = red[6][v] + red[7][v];
+      P.tile_ws[(tile - P.tile_begin) * RL + v] = (s01 + s23) + (s45 + s67);
+    }
+    __syncthreads();
+  }
+}
+
 // ---- K4: chunk reduce (fixed tree over the chunk's tiles) ---------------------
 // One CTA per chunk; warp w owns record entries v = w, w+8, ...; lane l sums
 // tiles l, l+32, l+64, l+96 pairwise, then a fixed shuffle tree.
+// lin (optional): per-chunk [G0_lin, G1_lin] of the K3l pre-pass, merged into
+// the record entries the gradient pass leaves at zero (0 + v == v exactly).
 __global__ void __launch_bounds__(kChunkThreads) chi2_chunk_kernel(
     const double* __restrict__ tile_ws, int64_t ntiles, int R, int chunk_tiles,
-    double* __restrict__ records) {
+    double* __restrict__ records, const double* __restrict__ lin = nullptr, int np = 0,
+    int lin0 = 0) {
   const int64_t chunk = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t t0 = chunk * chunk_tiles;
@@ -383,6 +455,11 @@ __global__ void __launch_bounds__(kChunkThreads) chi2_chunk_kernel(
     double a = (part[0] + part[1]) + (part[2] + part[3]);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) a += __shfl_down_sync(0xffffffffu, a, off);
+    if (lin != nullptr && lane == 0) {
+      const int L = np - lin0;
+      if (v >= 4 + lin0 && v < 4 + np) a = a + lin[chunk * 2 * L + (v - 4 - lin0)];
+      else if (v >= 4 + np + lin0 && v < 4 + 2 * np) a = a + lin[chunk * 2 * L + L + (v - 4 - np - lin0)];
+    }
     if (lane == 0) records[chunk * R + v] = a;
   }
 }
@@ -391,36 +468,31 @@ __global__ void __launch_bounds__(kChunkThreads) chi2_chunk_kernel(
 int g_chi2_tune = 0;  // experiment knob (ADC_CHI2_TUNE): 0 default, != 0 = paired bins
 
 template <class M, bool GRAD, bool FAST>
-static void launch_tiles_t(const Chi2Pass& P, int bpt, int blocks, cudaStream_t s) {
+static void launch_tiles_t(const Chi2Pass& P, int blocks, cudaStream_t s) {
   constexpr int MB = tile_min_blocks<M, GRAD>();
   if constexpr (std::is_same<M, GPoly>::value && FAST) {
-    if (bpt == 128 && g_chi2_tune != 0) {  // experiments: 2 = paired bins
-      chi2_tile_kernel<M, GRAD, FAST, 128, MB, true><<<blocks, kTileThreads, 0, s>>>(P);
+    if (g_chi2_tune != 0) {  // experiment: paired bins
+      chi2_tile_kernel<M, GRAD, FAST, MB, true><<<blocks, kTileThreads, 0, s>>>(P);
       return;
     }
   }
-  if (bpt == 128)
-    chi2_tile_kernel<M, GRAD, FAST, 128><<<blocks, kTileThreads, 0, s>>>(P);
-  else if (bpt == 32)
-    chi2_tile_kernel<M, GRAD, FAST, 32><<<blocks, kTileThreads, 0, s>>>(P);
-  else
-    chi2_tile_kernel<M, GRAD, FAST, 4><<<blocks, kTileThreads, 0, s>>>(P);
+  chi2_tile_kernel<M, GRAD, FAST><<<blocks, kTileThreads, 0, s>>>(P);
 }
 
 template <class M>
-static void launch_tiles_m(const Chi2Pass& P, bool grad, bool fast, int bpt, int blocks,
+static void launch_tiles_m(const Chi2Pass& P, bool grad, bool fast, int blocks,
                            cudaStream_t s) {
   if (grad) {
-    if (fast) launch_tiles_t<M, true, true>(P, bpt, blocks, s);
-    else launch_tiles_t<M, true, false>(P, bpt, blocks, s);
+    if (fast) launch_tiles_t<M, true, true>(P, blocks, s);
+    else launch_tiles_t<M, true, false>(P, blocks, s);
   } else {
-    if (fast) launch_tiles_t<M, false, true>(P, bpt, blocks, s);
-    else launch_tiles_t<M, false, false>(P, bpt, blocks, s);
+    if (fast) launch_tiles_t<M, false, true>(P, blocks, s);
+    else launch_tiles_t<M, false, false>(P, blocks, s);
   }
 }
 
-int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast, int bpt,
-                 int64_t chunk_tiles, double* records, cudaStream_t s) {
+int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast,
+                 int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin) {
   const int64_t ntiles = P.tile_end - P.tile_begin;
   if (ntiles <= 0) return ADC_OK;
   const int R = grad ? 4 + 3 * np : 4;
@@ -429,26 +501,46 @@ int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast, int
   // models, see tile_min_blocks), tiles grid-strided.
   const int64_t blocks = std::min<int64_t>(ntiles, (int64_t)sm_count() * (np <= 6 ? 2 : 1));
   if (model == ADC_MODEL_GPOLY) {
-    launch_tiles_m<GPoly>(P, grad, fast, bpt, (int)blocks, s);
+    launch_tiles_m<GPoly>(P, grad, fast, (int)blocks, s);
   } else {
     switch (np / 3) {
-      case 1: launch_tiles_m<GSum<1>>(P, grad, fast, bpt, (int)blocks, s); break;
-      case 2: launch_tiles_m<GSum<2>>(P, grad, fast, bpt, (int)blocks, s); break;
-      case 3: launch_tiles_m<GSum<3>>(P, grad, fast, bpt, (int)blocks, s); break;
-      case 4: launch_tiles_m<GSum<4>>(P, grad, fast, bpt, (int)blocks, s); break;
-      case 8: launch_tiles_m<GSum<8>>(P, grad, fast, bpt, (int)blocks, s); break;
+      case 1: launch_tiles_m<GSum<1>>(P, grad, fast, (int)blocks, s); break;
+      case 2: launch_tiles_m<GSum<2>>(P, grad, fast, (int)blocks, s); break;
+      case 3: launch_tiles_m<GSum<3>>(P, grad, fast, (int)blocks, s); break;
+      case 4: launch_tiles_m<GSum<4>>(P, grad, fast, (int)blocks, s); break;
+      case 8: launch_tiles_m<GSum<8>>(P, grad, fast, (int)blocks, s); break;
       default: return fail(ADC_E_ARG, "gsum: unsupported component count");
     }
   }
   ADCB_CUDA(cudaGetLastError());
   const int64_t nchunks = (ntiles + chunk_tiles - 1) / chunk_tiles;
-  chi2_chunk_kernel<<<(unsigned)nchunks, kChunkThreads, 0, s>>>(P.tile_ws, ntiles, R,
-                                                               (int)chunk_tiles, records);
+  const int lin0 = model == ADC_MODEL_GPOLY ? GPoly::LIN0 : np;
+  chi2_chunk_kernel<<<(unsigned)nchunks, kChunkThreads, 0, s>>>(
+      P.tile_ws, ntiles, R, (int)chunk_tiles, records, grad ? lin : nullptr, np, lin0);
   ADCB_CUDA(cudaGetLastError());
   return ADC_OK;
 }
 
-int chi2_multi_enqueue(const Chi2Pass& P, int model, int np, int ncand, int bpt,
+int chi2_lin_count(int model, int np) {
+  return model == ADC_MODEL_GPOLY ? GPoly::NP - GPoly::LIN0 : 0;
+}
+
+int chi2_lin_enqueue(const Chi2Pass& P, int model, int64_t chunk_tiles, double* lin_records,
+                     cudaStream_t s) {
+  const int64_t ntiles = P.tile_end - P.tile_begin;
+  if (ntiles <= 0 || model != ADC_MODEL_GPOLY) return ADC_OK;
+  const int64_t blocks = std::min<int64_t>(ntiles, (int64_t)sm_count() * 4);
+  chi2_lin_kernel<GPoly><<<(unsigned)blocks, kTileThreads, 0, s>>>(P);
+  ADCB_CUDA(cudaGetLastError());
+  const int64_t nchunks = (ntiles + chunk_tiles - 1) / chunk_tiles;
+  const int RL = 2 * (GPoly::NP - GPoly::LIN0);
+  chi2_chunk_kernel<<<(unsigned)nchunks, kChunkThreads, 0, s>>>(P.tile_ws, ntiles, RL,
+                                                               (int)chunk_tiles, lin_records);
+  ADCB_CUDA(cudaGetLastError());
+  return ADC_OK;
+}
+
+int chi2_multi_enqueue(const Chi2Pass& P, int model, int np, int ncand,
                        int64_t chunk_tiles, double* records, cudaStream_t s) {
   const int64_t ntiles = P.tile_end - P.tile_begin;
   if (ntiles <= 0) return ADC_OK;
@@ -457,9 +549,7 @@ int chi2_multi_enqueue(const Chi2Pass& P, int model, int np, int ncand, int bpt,
                   (unsigned)((ncand + kMultiGroup - 1) / kMultiGroup));
   auto go = [&](auto model_tag) {
     using M = decltype(model_tag);
-    if (bpt == 128) chi2_multi_kernel<M, 128><<<grid, kTileThreads, 0, s>>>(P, ncand);
-    else if (bpt == 32) chi2_multi_kernel<M, 32><<<grid, kTileThreads, 0, s>>>(P, ncand);
-    else chi2_multi_kernel<M, 4><<<grid, kTileThreads, 0, s>>>(P, ncand);
+    chi2_multi_kernel<M><<<grid, kTileThreads, 0, s>>>(P, ncand);
   };
   if (model == ADC_MODEL_GPOLY) {
     go(GPoly{});

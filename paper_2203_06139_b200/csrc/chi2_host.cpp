@@ -24,16 +24,26 @@ namespace {
 constexpr int64_t kTileThreads = 256;
 constexpr int64_t kChunkBins = int64_t(1) << 20;  // large histograms: 1 Mi-bin chunks
 
-// Bins per thread per tile: large histograms amortise the per-tile reduction
-// over more bins; small ones keep enough tiles to fill 148 SMs.
+// Bins per thread per tile.  Large histograms amortise the per-tile
+// reduction over ~128 bins per thread and size the tile so the histogram is a
+// whole number of waves of kWaveCtas resident CTAs (2 per SM x 148 SMs on a
+// B200): 1e8 bins -> 132 bins/thread, 2960 tiles = 10 full waves (at 128 the
+// last of 10.3 waves would run 31% full).  Small histograms keep 4 bins per
+// thread so there are enough tiles to fill the GPU.  A pure function of
+// `bins` (not of the device): the same layout on every GPU and world size.
+constexpr int64_t kWaveCtas = 296;
 int bpt_for(int64_t bins) {
-  if (bins >= (int64_t(1) << 24)) return 128;
-  if (bins >= (int64_t(1) << 22)) return 32;
-  return 4;
+  if (bins < (int64_t(1) << 22)) return 4;
+  const int64_t per_wave = kTileThreads * kWaveCtas;
+  int64_t waves = (bins + per_wave * 64) / (per_wave * 128);  // round(bins / (per_wave*128))
+  if (waves < 1) waves = 1;
+  const int64_t bpt = (bins + per_wave * waves * 4 - 1) / (per_wave * waves * 4) * 4;
+  return (int)std::max<int64_t>(4, bpt);
 }
 int64_t chunk_tiles_for(int64_t bins) {
   const int64_t tile = bpt_for(bins) * kTileThreads;
-  return bins >= (int64_t(1) << 22) ? kChunkBins / tile : 128;  // <= 128 (K4 handles 128)
+  if (bins < (int64_t(1) << 22)) return 128;
+  return std::max<int64_t>(1, std::min<int64_t>(128, (kChunkBins + tile / 2) / tile));
 }
 
 }  // namespace
@@ -121,6 +131,9 @@ struct adc_chi2_plan {
   double* records_multi = nullptr;
   double* h_rec_multi = nullptr;
   int64_t multi_passes = 0;
+  // q-independent basis sums of the linear parameters (chi2_lin_enqueue)
+  double* lin = nullptr;
+  bool lin_ready = false;
 };
 
 namespace {
@@ -145,6 +158,7 @@ Chi2Pass make_pass(const adc_chi2_plan* P) {
   pass.lo = P->lo;
   pass.width = P->width;
   pass.bin_end = P->L.bin_end;
+  pass.bpt = (int)(P->L.tile_bins / kTileThreads);
   pass.tile_begin = P->L.chunk_begin * P->L.chunk_tiles;
   pass.tile_end = (P->L.bin_end + P->L.tile_bins - 1) / P->L.tile_bins;
   if (pass.tile_end < pass.tile_begin) pass.tile_end = pass.tile_begin;
@@ -153,12 +167,26 @@ Chi2Pass make_pass(const adc_chi2_plan* P) {
 
 int64_t local_chunks(const adc_chi2_plan* P) { return P->L.chunk_end - P->L.chunk_begin; }
 
+// Once per plan: the linear parameters' q-independent G0/G1 chunk sums.
+int ensure_lin(adc_chi2_plan* P, cudaStream_t s) {
+  if (P->lin_ready) return ADC_OK;
+  const int L = chi2_lin_count(P->model, P->np);
+  if (L > 0) {
+    const int64_t nrec = std::max<int64_t>(1, local_chunks(P));
+    if (P->lin == nullptr) ADCB_CUDA(cudaMalloc(&P->lin, (size_t)nrec * 2 * L * sizeof(double)));
+    if (int rc = chi2_lin_enqueue(make_pass(P), P->model, P->L.chunk_tiles, P->lin, s)) return rc;
+    ADCB_CUDA(cudaStreamSynchronize(s));
+  }
+  P->lin_ready = true;
+  return ADC_OK;
+}
+
 int build_graph(adc_chi2_plan* P, int grad) {
   cudaGraph_t g = nullptr;
   ADCB_CUDA(cudaStreamBeginCapture(P->stream, cudaStreamCaptureModeThreadLocal));
   cudaMemcpyAsync(P->qdev, P->h_q, qdev_bytes(), cudaMemcpyHostToDevice, P->stream);
-  int rc = chi2_enqueue(make_pass(P), P->model, P->np, grad != 0, P->fast != 0, P->bpt,
-                        P->L.chunk_tiles, P->records, P->stream);
+  int rc = chi2_enqueue(make_pass(P), P->model, P->np, grad != 0, P->fast != 0,
+                        P->L.chunk_tiles, P->records, P->stream, P->lin);
   const size_t rec_bytes =
       (size_t)local_chunks(P) * adc_chi2_record_len(P->np, grad) * sizeof(double);
   cudaMemcpyAsync(P->h_rec, P->records, rec_bytes, cudaMemcpyDeviceToHost, P->stream);
@@ -182,6 +210,8 @@ int run_pass(adc_chi2_plan* P, const double* q, int grad) {
   if (int rc = check_domain(P, q)) return rc;
   ADCB_CUDA(cudaSetDevice(P->device));
   fill_qdev(P->model, P->np, q, P->h_q);
+  if (grad)
+    if (int rc = ensure_lin(P, P->stream)) return rc;
   if (P->graph[grad][P->fast] == nullptr)
     if (int rc = build_graph(P, grad)) return rc;
   ADCB_CUDA(cudaGraphLaunch(P->graph[grad][P->fast], P->stream));
@@ -264,6 +294,7 @@ extern "C" int adc_cuda_chi2_plan_destroy(adc_chi2_plan* P) {
   if (P->tile_ws_multi) cudaFree(P->tile_ws_multi);
   if (P->records_multi) cudaFree(P->records_multi);
   if (P->h_rec_multi) cudaFreeHost(P->h_rec_multi);
+  if (P->lin) cudaFree(P->lin);
   if (P->stream) cudaStreamDestroy(P->stream);
   delete P;
   return ADC_OK;
@@ -297,10 +328,12 @@ extern "C" int adc_cuda_chi2_partials(adc_chi2_plan* P, const double* q, int32_t
   cudaStream_t s = P->user_stream;  // the caller's stream (0 = legacy default stream)
   // h_q may still be read by an in-flight copy of a previous pass
   ADCB_CUDA(cudaStreamSynchronize(s));
+  if (want_grad)
+    if (int rc = ensure_lin(P, s)) return rc;
   fill_qdev(P->model, P->np, q, P->h_q);
   ADCB_CUDA(cudaMemcpyAsync(P->qdev, P->h_q, qdev_bytes(), cudaMemcpyHostToDevice, s));
-  return chi2_enqueue(make_pass(P), P->model, P->np, want_grad != 0, P->fast != 0, P->bpt,
-                      P->L.chunk_tiles, records_dev ? records_dev : P->records, s);
+  return chi2_enqueue(make_pass(P), P->model, P->np, want_grad != 0, P->fast != 0,
+                      P->L.chunk_tiles, records_dev ? records_dev : P->records, s, P->lin);
 }
 
 extern "C" int adc_cuda_chi2_gradient(adc_chi2_plan* P, const double* q, double* grad,
@@ -347,7 +380,7 @@ extern "C" int adc_cuda_chi2_multi(adc_chi2_plan* P, const double* qs, int32_t n
   Chi2Pass pass = make_pass(P);
   pass.qdev = P->qmulti;
   pass.tile_ws = P->tile_ws_multi;
-  if (int rc = chi2_multi_enqueue(pass, P->model, P->np, ncand, P->bpt, P->L.chunk_tiles,
+  if (int rc = chi2_multi_enqueue(pass, P->model, P->np, ncand, P->L.chunk_tiles,
                                   P->records_multi, P->stream))
     return rc;
   const int R = 1 + 3 * ncand;

@@ -17,12 +17,19 @@ struct Chi2Pass {
   double* tile_ws;       // [tile_end - tile_begin][R]
   double lo, width;      // Histogram::center = lo + (j + 0.5) * width
   int64_t bin_end;       // one past the last bin this rank reads
+  int bpt;               // bins per thread per tile (multiple of 4)
   int64_t tile_begin, tile_end;
 };
 
-int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast, int bpt,
-                 int64_t chunk_tiles, double* records, cudaStream_t s);
-int chi2_multi_enqueue(const Chi2Pass& P, int model, int np, int ncand, int bpt,
+// lin: per-chunk q-independent basis sums from chi2_lin_enqueue (gradient
+// passes of models with linear parameters; nullptr otherwise).
+int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast,
+                 int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin);
+int chi2_lin_count(int model, int np);  // L: number of linear parameters
+// Writes [G0_lin[L], G1_lin[L]] per local chunk (once per plan); uses P.tile_ws.
+int chi2_lin_enqueue(const Chi2Pass& P, int model, int64_t chunk_tiles, double* lin_records,
+                     cudaStream_t s);
+int chi2_multi_enqueue(const Chi2Pass& P, int model, int np, int ncand,
                        int64_t chunk_tiles, double* records, cudaStream_t s);
 void fill_qdev(int model, int np, const double* q, double* host_qdev);
 size_t qdev_bytes();

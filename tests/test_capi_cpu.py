@@ -114,4 +114,5 @@ def test_chi2_layout_shards_whole_chunks():
                 assert a.chunk_end == b.chunk_begin and a.bin_end == b.bin_begin
                 assert a.bin_end == min(bins, a.chunk_end * chunk_bins)
     L = adc.chi2_layout(10**8)
-    assert L.tile_bins == 32768 and L.chunk_tiles == 32 and L.nchunks == 96
+    # 132 bins per thread: 2960 tiles = 10 full waves of 296 CTAs
+    assert L.tile_bins == 132 * 256 and L.chunk_tiles == 31 and L.nchunks == 96
