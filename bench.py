@@ -414,15 +414,19 @@ def bench_fit_1e6(local, bins=1_000_000):
     eng = adc.FitEngine("gpoly", 6)
     eng.chi2(h, synth.GPOLY_INIT)  # upload + graph capture outside the timing
     eng.chi2_gradient(h, synth.GPOLY_INIT)
-    t0 = time.perf_counter()
-    r = eng.fit(h, synth.GPOLY_INIT, adc.FitOptions(budget=400))
-    dt = time.perf_counter() - t0
-    return {"workload": "chi2 fit, gpoly, 1e6 bins, GD + Armijo (BASELINE configs[2])",
-            "fit_seconds": dt, "iterations": r.iterations, "fit_iterations_per_s": r.iterations / dt,
-            "gradient_evals": r.gradient_evals, "chi2_evals": r.chi2_evals,
-            "passes_per_s": (r.gradient_evals + r.chi2_evals) / dt,
-            "gradient_ms_avg": r.gradient_wall_ns / max(1, r.gradient_evals) / 1e6,
-            "converged": r.converged, "params": [round(v, 6) for v in r.params]}
+    eng.fit(h, synth.GPOLY_INIT, adc.FitOptions(budget=2, use_hessian=True))
+    out = {"workload": "chi2 fit, gpoly, 1e6 bins, fit loop of fit.cpp:315-425 (BASELINE configs[2])"}
+    for name, hess in (("gd_armijo", False), ("newton_numeric_hessian", True)):
+        t0 = time.perf_counter()
+        r = eng.fit(h, synth.GPOLY_INIT, adc.FitOptions(budget=400, use_hessian=hess))
+        dt = time.perf_counter() - t0
+        out[name] = {"fit_seconds": dt, "iterations": r.iterations,
+                     "fit_iterations_per_s": r.iterations / dt,
+                     "gradient_evals": r.gradient_evals, "chi2_trials": r.chi2_evals,
+                     "gradient_ms_avg": r.gradient_wall_ns / max(1, r.gradient_evals) / 1e6,
+                     "converged": r.converged, "chi2": r.chi2,
+                     "mu_sigma": [round(r.params[1], 6), round(r.params[2], 6)]}
+    return out
 
 
 def bench_points_small(local, workload, steps=20, warm=3):

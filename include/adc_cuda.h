@@ -164,6 +164,12 @@ int adc_cuda_chi2(adc_chi2_plan* plan, const double* q, double* chi2);
  * vector.  The fit loop uses it to evaluate the Armijo trials t = 1, 1/2, ...
  * of fit.cpp:390-403 in batches.  Single device. */
 int adc_cuda_chi2_multi(adc_chi2_plan* plan, const double* qs, int32_t ncand, double* chi2s);
+/* Gradients (and nothing else) of ncand (<= 32) parameter vectors: ncand
+ * ordinary gradient passes enqueued back to back, one copy back, one sync;
+ * each result equals adc_cuda_chi2_gradient on that vector.  Used for the
+ * 2*np central-difference probes of the Newton option.  Single device. */
+int adc_cuda_chi2_gradient_multi(adc_chi2_plan* plan, const double* qs, int32_t ncand,
+                                 double* grads);
 /* Selects per-bin arithmetic: 0 = faithful (IEEE divisions exactly as the
  * generated code), 1 = fast (reciprocal multiplies; within the reduction
  * tolerance).  Default 1. */

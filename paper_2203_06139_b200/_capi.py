@@ -80,6 +80,7 @@ SIGNATURES = {
     "adc_cuda_chi2_gradient": (ctypes.c_int, [_VP, _D, _D, _D]),
     "adc_cuda_chi2": (ctypes.c_int, [_VP, _D, _D]),
     "adc_cuda_chi2_multi": (ctypes.c_int, [_VP, _D, _I32, _D]),
+    "adc_cuda_chi2_gradient_multi": (ctypes.c_int, [_VP, _D, _I32, _D]),
     "adc_cuda_chi2_set_precision": (ctypes.c_int, [_VP, _I32]),
     "adc_fit_default_options": (None, [ctypes.POINTER(FitOptions)]),
     "adc_cuda_fit": (ctypes.c_int, [_VP, _D, ctypes.POINTER(_I32), _I32,

@@ -131,6 +131,8 @@ struct adc_chi2_plan {
   double* records_multi = nullptr;
   double* h_rec_multi = nullptr;
   int64_t multi_passes = 0;
+  double* grad_multi_records = nullptr;  // adc_cuda_chi2_gradient_multi
+  double* h_grad_multi = nullptr;
   // q-independent basis sums of the linear parameters (chi2_lin_enqueue)
   double* lin = nullptr;
   bool lin_ready = false;
@@ -295,6 +297,8 @@ extern "C" int adc_cuda_chi2_plan_destroy(adc_chi2_plan* P) {
   if (P->records_multi) cudaFree(P->records_multi);
   if (P->h_rec_multi) cudaFreeHost(P->h_rec_multi);
   if (P->lin) cudaFree(P->lin);
+  if (P->grad_multi_records) cudaFree(P->grad_multi_records);
+  if (P->h_grad_multi) cudaFreeHost(P->h_grad_multi);
   if (P->stream) cudaStreamDestroy(P->stream);
   delete P;
   return ADC_OK;
@@ -406,6 +410,52 @@ extern "C" int adc_cuda_chi2_multi(adc_chi2_plan* P, const double* qs, int32_t n
   return ADC_OK;
 }
 
+extern "C" int adc_cuda_chi2_gradient_multi(adc_chi2_plan* P, const double* qs, int32_t ncand,
+                                            double* grads) {
+  clear_error();
+  if (P == nullptr || qs == nullptr || grads == nullptr) return fail(ADC_E_ARG, "null argument");
+  if (ncand < 1 || ncand > kMultiMax) return fail(ADC_E_ARG, "gradient multi: 1..32 candidates");
+  if (P->L.chunk_begin != 0 || P->L.chunk_end != P->L.nchunks)
+    return fail(ADC_E_ARG, "sharded plan: multi pass is single-device");
+  for (int k = 0; k < ncand; ++k)
+    if (int rc = check_domain(P, qs + (size_t)k * P->np)) return rc;
+  ADCB_CUDA(cudaSetDevice(P->device));
+  if (int rc = ensure_lin(P, P->stream)) return rc;
+  const size_t qb = qdev_bytes();
+  const int R = adc_chi2_record_len(P->np, 1);
+  const size_t per = (size_t)P->L.nchunks * R;
+  if (P->qmulti == nullptr) {
+    // same lazily allocated buffers as the multi value pass
+    double c2[1];
+    if (int rc = adc_cuda_chi2_multi(P, qs, 1, c2)) return rc;
+  }
+  if (P->grad_multi_records == nullptr) {
+    ADCB_CUDA(cudaMalloc(&P->grad_multi_records, per * kMultiMax * sizeof(double)));
+    ADCB_CUDA(cudaMallocHost(&P->h_grad_multi, per * kMultiMax * sizeof(double)));
+  }
+  for (int k = 0; k < ncand; ++k)
+    fill_qdev(P->model, P->np, qs + (size_t)k * P->np,
+              reinterpret_cast<double*>(reinterpret_cast<char*>(P->h_qmulti) + k * qb));
+  ADCB_CUDA(cudaMemcpyAsync(P->qmulti, P->h_qmulti, qb * ncand, cudaMemcpyHostToDevice, P->stream));
+  // ncand ordinary gradient passes back to back on one stream (each identical
+  // to adc_cuda_chi2_gradient), one copy back and one synchronisation.
+  for (int k = 0; k < ncand; ++k) {
+    Chi2Pass pass = make_pass(P);
+    pass.qdev = reinterpret_cast<const double*>(reinterpret_cast<const char*>(P->qmulti) + k * qb);
+    if (int rc = chi2_enqueue(pass, P->model, P->np, true, P->fast != 0, P->L.chunk_tiles,
+                              P->grad_multi_records + per * k, P->stream, P->lin))
+      return rc;
+  }
+  ADCB_CUDA(cudaMemcpyAsync(P->h_grad_multi, P->grad_multi_records, per * ncand * sizeof(double),
+                            cudaMemcpyDeviceToHost, P->stream));
+  ADCB_CUDA(cudaStreamSynchronize(P->stream));
+  for (int k = 0; k < ncand; ++k)
+    if (int rc = adc_chi2_finalize(P->np, P->events, P->h_grad_multi + per * k, P->L.nchunks, 1,
+                                   grads + (size_t)k * P->np, nullptr))
+      return rc;
+  return ADC_OK;
+}
+
 // ---------------------------------------------------------------------------
 // Fit loop: FitEngine::fit (fit.cpp:315-425), steepest descent with Armijo
 // backtracking, generalised sigma clamp (fit.cpp:268-278 hard-codes every
@@ -500,20 +550,32 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
     std::vector<double> direction = g;
     if (opts->use_hessian) {
       // Central differences of the gradient, 2*np extra passes (fit.cpp:346-381).
-      std::vector<double> hess((size_t)np * np, 0.0), gp(np), gm(np), probe = q;
+      // All 2*np probes go to the device in one batch (adc_cuda_chi2_gradient_multi);
+      // each probe's gradient is the one adc_cuda_chi2_gradient returns.
+      std::vector<double> hess((size_t)np * np, 0.0), probes((size_t)2 * np * np),
+          pg((size_t)2 * np * np), steps(np);
       for (int c = 0; c < np; ++c) {
-        const double x = probe[c];
-        const double step = std::cbrt(2.220446049250313e-16) * std::max(1.0, std::fabs(x));
-        const auto h0 = clk::now();
-        probe[c] = x + step;
-        if (int rc = adc_cuda_chi2_gradient(P, probe.data(), gp.data(), nullptr)) return rc;
-        probe[c] = x - step;
-        if (int rc = adc_cuda_chi2_gradient(P, probe.data(), gm.data(), nullptr)) return rc;
-        res.gradient_ns += (uint64_t)std::chrono::nanoseconds(clk::now() - h0).count();
-        res.gradient_evals += 2;
-        probe[c] = x;
-        for (int r = 0; r < np; ++r) hess[(size_t)r * np + c] = (gp[r] - gm[r]) / (2.0 * step);
+        const double x = q[c];
+        steps[c] = std::cbrt(2.220446049250313e-16) * std::max(1.0, std::fabs(x));
+        for (int s2 = 0; s2 < 2; ++s2) {
+          double* pr = &probes[(size_t)(2 * c + s2) * np];
+          std::memcpy(pr, q.data(), np * sizeof(double));
+          pr[c] = s2 == 0 ? x + steps[c] : x - steps[c];
+        }
       }
+      const auto h0 = clk::now();
+      for (int b = 0; b < 2 * np; b += kMultiMax) {
+        const int nb = std::min(kMultiMax, 2 * np - b);
+        if (int rc = adc_cuda_chi2_gradient_multi(P, &probes[(size_t)b * np], nb,
+                                                  &pg[(size_t)b * np]))
+          return rc;
+      }
+      res.gradient_ns += (uint64_t)std::chrono::nanoseconds(clk::now() - h0).count();
+      res.gradient_evals += 2 * np;
+      for (int c = 0; c < np; ++c)
+        for (int r = 0; r < np; ++r)
+          hess[(size_t)r * np + c] =
+              (pg[(size_t)(2 * c) * np + r] - pg[(size_t)(2 * c + 1) * np + r]) / (2.0 * steps[c]);
       double lambda = 0.0;
       bool ok = false;
       for (int attempt = 0; attempt < 10 && !ok; ++attempt) {

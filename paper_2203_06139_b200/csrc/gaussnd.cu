@@ -25,7 +25,7 @@
 
 namespace adcb {
 
-template <int W, int U, int PF>
+template <int W, int U, int PF, int PFD = 1>
 __global__ void __launch_bounds__(W * 32) gaussnd_tile_kernel(
     const double* __restrict__ x, const double* __restrict__ p, double* __restrict__ dx,
     double* __restrict__ dp, int64_t n, int dim, int64_t ld, double t4, double r1, int dpw,
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(W * 32) gaussnd_tile_kernel(
           // reverse sweep will read (dx, dp at the top of the range)
 #pragma unroll
           for (int k = 0; k < U; ++k) {
-            const int dn = d + U + k;
+            const int dn = d + U * PFD + k;
             if (dn < d1) {
               prefetch_l2(xi + (int64_t)dn * ld);
               prefetch_l2(pi + (int64_t)dn * ld);
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(W * 32) gaussnd_tile_kernel(
           const int64_t inext = i + (int64_t)gridDim.x * 32;
 #pragma unroll
           for (int k = 0; k < U; ++k) {
-            const int dn = d - 1 - U - k;
+            const int dn = d - 1 - U * PFD - k;
             if (dn >= d0) {
               prefetch_l2(dxi + (int64_t)dn * ld);
               prefetch_l2(dpi + (int64_t)dn * ld);
@@ -209,7 +209,8 @@ __global__ void __launch_bounds__(W * 32) gaussnd_tile_kernel(
 // 0 auto; 1/3/4 = one warp per 32-point tile (reference summation order) with
 // 8/16/32 rows in flight per thread (+ L2 prefetch of the next batch);
 // 5 = as 3 without prefetch; 6 = as 3 with bulk (TMA-unit) prefetch;
-// 2 = dims split over the warps of a CTA (7 = same with bulk prefetch).
+// 2 = dims split over the warps of a CTA (7 = same with bulk prefetch);
+// 8 = as 3 prefetching two batches ahead, 9 = U=8 prefetching three ahead.
 static int g_variant = 0;
 
 struct NdConfig {
@@ -217,11 +218,11 @@ struct NdConfig {
   size_t smem;
 };
 
-template <int W, int U, int PF = 1>
+template <int W, int U, int PF = 1, int PFD = 1>
 static int launch_tile(const NdConfig& c, int64_t n, int dim, int64_t ld, const double* x,
                        const double* p, double* dx, double* dp, double t4, double r1,
                        cudaStream_t s) {
-  auto k = gaussnd_tile_kernel<W, U, PF>;
+  auto k = gaussnd_tile_kernel<W, U, PF, PFD>;
   if (c.smem > 48 * 1024)
     ADCB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem));
   int occ = 0;
@@ -243,6 +244,7 @@ static NdConfig choose(int dim) {
   // W = 1 keeps the reference's summation order; it needs the whole u row of
   // a point on chip: 256 B per dim per warp.  Use it while >= 8 warps fit.
   if (variant == 1 || variant == 3 || variant == 4 || variant == 5 || variant == 6 ||
+      variant == 8 || variant == 9 ||
       (variant == 0 && (size_t)dim * 256 * 8 <= kSmemPerSm)) {
     c.w = 1;
     c.dpw = dim;
@@ -256,7 +258,7 @@ static NdConfig choose(int dim) {
     const size_t avail = per_cta - (size_t)c.w * 32 * 8 - 1024;
     c.dstage = std::min<int>(c.dpw, (int)(avail / ((size_t)c.w * 256)));
   }
-  c.u = variant == 1 ? 8 : variant == 4 ? 32 : 16;
+  c.u = (variant == 1 || variant == 9) ? 8 : variant == 4 ? 32 : 16;
   if (c.w > 1) c.u = 8;
   c.smem = ((size_t)c.w * 32 + (size_t)c.w * c.dstage * 32) * sizeof(double);
   return c;
@@ -283,6 +285,10 @@ int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, con
         return launch_tile<1, 16, 0>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
       if (g_variant == 6)
         return launch_tile<1, 16, 2>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+      if (g_variant == 8)
+        return launch_tile<1, 16, 1, 2>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+      if (g_variant == 9)
+        return launch_tile<1, 8, 1, 3>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
       return launch_tile<1, 16>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
     case 8: return launch_tile<8, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
     case 16:
@@ -293,7 +299,7 @@ int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, con
 }
 
 int gaussnd_set_variant(int v) {
-  if (v < 0 || v > 7) return fail(ADC_E_ARG, "gaussnd variant must be 0..7");
+  if (v < 0 || v > 9) return fail(ADC_E_ARG, "gaussnd variant must be 0..9");
   g_variant = v;
   return ADC_OK;
 }

@@ -127,6 +127,15 @@ class Chi2Plan:
                                       out.ctypes.data_as(dp)))
         return out
 
+    def gradient_multi(self, qs) -> np.ndarray:
+        """Gradients of several parameter vectors, one sync (each equals gradient())."""
+        qs = np.ascontiguousarray(qs, dtype=np.float64).reshape(-1, self.np)
+        out = np.zeros_like(qs)
+        dp = ctypes.POINTER(ctypes.c_double)
+        check(lib.adc_cuda_chi2_gradient_multi(self._p, qs.ctypes.data_as(dp), qs.shape[0],
+                                               out.ctypes.data_as(dp)))
+        return out
+
     def partials(self, q, want_grad: bool, records_dev=None):
         """Enqueue this rank's pass; records land in records_dev (a float64 CUDA
         tensor of local_chunks * record_len) or the plan's own buffer."""

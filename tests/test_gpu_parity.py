@@ -114,7 +114,7 @@ def test_listing1_domain_error():
 ND_KEYS = ["d100_n64", "d1000_n8", "d1_n33", "d37_n70", "d128_n40", "d129_n5"]
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9])
 @pytest.mark.parametrize("key", ND_KEYS)
 def test_gaussnd_golden(key, variant):
     g = golden("gaussnd_cases.npz")
@@ -282,6 +282,9 @@ def test_chi2_multi_bitwise_equals_single():
         single = np.array([pl.chi2(qk) for qk in qs])
         assert np.array_equal(multi, single), bins
         assert np.array_equal(pl.chi2_multi(qs[:5]), single[:5])
+        gm = pl.gradient_multi(qs[:12])
+        for k in range(12):
+            assert np.array_equal(gm[k], pl.gradient(qs[k])[0]), (bins, k)
 
 
 def test_fit_1e6_newton_converges_to_truth():
