@@ -331,30 +331,39 @@ __global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P,
     double acc[3 * G + 1];
 #pragma unroll
     for (int v = 0; v < 3 * G + 1; ++v) acc[v] = 0.0;
-    double jh = fadd((double)base, 0.5);
-    for (int k = 0; k < BPT; ++k) {
-      const int64_t j = base + (int64_t)k * kTileThreads;
-      if (j < P.bin_end) {
-        const double c = ld_stream(P.counts + j);
-        const double x = fadd(P.lo, fmul(jh, P.width));
-        const bool pos = c > 0.0;
-        const double w = pos ? 1.0 : 0.0;
-        const double ic = pos ? rcp_pos(c) : 0.0;
-        acc[3 * G] += c;
+    // Candidates outer, bins inner: each candidate's parameters stay in
+    // registers for the whole tile; the counts are re-read from L1.  Per
+    // candidate the bin order and the accumulation expressions are those of
+    // the single value pass (tile_bins / bin_term / bin_accumulate).
 #pragma unroll
-        for (int cnd = 0; cnd < G; ++cnd) {
-          if (cnd < ng) {
-            const typename M::Reg QR = M::load(Q[cnd]);
+    for (int cnd = 0; cnd < G; ++cnd) {
+      if (cnd < ng) {
+        const typename M::Reg QR = M::load(Q[cnd]);
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, c0 = 0.0;
+        double jh = fadd((double)base, 0.5);
+        for (int k = 0; k < BPT; ++k) {
+          const int64_t j = base + (int64_t)k * kTileThreads;
+          if (j < P.bin_end) {
+            const double c = P.counts[j];
+            const double x = fadd(P.lo, fmul(jh, P.width));
+            const bool pos = c > 0.0;
+            const double w = pos ? 1.0 : 0.0;
+            const double ic = pos ? rcp_pos(c) : 0.0;
             double m, bg[1];
             M::template eval<false, true>(x, QR, tab, m, bg);
             const double mc = m * ic;
-            acc[3 * cnd] += m;
-            acc[3 * cnd + 1] = __fma_rn(w, m, acc[3 * cnd + 1]);
-            acc[3 * cnd + 2] = __fma_rn(m, mc, acc[3 * cnd + 2]);
+            a0 += m;
+            a1 = __fma_rn(w, m, a1);
+            a2 = __fma_rn(m, mc, a2);
+            if (cnd == 0) c0 += c;
           }
+          jh = fadd(jh, (double)kTileThreads);
         }
+        acc[3 * cnd] = a0;
+        acc[3 * cnd + 1] = a1;
+        acc[3 * cnd + 2] = a2;
+        if (cnd == 0) acc[3 * G] = c0;
       }
-      jh = fadd(jh, (double)kTileThreads);
     }
 #pragma unroll
     for (int v = 0; v < 3 * G + 1; ++v) {

@@ -33,8 +33,8 @@ constexpr int64_t kChunkBins = int64_t(1) << 20;  // large histograms: 1 Mi-bin 
 // `bins` (not of the device): the same layout on every GPU and world size.
 constexpr int64_t kWaveCtas = 296;
 int bpt_for(int64_t bins) {
-  if (bins < (int64_t(1) << 22)) return 4;
   const int64_t per_wave = kTileThreads * kWaveCtas;
+  if (bins < per_wave * 8) return 4;  // < 606K bins: keep tiles small enough to fill the GPU
   int64_t waves = (bins + per_wave * 64) / (per_wave * 128);  // round(bins / (per_wave*128))
   if (waves < 1) waves = 1;
   const int64_t bpt = (bins + per_wave * waves * 4 - 1) / (per_wave * waves * 4) * 4;
@@ -42,7 +42,7 @@ int bpt_for(int64_t bins) {
 }
 int64_t chunk_tiles_for(int64_t bins) {
   const int64_t tile = bpt_for(bins) * kTileThreads;
-  if (bins < (int64_t(1) << 22)) return 128;
+  if (bpt_for(bins) == 4) return 128;
   return std::max<int64_t>(1, std::min<int64_t>(128, (kChunkBins + tile / 2) / tile));
 }
 

@@ -81,11 +81,11 @@ def test_chi2_two_ranks_gloo_bitwise(restate):
     sys.path.insert(0, ROOT)
     import paper_2203_06139_b200 as adc
     from paper_2203_06139_b200 import synth
-    bins = 3 * (1 << 20) + 12345            # 25 chunks of 128 Ki bins (the last partial)
+    bins = 5 * (1 << 20) + 123              # 5 chunks of ~1 Mi bins (the last partial)
     counts, ev = synth.histogram(bins, events=2e8, seed=3)
     q = np.array(synth.GPOLY_INIT)
     L = adc.chi2_layout(bins)
-    assert L.nchunks == 25  # odd: the two ranks own 12 and 13 chunks
+    assert L.nchunks == 5  # odd: the two ranks own 2 and 3 chunks
     g1, c1 = adc.finalize(6, ev, chunk_records(counts, -5.0, 5.0, q, L, 0, L.nchunks), True)
     ctx = mp.get_context("spawn")
     out_q = ctx.Queue()
