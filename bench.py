@@ -298,7 +298,18 @@ def bench_points(a, world, rank, local, dist):
     del dx, dp
     # ---- e2e: public API with pinned HOST buffers, H2D + D2H inside the timing
     e2e = None
-    if not a.no_e2e:
+    need = 4 * 8 * npts * dim  # pinned host bytes per rank
+    avail = None
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        pass
+    if not a.no_e2e and avail is not None and avail < 1.25 * need * world:
+        e2e = {"value": None, "unit": "pt*param/s",
+               "skipped": f"host RAM {avail / 1e9:.0f} GB < {1.25 * need * world / 1e9:.0f} GB "
+                          f"needed to pin {world} x {need / 1e9:.0f} GB"}
+    elif not a.no_e2e:
         hx = torch.empty(x.shape, dtype=torch.float64, pin_memory=True)
         hp = torch.empty(x.shape, dtype=torch.float64, pin_memory=True)
         hx.copy_(x)
