@@ -9,7 +9,8 @@ inputs resident in HBM (32 GB per GPU > the 126 MB L2, so no flush is needed
 between steps).  A step = one launch of gaussnd_grad_0_1 over all points of
 the rank.  Multi-GPU: points are independent, each rank owns its own 10M
 points (weak scaling), no collective on the data path; the chi2 secondary
-line does one all_gather of the chunk records per gradient.
+line does one all-gather of the chunk records per gradient, inside the library
+(NCCL in the pass graph).
 
 Rank 0 prints ONE JSON line.  `--impl reference` times the reference's own
 CPU implementation (oracle/_ref/ref_tool over the unmodified reference
@@ -363,31 +364,18 @@ def bench_chi2(world, rank, local, dist, bins=100_000_000, passes=20, warm=3):
     events = float(counts.sum())
     h = adc.Histogram(bins, -5.0, 5.0, events, counts)
     q = list(synth.GPOLY_INIT)
-    plan = adc.Chi2Plan("gpoly", 6, h, world=world, rank=rank)
+    # N > 1: the library's own communicator (NCCL over NVLink; the host
+    # transport over the process group for --dist-backend gloo).  The pass,
+    # the record all-gather and the fixed-order finalize run inside
+    # libadc_b200, captured in one CUDA graph per pass kind.
+    comm = adc.Comm.from_torch("nccl" if BACKEND == "nccl" else "host") if world > 1 else None
+    plan = adc.Chi2Plan("gpoly", 6, h, comm=comm)
     L = plan.layout
     R = adc.record_len(6, True)
-    nloc = L.chunk_end - L.chunk_begin
-    per = (L.nchunks + world - 1) // world
-    loc = torch.zeros(per * R, dtype=torch.float64, device=dev)
-    allr = torch.zeros(world * per * R, dtype=torch.float64, device=dev)
-    counts_by_rank = [((L.nchunks * (r + 1)) // world - (L.nchunks * r) // world)
-                      for r in range(world)]
+    loc = torch.zeros(max(1, L.chunk_end - L.chunk_begin) * R, dtype=torch.float64, device=dev)
 
     def one_pass():
-        plan.partials(q, True, loc)
-        if dist is not None:
-            torch.cuda.synchronize()
-            if BACKEND == "nccl":
-                dist.all_gather_into_tensor(allr, loc)   # the one exchange step (NVLink)
-                host = allr.cpu().numpy().reshape(world, per * R)
-            else:
-                parts = [torch.zeros(per * R, dtype=torch.float64) for _ in range(world)]
-                dist.all_gather(parts, loc.cpu())
-                host = torch.stack(parts).numpy()
-            rec = np.concatenate([host[r, :counts_by_rank[r] * R] for r in range(world)])
-        else:
-            rec = loc.cpu().numpy()[:nloc * R]
-        return adc.finalize(6, events, rec, True)
+        return plan.gradient(q)
 
     for _ in range(warm):
         one_pass()
@@ -408,9 +396,13 @@ def bench_chi2(world, rank, local, dist, bins=100_000_000, passes=20, warm=3):
            "passes_per_s": 1.0 / dt, "ms_per_pass": dt * 1e3,
            "device_ms_per_rank_pass": statistics.median(kt),
            "bins_per_s_device": (L.bin_end - L.bin_begin) / (statistics.median(kt) * 1e-3),
-           "collective": "all_gather of chunk records" if world > 1 else "none",
+           "collective": ("all-gather of chunk records inside libadc_b200 ("
+                          + ("ncclAllGather in the pass graph" if BACKEND == "nccl"
+                             else "host transport over gloo") + ")") if world > 1 else "none",
            "chi2": c2}
     plan.close()
+    if comm is not None:
+        comm.close()
     return out
 
 

@@ -34,7 +34,8 @@ typedef enum adc_status {
   ADC_E_LAUNCH = 4,    /* ErrorKind::Launch: config, refusal, buffer binding */
   ADC_E_IO = 5,        /* ErrorKind::Io */
   ADC_E_CUDA = 6,      /* CUDA runtime failure / no device */
-  ADC_E_ARG = 7        /* invalid argument to the C ABI itself */
+  ADC_E_ARG = 7,       /* invalid argument to the C ABI itself */
+  ADC_E_NCCL = 8       /* NCCL failure in the multi-GPU exchange */
 } adc_status;
 
 int adc_cuda_abi_version(void);
@@ -155,25 +156,69 @@ int adc_cuda_chi2_plan_layout(const adc_chi2_plan* plan, adc_chi2_layout* out);
 int adc_cuda_chi2_partials(adc_chi2_plan* plan, const double* q, int32_t want_grad,
                            double* records_dev);
 double* adc_cuda_chi2_plan_records(adc_chi2_plan* plan);
-/* Single-device convenience (world == 1): pass + D2H + finalize, synchronous.
+/* Pass + exchange + finalize, synchronous: whole-histogram plans, or sharded
+ * plans with a communicator attached (adc_cuda_chi2_plan_set_comm).
  * FitEngine::chi2_gradient(h, q, AdReverse, out) and FitEngine::chi2(h, q). */
 int adc_cuda_chi2_gradient(adc_chi2_plan* plan, const double* q, double* grad, double* chi2);
 int adc_cuda_chi2(adc_chi2_plan* plan, const double* q, double* chi2);
 /* chi2 of ncand (<= 32) parameter vectors qs[ncand][np] in ONE pass over the
  * bins (fast mode): each result is bit-identical to adc_cuda_chi2 on that
  * vector.  The fit loop uses it to evaluate the Armijo trials t = 1, 1/2, ...
- * of fit.cpp:390-403 in batches.  Single device. */
+ * of fit.cpp:390-403 in batches.  Sharded plans need a communicator. */
 int adc_cuda_chi2_multi(adc_chi2_plan* plan, const double* qs, int32_t ncand, double* chi2s);
 /* Gradients (and nothing else) of ncand (<= 32) parameter vectors: ncand
  * ordinary gradient passes enqueued back to back, one copy back, one sync;
  * each result equals adc_cuda_chi2_gradient on that vector.  Used for the
- * 2*np central-difference probes of the Newton option.  Single device. */
+ * 2*np central-difference probes of the Newton option.  Sharded plans need a
+ * communicator. */
 int adc_cuda_chi2_gradient_multi(adc_chi2_plan* plan, const double* qs, int32_t ncand,
                                  double* grads);
 /* Selects per-bin arithmetic: 0 = faithful (IEEE divisions exactly as the
  * generated code), 1 = fast (reciprocal multiplies; within the reduction
  * tolerance).  Default 1. */
 int adc_cuda_chi2_set_precision(adc_chi2_plan* plan, int32_t mode);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU exchange.  One process per GPU; each rank's plan
+ * covers a contiguous range of whole chunks (adc_chi2_make_layout) and the one
+ * exchange step of every pass is an all-gather of the chunk records (<= 32 KB
+ * at 1e8 bins), after which every rank runs the same fixed-order finalize.
+ * The result is therefore bitwise identical on every rank and for every world
+ * size.  With a communicator attached, every plan entry point below
+ * (adc_cuda_chi2, _gradient, _multi, _gradient_multi, adc_cuda_fit) works on
+ * a sharded plan exactly as on a whole-histogram plan.
+ *
+ * Two transports:
+ *  - NCCL (the product path on NVLink/NVSwitch): ncclAllGather enqueued on the
+ *    plan's stream right after the chunk kernel, captured into the same CUDA
+ *    graph as the pass.  Rank 0 calls adc_nccl_unique_id and the caller
+ *    distributes the 128 bytes (MPI, torch.distributed, a file, ...).
+ *  - host callback: the caller's own all-gather over host memory (MPI_Allgather,
+ *    gloo, ...): fn(ctx, send, recv, bytes) must place every rank's `bytes`
+ *    bytes at recv + rank * bytes and return 0.  Used to run several ranks on
+ *    one GPU in tests.
+ */
+typedef struct adc_comm adc_comm;
+typedef int (*adc_allgather_fn)(void* ctx, const void* send, void* recv, size_t bytes);
+enum { ADC_COMM_NCCL = 1, ADC_COMM_HOST = 2 };
+int adc_nccl_unique_id(unsigned char id[128]);
+/* Collective over the world: every rank calls it with the same id, on the
+ * device it will run its plan on (the current device). */
+int adc_cuda_comm_init_nccl(adc_comm** comm, const unsigned char id[128], int32_t world,
+                            int32_t rank);
+int adc_comm_init_host(adc_comm** comm, int32_t world, int32_t rank, adc_allgather_fn fn,
+                       void* ctx);
+int adc_comm_destroy(adc_comm* comm);
+int adc_comm_info(const adc_comm* comm, int32_t* world, int32_t* rank, int32_t* kind);
+/* Attaches comm (NULL detaches) to a plan created with the same world/rank.
+ * The plan does not own the communicator. */
+int adc_cuda_chi2_plan_set_comm(adc_chi2_plan* plan, adc_comm* comm);
+/* One call for a rank that holds only its own shard: world/rank come from
+ * comm, shard_counts is a DEVICE pointer to counts[bin_begin, bin_end) of the
+ * layout adc_chi2_make_layout(bins, world, rank) gives, and comm is attached. */
+int adc_cuda_chi2_plan_create_sharded(adc_chi2_plan** plan, int32_t model, int32_t np,
+                                      int64_t bins, double lo, double hi, double events,
+                                      const double* shard_counts, adc_comm* comm, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Fit loop (FitEngine::fit, proj/src/fit.cpp:315-425: steepest descent or the
@@ -204,7 +249,8 @@ typedef struct adc_fit_result {
 
 void adc_fit_default_options(adc_fit_options* o);
 /* params: in = init (np), out = final.  iterates: trace_iterates * np doubles
- * (or NULL).  Single device. */
+ * (or NULL).  Single device, or every rank of a sharded plan with a
+ * communicator attached (all ranks take the same steps). */
 int adc_cuda_fit(adc_chi2_plan* plan, double* params, const int32_t* clamp_idx, int32_t nclamp,
                  const adc_fit_options* opts, adc_fit_result* result, double* iterates);
 

@@ -8,11 +8,12 @@ built library raises: there is no CPU fallback.
 from ._capi import AdcError, LIB_PATH, lib  # noqa: F401
 from .launch import (BufferSet, LaunchConfig, LaunchOptions, LaunchStats, launch,  # noqa: F401
                      launch_batch, registry_find)
+from .comm import Comm  # noqa: F401
 from .fit import (Chi2Plan, FitEngine, FitOptions, FitResult, Histogram, chi2_layout,  # noqa: F401
                   finalize, record_len)
 
 __all__ = [
-    "AdcError", "BufferSet", "LaunchConfig", "LaunchOptions", "LaunchStats", "launch",
+    "AdcError", "BufferSet", "Comm", "LaunchConfig", "LaunchOptions", "LaunchStats", "launch",
     "launch_batch", "registry_find", "Chi2Plan", "FitEngine", "FitOptions", "FitResult",
     "Histogram", "chi2_layout", "finalize", "record_len",
 ]

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "chi2_internal.h"
+#include "comm_internal.h"
 #include "common.cuh"
 
 using namespace adcb;
@@ -113,6 +114,8 @@ struct adc_chi2_plan {
   double lo = 0, hi = 0, events = 0, width = 0;
   const double* counts = nullptr;
   adc_chi2_layout L{};
+  int world = 1, rank = 0;
+  int64_t maxc = 1;  // max chunks per rank: the padded per-rank record stride
   int bpt = 4;
   int fast = 1;
   int device = 0;
@@ -120,19 +123,24 @@ struct adc_chi2_plan {
   cudaStream_t user_stream = nullptr;  // caller's (0 = legacy default): adc_cuda_chi2_partials
   double* qdev = nullptr;
   double* tile_ws = nullptr;
-  double* records = nullptr;
+  double* records = nullptr;  // [maxc][R] (gradient / value pass)
   double* h_q = nullptr;
-  double* h_rec = nullptr;
   cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [grad][fast]
+  bool warm[2][2] = {{false, false}, {false, false}};  // one eager pass before capture
+  // exchange / copy-back staging, sized once for the largest pass kind
+  adc_comm* comm = nullptr;
+  size_t xcount = 0;          // doubles per rank the staging holds
+  double* gather = nullptr;   // device [world][xcount] (NCCL)
+  double* h_send = nullptr;   // pinned [xcount]  (host transport / single device)
+  double* h_gather = nullptr; // pinned [world][xcount]
+  std::vector<double> full;   // compacted [nb][nchunks][R]
   // batched line search (adc_cuda_chi2_multi): lazily allocated
   double* qmulti = nullptr;     // device [kMultiMax][QDev]
   double* h_qmulti = nullptr;   // pinned
   double* tile_ws_multi = nullptr;
-  double* records_multi = nullptr;
-  double* h_rec_multi = nullptr;
+  double* records_multi = nullptr;  // [maxc][1 + 3 kMultiMax]
   int64_t multi_passes = 0;
-  double* grad_multi_records = nullptr;  // adc_cuda_chi2_gradient_multi
-  double* h_grad_multi = nullptr;
+  double* grad_multi_records = nullptr;  // [kMultiMax][maxc][R] (adc_cuda_chi2_gradient_multi)
   // q-independent basis sums of the linear parameters (chi2_lin_enqueue)
   double* lin = nullptr;
   bool lin_ready = false;
@@ -169,6 +177,62 @@ Chi2Pass make_pass(const adc_chi2_plan* P) {
 
 int64_t local_chunks(const adc_chi2_plan* P) { return P->L.chunk_end - P->L.chunk_begin; }
 
+bool sharded(const adc_chi2_plan* P) {
+  return P->L.chunk_begin != 0 || P->L.chunk_end != P->L.nchunks;
+}
+
+int require_whole_or_comm(const adc_chi2_plan* P) {
+  if (sharded(P) && P->comm == nullptr)
+    return fail(ADC_E_ARG,
+                "sharded plan: attach a communicator (adc_cuda_chi2_plan_set_comm) or use "
+                "adc_cuda_chi2_partials + adc_chi2_finalize");
+  return ADC_OK;
+}
+
+// ---- exchange -----------------------------------------------------------------
+// A pass leaves nb blocks of records on the device, block b at
+// dev + b * maxc * R, each holding this rank's local chunks (padded to maxc).
+// collect_enqueue puts them (all ranks' for NCCL) into pinned host memory on
+// stream s; after the stream is synchronised, collect_finish runs the host
+// transport (if any) and compacts to P->full = [nb][nchunks][R] in global
+// chunk order — the same bytes whatever the world size.
+int collect_enqueue(adc_chi2_plan* P, const double* dev, int R, int nb, cudaStream_t s) {
+  const size_t count = (size_t)nb * P->maxc * R;
+  if (count > P->xcount) return fail(ADC_E_ARG, "exchange staging too small");
+  if (P->comm != nullptr && P->comm->kind == ADC_COMM_NCCL) {
+    if (int rc = comm_allgather_enqueue(P->comm, dev, P->gather, count, s)) return rc;
+    ADCB_CUDA(cudaMemcpyAsync(P->h_gather, P->gather, count * P->world * sizeof(double),
+                              cudaMemcpyDeviceToHost, s));
+  } else {
+    ADCB_CUDA(cudaMemcpyAsync(P->h_send, dev, count * sizeof(double), cudaMemcpyDeviceToHost, s));
+  }
+  return ADC_OK;
+}
+
+int collect_finish(adc_chi2_plan* P, int R, int nb, const double** out) {
+  const size_t count = (size_t)nb * P->maxc * R;
+  const double* src = P->h_gather;
+  if (P->comm == nullptr) {
+    src = P->h_send;  // world == 1: [nb][maxc = nchunks][R] is already compact
+    *out = src;
+    return ADC_OK;
+  }
+  if (P->comm->kind == ADC_COMM_HOST)
+    if (int rc = comm_allgather_host(P->comm, P->h_send, P->h_gather, count)) return rc;
+  const int64_t nchunks = P->L.nchunks;
+  P->full.resize((size_t)nb * nchunks * R);
+  for (int r = 0; r < P->world; ++r) {
+    adc_chi2_layout Lr{};
+    adc_chi2_make_layout(P->bins, P->world, r, &Lr);
+    const int64_t nloc = Lr.chunk_end - Lr.chunk_begin;
+    for (int b = 0; b < nb; ++b)
+      std::memcpy(&P->full[((size_t)b * nchunks + Lr.chunk_begin) * R],
+                  src + (size_t)r * count + (size_t)b * P->maxc * R, (size_t)nloc * R * sizeof(double));
+  }
+  *out = P->full.data();
+  return ADC_OK;
+}
+
 // Once per plan: the linear parameters' q-independent G0/G1 chunk sums.
 int ensure_lin(adc_chi2_plan* P, cudaStream_t s) {
   if (P->lin_ready) return ADC_OK;
@@ -183,15 +247,19 @@ int ensure_lin(adc_chi2_plan* P, cudaStream_t s) {
   return ADC_OK;
 }
 
+// q upload + tile/chunk kernels + exchange / copy back, on P->stream.
+int enqueue_pass(adc_chi2_plan* P, int grad) {
+  ADCB_CUDA(cudaMemcpyAsync(P->qdev, P->h_q, qdev_bytes(), cudaMemcpyHostToDevice, P->stream));
+  if (int rc = chi2_enqueue(make_pass(P), P->model, P->np, grad != 0, P->fast != 0,
+                            P->L.chunk_tiles, P->records, P->stream, P->lin))
+    return rc;
+  return collect_enqueue(P, P->records, adc_chi2_record_len(P->np, grad), 1, P->stream);
+}
+
 int build_graph(adc_chi2_plan* P, int grad) {
   cudaGraph_t g = nullptr;
   ADCB_CUDA(cudaStreamBeginCapture(P->stream, cudaStreamCaptureModeThreadLocal));
-  cudaMemcpyAsync(P->qdev, P->h_q, qdev_bytes(), cudaMemcpyHostToDevice, P->stream);
-  int rc = chi2_enqueue(make_pass(P), P->model, P->np, grad != 0, P->fast != 0,
-                        P->L.chunk_tiles, P->records, P->stream, P->lin);
-  const size_t rec_bytes =
-      (size_t)local_chunks(P) * adc_chi2_record_len(P->np, grad) * sizeof(double);
-  cudaMemcpyAsync(P->h_rec, P->records, rec_bytes, cudaMemcpyDeviceToHost, P->stream);
+  int rc = enqueue_pass(P, grad);
   cudaError_t e = cudaStreamEndCapture(P->stream, &g);
   if (rc != ADC_OK) {
     if (g) cudaGraphDestroy(g);
@@ -204,20 +272,48 @@ int build_graph(adc_chi2_plan* P, int grad) {
   return ADC_OK;
 }
 
-// One single-device pass through the captured graph; leaves the records in
-// h_rec.
-int run_pass(adc_chi2_plan* P, const double* q, int grad) {
-  if (P->L.chunk_begin != 0 || P->L.chunk_end != P->L.nchunks)
-    return fail(ADC_E_ARG, "sharded plan: use adc_cuda_chi2_partials + adc_chi2_finalize");
+void drop_graphs(adc_chi2_plan* P) {
+  for (int g = 0; g < 2; ++g)
+    for (int f = 0; f < 2; ++f) {
+      if (P->graph[g][f]) cudaGraphExecDestroy(P->graph[g][f]);
+      P->graph[g][f] = nullptr;
+      P->warm[g][f] = false;
+    }
+}
+
+// One pass (exchange included); returns the compacted records of all chunks.
+// The first pass of a kind runs eagerly (NCCL sets up its buffers lazily,
+// which must not happen under capture); later passes replay a CUDA graph.
+int run_pass(adc_chi2_plan* P, const double* q, int grad, const double** rec) {
+  if (int rc = require_whole_or_comm(P)) return rc;
   if (int rc = check_domain(P, q)) return rc;
   ADCB_CUDA(cudaSetDevice(P->device));
   fill_qdev(P->model, P->np, q, P->h_q);
   if (grad)
     if (int rc = ensure_lin(P, P->stream)) return rc;
-  if (P->graph[grad][P->fast] == nullptr)
-    if (int rc = build_graph(P, grad)) return rc;
-  ADCB_CUDA(cudaGraphLaunch(P->graph[grad][P->fast], P->stream));
+  if (!P->warm[grad][P->fast]) {
+    if (int rc = enqueue_pass(P, grad)) return rc;
+    P->warm[grad][P->fast] = true;
+  } else {
+    if (P->graph[grad][P->fast] == nullptr)
+      if (int rc = build_graph(P, grad)) return rc;
+    ADCB_CUDA(cudaGraphLaunch(P->graph[grad][P->fast], P->stream));
+  }
   ADCB_CUDA(cudaStreamSynchronize(P->stream));
+  return collect_finish(P, adc_chi2_record_len(P->np, grad), 1, rec);
+}
+
+int alloc_staging(adc_chi2_plan* P) {
+  if (P->h_send) cudaFreeHost(P->h_send);
+  if (P->h_gather) cudaFreeHost(P->h_gather);
+  if (P->gather) cudaFree(P->gather);
+  P->h_send = P->h_gather = P->gather = nullptr;
+  const size_t Rmax = (size_t)adc_chi2_record_len(P->np, 1);
+  P->xcount = (size_t)P->maxc * std::max<size_t>(kMultiMax * Rmax, 1 + 3 * kMultiMax);
+  const bool nccl = P->comm != nullptr && P->comm->kind == ADC_COMM_NCCL;
+  ADCB_CUDA(cudaMallocHost(&P->h_send, P->xcount * sizeof(double)));
+  ADCB_CUDA(cudaMallocHost(&P->h_gather, P->xcount * P->world * sizeof(double)));
+  if (nccl) ADCB_CUDA(cudaMalloc(&P->gather, P->xcount * P->world * sizeof(double)));
   return ADC_OK;
 }
 
@@ -254,6 +350,9 @@ extern "C" int adc_cuda_chi2_plan_create(adc_chi2_plan** out, int32_t model, int
   P->events = events;
   P->width = (hi - lo) / static_cast<double>(bins);  // Histogram::width (fit.hpp:30)
   P->counts = counts;
+  P->world = world;
+  P->rank = rank;
+  P->maxc = std::max<int64_t>(1, (P->L.nchunks + world - 1) / world);
   P->bpt = bpt_for(bins);
   cudaGetDevice(&P->device);
   auto cleanup = [&](int rc) {
@@ -268,37 +367,75 @@ extern "C" int adc_cuda_chi2_plan_create(adc_chi2_plan** out, int32_t model, int
   const int64_t ntiles_local = std::max<int64_t>(
       1, (P->L.bin_end + P->L.tile_bins - 1) / P->L.tile_bins - P->L.chunk_begin * P->L.chunk_tiles);
   const int Rmax = adc_chi2_record_len(np, 1);
-  const int64_t nrec = std::max<int64_t>(1, local_chunks(P));
   cudaError_t e;
   if ((e = cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaMalloc(&P->qdev, qdev_bytes())) != cudaSuccess ||
       (e = cudaMalloc(&P->tile_ws, (size_t)ntiles_local * Rmax * sizeof(double))) != cudaSuccess ||
-      (e = cudaMalloc(&P->records, (size_t)nrec * Rmax * sizeof(double))) != cudaSuccess ||
-      (e = cudaMallocHost(&P->h_q, qdev_bytes())) != cudaSuccess ||
-      (e = cudaMallocHost(&P->h_rec, (size_t)nrec * Rmax * sizeof(double))) != cudaSuccess)
+      (e = cudaMalloc(&P->records, (size_t)P->maxc * Rmax * sizeof(double))) != cudaSuccess ||
+      (e = cudaMemset(P->records, 0, (size_t)P->maxc * Rmax * sizeof(double))) != cudaSuccess ||
+      (e = cudaMallocHost(&P->h_q, qdev_bytes())) != cudaSuccess)
     return cleanup(cuda_fail(e, "chi2 plan allocation"));
+  if (int rc = alloc_staging(P)) return cleanup(rc);
   *out = P;
   return ADC_OK;
 }
 
+extern "C" int adc_cuda_chi2_plan_create_sharded(adc_chi2_plan** out, int32_t model, int32_t np,
+                                                 int64_t bins, double lo, double hi,
+                                                 double events, const double* shard_counts,
+                                                 adc_comm* comm, void* stream) {
+  clear_error();
+  if (out == nullptr) return fail(ADC_E_ARG, "plan: null output");
+  *out = nullptr;
+  if (comm == nullptr) return fail(ADC_E_ARG, "sharded plan: null communicator");
+  if (shard_counts == nullptr) return fail(ADC_E_ARG, "plan: null counts");
+  adc_chi2_layout L{};
+  if (int rc = adc_chi2_make_layout(bins, comm->world, comm->rank, &L)) return rc;
+  // The kernels index counts by global bin number; the shard starts at bin_begin.
+  const double* base = shard_counts - L.bin_begin;
+  if (int rc = adc_cuda_chi2_plan_create(out, model, np, bins, lo, hi, events, base, comm->world,
+                                         comm->rank, stream))
+    return rc;
+  if (int rc = adc_cuda_chi2_plan_set_comm(*out, comm)) {
+    adc_cuda_chi2_plan_destroy(*out);
+    *out = nullptr;
+    return rc;
+  }
+  return ADC_OK;
+}
+
+extern "C" int adc_cuda_chi2_plan_set_comm(adc_chi2_plan* P, adc_comm* comm) {
+  clear_error();
+  if (P == nullptr) return fail(ADC_E_ARG, "null plan");
+  if (comm != nullptr && (comm->world != P->world || comm->rank != P->rank))
+    return fail(ADC_E_ARG, "communicator world/rank differ from the plan's");
+  if (comm != nullptr && comm->kind == ADC_COMM_NCCL && comm->device != P->device)
+    return fail(ADC_E_ARG, "NCCL communicator is on another device than the plan");
+  if (comm == nullptr && P->world > 1)
+    return fail(ADC_E_ARG, "a sharded plan keeps its communicator");
+  ADCB_CUDA(cudaSetDevice(P->device));
+  ADCB_CUDA(cudaStreamSynchronize(P->stream));
+  drop_graphs(P);
+  P->comm = comm;
+  return alloc_staging(P);
+}
+
 extern "C" int adc_cuda_chi2_plan_destroy(adc_chi2_plan* P) {
   if (P == nullptr) return ADC_OK;
-  for (auto& row : P->graph)
-    for (auto& g : row)
-      if (g) cudaGraphExecDestroy(g);
+  drop_graphs(P);
   if (P->qdev) cudaFree(P->qdev);
   if (P->tile_ws) cudaFree(P->tile_ws);
   if (P->records) cudaFree(P->records);
   if (P->h_q) cudaFreeHost(P->h_q);
-  if (P->h_rec) cudaFreeHost(P->h_rec);
+  if (P->h_send) cudaFreeHost(P->h_send);
+  if (P->h_gather) cudaFreeHost(P->h_gather);
+  if (P->gather) cudaFree(P->gather);
   if (P->qmulti) cudaFree(P->qmulti);
   if (P->h_qmulti) cudaFreeHost(P->h_qmulti);
   if (P->tile_ws_multi) cudaFree(P->tile_ws_multi);
   if (P->records_multi) cudaFree(P->records_multi);
-  if (P->h_rec_multi) cudaFreeHost(P->h_rec_multi);
   if (P->lin) cudaFree(P->lin);
   if (P->grad_multi_records) cudaFree(P->grad_multi_records);
-  if (P->h_grad_multi) cudaFreeHost(P->h_grad_multi);
   if (P->stream) cudaStreamDestroy(P->stream);
   delete P;
   return ADC_OK;
@@ -332,6 +469,7 @@ extern "C" int adc_cuda_chi2_partials(adc_chi2_plan* P, const double* q, int32_t
   cudaStream_t s = P->user_stream;  // the caller's stream (0 = legacy default stream)
   // h_q may still be read by an in-flight copy of a previous pass
   ADCB_CUDA(cudaStreamSynchronize(s));
+  ADCB_CUDA(cudaStreamSynchronize(P->stream));
   if (want_grad)
     if (int rc = ensure_lin(P, s)) return rc;
   fill_qdev(P->model, P->np, q, P->h_q);
@@ -344,39 +482,46 @@ extern "C" int adc_cuda_chi2_gradient(adc_chi2_plan* P, const double* q, double*
                                       double* chi2) {
   clear_error();
   if (P == nullptr || q == nullptr || grad == nullptr) return fail(ADC_E_ARG, "null argument");
-  if (int rc = run_pass(P, q, 1)) return rc;
-  return adc_chi2_finalize(P->np, P->events, P->h_rec, P->L.nchunks, 1, grad, chi2);
+  const double* rec = nullptr;
+  if (int rc = run_pass(P, q, 1, &rec)) return rc;
+  return adc_chi2_finalize(P->np, P->events, rec, P->L.nchunks, 1, grad, chi2);
 }
 
 extern "C" int adc_cuda_chi2(adc_chi2_plan* P, const double* q, double* chi2) {
   clear_error();
   if (P == nullptr || q == nullptr || chi2 == nullptr) return fail(ADC_E_ARG, "null argument");
-  if (int rc = run_pass(P, q, 0)) return rc;
-  return adc_chi2_finalize(P->np, P->events, P->h_rec, P->L.nchunks, 0, nullptr, chi2);
+  const double* rec = nullptr;
+  if (int rc = run_pass(P, q, 0, &rec)) return rc;
+  return adc_chi2_finalize(P->np, P->events, rec, P->L.nchunks, 0, nullptr, chi2);
 }
+
+namespace {
+int ensure_multi(adc_chi2_plan* P) {
+  if (P->qmulti != nullptr) return ADC_OK;
+  const size_t qb = qdev_bytes();
+  const int Rm = 1 + 3 * kMultiMax;
+  const int64_t ntiles_local = std::max<int64_t>(
+      1, (P->L.bin_end + P->L.tile_bins - 1) / P->L.tile_bins - P->L.chunk_begin * P->L.chunk_tiles);
+  ADCB_CUDA(cudaMalloc(&P->qmulti, qb * kMultiMax));
+  ADCB_CUDA(cudaMallocHost(&P->h_qmulti, qb * kMultiMax));
+  ADCB_CUDA(cudaMalloc(&P->tile_ws_multi, (size_t)ntiles_local * Rm * sizeof(double)));
+  ADCB_CUDA(cudaMalloc(&P->records_multi, (size_t)P->maxc * Rm * sizeof(double)));
+  ADCB_CUDA(cudaMemset(P->records_multi, 0, (size_t)P->maxc * Rm * sizeof(double)));
+  return ADC_OK;
+}
+}  // namespace
 
 extern "C" int adc_cuda_chi2_multi(adc_chi2_plan* P, const double* qs, int32_t ncand,
                                    double* chi2s) {
   clear_error();
   if (P == nullptr || qs == nullptr || chi2s == nullptr) return fail(ADC_E_ARG, "null argument");
   if (ncand < 1 || ncand > kMultiMax) return fail(ADC_E_ARG, "chi2 multi: 1..32 candidates");
-  if (P->L.chunk_begin != 0 || P->L.chunk_end != P->L.nchunks)
-    return fail(ADC_E_ARG, "sharded plan: multi pass is single-device");
+  if (int rc = require_whole_or_comm(P)) return rc;
   for (int k = 0; k < ncand; ++k)
     if (int rc = check_domain(P, qs + (size_t)k * P->np)) return rc;
   ADCB_CUDA(cudaSetDevice(P->device));
+  if (int rc = ensure_multi(P)) return rc;
   const size_t qb = qdev_bytes();
-  const int Rm = 1 + 3 * kMultiMax;
-  const int64_t ntiles_local = std::max<int64_t>(
-      1, (P->L.bin_end + P->L.tile_bins - 1) / P->L.tile_bins - P->L.chunk_begin * P->L.chunk_tiles);
-  const int64_t nrec = std::max<int64_t>(1, local_chunks(P));
-  if (P->qmulti == nullptr) {
-    ADCB_CUDA(cudaMalloc(&P->qmulti, qb * kMultiMax));
-    ADCB_CUDA(cudaMallocHost(&P->h_qmulti, qb * kMultiMax));
-    ADCB_CUDA(cudaMalloc(&P->tile_ws_multi, (size_t)ntiles_local * Rm * sizeof(double)));
-    ADCB_CUDA(cudaMalloc(&P->records_multi, (size_t)nrec * Rm * sizeof(double)));
-    ADCB_CUDA(cudaMallocHost(&P->h_rec_multi, (size_t)nrec * Rm * sizeof(double)));
-  }
   for (int k = 0; k < ncand; ++k)
     fill_qdev(P->model, P->np, qs + (size_t)k * P->np,
               reinterpret_cast<double*>(reinterpret_cast<char*>(P->h_qmulti) + k * qb));
@@ -388,16 +533,16 @@ extern "C" int adc_cuda_chi2_multi(adc_chi2_plan* P, const double* qs, int32_t n
                                   P->records_multi, P->stream))
     return rc;
   const int R = 1 + 3 * ncand;
-  ADCB_CUDA(cudaMemcpyAsync(P->h_rec_multi, P->records_multi,
-                            (size_t)P->L.nchunks * R * sizeof(double), cudaMemcpyDeviceToHost,
-                            P->stream));
+  if (int rc = collect_enqueue(P, P->records_multi, R, 1, P->stream)) return rc;
   ADCB_CUDA(cudaStreamSynchronize(P->stream));
+  const double* rec = nullptr;
+  if (int rc = collect_finish(P, R, 1, &rec)) return rc;
   ++P->multi_passes;
   // Per candidate: the same records a single value pass produces -> same finalize.
   std::vector<double> rec4((size_t)P->L.nchunks * 4);
   for (int k = 0; k < ncand; ++k) {
     for (int64_t c = 0; c < P->L.nchunks; ++c) {
-      const double* r = P->h_rec_multi + c * R;
+      const double* r = rec + c * R;
       rec4[c * 4 + 0] = r[1 + 3 * k];
       rec4[c * 4 + 1] = r[2 + 3 * k];
       rec4[c * 4 + 2] = r[3 + 3 * k];
@@ -415,30 +560,25 @@ extern "C" int adc_cuda_chi2_gradient_multi(adc_chi2_plan* P, const double* qs, 
   clear_error();
   if (P == nullptr || qs == nullptr || grads == nullptr) return fail(ADC_E_ARG, "null argument");
   if (ncand < 1 || ncand > kMultiMax) return fail(ADC_E_ARG, "gradient multi: 1..32 candidates");
-  if (P->L.chunk_begin != 0 || P->L.chunk_end != P->L.nchunks)
-    return fail(ADC_E_ARG, "sharded plan: multi pass is single-device");
+  if (int rc = require_whole_or_comm(P)) return rc;
   for (int k = 0; k < ncand; ++k)
     if (int rc = check_domain(P, qs + (size_t)k * P->np)) return rc;
   ADCB_CUDA(cudaSetDevice(P->device));
   if (int rc = ensure_lin(P, P->stream)) return rc;
+  if (int rc = ensure_multi(P)) return rc;
   const size_t qb = qdev_bytes();
   const int R = adc_chi2_record_len(P->np, 1);
-  const size_t per = (size_t)P->L.nchunks * R;
-  if (P->qmulti == nullptr) {
-    // same lazily allocated buffers as the multi value pass
-    double c2[1];
-    if (int rc = adc_cuda_chi2_multi(P, qs, 1, c2)) return rc;
-  }
+  const size_t per = (size_t)P->maxc * R;
   if (P->grad_multi_records == nullptr) {
     ADCB_CUDA(cudaMalloc(&P->grad_multi_records, per * kMultiMax * sizeof(double)));
-    ADCB_CUDA(cudaMallocHost(&P->h_grad_multi, per * kMultiMax * sizeof(double)));
+    ADCB_CUDA(cudaMemset(P->grad_multi_records, 0, per * kMultiMax * sizeof(double)));
   }
   for (int k = 0; k < ncand; ++k)
     fill_qdev(P->model, P->np, qs + (size_t)k * P->np,
               reinterpret_cast<double*>(reinterpret_cast<char*>(P->h_qmulti) + k * qb));
   ADCB_CUDA(cudaMemcpyAsync(P->qmulti, P->h_qmulti, qb * ncand, cudaMemcpyHostToDevice, P->stream));
   // ncand ordinary gradient passes back to back on one stream (each identical
-  // to adc_cuda_chi2_gradient), one copy back and one synchronisation.
+  // to adc_cuda_chi2_gradient), one exchange / copy back and one synchronisation.
   for (int k = 0; k < ncand; ++k) {
     Chi2Pass pass = make_pass(P);
     pass.qdev = reinterpret_cast<const double*>(reinterpret_cast<const char*>(P->qmulti) + k * qb);
@@ -446,12 +586,13 @@ extern "C" int adc_cuda_chi2_gradient_multi(adc_chi2_plan* P, const double* qs, 
                               P->grad_multi_records + per * k, P->stream, P->lin))
       return rc;
   }
-  ADCB_CUDA(cudaMemcpyAsync(P->h_grad_multi, P->grad_multi_records, per * ncand * sizeof(double),
-                            cudaMemcpyDeviceToHost, P->stream));
+  if (int rc = collect_enqueue(P, P->grad_multi_records, R, ncand, P->stream)) return rc;
   ADCB_CUDA(cudaStreamSynchronize(P->stream));
+  const double* rec = nullptr;
+  if (int rc = collect_finish(P, R, ncand, &rec)) return rc;
   for (int k = 0; k < ncand; ++k)
-    if (int rc = adc_chi2_finalize(P->np, P->events, P->h_grad_multi + per * k, P->L.nchunks, 1,
-                                   grads + (size_t)k * P->np, nullptr))
+    if (int rc = adc_chi2_finalize(P->np, P->events, rec + (size_t)P->L.nchunks * R * k,
+                                   P->L.nchunks, 1, grads + (size_t)k * P->np, nullptr))
       return rc;
   return ADC_OK;
 }
@@ -459,8 +600,10 @@ extern "C" int adc_cuda_chi2_gradient_multi(adc_chi2_plan* P, const double* qs, 
 // ---------------------------------------------------------------------------
 // Fit loop: FitEngine::fit (fit.cpp:315-425), steepest descent with Armijo
 // backtracking, generalised sigma clamp (fit.cpp:268-278 hard-codes every
-// third index, which is only right for gsum).  The optional numeric-Hessian
-// Newton step (fit.cpp:346-381, off by default) is not part of this path.
+// third index, which is only right for gsum), and the optional numeric-Hessian
+// Newton step (fit.cpp:346-381, off by default).  On a sharded plan every rank
+// runs this loop; the exchanged, fixed-order results are bitwise identical on
+// all ranks, so every rank takes the same decisions and steps.
 extern "C" void adc_fit_default_options(adc_fit_options* o) {
   o->budget = 400;
   o->grad_tol = 1e-6;

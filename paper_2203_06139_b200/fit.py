@@ -84,24 +84,46 @@ def finalize(np_: int, events: float, records: np.ndarray, want_grad: bool = Tru
 
 
 class Chi2Plan:
-    """One histogram resident on one device (or one rank's shard of it)."""
+    """One histogram resident on one device (or one rank's shard of it).
 
-    def __init__(self, model: str, np_: int, h: Histogram, world: int = 1, rank: int = 0):
+    With a communicator (comm.Comm) a sharded plan runs the whole pass —
+    kernels, the record all-gather and the fixed-order finalize — so
+    gradient/chi2/chi2_multi/fit give the same bits on every rank and for
+    every world size."""
+
+    def __init__(self, model: str, np_: int, h: Histogram, world: int = 1, rank: int = 0,
+                 comm=None, _shard=None):
         import torch
         if model not in MODEL_IDS:
             raise AdcError("Arg", f"unknown model '{model}'")
         self.model, self.np, self.h = model, np_, h
-        counts = h.counts
+        self.comm = comm  # keep alive (the plan does not own it)
+        counts = h.counts if _shard is None else _shard
         if not hasattr(counts, "is_cuda"):
             counts = torch.from_numpy(np.ascontiguousarray(counts, dtype=np.float64)).cuda()
         self.counts = counts  # keep alive
         self._p = ctypes.c_void_p()
-        check(lib.adc_cuda_chi2_plan_create(
-            ctypes.byref(self._p), MODEL_IDS[model], np_, h.bins, float(h.lo), float(h.hi),
-            float(h.events), dptr(counts), world, rank,
-            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        if _shard is not None:
+            check(lib.adc_cuda_chi2_plan_create_sharded(
+                ctypes.byref(self._p), MODEL_IDS[model], np_, h.bins, float(h.lo), float(h.hi),
+                float(h.events), dptr(counts), comm._p, stream))
+        else:
+            if comm is not None:
+                world, rank = comm.world, comm.rank
+            check(lib.adc_cuda_chi2_plan_create(
+                ctypes.byref(self._p), MODEL_IDS[model], np_, h.bins, float(h.lo), float(h.hi),
+                float(h.events), dptr(counts), world, rank, stream))
+            if comm is not None:
+                check(lib.adc_cuda_chi2_plan_set_comm(self._p, comm._p))
         self.layout = Chi2Layout()
         check(lib.adc_cuda_chi2_plan_layout(self._p, ctypes.byref(self.layout)))
+
+    @classmethod
+    def sharded(cls, model: str, np_: int, h: Histogram, shard_counts, comm) -> "Chi2Plan":
+        """A rank holding only counts[bin_begin:bin_end] of
+        chi2_layout(h.bins, comm.world, comm.rank); h.counts is not read."""
+        return cls(model, np_, h, comm=comm, _shard=shard_counts)
 
     def set_precision(self, fast: bool):
         check(lib.adc_cuda_chi2_set_precision(self._p, 1 if fast else 0))
@@ -167,15 +189,17 @@ def default_clamp(model: str, np_: int):
 class FitEngine:
     """adc::FitEngine (fit.hpp:82-112), model-parameterised, B200 passes."""
 
-    def __init__(self, model: str = "gsum", np_: int = 3):
-        self.model, self.np = model, np_
+    def __init__(self, model: str = "gsum", np_: int = 3, comm=None):
+        """comm: a comm.Comm to shard every histogram over its ranks (each rank
+        calls the same methods; results are identical on all ranks)."""
+        self.model, self.np, self.comm = model, np_, comm
         self._plans = {}
 
     def _plan(self, h: Histogram) -> Chi2Plan:
         key = id(h)
         pl = self._plans.get(key)
         if pl is None or pl.h is not h:
-            pl = Chi2Plan(self.model, self.np, h)
+            pl = Chi2Plan(self.model, self.np, h, comm=self.comm)
             self._plans = {key: pl}
         return pl
 

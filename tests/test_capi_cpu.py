@@ -21,7 +21,7 @@ HEADER = os.path.join(ROOT, "include", "adc_cuda.h")
 def declared_symbols():
     text = open(HEADER).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(adc_(?:cuda|chi2|fit)_\w+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(adc_(?:cuda|chi2|fit|nccl|comm)_\w+)\s*\(", text)))
 
 
 def test_every_declared_symbol_is_exported_and_bound():
@@ -116,3 +116,16 @@ def test_chi2_layout_shards_whole_chunks():
     L = adc.chi2_layout(10**8)
     # 132 bins per thread: 2960 tiles = 10 full waves of 296 CTAs
     assert L.tile_bins == 132 * 256 and L.chunk_tiles == 31 and L.nchunks == 96
+
+
+def test_host_communicator_without_device():
+    # The host transport needs no device; compute still refuses without one.
+    import paper_2203_06139_b200 as adc
+    comm = adc.Comm.host(3, 2, lambda a: np.tile(a, 3))
+    assert comm.info() == (3, 2, 2)
+    with pytest.raises(adc.AdcError) as e:
+        adc.Comm.host(2, 2, lambda a: a)
+    assert e.value.kind == "Arg"
+    rc = _capi.lib.adc_cuda_chi2_plan_set_comm(None, comm._p)
+    assert rc == 7
+    comm.close()

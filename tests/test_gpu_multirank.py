@@ -1,0 +1,155 @@
+"""Native multi-GPU driver (include/adc_cuda.h, adc_comm): a sharded chi2 plan
+with a communicator runs kernels + the record all-gather + the fixed-order
+finalize inside the library, so gradient / chi2 / the batched line search /
+the fit loop are bitwise identical to the single-device plan on every rank.
+
+The box has one GPU: NCCL is exercised at world size 1 (same enqueue and
+graph-capture code as at N > 1), and world sizes 2 and 3 run as separate
+processes sharing the GPU over the host-callback transport (gloo)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2203_06139_b200 as adc  # noqa: E402
+from paper_2203_06139_b200 import synth  # noqa: E402
+
+from conftest import ROOT  # noqa: E402
+
+BINS = 3 * (1 << 20) + 4321  # 3 chunks + a partial one -> uneven shards
+
+
+def _problem(bins=BINS, seed=5):
+    counts, ev = synth.histogram(bins, events=100.0 * bins, seed=seed)
+    q = np.array(synth.GPOLY_INIT)
+    g = np.array([1e3, -2e3, 5e2, 10.0, -3.0, 1.0])
+    qs = np.stack([q - 2.0 ** -k * g for k in range(9)])
+    return counts, ev, q, qs
+
+
+def _results(plan, eng, h, q, qs):
+    out = {}
+    for k in range(3):  # eager first pass, then graph capture, then replay
+        out[f"grad{k}"], out[f"c2g{k}"] = plan.gradient(q)
+    out["c2"] = plan.chi2(q)
+    out["multi"] = plan.chi2_multi(qs)
+    out["gmulti"] = plan.gradient_multi(qs[:5])
+    r = eng.fit(h, q, adc.FitOptions(budget=15, trace_iterates=6))
+    out["fit_params"] = np.array(r.params)
+    out["fit_chi2"] = r.chi2
+    out["fit_its"] = np.array(r.iterates)
+    r = eng.fit(h, q, adc.FitOptions(budget=3, use_hessian=True))
+    out["newton_params"] = np.array(r.params)
+    return {k: np.asarray(v).tobytes() for k, v in out.items()}
+
+
+def _single_device(counts, ev, q, qs):
+    h = adc.Histogram(counts.size, -5.0, 5.0, ev, counts)
+    return _results(adc.Chi2Plan("gpoly", 6, h), adc.FitEngine("gpoly", 6), h, q, qs)
+
+
+def test_nccl_world1_bitwise_equals_single_device():
+    counts, ev, q, qs = _problem()
+    ref = _single_device(counts, ev, q, qs)
+    comm = adc.Comm.nccl(1, 0, adc.Comm.unique_id())
+    assert comm.info() == (1, 0, 1)
+    h = adc.Histogram(counts.size, -5.0, 5.0, ev, counts)
+    got = _results(adc.Chi2Plan("gpoly", 6, h, comm=comm), adc.FitEngine("gpoly", 6, comm=comm),
+                   h, q, qs)
+    for k in ref:
+        assert got[k] == ref[k], k
+    # one-call form for a rank holding only its shard
+    L = adc.chi2_layout(counts.size, 1, 0)
+    shard = torch.from_numpy(counts[L.bin_begin:L.bin_end].copy()).cuda()
+    pl = adc.Chi2Plan.sharded("gpoly", 6, h, shard, comm)
+    assert pl.gradient(q)[0].tobytes() == ref["grad0"][:48]
+    pl.close()
+    comm.close()
+
+
+def test_host_comm_world1_identity():
+    counts, ev, q, qs = _problem(bins=700_001, seed=8)
+    ref = _single_device(counts, ev, q, qs)
+    comm = adc.Comm.host(1, 0, lambda a: a.copy())
+    h = adc.Histogram(counts.size, -5.0, 5.0, ev, counts)
+    got = _results(adc.Chi2Plan("gpoly", 6, h, comm=comm), adc.FitEngine("gpoly", 6, comm=comm),
+                   h, q, qs)
+    assert got == ref
+
+
+def test_sharded_plan_without_comm_is_refused():
+    counts, ev, q, _ = _problem(bins=3 * (1 << 20), seed=2)
+    h = adc.Histogram(counts.size, -5.0, 5.0, ev, counts)
+    pl = adc.Chi2Plan("gpoly", 6, h, world=2, rank=1)
+    with pytest.raises(adc.AdcError) as e:
+        pl.gradient(q)
+    assert e.value.kind == "Arg" and "communicator" in str(e.value)
+
+
+def test_failing_host_callback_is_reported():
+    counts, ev, q, _ = _problem(bins=100_000, seed=2)
+    h = adc.Histogram(counts.size, -5.0, 5.0, ev, counts)
+
+    def boom(_a):
+        raise RuntimeError("link down")
+
+    comm = adc.Comm.host(1, 0, boom)
+    pl = adc.Chi2Plan("gpoly", 6, h, comm=comm)
+    with pytest.raises(adc.AdcError) as e:
+        pl.gradient(q)
+    assert e.value.kind == "Nccl"
+
+
+def _worker(rank, world, port, out_q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    import paper_2203_06139_b200 as adc_
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        counts, ev, q, qs = _problem()
+        comm = adc_.Comm.from_torch("host")
+        h = adc_.Histogram(counts.size, -5.0, 5.0, ev, counts)
+        L = adc_.chi2_layout(counts.size, world, rank)
+        shard = torch.from_numpy(counts[L.bin_begin:L.bin_end].copy()).cuda()
+        plan = adc_.Chi2Plan.sharded("gpoly", 6, h, shard, comm)
+        res = _results(plan, adc_.FitEngine("gpoly", 6, comm=comm), h, q, qs)
+        out_q.put((rank, res, None))
+    except Exception as e:  # noqa: BLE001
+        out_q.put((rank, None, repr(e)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ranks_share_gpu_host_comm_bitwise(world):
+    import torch.multiprocessing as mp
+    counts, ev, q, qs = _problem()
+    ref = _single_device(counts, ev, q, qs)
+    ctx = mp.get_context("spawn")
+    out_q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, out_q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [out_q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, got, err in res:
+        assert err is None, (rank, err)
+        for k in ref:
+            assert got[k] == ref[k], (rank, k)
