@@ -173,6 +173,14 @@ int adc_cuda_chi2_multi(adc_chi2_plan* plan, const double* qs, int32_t ncand, do
  * communicator. */
 int adc_cuda_chi2_gradient_multi(adc_chi2_plan* plan, const double* qs, int32_t ncand,
                                  double* grads);
+/* adc::GradientProvider (proj/include/adc/fit.hpp:52) of the gradient passes
+ * (chi2_gradient, the fit loop and its Hessian probes):
+ * ADC_PROVIDER_AD_REVERSE (default) = the generated <model>_grad_1;
+ * ADC_PROVIDER_NUMERIC = central differences of the model over q per bin,
+ * h_i = cbrt(eps) max(1, |q_i|), two model evaluations per parameter
+ * (FitEngine::model_gradient, fit.cpp:187-190 -> numdiff.cpp:38-87). */
+enum { ADC_PROVIDER_AD_REVERSE = 0, ADC_PROVIDER_NUMERIC = 1 };
+int adc_cuda_chi2_set_provider(adc_chi2_plan* plan, int32_t provider);
 /* Selects per-bin arithmetic: 0 = faithful (IEEE divisions exactly as the
  * generated code), 1 = fast (reciprocal multiplies; within the reduction
  * tolerance).  Default 1. */

@@ -13,6 +13,8 @@
 // Link with -ladc_b200 (paper_2203_06139_b200/libadc_b200.so).
 #pragma once
 
+#include <algorithm>
+#include <array>
 #include <cstdint>
 #include <map>
 #include <memory>
@@ -24,8 +26,8 @@
 
 namespace adc::b200 {
 
-// diag.hpp:17-23 order; Cuda/Arg are the device-side additions.
-enum class ErrorKind { Semantic, Transform, Eval, Launch, Io, Cuda, Arg };
+// diag.hpp:17-23 order; Cuda/Arg/Nccl are the device-side additions.
+enum class ErrorKind { Semantic, Transform, Eval, Launch, Io, Cuda, Arg, Nccl };
 
 class Error : public std::runtime_error {
  public:
@@ -159,10 +161,60 @@ struct FitResult {
   std::vector<std::vector<double>> iterates;
 };
 
+// ---- multi-GPU (one process per GPU) ---------------------------------------
+// Owns an adc_comm.  NCCL: rank 0 calls Comm::unique_id() and the application
+// distributes the 128 bytes (MPI_Bcast, a file, ...); every rank then builds
+// Comm::nccl(world, rank, id) on its device.  Host: any all-gather over host
+// memory (e.g. MPI_Allgather) as a callback.
+class Comm {
+ public:
+  static std::array<unsigned char, 128> unique_id() {
+    std::array<unsigned char, 128> id{};
+    check(adc_nccl_unique_id(id.data()));
+    return id;
+  }
+  static Comm nccl(int world, int rank, const std::array<unsigned char, 128>& id) {
+    adc_comm* c = nullptr;
+    check(adc_cuda_comm_init_nccl(&c, id.data(), world, rank));
+    return Comm(c);
+  }
+  static Comm host(int world, int rank, adc_allgather_fn fn, void* ctx) {
+    adc_comm* c = nullptr;
+    check(adc_comm_init_host(&c, world, rank, fn, ctx));
+    return Comm(c);
+  }
+  Comm(Comm&& o) noexcept : c_(o.c_) { o.c_ = nullptr; }
+  Comm& operator=(Comm&& o) noexcept {
+    std::swap(c_, o.c_);
+    return *this;
+  }
+  Comm(const Comm&) = delete;
+  Comm& operator=(const Comm&) = delete;
+  ~Comm() {
+    if (c_) adc_comm_destroy(c_);
+  }
+  int world() const { return info(0); }
+  int rank() const { return info(1); }
+  adc_comm* get() const { return c_; }
+
+ private:
+  explicit Comm(adc_comm* c) : c_(c) {}
+  int info(int which) const {
+    int32_t w = 0, r = 0, k = 0;
+    check(adc_comm_info(c_, &w, &r, &k));
+    return which == 0 ? w : r;
+  }
+  adc_comm* c_ = nullptr;
+};
+
 class FitEngine {
  public:
-  // model: "gsum" (np = 3K, fit.cpp:125-138) or "gpoly" (np = 6).
-  FitEngine(std::string model = "gsum", int np = 3) : model_(std::move(model)), np_(np) {
+  // model: "gsum" (np = 3K, fit.cpp:125-138) or "gpoly" (np = 6).  With a
+  // communicator every histogram is sharded over its ranks: each rank uploads
+  // only its own bin range, every rank calls the same methods and gets the
+  // same bits back (the exchange runs inside the library).
+  FitEngine(std::string model = "gsum", int np = 3, const Comm* comm = nullptr)
+      : model_(std::move(model)), np_(np), comm_(comm) {
     if (model_ != "gsum" && model_ != "gpoly")
       throw Error(ErrorKind::Arg, "unknown model '" + model_ + "'");
   }
@@ -212,12 +264,28 @@ class FitEngine {
   adc_chi2_plan* plan(const Histogram& h) {
     if (plan_ != nullptr && key_ == &h && key_counts_ == h.counts.data()) return plan_;
     release();
-    const size_t bytes = h.counts.size() * sizeof(double);
-    check(adc_cuda_alloc(&counts_, bytes));
-    check(adc_cuda_copy(counts_, h.counts.data(), bytes, 1));
-    check(adc_cuda_chi2_plan_create(&plan_, model_ == "gsum" ? ADC_MODEL_GSUM : ADC_MODEL_GPOLY,
-                                    np_, h.bins, h.lo, h.hi, static_cast<double>(h.events),
-                                    static_cast<const double*>(counts_), 1, 0, nullptr));
+    const int32_t model = model_ == "gsum" ? ADC_MODEL_GSUM : ADC_MODEL_GPOLY;
+    if (comm_ != nullptr) {
+      adc_chi2_layout L{};
+      check(adc_chi2_make_layout(h.bins, comm_->world(), comm_->rank(), &L));
+      const size_t bytes = static_cast<size_t>(std::max<int64_t>(1, L.bin_end - L.bin_begin)) *
+                           sizeof(double);
+      check(adc_cuda_alloc(&counts_, bytes));
+      if (L.bin_end > L.bin_begin)
+        check(adc_cuda_copy(counts_, h.counts.data() + L.bin_begin,
+                            static_cast<size_t>(L.bin_end - L.bin_begin) * sizeof(double), 1));
+      check(adc_cuda_chi2_plan_create_sharded(&plan_, model, np_, h.bins, h.lo, h.hi,
+                                              static_cast<double>(h.events),
+                                              static_cast<const double*>(counts_), comm_->get(),
+                                              nullptr));
+    } else {
+      const size_t bytes = h.counts.size() * sizeof(double);
+      check(adc_cuda_alloc(&counts_, bytes));
+      check(adc_cuda_copy(counts_, h.counts.data(), bytes, 1));
+      check(adc_cuda_chi2_plan_create(&plan_, model, np_, h.bins, h.lo, h.hi,
+                                      static_cast<double>(h.events),
+                                      static_cast<const double*>(counts_), 1, 0, nullptr));
+    }
     key_ = &h;
     key_counts_ = h.counts.data();
     return plan_;
@@ -231,6 +299,7 @@ class FitEngine {
 
   std::string model_;
   int np_;
+  const Comm* comm_ = nullptr;
   adc_chi2_plan* plan_ = nullptr;
   void* counts_ = nullptr;
   const Histogram* key_ = nullptr;

@@ -27,6 +27,7 @@
 #include "adc/eval.hpp"
 #include "adc/fit.hpp"
 #include "adc/launch.hpp"
+#include "adc/numdiff.hpp"
 #include "adc/parser.hpp"
 #include "adc/printer.hpp"
 #include "adc/tooling.hpp"
@@ -283,6 +284,7 @@ struct ModelEngine {
   std::string grad;
   Program prog;
   std::vector<int> clamp_idx;
+  bool numeric = false;  // GradientProvider::Numeric: central_gradient (fit.cpp:187-190)
 
   ModelEngine(const std::string& name, Module m, std::string g, std::vector<int> clamp)
       : model(name), grad(std::move(g)), prog(std::move(m)), clamp_idx(std::move(clamp)) {}
@@ -299,6 +301,12 @@ struct ModelEngine {
     return *prog.eval(model, a).value;
   }
   void eval_grad(double x, const std::vector<double>& q, std::vector<double>& out) const {
+    if (numeric) {  // FitEngine::model_gradient, GradientProvider::Numeric branch
+      ArgPack a = pack(x, q);
+      CentralGradient g = central_gradient(prog, model, a, {"q"});
+      out = std::move(g.values);
+      return;
+    }
     out.assign(q.size(), 0.0);
     ArgPack a = pack(x, q);
     a.add_array(out.data(), static_cast<int64_t>(out.size()));
@@ -476,7 +484,18 @@ struct ModelEngine {
   }
 };
 
-ModelEngine make_engine(const std::string& model) {
+// "<model>" or "<model>:numeric" (the GradientProvider).
+GradientProvider split_provider(std::string& model) {
+  const auto colon = model.find(':');
+  if (colon == std::string::npos) return GradientProvider::AdReverse;
+  const std::string p = model.substr(colon + 1);
+  model = model.substr(0, colon);
+  if (p != "numeric") die("unknown provider '" + p + "'");
+  return GradientProvider::Numeric;
+}
+
+ModelEngine make_engine(std::string model) {
+  const GradientProvider prov = split_provider(model);
   Module m = load_named(model);
   std::string g = add_gradient(m, model, {"q"});
   std::vector<int> clamp;
@@ -485,7 +504,9 @@ ModelEngine make_engine(const std::string& model) {
   } else {
     clamp = {2};  // gpoly: only q[2] is a width
   }
-  return ModelEngine(model, std::move(m), g, clamp);
+  ModelEngine e(model, std::move(m), g, clamp);
+  e.numeric = prov == GradientProvider::Numeric;
+  return e;
 }
 
 Histogram read_hist(int64_t bins, double lo, double hi, const std::string& path) {
@@ -512,6 +533,7 @@ int cmd_chi2_in(int argc, char** argv) {
   std::vector<double> q;
   for (int i = 8; i < argc; ++i) q.push_back(std::atof(argv[i]));
   ModelEngine eng = make_engine(model);
+  const GradientProvider prov = split_provider(model);
   std::vector<double> g;
   double c2 = 0;
   std::vector<double> tg, tc;
@@ -528,7 +550,7 @@ int cmd_chi2_in(int argc, char** argv) {
   if (model == "gsum") {
     FitEngine fe;
     std::vector<double> g2;
-    fe.chi2_gradient(h, q, GradientProvider::AdReverse, g2);
+    fe.chi2_gradient(h, q, prov, g2);
     engine_match = g2 == g && fe.chi2(h, q) == c2;
   }
   std::ofstream out(argv[6], std::ios::binary);
@@ -558,13 +580,14 @@ int cmd_fit_in(int argc, char** argv) {
   std::vector<double> q;
   for (int i = 9; i < argc; ++i) q.push_back(std::atof(argv[i]));
   ModelEngine eng = make_engine(model);
+  const GradientProvider prov = split_provider(model);
   auto t0 = clk::now();
   FitResult r = eng.fit(h, q, o);
   double sec = secs(t0, clk::now());
   bool engine_match = true;
   if (model == "gsum") {
     FitEngine fe;
-    FitResult r2 = fe.fit(h, GradientProvider::AdReverse, q, o);
+    FitResult r2 = fe.fit(h, prov, q, o);
     engine_match = r2.params == r.params && r2.iterates == r.iterates && r2.chi2 == r.chi2 &&
                    r2.iterations == r.iterations;
   }

@@ -228,6 +228,32 @@ void rs_model_grad(int model, double x, const double* q, int64_t np, double* slo
   else gpoly_grad_1(x, q, slot);
 }
 
+/* FitEngine::model_gradient, GradientProvider::Numeric branch (fit.cpp:187-190):
+ * central_gradient (numdiff.cpp:38-87) over q: per element, step
+ * h = cbrt(eps) * max(1, |q_i|) (numdiff.cpp:8-13), two primal evaluations at
+ * q_i + h and q_i - h, value (f+ - f-) / (2h). */
+void rs_model_grad_numeric(int model, double x, const double* q, int64_t np, double* slot) {
+  double work[64];
+  const double h0 = cbrt(2.220446049250313e-16);
+  for (int64_t i = 0; i < np; ++i) work[i] = q[i];
+  for (int64_t i = 0; i < np; ++i) {
+    const double xi = work[i];
+    const double h = h0 * fmax(1.0, fabs(xi));
+    work[i] = xi + 1.0 * h;
+    const double fp = rs_model(model, x, work, np);
+    work[i] = xi + -1.0 * h;
+    const double fm = rs_model(model, x, work, np);
+    work[i] = xi;
+    slot[i] = (fp - fm) / (2.0 * h);
+  }
+}
+
+static void model_grad_p(int model, int provider, double x, const double* q, int64_t np,
+                         double* slot) {
+  if (provider == RS_PROVIDER_NUMERIC) rs_model_grad_numeric(model, x, q, np, slot);
+  else rs_model_grad(model, x, q, np, slot);
+}
+
 /* Histogram::center, fit.hpp:30-31. */
 static double center(int64_t i, double lo, double hi, int64_t bins) {
   double width = (hi - lo) / (double)bins;
@@ -256,6 +282,11 @@ double rs_chi2(int model, const double* counts, int64_t bins, double lo, double 
 
 void rs_chi2_gradient(int model, const double* counts, int64_t bins, double lo, double hi,
                       double events, const double* q, int64_t np, double* out) {
+  rs_chi2_gradient_p(model, RS_PROVIDER_AD, counts, bins, lo, hi, events, q, np, out);
+}
+
+void rs_chi2_gradient_p(int model, int provider, const double* counts, int64_t bins, double lo,
+                        double hi, double events, const double* q, int64_t np, double* out) {
   for (int64_t i = 0; i < np; ++i) out[i] = 0.0;
   double* m = (double*)malloc((size_t)bins * sizeof(double));
   double bin_grad[64];
@@ -280,7 +311,7 @@ void rs_chi2_gradient(int model, const double* counts, int64_t bins, double lo, 
       w += -2.0 * r / c * events / s;
     }
     if (w == 0.0) continue;
-    rs_model_grad(model, center(j, lo, hi, bins), q, np, bin_grad);
+    model_grad_p(model, provider, center(j, lo, hi, bins), q, np, bin_grad);
     for (int64_t i = 0; i < np; ++i) out[i] += w * bin_grad[i];
   }
   free(m);
@@ -299,6 +330,16 @@ static double nval(const nsum* a) { return a->s + a->c; }
 void rs_chi2_gradient_compensated(int model, const double* counts, int64_t bins, double lo,
                                   double hi, double events, const double* q, int64_t np,
                                   double* out, double* abs_out) {
+  rs_chi2_gradient_compensated_p(model, RS_PROVIDER_AD, counts, bins, lo, hi, events, q, np, out,
+                                 abs_out, NULL);
+}
+
+void rs_chi2_gradient_compensated_p(int model, int provider, const double* counts, int64_t bins,
+                                    double lo, double hi, double events, const double* q,
+                                    int64_t np, double* out, double* abs_out, double* fd_out) {
+  nsum facc[64];
+  memset(facc, 0, sizeof facc);
+  const double h0 = cbrt(2.220446049250313e-16);
   double* m = (double*)malloc((size_t)bins * sizeof(double));
   double bin_grad[64];
   nsum acc[64], aacc[64];
@@ -325,15 +366,19 @@ void rs_chi2_gradient_compensated(int model, const double* counts, int64_t bins,
       w += -2.0 * r / c * events / S;
     }
     if (w == 0.0) continue;
-    rs_model_grad(model, center(j, lo, hi, bins), q, np, bin_grad);
+    model_grad_p(model, provider, center(j, lo, hi, bins), q, np, bin_grad);
     for (int64_t i = 0; i < np; ++i) {
       nadd(&acc[i], w * bin_grad[i]);
       nadd(&aacc[i], fabs(w * bin_grad[i]));
+      /* one ulp of the primal, amplified by the difference quotient 1/(2h) */
+      nadd(&facc[i], fabs(w) * fabs(m[j]) * 2.220446049250313e-16 /
+                         (2.0 * h0 * fmax(1.0, fabs(q[i]))));
     }
   }
   for (int64_t i = 0; i < np; ++i) {
     out[i] = nval(&acc[i]);
     if (abs_out) abs_out[i] = nval(&aacc[i]);
+    if (fd_out) fd_out[i] = nval(&facc[i]);
   }
   free(m);
 }

@@ -37,6 +37,10 @@ class Restate:
         lib.rs_chi2.restype = d
         lib.rs_chi2_gradient.argtypes = [i, _D, i64, d, d, d, _D, i64, _D]
         lib.rs_chi2_gradient_compensated.argtypes = [i, _D, i64, d, d, d, _D, i64, _D, _D]
+        lib.rs_chi2_gradient_p.argtypes = [i, i, _D, i64, d, d, d, _D, i64, _D]
+        lib.rs_chi2_gradient_compensated_p.argtypes = [i, i, _D, i64, d, d, d, _D, i64, _D, _D,
+                                                       _D]
+        lib.rs_model_grad_numeric.argtypes = [i, d, _D, i64, _D]
         lib.rs_chi2_compensated.argtypes = [i, _D, i64, d, d, d, _D, i64, _D]
         lib.rs_chi2_compensated.restype = d
 
@@ -68,6 +72,30 @@ class Restate:
         self.lib.rs_chi2_gradient(MODELS[model], _p(counts), counts.size, lo, hi, events, _p(q),
                                   q.size, _p(out))
         return out
+
+    def model_grad_numeric(self, model, x, q):
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        out = np.zeros(q.size)
+        self.lib.rs_model_grad_numeric(MODELS[model], x, _p(q), q.size, _p(out))
+        return out
+
+    def chi2_gradient_numeric(self, model, counts, lo, hi, events, q):
+        """Sequential fit.cpp:224-259 with GradientProvider::Numeric."""
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        out = np.zeros(q.size)
+        self.lib.rs_chi2_gradient_p(MODELS[model], 1, _p(counts), counts.size, lo, hi, events,
+                                    _p(q), q.size, _p(out))
+        return out
+
+    def chi2_gradient_numeric_compensated(self, model, counts, lo, hi, events, q):
+        """Returns (gradient, scale, fd_scale): the Numeric provider with compensated
+        sums; tolerance 1e-12 * scale + 4 * fd_scale (one primal ulp per probe
+        evaluation on each side, amplified by 1/(2h))."""
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        out, scale, fd = np.zeros(q.size), np.zeros(q.size), np.zeros(q.size)
+        self.lib.rs_chi2_gradient_compensated_p(MODELS[model], 1, _p(counts), counts.size, lo, hi,
+                                                events, _p(q), q.size, _p(out), _p(scale), _p(fd))
+        return out, scale, fd
 
     def chi2_gradient_compensated(self, model, counts, lo, hi, events, q):
         """Returns (gradient, scale) with scale_i = sum_j |w_j dm_j/dq_i|."""

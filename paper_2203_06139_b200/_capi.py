@@ -87,6 +87,7 @@ SIGNATURES = {
     "adc_cuda_chi2_multi": (ctypes.c_int, [_VP, _D, _I32, _D]),
     "adc_cuda_chi2_gradient_multi": (ctypes.c_int, [_VP, _D, _I32, _D]),
     "adc_cuda_chi2_set_precision": (ctypes.c_int, [_VP, _I32]),
+    "adc_cuda_chi2_set_provider": (ctypes.c_int, [_VP, _I32]),
     "adc_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
     "adc_cuda_comm_init_nccl": (ctypes.c_int, [ctypes.POINTER(_VP), ctypes.c_char_p, _I32, _I32]),
     "adc_comm_init_host": (ctypes.c_int, [ctypes.POINTER(_VP), _I32, _I32, ALLGATHER_FN, _VP]),

@@ -36,6 +36,17 @@ struct QDev {
   double q[kMaxNp];
   double inv[kMaxNp];  // 1/q for width parameters (fast mode)
 };
+// GradientProvider::Numeric (fit.cpp:187-190 -> central_gradient,
+// numdiff.cpp:38-87): per parameter the two probe values q_i +- h_i with
+// h_i = cbrt(eps) max(1, |q_i|), their width reciprocals, 2h_i and 1/(2h_i).
+// Stored right after QDev (fill_qdev), computed on the host with the same
+// libm as the reference.
+struct QNum {
+  double qp[kMaxNp], qm[kMaxNp];
+  double invp[kMaxNp], invm[kMaxNp];
+  double h2[kMaxNp], rh2[kMaxNp];
+};
+static_assert(sizeof(QDev) + sizeof(QNum) == kQDoubles * sizeof(double), "QDev layout");
 
 // ---- fast-mode math ----------------------------------------------------------
 // exp_nonpos (fastmath.cuh): table-driven exp for the models' non-positive
@@ -69,6 +80,18 @@ struct GPoly {
   };
   __device__ static __forceinline__ Reg load(const QDev& Q) {
     return Reg{Q.q[0], Q.q[1], Q.q[2], Q.q[3], Q.q[4], Q.q[5], Q.inv[2]};
+  }
+  // The parameter vector with q[i] replaced by v (inv = 1/v for the width).
+  __device__ static __forceinline__ Reg with(Reg r, int i, double v, double inv) {
+    switch (i) {
+      case 0: r.q0 = v; break;
+      case 1: r.q1 = v; break;
+      case 2: r.q2 = v; r.inv2 = inv; break;
+      case 3: r.q3 = v; break;
+      case 4: r.q4 = v; break;
+      default: r.q5 = v; break;
+    }
+    return r;
   }
   template <bool GRAD, bool FAST>
   __device__ static __forceinline__ void eval(double x, const Reg& Q, const double* tab, double& m,
@@ -117,6 +140,11 @@ struct GSum {
     for (int i = 0; i < 3 * K; ++i) r.q[i] = Q.q[i];
 #pragma unroll
     for (int j = 0; j < K; ++j) r.inv[j] = Q.inv[3 * j + 2];
+    return r;
+  }
+  __device__ static __forceinline__ Reg with(Reg r, int i, double v, double inv) {
+    r.q[i] = v;
+    if (i % 3 == 2) r.inv[i / 3] = inv;
     return r;
   }
   template <bool GRAD, bool FAST>
@@ -170,6 +198,28 @@ struct BinTerm {
   double bg[GRAD ? M::NP : 1];
 };
 
+// Numeric provider: dm/dq_i = (m(q + h_i e_i) - m(q - h_i e_i)) / (2 h_i),
+// two full model evaluations per parameter exactly as central_gradient
+// (numdiff.cpp:62-79) runs the primal at the probes.  Each derivative is
+// folded into G0/G1/G2 as soon as it is known (same per-entry expressions and
+// bin order as bin_accumulate), so no per-bin gradient vector is held.
+template <class M, bool FAST>
+__device__ __forceinline__ void numeric_fold(double x, const typename M::Reg& QR, const QNum& N,
+                                             const double* tab, double w, double mc, double* acc) {
+  constexpr int NP = M::NP;
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    double mp, mm, dummy[1];
+    M::template eval<false, FAST>(x, M::with(QR, i, N.qp[i], N.invp[i]), tab, mp, dummy);
+    M::template eval<false, FAST>(x, M::with(QR, i, N.qm[i], N.invm[i]), tab, mm, dummy);
+    const double d0 = fsub(mp, mm);
+    const double d = FAST ? fmul(d0, N.rh2[i]) : fdiv(d0, N.h2[i]);
+    acc[4 + i] += d;
+    acc[4 + NP + i] = __fma_rn(w, d, acc[4 + NP + i]);
+    acc[4 + 2 * NP + i] = __fma_rn(mc, d, acc[4 + 2 * NP + i]);
+  }
+}
+
 // jh = j + 0.5 exactly (j < 2^52), so x is bit-identical to Histogram::center.
 template <class M, bool GRAD, bool FAST>
 __device__ __forceinline__ void bin_term(const Chi2Pass& P, const typename M::Reg& QR,
@@ -187,6 +237,7 @@ __device__ __forceinline__ void bin_term(const Chi2Pass& P, const typename M::Re
 template <class M, bool GRAD, bool FAST>
 __device__ __forceinline__ void bin_accumulate(const BinTerm<M, GRAD, FAST>& t, double* acc) {
   constexpr int NP = M::NP;
+  constexpr int LIN0 = M::LIN0;
   acc[0] += t.m;
   acc[1] = __fma_rn(t.w, t.m, acc[1]);
   acc[2] = __fma_rn(t.m, t.mc, acc[2]);
@@ -194,7 +245,7 @@ __device__ __forceinline__ void bin_accumulate(const BinTerm<M, GRAD, FAST>& t, 
   if constexpr (GRAD) {
 #pragma unroll
     for (int i = 0; i < NP; ++i) {
-      if (i < M::LIN0) {  // q-independent G0 / G1 entries come from the lin pre-pass
+      if (i < LIN0) {  // q-independent G0 / G1 entries come from the lin pre-pass
         acc[4 + i] += t.bg[i];
         acc[4 + NP + i] = __fma_rn(t.w, t.bg[i], acc[4 + NP + i]);
       }
@@ -206,9 +257,10 @@ __device__ __forceinline__ void bin_accumulate(const BinTerm<M, GRAD, FAST>& t, 
 // PAIR evaluates two independent bins before folding either, giving the
 // scheduler two dependency chains to interleave (the model's exp chain is
 // ~15 dependent FP64 ops deep).  The accumulation order is unchanged.
-template <class M, bool GRAD, bool FAST, bool CHECK, bool PAIR>
+template <class M, bool GRAD, bool FAST, bool CHECK, bool PAIR, bool NUM>
 __device__ __forceinline__ void tile_bins(const Chi2Pass& P, const typename M::Reg& QR,
-                                          const double* tab, int64_t base, double* acc) {
+                                          const double* tab, int64_t base, double* acc,
+                                          const QNum* N) {
   constexpr int PD = kPD;  // P.bpt is a multiple of kPD (adc_chi2_make_layout)
   const int BPT = P.bpt;
   constexpr int STEP = PAIR && PD >= 2 ? 2 : 1;
@@ -222,7 +274,7 @@ __device__ __forceinline__ void tile_bins(const Chi2Pass& P, const typename M::R
   for (int k0 = 0; k0 < BPT; k0 += PD) {
 #pragma unroll
     for (int kk = 0; kk < PD; kk += STEP) {
-      BinTerm<M, GRAD, FAST> t[STEP];
+      BinTerm<M, GRAD && !NUM, FAST> t[STEP];
       bool valid[STEP];
 #pragma unroll
       for (int u = 0; u < STEP; ++u) {
@@ -233,22 +285,44 @@ __device__ __forceinline__ void tile_bins(const Chi2Pass& P, const typename M::R
         ring[kk + u] = (k + PD < BPT && (!CHECK || jn < P.bin_end)) ? ld_stream(P.counts + jn)
                                                                      : 0.0;
         valid[u] = !CHECK || j < P.bin_end;
-        if (valid[u]) bin_term<M, GRAD, FAST>(P, QR, tab, jh, c, t[u]);
+        if constexpr (NUM) {
+          // value terms, then the finite-difference gradient folded in place;
+          // finite differences of a linear term are not exactly its basis, so
+          // every G entry is accumulated here (no lin pre-pass)
+          if (valid[u]) {
+            BinTerm<M, false, FAST> tv;
+            bin_term<M, false, FAST>(P, QR, tab, jh, c, tv);
+            bin_accumulate<M, false, FAST>(tv, acc);
+            numeric_fold<M, FAST>(fadd(P.lo, fmul(jh, P.width)), QR, *N, tab, tv.w, tv.mc, acc);
+          }
+        } else {
+          if (valid[u]) bin_term<M, GRAD, FAST>(P, QR, tab, jh, c, t[u]);
+        }
         jh = fadd(jh, (double)kTileThreads);
       }
+      if constexpr (!NUM) {
 #pragma unroll
-      for (int u = 0; u < STEP; ++u)
-        if (valid[u]) bin_accumulate<M, GRAD, FAST>(t[u], acc);
+        for (int u = 0; u < STEP; ++u)
+          if (valid[u]) bin_accumulate<M, GRAD, FAST>(t[u], acc);
+      }
     }
   }
 }
 
 template <class M, bool GRAD, bool FAST, int MINB = tile_min_blocks<M, GRAD>(),
-          bool PAIR = false>
+          bool PAIR = false, bool NUM = false>
 __global__ void __launch_bounds__(kTileThreads, MINB) chi2_tile_kernel(Chi2Pass P) {
   constexpr int NP = M::NP;
   constexpr int R = GRAD ? 4 + 3 * NP : 4;
   __shared__ QDev Q;
+  const QNum* Np = nullptr;
+  if constexpr (NUM) {
+    __shared__ QNum Ns;
+    const double* src = P.qdev + 2 * kMaxNp;
+    double* dst = reinterpret_cast<double*>(&Ns);
+    for (int v = threadIdx.x; v < 6 * kMaxNp; v += kTileThreads) dst[v] = src[v];
+    Np = &Ns;
+  }
   __shared__ double red[kTileThreads / 32][R];
   __shared__ double tab[64];
   if (threadIdx.x < kMaxNp) {
@@ -274,9 +348,9 @@ __global__ void __launch_bounds__(kTileThreads, MINB) chi2_tile_kernel(Chi2Pass 
 #pragma unroll
     for (int v = 0; v < R; ++v) acc[v] = 0.0;
     if ((tile + 1) * TB <= P.bin_end)
-      tile_bins<M, GRAD, FAST, false, PAIR>(P, QR, tab, base, acc);
+      tile_bins<M, GRAD, FAST, false, PAIR, NUM>(P, QR, tab, base, acc, Np);
     else
-      tile_bins<M, GRAD, FAST, true, PAIR>(P, QR, tab, base, acc);
+      tile_bins<M, GRAD, FAST, true, PAIR, NUM>(P, QR, tab, base, acc, Np);
     // fixed shuffle tree, then fixed cross-warp tree
 #pragma unroll
     for (int v = 0; v < R; ++v) {
@@ -316,7 +390,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P,
   const int ng = min(G, ncand - g0);
   for (int t = threadIdx.x; t < G * kMaxNp; t += kTileThreads) {
     const int c = t / kMaxNp, i = t % kMaxNp;
-    const double* src = P.qdev + (size_t)(g0 + (c < ng ? c : 0)) * 2 * kMaxNp;
+    const double* src = P.qdev + (size_t)(g0 + (c < ng ? c : 0)) * kQDoubles;
     Q[c].q[i] = src[i];
     Q[c].inv[i] = src[kMaxNp + i];
   }
@@ -489,8 +563,14 @@ static void launch_tiles_t(const Chi2Pass& P, int blocks, cudaStream_t s) {
 }
 
 template <class M>
-static void launch_tiles_m(const Chi2Pass& P, bool grad, bool fast, int blocks,
+static void launch_tiles_m(const Chi2Pass& P, bool grad, bool fast, bool num, int blocks,
                            cudaStream_t s) {
+  constexpr int MB = tile_min_blocks<M, true>();
+  if (grad && num) {  // GradientProvider::Numeric
+    if (fast) chi2_tile_kernel<M, true, true, MB, false, true><<<blocks, kTileThreads, 0, s>>>(P);
+    else chi2_tile_kernel<M, true, false, MB, false, true><<<blocks, kTileThreads, 0, s>>>(P);
+    return;
+  }
   if (grad) {
     if (fast) launch_tiles_t<M, true, true>(P, blocks, s);
     else launch_tiles_t<M, true, false>(P, blocks, s);
@@ -501,7 +581,9 @@ static void launch_tiles_m(const Chi2Pass& P, bool grad, bool fast, int blocks,
 }
 
 int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast,
-                 int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin) {
+                 int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin,
+                 bool numeric) {
+  if (numeric) lin = nullptr;  // the numeric gradient accumulates every entry itself
   const int64_t ntiles = P.tile_end - P.tile_begin;
   if (ntiles <= 0) return ADC_OK;
   const int R = grad ? 4 + 3 * np : 4;
@@ -510,14 +592,14 @@ int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast,
   // models, see tile_min_blocks), tiles grid-strided.
   const int64_t blocks = std::min<int64_t>(ntiles, (int64_t)sm_count() * (np <= 6 ? 2 : 1));
   if (model == ADC_MODEL_GPOLY) {
-    launch_tiles_m<GPoly>(P, grad, fast, (int)blocks, s);
+    launch_tiles_m<GPoly>(P, grad, fast, numeric, (int)blocks, s);
   } else {
     switch (np / 3) {
-      case 1: launch_tiles_m<GSum<1>>(P, grad, fast, (int)blocks, s); break;
-      case 2: launch_tiles_m<GSum<2>>(P, grad, fast, (int)blocks, s); break;
-      case 3: launch_tiles_m<GSum<3>>(P, grad, fast, (int)blocks, s); break;
-      case 4: launch_tiles_m<GSum<4>>(P, grad, fast, (int)blocks, s); break;
-      case 8: launch_tiles_m<GSum<8>>(P, grad, fast, (int)blocks, s); break;
+      case 1: launch_tiles_m<GSum<1>>(P, grad, fast, numeric, (int)blocks, s); break;
+      case 2: launch_tiles_m<GSum<2>>(P, grad, fast, numeric, (int)blocks, s); break;
+      case 3: launch_tiles_m<GSum<3>>(P, grad, fast, numeric, (int)blocks, s); break;
+      case 4: launch_tiles_m<GSum<4>>(P, grad, fast, numeric, (int)blocks, s); break;
+      case 8: launch_tiles_m<GSum<8>>(P, grad, fast, numeric, (int)blocks, s); break;
       default: return fail(ADC_E_ARG, "gsum: unsupported component count");
     }
   }
@@ -582,17 +664,32 @@ int chi2_multi_enqueue(const Chi2Pass& P, int model, int np, int ncand,
 }
 
 void fill_qdev(int model, int np, const double* q, double* host_qdev) {
-  std::memset(host_qdev, 0, sizeof(QDev));
+  std::memset(host_qdev, 0, sizeof(QDev) + sizeof(QNum));
   QDev* Q = reinterpret_cast<QDev*>(host_qdev);
+  QNum* N = reinterpret_cast<QNum*>(host_qdev + 2 * kMaxNp);
   for (int i = 0; i < np; ++i) Q->q[i] = q[i];
+  // numdiff.cpp:8-13 and 62-79: h = cbrt(eps) * max(1, |x|), probe = x + sign * h
+  const double h0 = std::cbrt(2.220446049250313e-16);
+  for (int i = 0; i < np; ++i) {
+    const double h = h0 * std::max(1.0, std::fabs(q[i]));
+    N->qp[i] = q[i] + 1.0 * h;
+    N->qm[i] = q[i] + -1.0 * h;
+    N->h2[i] = 2.0 * h;
+    N->rh2[i] = 1.0 / N->h2[i];
+  }
+  auto width = [&](int j) {
+    Q->inv[j] = 1.0 / q[j];
+    N->invp[j] = 1.0 / N->qp[j];
+    N->invm[j] = 1.0 / N->qm[j];
+  };
   if (model == ADC_MODEL_GPOLY) {
-    Q->inv[2] = 1.0 / q[2];
+    width(2);
   } else {
-    for (int j = 2; j < np; j += 3) Q->inv[j] = 1.0 / q[j];
+    for (int j = 2; j < np; j += 3) width(j);
   }
 }
 
-size_t qdev_bytes() { return sizeof(QDev); }
+size_t qdev_bytes() { return sizeof(QDev) + sizeof(QNum); }
 
 int chi2_set_tune(int v) {
   g_chi2_tune = v;

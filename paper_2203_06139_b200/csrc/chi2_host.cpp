@@ -118,6 +118,7 @@ struct adc_chi2_plan {
   int64_t maxc = 1;  // max chunks per rank: the padded per-rank record stride
   int bpt = 4;
   int fast = 1;
+  int provider = ADC_PROVIDER_AD_REVERSE;  // of the gradient passes
   int device = 0;
   cudaStream_t stream = nullptr;       // plan-owned: graph replays
   cudaStream_t user_stream = nullptr;  // caller's (0 = legacy default): adc_cuda_chi2_partials
@@ -125,8 +126,9 @@ struct adc_chi2_plan {
   double* tile_ws = nullptr;
   double* records = nullptr;  // [maxc][R] (gradient / value pass)
   double* h_q = nullptr;
-  cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [grad][fast]
-  bool warm[2][2] = {{false, false}, {false, false}};  // one eager pass before capture
+  // [kind][fast], kind 0 = value, 1 = AD gradient, 2 = numeric gradient
+  cudaGraphExec_t graph[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
+  bool warm[3][2] = {{false, false}, {false, false}, {false, false}};  // eager pass before capture
   // exchange / copy-back staging, sized once for the largest pass kind
   adc_comm* comm = nullptr;
   size_t xcount = 0;          // doubles per rank the staging holds
@@ -148,17 +150,26 @@ struct adc_chi2_plan {
 
 namespace {
 
-int check_domain(const adc_chi2_plan* P, const double* q) {
+int check_domain(const adc_chi2_plan* P, const double* q, bool probes = false) {
   // Divisions by the width parameters are the interpreter's checked
-  // divisions (eval.cpp:543) in gpoly/gsum and their gradients.
+  // divisions (eval.cpp:543) in gpoly/gsum and their gradients; the numeric
+  // provider also evaluates the model at q_i +- h (numdiff.cpp:62-79).
+  auto bad = [&](int j) {
+    if (q[j] == 0.0) return true;
+    if (!probes) return false;
+    const double h = std::cbrt(2.220446049250313e-16) * std::max(1.0, std::fabs(q[j]));
+    return q[j] + 1.0 * h == 0.0 || q[j] + -1.0 * h == 0.0;
+  };
   if (P->model == ADC_MODEL_GPOLY) {
-    if (q[2] == 0.0) return fail(ADC_E_EVAL, "division by zero");
+    if (bad(2)) return fail(ADC_E_EVAL, "division by zero");
   } else {
     for (int j = 2; j < P->np; j += 3)
-      if (q[j] == 0.0) return fail(ADC_E_EVAL, "division by zero");
+      if (bad(j)) return fail(ADC_E_EVAL, "division by zero");
   }
   return ADC_OK;
 }
+
+bool numeric(const adc_chi2_plan* P) { return P->provider == ADC_PROVIDER_NUMERIC; }
 
 Chi2Pass make_pass(const adc_chi2_plan* P) {
   Chi2Pass pass{};
@@ -251,7 +262,8 @@ int ensure_lin(adc_chi2_plan* P, cudaStream_t s) {
 int enqueue_pass(adc_chi2_plan* P, int grad) {
   ADCB_CUDA(cudaMemcpyAsync(P->qdev, P->h_q, qdev_bytes(), cudaMemcpyHostToDevice, P->stream));
   if (int rc = chi2_enqueue(make_pass(P), P->model, P->np, grad != 0, P->fast != 0,
-                            P->L.chunk_tiles, P->records, P->stream, P->lin))
+                            P->L.chunk_tiles, P->records, P->stream, P->lin,
+                            grad != 0 && numeric(P)))
     return rc;
   return collect_enqueue(P, P->records, adc_chi2_record_len(P->np, grad), 1, P->stream);
 }
@@ -266,14 +278,14 @@ int build_graph(adc_chi2_plan* P, int grad) {
     return rc;
   }
   if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
-  e = cudaGraphInstantiate(&P->graph[grad][P->fast], g, 0);
+  e = cudaGraphInstantiate(&P->graph[grad ? 1 + numeric(P) : 0][P->fast], g, 0);
   cudaGraphDestroy(g);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
   return ADC_OK;
 }
 
 void drop_graphs(adc_chi2_plan* P) {
-  for (int g = 0; g < 2; ++g)
+  for (int g = 0; g < 3; ++g)
     for (int f = 0; f < 2; ++f) {
       if (P->graph[g][f]) cudaGraphExecDestroy(P->graph[g][f]);
       P->graph[g][f] = nullptr;
@@ -286,18 +298,19 @@ void drop_graphs(adc_chi2_plan* P) {
 // which must not happen under capture); later passes replay a CUDA graph.
 int run_pass(adc_chi2_plan* P, const double* q, int grad, const double** rec) {
   if (int rc = require_whole_or_comm(P)) return rc;
-  if (int rc = check_domain(P, q)) return rc;
+  if (int rc = check_domain(P, q, grad && numeric(P))) return rc;
   ADCB_CUDA(cudaSetDevice(P->device));
   fill_qdev(P->model, P->np, q, P->h_q);
   if (grad)
     if (int rc = ensure_lin(P, P->stream)) return rc;
-  if (!P->warm[grad][P->fast]) {
+  const int kind = grad ? 1 + numeric(P) : 0;
+  if (!P->warm[kind][P->fast]) {
     if (int rc = enqueue_pass(P, grad)) return rc;
-    P->warm[grad][P->fast] = true;
+    P->warm[kind][P->fast] = true;
   } else {
-    if (P->graph[grad][P->fast] == nullptr)
+    if (P->graph[kind][P->fast] == nullptr)
       if (int rc = build_graph(P, grad)) return rc;
-    ADCB_CUDA(cudaGraphLaunch(P->graph[grad][P->fast], P->stream));
+    ADCB_CUDA(cudaGraphLaunch(P->graph[kind][P->fast], P->stream));
   }
   ADCB_CUDA(cudaStreamSynchronize(P->stream));
   return collect_finish(P, adc_chi2_record_len(P->np, grad), 1, rec);
@@ -456,6 +469,14 @@ extern "C" int adc_cuda_chi2_set_precision(adc_chi2_plan* P, int32_t mode) {
   return ADC_OK;
 }
 
+extern "C" int adc_cuda_chi2_set_provider(adc_chi2_plan* P, int32_t provider) {
+  clear_error();
+  if (P == nullptr || (provider != ADC_PROVIDER_AD_REVERSE && provider != ADC_PROVIDER_NUMERIC))
+    return fail(ADC_E_ARG, "provider is ADC_PROVIDER_AD_REVERSE or ADC_PROVIDER_NUMERIC");
+  P->provider = provider;
+  return ADC_OK;
+}
+
 extern "C" double* adc_cuda_chi2_plan_records(adc_chi2_plan* P) {
   return P ? P->records : nullptr;
 }
@@ -464,7 +485,7 @@ extern "C" int adc_cuda_chi2_partials(adc_chi2_plan* P, const double* q, int32_t
                                       double* records_dev) {
   clear_error();
   if (P == nullptr || q == nullptr) return fail(ADC_E_ARG, "null argument");
-  if (int rc = check_domain(P, q)) return rc;
+  if (int rc = check_domain(P, q, want_grad && numeric(P))) return rc;
   ADCB_CUDA(cudaSetDevice(P->device));
   cudaStream_t s = P->user_stream;  // the caller's stream (0 = legacy default stream)
   // h_q may still be read by an in-flight copy of a previous pass
@@ -475,7 +496,8 @@ extern "C" int adc_cuda_chi2_partials(adc_chi2_plan* P, const double* q, int32_t
   fill_qdev(P->model, P->np, q, P->h_q);
   ADCB_CUDA(cudaMemcpyAsync(P->qdev, P->h_q, qdev_bytes(), cudaMemcpyHostToDevice, s));
   return chi2_enqueue(make_pass(P), P->model, P->np, want_grad != 0, P->fast != 0,
-                      P->L.chunk_tiles, records_dev ? records_dev : P->records, s, P->lin);
+                      P->L.chunk_tiles, records_dev ? records_dev : P->records, s, P->lin,
+                      want_grad && numeric(P));
 }
 
 extern "C" int adc_cuda_chi2_gradient(adc_chi2_plan* P, const double* q, double* grad,
@@ -562,7 +584,7 @@ extern "C" int adc_cuda_chi2_gradient_multi(adc_chi2_plan* P, const double* qs, 
   if (ncand < 1 || ncand > kMultiMax) return fail(ADC_E_ARG, "gradient multi: 1..32 candidates");
   if (int rc = require_whole_or_comm(P)) return rc;
   for (int k = 0; k < ncand; ++k)
-    if (int rc = check_domain(P, qs + (size_t)k * P->np)) return rc;
+    if (int rc = check_domain(P, qs + (size_t)k * P->np, numeric(P))) return rc;
   ADCB_CUDA(cudaSetDevice(P->device));
   if (int rc = ensure_lin(P, P->stream)) return rc;
   if (int rc = ensure_multi(P)) return rc;
@@ -583,7 +605,7 @@ extern "C" int adc_cuda_chi2_gradient_multi(adc_chi2_plan* P, const double* qs, 
     Chi2Pass pass = make_pass(P);
     pass.qdev = reinterpret_cast<const double*>(reinterpret_cast<const char*>(P->qmulti) + k * qb);
     if (int rc = chi2_enqueue(pass, P->model, P->np, true, P->fast != 0, P->L.chunk_tiles,
-                              P->grad_multi_records + per * k, P->stream, P->lin))
+                              P->grad_multi_records + per * k, P->stream, P->lin, numeric(P)))
       return rc;
   }
   if (int rc = collect_enqueue(P, P->grad_multi_records, R, ncand, P->stream)) return rc;

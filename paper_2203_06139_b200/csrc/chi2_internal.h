@@ -9,6 +9,7 @@
 namespace adcb {
 
 constexpr int kMaxNp = 24;
+constexpr int kQDoubles = 8 * kMaxNp;  // QDev (q, 1/q) + QNum (numeric probes), chi2.cu
 constexpr int kMultiMax = 32;  // line-search candidates per multi pass  // gsum up to K = 8 components (the reference bench K list 1,2,4,8)
 
 struct Chi2Pass {
@@ -23,8 +24,10 @@ struct Chi2Pass {
 
 // lin: per-chunk q-independent basis sums from chi2_lin_enqueue (gradient
 // passes of models with linear parameters; nullptr otherwise).
+// numeric: GradientProvider::Numeric (central differences of the model).
 int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast,
-                 int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin);
+                 int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin,
+                 bool numeric = false);
 int chi2_lin_count(int model, int np);  // L: number of linear parameters
 // Writes [G0_lin[L], G1_lin[L]] per local chunk (once per plan); uses P.tile_ws.
 int chi2_lin_enqueue(const Chi2Pass& P, int model, int64_t chunk_tiles, double* lin_records,

@@ -18,6 +18,13 @@ from ._capi import (MODEL_IDS, AdcError, Chi2Layout, FitOptions as _FitOptionsC,
                     check, dbl_array, dptr, lib)
 
 
+class GradientProvider:
+    """adc::GradientProvider (fit.hpp:52): the generated reverse-mode gradient
+    of the model, or central differences of the model (numdiff.cpp:38-87)."""
+    AdReverse = 0
+    Numeric = 1
+
+
 @dataclass
 class Histogram:
     """fit.hpp:23-34.  counts: numpy float64 (host) or a float64 CUDA tensor."""
@@ -128,6 +135,10 @@ class Chi2Plan:
     def set_precision(self, fast: bool):
         check(lib.adc_cuda_chi2_set_precision(self._p, 1 if fast else 0))
 
+    def set_provider(self, provider: int):
+        """GradientProvider.AdReverse (default) or GradientProvider.Numeric."""
+        check(lib.adc_cuda_chi2_set_provider(self._p, int(provider)))
+
     def gradient(self, q):
         g = np.zeros(self.np)
         c2 = ctypes.c_double()
@@ -209,12 +220,19 @@ class FitEngine:
     def chi2(self, h: Histogram, q) -> float:
         return self._plan(h).chi2(q)
 
-    def chi2_gradient(self, h: Histogram, q) -> np.ndarray:
-        return self._plan(h).gradient(q)[0]
+    def chi2_gradient(self, h: Histogram, q,
+                      provider: int = GradientProvider.AdReverse) -> np.ndarray:
+        """FitEngine::chi2_gradient(h, q, provider, out) (fit.cpp:224-259)."""
+        pl = self._plan(h)
+        pl.set_provider(provider)
+        return pl.gradient(q)[0]
 
-    def fit(self, h: Histogram, init, opts: FitOptions | None = None, clamp=None) -> FitResult:
+    def fit(self, h: Histogram, init, opts: FitOptions | None = None, clamp=None,
+            provider: int = GradientProvider.AdReverse) -> FitResult:
+        """FitEngine::fit(h, provider, init, opts) (fit.cpp:315-425)."""
         opts = opts or FitOptions()
         pl = self._plan(h)
+        pl.set_provider(provider)
         o = _FitOptionsC(opts.budget, opts.grad_tol, opts.chi2_rel_tol, opts.sigma_min,
                          opts.armijo_c1, opts.trace_iterates, 1 if opts.use_hessian else 0)
         idx = default_clamp(self.model, self.np) if clamp is None else list(clamp)

@@ -3,9 +3,13 @@
 //   cxx_api_check cpu — error contract without a GPU (no CPU fallback)
 //   cxx_api_check gpu — Listing-1 launch, batched N-dim, FitEngine vs the C oracle
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
+#include <cstring>
+#include <mutex>
 #include <random>
 #include <string>
+#include <thread>
 
 #include "adcx/adc_b200.hpp"
 #include "restate.h"
@@ -36,6 +40,43 @@ static double relmax(const std::vector<double>& a, const std::vector<double>& b)
     if (s > 0) w = std::max(w, std::fabs(a[i] - b[i]) / s);
   }
   return w;
+}
+
+// Host all-gather between threads of one process (two ranks sharing one GPU).
+struct ThreadGather {
+  int world;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0, gen = 0;
+  std::vector<std::vector<char>> slot;
+  explicit ThreadGather(int w) : world(w), slot(w) {}
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const int g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+struct RankCtx {
+  ThreadGather* g;
+  int rank;
+};
+static int thread_allgather(void* ctx, const void* send, void* recv, size_t bytes) {
+  auto* c = static_cast<RankCtx*>(ctx);
+  {
+    std::lock_guard<std::mutex> lk(c->g->mu);
+    c->g->slot[c->rank].assign(static_cast<const char*>(send), static_cast<const char*>(send) + bytes);
+  }
+  c->g->barrier();
+  for (int r = 0; r < c->g->world; ++r)
+    std::memcpy(static_cast<char*>(recv) + r * bytes, c->g->slot[r].data(), bytes);
+  c->g->barrier();
+  return 0;
 }
 
 int main(int argc, char** argv) {
@@ -111,6 +152,67 @@ int main(int argc, char** argv) {
                 r.chi2, r.params[1], r.params[2]);
     EXPECT(r.chi2 < c0 && std::fabs(r.params[1]) < 0.05 && std::fabs(r.params[2] - 1.5) < 0.05,
            "FitEngine::fit recovers mu and sigma (test_fit.cpp:81-93 bounds)");
+
+    // Multi-GPU API: a 3-chunk gpoly histogram sharded over 2 ranks (threads
+    // sharing this GPU, host transport) and over NCCL at world size 1: the
+    // gradient and the whole fit are bitwise those of the single engine.
+    Histogram big;
+    big.bins = 3 * (1 << 20) + 77;
+    big.lo = -5;
+    big.hi = 5;
+    big.counts.resize(big.bins);
+    double tb = 0;
+    for (int j = 0; j < big.bins; ++j) {
+      const double x = big.center(j);
+      big.counts[j] = j % 100 == 0 ? 0.0 : std::round(150 * std::exp(-0.5 * x * x / 2.25) + 20 - x);
+      tb += big.counts[j];
+    }
+    big.events = (uint64_t)tb;
+    const std::vector<double> qp = {120.0, 0.3, 1.2, 25.0, -0.5, 0.01};
+    FitOptions fo;
+    fo.budget = 8;
+    std::vector<double> g1;
+    FitEngine single("gpoly", 6);
+    single.chi2_gradient(big, qp, g1);
+    const FitResult f1 = single.fit(big, qp, fo);
+    ThreadGather tg(2);
+    std::vector<std::vector<double>> gr(2);
+    std::vector<FitResult> fr(2);
+    std::vector<std::string> errs(2);
+    std::vector<std::thread> th;
+    for (int rank = 0; rank < 2; ++rank)
+      th.emplace_back([&, rank] {
+        try {
+          RankCtx ctx{&tg, rank};
+          Comm comm = Comm::host(2, rank, thread_allgather, &ctx);
+          FitEngine e("gpoly", 6, &comm);
+          e.chi2_gradient(big, qp, gr[rank]);
+          fr[rank] = e.fit(big, qp, fo);
+        } catch (const std::exception& ex) {
+          errs[rank] = ex.what();
+        }
+      });
+    for (auto& t : th) t.join();
+    bool same = errs[0].empty() && errs[1].empty();
+    for (int rank = 0; rank < 2 && same; ++rank)
+      same = std::memcmp(gr[rank].data(), g1.data(), 6 * sizeof(double)) == 0 &&
+             std::memcmp(fr[rank].params.data(), f1.params.data(), 6 * sizeof(double)) == 0 &&
+             fr[rank].iterations == f1.iterations && fr[rank].chi2 == f1.chi2;
+    if (!errs[0].empty()) std::printf("     rank 0: %s\n", errs[0].c_str());
+    EXPECT(same, "2 ranks (host transport): gradient and fit bitwise equal to one engine");
+    std::string nerr;
+    std::vector<double> gn;
+    try {
+      Comm nc = Comm::nccl(1, 0, Comm::unique_id());
+      FitEngine e("gpoly", 6, &nc);
+      e.chi2_gradient(big, qp, gn);
+      e.chi2_gradient(big, qp, gn);  // graph replay with the NCCL all-gather inside
+    } catch (const std::exception& ex) {
+      nerr = ex.what();
+    }
+    if (!nerr.empty()) std::printf("     nccl: %s\n", nerr.c_str());
+    EXPECT(nerr.empty() && std::memcmp(gn.data(), g1.data(), 6 * sizeof(double)) == 0,
+           "NCCL communicator (world 1): gradient bitwise equal to one engine");
   }
   std::printf("%d failure(s)\n", failures);
   return failures ? 1 : 0;

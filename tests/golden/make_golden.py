@@ -120,6 +120,33 @@ def main():
                    f"{key}_model": model})
     np.savez(os.path.join(OUT, "chi2_cases.npz"), **ch)
 
+    # GradientProvider::Numeric (fit.cpp:187-190 -> central_gradient,
+    # numdiff.cpp:38-87): chi2 gradient and a short fit, per model.
+    nu = {}
+    for key, model, bins, events, qtrue, q in (
+        ("gpoly_b2000", "gpoly", 2000, 1e6, synth.GPOLY_TRUTH, synth.GPOLY_INIT),
+        ("gsum1_b1000", "gsum", 1000, 1e5, (1.0, 0.0, 1.5), (0.8, 0.3, 1.2)),
+        ("gsum2_b1500", "gsum", 1500, 2e5, (1.0, -5 / 3, 1.5, 1.0, 5 / 3, 1.0),
+         (0.8, -1.3666666666666667, 1.2, 0.8, 1.9666666666666668, 0.8)),
+    ):
+        counts, ev = synth.histogram(bins, -5.0, 5.0, events, model, qtrue, seed=bins)
+        counts.astype("<f8").tofile(ti)
+        meta = run("chi2-in", model + ":numeric", bins, -5.0, 5.0, ti, to, 1,
+                   *[repr(float(v)) for v in q])
+        assert meta["fitengine_match"]
+        o = f64(to, 1 + len(q))
+        nu.update({f"{key}_counts": counts, f"{key}_q": np.array(q, dtype=np.float64),
+                   f"{key}_grad": o[1:], f"{key}_events": ev, f"{key}_model": model})
+        meta = run("fit-in", model + ":numeric", bins, -5.0, 5.0, ti, to, 10, "12",
+                   *[repr(float(v)) for v in q])
+        assert meta["fitengine_match"]
+        np_ = len(q)
+        o = f64(to, 5 + np_ + 10 * np_)
+        nu.update({f"{key}_fit_chi2": o[0], f"{key}_fit_iterations": o[1],
+                   f"{key}_fit_params": o[5:5 + np_],
+                   f"{key}_fit_iterates": o[5 + np_:].reshape(10, np_)})
+    np.savez(os.path.join(OUT, "chi2_numeric_cases.npz"), **nu)
+
     # Fit loop iterates (fit.cpp:315-425), trace 10, budget 12.
     fi = {}
     for key, model, bins, events, qtrue, q, budget in (

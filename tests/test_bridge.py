@@ -28,7 +28,7 @@ def cxx_check(tmp_path_factory):
                     "-I", os.path.join(ROOT, "oracle"),
                     os.path.join(ROOT, "tests", "cpu", "cxx_api_check.cpp"),
                     os.path.join(ROOT, "oracle", "restate.c"), "-x", "none",
-                    "-L", LIBDIR, "-ladc_b200", f"-Wl,-rpath,{LIBDIR}", "-o", str(exe)],
+                    "-L", LIBDIR, "-ladc_b200", f"-Wl,-rpath,{LIBDIR}", "-o", str(exe), "-lpthread"],
                    check=True)
     return str(exe)
 

@@ -299,3 +299,56 @@ def test_fit_1e6_newton_converges_to_truth():
     # Gaussian parameters recovered to the reference's bounds (test_fit.cpp:81-93)
     assert abs(r.params[1] - synth.GPOLY_TRUTH[1]) < 0.05
     assert abs(r.params[2] - synth.GPOLY_TRUTH[2]) < 0.05
+
+
+# ---------------------------------------------------------------------------- Numeric provider
+@pytest.mark.parametrize("key", ["gpoly_b2000", "gsum1_b1000", "gsum2_b1500"])
+@pytest.mark.parametrize("fast", [True, False])
+def test_chi2_numeric_provider(restate, key, fast):
+    """GradientProvider::Numeric (fit.cpp:187-190 -> central_gradient,
+    numdiff.cpp:38-87) against the reference's own numbers and the compensated
+    restatement.  Tolerance: the reduction bound 1e-12 * sum|terms| plus the
+    finite-difference amplification of the primal's last-ulp differences
+    (libdevice / table exp vs glibc): K ulps of m_j times |w_j| / (2h_i),
+    K = 4 faithful, 16 fast (reciprocal multiplies add ulps to z and m)."""
+    g = golden("chi2_numeric_cases.npz")
+    model = str(g[f"{key}_model"])
+    counts, q, ev = g[f"{key}_counts"], g[f"{key}_q"], float(g[f"{key}_events"])
+    h = adc.Histogram(counts.size, -5.0, 5.0, ev, counts)
+    eng = adc.FitEngine(model, q.size)
+    eng._plan(h).set_precision(fast)
+    grad = eng.chi2_gradient(h, q, adc.GradientProvider.Numeric)
+    ref, scale, fd = restate.chi2_gradient_numeric_compensated(model, counts, -5.0, 5.0, ev, q)
+    tol = 1e-12 * scale + (16.0 if fast else 4.0) * fd
+    assert np.all(np.abs(grad - ref) <= tol), (grad - ref, tol)
+    assert np.all(np.abs(grad - g[f"{key}_grad"]) <= tol + 1e-12 * scale)
+    # the AD provider is a different (exact) gradient of the same chi2
+    ad = eng.chi2_gradient(h, q, adc.GradientProvider.AdReverse)
+    assert np.all(np.abs(ad - grad) <= 1e-6 * scale)
+    assert not np.array_equal(ad, grad)
+
+
+@pytest.mark.parametrize("key", ["gpoly_b2000", "gsum1_b1000", "gsum2_b1500"])
+def test_fit_numeric_provider_matches_reference(key):
+    """FitEngine::fit(h, Numeric, ...) iterates (fit-in <model>:numeric, budget 12)."""
+    g = golden("chi2_numeric_cases.npz")
+    model = str(g[f"{key}_model"])
+    counts, q, ev = g[f"{key}_counts"], g[f"{key}_q"], float(g[f"{key}_events"])
+    h = adc.Histogram(counts.size, -5.0, 5.0, ev, counts)
+    res = adc.FitEngine(model, q.size).fit(h, q, adc.FitOptions(budget=12, trace_iterates=10),
+                                           provider=adc.GradientProvider.Numeric)
+    assert res.iterations == int(g[f"{key}_fit_iterations"])
+    assert rel_err(res.chi2, g[f"{key}_fit_chi2"]) <= 1e-9
+    its = g[f"{key}_fit_iterates"]
+    for k in range(min(10, res.iterations + 1)):
+        assert rel_err(np.asarray(res.iterates[k]), its[k]).max() <= 1e-6, k
+
+
+def test_numeric_provider_probe_domain_error():
+    # a width whose probe q - h hits 0 is the interpreter's division by zero
+    counts, ev = synth.histogram(1000, events=1e5)
+    h = adc.Histogram(1000, -5.0, 5.0, ev, counts)
+    h0 = np.cbrt(2.220446049250313e-16)
+    with pytest.raises(adc.AdcError) as e:
+        adc.FitEngine("gpoly", 6).chi2_gradient(h, [1, 0, h0, 0, 0, 0], adc.GradientProvider.Numeric)
+    assert e.value.kind == "Eval"

@@ -69,3 +69,20 @@ def test_fingerprints_file():
     with open(os.path.join(GOLDEN, "gradient_fingerprints.json")) as fh:
         fps = json.load(fh)
     assert set(fps) == {"gauss_grad_0_1", "gaussnd_grad_0_1", "gpoly_grad_1", "gsum_grad_1"}
+
+
+@pytest.mark.parametrize("key", ["gpoly_b2000", "gsum1_b1000", "gsum2_b1500"])
+def test_chi2_numeric_provider_bitexact(restate, key):
+    # GradientProvider::Numeric (fit.cpp:187-190, central_gradient numdiff.cpp:38-87):
+    # the reference's value for gsum comes from the unmodified FitEngine.
+    g = golden("chi2_numeric_cases.npz")
+    model = str(g[f"{key}_model"])
+    counts, q, ev = g[f"{key}_counts"], g[f"{key}_q"], float(g[f"{key}_events"])
+    assert np.array_equal(restate.chi2_gradient_numeric(model, counts, -5.0, 5.0, ev, q),
+                          g[f"{key}_grad"])
+    gc, scale, fd = restate.chi2_gradient_numeric_compensated(model, counts, -5.0, 5.0, ev, q)
+    assert np.all(np.abs(gc - g[f"{key}_grad"]) <= 1e-12 * scale)
+    assert np.all(fd > 0) and np.all(fd < 1e-6 * scale)
+    # numeric and AD agree to finite-difference accuracy (test_fit.cpp:62-79: 1e-6)
+    ad, _ = restate.chi2_gradient_compensated(model, counts, -5.0, 5.0, ev, q)
+    assert np.all(np.abs(gc - ad) <= 1e-6 * scale)
