@@ -69,7 +69,8 @@ enum {
   ADC_KERNEL_GAUSS_GRAD_0_1 = 0,   /* proj/tests/golden/gauss_grad_0_1.golden */
   ADC_KERNEL_GAUSSND_GRAD_0_1 = 1, /* oracle/dsl/gaussnd.dsl, wrt {x, p} */
   ADC_KERNEL_GSUM_GRAD_1 = 2,      /* fit.cpp:125-138 model, wrt {q} */
-  ADC_KERNEL_GPOLY_GRAD_1 = 3      /* oracle/dsl/gpoly.dsl, wrt {q} */
+  ADC_KERNEL_GPOLY_GRAD_1 = 3,     /* oracle/dsl/gpoly.dsl, wrt {q} */
+  ADC_KERNEL_GAUSS_GRAD = 4        /* kernels.dsl gauss, wrt {x, p, sigma} (compute_shared) */
 };
 
 /* ---------------------------------------------------------------------------
@@ -87,6 +88,22 @@ int adc_cuda_compute_gauss(int64_t grid_dim, int64_t block_dim, int64_t n, const
  * streams so PCIe traffic overlaps the kernel.  Synchronous. */
 int adc_cuda_compute_gauss_host(int64_t grid_dim, int64_t block_dim, int64_t n, const double* x,
                                 const double* p, double sigma, double* dx, double* dp);
+
+/* Listing-1's hazardous twin `compute_shared` (proj/corpus/kernels.dsl:16-21):
+ * every thread calls gauss_grad(x[i], p[i], sigma, dx[i], dp[i], dsigma), so all
+ * threads accumulate into the one-element slot dsigma.  The reference's
+ * race_check flags dsigma and launch refuses (launch.cpp:261-267, same
+ * message, ADC_E_LAUNCH) unless `unsafe`; forced, the reference uses CAS
+ * atomics in an unspecified order (eval.cpp:414-423).  Here the forced run is
+ * DETERMINISTIC: dx, dp private as in `compute`, the sigma contributions summed
+ * in a fixed order (per thread in point order, fixed CTA tree, one fixed final
+ * tree) and added to dsigma[0] once.  Same bits on every run and device. */
+int adc_cuda_compute_gauss_shared(int64_t grid_dim, int64_t block_dim, int64_t n,
+                                  const double* x, const double* p, double sigma, double* dx,
+                                  double* dp, double* dsigma, int32_t unsafe, void* stream);
+int adc_cuda_compute_gauss_shared_host(int64_t grid_dim, int64_t block_dim, int64_t n,
+                                       const double* x, const double* p, double sigma, double* dx,
+                                       double* dp, double* dsigma, int32_t unsafe);
 
 /* ---------------------------------------------------------------------------
  * Batched N-dim Gaussian gradient gaussnd_grad_0_1(x, p, sigma, dim, dx, dp)

@@ -68,7 +68,7 @@ struct BufferSet {
 };
 
 struct LaunchOptions {
-  bool unsafe = false;    // hazardous kernels have no B200 kernel: refused either way
+  bool unsafe = false;    // forces compute_shared (deterministic fixed-order dsigma reduction)
   unsigned workers = 0;   // accepted for drop-in use; the GPU result does not depend on it
   bool sequential = false;
 };
@@ -77,25 +77,24 @@ struct LaunchStats {
   std::vector<uint32_t> thread_statements;  // 3 per active thread, 2 per padding thread
 };
 
-// adc::launch (launch.cpp:252-346) for the Listing-1 kernel `compute`
-// (kernels.dsl:9-14) with host buffers; callee_fingerprint 0 = the registry's.
+// adc::launch (launch.cpp:252-346) for the Listing-1 kernels `compute`
+// (kernels.dsl:9-14) and, forced with opts.unsafe, `compute_shared`
+// (kernels.dsl:16-21), with host buffers; callee_fingerprint 0 = the registry's.
 inline LaunchStats launch(const std::string& kernel, const LaunchConfig& cfg, BufferSet& buffers,
                           const LaunchOptions& opts = {}, uint64_t callee_fingerprint = 0) {
   cfg.validate();
-  if (kernel == "compute_shared") {
-    if (!opts.unsafe)
-      throw Error(ErrorKind::Launch,
-                  "launch refused, hazardous parameter(s): dsigma (whole array shared with a "
-                  "writing callee across threads); pass the unsafe flag to force");
-    throw Error(ErrorKind::Launch, "no B200 kernel registered for 'gauss_grad'");
-  }
-  if (kernel != "compute") throw Error(ErrorKind::Launch, "unknown kernel '" + kernel + "'");
+  const bool shared = kernel == "compute_shared";
+  if (shared && !opts.unsafe)
+    throw Error(ErrorKind::Launch,
+                "launch refused, hazardous parameter(s): dsigma (whole array shared with a "
+                "writing callee across threads); pass the unsafe flag to force");
+  if (!shared && kernel != "compute")
+    throw Error(ErrorKind::Launch, "unknown kernel '" + kernel + "'");
+  const int32_t kid = shared ? ADC_KERNEL_GAUSS_GRAD : ADC_KERNEL_GAUSS_GRAD_0_1;
   int32_t id = -1;
   check(adc_cuda_registry_find(
-      "gauss_grad_0_1",
-      callee_fingerprint ? callee_fingerprint
-                         : adc_cuda_registry_fingerprint(ADC_KERNEL_GAUSS_GRAD_0_1),
-      &id));
+      adc_cuda_registry_name(kid),
+      callee_fingerprint ? callee_fingerprint : adc_cuda_registry_fingerprint(kid), &id));
   for (const char* name : {"x", "p", "dx", "dp"}) {
     auto it = buffers.arrays.find(name);
     if (it == buffers.arrays.end())
@@ -108,10 +107,20 @@ inline LaunchStats launch(const std::string& kernel, const LaunchConfig& cfg, Bu
   }
   auto s = buffers.scalars.find("sigma");
   if (s == buffers.scalars.end()) throw Error(ErrorKind::Launch, "missing scalar value 'sigma'");
-  check(adc_cuda_compute_gauss_host(cfg.grid_dim, cfg.block_dim, cfg.n,
-                                    buffers.arrays["x"].data(), buffers.arrays["p"].data(),
-                                    s->second, buffers.arrays["dx"].data(),
-                                    buffers.arrays["dp"].data()));
+  if (shared) {
+    auto ds = buffers.arrays.find("dsigma");
+    if (ds == buffers.arrays.end()) throw Error(ErrorKind::Launch, "missing buffer 'dsigma'");
+    if (ds->second.empty()) throw Error(ErrorKind::Launch, "buffer 'dsigma' is empty");
+    check(adc_cuda_compute_gauss_shared_host(
+        cfg.grid_dim, cfg.block_dim, cfg.n, buffers.arrays["x"].data(),
+        buffers.arrays["p"].data(), s->second, buffers.arrays["dx"].data(),
+        buffers.arrays["dp"].data(), ds->second.data(), 1));
+  } else {
+    check(adc_cuda_compute_gauss_host(cfg.grid_dim, cfg.block_dim, cfg.n,
+                                      buffers.arrays["x"].data(), buffers.arrays["p"].data(),
+                                      s->second, buffers.arrays["dx"].data(),
+                                      buffers.arrays["dp"].data()));
+  }
   LaunchStats st;
   st.thread_statements.assign(static_cast<size_t>(cfg.grid_dim * cfg.block_dim), 2u);
   for (int64_t g = 0; g < cfg.n; ++g) st.thread_statements[static_cast<size_t>(g)] = 3u;

@@ -151,16 +151,20 @@ LaunchStats launch(const Program& p, const std::string& kernel, const LaunchConf
   }
   // Kernel shape + registry lookup by the callee's printed text.
   Listing1 l1;
-  if (report.has_hazard() || !match_listing1(*k, l1))
-    throw Error(ErrorKind::Launch, "no B200 kernel for '" + kernel + "'");
+  if (!match_listing1(*k, l1)) throw Error(ErrorKind::Launch, "no B200 kernel for '" + kernel + "'");
   const FunctionDef* callee = p.module().find(l1.call->callee);
   if (callee == nullptr) throw Error(ErrorKind::Launch, "unknown callee '" + l1.call->callee + "'");
   int32_t id = -1;
   check(adc_cuda_registry_find(callee->name.c_str(), fingerprint(*callee), &id));
-  if (id != ADC_KERNEL_GAUSS_GRAD_0_1 || l1.call->call_args.size() != 5)
+  const size_t nargs = l1.call->call_args.size();
+  // gauss_grad_0_1(x[i], p[i], sigma, dx[i], dp[i]) (compute), or the forced
+  // hazardous gauss_grad(x[i], p[i], sigma, dx[i], dp[i], dsigma)
+  // (compute_shared): only the shared slot may be a whole array.
+  const bool shared = id == ADC_KERNEL_GAUSS_GRAD && nargs == 6;
+  if (!(id == ADC_KERNEL_GAUSS_GRAD_0_1 && nargs == 5) && !shared)
     throw Error(ErrorKind::Launch, "no B200 launch path for '" + callee->name + "'");
-  // gauss_grad_0_1(x[i], p[i], sigma, dx[i], dp[i]): slices at the thread index
-  // and one by-value real.
+  if (report.has_hazard() && !shared)
+    throw Error(ErrorKind::Launch, "no B200 kernel for '" + kernel + "'");
   std::vector<double*> arr;
   double sigma = 0.0;
   for (size_t a = 0; a < 5; ++a) {
@@ -176,8 +180,17 @@ LaunchStats launch(const Program& p, const std::string& kernel, const LaunchConf
   }
   LaunchStats st;
   analytic_counts(p, kernel, *k, cfg, buffers, st);
-  check(adc_cuda_compute_gauss_host(cfg.grid_dim, cfg.block_dim, cfg.n, arr[0], arr[1], sigma,
-                                    arr[2], arr[3]));
+  if (shared) {
+    const Expr& e = *l1.call->call_args[5];
+    if (e.kind != ExprKind::VarRef) throw Error(ErrorKind::Launch, "unsupported dsigma argument");
+    std::vector<double>& ds = buffers.arrays.at(e.name);
+    if (ds.empty()) throw Error(ErrorKind::Launch, "buffer '" + e.name + "' is empty");
+    check(adc_cuda_compute_gauss_shared_host(cfg.grid_dim, cfg.block_dim, cfg.n, arr[0], arr[1],
+                                             sigma, arr[2], arr[3], ds.data(), 1));
+  } else {
+    check(adc_cuda_compute_gauss_host(cfg.grid_dim, cfg.block_dim, cfg.n, arr[0], arr[1], sigma,
+                                      arr[2], arr[3]));
+  }
   return st;
 }
 

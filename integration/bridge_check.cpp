@@ -120,6 +120,40 @@ static void gpu_checks(const Program& p) {
     EXPECT(rs.thread_statements == gs.thread_statements, "LaunchStats.thread_statements equal");
     EXPECT(rs.counts == gs.counts, "LaunchStats.counts (op counters) equal");
   }
+  // compute_shared forced: the reference's sequential run vs the B200's
+  // fixed-order reduction (test_launch.cpp:148-165 precedent: 1e-9).
+  {
+    const int64_t n = 100003;
+    std::mt19937_64 rng(99);
+    BufferSet ref, gpu;
+    std::vector<double> x(n), px(n);
+    for (int64_t i = 0; i < n; ++i) {
+      x[i] = std::uniform_real_distribution<double>(-3, 3)(rng);
+      px[i] = std::uniform_real_distribution<double>(-2, 2)(rng);
+    }
+    for (BufferSet* b : {&ref, &gpu}) {
+      b->arrays["x"] = x;
+      b->arrays["p"] = px;
+      b->scalars["sigma"] = 1.1;
+      b->arrays["dx"] = std::vector<double>(n, 0.0);
+      b->arrays["dp"] = std::vector<double>(n, 0.0);
+      b->arrays["dsigma"] = std::vector<double>(1, 0.5);
+    }
+    LaunchOptions forced;
+    forced.unsafe = true;
+    forced.sequential = true;
+    LaunchConfig cfg{n / 256 + 1, 256, n};
+    LaunchStats rs = adc::launch(p, "compute_shared", cfg, ref, forced);
+    LaunchStats gs = b200_bridge::launch(p, "compute_shared", cfg, gpu, forced);
+    double worst = 0;
+    for (int64_t i = 0; i < n; ++i)
+      worst = std::max({worst, rel(ref.arrays["dx"][i], gpu.arrays["dx"][i]),
+                        rel(ref.arrays["dp"][i], gpu.arrays["dp"][i])});
+    const double ds = rel(ref.arrays["dsigma"][0], gpu.arrays["dsigma"][0]);
+    std::printf("     compute_shared: dx/dp worst rel %.3g, dsigma rel %.3g\n", worst, ds);
+    EXPECT(worst <= 1e-12 && ds <= 1e-9, "bridged forced compute_shared matches the reference");
+    EXPECT(rs.counts == gs.counts, "compute_shared LaunchStats.counts equal");
+  }
   // FitEngine (gsum K=1, 2) chi2 and gradient on the GPU vs the reference engine.
   b200_bridge::set_model_source(kGsumDsl);
   FitEngine eng;

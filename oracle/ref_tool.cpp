@@ -217,6 +217,46 @@ int cmd_gauss1d_in(int argc, char** argv) {
   return 0;
 }
 
+// gauss-shared-in <n> <sigma> <block> <in.bin> <out.bin>
+//   Listing-1's hazardous twin `compute_shared` (kernels.dsl:16-21): every
+//   thread accumulates into the one-element slot dsigma.  The default launch
+//   must refuse (launch.cpp:261-267); the forced sequential launch
+//   (LaunchOptions{unsafe, sequential}, test_launch.cpp:148-153) gives the
+//   point-order sum.  in = x, p, dx0, dp0 (n each) + dsigma0; out = dx, dp, dsigma.
+int cmd_gauss_shared_in(int argc, char** argv) {
+  if (argc < 6) die("gauss-shared-in <n> <sigma> <block> <in> <out>");
+  const int64_t n = std::atoll(argv[1]);
+  const double sigma = std::atof(argv[2]);
+  const int64_t block = std::atoll(argv[3]);
+  std::vector<double> all = read_f64(argv[4], static_cast<size_t>(4 * n + 1));
+  Program prog(load_named("kernels"));
+  LaunchConfig cfg{n / block + 1, block, n};
+  BufferSet b;
+  b.arrays["x"].assign(all.begin(), all.begin() + n);
+  b.arrays["p"].assign(all.begin() + n, all.begin() + 2 * n);
+  b.arrays["dx"].assign(all.begin() + 2 * n, all.begin() + 3 * n);
+  b.arrays["dp"].assign(all.begin() + 3 * n, all.begin() + 4 * n);
+  b.arrays["dsigma"].assign(1, all[4 * n]);
+  b.scalars["sigma"] = sigma;
+  bool refused = false;
+  try {
+    launch(prog, "compute_shared", cfg, b);
+  } catch (const Error& e) {
+    refused = e.kind() == ErrorKind::Launch;
+  }
+  LaunchOptions lo;
+  lo.unsafe = true;
+  lo.sequential = true;
+  launch(prog, "compute_shared", cfg, b, lo);
+  std::ofstream out(argv[5], std::ios::binary);
+  write_f64(out, b.arrays["dx"]);
+  write_f64(out, b.arrays["dp"]);
+  write_f64(out, b.arrays["dsigma"]);
+  std::printf("{\"n\": %lld, \"refused_by_default\": %s}\n", (long long)n,
+              refused ? "true" : "false");
+  return refused ? 0 : 1;
+}
+
 // gaussnd-in <dim> <n> <sigma> <in.bin> <out.bin> [workers]
 //   in = x, p, dx0, dp0 in structure-of-arrays layout ([d*n + i]); each point
 //   is gathered into contiguous rows and run through
@@ -737,6 +777,7 @@ int main(int argc, char** argv) {
     if (cmd == "gauss1d") return cmd_gauss1d(argc - 1, argv + 1);
     if (cmd == "gauss1d-in") return cmd_gauss1d_in(argc - 1, argv + 1);
     if (cmd == "gaussnd-in") return cmd_gaussnd_in(argc - 1, argv + 1);
+    if (cmd == "gauss-shared-in") return cmd_gauss_shared_in(argc - 1, argv + 1);
     if (cmd == "chi2-in") return cmd_chi2_in(argc - 1, argv + 1);
     if (cmd == "fit-in") return cmd_fit_in(argc - 1, argv + 1);
     if (cmd == "gaussnd-bench") return cmd_gaussnd_bench(argc - 1, argv + 1);

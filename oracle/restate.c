@@ -49,6 +49,92 @@ void rs_gauss_grad_batch(const double* x, const double* p, double sigma, double*
   for (int64_t g = 0; g < n; ++g) gauss_grad_0_1(x[g], p[g], sigma, dx + g, dp + g);
 }
 
+/* gauss_grad (all of x, p, sigma): the printed output of
+ * differentiate_gradient(gauss, {x, p, sigma}) (ref_tool print kernels gauss
+ * x p sigma), statement for statement.  The three _d_sigma[0] += statements
+ * are returned separately in sig[0..2] so the caller decides how they reach
+ * the shared slot. */
+static void gauss_grad_all(double x, double p, double sigma, double* _d_x, double* _d_p,
+                           double* sig) {
+  double _d__t0 = 0, _d__t1 = 0, _d__t2 = 0, _d__t3 = 0, _d__t4 = 0, _d_t = 0, _d__t7 = 0,
+         _d__t8 = 0, _d__t9 = 0, _d__t10 = 0;
+  double _t0 = x - p;
+  double _t1 = -_t0;
+  double _t2 = _t1 * _t0;
+  double _t3 = 2 * sigma;
+  double _t4 = _t3 * sigma;
+  double t = _t2 / _t4;
+  double _t5 = 2 * kPI;
+  double _t6 = pow(_t5, -0.5);
+  double _t7 = pow(sigma, -0.5);
+  double _t8 = _t6 * _t7;
+  double _t9 = exp(t);
+  _d__t10 += 1;
+  double _r0 = _d__t10;
+  _d__t8 += _r0 * _t9;
+  _d__t9 += _t8 * _r0;
+  double _r1 = _d__t9;
+  double _q0 = _t9;
+  _d_t += _r1 * _q0;
+  double _r2 = _d__t8;
+  _d__t7 += _t6 * _r2;
+  double _r3 = _d__t7;
+  sig[0] = _r3 * (-0.5 * pow(sigma, -1.5));
+  double _r4 = _d_t;
+  double _q1 = t;
+  _d__t2 += _r4 / _t4;
+  _d__t4 += -(_r4 * _q1 / _t4);
+  double _r5 = _d__t4;
+  _d__t3 += _r5 * sigma;
+  sig[1] = _t3 * _r5;
+  double _r6 = _d__t3;
+  sig[2] = 2 * _r6;
+  double _r7 = _d__t2;
+  _d__t1 += _r7 * _t0;
+  _d__t0 += _t1 * _r7;
+  double _r8 = _d__t1;
+  _d__t0 += -_r8;
+  double _r9 = _d__t0;
+  _d_x[0] += _r9;
+  _d_p[0] += -_r9;
+}
+
+void rs_gauss_grad_shared_batch(const double* x, const double* p, double sigma, double* dx,
+                                double* dp, double* dsigma, int64_t n) {
+  for (int64_t g = 0; g < n; ++g) {
+    double sig[3];
+    gauss_grad_all(x[g], p[g], sigma, dx + g, dp + g, sig);
+    dsigma[0] += sig[0];
+    dsigma[0] += sig[1];
+    dsigma[0] += sig[2];
+  }
+}
+
+/* ---- compensated (Neumaier) sums ------------------------------------------ */
+typedef struct { double s, c; } nsum;
+static void nadd(nsum* a, double v) {
+  double t = a->s + v;
+  if (fabs(a->s) >= fabs(v)) a->c += (a->s - t) + v;
+  else a->c += (v - t) + a->s;
+  a->s = t;
+}
+static double nval(const nsum* a) { return a->s + a->c; }
+
+void rs_gauss_shared_dsigma_compensated(const double* x, const double* p, double sigma, int64_t n,
+                                        double* total, double* abs_total) {
+  nsum s = {0, 0}, a = {0, 0};
+  for (int64_t g = 0; g < n; ++g) {
+    double sig[3], dx = 0, dp = 0;
+    gauss_grad_all(x[g], p[g], sigma, &dx, &dp, sig);
+    for (int k = 0; k < 3; ++k) {
+      nadd(&s, sig[k]);
+      nadd(&a, fabs(sig[k]));
+    }
+  }
+  *total = nval(&s);
+  *abs_total = nval(&a);
+}
+
 /* gaussnd_grad_0_1 as emitted by differentiate_gradient (reverse.cpp:335-553):
  * forward loop pushes _t0,_t1,t; reverse loop pops them.  Only _t0 is read by
  * an adjoint rule, so the tape is replaced by the per-element recomputation
@@ -318,14 +404,6 @@ void rs_chi2_gradient_p(int model, int provider, const double* counts, int64_t b
 }
 
 /* ---- compensated (Neumaier) variants -------------------------------------- */
-typedef struct { double s, c; } nsum;
-static void nadd(nsum* a, double v) {
-  double t = a->s + v;
-  if (fabs(a->s) >= fabs(v)) a->c += (a->s - t) + v;
-  else a->c += (v - t) + a->s;
-  a->s = t;
-}
-static double nval(const nsum* a) { return a->s + a->c; }
 
 void rs_chi2_gradient_compensated(int model, const double* counts, int64_t bins, double lo,
                                   double hi, double events, const double* q, int64_t np,

@@ -5,6 +5,8 @@
  * Every function transcribes the code the reference generates or runs, one
  * IEEE operation per source operation, compiled with -ffp-contract=off:
  *   rs_gauss_grad_0_1   <- proj/tests/golden/gauss_grad_0_1.golden:1-42
+ *   rs_gauss_grad_shared_batch <- compute_shared (kernels.dsl:16-21) calling
+ *                          differentiate_gradient(gauss, {x, p, sigma})
  *   rs_gaussnd_grad_0_1 <- differentiate_gradient(gaussnd,{x,p}) output
  *                          (oracle/dsl/gaussnd.dsl; reverse.cpp:703-725)
  *   rs_gsum / rs_gsum_grad_1   <- fit.cpp:125-138 model + its generated gradient
@@ -32,6 +34,16 @@ enum { RS_PROVIDER_AD = 0, RS_PROVIDER_NUMERIC = 1 };
 /* Listing-1 batch: for g in [0,n): gauss_grad_0_1(x[g],p[g],sigma,&dx[g],&dp[g]) */
 void rs_gauss_grad_batch(const double* x, const double* p, double sigma, double* dx, double* dp,
                          int64_t n);
+
+/* compute_shared (kernels.dsl:16-21) forced sequential: gauss_grad over x, p,
+ * sigma per point; dx, dp private, the three sigma contributions added to
+ * dsigma[0] in point order (launch with LaunchOptions{unsafe, sequential}). */
+void rs_gauss_grad_shared_batch(const double* x, const double* p, double sigma, double* dx,
+                                double* dp, double* dsigma, int64_t n);
+/* Compensated total of all sigma contributions and of their magnitudes (the
+ * tolerance scale for an order-changed reduction). */
+void rs_gauss_shared_dsigma_compensated(const double* x, const double* p, double sigma, int64_t n,
+                                        double* total, double* abs_total);
 
 /* N-dim batch over structure-of-arrays rows: element (d, i) at [d*ld + i]. */
 void rs_gaussnd_grad_batch(const double* x, const double* p, double sigma, int64_t dim, int64_t n,

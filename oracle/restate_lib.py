@@ -29,6 +29,8 @@ class Restate:
         self.lib = lib
         i64, d, i = ctypes.c_int64, ctypes.c_double, ctypes.c_int
         lib.rs_gauss_grad_batch.argtypes = [_D, _D, d, _D, _D, i64]
+        lib.rs_gauss_grad_shared_batch.argtypes = [_D, _D, d, _D, _D, _D, i64]
+        lib.rs_gauss_shared_dsigma_compensated.argtypes = [_D, _D, d, i64, _D, _D]
         lib.rs_gaussnd_grad_batch.argtypes = [_D, _D, d, i64, i64, i64, _D, _D]
         lib.rs_model.argtypes = [i, d, _D, i64]
         lib.rs_model.restype = d
@@ -47,6 +49,17 @@ class Restate:
     def gauss_grad(self, x, p, sigma, dx, dp):
         """In-place accumulate, like the reference slots."""
         self.lib.rs_gauss_grad_batch(_p(x), _p(p), sigma, _p(dx), _p(dp), x.size)
+
+    def gauss_grad_shared(self, x, p, sigma, dx, dp, dsigma):
+        """compute_shared, forced sequential: accumulates into dx, dp, dsigma[0]."""
+        self.lib.rs_gauss_grad_shared_batch(_p(x), _p(p), sigma, _p(dx), _p(dp), _p(dsigma),
+                                            x.size)
+
+    def gauss_shared_dsigma_compensated(self, x, p, sigma):
+        """(total, sum of magnitudes) of every sigma contribution."""
+        t, a = np.zeros(1), np.zeros(1)
+        self.lib.rs_gauss_shared_dsigma_compensated(_p(x), _p(p), sigma, x.size, _p(t), _p(a))
+        return float(t[0]), float(a[0])
 
     def gaussnd_grad(self, x, p, sigma, dx, dp):
         dim, n = x.shape

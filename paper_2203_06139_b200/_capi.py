@@ -70,6 +70,10 @@ SIGNATURES = {
     "adc_cuda_registry_fingerprint": (ctypes.c_uint64, [_I32]),
     "adc_cuda_compute_gauss": (ctypes.c_int, [_I64, _I64, _I64, _VP, _VP, _DBL, _VP, _VP, _VP]),
     "adc_cuda_compute_gauss_host": (ctypes.c_int, [_I64, _I64, _I64, _VP, _VP, _DBL, _VP, _VP]),
+    "adc_cuda_compute_gauss_shared": (ctypes.c_int, [_I64, _I64, _I64, _VP, _VP, _DBL, _VP, _VP,
+                                                     _VP, _I32, _VP]),
+    "adc_cuda_compute_gauss_shared_host": (ctypes.c_int, [_I64, _I64, _I64, _VP, _VP, _DBL, _VP,
+                                                          _VP, _VP, _I32]),
     "adc_cuda_gaussnd_grad": (ctypes.c_int, [_I64, _I64, _I64, _VP, _VP, _DBL, _VP, _VP, _VP]),
     "adc_cuda_gaussnd_grad_host": (ctypes.c_int, [_I64, _I64, _I64, _VP, _VP, _DBL, _VP, _VP]),
     "adc_cuda_gaussnd_set_variant": (ctypes.c_int, [_I32]),

@@ -15,6 +15,9 @@ int launch_gauss_grad(int64_t n, const double* x, const double* p, double sigma,
 int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, const double* p,
                         double sigma, double* dx, double* dp, cudaStream_t s);
 int gaussnd_set_variant(int v);
+int64_t gauss_shared_blocks(int64_t n);
+int launch_gauss_shared(int64_t n, const double* x, const double* p, double sigma, double* dx,
+                        double* dp, double* dsigma, double* partials, cudaStream_t stream);
 
 static thread_local std::string t_error;
 
@@ -168,6 +171,7 @@ constexpr RegEntry kRegistry[] = {
     {"gaussnd_grad_0_1", 0x4676b5ba30fbac81ull},
     {"gsum_grad_1", 0x04bab8a0562c8d71ull},
     {"gpoly_grad_1", 0xfe0da677548ccdafull},
+    {"gauss_grad", 0xba4901bef94e1d4dull},  // compute_shared's callee (x, p, sigma)
 };
 constexpr int32_t kRegistrySize = sizeof(kRegistry) / sizeof(kRegistry[0]);
 }  // namespace
@@ -254,6 +258,65 @@ extern "C" int adc_cuda_compute_gauss_host(int64_t grid, int64_t block, int64_t 
   ADCB_CUDA(cudaStreamSynchronize(g_staging.stream[0]));
   ADCB_CUDA(cudaStreamSynchronize(g_staging.stream[1]));
   return ADC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// compute_shared: race_check flags dsigma (launch.cpp:112-240); refused unless
+// forced (launch.cpp:261-267, same message); forced runs are deterministic.
+static int refuse_shared(int32_t unsafe) {
+  if (unsafe) return ADC_OK;
+  return fail(ADC_E_LAUNCH,
+              "launch refused, hazardous parameter(s): dsigma (whole array shared with a writing "
+              "callee across threads); pass the unsafe flag to force");
+}
+
+extern "C" int adc_cuda_compute_gauss_shared(int64_t grid, int64_t block, int64_t n,
+                                             const double* x, const double* p, double sigma,
+                                             double* dx, double* dp, double* dsigma,
+                                             int32_t unsafe, void* stream) {
+  clear_error();
+  if (int rc = validate_config(grid, block, n)) return rc;
+  if (int rc = refuse_shared(unsafe)) return rc;
+  if (!x || !p || !dx || !dp || !dsigma) return fail(ADC_E_LAUNCH, "missing buffer");
+  if (int rc = require_device()) return rc;
+  // CTA partials of the dsigma reduction: stream-ordered scratch.
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* ws = nullptr;
+  ADCB_CUDA(cudaMallocAsync(&ws, (size_t)gauss_shared_blocks(n) * sizeof(double), s));
+  const int rc = launch_gauss_shared(n, x, p, sigma, dx, dp, dsigma, ws, s);
+  cudaFreeAsync(ws, s);
+  return rc;
+}
+
+extern "C" int adc_cuda_compute_gauss_shared_host(int64_t grid, int64_t block, int64_t n,
+                                                  const double* x, const double* p, double sigma,
+                                                  double* dx, double* dp, double* dsigma,
+                                                  int32_t unsafe) {
+  clear_error();
+  if (int rc = validate_config(grid, block, n)) return rc;
+  if (int rc = refuse_shared(unsafe)) return rc;
+  if (!x || !p || !dx || !dp || !dsigma) return fail(ADC_E_LAUNCH, "missing buffer");
+  if (int rc = require_device()) return rc;
+  // One device copy of every buffer (the reduction spans all points).
+  double* d = nullptr;
+  const size_t bytes = (size_t)n * sizeof(double);
+  ADCB_CUDA(cudaMalloc(&d, 4 * bytes + 1184 * sizeof(double) + sizeof(double)));
+  double *X = d, *P = d + n, *DX = d + 2 * n, *DP = d + 3 * n, *WS = d + 4 * n, *DS = WS + 1184;
+  auto run = [&]() -> int {
+    ADCB_CUDA(cudaMemcpy(X, x, bytes, cudaMemcpyHostToDevice));
+    ADCB_CUDA(cudaMemcpy(P, p, bytes, cudaMemcpyHostToDevice));
+    ADCB_CUDA(cudaMemcpy(DX, dx, bytes, cudaMemcpyHostToDevice));
+    ADCB_CUDA(cudaMemcpy(DP, dp, bytes, cudaMemcpyHostToDevice));
+    ADCB_CUDA(cudaMemcpy(DS, dsigma, sizeof(double), cudaMemcpyHostToDevice));
+    if (int rc = launch_gauss_shared(n, X, P, sigma, DX, DP, DS, WS, nullptr)) return rc;
+    ADCB_CUDA(cudaMemcpy(dx, DX, bytes, cudaMemcpyDeviceToHost));
+    ADCB_CUDA(cudaMemcpy(dp, DP, bytes, cudaMemcpyDeviceToHost));
+    ADCB_CUDA(cudaMemcpy(dsigma, DS, sizeof(double), cudaMemcpyDeviceToHost));
+    return ADC_OK;
+  };
+  const int rc = run();
+  cudaFree(d);
+  return rc;
 }
 
 // ---------------------------------------------------------------------------

@@ -105,20 +105,23 @@ def _stream_of(a):
 
 def launch(kernel: str, cfg: LaunchConfig, buffers: BufferSet,
            opts: LaunchOptions | None = None, callee_fingerprint: int | None = None) -> LaunchStats:
-    """adc::launch (launch.cpp:252-346) for the Listing-1 kernels of kernels.dsl."""
+    """adc::launch (launch.cpp:252-346) for the Listing-1 kernels of kernels.dsl:
+    `compute` (private slots) and `compute_shared` (the shared dsigma slot:
+    refused unless opts.unsafe, then reduced in a fixed order, deterministic)."""
     opts = opts or LaunchOptions()
     cfg.validate()
-    if kernel == "compute_shared":
+    shared = kernel == "compute_shared"
+    if shared:
         # race_check reports dsigma as a shared-write hazard (launch.cpp:261-267).
         if not opts.unsafe:
             raise AdcError("Launch", "launch refused, hazardous parameter(s): dsigma (whole array "
                                      "shared with a writing callee across threads); pass the "
                                      "unsafe flag to force")
-        raise AdcError("Launch", "no B200 kernel registered for 'gauss_grad'")
-    if kernel != "compute":
+    elif kernel != "compute":
         raise AdcError("Launch", f"unknown kernel '{kernel}'")
-    fp = _fingerprints()["gauss_grad_0_1"] if callee_fingerprint is None else callee_fingerprint
-    registry_find("gauss_grad_0_1", fp)
+    callee = "gauss_grad" if shared else "gauss_grad_0_1"
+    fp = _fingerprints()[callee] if callee_fingerprint is None else callee_fingerprint
+    registry_find(callee, fp)
     arrs = {}
     for name, typ in COMPUTE_PARAMS:
         if typ == "real[]":
@@ -134,16 +137,32 @@ def launch(kernel: str, cfg: LaunchConfig, buffers: BufferSet,
             raise AdcError("Launch", f"missing scalar value '{name}'")
     sigma = float(buffers.scalars["sigma"])
     x, p, dx, dp = (arrs[k] for k in ("x", "p", "dx", "dp"))
-    if _is_torch(x):
-        for a in (x, p, dx, dp):
-            if not (a.is_cuda and a.is_contiguous()) or str(a.dtype) != "torch.float64":
+    for a in (x, p, dx, dp):
+        if _is_torch(x):
+            if not (_is_torch(a) and a.is_cuda and a.is_contiguous()) or \
+                    str(a.dtype) != "torch.float64":
                 raise AdcError("Launch", "device buffers must be contiguous float64 CUDA tensors")
+        elif _is_torch(a) or a.dtype != np.float64 or not a.flags.c_contiguous:
+            raise AdcError("Launch", "host buffers must be contiguous float64 arrays")
+    if shared:
+        if "dsigma" not in buffers.arrays:
+            raise AdcError("Launch", "missing buffer 'dsigma'")
+        ds = buffers.arrays["dsigma"]
+        if (ds.numel() if _is_torch(ds) else ds.size) < 1:
+            raise AdcError("Launch", "buffer 'dsigma' is empty")
+        if _is_torch(x):
+            check(lib.adc_cuda_compute_gauss_shared(cfg.grid_dim, cfg.block_dim, cfg.n, dptr(x),
+                                                    dptr(p), sigma, dptr(dx), dptr(dp), dptr(ds),
+                                                    1, _stream_of(x)))
+        else:
+            check(lib.adc_cuda_compute_gauss_shared_host(cfg.grid_dim, cfg.block_dim, cfg.n,
+                                                         dptr(x), dptr(p), sigma, dptr(dx),
+                                                         dptr(dp), dptr(ds), 1))
+        return LaunchStats(active=cfg.n, idle=cfg.grid_dim * cfg.block_dim - cfg.n)
+    if _is_torch(x):
         check(lib.adc_cuda_compute_gauss(cfg.grid_dim, cfg.block_dim, cfg.n, dptr(x), dptr(p),
                                          sigma, dptr(dx), dptr(dp), _stream_of(x)))
     else:
-        for a in (x, p, dx, dp):
-            if a.dtype != np.float64 or not a.flags.c_contiguous:
-                raise AdcError("Launch", "host buffers must be contiguous float64 arrays")
         check(lib.adc_cuda_compute_gauss_host(cfg.grid_dim, cfg.block_dim, cfg.n, dptr(x),
                                               dptr(p), sigma, dptr(dx), dptr(dp)))
     return LaunchStats(active=cfg.n, idle=cfg.grid_dim * cfg.block_dim - cfg.n)

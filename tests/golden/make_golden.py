@@ -52,7 +52,8 @@ def main():
     # are committed, not the generated text.
     assert run("golden-check")["golden_match"]
     fps = {}
-    for mod, fn, wrt in (("kernels", "gauss", ("x", "p")), ("gaussnd", "gaussnd", ("x", "p")),
+    for mod, fn, wrt in (("kernels", "gauss", ("x", "p")), ("kernels", "gauss", ("x", "p", "sigma")),
+                         ("gaussnd", "gaussnd", ("x", "p")),
                          ("gpoly", "gpoly", ("q",)), ("gsum", "gsum", ("q",))):
         text = run("print", mod, fn, *wrt)
         name = text.split("(")[0].split()[-1]
@@ -84,6 +85,22 @@ def main():
         cases[name] = dict(x=x, p=p, dx0=dx0, dp0=dp0, dx=o[0], dp=o[1], sigma=sigma, block=block)
     np.savez(os.path.join(OUT, "gauss1d_cases.npz"),
              **{f"{k}_{f}": v for k, d in cases.items() for f, v in d.items()})
+
+    # compute_shared (kernels.dsl:16-21): refused by default, forced sequential
+    # point-order accumulation into the shared dsigma slot.
+    sh = {}
+    for name, n, sigma, block, seed in (("n100", 100, 1.3, 32, 21), ("n4097", 4097, 0.9, 256, 22)):
+        r = np.random.Generator(np.random.PCG64(seed))
+        x, p = r.uniform(-3, 3, n), r.uniform(-2, 2, n)
+        dx0, dp0, ds0 = r.standard_normal(n), r.standard_normal(n), np.array([0.25])
+        np.concatenate([x, p, dx0, dp0, ds0]).astype("<f8").tofile(ti)
+        meta = run("gauss-shared-in", n, sigma, block, ti, to)
+        assert meta["refused_by_default"]
+        o = f64(to, 2 * n + 1)
+        sh.update({f"{name}_x": x, f"{name}_p": p, f"{name}_dx0": dx0, f"{name}_dp0": dp0,
+                   f"{name}_dsigma0": ds0, f"{name}_dx": o[:n], f"{name}_dp": o[n:2 * n],
+                   f"{name}_dsigma": o[2 * n:], f"{name}_sigma": sigma, f"{name}_block": block})
+    np.savez(os.path.join(OUT, "gauss_shared_cases.npz"), **sh)
 
     # N-dim Gaussian, SoA layout, nonzero initial slots (accumulate semantics).
     nd = {}

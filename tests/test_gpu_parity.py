@@ -352,3 +352,62 @@ def test_numeric_provider_probe_domain_error():
     with pytest.raises(adc.AdcError) as e:
         adc.FitEngine("gpoly", 6).chi2_gradient(h, [1, 0, h0, 0, 0, 0], adc.GradientProvider.Numeric)
     assert e.value.kind == "Eval"
+
+
+# ---------------------------------------------------------------------------- compute_shared
+@pytest.mark.parametrize("case", ["n100", "n4097"])
+@pytest.mark.parametrize("device", [True, False])
+def test_compute_shared_forced_deterministic(restate, case, device):
+    """compute_shared (kernels.dsl:16-21) forced: dx, dp per point within 1e-12
+    (as `compute`); dsigma = dsigma0 + a fixed-order sum of all contributions,
+    within 1e-12 * sum|contributions| of the compensated total and within the
+    reference's own 1e-9 (test_launch.cpp:165) of its sequential result;
+    identical bits on every run."""
+    g = golden("gauss_shared_cases.npz")
+    n, sigma, block = g[f"{case}_x"].size, float(g[f"{case}_sigma"]), int(g[f"{case}_block"])
+    cfg = adc.LaunchConfig(n // block + 1, block, n)
+
+    def run():
+        arrs = {k: g[f"{case}_{k}"].copy() for k in ("x", "p")}
+        arrs.update(dx=g[f"{case}_dx0"].copy(), dp=g[f"{case}_dp0"].copy(),
+                    dsigma=g[f"{case}_dsigma0"].copy())
+        if device:
+            arrs = {k: t(v) for k, v in arrs.items()}
+        adc.launch("compute_shared", cfg, adc.BufferSet(arrays=arrs, scalars={"sigma": sigma}),
+                   adc.LaunchOptions(unsafe=True))
+        return {k: host(v) if device else v for k, v in arrs.items()}
+
+    a = run()
+    assert rel_err(a["dx"], g[f"{case}_dx"]).max() <= REL
+    assert rel_err(a["dp"], g[f"{case}_dp"]).max() <= REL
+    tot, scale = restate.gauss_shared_dsigma_compensated(g[f"{case}_x"], g[f"{case}_p"], sigma)
+    d0 = g[f"{case}_dsigma0"][0]
+    assert abs(a["dsigma"][0] - (d0 + tot)) <= 1e-12 * (scale + abs(d0))
+    assert rel_err(a["dsigma"][0], g[f"{case}_dsigma"][0]) <= 1e-9
+    b = run()
+    assert a["dsigma"].tobytes() == b["dsigma"].tobytes()
+
+
+def test_compute_shared_large_vs_oracle(restate):
+    n = 3_000_017
+    rng = np.random.Generator(np.random.PCG64(4))
+    x, p = rng.uniform(-3, 3, n), rng.uniform(-2, 2, n)
+    dx, dp, ds = np.zeros(n), np.zeros(n), np.zeros(1)
+    bufs = {"x": t(x), "p": t(p), "dx": t(dx), "dp": t(dp), "dsigma": t(ds)}
+    adc.launch("compute_shared", adc.LaunchConfig(n // 256 + 1, 256, n),
+               adc.BufferSet(arrays=bufs, scalars={"sigma": 1.1}), adc.LaunchOptions(unsafe=True))
+    rx, rp, rs = np.zeros(n), np.zeros(n), np.zeros(1)
+    restate.gauss_grad_shared(x, p, 1.1, rx, rp, rs)
+    assert rel_err(host(bufs["dx"]), rx).max() <= REL
+    tot, scale = restate.gauss_shared_dsigma_compensated(x, p, 1.1)
+    assert abs(host(bufs["dsigma"])[0] - tot) <= 1e-12 * scale
+
+
+def test_compute_shared_refused_without_unsafe():
+    n = 64
+    bufs = {k: t(np.zeros(n)) for k in ("x", "p", "dx", "dp")}
+    bufs["dsigma"] = t(np.zeros(1))
+    with pytest.raises(adc.AdcError) as e:
+        adc.launch("compute_shared", adc.LaunchConfig(1, 64, n),
+                   adc.BufferSet(arrays=bufs, scalars={"sigma": 1.0}))
+    assert e.value.kind == "Launch" and str(e.value).startswith("launch refused")

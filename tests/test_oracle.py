@@ -68,7 +68,23 @@ def test_chi2_bitexact_and_compensated(restate, key):
 def test_fingerprints_file():
     with open(os.path.join(GOLDEN, "gradient_fingerprints.json")) as fh:
         fps = json.load(fh)
-    assert set(fps) == {"gauss_grad_0_1", "gaussnd_grad_0_1", "gpoly_grad_1", "gsum_grad_1"}
+    assert set(fps) == {"gauss_grad", "gauss_grad_0_1", "gaussnd_grad_0_1", "gpoly_grad_1",
+                        "gsum_grad_1"}
+
+
+@pytest.mark.parametrize("case", ["n100", "n4097"])
+def test_gauss_shared_sequential_bitexact(restate, case):
+    # compute_shared forced sequential (test_launch.cpp:148-153): the restatement
+    # is the reference's own arithmetic and order, bit for bit.
+    g = golden("gauss_shared_cases.npz")
+    dx, dp, ds = g[f"{case}_dx0"].copy(), g[f"{case}_dp0"].copy(), g[f"{case}_dsigma0"].copy()
+    restate.gauss_grad_shared(g[f"{case}_x"], g[f"{case}_p"], float(g[f"{case}_sigma"]), dx, dp, ds)
+    assert dx.tobytes() == g[f"{case}_dx"].tobytes()
+    assert dp.tobytes() == g[f"{case}_dp"].tobytes()
+    assert ds.tobytes() == g[f"{case}_dsigma"].tobytes()
+    tot, scale = restate.gauss_shared_dsigma_compensated(g[f"{case}_x"], g[f"{case}_p"],
+                                                         float(g[f"{case}_sigma"]))
+    assert abs((g[f"{case}_dsigma0"][0] + tot) - g[f"{case}_dsigma"][0]) <= 1e-12 * (scale + 0.25)
 
 
 @pytest.mark.parametrize("key", ["gpoly_b2000", "gsum1_b1000", "gsum2_b1500"])
