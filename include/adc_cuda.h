@@ -160,11 +160,15 @@ int adc_chi2_finalize(int32_t np, double events, const double* records, int64_t 
 typedef struct adc_chi2_plan adc_chi2_plan;
 /* counts: DEVICE pointer to the full histogram (float64[bins]); only this
  * rank's bin range is read.  The plan owns its workspace, a CUDA graph per
- * pass kind and a pinned result buffer. */
+ * pass kind and a pinned result buffer.  What depends on the counts alone
+ * (1/c per bin, 8 B/bin of device memory, and the q-independent chunk sums)
+ * is computed once, before the first pass: call adc_cuda_chi2_plan_refresh
+ * after changing the counts in place. */
 int adc_cuda_chi2_plan_create(adc_chi2_plan** plan, int32_t model, int32_t np, int64_t bins,
                               double lo, double hi, double events, const double* counts,
                               int32_t world, int32_t rank, void* stream);
 int adc_cuda_chi2_plan_destroy(adc_chi2_plan* plan);
+int adc_cuda_chi2_plan_refresh(adc_chi2_plan* plan);
 int adc_cuda_chi2_plan_layout(const adc_chi2_plan* plan, adc_chi2_layout* out);
 /* Enqueue this rank's pass: chunk records for [chunk_begin, chunk_end) are
  * written to records_dev + (chunk - chunk_begin) * record_len (device

@@ -83,6 +83,7 @@ SIGNATURES = {
     "adc_cuda_chi2_plan_create": (ctypes.c_int, [ctypes.POINTER(_VP), _I32, _I32, _I64, _DBL,
                                                  _DBL, _DBL, _VP, _I32, _I32, _VP]),
     "adc_cuda_chi2_plan_destroy": (ctypes.c_int, [_VP]),
+    "adc_cuda_chi2_plan_refresh": (ctypes.c_int, [_VP]),
     "adc_cuda_chi2_plan_layout": (ctypes.c_int, [_VP, ctypes.POINTER(Chi2Layout)]),
     "adc_cuda_chi2_partials": (ctypes.c_int, [_VP, _D, _I32, _VP]),
     "adc_cuda_chi2_plan_records": (_VP, [_VP]),

@@ -6,7 +6,11 @@
 // evaluated in registers and folded into
 //   S += m; [c>0]: A1 += m; A2 += m*(m/c); C0 += c; G1 += dm; G2 += (m/c) dm
 //   G0 += dm
-// (record layout [S, A1, A2, C0, G0[np], G1[np], G2[np]]).  adc_chi2_finalize
+// (record layout [S, A1, A2, C0, G0[np], G1[np], G2[np]]).
+// Everything that depends on the counts alone is computed once per plan
+// (K0 chi2_inverse_kernel: ic_j = [c_j > 0] / c_j, IEEE-rounded; K3l
+// chi2_lin_kernel: C0 and the linear parameters' G0/G1), so a pass streams
+// ic (8 B/bin) and spends its FP64 work on the model and its gradient only.  adc_chi2_finalize
 // (chi2_host.cpp) turns the records into chi2 and its gradient with the exact
 // algebra of fit.cpp:231-258 (see include/adc_cuda.h).
 //
@@ -51,15 +55,6 @@ static_assert(sizeof(QDev) + sizeof(QNum) == kQDoubles * sizeof(double), "QDev l
 // ---- fast-mode math ----------------------------------------------------------
 // exp_nonpos (fastmath.cuh): table-driven exp for the models' non-positive
 // arguments, ~11 FP64 ops with its constants in uniform registers.
-// 1/c for a positive count: MUFU.RCP64H seed + two Newton steps.
-__device__ __forceinline__ double rcp_pos(double c) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(c));
-  double e = __fma_rn(-c, r, 1.0);
-  r = __fma_rn(r, e, r);
-  e = __fma_rn(-c, r, 1.0);
-  return __fma_rn(r, e, r);
-}
 
 // ---- models ------------------------------------------------------------------
 // gpoly (oracle/dsl/gpoly.dsl) and its generated gpoly_grad_1; gsum
@@ -176,11 +171,12 @@ struct GSum {
 };
 
 // ---- K3: tile pass -------------------------------------------------------------
-// Per thread: bins base + k*256 (k < BPT) in increasing k, counts streamed
+// Per thread: bins base + k*256 (k < BPT) in increasing k, ic streamed
 // through a PD-deep register ring (+ an L2 prefetch of the next tile), so the
 // FP64 pipe is not left waiting on HBM.  Accumulation is branch-free: with
-// w = [c > 0] and ic = [c > 0]/c,
-//   S += m; A1 += w m; A2 += m (m ic); C0 += c; G0 += dm; G1 += w dm; G2 += (m ic) dm.
+// w = [c > 0] = [ic > 0] and ic = [c > 0]/c,
+//   S += m; A1 += w m; A2 += m (m ic); G0 += dm; G1 += w dm; G2 += (m ic) dm
+// (C0 and the linear parameters' G0/G1 come from the once-per-plan K3l pass).
 // Full tiles skip the per-bin bounds test.
 constexpr int kPD = 4;
 
@@ -194,7 +190,7 @@ constexpr int tile_min_blocks() {
 
 template <class M, bool GRAD, bool FAST>
 struct BinTerm {
-  double m, c, w, mc;
+  double m, w, mc;
   double bg[GRAD ? M::NP : 1];
 };
 
@@ -221,16 +217,14 @@ __device__ __forceinline__ void numeric_fold(double x, const typename M::Reg& QR
 }
 
 // jh = j + 0.5 exactly (j < 2^52), so x is bit-identical to Histogram::center.
+// ic = [c > 0] / c from the plan's K0 pass (so ic > 0 exactly when c > 0).
 template <class M, bool GRAD, bool FAST>
 __device__ __forceinline__ void bin_term(const Chi2Pass& P, const typename M::Reg& QR,
-                                         const double* tab, double jh, double c,
+                                         const double* tab, double jh, double ic,
                                          BinTerm<M, GRAD, FAST>& t) {
   const double x = fadd(P.lo, fmul(jh, P.width));  // Histogram::center: lo + (j + 0.5) * width
   M::template eval<GRAD, FAST>(x, QR, tab, t.m, t.bg);
-  const bool pos = c > 0.0;
-  t.c = c;
-  t.w = pos ? 1.0 : 0.0;
-  const double ic = pos ? (FAST ? rcp_pos(c) : 1.0 / c) : 0.0;
+  t.w = ic > 0.0 ? 1.0 : 0.0;
   t.mc = t.m * ic;
 }
 
@@ -241,7 +235,7 @@ __device__ __forceinline__ void bin_accumulate(const BinTerm<M, GRAD, FAST>& t, 
   acc[0] += t.m;
   acc[1] = __fma_rn(t.w, t.m, acc[1]);
   acc[2] = __fma_rn(t.m, t.mc, acc[2]);
-  acc[3] += t.c;
+  // acc[3] (C0) comes from the K3l pre-pass
   if constexpr (GRAD) {
 #pragma unroll
     for (int i = 0; i < NP; ++i) {
@@ -268,7 +262,7 @@ __device__ __forceinline__ void tile_bins(const Chi2Pass& P, const typename M::R
 #pragma unroll
   for (int k = 0; k < PD; ++k) {
     const int64_t j = base + (int64_t)k * kTileThreads;
-    ring[k] = (!CHECK || j < P.bin_end) ? ld_stream(P.counts + j) : 0.0;
+    ring[k] = (!CHECK || j < P.bin_end) ? ld_stream(P.icounts + j) : 0.0;
   }
   double jh = fadd((double)base, 0.5);  // advanced by 256.0 per bin: exact integers + 0.5
   for (int k0 = 0; k0 < BPT; k0 += PD) {
@@ -282,7 +276,7 @@ __device__ __forceinline__ void tile_bins(const Chi2Pass& P, const typename M::R
         const int64_t j = base + (int64_t)k * kTileThreads;
         const double c = ring[kk + u];
         const int64_t jn = j + (int64_t)PD * kTileThreads;
-        ring[kk + u] = (k + PD < BPT && (!CHECK || jn < P.bin_end)) ? ld_stream(P.counts + jn)
+        ring[kk + u] = (k + PD < BPT && (!CHECK || jn < P.bin_end)) ? ld_stream(P.icounts + jn)
                                                                      : 0.0;
         valid[u] = !CHECK || j < P.bin_end;
         if constexpr (NUM) {
@@ -342,7 +336,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) chi2_tile_kernel(Chi2Pass 
 #pragma unroll 4
       for (int k = 0; k < BPT; k += 4)
         if (nb + (int64_t)k * kTileThreads < P.bin_end)
-          prefetch_l2(P.counts + nb + (int64_t)k * kTileThreads);
+          prefetch_l2(P.icounts + nb + (int64_t)k * kTileThreads);
     }
     double acc[R];
 #pragma unroll
@@ -413,30 +407,27 @@ __global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P,
     for (int cnd = 0; cnd < G; ++cnd) {
       if (cnd < ng) {
         const typename M::Reg QR = M::load(Q[cnd]);
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, c0 = 0.0;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
         double jh = fadd((double)base, 0.5);
         for (int k = 0; k < BPT; ++k) {
           const int64_t j = base + (int64_t)k * kTileThreads;
           if (j < P.bin_end) {
-            const double c = P.counts[j];
+            const double ic = P.icounts[j];
             const double x = fadd(P.lo, fmul(jh, P.width));
-            const bool pos = c > 0.0;
-            const double w = pos ? 1.0 : 0.0;
-            const double ic = pos ? rcp_pos(c) : 0.0;
+            const double w = ic > 0.0 ? 1.0 : 0.0;
             double m, bg[1];
             M::template eval<false, true>(x, QR, tab, m, bg);
             const double mc = m * ic;
             a0 += m;
             a1 = __fma_rn(w, m, a1);
             a2 = __fma_rn(m, mc, a2);
-            if (cnd == 0) c0 += c;
           }
           jh = fadd(jh, (double)kTileThreads);
         }
         acc[3 * cnd] = a0;
         acc[3 * cnd + 1] = a1;
         acc[3 * cnd + 2] = a2;
-        if (cnd == 0) acc[3 * G] = c0;
+
       }
     }
 #pragma unroll
@@ -462,15 +453,30 @@ __global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P,
   }
 }
 
-// ---- K3l: q-independent basis sums (once per plan) ------------------------------
-// For the linear parameters: G0_i = sum phi_i(x_j), G1_i = sum [c_j > 0] phi_i(x_j),
-// accumulated with exactly the per-thread order and trees of the gradient
-// pass, so merging them (chunk kernel) gives the same bits as accumulating
-// them in every pass.  Record per tile / chunk: [G0_lin..., G1_lin...].
+// ---- K0: inverse counts (once per plan) -----------------------------------------
+// ic_j = [c_j > 0] / c_j with an IEEE division: the faithful per-bin 1/c of
+// the single-pass algebra, hoisted out of every pass (the histogram is fixed
+// for the lifetime of a plan).
+__global__ void __launch_bounds__(256) chi2_inverse_kernel(const double* __restrict__ counts,
+                                                           double* __restrict__ ic, int64_t begin,
+                                                           int64_t end) {
+  for (int64_t j = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < end;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const double c = ld_stream(counts + j);
+    ic[j] = c > 0.0 ? fdiv(1.0, c) : 0.0;
+  }
+}
+
+// ---- K3l: q-independent sums (once per plan) ------------------------------------
+// C0 = sum [c_j > 0] c_j and, for the linear parameters, G0_i = sum phi_i(x_j),
+// G1_i = sum [c_j > 0] phi_i(x_j), accumulated with exactly the per-thread order
+// and trees of a pass, so merging them (chunk kernel) gives the same bits as
+// accumulating them in every pass.  Record per tile / chunk:
+// [G0_lin[L], G1_lin[L], C0].
 template <class M>
 __global__ void __launch_bounds__(kTileThreads) chi2_lin_kernel(Chi2Pass P) {
   constexpr int L = M::NP - M::LIN0;
-  constexpr int RL = 2 * (L > 0 ? L : 1);
+  constexpr int RL = 2 * L + 1;
   __shared__ double red[kTileThreads / 32][RL];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int BPT = P.bpt;
@@ -494,6 +500,7 @@ __global__ void __launch_bounds__(kTileThreads) chi2_lin_kernel(Chi2Pass P) {
           acc[i] += phi[i];
           acc[L + i] = __fma_rn(w, phi[i], acc[L + i]);
         }
+        acc[2 * L] += c > 0.0 ? c : 0.0;
       }
       jh = fadd(jh, (double)kTileThreads);
     }
@@ -519,12 +526,19 @@ __global__ void __launch_bounds__(kTileThreads) chi2_lin_kernel(Chi2Pass P) {
 // ---- K4: chunk reduce (fixed tree over the chunk's tiles) ---------------------
 // One CTA per chunk; warp w owns record entries v = w, w+8, ...; lane l sums
 // tiles l, l+32, l+64, l+96 pairwise, then a fixed shuffle tree.
-// lin (optional): per-chunk [G0_lin, G1_lin] of the K3l pre-pass, merged into
-// the record entries the gradient pass leaves at zero (0 + v == v exactly).
+// lin (optional): per-chunk [G0_lin[L], G1_lin[L], C0] of the K3l pre-pass,
+// merged into the record entries a pass leaves at zero (0 + v == v exactly):
+// C0 at c0_pos, and (gradient passes of the AD provider, g0_pos >= 0) the
+// linear G0 entries at g0_pos.. and G1 entries at g1_pos...
+struct LinMerge {
+  const double* lin = nullptr;
+  int L = 0;
+  int c0_pos = -1, g0_pos = -1, g1_pos = -1;
+};
+
 __global__ void __launch_bounds__(kChunkThreads) chi2_chunk_kernel(
     const double* __restrict__ tile_ws, int64_t ntiles, int R, int chunk_tiles,
-    double* __restrict__ records, const double* __restrict__ lin = nullptr, int np = 0,
-    int lin0 = 0) {
+    double* __restrict__ records, LinMerge lm = LinMerge{}) {
   const int64_t chunk = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t t0 = chunk * chunk_tiles;
@@ -538,10 +552,12 @@ __global__ void __launch_bounds__(kChunkThreads) chi2_chunk_kernel(
     double a = (part[0] + part[1]) + (part[2] + part[3]);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) a += __shfl_down_sync(0xffffffffu, a, off);
-    if (lin != nullptr && lane == 0) {
-      const int L = np - lin0;
-      if (v >= 4 + lin0 && v < 4 + np) a = a + lin[chunk * 2 * L + (v - 4 - lin0)];
-      else if (v >= 4 + np + lin0 && v < 4 + 2 * np) a = a + lin[chunk * 2 * L + L + (v - 4 - np - lin0)];
+    if (lm.lin != nullptr && lane == 0) {
+      const int L = lm.L, RL = 2 * L + 1;
+      const double* l = lm.lin + chunk * RL;
+      if (v == lm.c0_pos) a = a + l[2 * L];
+      else if (lm.g0_pos >= 0 && v >= lm.g0_pos && v < lm.g0_pos + L) a = a + l[v - lm.g0_pos];
+      else if (lm.g1_pos >= 0 && v >= lm.g1_pos && v < lm.g1_pos + L) a = a + l[L + v - lm.g1_pos];
     }
     if (lane == 0) records[chunk * R + v] = a;
   }
@@ -583,7 +599,7 @@ static void launch_tiles_m(const Chi2Pass& P, bool grad, bool fast, bool num, in
 int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast,
                  int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin,
                  bool numeric) {
-  if (numeric) lin = nullptr;  // the numeric gradient accumulates every entry itself
+
   const int64_t ntiles = P.tile_end - P.tile_begin;
   if (ntiles <= 0) return ADC_OK;
   const int R = grad ? 4 + 3 * np : 4;
@@ -606,8 +622,16 @@ int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast,
   ADCB_CUDA(cudaGetLastError());
   const int64_t nchunks = (ntiles + chunk_tiles - 1) / chunk_tiles;
   const int lin0 = model == ADC_MODEL_GPOLY ? GPoly::LIN0 : np;
-  chi2_chunk_kernel<<<(unsigned)nchunks, kChunkThreads, 0, s>>>(
-      P.tile_ws, ntiles, R, (int)chunk_tiles, records, grad ? lin : nullptr, np, lin0);
+  LinMerge lm;
+  lm.lin = lin;
+  lm.L = np - lin0;
+  lm.c0_pos = 3;
+  if (grad && !numeric && lm.L > 0) {  // finite differences of a linear term are not its basis
+    lm.g0_pos = 4 + lin0;
+    lm.g1_pos = 4 + np + lin0;
+  }
+  chi2_chunk_kernel<<<(unsigned)nchunks, kChunkThreads, 0, s>>>(P.tile_ws, ntiles, R,
+                                                               (int)chunk_tiles, records, lm);
   ADCB_CUDA(cudaGetLastError());
   return ADC_OK;
 }
@@ -617,14 +641,26 @@ int chi2_lin_count(int model, int np) {
 }
 
 int chi2_lin_enqueue(const Chi2Pass& P, int model, int64_t chunk_tiles, double* lin_records,
-                     cudaStream_t s) {
+                     double* icounts_local, cudaStream_t s) {
   const int64_t ntiles = P.tile_end - P.tile_begin;
-  if (ntiles <= 0 || model != ADC_MODEL_GPOLY) return ADC_OK;
+  if (ntiles <= 0) return ADC_OK;
+  // K0 over this rank's bins (icounts_local = ic[bin_begin..bin_end))
+  const int64_t bin_begin = P.tile_begin * (int64_t)P.bpt * kTileThreads;
+  const int64_t nb = P.bin_end - bin_begin;
+  const int64_t iblocks = std::min<int64_t>((nb + 255) / 256, (int64_t)sm_count() * 8);
+  chi2_inverse_kernel<<<(unsigned)iblocks, 256, 0, s>>>(P.counts, icounts_local - bin_begin,
+                                                        bin_begin, P.bin_end);
+  ADCB_CUDA(cudaGetLastError());
   const int64_t blocks = std::min<int64_t>(ntiles, (int64_t)sm_count() * 4);
-  chi2_lin_kernel<GPoly><<<(unsigned)blocks, kTileThreads, 0, s>>>(P);
+  int RL = 1;
+  if (model == ADC_MODEL_GPOLY) {
+    chi2_lin_kernel<GPoly><<<(unsigned)blocks, kTileThreads, 0, s>>>(P);
+    RL = 2 * (GPoly::NP - GPoly::LIN0) + 1;
+  } else {
+    chi2_lin_kernel<GSum<1>><<<(unsigned)blocks, kTileThreads, 0, s>>>(P);  // C0 only
+  }
   ADCB_CUDA(cudaGetLastError());
   const int64_t nchunks = (ntiles + chunk_tiles - 1) / chunk_tiles;
-  const int RL = 2 * (GPoly::NP - GPoly::LIN0);
   chi2_chunk_kernel<<<(unsigned)nchunks, kChunkThreads, 0, s>>>(P.tile_ws, ntiles, RL,
                                                                (int)chunk_tiles, lin_records);
   ADCB_CUDA(cudaGetLastError());
@@ -632,7 +668,7 @@ int chi2_lin_enqueue(const Chi2Pass& P, int model, int64_t chunk_tiles, double* 
 }
 
 int chi2_multi_enqueue(const Chi2Pass& P, int model, int np, int ncand,
-                       int64_t chunk_tiles, double* records, cudaStream_t s) {
+                       int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin) {
   const int64_t ntiles = P.tile_end - P.tile_begin;
   if (ntiles <= 0) return ADC_OK;
   if (ncand < 1 || ncand > kMultiMax) return fail(ADC_E_ARG, "chi2 multi: bad candidate count");
@@ -657,8 +693,12 @@ int chi2_multi_enqueue(const Chi2Pass& P, int model, int np, int ncand,
   ADCB_CUDA(cudaGetLastError());
   const int R = 1 + 3 * ncand;
   const int64_t nchunks = (ntiles + chunk_tiles - 1) / chunk_tiles;
+  LinMerge lm;
+  lm.lin = lin;
+  lm.L = chi2_lin_count(model, np);
+  lm.c0_pos = 0;
   chi2_chunk_kernel<<<(unsigned)nchunks, kChunkThreads, 0, s>>>(P.tile_ws, ntiles, R,
-                                                               (int)chunk_tiles, records);
+                                                               (int)chunk_tiles, records, lm);
   ADCB_CUDA(cudaGetLastError());
   return ADC_OK;
 }

@@ -144,7 +144,8 @@ struct adc_chi2_plan {
   int64_t multi_passes = 0;
   double* grad_multi_records = nullptr;  // [kMultiMax][maxc][R] (adc_cuda_chi2_gradient_multi)
   // q-independent basis sums of the linear parameters (chi2_lin_enqueue)
-  double* lin = nullptr;
+  double* lin = nullptr;      // per local chunk [G0_lin[L], G1_lin[L], C0]
+  double* icounts = nullptr;  // [c > 0]/c for this rank's bins (from bin_begin)
   bool lin_ready = false;
 };
 
@@ -174,6 +175,7 @@ bool numeric(const adc_chi2_plan* P) { return P->provider == ADC_PROVIDER_NUMERI
 Chi2Pass make_pass(const adc_chi2_plan* P) {
   Chi2Pass pass{};
   pass.counts = P->counts;
+  pass.icounts = P->icounts - P->L.bin_begin;
   pass.qdev = P->qdev;
   pass.tile_ws = P->tile_ws;
   pass.lo = P->lo;
@@ -245,15 +247,18 @@ int collect_finish(adc_chi2_plan* P, int R, int nb, const double** out) {
 }
 
 // Once per plan: the linear parameters' q-independent G0/G1 chunk sums.
+// Once per plan (and after adc_cuda_chi2_plan_refresh): everything that
+// depends on the counts alone — ic = [c > 0]/c per bin, C0 and the linear
+// parameters' G0/G1 per chunk.
 int ensure_lin(adc_chi2_plan* P, cudaStream_t s) {
   if (P->lin_ready) return ADC_OK;
   const int L = chi2_lin_count(P->model, P->np);
-  if (L > 0) {
-    const int64_t nrec = std::max<int64_t>(1, local_chunks(P));
-    if (P->lin == nullptr) ADCB_CUDA(cudaMalloc(&P->lin, (size_t)nrec * 2 * L * sizeof(double)));
-    if (int rc = chi2_lin_enqueue(make_pass(P), P->model, P->L.chunk_tiles, P->lin, s)) return rc;
-    ADCB_CUDA(cudaStreamSynchronize(s));
-  }
+  const int64_t nrec = std::max<int64_t>(1, local_chunks(P));
+  if (P->lin == nullptr)
+    ADCB_CUDA(cudaMalloc(&P->lin, (size_t)nrec * (2 * L + 1) * sizeof(double)));
+  if (int rc = chi2_lin_enqueue(make_pass(P), P->model, P->L.chunk_tiles, P->lin, P->icounts, s))
+    return rc;
+  ADCB_CUDA(cudaStreamSynchronize(s));
   P->lin_ready = true;
   return ADC_OK;
 }
@@ -301,8 +306,7 @@ int run_pass(adc_chi2_plan* P, const double* q, int grad, const double** rec) {
   if (int rc = check_domain(P, q, grad && numeric(P))) return rc;
   ADCB_CUDA(cudaSetDevice(P->device));
   fill_qdev(P->model, P->np, q, P->h_q);
-  if (grad)
-    if (int rc = ensure_lin(P, P->stream)) return rc;
+  if (int rc = ensure_lin(P, P->stream)) return rc;
   const int kind = grad ? 1 + numeric(P) : 0;
   if (!P->warm[kind][P->fast]) {
     if (int rc = enqueue_pass(P, grad)) return rc;
@@ -386,7 +390,9 @@ extern "C" int adc_cuda_chi2_plan_create(adc_chi2_plan** out, int32_t model, int
       (e = cudaMalloc(&P->tile_ws, (size_t)ntiles_local * Rmax * sizeof(double))) != cudaSuccess ||
       (e = cudaMalloc(&P->records, (size_t)P->maxc * Rmax * sizeof(double))) != cudaSuccess ||
       (e = cudaMemset(P->records, 0, (size_t)P->maxc * Rmax * sizeof(double))) != cudaSuccess ||
-      (e = cudaMallocHost(&P->h_q, qdev_bytes())) != cudaSuccess)
+      (e = cudaMallocHost(&P->h_q, qdev_bytes())) != cudaSuccess ||
+      (e = cudaMalloc(&P->icounts, (size_t)std::max<int64_t>(1, P->L.bin_end - P->L.bin_begin) *
+                                       sizeof(double))) != cudaSuccess)
     return cleanup(cuda_fail(e, "chi2 plan allocation"));
   if (int rc = alloc_staging(P)) return cleanup(rc);
   *out = P;
@@ -448,6 +454,7 @@ extern "C" int adc_cuda_chi2_plan_destroy(adc_chi2_plan* P) {
   if (P->tile_ws_multi) cudaFree(P->tile_ws_multi);
   if (P->records_multi) cudaFree(P->records_multi);
   if (P->lin) cudaFree(P->lin);
+  if (P->icounts) cudaFree(P->icounts);
   if (P->grad_multi_records) cudaFree(P->grad_multi_records);
   if (P->stream) cudaStreamDestroy(P->stream);
   delete P;
@@ -466,6 +473,15 @@ extern "C" int adc_cuda_chi2_set_precision(adc_chi2_plan* P, int32_t mode) {
   if (P == nullptr || mode < 0 || mode > 1) return fail(ADC_E_ARG, "precision mode is 0 or 1");
   P->fast = mode;
   if (const char* t = getenv("ADC_CHI2_TUNE")) chi2_set_tune(atoi(t));
+  return ADC_OK;
+}
+
+extern "C" int adc_cuda_chi2_plan_refresh(adc_chi2_plan* P) {
+  clear_error();
+  if (P == nullptr) return fail(ADC_E_ARG, "null plan");
+  ADCB_CUDA(cudaSetDevice(P->device));
+  ADCB_CUDA(cudaStreamSynchronize(P->stream));
+  P->lin_ready = false;  // recomputed (1/c, C0, linear sums) before the next pass
   return ADC_OK;
 }
 
@@ -491,8 +507,7 @@ extern "C" int adc_cuda_chi2_partials(adc_chi2_plan* P, const double* q, int32_t
   // h_q may still be read by an in-flight copy of a previous pass
   ADCB_CUDA(cudaStreamSynchronize(s));
   ADCB_CUDA(cudaStreamSynchronize(P->stream));
-  if (want_grad)
-    if (int rc = ensure_lin(P, s)) return rc;
+  if (int rc = ensure_lin(P, s)) return rc;
   fill_qdev(P->model, P->np, q, P->h_q);
   ADCB_CUDA(cudaMemcpyAsync(P->qdev, P->h_q, qdev_bytes(), cudaMemcpyHostToDevice, s));
   return chi2_enqueue(make_pass(P), P->model, P->np, want_grad != 0, P->fast != 0,
@@ -542,6 +557,7 @@ extern "C" int adc_cuda_chi2_multi(adc_chi2_plan* P, const double* qs, int32_t n
   for (int k = 0; k < ncand; ++k)
     if (int rc = check_domain(P, qs + (size_t)k * P->np)) return rc;
   ADCB_CUDA(cudaSetDevice(P->device));
+  if (int rc = ensure_lin(P, P->stream)) return rc;
   if (int rc = ensure_multi(P)) return rc;
   const size_t qb = qdev_bytes();
   for (int k = 0; k < ncand; ++k)
@@ -552,7 +568,7 @@ extern "C" int adc_cuda_chi2_multi(adc_chi2_plan* P, const double* qs, int32_t n
   pass.qdev = P->qmulti;
   pass.tile_ws = P->tile_ws_multi;
   if (int rc = chi2_multi_enqueue(pass, P->model, P->np, ncand, P->L.chunk_tiles,
-                                  P->records_multi, P->stream))
+                                  P->records_multi, P->stream, P->lin))
     return rc;
   const int R = 1 + 3 * ncand;
   if (int rc = collect_enqueue(P, P->records_multi, R, 1, P->stream)) return rc;

@@ -13,7 +13,8 @@ constexpr int kQDoubles = 8 * kMaxNp;  // QDev (q, 1/q) + QNum (numeric probes),
 constexpr int kMultiMax = 32;  // line-search candidates per multi pass  // gsum up to K = 8 components (the reference bench K list 1,2,4,8)
 
 struct Chi2Pass {
-  const double* counts;  // full histogram, device
+  const double* counts;   // full histogram, device (read by the once-per-plan passes)
+  const double* icounts;  // [c > 0] / c per bin, same global indexing (read by every pass)
   const double* qdev;    // QDev (2 * kMaxNp doubles), device
   double* tile_ws;       // [tile_end - tile_begin][R]
   double lo, width;      // Histogram::center = lo + (j + 0.5) * width
@@ -29,11 +30,13 @@ int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast,
                  int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin,
                  bool numeric = false);
 int chi2_lin_count(int model, int np);  // L: number of linear parameters
-// Writes [G0_lin[L], G1_lin[L]] per local chunk (once per plan); uses P.tile_ws.
+// Once per plan: ic = [c > 0]/c into icounts_local (this rank's bins, indexed
+// from bin_begin), then [G0_lin[L], G1_lin[L], C0] per local chunk into
+// lin_records (2L + 1 doubles each); uses P.tile_ws.
 int chi2_lin_enqueue(const Chi2Pass& P, int model, int64_t chunk_tiles, double* lin_records,
-                     cudaStream_t s);
+                     double* icounts_local, cudaStream_t s);
 int chi2_multi_enqueue(const Chi2Pass& P, int model, int np, int ncand,
-                       int64_t chunk_tiles, double* records, cudaStream_t s);
+                       int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin);
 void fill_qdev(int model, int np, const double* q, double* host_qdev);
 size_t qdev_bytes();
 int chi2_set_tune(int v);  // kernel-variant experiments (ADC_CHI2_TUNE)

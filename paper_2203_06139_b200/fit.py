@@ -135,6 +135,11 @@ class Chi2Plan:
     def set_precision(self, fast: bool):
         check(lib.adc_cuda_chi2_set_precision(self._p, 1 if fast else 0))
 
+    def refresh(self):
+        """Recompute what depends on the counts alone (1/c, C0, linear sums)
+        after the device counts were changed in place."""
+        check(lib.adc_cuda_chi2_plan_refresh(self._p))
+
     def set_provider(self, provider: int):
         """GradientProvider.AdReverse (default) or GradientProvider.Numeric."""
         check(lib.adc_cuda_chi2_set_provider(self._p, int(provider)))

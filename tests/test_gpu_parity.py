@@ -411,3 +411,22 @@ def test_compute_shared_refused_without_unsafe():
         adc.launch("compute_shared", adc.LaunchConfig(1, 64, n),
                    adc.BufferSet(arrays=bufs, scalars={"sigma": 1.0}))
     assert e.value.kind == "Launch" and str(e.value).startswith("launch refused")
+
+
+def test_plan_refresh_after_counts_change(restate):
+    # The plan snapshots what depends on the counts alone (1/c, C0, linear
+    # sums); refresh() picks up an in-place change of device counts.
+    counts, ev = synth.histogram(50_000, events=5e6, seed=31)
+    dc = t(counts)
+    h = adc.Histogram(counts.size, -5.0, 5.0, ev, dc)
+    pl = adc.Chi2Plan("gpoly", 6, h)
+    q = np.array(synth.GPOLY_INIT)
+    g1, c1 = pl.gradient(q)
+    dc[::7] += 3.0
+    torch.cuda.synchronize()
+    pl.refresh()
+    g2, c2 = pl.gradient(q)
+    c_new = host(dc)
+    ref, scale = restate.chi2_gradient_compensated("gpoly", c_new, -5.0, 5.0, ev, q)
+    assert np.all(np.abs(g2 - ref) <= 1e-12 * scale)
+    assert not np.array_equal(g1, g2)
