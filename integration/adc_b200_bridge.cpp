@@ -235,9 +235,13 @@ adc_chi2_plan* plan_for(const FitEngine& engine, const Histogram& h, size_t np) 
 void set_model_source(const std::string& source) { t_model_source = source; }
 
 void chi2_gradient(const FitEngine& engine, const Histogram& h, const std::vector<double>& q,
-                   std::vector<double>& out) {
+                   std::vector<double>& out, GradientProvider provider) {
   out.assign(q.size(), 0.0);
-  check(adc_cuda_chi2_gradient(plan_for(engine, h, q.size()), q.data(), out.data(), nullptr));
+  adc_chi2_plan* plan = plan_for(engine, h, q.size());
+  check(adc_cuda_chi2_set_provider(plan, provider == GradientProvider::Numeric
+                                             ? ADC_PROVIDER_NUMERIC
+                                             : ADC_PROVIDER_AD_REVERSE));
+  check(adc_cuda_chi2_gradient(plan, q.data(), out.data(), nullptr));
 }
 
 double chi2(const FitEngine& engine, const Histogram& h, const std::vector<double>& q) {

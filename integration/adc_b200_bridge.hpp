@@ -29,9 +29,12 @@ void set_model_source(const std::string& source);
 
 /// FitEngine::chi2_gradient / chi2 (fit.cpp:206-259) for the reference model
 /// (gsum, fit.cpp:125-138) with the histogram on the GPU.  The model's
-/// generated gradient text is checked against the B200 registry first.
+/// generated gradient text is checked against the B200 registry first; the
+/// provider is the caller's (AdReverse: the generated gradient; Numeric:
+/// central differences of the model, numdiff.cpp:38-87).
 void chi2_gradient(const FitEngine& engine, const Histogram& h, const std::vector<double>& q,
-                   std::vector<double>& out);
+                   std::vector<double>& out,
+                   GradientProvider provider = GradientProvider::AdReverse);
 double chi2(const FitEngine& engine, const Histogram& h, const std::vector<double>& q);
 
 }  // namespace adc::b200_bridge

@@ -171,6 +171,14 @@ static void gpu_checks(const Program& p) {
     std::printf("     gsum K=%d: gradient worst |diff|/max|g| %.3g, chi2 rel %.3g\n", k, worst,
                 rel(cr, cg));
     EXPECT(worst <= 1e-11 && rel(cr, cg) <= 1e-12, "bridged FitEngine chi2/gradient match");
+    // GradientProvider::Numeric through the bridge vs the reference's numeric provider
+    std::vector<double> nr, ng;
+    eng.chi2_gradient(h, q, GradientProvider::Numeric, nr);
+    b200_bridge::chi2_gradient(eng, h, q, ng, GradientProvider::Numeric);
+    double nw = 0;
+    for (size_t i = 0; i < q.size(); ++i) nw = std::max(nw, std::fabs(nr[i] - ng[i]) / gmax);
+    std::printf("     gsum K=%d numeric provider: worst |diff|/max|g| %.3g\n", k, nw);
+    EXPECT(nw <= 1e-8, "bridged FitEngine numeric-provider gradient matches");
   }
 }
 
