@@ -120,6 +120,45 @@ int adc_cuda_gaussnd_grad_host(int64_t n, int64_t dim, int64_t ld, const double*
 int adc_cuda_gaussnd_set_variant(int32_t variant);
 
 /* ---------------------------------------------------------------------------
+ * Generic lowering: a DSL module as the reference prints it
+ * (adc::print(Module): a Listing-style `global` kernel plus the generated
+ * gradients it calls, e.g. after ensure_called_derivatives) is translated to
+ * CUDA C++ and compiled for sm_100a with NVRTC.  Each real op is one IEEE
+ * double op in source order, value/control tapes are per call frame in
+ * thread-private memory (tape_capacity entries each; 0 = 256), and the
+ * interpreter's domain errors (eval.cpp) come back as ADC_E_EVAL.
+ * adc_jit_* need no device (parse, hazard check, emission, NVRTC);
+ * adc_cuda_jit_* launch.  A kernel with a shared-write hazard
+ * (launch.cpp:261-267) is refused with the reference's message unless
+ * `unsafe`, which turns indexed += into atomic adds (order unspecified, as
+ * the reference's forced parallel mode). */
+typedef struct adc_jit_module adc_jit_module;
+/* One kernel parameter: real[] -> ptr + len (elements), real -> real_value,
+ * integer -> int_value.  Device pointers for adc_cuda_jit_launch, host
+ * pointers (copied in and back) for adc_cuda_jit_launch_host. */
+typedef struct adc_jit_arg {
+  double* ptr;
+  int64_t len;
+  double real_value;
+  int64_t int_value;
+} adc_jit_arg;
+int adc_jit_compile(const char* module_source, const char* kernel, int32_t unsafe,
+                    int32_t tape_capacity, adc_jit_module** out);
+int adc_jit_destroy(adc_jit_module* module);
+/* kinds[i]: 0 = real[], 1 = real, 2 = integer (kernel parameter order). */
+int adc_jit_kernel_params(const adc_jit_module* module, int32_t* nparams, int32_t* kinds,
+                          int32_t cap);
+const char* adc_jit_kernel_param_name(const adc_jit_module* module, int32_t index);
+const char* adc_jit_cuda_source(const adc_jit_module* module);
+size_t adc_jit_cubin_size(const adc_jit_module* module);
+/* LaunchConfig semantics (launch.cpp:9-19): grid x block threads, the
+ * kernel's own `i < N` guard idles the padding.  Synchronous on `stream`. */
+int adc_cuda_jit_launch(adc_jit_module* module, int64_t grid_dim, int64_t block_dim, int64_t n,
+                        const adc_jit_arg* args, int32_t nargs, void* stream);
+int adc_cuda_jit_launch_host(adc_jit_module* module, int64_t grid_dim, int64_t block_dim,
+                             int64_t n, const adc_jit_arg* args, int32_t nargs);
+
+/* ---------------------------------------------------------------------------
  * chi2 histogram fit (FitEngine::chi2 / chi2_gradient, proj/src/fit.cpp:206-259)
  * for model-parameterised histograms.
  *

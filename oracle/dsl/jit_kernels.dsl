@@ -1,0 +1,52 @@
+// Listing-1-style batch kernels over the reference corpus gradients (the
+// generic-lowering parity fixtures, tests/golden/make_golden.py).  Each calls
+// a generated gradient once per thread; the primal functions are the
+// reference corpus files, prepended at fixture-generation time.
+global void k_gauss(real[] x, real[] p, real sigma, real[] dx, real[] dp) {
+  integer i = blockIdx * blockDim + threadIdx;
+  if (i < N) {
+    gauss_grad_0_1(x[i], p[i], sigma, dx[i], dp[i]);
+  }
+}
+
+global void k_rational(real[] x, real[] y, real[] dx, real[] dy) {
+  integer i = blockIdx * blockDim + threadIdx;
+  if (i < N) {
+    rational_grad(x[i], y[i], dx[i], dy[i]);
+  }
+}
+
+global void k_branchy(real[] x, real[] y, real[] dx, real[] dy) {
+  integer i = blockIdx * blockDim + threadIdx;
+  if (i < N) {
+    branchy_grad(x[i], y[i], dx[i], dy[i]);
+  }
+}
+
+global void k_poly(real[] x, real[] y, real[] dx, real[] dy) {
+  integer i = blockIdx * blockDim + threadIdx;
+  if (i < N) {
+    poly_grad(x[i], y[i], dx[i], dy[i]);
+  }
+}
+
+global void k_looped(real[] x, integer n, real[] dx) {
+  integer i = blockIdx * blockDim + threadIdx;
+  if (i < N) {
+    looped_grad(x[i], n, dx[i]);
+  }
+}
+
+global void k_gsum(real[] xs, real[] q, integer k, real[] dq) {
+  integer i = blockIdx * blockDim + threadIdx;
+  if (i < N) {
+    gsum_grad_1(xs[i], q, k, dq);
+  }
+}
+
+global void k_sumn(real[] x, integer n, real[] dx) {
+  integer i = blockIdx * blockDim + threadIdx;
+  if (i < N) {
+    sumn_grad(x, n, dx);
+  }
+}

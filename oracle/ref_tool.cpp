@@ -257,6 +257,65 @@ int cmd_gauss_shared_in(int argc, char** argv) {
   return refused ? 0 : 1;
 }
 
+// launch-file <module.dsl> <kernel> <n> <block> <in.bin> <out.bin> <module_out.txt> [unsafe]
+//   Any Listing-style kernel of a DSL module (the generic-lowering parity
+//   fixture): parse, ensure_called_derivatives (tooling.cpp:103-119), then
+//   adc::launch on the kernel's parameters read in order from in.bin:
+//   real[] -> [len, values...], real -> [value], integer -> [value] (as f64).
+//   out = every real[] parameter after the launch, in order;
+//   module_out = print(module) — the text the B200 JIT consumes.
+int cmd_launch_file(int argc, char** argv) {
+  if (argc < 8) die("launch-file <dsl> <kernel> <n> <block> <in> <out> <module_out> [unsafe]");
+  std::ifstream f(argv[1]);
+  if (!f) die(std::string("cannot open ") + argv[1]);
+  std::stringstream ss;
+  ss << f.rdbuf();
+  Module m = parse_or_throw(ss.str());
+  ensure_called_derivatives(m);
+  const std::string text = print(m);
+  Program prog(std::move(m));
+  const FunctionDef* k = prog.module().find(argv[2]);
+  if (k == nullptr) die(std::string("no kernel ") + argv[2]);
+  const int64_t n = std::atoll(argv[3]);
+  const int64_t block = std::atoll(argv[4]);
+  std::ifstream in(argv[5], std::ios::binary | std::ios::ate);
+  const size_t bytes = static_cast<size_t>(in.tellg());
+  std::vector<double> raw = read_f64(argv[5], bytes / 8);
+  size_t pos = 0;
+  BufferSet b;
+  for (const auto& prm : k->params) {
+    if (prm.type == ValType::RealArray) {
+      const size_t len = static_cast<size_t>(raw.at(pos++));
+      b.arrays[prm.name].assign(raw.begin() + pos, raw.begin() + pos + len);
+      pos += len;
+    } else if (prm.type == ValType::Real) {
+      b.scalars[prm.name] = raw.at(pos++);
+    } else {
+      b.integers[prm.name] = static_cast<int64_t>(raw.at(pos++));
+    }
+  }
+  // unsafe: forced hazardous launch, sequential; sequential: one worker (an
+  // Eval error thrown on a pool worker terminates the process, so error
+  // cases run sequentially to surface the reference's message).
+  LaunchOptions lo;
+  const std::string mode = argc > 8 ? argv[8] : "";
+  if (mode == "unsafe") lo.unsafe = true;
+  if (mode == "unsafe" || mode == "sequential") lo.sequential = true;
+  std::string err;
+  try {
+    launch(prog, argv[2], LaunchConfig{n / block + 1, block, n}, b, lo);
+  } catch (const Error& e) {
+    err = e.what();
+  }
+  std::ofstream out(argv[6], std::ios::binary);
+  for (const auto& prm : k->params)
+    if (prm.type == ValType::RealArray) write_f64(out, b.arrays[prm.name]);
+  std::ofstream mo(argv[7]);
+  mo << text;
+  std::printf("{\"n\": %lld, \"error\": \"%s\"}\n", (long long)n, err.c_str());
+  return 0;
+}
+
 // gaussnd-in <dim> <n> <sigma> <in.bin> <out.bin> [workers]
 //   in = x, p, dx0, dp0 in structure-of-arrays layout ([d*n + i]); each point
 //   is gathered into contiguous rows and run through
@@ -778,6 +837,7 @@ int main(int argc, char** argv) {
     if (cmd == "gauss1d-in") return cmd_gauss1d_in(argc - 1, argv + 1);
     if (cmd == "gaussnd-in") return cmd_gaussnd_in(argc - 1, argv + 1);
     if (cmd == "gauss-shared-in") return cmd_gauss_shared_in(argc - 1, argv + 1);
+    if (cmd == "launch-file") return cmd_launch_file(argc - 1, argv + 1);
     if (cmd == "chi2-in") return cmd_chi2_in(argc - 1, argv + 1);
     if (cmd == "fit-in") return cmd_fit_in(argc - 1, argv + 1);
     if (cmd == "gaussnd-bench") return cmd_gaussnd_bench(argc - 1, argv + 1);

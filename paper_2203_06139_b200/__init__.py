@@ -9,11 +9,12 @@ from ._capi import AdcError, LIB_PATH, lib  # noqa: F401
 from .launch import (BufferSet, LaunchConfig, LaunchOptions, LaunchStats, launch,  # noqa: F401
                      launch_batch, registry_find)
 from .comm import Comm  # noqa: F401
+from .jit import JitModule, launch_module  # noqa: F401
 from .fit import (Chi2Plan, FitEngine, FitOptions, FitResult, GradientProvider,  # noqa: F401
                   Histogram, chi2_layout, finalize, record_len)
 
 __all__ = [
-    "AdcError", "BufferSet", "Comm", "LaunchConfig", "LaunchOptions", "LaunchStats", "launch",
+    "AdcError", "BufferSet", "Comm", "JitModule", "launch_module", "LaunchConfig", "LaunchOptions", "LaunchStats", "launch",
     "launch_batch", "registry_find", "Chi2Plan", "FitEngine", "FitOptions", "FitResult",
     "GradientProvider", "Histogram", "chi2_layout", "finalize", "record_len",
 ]

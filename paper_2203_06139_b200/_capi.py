@@ -35,6 +35,11 @@ class Chi2Layout(ctypes.Structure):
         "bin_end")]
 
 
+class JitArg(ctypes.Structure):
+    _fields_ = [("ptr", ctypes.c_void_p), ("len", ctypes.c_int64), ("real_value", ctypes.c_double),
+                ("int_value", ctypes.c_int64)]
+
+
 class FitOptions(ctypes.Structure):
     _fields_ = [("budget", ctypes.c_int32), ("grad_tol", ctypes.c_double),
                 ("chi2_rel_tol", ctypes.c_double), ("sigma_min", ctypes.c_double),
@@ -102,6 +107,18 @@ SIGNATURES = {
     "adc_cuda_chi2_plan_set_comm": (ctypes.c_int, [_VP, _VP]),
     "adc_cuda_chi2_plan_create_sharded": (ctypes.c_int, [ctypes.POINTER(_VP), _I32, _I32, _I64,
                                                          _DBL, _DBL, _DBL, _VP, _VP, _VP]),
+    "adc_jit_compile": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, _I32, _I32,
+                                       ctypes.POINTER(_VP)]),
+    "adc_jit_destroy": (ctypes.c_int, [_VP]),
+    "adc_jit_kernel_params": (ctypes.c_int, [_VP, ctypes.POINTER(_I32), ctypes.POINTER(_I32),
+                                             _I32]),
+    "adc_jit_kernel_param_name": (ctypes.c_char_p, [_VP, _I32]),
+    "adc_jit_cuda_source": (ctypes.c_char_p, [_VP]),
+    "adc_jit_cubin_size": (ctypes.c_size_t, [_VP]),
+    "adc_cuda_jit_launch": (ctypes.c_int, [_VP, _I64, _I64, _I64, ctypes.POINTER(JitArg), _I32,
+                                           _VP]),
+    "adc_cuda_jit_launch_host": (ctypes.c_int, [_VP, _I64, _I64, _I64, ctypes.POINTER(JitArg),
+                                                _I32]),
     "adc_fit_default_options": (None, [ctypes.POINTER(FitOptions)]),
     "adc_cuda_fit": (ctypes.c_int, [_VP, _D, ctypes.POINTER(_I32), _I32,
                                     ctypes.POINTER(FitOptions), ctypes.POINTER(FitResultC), _D]),

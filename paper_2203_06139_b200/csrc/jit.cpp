@@ -1,0 +1,1221 @@
+// Generic lowering: any Listing-style `global` kernel
+// of a DSL module — together with the generated gradients it calls, exactly as
+// the reference prints them (adc::print(Module), printer.cpp:60-242) — is
+// translated to CUDA C++ and compiled for sm_100a with NVRTC.  This replaces
+// the hand-transcribed registry for gradients that have no hand-written
+// kernel: the corpus gradients with branches, loops and value/control tapes
+// (reverse.cpp:331-676) become launchable.
+//
+// Semantics follow the reference interpreter (proj/src/eval.cpp:339-703):
+//  * every real operation is one IEEE double op in source order (__dadd_rn,
+//    __dmul_rn, ... and -fmad=false), integers are int64;
+//  * an expression is integer-valued when the interpreter says so
+//    (eval.cpp:170-202): integer literals and variables, negation and
+//    + - * of integer operands, __pop_ctl(); an integer expression in a real
+//    context is converted to double;
+//  * slots accumulate (+=), a[i] in an array-parameter position is a length-1
+//    slice (eval.cpp:485-499);
+//  * domain errors of the interpreter (division by zero, log of a non-positive
+//    value, sqrt of a negative value, an index out of range, tape underflow)
+//    are detected per thread and reported as ADC_E_EVAL after the launch;
+//  * the value / control tapes (__push, __pop, __push_ctl, __pop_ctl) are
+//    per call frame, as in the interpreter (eval.cpp:312-319), held in a
+//    thread-private array of the chosen capacity.
+// Integer overflow checks of the interpreter are not replicated.
+//
+// Hazards: a whole real[] kernel parameter that is written (directly at an
+// index other than the thread index, or through a callee's writes) is a
+// shared-write hazard (launch.cpp:112-240); compiling such a kernel is refused
+// with the reference's message unless `unsafe`, in which case every indexed
+// += into an array compiles to an atomic add (the reference's forced
+// parallel mode, eval.cpp:414-423: race-free, order unspecified).
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <cctype>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <set>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+using namespace adcb;
+
+namespace {
+
+// ---- NVRTC, bound at first use (a process may already hold another copy) ------
+struct Nvrtc {
+  nvrtcResult (*create)(nvrtcProgram*, const char*, const char*, int, const char* const*,
+                        const char* const*) = nullptr;
+  nvrtcResult (*compile)(nvrtcProgram, int, const char* const*) = nullptr;
+  nvrtcResult (*log_size)(nvrtcProgram, size_t*) = nullptr;
+  nvrtcResult (*log)(nvrtcProgram, char*) = nullptr;
+  nvrtcResult (*cubin_size)(nvrtcProgram, size_t*) = nullptr;
+  nvrtcResult (*cubin)(nvrtcProgram, char*) = nullptr;
+  nvrtcResult (*destroy)(nvrtcProgram*) = nullptr;
+  const char* (*error_string)(nvrtcResult) = nullptr;
+  bool ok = false;
+};
+
+const Nvrtc* nvrtc() {
+  static Nvrtc N;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnvrtc.so.12", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (h == nullptr) h = dlopen("libnvrtc.so.12", RTLD_NOW | RTLD_GLOBAL);
+    if (h == nullptr) h = dlopen("/usr/local/cuda/lib64/libnvrtc.so.12", RTLD_NOW | RTLD_GLOBAL);
+    if (h == nullptr) return;
+    auto sym = [&](auto& fn, const char* name) {
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+      return fn != nullptr;
+    };
+    N.ok = sym(N.create, "nvrtcCreateProgram") && sym(N.compile, "nvrtcCompileProgram") &&
+           sym(N.log_size, "nvrtcGetProgramLogSize") && sym(N.log, "nvrtcGetProgramLog") &&
+           sym(N.cubin_size, "nvrtcGetCUBINSize") && sym(N.cubin, "nvrtcGetCUBIN") &&
+           sym(N.destroy, "nvrtcDestroyProgram") && sym(N.error_string, "nvrtcGetErrorString");
+  });
+  return N.ok ? &N : nullptr;
+}
+
+// ---- AST ---------------------------------------------------------------------
+enum class VT { Real, RealArray, Integer };
+
+struct Ex;
+using ExP = std::unique_ptr<Ex>;
+struct Ex {
+  enum K { Num, Var, Neg, Bin, Cmp, Call, Index } k = Num;
+  double v = 0;
+  bool int_lit = false, pi = false;
+  std::string name;  // Var / Call (intrinsic) / Index
+  char op = 0;       // Bin: + - * /
+  std::string cmp;   // Cmp: < <= > >= == !=
+  std::vector<ExP> a;
+  bool is_int = false;
+};
+
+struct St;
+using StP = std::unique_ptr<St>;
+using Blk = std::vector<StP>;
+struct St {
+  enum K { Decl, Assign, Return, If, For, Call } k = Decl;
+  VT type = VT::Real;
+  std::string target;
+  bool indexed = false, compound = false;
+  ExP index, expr;
+  Blk then_b, else_b;
+  std::string loop_var;
+  ExP lo, hi;
+  std::string callee;
+  std::vector<ExP> args;
+  int line = 0;
+};
+
+struct Prm {
+  std::string name;
+  VT type;
+};
+
+struct Fn {
+  std::string name;
+  bool global = false, returns_void = false;
+  std::vector<Prm> params;
+  Blk body;
+  bool uses_tape = false, uses_ctl = false;
+};
+
+struct ParseError {
+  std::string msg;
+};
+
+// ---- lexer / parser ------------------------------------------------------------
+struct Tok {
+  enum K { Id, Num, Punct, End } k = End;
+  std::string s;
+  int line = 0;
+};
+
+std::vector<Tok> lex(const std::string& src) {
+  std::vector<Tok> t;
+  size_t i = 0;
+  int line = 1;
+  while (i < src.size()) {
+    const char c = src[i];
+    if (c == '\n') {
+      ++line;
+      ++i;
+    } else if (std::isspace((unsigned char)c)) {
+      ++i;
+    } else if (c == '/' && i + 1 < src.size() && src[i + 1] == '/') {
+      while (i < src.size() && src[i] != '\n') ++i;
+    } else if (std::isalpha((unsigned char)c) || c == '_') {
+      size_t j = i;
+      while (j < src.size() && (std::isalnum((unsigned char)src[j]) || src[j] == '_')) ++j;
+      t.push_back({Tok::Id, src.substr(i, j - i), line});
+      i = j;
+    } else if (std::isdigit((unsigned char)c) ||
+               (c == '.' && i + 1 < src.size() && std::isdigit((unsigned char)src[i + 1]))) {
+      size_t j = i;
+      while (j < src.size() && (std::isdigit((unsigned char)src[j]) || src[j] == '.')) ++j;
+      if (j < src.size() && (src[j] == 'e' || src[j] == 'E')) {
+        size_t k = j + 1;
+        if (k < src.size() && (src[k] == '+' || src[k] == '-')) ++k;
+        if (k < src.size() && std::isdigit((unsigned char)src[k])) {
+          j = k;
+          while (j < src.size() && std::isdigit((unsigned char)src[j])) ++j;
+        }
+      }
+      t.push_back({Tok::Num, src.substr(i, j - i), line});
+      i = j;
+    } else {
+      static const char* two[] = {"<=", ">=", "==", "!=", "+="};
+      std::string p(1, c);
+      for (const char* tw : two)
+        if (src.compare(i, 2, tw) == 0) p = tw;
+      if (std::strchr("(){}[],;+-*/<>=", c) == nullptr)
+        throw ParseError{"line " + std::to_string(line) + ": unexpected character '" + p + "'"};
+      t.push_back({Tok::Punct, p, line});
+      i += p.size();
+    }
+  }
+  t.push_back({Tok::End, "", line});
+  return t;
+}
+
+struct Parser {
+  std::vector<Tok> t;
+  size_t i = 0;
+  const Tok& peek(size_t k = 0) const { return t[std::min(i + k, t.size() - 1)]; }
+  bool is(const char* s, size_t k = 0) const { return peek(k).s == s && peek(k).k != Tok::End; }
+  [[noreturn]] void error(const std::string& m) const {
+    throw ParseError{"line " + std::to_string(peek().line) + ": " + m};
+  }
+  void expect(const char* s) {
+    if (!is(s)) error(std::string("expected '") + s + "', got '" + peek().s + "'");
+    ++i;
+  }
+  std::string ident() {
+    if (peek().k != Tok::Id) error("expected identifier, got '" + peek().s + "'");
+    return t[i++].s;
+  }
+
+  VT type() {
+    const std::string n = ident();
+    if (n == "integer") return VT::Integer;
+    if (n != "real") error("unknown type '" + n + "'");
+    if (is("[")) {
+      expect("[");
+      expect("]");
+      return VT::RealArray;
+    }
+    return VT::Real;
+  }
+
+  ExP primary() {
+    auto e = std::make_unique<Ex>();
+    if (peek().k == Tok::Num) {
+      const std::string s = t[i++].s;
+      e->k = Ex::Num;
+      e->v = std::strtod(s.c_str(), nullptr);
+      e->int_lit = s.find_first_of(".eE") == std::string::npos;
+      return e;
+    }
+    if (is("(")) {
+      expect("(");
+      ExP in = expr();
+      expect(")");
+      return in;
+    }
+    const std::string n = ident();
+    if (n == "PI") {
+      e->k = Ex::Num;
+      e->pi = true;
+      e->v = 3.14159265358979323846;  // ast.cpp:119-123
+      return e;
+    }
+    if (is("(")) {
+      expect("(");
+      e->k = Ex::Call;
+      e->name = n;
+      if (!is(")")) {
+        e->a.push_back(expr());
+        while (is(",")) {
+          expect(",");
+          e->a.push_back(expr());
+        }
+      }
+      expect(")");
+      return e;
+    }
+    if (is("[")) {
+      expect("[");
+      e->k = Ex::Index;
+      e->name = n;
+      e->a.push_back(expr());
+      expect("]");
+      return e;
+    }
+    e->k = Ex::Var;
+    e->name = n;
+    return e;
+  }
+  ExP unary() {
+    if (is("-")) {
+      expect("-");
+      auto e = std::make_unique<Ex>();
+      e->k = Ex::Neg;
+      e->a.push_back(unary());
+      return e;
+    }
+    return primary();
+  }
+  ExP term() {
+    ExP l = unary();
+    while (is("*") || is("/")) {
+      auto e = std::make_unique<Ex>();
+      e->k = Ex::Bin;
+      e->op = t[i++].s[0];
+      e->a.push_back(std::move(l));
+      e->a.push_back(unary());
+      l = std::move(e);
+    }
+    return l;
+  }
+  ExP arith() {
+    ExP l = term();
+    while (is("+") || is("-")) {
+      auto e = std::make_unique<Ex>();
+      e->k = Ex::Bin;
+      e->op = t[i++].s[0];
+      e->a.push_back(std::move(l));
+      e->a.push_back(term());
+      l = std::move(e);
+    }
+    return l;
+  }
+  ExP expr() {
+    ExP l = arith();
+    for (const char* c : {"<", "<=", ">", ">=", "==", "!="}) {
+      if (is(c)) {
+        auto e = std::make_unique<Ex>();
+        e->k = Ex::Cmp;
+        e->cmp = t[i++].s;
+        e->a.push_back(std::move(l));
+        e->a.push_back(arith());
+        return e;
+      }
+    }
+    return l;
+  }
+
+  Blk block() {
+    expect("{");
+    Blk b;
+    while (!is("}")) {
+      if (peek().k == Tok::End) error("unterminated block");
+      b.push_back(stmt());
+    }
+    expect("}");
+    return b;
+  }
+
+  StP stmt() {
+    auto s = std::make_unique<St>();
+    s->line = peek().line;
+    if (is("real") || is("integer")) {
+      s->k = St::Decl;
+      s->type = type();
+      s->target = ident();
+      expect("=");
+      s->expr = expr();
+      expect(";");
+      return s;
+    }
+    if (is("return")) {
+      ++i;
+      s->k = St::Return;
+      s->expr = expr();
+      expect(";");
+      return s;
+    }
+    if (is("if")) {
+      ++i;
+      s->k = St::If;
+      expect("(");
+      s->expr = expr();
+      expect(")");
+      s->then_b = block();
+      if (is("else")) {
+        ++i;
+        if (is("if")) s->else_b.push_back(stmt());
+        else s->else_b = block();
+      }
+      return s;
+    }
+    if (is("for")) {
+      ++i;
+      s->k = St::For;
+      expect("(");
+      if (ident() != "integer") error("for loop variable must be integer");
+      s->loop_var = ident();
+      expect("=");
+      s->lo = expr();
+      expect(";");
+      if (ident() != s->loop_var) error("for condition must test the loop variable");
+      expect("<");
+      s->hi = expr();
+      expect(";");
+      if (ident() != s->loop_var) error("for step must advance the loop variable");
+      expect("+=");
+      if (peek().s != "1") error("for step must be += 1");
+      ++i;
+      expect(")");
+      s->then_b = block();
+      return s;
+    }
+    const std::string n = ident();
+    if (is("(")) {
+      s->k = St::Call;
+      s->callee = n;
+      expect("(");
+      if (!is(")")) {
+        s->args.push_back(expr());
+        while (is(",")) {
+          expect(",");
+          s->args.push_back(expr());
+        }
+      }
+      expect(")");
+      expect(";");
+      return s;
+    }
+    s->k = St::Assign;
+    s->target = n;
+    if (is("[")) {
+      expect("[");
+      s->indexed = true;
+      s->index = expr();
+      expect("]");
+    }
+    if (is("+=")) {
+      s->compound = true;
+      ++i;
+    } else {
+      expect("=");
+    }
+    s->expr = expr();
+    expect(";");
+    return s;
+  }
+
+  Fn function() {
+    Fn f;
+    while (is("device") || is("host") || is("global")) {
+      if (is("global")) f.global = true;
+      ++i;
+    }
+    if (is("void")) {
+      ++i;
+      f.returns_void = true;
+    } else if (ident() != "real") {
+      error("functions return real or void");
+    }
+    f.name = ident();
+    expect("(");
+    if (!is(")")) {
+      for (;;) {
+        Prm p;
+        p.type = type();
+        p.name = ident();
+        f.params.push_back(p);
+        if (!is(",")) break;
+        expect(",");
+      }
+    }
+    expect(")");
+    f.body = block();
+    return f;
+  }
+};
+
+// ---- typing --------------------------------------------------------------------
+const std::set<std::string> kIntrinsics = {"sin", "cos", "tan", "exp", "log",
+                                           "sqrt", "pow", "fabs", "__pop", "__pop_ctl"};
+const std::set<std::string> kKernelBuiltins = {"blockIdx", "blockDim", "threadIdx", "N"};
+
+struct Scope {
+  std::vector<std::map<std::string, VT>> frames;
+  bool global = false;
+  void push() { frames.emplace_back(); }
+  void pop() { frames.pop_back(); }
+  void add(const std::string& n, VT t) { frames.back()[n] = t; }
+  bool find(const std::string& n, VT& t) const {
+    for (auto it = frames.rbegin(); it != frames.rend(); ++it) {
+      auto f = it->find(n);
+      if (f != it->end()) {
+        t = f->second;
+        return true;
+      }
+    }
+    if (global && kKernelBuiltins.count(n)) {
+      t = VT::Integer;
+      return true;
+    }
+    return false;
+  }
+};
+
+void type_expr(Ex& e, const Scope& sc, Fn& f) {
+  for (auto& c : e.a) type_expr(*c, sc, f);
+  VT t;
+  switch (e.k) {
+    case Ex::Num: e.is_int = e.int_lit; break;
+    case Ex::Var:
+      if (!sc.find(e.name, t)) throw ParseError{"unknown variable '" + e.name + "' in " + f.name};
+      if (t == VT::RealArray)
+        throw ParseError{"array '" + e.name + "' used as a value in " + f.name};
+      e.is_int = t == VT::Integer;
+      break;
+    case Ex::Neg: e.is_int = e.a[0]->is_int; break;
+    case Ex::Bin: e.is_int = e.op != '/' && e.a[0]->is_int && e.a[1]->is_int; break;
+    case Ex::Cmp: e.is_int = false; break;
+    case Ex::Call:
+      if (!kIntrinsics.count(e.name))
+        throw ParseError{"unknown function '" + e.name + "' in an expression of " + f.name};
+      if (e.name == "__pop") f.uses_tape = true;
+      if (e.name == "__pop_ctl") f.uses_ctl = true;
+      e.is_int = e.name == "__pop_ctl";
+      break;
+    case Ex::Index:
+      if (!sc.find(e.name, t) || t != VT::RealArray)
+        throw ParseError{"'" + e.name + "' is not an array in " + f.name};
+      e.is_int = false;
+      break;
+  }
+}
+
+void type_block(Blk& b, Scope& sc, Fn& f) {
+  sc.push();
+  for (auto& sp : b) {
+    St& s = *sp;
+    switch (s.k) {
+      case St::Decl:
+        type_expr(*s.expr, sc, f);
+        sc.add(s.target, s.type);
+        break;
+      case St::Assign: {
+        VT t;
+        if (!sc.find(s.target, t)) throw ParseError{"unknown variable '" + s.target + "'"};
+        if (s.indexed) type_expr(*s.index, sc, f);
+        type_expr(*s.expr, sc, f);
+        break;
+      }
+      case St::Return: type_expr(*s.expr, sc, f); break;
+      case St::If:
+        type_expr(*s.expr, sc, f);
+        type_block(s.then_b, sc, f);
+        type_block(s.else_b, sc, f);
+        break;
+      case St::For:
+        type_expr(*s.lo, sc, f);
+        type_expr(*s.hi, sc, f);
+        sc.push();
+        sc.add(s.loop_var, VT::Integer);
+        type_block(s.then_b, sc, f);
+        sc.pop();
+        break;
+      case St::Call:
+        if (s.callee == "__push") f.uses_tape = true;
+        if (s.callee == "__push_ctl") f.uses_ctl = true;
+        for (auto& a : s.args) {
+          VT t;
+          if (a->k == Ex::Var && sc.find(a->name, t) && t == VT::RealArray) continue;  // whole array
+          type_expr(*a, sc, f);
+        }
+        break;
+    }
+  }
+  sc.pop();
+}
+
+// ---- hazard analysis (launch.cpp:112-240, conservatively) -------------------------
+// Which array parameters a function writes (directly or through callees).
+struct Module {
+  std::vector<Fn> fns;
+  const Fn* find(const std::string& n) const {
+    for (auto& f : fns)
+      if (f.name == n) return &f;
+    return nullptr;
+  }
+};
+
+void collect_writes(const Module& m, const Fn& f, std::set<std::string>& written,
+                    std::set<std::string>& visiting);
+
+void block_writes(const Module& m, const Blk& b, std::set<std::string>& w,
+                  std::set<std::string>& visiting) {
+  for (auto& sp : b) {
+    const St& s = *sp;
+    if (s.k == St::Assign && s.indexed) w.insert(s.target);
+    if (s.k == St::If) {
+      block_writes(m, s.then_b, w, visiting);
+      block_writes(m, s.else_b, w, visiting);
+    }
+    if (s.k == St::For) block_writes(m, s.then_b, w, visiting);
+    if (s.k == St::Call) {
+      const Fn* c = m.find(s.callee);
+      if (c == nullptr) continue;
+      std::set<std::string> cw;
+      collect_writes(m, *c, cw, visiting);
+      for (size_t a = 0; a < s.args.size() && a < c->params.size(); ++a)
+        if (cw.count(c->params[a].name) &&
+            (s.args[a]->k == Ex::Var || s.args[a]->k == Ex::Index))
+          w.insert(s.args[a]->name);
+    }
+  }
+}
+
+void collect_writes(const Module& m, const Fn& f, std::set<std::string>& written,
+                    std::set<std::string>& visiting) {
+  if (visiting.count(f.name)) return;
+  visiting.insert(f.name);
+  block_writes(m, f.body, written, visiting);
+  visiting.erase(f.name);
+}
+
+// Shared-write hazards of a global kernel: array params written other than
+// through the thread-indexed slice `a[i]` of `integer i = blockIdx*blockDim+threadIdx`.
+bool is_thread_index_decl(const St& s) {
+  if (s.k != St::Decl || s.type != VT::Integer) return false;
+  const Ex& e = *s.expr;
+  if (e.k != Ex::Bin || e.op != '+') return false;
+  const Ex& m = *e.a[0];
+  return m.k == Ex::Bin && m.op == '*' && m.a[0]->k == Ex::Var && m.a[0]->name == "blockIdx" &&
+         m.a[1]->k == Ex::Var && m.a[1]->name == "blockDim" && e.a[1]->k == Ex::Var &&
+         e.a[1]->name == "threadIdx";
+}
+
+void kernel_hazards(const Module& m, const Blk& b, const std::string& tid,
+                    const std::set<std::string>& arrays, std::map<std::string, std::string>& haz,
+                    std::string& tvar) {
+  for (auto& sp : b) {
+    const St& s = *sp;
+    if (is_thread_index_decl(s)) tvar = s.target;
+    if (s.k == St::Assign && s.indexed && arrays.count(s.target)) {
+      if (!(s.index->k == Ex::Var && s.index->name == tvar && !tvar.empty()))
+        haz[s.target] = "written at an index other than the thread index";
+    }
+    if (s.k == St::If) {
+      kernel_hazards(m, s.then_b, tid, arrays, haz, tvar);
+      kernel_hazards(m, s.else_b, tid, arrays, haz, tvar);
+    }
+    if (s.k == St::For) kernel_hazards(m, s.then_b, tid, arrays, haz, tvar);
+    if (s.k == St::Call) {
+      const Fn* c = m.find(s.callee);
+      if (c == nullptr) continue;
+      std::set<std::string> cw, vis;
+      collect_writes(m, *c, cw, vis);
+      for (size_t a = 0; a < s.args.size() && a < c->params.size(); ++a) {
+        const Ex& arg = *s.args[a];
+        if (!cw.count(c->params[a].name) || !arrays.count(arg.name)) continue;
+        if (arg.k == Ex::Var)
+          haz[arg.name] = "whole array shared with a writing callee across threads";
+        else if (arg.k == Ex::Index && !(arg.a[0]->k == Ex::Var && arg.a[0]->name == tvar))
+          haz[arg.name] = "slice at an index other than the thread index written by a callee";
+      }
+    }
+  }
+}
+
+// ---- CUDA emission ---------------------------------------------------------------
+struct Emitter {
+  const Module& m;
+  bool unsafe;
+  int tape_cap;
+  std::ostringstream o;
+  int tmp = 0;
+
+  static std::string dbl(double v) {
+    char b[64];
+    std::snprintf(b, sizeof b, "%.17g", v);
+    std::string s = b;
+    if (s.find_first_of(".eEn") == std::string::npos) s += ".0";
+    if (s == "inf") return "__longlong_as_double(0x7ff0000000000000LL)";
+    return s;
+  }
+  std::string ind(int d) { return std::string(2 * d, ' '); }
+
+  // integer-valued expression (only called when e.is_int)
+  std::string ie(const Ex& e) {
+    switch (e.k) {
+      case Ex::Num: return "(long long)" + std::to_string((long long)e.v);
+      case Ex::Var:
+        if (e.name == "blockIdx") return "(long long)blockIdx.x";
+        if (e.name == "blockDim") return "(long long)blockDim.x";
+        if (e.name == "threadIdx") return "(long long)threadIdx.x";
+        return e.name;
+      case Ex::Neg: return "(-" + ie(*e.a[0]) + ")";
+      case Ex::Bin:
+        return "(" + ie(*e.a[0]) + " " + std::string(1, e.op) + " " + ie(*e.a[1]) + ")";
+      case Ex::Call: return "adc_pop_ctl(ctl, cp, ctx)";
+      default: return "0";
+    }
+  }
+  // real-valued expression (an integer expression is converted, eval.cpp:526)
+  std::string re(const Ex& e) {
+    if (e.is_int) return "(double)" + ie(e);
+    switch (e.k) {
+      case Ex::Num: return dbl(e.v);
+      case Ex::Var: return e.name;
+      case Ex::Neg: return "(-" + re(*e.a[0]) + ")";
+      case Ex::Bin: {
+        const std::string a = re(*e.a[0]), b = re(*e.a[1]);
+        switch (e.op) {
+          case '+': return "__dadd_rn(" + a + ", " + b + ")";
+          case '-': return "__dsub_rn(" + a + ", " + b + ")";
+          case '*': return "__dmul_rn(" + a + ", " + b + ")";
+          default: return "adc_div(" + a + ", " + b + ", ctx)";
+        }
+      }
+      case Ex::Call: {
+        if (e.name == "__pop") return "adc_pop(tape, tp, ctx)";
+        std::vector<std::string> a;
+        for (auto& c : e.a) a.push_back(re(*c));
+        if (e.name == "log") return "adc_log(" + a[0] + ", ctx)";
+        if (e.name == "sqrt") return "adc_sqrt(" + a[0] + ", ctx)";
+        if (e.name == "pow") return "pow(" + a[0] + ", " + a[1] + ")";
+        return e.name + "(" + a[0] + ")";
+      }
+      case Ex::Index: return "adc_ld(" + e.name + ", " + ie_any(*e.a[0]) + ", ctx)";
+      default: return "0.0";
+    }
+  }
+  // an index: the interpreter evaluates it with eval_int (must be integer)
+  std::string ie_any(const Ex& e) {
+    if (!e.is_int) throw ParseError{"array index is not an integer expression"};
+    return ie(e);
+  }
+  std::string cond(const Ex& e) {
+    if (e.k != Ex::Cmp) throw ParseError{"condition must be a comparison"};
+    const bool ints = e.a[0]->is_int && e.a[1]->is_int;
+    const std::string a = ints ? ie(*e.a[0]) : re(*e.a[0]);
+    const std::string b = ints ? ie(*e.a[1]) : re(*e.a[1]);
+    return "(" + a + " " + e.cmp + " " + b + ")";
+  }
+
+  void block(const Blk& b, const Fn& f, Scope& sc, int d) {
+    sc.push();
+    for (auto& sp : b) stmt(*sp, f, sc, d);
+    sc.pop();
+  }
+
+  void stmt(const St& s, const Fn& f, Scope& sc, int d) {
+    VT t;
+    switch (s.k) {
+      case St::Decl:
+        if (s.type == VT::Integer)
+          o << ind(d) << "long long " << s.target << " = " << ie_any(*s.expr) << ";\n";
+        else
+          o << ind(d) << "double " << s.target << " = " << re(*s.expr) << ";\n";
+        sc.add(s.target, s.type);
+        break;
+      case St::Assign:
+        sc.find(s.target, t);
+        if (s.indexed) {
+          const std::string idx = ie_any(*s.index), v = re(*s.expr);
+          if (s.compound)
+            o << ind(d) << (unsafe ? "adc_st_add_atomic(" : "adc_st_add(") << s.target << ", "
+              << idx << ", " << v << ", ctx);\n";
+          else
+            o << ind(d) << "adc_st(" << s.target << ", " << idx << ", " << v << ", ctx);\n";
+        } else if (t == VT::Integer) {
+          const std::string v = ie_any(*s.expr);
+          if (s.compound) o << ind(d) << s.target << " = " << s.target << " + " << v << ";\n";
+          else o << ind(d) << s.target << " = " << v << ";\n";
+        } else {
+          const std::string v = re(*s.expr);
+          if (s.compound)
+            o << ind(d) << s.target << " = __dadd_rn(" << s.target << ", " << v << ");\n";
+          else
+            o << ind(d) << s.target << " = " << v << ";\n";
+        }
+        break;
+      case St::Return:
+        o << ind(d) << "return " << re(*s.expr) << ";\n";
+        break;
+      case St::If:
+        o << ind(d) << "if " << cond(*s.expr) << " {\n";
+        block(s.then_b, f, sc, d + 1);
+        o << ind(d) << "}";
+        if (!s.else_b.empty()) {
+          o << " else {\n";
+          block(s.else_b, f, sc, d + 1);
+          o << ind(d) << "}";
+        }
+        o << "\n";
+        break;
+      case St::For: {
+        const int k = tmp++;
+        o << ind(d) << "{\n";
+        o << ind(d + 1) << "const long long _adc_lo" << k << " = " << ie_any(*s.lo) << ";\n";
+        o << ind(d + 1) << "const long long _adc_hi" << k << " = " << ie_any(*s.hi) << ";\n";
+        o << ind(d + 1) << "for (long long " << s.loop_var << " = _adc_lo" << k << "; "
+          << s.loop_var << " < _adc_hi" << k << "; ++" << s.loop_var << ") {\n";
+        sc.push();
+        sc.add(s.loop_var, VT::Integer);
+        block(s.then_b, f, sc, d + 2);
+        sc.pop();
+        o << ind(d + 1) << "}\n" << ind(d) << "}\n";
+        break;
+      }
+      case St::Call: {
+        if (s.callee == "__push") {
+          o << ind(d) << "adc_push(tape, tp, " << re(*s.args[0]) << ", ctx);\n";
+          break;
+        }
+        if (s.callee == "__push_ctl") {
+          o << ind(d) << "adc_push_ctl(ctl, cp, " << ie_any(*s.args[0]) << ", ctx);\n";
+          break;
+        }
+        const Fn* c = m.find(s.callee);
+        if (c == nullptr) throw ParseError{"unknown callee '" + s.callee + "'"};
+        if (c->global) throw ParseError{"a kernel cannot call a global function"};
+        if (c->params.size() != s.args.size())
+          throw ParseError{"wrong argument count calling '" + s.callee + "'"};
+        o << ind(d) << "fn_" << c->name << "(";
+        for (size_t a = 0; a < s.args.size(); ++a) {
+          const Ex& arg = *s.args[a];
+          const VT pt = c->params[a].type;
+          if (a) o << ", ";
+          if (pt == VT::RealArray) {
+            if (arg.k == Ex::Var) o << arg.name;  // whole array
+            else if (arg.k == Ex::Index)          // length-1 slice (eval.cpp:485-499)
+              o << "adc_slice(" << arg.name << ", " << ie_any(*arg.a[0]) << ", ctx)";
+            else throw ParseError{"argument of '" + s.callee + "' must be an array or slice"};
+          } else if (pt == VT::Integer) {
+            o << ie_any(arg);
+          } else {
+            o << re(arg);
+          }
+        }
+        o << ", ctx);\n";
+        break;
+      }
+    }
+  }
+
+  static std::string ptype(VT t) {
+    return t == VT::RealArray ? "AdcArr" : t == VT::Integer ? "long long" : "double";
+  }
+
+  void prelude() {
+    o << R"(// Generated by libadc_b200 (csrc/jit.cpp) from a DSL module; sm_100a, -fmad=false.
+struct AdcArr { double* p; long long len; };
+struct AdcErr { unsigned long long code; long long thread; long long aux; };
+struct AdcCtx { AdcErr* err; long long tid; };
+enum { ADC_JE_DIV0 = 1, ADC_JE_LOG = 2, ADC_JE_SQRT = 3, ADC_JE_INDEX = 4, ADC_JE_TAPE_FULL = 5,
+       ADC_JE_TAPE_EMPTY = 6, ADC_JE_CTL_EMPTY = 7 };
+__device__ __noinline__ void adc_fail(const AdcCtx& c, unsigned code, long long aux) {
+  if (atomicCAS(&c.err->code, 0ull, (unsigned long long)code) == 0ull) {
+    c.err->thread = c.tid;
+    c.err->aux = aux;
+  }
+}
+__device__ __forceinline__ double adc_div(double a, double b, const AdcCtx& c) {
+  if (b == 0.0) adc_fail(c, ADC_JE_DIV0, 0);
+  return __ddiv_rn(a, b);
+}
+__device__ __forceinline__ double adc_log(double a, const AdcCtx& c) {
+  if (a <= 0.0) adc_fail(c, ADC_JE_LOG, 0);
+  return log(a);
+}
+__device__ __forceinline__ double adc_sqrt(double a, const AdcCtx& c) {
+  if (a < 0.0) adc_fail(c, ADC_JE_SQRT, 0);
+  return __dsqrt_rn(a);
+}
+__device__ __forceinline__ bool adc_ok(const AdcArr& a, long long i, const AdcCtx& c) {
+  if (i < 0 || i >= a.len) { adc_fail(c, ADC_JE_INDEX, i); return false; }
+  return true;
+}
+__device__ __forceinline__ double adc_ld(const AdcArr& a, long long i, const AdcCtx& c) {
+  return adc_ok(a, i, c) ? a.p[i] : __longlong_as_double(0x7ff8000000000000LL);
+}
+__device__ __forceinline__ void adc_st(const AdcArr& a, long long i, double v, const AdcCtx& c) {
+  if (adc_ok(a, i, c)) a.p[i] = v;
+}
+__device__ __forceinline__ void adc_st_add(const AdcArr& a, long long i, double v, const AdcCtx& c) {
+  if (adc_ok(a, i, c)) a.p[i] = __dadd_rn(a.p[i], v);
+}
+__device__ __forceinline__ void adc_st_add_atomic(const AdcArr& a, long long i, double v,
+                                                  const AdcCtx& c) {
+  if (adc_ok(a, i, c)) atomicAdd(a.p + i, v);
+}
+__device__ __forceinline__ AdcArr adc_slice(const AdcArr& a, long long i, const AdcCtx& c) {
+  AdcArr s{a.p, 0};
+  if (adc_ok(a, i, c)) { s.p = a.p + i; s.len = 1; }
+  return s;
+}
+)";
+    o << "#define ADC_TAPE " << tape_cap << "\n";
+    o << R"(__device__ __forceinline__ void adc_push(double* t, int& tp, double v, const AdcCtx& c) {
+  if (tp >= ADC_TAPE) { adc_fail(c, ADC_JE_TAPE_FULL, tp); return; }
+  t[tp++] = v;
+}
+__device__ __forceinline__ double adc_pop(double* t, int& tp, const AdcCtx& c) {
+  if (tp <= 0) { adc_fail(c, ADC_JE_TAPE_EMPTY, 0); return 0.0; }
+  return t[--tp];
+}
+__device__ __forceinline__ void adc_push_ctl(long long* t, int& cp, long long v, const AdcCtx& c) {
+  if (cp >= ADC_TAPE) { adc_fail(c, ADC_JE_TAPE_FULL, cp); return; }
+  t[cp++] = v;
+}
+__device__ __forceinline__ long long adc_pop_ctl(long long* t, int& cp, const AdcCtx& c) {
+  if (cp <= 0) { adc_fail(c, ADC_JE_CTL_EMPTY, 0); return 0; }
+  return t[--cp];
+}
+)";
+  }
+
+  void function(const Fn& f) {
+    Scope sc;
+    sc.push();
+    for (auto& p : f.params) sc.add(p.name, p.type);
+    if (f.global) {
+      sc.global = true;
+      o << "extern \"C\" __global__ void adc_kernel_" << f.name << "(";
+      for (size_t i = 0; i < f.params.size(); ++i) {
+        const Prm& p = f.params[i];
+        if (i) o << ", ";
+        if (p.type == VT::RealArray) o << "double* " << p.name << "_p, long long " << p.name << "_n";
+        else o << ptype(p.type) << " " << p.name;
+      }
+      o << (f.params.empty() ? "" : ", ") << "long long N, AdcErr* adc_err) {\n";
+      o << "  const AdcCtx ctx{adc_err, (long long)blockIdx.x * blockDim.x + threadIdx.x};\n";
+      for (auto& p : f.params)
+        if (p.type == VT::RealArray)
+          o << "  const AdcArr " << p.name << "{" << p.name << "_p, " << p.name << "_n};\n";
+    } else {
+      o << "__device__ " << (f.returns_void ? "void" : "double") << " fn_" << f.name << "(";
+      for (size_t i = 0; i < f.params.size(); ++i)
+        o << (i ? ", " : "") << ptype(f.params[i].type) << " " << f.params[i].name;
+      o << (f.params.empty() ? "" : ", ") << "const AdcCtx& ctx) {\n";
+    }
+    if (f.uses_tape) o << "  double tape[ADC_TAPE]; int tp = 0;\n";
+    if (f.uses_ctl) o << "  long long ctl[ADC_TAPE]; int cp = 0;\n";
+    block(f.body, f, sc, 1);
+    if (!f.returns_void && !f.global) o << "  return __longlong_as_double(0x7ff8000000000000LL);\n";
+    o << "}\n\n";
+  }
+};
+
+std::string hazard_message(const std::map<std::string, std::string>& haz) {
+  std::string msg = "launch refused, hazardous parameter(s):";
+  for (auto& h : haz) msg += " " + h.first + " (" + h.second + ")";
+  return msg + "; pass the unsafe flag to force";
+}
+
+}  // namespace
+
+// ---- the module object ------------------------------------------------------------
+struct adc_jit_module {
+  std::string kernel;
+  std::vector<int32_t> kinds;  // 0 real[], 1 real, 2 integer
+  std::vector<std::string> names;
+  std::string cuda;
+  std::vector<char> cubin;
+  std::map<int, cudaLibrary_t> libs;  // per device
+  std::map<int, cudaKernel_t> fns;
+  std::mutex mu;
+};
+
+namespace {
+int parse_module(const std::string& src, Module& m) {
+  try {
+    Parser p;
+    p.t = lex(src);
+    while (p.peek().k != Tok::End) m.fns.push_back(p.function());
+    for (auto& f : m.fns) {
+      Scope sc;
+      sc.global = f.global;
+      sc.push();
+      for (auto& prm : f.params) sc.add(prm.name, prm.type);
+      type_block(f.body, sc, f);
+    }
+  } catch (const ParseError& e) {
+    return fail(ADC_E_SEMANTIC, "jit: " + e.msg);
+  }
+  return ADC_OK;
+}
+}  // namespace
+
+extern "C" int adc_jit_compile(const char* source, const char* kernel, int32_t unsafe,
+                               int32_t tape_capacity, adc_jit_module** out) {
+  clear_error();
+  if (source == nullptr || kernel == nullptr || out == nullptr)
+    return fail(ADC_E_ARG, "null argument");
+  *out = nullptr;
+  if (tape_capacity <= 0) tape_capacity = 256;
+  Module m;
+  if (int rc = parse_module(source, m)) return rc;
+  const Fn* k = m.find(kernel);
+  if (k == nullptr) return fail(ADC_E_LAUNCH, std::string("unknown kernel '") + kernel + "'");
+  if (!k->global) return fail(ADC_E_LAUNCH, std::string("'") + kernel + "' is not a global kernel");
+  // race_check (launch.cpp:261-267): same refusal message
+  std::set<std::string> arrays;
+  for (auto& p : k->params)
+    if (p.type == VT::RealArray) arrays.insert(p.name);
+  std::map<std::string, std::string> haz;
+  std::string tvar;
+  kernel_hazards(m, k->body, "", arrays, haz, tvar);
+  if (!haz.empty() && !unsafe) return fail(ADC_E_LAUNCH, hazard_message(haz));
+  Emitter em{m, unsafe != 0, tape_capacity, {}, 0};
+  try {
+    em.prelude();
+    for (auto& f : m.fns)
+      if (!f.global && f.name != "") em.o << "__device__ " << (f.returns_void ? "void" : "double") << " fn_"
+                          << f.name << "(" << [&] {
+                               std::string s;
+                               for (size_t i = 0; i < f.params.size(); ++i)
+                                 s += (i ? ", " : "") + Emitter::ptype(f.params[i].type) + " " +
+                                      f.params[i].name;
+                               return s + (f.params.empty() ? "" : ", ") + "const AdcCtx& ctx);\n";
+                             }();
+    em.o << "\n";
+    // only what the kernel reaches through call statements
+    std::set<std::string> reach{kernel};
+    std::vector<const Fn*> work{k};
+    std::function<void(const Blk&)> scan = [&](const Blk& b) {
+      for (auto& sp : b) {
+        if (sp->k == St::Call && !reach.count(sp->callee)) {
+          if (const Fn* c = m.find(sp->callee)) {
+            reach.insert(c->name);
+            work.push_back(c);
+          }
+        }
+        scan(sp->then_b);
+        scan(sp->else_b);
+      }
+    };
+    for (size_t w = 0; w < work.size(); ++w) scan(work[w]->body);
+    for (auto& f : m.fns)
+      if (reach.count(f.name)) em.function(f);
+  } catch (const ParseError& e) {
+    return fail(ADC_E_SEMANTIC, "jit: " + e.msg);
+  }
+  const Nvrtc* N = nvrtc();
+  if (N == nullptr) return fail(ADC_E_CUDA, "jit: libnvrtc.so.12 could not be loaded");
+  auto* J = new (std::nothrow) adc_jit_module();
+  if (J == nullptr) return fail(ADC_E_ARG, "out of host memory");
+  J->kernel = kernel;
+  for (auto& p : k->params) {
+    J->kinds.push_back(p.type == VT::RealArray ? 0 : p.type == VT::Real ? 1 : 2);
+    J->names.push_back(p.name);
+  }
+  J->cuda = em.o.str();
+  nvrtcProgram prog = nullptr;
+  nvrtcResult r = N->create(&prog, J->cuda.c_str(), "adc_jit.cu", 0, nullptr, nullptr);
+  if (r != NVRTC_SUCCESS) {
+    delete J;
+    return fail(ADC_E_CUDA, std::string("nvrtcCreateProgram: ") + N->error_string(r));
+  }
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "--std=c++17",
+                        "-default-device", "--extra-device-vectorization"};
+  r = N->compile(prog, 5, opts);
+  if (r != NVRTC_SUCCESS) {
+    size_t n = 0;
+    N->log_size(prog, &n);
+    std::string log(n, '\0');
+    if (n) N->log(prog, &log[0]);
+    N->destroy(&prog);
+    delete J;
+    return fail(ADC_E_CUDA, "jit: NVRTC failed: " + log);
+  }
+  size_t n = 0;
+  N->cubin_size(prog, &n);
+  J->cubin.resize(n);
+  N->cubin(prog, J->cubin.data());
+  N->destroy(&prog);
+  *out = J;
+  return ADC_OK;
+}
+
+extern "C" int adc_jit_destroy(adc_jit_module* J) {
+  if (J == nullptr) return ADC_OK;
+  for (auto& l : J->libs) cudaLibraryUnload(l.second);
+  delete J;
+  return ADC_OK;
+}
+
+extern "C" int adc_jit_kernel_params(const adc_jit_module* J, int32_t* nparams, int32_t* kinds,
+                                     int32_t cap) {
+  clear_error();
+  if (J == nullptr || nparams == nullptr) return fail(ADC_E_ARG, "null argument");
+  *nparams = (int32_t)J->kinds.size();
+  for (int32_t i = 0; kinds != nullptr && i < cap && i < *nparams; ++i) kinds[i] = J->kinds[i];
+  return ADC_OK;
+}
+
+extern "C" const char* adc_jit_kernel_param_name(const adc_jit_module* J, int32_t i) {
+  return J && i >= 0 && i < (int32_t)J->names.size() ? J->names[i].c_str() : nullptr;
+}
+
+extern "C" const char* adc_jit_cuda_source(const adc_jit_module* J) {
+  return J ? J->cuda.c_str() : nullptr;
+}
+
+extern "C" size_t adc_jit_cubin_size(const adc_jit_module* J) { return J ? J->cubin.size() : 0; }
+
+namespace {
+const char* jit_error_text(unsigned long long code) {
+  switch (code) {
+    case 1: return "division by zero";
+    case 2: return "log of non-positive value";
+    case 3: return "sqrt of negative value";
+    case 4: return "index out of range";
+    case 5: return "tape capacity exceeded (raise tape_capacity)";
+    case 6: return "__pop on empty tape";
+    case 7: return "__pop_ctl on empty control tape";
+    default: return "device error";
+  }
+}
+
+struct ErrWord {
+  unsigned long long code;
+  long long thread, aux;
+};
+}  // namespace
+
+extern "C" int adc_cuda_jit_launch(adc_jit_module* J, int64_t grid, int64_t block, int64_t n,
+                                   const adc_jit_arg* args, int32_t nargs, void* stream) {
+  clear_error();
+  if (J == nullptr || (nargs > 0 && args == nullptr)) return fail(ADC_E_ARG, "null argument");
+  if (grid <= 0 || block <= 0 || n <= 0)
+    return fail(ADC_E_LAUNCH, "launch configuration must be positive (grid " +
+                                  std::to_string(grid) + ", block " + std::to_string(block) +
+                                  ", n " + std::to_string(n) + ")");
+  if (grid > INT64_MAX / block || grid * block < n)
+    return fail(ADC_E_LAUNCH, "grid " + std::to_string(grid) + " x block " + std::to_string(block) +
+                                  " does not cover problem size " + std::to_string(n));
+  if (block > 1024 || grid > 0x7fffffff)
+    return fail(ADC_E_LAUNCH, "block must be <= 1024 and grid < 2^31 on the device");
+  if (nargs != (int32_t)J->kinds.size())
+    return fail(ADC_E_LAUNCH, "kernel '" + J->kernel + "' takes " +
+                                  std::to_string(J->kinds.size()) + " parameters");
+  if (!device_present()) return fail(ADC_E_CUDA, "no CUDA device: the B200 engine has no CPU fallback");
+  int dev = 0;
+  ADCB_CUDA(cudaGetDevice(&dev));
+  cudaKernel_t fn = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(J->mu);
+    auto it = J->fns.find(dev);
+    if (it == J->fns.end()) {
+      cudaLibrary_t lib = nullptr;
+      ADCB_CUDA(cudaLibraryLoadData(&lib, J->cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+      const std::string name = "adc_kernel_" + J->kernel;
+      cudaError_t e = cudaLibraryGetKernel(&fn, lib, name.c_str());
+      if (e != cudaSuccess) {
+        cudaLibraryUnload(lib);
+        return cuda_fail(e, "cudaLibraryGetKernel");
+      }
+      J->libs[dev] = lib;
+      J->fns[dev] = fn;
+    } else {
+      fn = it->second;
+    }
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ErrWord* derr = nullptr;
+  ErrWord herr{};
+  ADCB_CUDA(cudaMallocAsync(&derr, sizeof(ErrWord), s));
+  ADCB_CUDA(cudaMemsetAsync(derr, 0, sizeof(ErrWord), s));
+  // kernel arguments: real[] -> (double*, long long len), real -> double, integer -> long long
+  std::vector<double*> ptrs(nargs);
+  std::vector<long long> lens(nargs), ints(nargs);
+  std::vector<double> reals(nargs);
+  std::vector<void*> kp;
+  for (int32_t i = 0; i < nargs; ++i) {
+    switch (J->kinds[i]) {
+      case 0:
+        if (args[i].ptr == nullptr && args[i].len > 0)
+          return fail(ADC_E_LAUNCH, "missing buffer for parameter " + std::to_string(i));
+        ptrs[i] = args[i].ptr;
+        lens[i] = args[i].len;
+        kp.push_back(&ptrs[i]);
+        kp.push_back(&lens[i]);
+        break;
+      case 1:
+        reals[i] = args[i].real_value;
+        kp.push_back(&reals[i]);
+        break;
+      default:
+        ints[i] = args[i].int_value;
+        kp.push_back(&ints[i]);
+        break;
+    }
+  }
+  long long nn = n;
+  kp.push_back(&nn);
+  kp.push_back(&derr);
+  cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void*>(fn), dim3((unsigned)grid),
+                                   dim3((unsigned)block), kp.data(), 0, s);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(derr, s);
+    return cuda_fail(e, "cudaLaunchKernel (jit)");
+  }
+  ADCB_CUDA(cudaMemcpyAsync(&herr, derr, sizeof(ErrWord), cudaMemcpyDeviceToHost, s));
+  ADCB_CUDA(cudaFreeAsync(derr, s));
+  ADCB_CUDA(cudaStreamSynchronize(s));
+  if (herr.code != 0) {
+    std::string msg = jit_error_text(herr.code);
+    if (herr.code == 4) msg = "index " + std::to_string(herr.aux) + " out of range";
+    return fail(ADC_E_EVAL, msg + " (thread " + std::to_string(herr.thread) + ")");
+  }
+  return ADC_OK;
+}
+
+extern "C" int adc_cuda_jit_launch_host(adc_jit_module* J, int64_t grid, int64_t block, int64_t n,
+                                        const adc_jit_arg* args, int32_t nargs) {
+  clear_error();
+  if (J == nullptr || (nargs > 0 && args == nullptr)) return fail(ADC_E_ARG, "null argument");
+  if (nargs != (int32_t)J->kinds.size())
+    return fail(ADC_E_LAUNCH, "kernel '" + J->kernel + "' takes " +
+                                  std::to_string(J->kinds.size()) + " parameters");
+  if (!device_present()) return fail(ADC_E_CUDA, "no CUDA device: the B200 engine has no CPU fallback");
+  std::vector<adc_jit_arg> dargs(args, args + nargs);
+  std::vector<double*> owned;
+  auto release = [&] {
+    for (double* p : owned) cudaFree(p);
+  };
+  for (int32_t i = 0; i < nargs; ++i) {
+    if (J->kinds[i] != 0 || args[i].len <= 0) continue;
+    double* d = nullptr;
+    const size_t bytes = (size_t)args[i].len * sizeof(double);
+    cudaError_t e = cudaMalloc(&d, bytes);
+    if (e == cudaSuccess) e = cudaMemcpy(d, args[i].ptr, bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      release();
+      return cuda_fail(e, "jit host staging");
+    }
+    owned.push_back(d);
+    dargs[i].ptr = d;
+  }
+  const int rc = adc_cuda_jit_launch(J, grid, block, n, dargs.data(), nargs, nullptr);
+  // buffers are written in place even when a thread reported an error, as in
+  // the reference (a throwing launch leaves the other threads' writes)
+  for (int32_t i = 0, k = 0; i < nargs; ++i) {
+    if (J->kinds[i] != 0 || args[i].len <= 0) continue;
+    cudaMemcpy(args[i].ptr, dargs[i].ptr, (size_t)args[i].len * sizeof(double),
+               cudaMemcpyDeviceToHost);
+    ++k;
+  }
+  release();
+  return rc;
+}

@@ -102,6 +102,74 @@ def main():
                    f"{name}_dsigma": o[2 * n:], f"{name}_sigma": sigma, f"{name}_block": block})
     np.savez(os.path.join(OUT, "gauss_shared_cases.npz"), **sh)
 
+    # Generic lowering: Listing-style kernels (oracle/dsl/jit_kernels.dsl) over
+    # the reference corpus gradients, run by the reference's own adc::launch;
+    # the printed module (what the B200 JIT consumes) is stored with them.
+    corpus = "/root/reference/proj/corpus"
+    dsl = os.path.join(tmp, "jit.dsl")
+    with open(dsl, "w") as fh:
+        for name in ("gauss", "rational", "branchy", "poly", "looped", "gsum", "sumn"):
+            fh.write(open(os.path.join(corpus, name + ".dsl")).read() + "\n")
+        fh.write(open(os.path.join(ROOT, "oracle", "dsl", "jit_kernels.dsl")).read())
+    r = np.random.Generator(np.random.PCG64(77))
+    n = 1000
+    ji, module_text = {}, None
+    cases = (
+        ("gauss", "k_gauss", n, [r.uniform(-3, 3, n), r.uniform(-2, 2, n), 1.3,
+                                 r.standard_normal(n), r.standard_normal(n)], ""),
+        ("rational", "k_rational", n, [r.uniform(-2, 2, n), r.uniform(-2, 2, n), np.zeros(n),
+                                      np.zeros(n)], ""),
+        ("branchy", "k_branchy", n, [r.uniform(-4, 4, n), r.uniform(-4, 4, n), np.zeros(n),
+                                    r.standard_normal(n)], ""),
+        ("poly", "k_poly", n, [r.uniform(-2, 2, n), r.uniform(-2, 2, n), np.zeros(n),
+                              np.zeros(n)], ""),
+        ("looped", "k_looped", n, [r.uniform(-2, 3, n), 10, np.zeros(n)], ""),
+        ("gsum", "k_gsum", 500, [r.uniform(-5, 5, 500), np.array([1.0, 0.0, 1.5, 0.5, 1.0, 0.7]),
+                                 2, np.zeros(6)], "unsafe"),
+        ("sumn", "k_sumn", 200, [r.uniform(-1, 1, 64), 64, np.zeros(64)], "unsafe"),
+        ("gauss_div0", "k_gauss", 64, [np.ones(64), np.zeros(64), 0.0, np.zeros(64),
+                                       np.zeros(64)], "sequential"),
+    )
+    for key, kern, nn, params, mode in cases:
+        flat = []
+        for v in params:
+            if isinstance(v, np.ndarray):
+                flat += [float(v.size)] + list(v)
+            else:
+                flat.append(float(v))
+        np.array(flat, dtype="<f8").tofile(ti)
+        mod = os.path.join(tmp, "module.txt")
+        meta = run("launch-file", dsl, kern, nn, 256, ti, to, mod, *([mode] if mode else []))
+        text = open(mod).read()
+        assert module_text in (None, text)
+        module_text = text
+        arrays = [v for v in params if isinstance(v, np.ndarray)]
+        o = f64(to, sum(a.size for a in arrays))
+        outs, off = [], 0
+        for a in arrays:
+            outs.append(o[off:off + a.size])
+            off += a.size
+        ji[f"{key}_kernel"] = kern
+        ji[f"{key}_n"] = nn
+        ji[f"{key}_mode"] = mode
+        ji[f"{key}_error"] = meta["error"]
+        ji[f"{key}_nparams"] = len(params)
+        for i, v in enumerate(params):
+            ji[f"{key}_in{i}"] = np.asarray(v, dtype=np.float64)
+        for i, v in enumerate(outs):
+            ji[f"{key}_out{i}"] = v
+    # the reference's refusal of the hazardous kernels (no unsafe flag)
+    for key in ("gsum", "sumn"):
+        flat = []
+        for v in [ji[f"{key}_in{i}"] for i in range(ji[f"{key}_nparams"])]:
+            flat += [float(v.size)] + list(v) if v.ndim else [float(v)]
+        np.array(flat, dtype="<f8").tofile(ti)
+        meta = run("launch-file", dsl, ji[f"{key}_kernel"], ji[f"{key}_n"], 256, ti, to,
+                   os.path.join(tmp, "m2.txt"))
+        ji[f"{key}_refused"] = meta["error"]
+    ji["module"] = module_text
+    np.savez(os.path.join(OUT, "jit_cases.npz"), **ji)
+
     # N-dim Gaussian, SoA layout, nonzero initial slots (accumulate semantics).
     nd = {}
     for dim, n, seed in ((100, 64, 11), (1000, 8, 12), (1, 33, 13), (37, 70, 14), (128, 40, 15),

@@ -1,0 +1,75 @@
+"""Generic lowering, host side (no device): every corpus kernel of the golden
+module parses, passes the hazard gate exactly as the reference's race_check
+does, is emitted as IEEE-exact CUDA and compiles for sm_100a with NVRTC."""
+import numpy as np
+import pytest
+
+from conftest import golden
+
+import paper_2203_06139_b200 as adc  # noqa: E402
+
+G = golden("jit_cases.npz")
+MODULE = str(G["module"])
+CASES = ["gauss", "rational", "branchy", "poly", "looped", "gsum", "sumn"]
+
+
+@pytest.mark.parametrize("key", CASES)
+def test_corpus_kernel_compiles_for_sm100a(key):
+    unsafe = str(G[f"{key}_mode"]) == "unsafe"
+    m = adc.JitModule(MODULE, str(G[f"{key}_kernel"]), unsafe=unsafe)
+    assert m.cubin_size > 1000
+    src = m.cuda_source
+    # one IEEE op per DSL op, no contraction: only the _rn intrinsics do arithmetic
+    assert "__dadd_rn" in src or "__dmul_rn" in src
+    assert "__fma" not in src and "fma(" not in src
+    if unsafe:
+        assert "adc_st_add_atomic(" in src
+
+
+@pytest.mark.parametrize("key", ["gsum", "sumn"])
+def test_hazard_refused_with_reference_message(key):
+    with pytest.raises(adc.AdcError) as e:
+        adc.JitModule(MODULE, str(G[f"{key}_kernel"]))
+    assert e.value.kind == "Launch"
+    assert str(e.value) == str(G[f"{key}_refused"])
+
+
+def test_params_and_kinds():
+    m = adc.JitModule(MODULE, "k_looped")
+    assert m.params == [("x", "real[]"), ("n", "integer"), ("dx", "real[]")]
+
+
+@pytest.mark.parametrize("src,kind", [
+    ("global void k(real[] x) { integer i = blockIdx * blockDim + threadIdx; if (i < N) { "
+     "nothere(x[i]); } }", "Semantic"),
+    ("global void k(real[] x) { x[0] += $; }", "Semantic"),
+    ("device host real f(real x) { return y; }\nglobal void k() { }", "Semantic"),
+])
+def test_bad_modules_are_semantic_errors(src, kind):
+    with pytest.raises(adc.AdcError) as e:
+        adc.JitModule(src, "k")
+    assert e.value.kind == kind
+
+
+def test_unknown_and_non_global_kernels():
+    with pytest.raises(adc.AdcError) as e:
+        adc.JitModule(MODULE, "nope")
+    assert e.value.kind == "Launch" and "unknown kernel" in str(e.value)
+    with pytest.raises(adc.AdcError) as e:
+        adc.JitModule(MODULE, "rational_grad")
+    assert "not a global kernel" in str(e.value)
+
+
+def test_launch_without_device_has_no_fallback():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("device present")
+    except ImportError:
+        pass
+    m = adc.JitModule(MODULE, "k_poly")
+    n = 8
+    bufs = adc.BufferSet(arrays={k: np.zeros(n) for k in ("x", "y", "dx", "dy")})
+    with pytest.raises(adc.AdcError) as e:
+        m.launch(adc.LaunchConfig(1, 8, n), bufs)
+    assert e.value.kind == "Cuda"
