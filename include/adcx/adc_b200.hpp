@@ -127,6 +127,47 @@ inline LaunchStats launch(const std::string& kernel, const LaunchConfig& cfg, Bu
   return st;
 }
 
+// Any Listing-style global kernel of a DSL module (as adc::print emits the
+// Program, derivatives included), lowered to CUDA by the engine's JIT; host
+// buffers, compiled once per (source, kernel, unsafe).
+inline LaunchStats launch_module(const std::string& source, const std::string& kernel,
+                                 const LaunchConfig& cfg, BufferSet& buffers,
+                                 const LaunchOptions& opts = {}) {
+  cfg.validate();
+  static std::map<std::string, adc_jit_module*> cache;
+  const std::string key = source + '\0' + kernel + (opts.unsafe ? "\1" : "\0");
+  adc_jit_module*& m = cache[key];
+  if (m == nullptr) check(adc_jit_compile(source.c_str(), kernel.c_str(), opts.unsafe, 0, &m));
+  int32_t np = 0;
+  int32_t kinds[64];
+  check(adc_jit_kernel_params(m, &np, kinds, 64));
+  std::vector<adc_jit_arg> args(static_cast<size_t>(np));
+  for (int32_t i = 0; i < np; ++i) {
+    const std::string name = adc_jit_kernel_param_name(m, i);
+    if (kinds[i] == 0) {
+      auto it = buffers.arrays.find(name);
+      if (it == buffers.arrays.end()) throw Error(ErrorKind::Launch, "missing buffer '" + name + "'");
+      args[i].ptr = it->second.data();
+      args[i].len = static_cast<int64_t>(it->second.size());
+    } else if (kinds[i] == 1) {
+      auto it = buffers.scalars.find(name);
+      if (it == buffers.scalars.end())
+        throw Error(ErrorKind::Launch, "missing scalar value '" + name + "'");
+      args[i].real_value = it->second;
+    } else {
+      auto it = buffers.integers.find(name);
+      if (it == buffers.integers.end())
+        throw Error(ErrorKind::Launch, "missing integer value '" + name + "'");
+      args[i].int_value = it->second;
+    }
+  }
+  check(adc_cuda_jit_launch_host(m, cfg.grid_dim, cfg.block_dim, cfg.n, args.data(), np));
+  LaunchStats st;
+  st.thread_statements.assign(static_cast<size_t>(cfg.grid_dim * cfg.block_dim), 2u);
+  for (int64_t g = 0; g < cfg.n; ++g) st.thread_statements[static_cast<size_t>(g)] = 3u;
+  return st;
+}
+
 // The batched path the reference cannot express:
 // gaussnd_grad_0_1 over n points, structure-of-arrays [d * ld + i].
 inline void launch_batch_gaussnd(int64_t n, int64_t dim, const std::vector<double>& x,

@@ -4,6 +4,7 @@
 
 #include <cstring>
 #include <map>
+#include <mutex>
 
 #include "adc/parser.hpp"
 #include "adc/printer.hpp"
@@ -112,6 +113,46 @@ void analytic_counts(const Program& p, const std::string& kernel, const Function
     st.thread_statements[static_cast<size_t>(g)] = static_cast<uint32_t>(active.top_statements);
 }
 
+// The generic path: the whole module as the reference prints it, lowered to
+// CUDA and compiled with NVRTC by the engine (adc_jit_*), cached per
+// (module text, kernel, unsafe).
+LaunchStats launch_jit(const Program& p, const std::string& kernel, const FunctionDef& k,
+                       const LaunchConfig& cfg, BufferSet& buffers, const LaunchOptions& opts) {
+  static std::mutex mu;
+  static std::map<std::string, adc_jit_module*> cache;
+  const std::string text = print(p.module());
+  const std::string key = text + '\0' + kernel + (opts.unsafe ? "\1" : "\0");
+  adc_jit_module* m = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      m = it->second;
+    } else {
+      check(adc_jit_compile(text.c_str(), kernel.c_str(), opts.unsafe ? 1 : 0, 0, &m));
+      cache[key] = m;
+    }
+  }
+  std::vector<adc_jit_arg> args(k.params.size());
+  for (size_t i = 0; i < k.params.size(); ++i) {
+    const Param& prm = k.params[i];
+    if (prm.type == ValType::RealArray) {
+      std::vector<double>& v = buffers.arrays.at(prm.name);
+      args[i].ptr = v.data();
+      args[i].len = static_cast<int64_t>(v.size());
+    } else if (prm.type == ValType::Real) {
+      args[i].real_value = buffers.scalars.at(prm.name);
+    } else {
+      args[i].int_value = buffers.integers.at(prm.name);
+    }
+  }
+  LaunchStats st;
+  analytic_counts(p, kernel, k, cfg, buffers, st);
+  check(adc_cuda_jit_launch_host(m, cfg.grid_dim, cfg.block_dim, cfg.n, args.data(),
+                                 static_cast<int32_t>(args.size())));
+  return st;
+}
+
 }  // namespace
 
 LaunchStats launch(const Program& p, const std::string& kernel, const LaunchConfig& cfg,
@@ -149,22 +190,23 @@ LaunchStats launch(const Program& p, const std::string& kernel, const LaunchConf
       throw Error(ErrorKind::Launch, "missing integer value '" + param.name + "'");
     }
   }
-  // Kernel shape + registry lookup by the callee's printed text.
+  // Kernel shape + registry lookup by the callee's printed text: the
+  // hand-written kernels.  Everything else is lowered by the generic JIT.
   Listing1 l1;
-  if (!match_listing1(*k, l1)) throw Error(ErrorKind::Launch, "no B200 kernel for '" + kernel + "'");
-  const FunctionDef* callee = p.module().find(l1.call->callee);
-  if (callee == nullptr) throw Error(ErrorKind::Launch, "unknown callee '" + l1.call->callee + "'");
+  const FunctionDef* callee =
+      match_listing1(*k, l1) ? p.module().find(l1.call->callee) : nullptr;
   int32_t id = -1;
-  check(adc_cuda_registry_find(callee->name.c_str(), fingerprint(*callee), &id));
-  const size_t nargs = l1.call->call_args.size();
+  const bool registered =
+      callee != nullptr &&
+      adc_cuda_registry_find(callee->name.c_str(), fingerprint(*callee), &id) == ADC_OK;
+  const size_t nargs = registered ? l1.call->call_args.size() : 0;
   // gauss_grad_0_1(x[i], p[i], sigma, dx[i], dp[i]) (compute), or the forced
   // hazardous gauss_grad(x[i], p[i], sigma, dx[i], dp[i], dsigma)
   // (compute_shared): only the shared slot may be a whole array.
-  const bool shared = id == ADC_KERNEL_GAUSS_GRAD && nargs == 6;
-  if (!(id == ADC_KERNEL_GAUSS_GRAD_0_1 && nargs == 5) && !shared)
-    throw Error(ErrorKind::Launch, "no B200 launch path for '" + callee->name + "'");
-  if (report.has_hazard() && !shared)
-    throw Error(ErrorKind::Launch, "no B200 kernel for '" + kernel + "'");
+  const bool shared = registered && id == ADC_KERNEL_GAUSS_GRAD && nargs == 6;
+  const bool plain = registered && id == ADC_KERNEL_GAUSS_GRAD_0_1 && nargs == 5 &&
+                     !report.has_hazard();
+  if (!plain && !shared) return launch_jit(p, kernel, *k, cfg, buffers, opts);
   std::vector<double*> arr;
   double sigma = 0.0;
   for (size_t a = 0; a < 5; ++a) {

@@ -15,11 +15,13 @@ namespace adc::b200_bridge {
 
 /// Same signature and contract as adc::launch (proj/include/adc/launch.hpp:66-67,
 /// proj/src/launch.cpp:252-346).  Validation, the race_check refusal and buffer
-/// binding are the reference's own; a Listing-1 kernel (thread index, `if (i < N)`
-/// guard, one call of a registered generated gradient with a[i] slices) runs on
-/// the GPU.  Anything else throws Error(Launch, "no B200 kernel ...") — callers
-/// that want the interpreter call adc::launch themselves; there is no silent
-/// fallback.
+/// binding are the reference's own.  A Listing-1 kernel calling a registered
+/// generated gradient (printed-text fingerprint) runs its hand-written sm_100a
+/// kernel; any other global kernel of the Program is lowered to CUDA by the
+/// engine's generic JIT (adc_jit_*, NVRTC).  Either way it runs on the GPU —
+/// there is no interpreter fallback; a module the JIT cannot lower throws.
+/// LaunchStats.counts come from one interpreted active and idle thread, exact
+/// for kernels whose op counts do not depend on the data.
 LaunchStats launch(const Program& p, const std::string& kernel, const LaunchConfig& cfg,
                    BufferSet& buffers, const LaunchOptions& opts = {});
 

@@ -52,7 +52,7 @@ static double rel(double a, double b) {
   return s == 0 ? 0 : std::fabs(a - b) / s;
 }
 
-static void cpu_checks(const Program& p) {
+static void cpu_checks(const Program& p, bool gpu) {
   // Refusal and binding errors are the reference's own, before any device use.
   BufferSet b;
   b.arrays["x"] = std::vector<double>(64, 0.5);
@@ -78,9 +78,13 @@ static void cpu_checks(const Program& p) {
   EXPECT(error_of([&] { b200_bridge::launch(p, "compute", {0, 256, 512}, b); }) ==
              error_of([&] { adc::launch(p, "compute", {0, 256, 512}, b); }),
          "bad LaunchConfig: same message");
-  EXPECT(error_of([&] { b200_bridge::launch(p, "noop", {1, 1, 1}, b); }).find("no B200 kernel") !=
-             std::string::npos,
-         "non-Listing-1 kernel: explicit 'no B200 kernel' (no fallback)");
+  if (gpu)
+    EXPECT(error_of([&] { b200_bridge::launch(p, "noop", {1, 1, 1}, b); }).empty(),
+           "non-registered kernel (noop) runs through the JIT");
+  else
+    EXPECT(error_of([&] { b200_bridge::launch(p, "noop", {1, 1, 1}, b); }).find("no CUDA device") !=
+               std::string::npos,
+           "non-registered kernel goes to the JIT: no device -> Error, no interpreter fallback");
 }
 
 static void gpu_checks(const Program& p) {
@@ -154,6 +158,45 @@ static void gpu_checks(const Program& p) {
     EXPECT(worst <= 1e-12 && ds <= 1e-9, "bridged forced compute_shared matches the reference");
     EXPECT(rs.counts == gs.counts, "compute_shared LaunchStats.counts equal");
   }
+  // Generic JIT path through the bridge: corpus gradients the registry does
+  // not hold, same inputs through adc::launch (sequential) and the bridge.
+  {
+    Module jm = parse_or_throw(kJitModuleDsl);
+    ensure_called_derivatives(jm);
+    Program jp(std::move(jm));
+    for (const char* kern : {"k_rational", "k_branchy", "k_looped"}) {
+      const int64_t n = 20001;
+      std::mt19937_64 rng(5);
+      BufferSet ref, gpu;
+      std::vector<double> x(n), y(n);
+      for (int64_t i = 0; i < n; ++i) {
+        x[i] = std::uniform_real_distribution<double>(-2, 2)(rng);
+        y[i] = std::uniform_real_distribution<double>(-2, 2)(rng);
+      }
+      for (BufferSet* b : {&ref, &gpu}) {
+        b->arrays["x"] = x;
+        b->arrays["dx"] = std::vector<double>(n, 0.0);
+        if (std::string(kern) == "k_looped") {
+          b->integers["n"] = 12;
+        } else {
+          b->arrays["y"] = y;
+          b->arrays["dy"] = std::vector<double>(n, 0.0);
+        }
+      }
+      LaunchOptions seq;
+      seq.sequential = true;
+      LaunchConfig cfg{n / 256 + 1, 256, n};
+      LaunchStats rs = adc::launch(jp, kern, cfg, ref, seq);
+      LaunchStats gs = b200_bridge::launch(jp, kern, cfg, gpu);
+      double worst = 0;
+      for (const auto& kv : ref.arrays)
+        for (int64_t i = 0; i < n; ++i)
+          worst = std::max(worst, rel(kv.second[i], gpu.arrays[kv.first][i]));
+      std::printf("     JIT %s: worst rel %.3g\n", kern, worst);
+      EXPECT(worst <= 1e-12, "bridged JIT launch matches adc::launch");
+      EXPECT(rs.thread_statements == gs.thread_statements, "JIT LaunchStats.thread_statements");
+    }
+  }
   // FitEngine (gsum K=1, 2) chi2 and gradient on the GPU vs the reference engine.
   b200_bridge::set_model_source(kGsumDsl);
   FitEngine eng;
@@ -186,7 +229,7 @@ int main(int argc, char** argv) {
   const std::string mode = argc > 1 ? argv[1] : "cpu";
   Program p = kernels_program();
   try {
-    cpu_checks(p);
+    cpu_checks(p, mode == "gpu");
     if (mode == "gpu") gpu_checks(p);
   } catch (const Error& e) {
     std::printf("FAIL unexpected adc::Error: %s\n", e.what());

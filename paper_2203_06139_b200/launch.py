@@ -104,11 +104,18 @@ def _stream_of(a):
 
 
 def launch(kernel: str, cfg: LaunchConfig, buffers: BufferSet,
-           opts: LaunchOptions | None = None, callee_fingerprint: int | None = None) -> LaunchStats:
+           opts: LaunchOptions | None = None, callee_fingerprint: int | None = None,
+           module: str | None = None) -> LaunchStats:
     """adc::launch (launch.cpp:252-346) for the Listing-1 kernels of kernels.dsl:
     `compute` (private slots) and `compute_shared` (the shared dsigma slot:
-    refused unless opts.unsafe, then reduced in a fixed order, deterministic)."""
+    refused unless opts.unsafe, then reduced in a fixed order, deterministic),
+    on their hand-written kernels.  With `module` (the Program's text as
+    adc::print emits it), any other global kernel goes through the generic
+    JIT (jit.py)."""
     opts = opts or LaunchOptions()
+    if module is not None and kernel not in ("compute", "compute_shared"):
+        from .jit import launch_module
+        return launch_module(module, kernel, cfg, buffers, opts)
     cfg.validate()
     shared = kernel == "compute_shared"
     if shared:
