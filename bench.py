@@ -341,6 +341,20 @@ def bench_points(a, world, rank, local, dist):
     return value, elapsed_ms / a.steps, roof, e2e, clocks.summary(), desc, dim, npts
 
 
+def chi2_roofline(bins, ms):
+    """FP64-pipe roofline of the chi2 gradient pass: W = 62 FP64 instructions per
+    bin over the device pass time; peak =
+    SMs x 64 FP64 lanes x max SM clock (MEASURED_PEAKS.json sm_max_mhz)."""
+    import torch
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    mhz = peaks().get("sm_max_mhz", 1965.0)
+    peak = sms * 64 * mhz * 1e6 / 1e12
+    achieved = 62.0 * bins / (ms * 1e-3) / 1e12
+    return {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "T FP64 instr/s",
+            "frac": achieved / peak, "work_per_bin": "62 FP64 instr (SURVEY.md §8(d))",
+            "peak_source": f"{sms} SMs x 64 lanes x {mhz:.0f} MHz"}
+
+
 def bench_chi2(world, rank, local, dist, bins=100_000_000, passes=20, warm=3):
     """chi2 fit gradient over `bins` bins (BASELINE configs[4]); per rank a
     shard of whole chunks, one all_gather of the chunk records per pass."""
@@ -391,6 +405,14 @@ def bench_chi2(world, rank, local, dist, bins=100_000_000, passes=20, warm=3):
         e0, e1 = event_time(lambda: plan.partials(q, True, loc), stream)
         torch.cuda.synchronize()
         kt.append(e0.elapsed_time(e1))
+    # the paper's Fig. 2 comparison: the Numeric provider's pass on the same plan
+    plan.set_provider(adc.GradientProvider.Numeric)
+    nt = []
+    for _ in range(5):
+        e0, e1 = event_time(lambda: plan.partials(q, True, loc), stream)
+        torch.cuda.synchronize()
+        nt.append(e0.elapsed_time(e1))
+    plan.set_provider(adc.GradientProvider.AdReverse)
     out = {"workload": f"chi2 gradient, gpoly (Gaussian + quadratic bkg), {bins:.0e} bins over "
                        f"{world} GPU(s) (BASELINE configs[4])",
            "passes_per_s": 1.0 / dt, "ms_per_pass": dt * 1e3,
@@ -399,7 +421,10 @@ def bench_chi2(world, rank, local, dist, bins=100_000_000, passes=20, warm=3):
            "collective": ("all-gather of chunk records inside libadc_b200 ("
                           + ("ncclAllGather in the pass graph" if BACKEND == "nccl"
                              else "host transport over gloo") + ")") if world > 1 else "none",
-           "chi2": c2}
+           "chi2": c2,
+           "roofline": chi2_roofline(L.bin_end - L.bin_begin, statistics.median(kt)),
+           "numeric_provider_device_ms_per_rank_pass": statistics.median(nt[1:]),
+           "ad_over_numeric_speedup": statistics.median(nt[1:]) / statistics.median(kt)}
     plan.close()
     if comm is not None:
         comm.close()
@@ -465,6 +490,43 @@ def bench_points_small(local, workload, steps=20, warm=3):
             "note": "device-resident, CUDA events per launch"}
 
 
+def bench_jit(local, npts=100_000_000, steps=10, warm=3):
+    """Generic lowering (JIT) throughput: the reference corpus gradients
+    rational_grad and looped_grad (printed module committed in
+    tests/golden/jit_cases.npz) over 1e8 points, one thread per point through
+    NVRTC-compiled kernels; 48 B per point (x, y read; dx, dy read+written)."""
+    import numpy as np
+    import torch
+    import paper_2203_06139_b200 as adc
+    module = str(np.load(os.path.join(ROOT, "tests", "golden", "jit_cases.npz"))["module"])
+    dev = torch.device("cuda", local)
+    g = torch.Generator(device=dev)
+    g.manual_seed(5)
+    x = torch.rand(npts, dtype=torch.float64, device=dev, generator=g) * 4 - 2
+    y = torch.rand(npts, dtype=torch.float64, device=dev, generator=g) * 4 - 2
+    dx, dy = torch.zeros_like(x), torch.zeros_like(x)
+    cfg = adc.LaunchConfig(npts // 256 + 1, 256, npts)
+    out = []
+    stream = torch.cuda.current_stream(dev)
+    for kern, bufs, bytes_pt in (
+            ("k_rational", adc.BufferSet(arrays={"x": x, "y": y, "dx": dx, "dy": dy}), 48),
+            ("k_looped", adc.BufferSet(arrays={"x": x, "dx": dx}, integers={"n": 10}), 24)):
+        mod = adc.JitModule(module, kern)
+        step = lambda: mod.launch(cfg, bufs)  # noqa: E731
+        for _ in range(warm):
+            step()
+        torch.cuda.synchronize()
+        evs = [event_time(step, stream) for _ in range(steps)]
+        torch.cuda.synchronize()
+        ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in evs)
+        nparam = 2 if kern == "k_rational" else 1
+        out.append({"kernel": kern, "points": npts, "ms_per_launch": ms,
+                    "value": npts * nparam / (ms * 1e-3), "unit": "pt*param/s",
+                    "hbm_gbs": bytes_pt * npts / (ms * 1e-3) / 1e9})
+    return {"workload": "generic JIT (DSL -> CUDA -> NVRTC sm_100a): corpus gradients over 1e8 "
+                        "points, launch incl. the per-launch error-word check", "kernels": out}
+
+
 def ours_arm(a, world, rank, local):
     import torch
     local = device_index(local)
@@ -478,7 +540,8 @@ def ours_arm(a, world, rank, local):
         if world == 1:
             jobs += [lambda: bench_fit_1e6(local),
                      lambda: bench_points_small(local, "gauss1d"),
-                     lambda: bench_points_small(local, "gaussnd1000")]
+                     lambda: bench_points_small(local, "gaussnd1000"),
+                     lambda: bench_jit(local)]
         for job in jobs:
             try:
                 secondary.append(job())

@@ -32,6 +32,7 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 
+#include <algorithm>
 #include <cctype>
 #include <cmath>
 #include <cstdio>
@@ -640,6 +641,7 @@ struct Emitter {
   const Module& m;
   bool unsafe;
   int tape_cap;
+  bool prefetch = true;
   std::ostringstream o;
   int tmp = 0;
 
@@ -725,6 +727,17 @@ struct Emitter {
           o << ind(d) << "long long " << s.target << " = " << ie_any(*s.expr) << ";\n";
         else
           o << ind(d) << "double " << s.target << " = " << re(*s.expr) << ";\n";
+        if (f.global && prefetch && is_thread_index_decl(s)) {
+          // Every array the kernel touches at the thread index: start its DRAM
+          // read now (L2 prefetch), so a thread's loads of x[i], ... and of
+          // the slots' read-modify-writes are in flight together.
+          std::set<std::string> seen;
+          prefetch_scan(f.body, s.target, seen);
+          for (const auto& a : seen)
+            o << ind(d) << "if (" << s.target << " >= 0 && " << s.target << " < " << a
+              << ".len) asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(" << a << ".p + "
+              << s.target << "));\n";
+        }
         sc.add(s.target, s.type);
         break;
       case St::Assign:
@@ -809,6 +822,22 @@ struct Emitter {
         o << ", ctx);\n";
         break;
       }
+    }
+  }
+
+  // arrays of the kernel indexed exactly by the thread-index variable
+  void prefetch_scan_expr(const Ex& e, const std::string& tv, std::set<std::string>& out) {
+    if (e.k == Ex::Index && e.a[0]->k == Ex::Var && e.a[0]->name == tv) out.insert(e.name);
+    for (auto& c : e.a) prefetch_scan_expr(*c, tv, out);
+  }
+  void prefetch_scan(const Blk& b, const std::string& tv, std::set<std::string>& out) {
+    for (auto& sp : b) {
+      const St& s = *sp;
+      if (s.expr) prefetch_scan_expr(*s.expr, tv, out);
+      if (s.indexed && s.index->k == Ex::Var && s.index->name == tv) out.insert(s.target);
+      for (auto& a : s.args) prefetch_scan_expr(*a, tv, out);
+      prefetch_scan(s.then_b, tv, out);
+      prefetch_scan(s.else_b, tv, out);
     }
   }
 
@@ -925,7 +954,14 @@ std::string hazard_message(const std::map<std::string, std::string>& haz) {
 }  // namespace
 
 // ---- the module object ------------------------------------------------------------
+struct ErrWordT {
+  unsigned long long code;
+  long long thread, aux;
+};
+
 struct adc_jit_module {
+  std::map<int, ErrWordT*> derr;  // per device, reset before every launch
+  ErrWordT* herr = nullptr;       // pinned
   std::string kernel;
   std::vector<int32_t> kinds;  // 0 real[], 1 real, 2 integer
   std::vector<std::string> names;
@@ -976,7 +1012,8 @@ extern "C" int adc_jit_compile(const char* source, const char* kernel, int32_t u
   std::string tvar;
   kernel_hazards(m, k->body, "", arrays, haz, tvar);
   if (!haz.empty() && !unsafe) return fail(ADC_E_LAUNCH, hazard_message(haz));
-  Emitter em{m, unsafe != 0, tape_capacity, {}, 0};
+  Emitter em{m, unsafe != 0, tape_capacity};
+  if (const char* e = getenv("ADC_JIT_PREFETCH")) em.prefetch = atoi(e) != 0;  // experiment knob
   try {
     em.prelude();
     for (auto& f : m.fns)
@@ -1050,6 +1087,8 @@ extern "C" int adc_jit_compile(const char* source, const char* kernel, int32_t u
 extern "C" int adc_jit_destroy(adc_jit_module* J) {
   if (J == nullptr) return ADC_OK;
   for (auto& l : J->libs) cudaLibraryUnload(l.second);
+  for (auto& e : J->derr) cudaFree(e.second);
+  if (J->herr) cudaFreeHost(J->herr);
   delete J;
   return ADC_OK;
 }
@@ -1087,10 +1126,6 @@ const char* jit_error_text(unsigned long long code) {
   }
 }
 
-struct ErrWord {
-  unsigned long long code;
-  long long thread, aux;
-};
 }  // namespace
 
 extern "C" int adc_cuda_jit_launch(adc_jit_module* J, int64_t grid, int64_t block, int64_t n,
@@ -1113,8 +1148,16 @@ extern "C" int adc_cuda_jit_launch(adc_jit_module* J, int64_t grid, int64_t bloc
   int dev = 0;
   ADCB_CUDA(cudaGetDevice(&dev));
   cudaKernel_t fn = nullptr;
+  ErrWordT* derr = nullptr;
+  std::unique_lock<std::mutex> lock(J->mu);  // one launch of a module at a time (shared error word)
   {
-    std::lock_guard<std::mutex> lock(J->mu);
+    if (J->herr == nullptr) ADCB_CUDA(cudaMallocHost(&J->herr, sizeof(ErrWordT)));
+    if (J->derr.count(dev) == 0) {
+      ErrWordT* d = nullptr;
+      ADCB_CUDA(cudaMalloc(&d, sizeof(ErrWordT)));
+      J->derr[dev] = d;
+    }
+    derr = J->derr[dev];
     auto it = J->fns.find(dev);
     if (it == J->fns.end()) {
       cudaLibrary_t lib = nullptr;
@@ -1132,10 +1175,7 @@ extern "C" int adc_cuda_jit_launch(adc_jit_module* J, int64_t grid, int64_t bloc
     }
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  ErrWord* derr = nullptr;
-  ErrWord herr{};
-  ADCB_CUDA(cudaMallocAsync(&derr, sizeof(ErrWord), s));
-  ADCB_CUDA(cudaMemsetAsync(derr, 0, sizeof(ErrWord), s));
+  ADCB_CUDA(cudaMemsetAsync(derr, 0, sizeof(ErrWordT), s));
   // kernel arguments: real[] -> (double*, long long len), real -> double, integer -> long long
   std::vector<double*> ptrs(nargs);
   std::vector<long long> lens(nargs), ints(nargs);
@@ -1166,13 +1206,10 @@ extern "C" int adc_cuda_jit_launch(adc_jit_module* J, int64_t grid, int64_t bloc
   kp.push_back(&derr);
   cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void*>(fn), dim3((unsigned)grid),
                                    dim3((unsigned)block), kp.data(), 0, s);
-  if (e != cudaSuccess) {
-    cudaFreeAsync(derr, s);
-    return cuda_fail(e, "cudaLaunchKernel (jit)");
-  }
-  ADCB_CUDA(cudaMemcpyAsync(&herr, derr, sizeof(ErrWord), cudaMemcpyDeviceToHost, s));
-  ADCB_CUDA(cudaFreeAsync(derr, s));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel (jit)");
+  ADCB_CUDA(cudaMemcpyAsync(J->herr, derr, sizeof(ErrWordT), cudaMemcpyDeviceToHost, s));
   ADCB_CUDA(cudaStreamSynchronize(s));
+  const ErrWordT herr = *J->herr;
   if (herr.code != 0) {
     std::string msg = jit_error_text(herr.code);
     if (herr.code == 4) msg = "index " + std::to_string(herr.aux) + " out of range";
