@@ -364,19 +364,11 @@ def bench_chi2(world, rank, local, dist, bins=100_000_000, passes=20, warm=3):
     from paper_2203_06139_b200 import synth
 
     dev = torch.device("cuda", local)
-    g = torch.Generator(device=dev)
-    g.manual_seed(77)
-    # counts ~ Poisson(E m_j / S) with the gpoly truth, generated on the device
-    width = 10.0 / bins
-    xs = -5.0 + (torch.arange(bins, dtype=torch.float64, device=dev) + 0.5) * width
-    q0 = synth.GPOLY_TRUTH
-    m = q0[0] * torch.exp(-0.5 * ((xs - q0[1]) / q0[2]) ** 2) + q0[3] + q0[4] * xs + q0[5] * xs * xs
-    lam = m * (bins * 100.0 / float(m.sum()))
-    counts = torch.poisson(lam, generator=g)
-    counts[::100] = 0
-    del xs, m, lam
-    events = float(counts.sum())
-    h = adc.Histogram(bins, -5.0, 5.0, events, counts)
+    # counts ~ Poisson(E m_j / S) at the gpoly truth, sampled on the device
+    # (K6, counter-based: the same histogram on every rank), every 100th bin 0
+    h = adc.sample_histogram("gpoly", synth.GPOLY_TRUTH, bins, -5.0, 5.0, bins * 100.0, seed=77,
+                             zero_every=100, device=dev)
+    counts, events = h.counts, h.events
     q = list(synth.GPOLY_INIT)
     # N > 1: the library's own communicator (NCCL over NVLink; the host
     # transport over the process group for --dist-backend gloo).  The pass,

@@ -288,6 +288,18 @@ int adc_cuda_chi2_plan_create_sharded(adc_chi2_plan** plan, int32_t model, int32
                                       int64_t bins, double lo, double hi, double events,
                                       const double* shard_counts, adc_comm* comm, void* stream);
 
+/* On-device histogram sampling (the reference's
+ * sample_histogram, fit.cpp:70-104, draws events by rejection and cannot feed
+ * 1e8 bins): counts_dev[j] ~ Poisson(events * m_j / sum_k m_k) with m the
+ * model at q (faithful per-bin arithmetic), every zero_every-th bin forced to
+ * 0 (0 = none).  Counter-based Philox4x32-10 keyed by seed: the histogram is a
+ * pure function of the arguments on any device.  *total = sum of the counts
+ * (the Histogram's `events`, as the reference sampler guarantees).
+ * Synchronous on `stream`. */
+int adc_cuda_histogram_sample(int32_t model, int32_t np, const double* q, int64_t bins, double lo,
+                              double hi, double events, uint64_t seed, int64_t zero_every,
+                              double* counts_dev, double* total, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Fit loop (FitEngine::fit, proj/src/fit.cpp:315-425: steepest descent or the
  * optional damped Newton step from a central-difference Hessian of the

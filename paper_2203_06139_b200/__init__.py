@@ -11,10 +11,11 @@ from .launch import (BufferSet, LaunchConfig, LaunchOptions, LaunchStats, launch
 from .comm import Comm  # noqa: F401
 from .jit import JitModule, launch_module  # noqa: F401
 from .fit import (Chi2Plan, FitEngine, FitOptions, FitResult, GradientProvider,  # noqa: F401
-                  Histogram, chi2_layout, finalize, record_len)
+                  Histogram, chi2_layout, finalize, record_len,
+                  sample_histogram)
 
 __all__ = [
     "AdcError", "BufferSet", "Comm", "JitModule", "launch_module", "LaunchConfig", "LaunchOptions", "LaunchStats", "launch",
     "launch_batch", "registry_find", "Chi2Plan", "FitEngine", "FitOptions", "FitResult",
-    "GradientProvider", "Histogram", "chi2_layout", "finalize", "record_len",
+    "GradientProvider", "Histogram", "chi2_layout", "sample_histogram", "finalize", "record_len",
 ]

@@ -119,6 +119,8 @@ SIGNATURES = {
                                            _VP]),
     "adc_cuda_jit_launch_host": (ctypes.c_int, [_VP, _I64, _I64, _I64, ctypes.POINTER(JitArg),
                                                 _I32]),
+    "adc_cuda_histogram_sample": (ctypes.c_int, [_I32, _I32, _D, _I64, _DBL, _DBL, _DBL,
+                                                 ctypes.c_uint64, _I64, _VP, _D, _VP]),
     "adc_fit_default_options": (None, [ctypes.POINTER(FitOptions)]),
     "adc_cuda_fit": (ctypes.c_int, [_VP, _D, ctypes.POINTER(_I32), _I32,
                                     ctypes.POINTER(FitOptions), ctypes.POINTER(FitResultC), _D]),

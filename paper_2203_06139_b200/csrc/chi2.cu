@@ -736,4 +736,194 @@ int chi2_set_tune(int v) {
   return ADC_OK;
 }
 
+// ---- K6: on-device histogram sampling ---------------------
+// The reference's sample_histogram (fit.cpp:70-104) draws events by rejection
+// and cannot feed 1e8 bins.  Here each bin's count is drawn directly:
+// c_j ~ Poisson(E m_j / S), S = sum_j m_j, with m the model at the truth
+// parameters (the faithful per-bin arithmetic of the passes).  Randomness is
+// counter-based (Philox4x32-10 keyed by the seed, counter = (bin, draw)), so
+// the histogram is a pure function of (model, q, bins, range, E, seed): the
+// same bits on any device, grid or world size.  Large means use Hörmann's
+// transformed rejection (PTRS, 1993), small ones the multiplication method.
+// S and the event total are reduced in a fixed order (no atomics).
+namespace {
+struct Philox {
+  uint32_t k0, k1;
+  __device__ __forceinline__ uint4 operator()(uint32_t c0, uint32_t c1, uint32_t c2,
+                                              uint32_t c3) const {
+    uint32_t a = k0, b = k1;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+      const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+      const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+      const uint32_t n0 = hi1 ^ c1 ^ a, n2 = hi0 ^ c3 ^ b;
+      c0 = n0;
+      c1 = lo1;
+      c2 = n2;
+      c3 = lo0;
+      a += 0x9E3779B9u;
+      b += 0xBB67AE85u;
+    }
+    return make_uint4(c0, c1, c2, c3);
+  }
+};
+
+// Two uniforms in (0, 1) from one Philox block (53-bit mantissas).
+__device__ __forceinline__ double2 uniforms(const Philox& ph, uint64_t bin, uint32_t draw) {
+  const uint4 r = ph((uint32_t)bin, (uint32_t)(bin >> 32), draw, 0x5EEDu);
+  const uint64_t u0 = ((uint64_t)r.x << 21) ^ (r.y >> 11);
+  const uint64_t u1 = ((uint64_t)r.z << 21) ^ (r.w >> 11);
+  return make_double2(((double)(u0 & ((1ull << 53) - 1)) + 0.5) * 0x1.0p-53,
+                      ((double)(u1 & ((1ull << 53) - 1)) + 0.5) * 0x1.0p-53);
+}
+
+__device__ double poisson(double lam, const Philox& ph, uint64_t bin) {
+  uint32_t draw = 0;
+  if (!(lam > 0.0)) return 0.0;
+  if (lam < 10.0) {  // multiplication method
+    const double L = exp(-lam);
+    double p = 1.0, k = -1.0;
+    for (;;) {
+      const double2 u = uniforms(ph, bin, draw++);
+      k += 1.0;
+      p *= u.x;
+      if (p <= L) return k;
+      k += 1.0;
+      p *= u.y;
+      if (p <= L) return k;
+    }
+  }
+  // PTRS (Hörmann 1993)
+  const double slam = sqrt(lam), loglam = log(lam);
+  const double b = 0.931 + 2.53 * slam, a = -0.059 + 0.02483 * b;
+  const double inv_alpha = 1.1239 + 1.1328 / (b - 3.4), vr = 0.9277 - 3.6224 / (b - 2.0);
+  for (;;) {
+    const double2 u2 = uniforms(ph, bin, draw++);
+    const double U = u2.x - 0.5, V = u2.y;
+    const double us = 0.5 - fabs(U);
+    const double k = floor((2.0 * a / us + b) * U + lam + 0.43);
+    if (us >= 0.07 && V <= vr) return k;
+    if (k < 0.0 || (us < 0.013 && V > us)) continue;
+    if (log(V) + log(inv_alpha) - log(a / (us * us) + b) <= -lam + k * loglam - lgamma(k + 1.0))
+      return k;
+  }
+}
+
+constexpr int kGenThreads = 256;
+constexpr int64_t kGenTile = 16 * kGenThreads;  // bins per block, fixed
+
+template <class M>
+__global__ void __launch_bounds__(kGenThreads) sample_sum_kernel(Chi2Pass P, int64_t bins,
+                                                                 double* partials) {
+  __shared__ QDev Q;
+  __shared__ double red[kGenThreads / 32];
+  if (threadIdx.x < kMaxNp) {
+    Q.q[threadIdx.x] = P.qdev[threadIdx.x];
+    Q.inv[threadIdx.x] = P.qdev[kMaxNp + threadIdx.x];
+  }
+  __syncthreads();
+  const typename M::Reg QR = M::load(Q);
+  double acc = 0.0;
+  for (int64_t j = blockIdx.x * kGenTile + threadIdx.x;
+       j < min(bins, (int64_t)(blockIdx.x + 1) * kGenTile); j += kGenThreads) {
+    const double x = fadd(P.lo, fmul(fadd((double)j, 0.5), P.width));
+    double m, bg[1];
+    M::template eval<false, false>(x, QR, nullptr, m, bg);
+    acc += m;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    partials[blockIdx.x] =
+        ((red[0] + red[1]) + (red[2] + red[3])) + ((red[4] + red[5]) + (red[6] + red[7]));
+}
+
+// One CTA: fixed-order total of nblocks partials into *out.
+__global__ void __launch_bounds__(kGenThreads) sample_total_kernel(const double* partials,
+                                                                   int64_t nblocks, double* out) {
+  __shared__ double red[kGenThreads / 32];
+  double acc = 0.0;
+  for (int64_t b = threadIdx.x; b < nblocks; b += kGenThreads) acc += partials[b];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    *out = ((red[0] + red[1]) + (red[2] + red[3])) + ((red[4] + red[5]) + (red[6] + red[7]));
+}
+
+template <class M>
+__global__ void __launch_bounds__(kGenThreads) sample_counts_kernel(
+    Chi2Pass P, int64_t bins, double events, const double* S, uint64_t seed, int64_t zero_every,
+    double* counts, double* partials) {
+  __shared__ QDev Q;
+  __shared__ double red[kGenThreads / 32];
+  if (threadIdx.x < kMaxNp) {
+    Q.q[threadIdx.x] = P.qdev[threadIdx.x];
+    Q.inv[threadIdx.x] = P.qdev[kMaxNp + threadIdx.x];
+  }
+  __syncthreads();
+  const typename M::Reg QR = M::load(Q);
+  const Philox ph{(uint32_t)seed, (uint32_t)(seed >> 32)};
+  const double scale = events / *S;
+  double acc = 0.0;
+  for (int64_t j = blockIdx.x * kGenTile + threadIdx.x;
+       j < min(bins, (int64_t)(blockIdx.x + 1) * kGenTile); j += kGenThreads) {
+    const double x = fadd(P.lo, fmul(fadd((double)j, 0.5), P.width));
+    double m, bg[1];
+    M::template eval<false, false>(x, QR, nullptr, m, bg);
+    double c = poisson(scale * m, ph, (uint64_t)j);
+    if (zero_every > 0 && j % zero_every == 0) c = 0.0;
+    counts[j] = c;
+    acc += c;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    partials[blockIdx.x] =
+        ((red[0] + red[1]) + (red[2] + red[3])) + ((red[4] + red[5]) + (red[6] + red[7]));
+}
+}  // namespace
+
+int histogram_sample_enqueue(int model, int np, const double* qdev, int64_t bins, double lo,
+                             double width, double events, uint64_t seed, int64_t zero_every,
+                             double* counts, double* ws, cudaStream_t s) {
+  Chi2Pass P{};
+  P.qdev = qdev;
+  P.lo = lo;
+  P.width = width;
+  const int64_t nblocks = (bins + kGenTile - 1) / kGenTile;
+  double* partials = ws;            // [nblocks]
+  double* S = ws + nblocks;         // [1]
+  double* total = ws + nblocks + 1; // [1]
+  auto go = [&](auto tag) {
+    using M = decltype(tag);
+    sample_sum_kernel<M><<<(unsigned)nblocks, kGenThreads, 0, s>>>(P, bins, partials);
+    sample_total_kernel<<<1, kGenThreads, 0, s>>>(partials, nblocks, S);
+    sample_counts_kernel<M><<<(unsigned)nblocks, kGenThreads, 0, s>>>(
+        P, bins, events, S, seed, zero_every, counts, partials);
+    sample_total_kernel<<<1, kGenThreads, 0, s>>>(partials, nblocks, total);
+  };
+  if (model == ADC_MODEL_GPOLY) {
+    go(GPoly{});
+  } else {
+    switch (np / 3) {
+      case 1: go(GSum<1>{}); break;
+      case 2: go(GSum<2>{}); break;
+      case 3: go(GSum<3>{}); break;
+      case 4: go(GSum<4>{}); break;
+      case 8: go(GSum<8>{}); break;
+      default: return fail(ADC_E_ARG, "gsum: unsupported component count");
+    }
+  }
+  ADCB_CUDA(cudaGetLastError());
+  return ADC_OK;
+}
+
+int64_t histogram_sample_ws_doubles(int64_t bins) { return (bins + kGenTile - 1) / kGenTile + 2; }
+
 }  // namespace adcb

@@ -636,6 +636,43 @@ extern "C" int adc_cuda_chi2_gradient_multi(adc_chi2_plan* P, const double* qs, 
 }
 
 // ---------------------------------------------------------------------------
+// On-device histogram sampling (K6, chi2.cu).
+extern "C" int adc_cuda_histogram_sample(int32_t model, int32_t np, const double* q, int64_t bins,
+                                         double lo, double hi, double events, uint64_t seed,
+                                         int64_t zero_every, double* counts, double* total,
+                                         void* stream) {
+  clear_error();
+  if (q == nullptr || counts == nullptr) return fail(ADC_E_ARG, "null argument");
+  if (bins <= 0) return fail(ADC_E_ARG, "histogram must have at least one bin");
+  if (!(hi > lo)) return fail(ADC_E_EVAL, "degenerate histogram range");
+  if (!(events > 0)) return fail(ADC_E_ARG, "events must be positive");
+  if (model == ADC_MODEL_GPOLY ? np != 6 : (model != ADC_MODEL_GSUM || np % 3 != 0))
+    return fail(ADC_E_ARG, "model / parameter count mismatch");
+  if (!device_present()) return fail(ADC_E_CUDA, "no CUDA device: the B200 engine has no CPU fallback");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<double> hq(qdev_bytes() / sizeof(double));
+  fill_qdev(model, np, q, hq.data());
+  double* qd = nullptr;
+  double* ws = nullptr;
+  const int64_t wsn = histogram_sample_ws_doubles(bins);
+  ADCB_CUDA(cudaMallocAsync(&qd, qdev_bytes(), s));
+  ADCB_CUDA(cudaMallocAsync(&ws, (size_t)wsn * sizeof(double), s));
+  ADCB_CUDA(cudaMemcpyAsync(qd, hq.data(), qdev_bytes(), cudaMemcpyHostToDevice, s));
+  int rc = histogram_sample_enqueue(model, np, qd, bins, lo, (hi - lo) / (double)bins, events,
+                                    seed, zero_every, counts, ws, s);
+  double tot = 0.0;
+  if (rc == ADC_OK) {
+    cudaError_t e = cudaMemcpyAsync(&tot, ws + wsn - 1, sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = cuda_fail(e, "histogram sample");
+  }
+  cudaFreeAsync(qd, s);
+  cudaFreeAsync(ws, s);
+  if (rc == ADC_OK && total != nullptr) *total = tot;
+  return rc;
+}
+
+// ---------------------------------------------------------------------------
 // Fit loop: FitEngine::fit (fit.cpp:315-425), steepest descent with Armijo
 // backtracking, generalised sigma clamp (fit.cpp:268-278 hard-codes every
 // third index, which is only right for gsum), and the optional numeric-Hessian

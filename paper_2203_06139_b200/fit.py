@@ -67,6 +67,22 @@ class FitResult:
     iterates: List[List[float]] = field(default_factory=list)
 
 
+def sample_histogram(model: str, q, bins: int, lo: float, hi: float, events: float,
+                     seed: int = 42, zero_every: int = 0, device=None) -> Histogram:
+    """On-device histogram: counts[j] ~ Poisson(events m_j / sum m) at the
+    parameters q (counter-based Philox, a pure function of the arguments);
+    Histogram.events = sum of the counts (fit.cpp:88, 94-102)."""
+    import torch
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    counts = torch.empty(bins, dtype=torch.float64, device=device or "cuda")
+    total = ctypes.c_double()
+    check(lib.adc_cuda_histogram_sample(
+        MODEL_IDS[model], q.size, q.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), bins,
+        float(lo), float(hi), float(events), seed & 0xFFFFFFFFFFFFFFFF, zero_every, dptr(counts),
+        ctypes.byref(total), ctypes.c_void_p(torch.cuda.current_stream(counts.device).cuda_stream)))
+    return Histogram(bins, lo, hi, total.value, counts)
+
+
 def chi2_layout(bins: int, world: int = 1, rank: int = 0) -> Chi2Layout:
     L = Chi2Layout()
     check(lib.adc_chi2_make_layout(bins, world, rank, ctypes.byref(L)))

@@ -430,3 +430,40 @@ def test_plan_refresh_after_counts_change(restate):
     ref, scale = restate.chi2_gradient_compensated("gpoly", c_new, -5.0, 5.0, ev, q)
     assert np.all(np.abs(g2 - ref) <= 1e-12 * scale)
     assert not np.array_equal(g1, g2)
+
+
+# ---------------------------------------------------------------------------- histogram sampling
+@pytest.mark.parametrize("events", [1e8, 3e6])
+def test_sample_histogram_statistics_and_determinism(events):
+    """K6: counts ~ Poisson(E m_j / S) (PTRS for large means, multiplication
+    below 10): standardised residuals have mean 0 and variance 1; the same
+    seed gives the same bits; Histogram.events is the exact count total."""
+    bins = 1_000_000
+    q = np.array(synth.GPOLY_TRUTH)
+    h = adc.sample_histogram("gpoly", q, bins, -5.0, 5.0, events, seed=7)
+    c = host(h.counts)
+    assert np.all(c == np.floor(c)) and np.all(c >= 0)
+    assert h.events == c.sum()
+    x = -5.0 + (np.arange(bins) + 0.5) * (10.0 / bins)
+    m = np.array([0.0] * bins)
+    z = (x - q[1]) / q[2]
+    m = q[0] * np.exp(-0.5 * z * z) + q[3] + q[4] * x + q[5] * x * x
+    lam = events * m / m.sum()
+    r = (c - lam) / np.sqrt(lam)
+    assert abs(r.mean()) < 5 / np.sqrt(bins)
+    assert abs(r.var() - 1.0) < 0.01
+    h2 = adc.sample_histogram("gpoly", q, bins, -5.0, 5.0, events, seed=7)
+    assert host(h2.counts).tobytes() == c.tobytes()
+    h3 = adc.sample_histogram("gpoly", q, bins, -5.0, 5.0, events, seed=8)
+    assert not np.array_equal(host(h3.counts), c)
+
+
+def test_sample_histogram_zero_every_and_fit():
+    h = adc.sample_histogram("gpoly", synth.GPOLY_TRUTH, 1_000_000, -5.0, 5.0, 1e8, seed=3,
+                             zero_every=100)
+    c = host(h.counts)
+    assert np.all(c[::100] == 0) and np.all(c[1::100] > 0)
+    r = adc.FitEngine("gpoly", 6).fit(h, synth.GPOLY_INIT,
+                                      adc.FitOptions(budget=200, use_hessian=True))
+    assert abs(r.params[1] - synth.GPOLY_TRUTH[1]) < 0.05
+    assert abs(r.params[2] - synth.GPOLY_TRUTH[2]) < 0.05
