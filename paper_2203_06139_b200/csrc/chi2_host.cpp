@@ -26,18 +26,22 @@ constexpr int64_t kTileThreads = 256;
 constexpr int64_t kChunkBins = int64_t(1) << 20;  // large histograms: 1 Mi-bin chunks
 
 // Bins per thread per tile.  Large histograms amortise the per-tile
-// reduction over ~128 bins per thread and size the tile so the histogram is a
-// whole number of waves of kWaveCtas resident CTAs (2 per SM x 148 SMs on a
-// B200): 1e8 bins -> 132 bins/thread, 2960 tiles = 10 full waves (at 128 the
-// last of 10.3 waves would run 31% full).  Small histograms keep 4 bins per
-// thread so there are enough tiles to fill the GPU.  A pure function of
-// `bins` (not of the device): the same layout on every GPU and world size.
+// reduction over ~80-130 bins per thread and size the tile so the histogram
+// is a whole number of waves of kWaveCtas resident CTAs (2 per SM x 148 SMs
+// on a B200).  From 6 waves up the wave count is rounded up to a multiple of
+// 8, so each rank of a 2-, 4- or 8-GPU split also gets (close to) whole
+// waves: 1e8 bins -> 84 bins/thread, 4651 tiles = 15.7 waves on one GPU,
+// 1.97 per rank on eight (128 bins/thread would be 10.3 and 1.25 -> 2 waves,
+// a 38% loss at 8 GPUs).  Small histograms keep 4 bins per thread so there
+// are enough tiles to fill the GPU.  A pure function of `bins` (not of the
+// device or world size): the same layout everywhere, hence the same bits.
 constexpr int64_t kWaveCtas = 296;
 int bpt_for(int64_t bins) {
   const int64_t per_wave = kTileThreads * kWaveCtas;
   if (bins < per_wave * 8) return 4;  // < 606K bins: keep tiles small enough to fill the GPU
   int64_t waves = (bins + per_wave * 64) / (per_wave * 128);  // round(bins / (per_wave*128))
   if (waves < 1) waves = 1;
+  if (waves >= 6) waves = (waves + 7) / 8 * 8;
   const int64_t bpt = (bins + per_wave * waves * 4 - 1) / (per_wave * waves * 4) * 4;
   return (int)std::max<int64_t>(4, bpt);
 }

@@ -17,7 +17,7 @@ counts[::100] = 0
 h = adc.Histogram(bins, -5.0, 5.0, float(counts.sum()), counts)
 pl = adc.Chi2Plan("gpoly", 6, h)
 q = list(synth.GPOLY_INIT)
-for tune in (0, 2):
+for tune in [int(t) for t in (sys.argv[2].split(',') if len(sys.argv) > 2 else ['0', '2'])]:
     os.environ["ADC_CHI2_TUNE"] = str(tune)
     pl.set_precision(True)
     for grad in (True, False):
@@ -35,3 +35,25 @@ for tune in (0, 2):
             ts.append(a.elapsed_time(b))
         print(f"tune={tune} grad={grad}: {np.median(ts):.4f} ms (min {min(ts):.4f})  "
               f"{62e-9 * bins / (np.median(ts) * 1e-3) if grad else 0:.2f} T fp64-alg/s")
+
+# per-rank device pass time of a W-way split (rank 0's shard, same layout)
+os.environ["ADC_CHI2_TUNE"] = "0"
+for world in (1, 2, 4, 8):
+    pr = adc.Chi2Plan("gpoly", 6, h, world=world, rank=0)
+    for _ in range(3):
+        pr.partials(q, True)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(10):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        pr.partials(q, True)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    L = pr.layout
+    print(f"world={world}: rank-0 shard {L.bin_end - L.bin_begin} bins, "
+          f"{np.median(ts):.4f} ms -> ideal-scaling ratio "
+          f"{np.median(ts) * world:.4f} ms-equivalent")
+    pr.close()
