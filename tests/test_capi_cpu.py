@@ -114,8 +114,12 @@ def test_chi2_layout_shards_whole_chunks():
                 assert a.chunk_end == b.chunk_begin and a.bin_end == b.bin_begin
                 assert a.bin_end == min(bins, a.chunk_end * chunk_bins)
     L = adc.chi2_layout(10**8)
-    # 132 bins per thread: 2960 tiles = 10 full waves of 296 CTAs
-    assert L.tile_bins == 132 * 256 and L.chunk_tiles == 31 and L.nchunks == 96
+    # 84 bins per thread: 4651 tiles = 15.7 waves of 296 CTAs on one GPU, and
+    # at most 12 chunks x 49 tiles = 588 tiles = 1.99 waves per rank on eight
+    assert L.tile_bins == 84 * 256 and L.chunk_tiles == 49 and L.nchunks == 95
+    per_rank = [(lambda s: (s.chunk_end - s.chunk_begin) * L.chunk_tiles)(
+        adc.chi2_layout(10**8, 8, r)) for r in range(8)]
+    assert max(per_rank) <= 2 * 296
 
 
 def test_host_communicator_without_device():
