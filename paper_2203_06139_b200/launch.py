@@ -81,16 +81,28 @@ class LaunchStats:
         return ts
 
 
+_FP = None
+_FOUND = {}
+
+
 def _fingerprints():
-    """The registry's own (name -> fingerprint) table (include/adc_cuda.h)."""
-    return {lib.adc_cuda_registry_name(i).decode(): lib.adc_cuda_registry_fingerprint(i)
-            for i in range(lib.adc_cuda_registry_size())}
+    """The registry's own (name -> fingerprint) table (include/adc_cuda.h);
+    the registry is compiled in, so it is read once."""
+    global _FP
+    if _FP is None:
+        _FP = {lib.adc_cuda_registry_name(i).decode(): lib.adc_cuda_registry_fingerprint(i)
+               for i in range(lib.adc_cuda_registry_size())}
+    return _FP
 
 
 def registry_find(name: str, fingerprint: int) -> int:
+    key = (name, fingerprint)
+    if key in _FOUND:  # hits only: a miss always goes to the library (and raises)
+        return _FOUND[key]
     import ctypes
     kid = ctypes.c_int32(-1)
     check(lib.adc_cuda_registry_find(name.encode(), fingerprint, ctypes.byref(kid)))
+    _FOUND[key] = kid.value
     return kid.value
 
 
