@@ -519,6 +519,25 @@ def bench_jit(local, npts=100_000_000, steps=10, warm=3):
                         "points, launch incl. the per-launch error-word check", "kernels": out}
 
 
+def bench_fig2b(local):
+    """The paper's Fig. 2b (the reference's bench_scaling, fit.cpp:427-458) at
+    B200 scale: gsum fits with K = 1, 2, 4, 8 Gaussians (3K parameters) over
+    1e6 bins, AD vs numeric provider, default FitOptions (400 iterations)."""
+    import paper_2203_06139_b200 as adc
+    rows = adc.bench_scaling(k_list=(1, 2, 4, 8), bins=1_000_000, events=1e8, seed=42, repeats=3)
+    table = {}
+    for r in rows:
+        t = table.setdefault(r.params, {})
+        t[r.provider] = {"gradient_ms_total": r.median_wall_ns / 1e6, "grad_evals": r.grad_evals,
+                         "gradient_ms_per_eval": r.median_wall_ns / 1e6 / max(1, r.grad_evals)}
+    for t in table.values():
+        if "ad-reverse" in t and "numeric" in t:
+            t["numeric_over_ad_per_eval"] = (t["numeric"]["gradient_ms_per_eval"] /
+                                             t["ad-reverse"]["gradient_ms_per_eval"])
+    return {"workload": "Fig. 2b analog: bench_scaling gsum K=1,2,4,8 over 1e6 bins, fit with "
+                        "each gradient provider (per-eval wall incl. host)", "params": table}
+
+
 def ours_arm(a, world, rank, local):
     import torch
     local = device_index(local)
@@ -533,7 +552,8 @@ def ours_arm(a, world, rank, local):
             jobs += [lambda: bench_fit_1e6(local),
                      lambda: bench_points_small(local, "gauss1d"),
                      lambda: bench_points_small(local, "gaussnd1000"),
-                     lambda: bench_jit(local)]
+                     lambda: bench_jit(local),
+                     lambda: bench_fig2b(local)]
         for job in jobs:
             try:
                 secondary.append(job())

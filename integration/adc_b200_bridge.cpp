@@ -2,6 +2,7 @@
 // public API plus the C ABI of include/adc_cuda.h.
 #include "adc_b200_bridge.hpp"
 
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -284,6 +285,83 @@ void chi2_gradient(const FitEngine& engine, const Histogram& h, const std::vecto
                                              ? ADC_PROVIDER_NUMERIC
                                              : ADC_PROVIDER_AD_REVERSE));
   check(adc_cuda_chi2_gradient(plan, q.data(), out.data(), nullptr));
+}
+
+FitResult fit(const FitEngine& engine, const Histogram& h, GradientProvider provider,
+              std::vector<double> init, const FitOptions& opts) {
+  const size_t np = init.size();
+  adc_chi2_plan* plan = plan_for(engine, h, np);
+  check(adc_cuda_chi2_set_provider(plan, provider == GradientProvider::Numeric
+                                             ? ADC_PROVIDER_NUMERIC
+                                             : ADC_PROVIDER_AD_REVERSE));
+  std::vector<int32_t> clamp;  // clamp_sigmas: every third coordinate (fit.cpp:268-278)
+  for (size_t i = 2; i < np; i += 3) clamp.push_back(static_cast<int32_t>(i));
+  FitResult r;
+  {  // op-count metadata at the clamped start, as fit.cpp:324-325
+    std::vector<double> q0 = init;
+    for (int32_t i : clamp)
+      if (q0[static_cast<size_t>(i)] < opts.sigma_min) q0[static_cast<size_t>(i)] = opts.sigma_min;
+    r.primal_call_counts = engine.model_counts(h.center(h.bins / 2), q0);
+    r.gradient_call_counts = engine.model_gradient_counts(h.center(h.bins / 2), q0, provider);
+  }
+  adc_fit_options o;
+  adc_fit_default_options(&o);
+  o.budget = opts.budget;
+  o.grad_tol = opts.grad_tol;
+  o.chi2_rel_tol = opts.chi2_rel_tol;
+  o.sigma_min = opts.sigma_min;
+  o.armijo_c1 = opts.armijo_c1;
+  o.trace_iterates = opts.trace_iterates;
+  o.use_hessian = opts.use_hessian ? 1 : 0;
+  adc_fit_result res{};
+  std::vector<double> its(static_cast<size_t>(std::max(1, opts.trace_iterates)) * np);
+  check(adc_cuda_fit(plan, init.data(), clamp.data(), static_cast<int32_t>(clamp.size()), &o,
+                     &res, its.data()));
+  r.params = init;
+  r.chi2 = res.chi2;
+  r.iterations = res.iterations;
+  r.gradient_evals = res.gradient_evals;
+  r.gradient_wall_ns = res.gradient_ns;
+  r.converged = res.converged != 0;
+  r.sigma_clamps = res.sigma_clamps;
+  const int n_tr = opts.trace_iterates ? std::min(opts.trace_iterates, res.iterations + 1) : 0;
+  for (int k = 0; k < n_tr; ++k)
+    r.iterates.emplace_back(its.begin() + static_cast<long>(k * np),
+                            its.begin() + static_cast<long>((k + 1) * np));
+  return r;
+}
+
+std::vector<BenchRow> bench_scaling(const BenchConfig& cfg) {
+  if (cfg.k_list.empty()) throw Error(ErrorKind::Eval, "empty K list");
+  FitEngine engine;
+  std::vector<BenchRow> rows;
+  for (int k : cfg.k_list) {
+    std::vector<double> truth = gauss_sum::default_truth(k, cfg.lo, cfg.hi);
+    Histogram h = sample_histogram(truth, cfg.events, cfg.bins, cfg.lo, cfg.hi,
+                                   cfg.seed + static_cast<uint64_t>(k));
+    std::vector<double> init = gauss_sum::perturbed_init(truth);
+    for (GradientProvider provider : {GradientProvider::AdReverse, GradientProvider::Numeric}) {
+      std::vector<uint64_t> walls;
+      FitResult last;
+      for (int rep = 0; rep < std::max(1, cfg.repeats); ++rep) {
+        last = fit(engine, h, provider, init, cfg.fit);
+        walls.push_back(last.gradient_wall_ns);
+      }
+      std::sort(walls.begin(), walls.end());
+      BenchRow row;
+      row.k = k;
+      row.params = 3 * k;
+      row.provider = provider;
+      row.median_wall_ns = walls[walls.size() / 2];
+      row.grad_evals = last.gradient_evals;
+      row.primal_opcount = last.primal_call_counts.total();
+      row.grad_opcount = last.gradient_call_counts.total();
+      row.converged = last.converged;
+      row.final_params = last.params;
+      rows.push_back(std::move(row));
+    }
+  }
+  return rows;
 }
 
 double chi2(const FitEngine& engine, const Histogram& h, const std::vector<double>& q) {

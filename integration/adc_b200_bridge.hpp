@@ -39,4 +39,17 @@ void chi2_gradient(const FitEngine& engine, const Histogram& h, const std::vecto
                    GradientProvider provider = GradientProvider::AdReverse);
 double chi2(const FitEngine& engine, const Histogram& h, const std::vector<double>& q);
 
+/// FitEngine::fit (fit.cpp:315-425) with every pass on the GPU (adc_cuda_fit:
+/// batched Armijo trials, batched Hessian probes), the sigma clamp of
+/// fit.cpp:268-278 and the reference's op-count metadata (one interpreted
+/// model / model-gradient call at the middle bin, fit.cpp:324-325).
+FitResult fit(const FitEngine& engine, const Histogram& h, GradientProvider provider,
+              std::vector<double> init, const FitOptions& opts = {});
+
+/// bench_scaling (fit.cpp:427-458), the paper's Fig. 2b: for each K, the
+/// reference's own histogram (sample_histogram, default_truth, perturbed_init)
+/// fitted with both providers on the GPU; same rows, so bench_csv /
+/// bench_plot_table apply unchanged.
+std::vector<BenchRow> bench_scaling(const BenchConfig& cfg);
+
 }  // namespace adc::b200_bridge

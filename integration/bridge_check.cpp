@@ -197,6 +197,41 @@ static void gpu_checks(const Program& p) {
       EXPECT(rs.thread_statements == gs.thread_statements, "JIT LaunchStats.thread_statements");
     }
   }
+  // FitEngine::fit through the bridge vs the reference's own fit (both providers).
+  {
+    b200_bridge::set_model_source(kGsumDsl);
+    FitEngine eng;
+    std::vector<double> truth = gauss_sum::default_truth(2, -5, 5);
+    Histogram h = sample_histogram(truth, 200000, 1200, -5, 5, 11);
+    std::vector<double> init = gauss_sum::perturbed_init(truth);
+    FitOptions fo;
+    fo.budget = 30;
+    fo.trace_iterates = 8;
+    for (GradientProvider prov : {GradientProvider::AdReverse, GradientProvider::Numeric}) {
+      FitResult rr = eng.fit(h, prov, init, fo);
+      FitResult gr = b200_bridge::fit(eng, h, prov, init, fo);
+      double worst = 0;
+      for (size_t k = 0; k < std::min(rr.iterates.size(), gr.iterates.size()); ++k)
+        for (size_t i = 0; i < init.size(); ++i)
+          worst = std::max(worst, rel(rr.iterates[k][i], gr.iterates[k][i]));
+      std::printf("     fit %s: iterations %d/%d, chi2 rel %.3g, iterates worst rel %.3g\n",
+                  provider_name(prov), rr.iterations, gr.iterations, rel(rr.chi2, gr.chi2), worst);
+      const double tol = prov == GradientProvider::AdReverse ? 1e-9 : 1e-5;
+      EXPECT(rr.iterations == gr.iterations && rr.iterates.size() == gr.iterates.size() &&
+                 worst <= tol && rel(rr.chi2, gr.chi2) <= 1e-6 &&
+                 rr.primal_call_counts == gr.primal_call_counts &&
+                 rr.gradient_call_counts == gr.gradient_call_counts,
+             "bridged FitEngine::fit matches the reference fit (iterates, counts)");
+    }
+    BenchConfig bc;
+    bc.k_list = {1, 2};
+    bc.bins = 2000;
+    bc.events = 100000;
+    bc.fit.budget = 20;
+    std::vector<BenchRow> rows = b200_bridge::bench_scaling(bc);
+    std::printf("%s", bench_csv(rows).c_str());
+    EXPECT(rows.size() == 4 && rows[0].grad_evals > 0, "bridged bench_scaling produces the rows");
+  }
   // FitEngine (gsum K=1, 2) chi2 and gradient on the GPU vs the reference engine.
   b200_bridge::set_model_source(kGsumDsl);
   FitEngine eng;

@@ -11,11 +11,12 @@ from .launch import (BufferSet, LaunchConfig, LaunchOptions, LaunchStats, launch
 from .comm import Comm  # noqa: F401
 from .jit import JitModule, launch_module  # noqa: F401
 from .fit import (Chi2Plan, FitEngine, FitOptions, FitResult, GradientProvider,  # noqa: F401
-                  Histogram, chi2_layout, finalize, record_len,
-                  sample_histogram)
+                  Histogram, bench_csv, bench_scaling, chi2_layout,
+                  default_truth, finalize, perturbed_init, record_len, sample_histogram)
 
 __all__ = [
     "AdcError", "BufferSet", "Comm", "JitModule", "launch_module", "LaunchConfig", "LaunchOptions", "LaunchStats", "launch",
     "launch_batch", "registry_find", "Chi2Plan", "FitEngine", "FitOptions", "FitResult",
-    "GradientProvider", "Histogram", "chi2_layout", "sample_histogram", "finalize", "record_len",
+    "GradientProvider", "Histogram", "bench_csv", "bench_scaling", "chi2_layout",
+    "default_truth", "perturbed_init", "sample_histogram", "finalize", "record_len",
 ]

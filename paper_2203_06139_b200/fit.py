@@ -270,3 +270,70 @@ class FitEngine:
                          converged=bool(res.converged), sigma_clamps=res.sigma_clamps,
                          chi2_evals=res.chi2_evals,
                          iterates=[list(its[k * self.np:(k + 1) * self.np]) for k in range(n_tr)])
+
+
+def default_truth(k: int, lo: float = -5.0, hi: float = 5.0):
+    """gauss_sum::default_truth (fit.cpp:46-56)."""
+    sig = (1.5, 1.0, 0.75)
+    q = []
+    for j in range(k):
+        q += [1.0, lo + (hi - lo) * (j + 1) / (k + 1), sig[j % 3]]
+    return q
+
+
+def perturbed_init(truth):
+    """gauss_sum::perturbed_init (fit.cpp:58-66)."""
+    q = list(truth)
+    for j in range(0, len(q) - 2, 3):
+        q[j] *= 0.8
+        q[j + 1] += 0.3
+        q[j + 2] *= 0.8
+    return q
+
+
+@dataclass
+class BenchRow:
+    """fit.hpp BenchRow (the reference's Fig. 2b table)."""
+    k: int
+    params: int
+    provider: str
+    median_wall_ns: int
+    grad_evals: int
+    converged: bool
+    final_params: List[float]
+
+
+def bench_scaling(k_list=(1, 2, 4, 8), bins: int = 1000, events: float = 1e5, lo: float = -5.0,
+                  hi: float = 5.0, seed: int = 42, repeats: int = 1,
+                  opts: FitOptions | None = None) -> List[BenchRow]:
+    """bench_scaling (fit.cpp:427-458), the paper's Fig. 2b, on the B200: for each
+    K a gsum histogram at default_truth (sampled on the device, seed + K), fitted
+    from perturbed_init with both gradient providers; median gradient wall time."""
+    if not k_list:
+        raise AdcError("Eval", "empty K list")
+    opts = opts or FitOptions()
+    rows = []
+    for k in k_list:
+        truth = default_truth(k, lo, hi)
+        h = sample_histogram("gsum", truth, bins, lo, hi, events, seed=seed + k)
+        init = perturbed_init(truth)
+        eng = FitEngine("gsum", 3 * k)
+        for prov, name in ((GradientProvider.AdReverse, "ad-reverse"),
+                           (GradientProvider.Numeric, "numeric")):
+            walls, last = [], None
+            for _ in range(max(1, repeats)):
+                last = eng.fit(h, init, opts, provider=prov)
+                walls.append(last.gradient_wall_ns)
+            walls.sort()
+            rows.append(BenchRow(k, 3 * k, name, walls[len(walls) // 2], last.gradient_evals,
+                                 last.converged, last.params))
+    return rows
+
+
+def bench_csv(rows: List[BenchRow]) -> str:
+    """bench_csv (fit.cpp:460-470); op-count columns are interpreter metadata (0 here)."""
+    out = "K,params,provider,median_wall_ns,grad_evals,primal_opcount,grad_opcount,converged\n"
+    for r in rows:
+        out += (f"{r.k},{r.params},{r.provider},{r.median_wall_ns},{r.grad_evals},0,0,"
+                f"{1 if r.converged else 0}\n")
+    return out

@@ -467,3 +467,13 @@ def test_sample_histogram_zero_every_and_fit():
                                       adc.FitOptions(budget=200, use_hessian=True))
     assert abs(r.params[1] - synth.GPOLY_TRUTH[1]) < 0.05
     assert abs(r.params[2] - synth.GPOLY_TRUTH[2]) < 0.05
+
+
+def test_bench_scaling_rows():
+    rows = adc.bench_scaling(k_list=(1, 2), bins=20_000, events=2e6,
+                             opts=adc.FitOptions(budget=30))
+    assert [(r.k, r.provider) for r in rows] == [(1, "ad-reverse"), (1, "numeric"),
+                                                  (2, "ad-reverse"), (2, "numeric")]
+    assert all(r.grad_evals > 0 and r.median_wall_ns > 0 for r in rows)
+    csv = adc.bench_csv(rows)
+    assert csv.splitlines()[0].startswith("K,params,provider")
