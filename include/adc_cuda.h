@@ -221,12 +221,12 @@ double* adc_cuda_chi2_plan_records(adc_chi2_plan* plan);
  * FitEngine::chi2_gradient(h, q, AdReverse, out) and FitEngine::chi2(h, q). */
 int adc_cuda_chi2_gradient(adc_chi2_plan* plan, const double* q, double* grad, double* chi2);
 int adc_cuda_chi2(adc_chi2_plan* plan, const double* q, double* chi2);
-/* chi2 of ncand (<= 32) parameter vectors qs[ncand][np] in ONE pass over the
+/* chi2 of ncand (<= 64) parameter vectors qs[ncand][np] in ONE pass over the
  * bins (fast mode): each result is bit-identical to adc_cuda_chi2 on that
  * vector.  The fit loop uses it to evaluate the Armijo trials t = 1, 1/2, ...
  * of fit.cpp:390-403 in batches.  Sharded plans need a communicator. */
 int adc_cuda_chi2_multi(adc_chi2_plan* plan, const double* qs, int32_t ncand, double* chi2s);
-/* Gradients (and nothing else) of ncand (<= 32) parameter vectors: ncand
+/* Gradients (and nothing else) of ncand (<= 64) parameter vectors: ncand
  * ordinary gradient passes enqueued back to back, one copy back, one sync;
  * each result equals adc_cuda_chi2_gradient on that vector.  Used for the
  * 2*np central-difference probes of the Newton option.  Sharded plans need a

@@ -388,9 +388,17 @@ __global__ void __launch_bounds__(kTileThreads, MINB) chi2_tile_kernel(Chi2Pass 
 // Record layout per tile / chunk: [C0, (S, A1, A2) x ncand].
 constexpr int kMultiGroup = 8;
 
+
+
+// candidates evaluated together per bin (independent chains), as registers allow
+template <class M>
+__host__ __device__ constexpr int multi_ilp() {
+  return M::NP <= 6 ? 4 : M::NP <= 12 ? 2 : 1;
+}
+
 template <class M>
 __global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P, int ncand) {
-  constexpr int G = kMultiGroup;
+  constexpr int G = kMultiGroup, CG = multi_ilp<M>();
   __shared__ QDev Q[G];
   __shared__ double red[kTileThreads / 32][3 * G + 1];
   __shared__ double tab[64];
@@ -410,49 +418,58 @@ __global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P,
   const int64_t TB = (int64_t)BPT * kTileThreads;
   for (int64_t tile = P.tile_begin + blockIdx.x; tile < P.tile_end; tile += gridDim.x) {
     const int64_t base = tile * TB + threadIdx.x;
-    double acc[3 * G + 1];
+    // CG candidates at a time, bins inner: the CG model evaluations of a bin
+    // are independent chains the scheduler interleaves, and the bin's centre
+    // and 1/c are shared.  Per candidate the bin order, the accumulation
+    // expressions and the trees are those of the single value pass
+    // (tile_bins / bin_term / bin_accumulate), so each candidate's record is
+    // bit-identical to a separate chi2 pass.
 #pragma unroll
-    for (int v = 0; v < 3 * G + 1; ++v) acc[v] = 0.0;
-    // Candidates outer, bins inner: each candidate's parameters stay in
-    // registers for the whole tile; the counts are re-read from L1.  Per
-    // candidate the bin order and the accumulation expressions are those of
-    // the single value pass (tile_bins / bin_term / bin_accumulate).
+    for (int c0 = 0; c0 < G; c0 += CG) {
+      if (c0 < ng) {
+        typename M::Reg QR[CG];
 #pragma unroll
-    for (int cnd = 0; cnd < G; ++cnd) {
-      if (cnd < ng) {
-        const typename M::Reg QR = M::load(Q[cnd]);
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        for (int cc = 0; cc < CG; ++cc) QR[cc] = M::load(Q[c0 + cc]);
+        double a0[CG], a1[CG], a2[CG];
+#pragma unroll
+        for (int cc = 0; cc < CG; ++cc) a0[cc] = a1[cc] = a2[cc] = 0.0;
         double jh = fadd((double)base, 0.5);
         for (int k = 0; k < BPT; ++k) {
           const int64_t j = base + (int64_t)k * kTileThreads;
           if (j < P.bin_end) {
-            const double ic = P.icounts[j];
+            const double ic = ld_stream(P.icounts + j);
             const double x = fadd(P.lo, fmul(jh, P.width));
             const double w = ic > 0.0 ? 1.0 : 0.0;
-            double m, bg[1];
-            M::template eval<false, true>(x, QR, tab, m, bg);
-            const double mc = m * ic;
-            a0 += m;
-            a1 = __fma_rn(w, m, a1);
-            a2 = __fma_rn(m, mc, a2);
+#pragma unroll
+            for (int cc = 0; cc < CG; ++cc) {
+              double m, bg[1];
+              M::template eval<false, true>(x, QR[cc], tab, m, bg);
+              const double mc = m * ic;
+              a0[cc] += m;
+              a1[cc] = __fma_rn(w, m, a1[cc]);
+              a2[cc] = __fma_rn(m, mc, a2[cc]);
+            }
           }
           jh = fadd(jh, (double)kTileThreads);
         }
-        acc[3 * cnd] = a0;
-        acc[3 * cnd + 1] = a1;
-        acc[3 * cnd + 2] = a2;
-
+        // this group's fixed shuffle trees
+#pragma unroll
+        for (int cc = 0; cc < CG; ++cc) {
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            a0[cc] += __shfl_down_sync(0xffffffffu, a0[cc], off);
+            a1[cc] += __shfl_down_sync(0xffffffffu, a1[cc], off);
+            a2[cc] += __shfl_down_sync(0xffffffffu, a2[cc], off);
+          }
+          if (lane == 0) {
+            red[warp][3 * (c0 + cc)] = a0[cc];
+            red[warp][3 * (c0 + cc) + 1] = a1[cc];
+            red[warp][3 * (c0 + cc) + 2] = a2[cc];
+          }
+        }
       }
     }
-#pragma unroll
-    for (int v = 0; v < 3 * G + 1; ++v) {
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) acc[v] += __shfl_down_sync(0xffffffffu, acc[v], off);
-    }
-    if (lane == 0) {
-#pragma unroll
-      for (int v = 0; v < 3 * G + 1; ++v) red[warp][v] = acc[v];
-    }
+    if (lane == 0) red[warp][3 * G] = 0.0;  // C0: merged from the K3l pre-pass
     __syncthreads();
     for (int v = threadIdx.x; v < 3 * ng + 1; v += kTileThreads) {
       const int src = v < 3 * ng ? v : 3 * G;  // C0 is the last local entry

@@ -556,7 +556,7 @@ extern "C" int adc_cuda_chi2_multi(adc_chi2_plan* P, const double* qs, int32_t n
                                    double* chi2s) {
   clear_error();
   if (P == nullptr || qs == nullptr || chi2s == nullptr) return fail(ADC_E_ARG, "null argument");
-  if (ncand < 1 || ncand > kMultiMax) return fail(ADC_E_ARG, "chi2 multi: 1..32 candidates");
+  if (ncand < 1 || ncand > kMultiMax) return fail(ADC_E_ARG, "chi2 multi: 1..64 candidates");
   if (int rc = require_whole_or_comm(P)) return rc;
   for (int k = 0; k < ncand; ++k)
     if (int rc = check_domain(P, qs + (size_t)k * P->np)) return rc;
@@ -601,7 +601,7 @@ extern "C" int adc_cuda_chi2_gradient_multi(adc_chi2_plan* P, const double* qs, 
                                             double* grads) {
   clear_error();
   if (P == nullptr || qs == nullptr || grads == nullptr) return fail(ADC_E_ARG, "null argument");
-  if (ncand < 1 || ncand > kMultiMax) return fail(ADC_E_ARG, "gradient multi: 1..32 candidates");
+  if (ncand < 1 || ncand > kMultiMax) return fail(ADC_E_ARG, "gradient multi: 1..64 candidates");
   if (int rc = require_whole_or_comm(P)) return rc;
   for (int k = 0; k < ncand; ++k)
     if (int rc = check_domain(P, qs + (size_t)k * P->np, numeric(P))) return rc;
@@ -758,6 +758,7 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
   ++res.chi2_evals;
   if (opts->trace_iterates > 0) trace(q);
   std::vector<double> g(np), trial(np);
+  int first_batch = 32;  // line-search batch size, adapted per iteration
   for (int iter = 0; iter < opts->budget; ++iter) {
     auto t0 = clk::now();
     if (int rc = adc_cuda_chi2_gradient(P, q.data(), g.data(), nullptr)) return rc;
@@ -817,17 +818,20 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
     bool accepted = false;
     if (P->fast) {
       // Batched Armijo: the trials t = 1, 1/2, 1/4, ... of the sequential
-      // search (fit.cpp:390-403) evaluated kMultiMax at a time in one pass;
-      // the first accepted one is taken, so the iterate is the same as the
+      // search (fit.cpp:390-403) evaluated in batches, one pass each; the
+      // first accepted one is taken, so the iterate is the same as the
       // sequential search's (each candidate's chi2 is bit-identical to a
-      // single value pass).
+      // single value pass).  The first batch of an iteration is sized from
+      // the previous iteration's accepted trial (+8), so a typical search is
+      // one pass; later batches take kMultiMax.
       std::vector<double> trials, tvals, c2s(kMultiMax);
       std::vector<int> cls;
+      int want = first_batch, tried = 0;
       while (t >= 1e-18 && !accepted) {
         trials.clear();
         tvals.clear();
         cls.clear();
-        for (double tt = t; tt >= 1e-18 && (int)tvals.size() < kMultiMax; tt *= 0.5) {
+        for (double tt = t; tt >= 1e-18 && (int)tvals.size() < want; tt *= 0.5) {
           trial = q;
           for (int i = 0; i < np; ++i) trial[i] -= tt * direction[i];
           cls.push_back(clamp(trial));
@@ -839,6 +843,7 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
           return rc;
         for (size_t k = 0; k < tvals.size(); ++k) {
           ++res.chi2_evals;
+          ++tried;
           if (c2s[k] <= cur - opts->armijo_c1 * tvals[k] * gd) {
             accepted = true;
             next = c2s[k];
@@ -848,7 +853,9 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
           }
         }
         t = tvals.back() * 0.5;
+        want = kMultiMax;
       }
+      if (accepted) first_batch = std::min(kMultiMax, std::max(8, (tried + 8 + 7) / 8 * 8));
     } else {
       while (t >= 1e-18) {
         trial = q;

@@ -10,7 +10,7 @@ namespace adcb {
 
 constexpr int kMaxNp = 24;
 constexpr int kQDoubles = 8 * kMaxNp;  // QDev (q, 1/q) + QNum (numeric probes), chi2.cu
-constexpr int kMultiMax = 32;  // line-search candidates per multi pass  // gsum up to K = 8 components (the reference bench K list 1,2,4,8)
+constexpr int kMultiMax = 64;  // line-search candidates (or gradients) per multi pass
 
 struct Chi2Pass {
   const double* counts;   // full histogram, device (read by the once-per-plan passes)
