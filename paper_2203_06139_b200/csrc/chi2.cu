@@ -248,16 +248,16 @@ __device__ __forceinline__ void bin_accumulate(const BinTerm<M, GRAD, FAST>& t, 
   }
 }
 
-// PAIR evaluates two independent bins before folding either, giving the
+// ILP evaluates that many independent bins before folding any, giving the
 // scheduler two dependency chains to interleave (the model's exp chain is
 // ~15 dependent FP64 ops deep).  The accumulation order is unchanged.
-template <class M, bool GRAD, bool FAST, bool CHECK, bool PAIR, bool NUM>
+template <class M, bool GRAD, bool FAST, bool CHECK, int ILP, bool NUM>
 __device__ __forceinline__ void tile_bins(const Chi2Pass& P, const typename M::Reg& QR,
                                           const double* tab, int64_t base, double* acc,
                                           const QNum* N) {
   constexpr int PD = kPD;  // P.bpt is a multiple of kPD (adc_chi2_make_layout)
   const int BPT = P.bpt;
-  constexpr int STEP = PAIR && PD >= 2 ? 2 : 1;
+  constexpr int STEP = ILP <= PD ? ILP : PD;
   double ring[PD];
 #pragma unroll
   for (int k = 0; k < PD; ++k) {
@@ -313,7 +313,7 @@ __host__ __device__ constexpr bool pass_zero_entry(int v) {
 }
 
 template <class M, bool GRAD, bool FAST, int MINB = tile_min_blocks<M, GRAD>(),
-          bool PAIR = false, bool NUM = false>
+          int ILP = 1, bool NUM = false>
 __global__ void __launch_bounds__(kTileThreads, MINB) chi2_tile_kernel(Chi2Pass P) {
   constexpr int NP = M::NP;
   constexpr int R = GRAD ? 4 + 3 * NP : 4;
@@ -351,9 +351,9 @@ __global__ void __launch_bounds__(kTileThreads, MINB) chi2_tile_kernel(Chi2Pass 
 #pragma unroll
     for (int v = 0; v < R; ++v) acc[v] = 0.0;
     if ((tile + 1) * TB <= P.bin_end)
-      tile_bins<M, GRAD, FAST, false, PAIR, NUM>(P, QR, tab, base, acc, Np);
+      tile_bins<M, GRAD, FAST, false, ILP, NUM>(P, QR, tab, base, acc, Np);
     else
-      tile_bins<M, GRAD, FAST, true, PAIR, NUM>(P, QR, tab, base, acc, Np);
+      tile_bins<M, GRAD, FAST, true, ILP, NUM>(P, QR, tab, base, acc, Np);
     // fixed shuffle tree, then fixed cross-warp tree; entries a pass never
     // touches (C0 and the linear G0/G1: the K3l pre-pass supplies them) are
     // exact zeros and skip the tree
@@ -601,21 +601,26 @@ template <class M, bool GRAD, bool FAST>
 static void launch_tiles_t(const Chi2Pass& P, int blocks, cudaStream_t s) {
   constexpr int MB = tile_min_blocks<M, GRAD>();
   if constexpr (std::is_same<M, GPoly>::value && FAST) {
-    // experiments: 1 = unpaired; 3 = paired, 3 CTAs/SM; 4 = unpaired, 3 CTAs/SM
+    // experiments: 1 = one bin at a time; 3 = 2 bins, 3 CTAs/SM; 4 = 1 bin,
+    // 3 CTAs/SM; 5 = 4 bins
     if (g_chi2_tune == 3) {
-      chi2_tile_kernel<M, GRAD, FAST, 3, true><<<sm_count() * 3, kTileThreads, 0, s>>>(P);
+      chi2_tile_kernel<M, GRAD, FAST, 3, 2><<<sm_count() * 3, kTileThreads, 0, s>>>(P);
       return;
     }
     if (g_chi2_tune == 4) {
-      chi2_tile_kernel<M, GRAD, FAST, 3, false><<<sm_count() * 3, kTileThreads, 0, s>>>(P);
+      chi2_tile_kernel<M, GRAD, FAST, 3, 1><<<sm_count() * 3, kTileThreads, 0, s>>>(P);
       return;
     }
-    if (g_chi2_tune == 1) {  // unpaired
+    if (g_chi2_tune == 5) {
+      chi2_tile_kernel<M, GRAD, FAST, MB, 4><<<blocks, kTileThreads, 0, s>>>(P);
+      return;
+    }
+    if (g_chi2_tune == 1) {
       chi2_tile_kernel<M, GRAD, FAST><<<blocks, kTileThreads, 0, s>>>(P);
       return;
     }
     // default: two bins evaluated before either is folded (measured 1.5% faster)
-    chi2_tile_kernel<M, GRAD, FAST, MB, true><<<blocks, kTileThreads, 0, s>>>(P);
+    chi2_tile_kernel<M, GRAD, FAST, MB, 2><<<blocks, kTileThreads, 0, s>>>(P);
     return;
   }
   chi2_tile_kernel<M, GRAD, FAST><<<blocks, kTileThreads, 0, s>>>(P);
@@ -626,8 +631,8 @@ static void launch_tiles_m(const Chi2Pass& P, bool grad, bool fast, bool num, in
                            cudaStream_t s) {
   constexpr int MB = tile_min_blocks<M, true>();
   if (grad && num) {  // GradientProvider::Numeric
-    if (fast) chi2_tile_kernel<M, true, true, MB, false, true><<<blocks, kTileThreads, 0, s>>>(P);
-    else chi2_tile_kernel<M, true, false, MB, false, true><<<blocks, kTileThreads, 0, s>>>(P);
+    if (fast) chi2_tile_kernel<M, true, true, MB, 1, true><<<blocks, kTileThreads, 0, s>>>(P);
+    else chi2_tile_kernel<M, true, false, MB, 1, true><<<blocks, kTileThreads, 0, s>>>(P);
     return;
   }
   if (grad) {
