@@ -519,6 +519,37 @@ def bench_jit(local, npts=100_000_000, steps=10, warm=3):
                         "points, launch incl. the per-launch error-word check", "kernels": out}
 
 
+def bench_shared_p(local, dim=100, npts=10_000_000, steps=10, warm=3):
+    """Shared mean vector: dp[dim] = sum over 10M points of
+    gaussnd_grad_0_1's shared slot, reduced in a fixed order; dp-only (x
+    streamed by 2-D TMA tensor loads) and with private dx slots."""
+    import torch
+    import paper_2203_06139_b200 as adc
+    dev = torch.device("cuda", local)
+    g = torch.Generator(device=dev)
+    g.manual_seed(11)
+    p = torch.rand(dim, dtype=torch.float64, device=dev, generator=g) * 4 - 2
+    x = p[:, None] + 0.1 * torch.randn((dim, npts), dtype=torch.float64, device=dev, generator=g)
+    dp = torch.zeros(dim, dtype=torch.float64, device=dev)
+    opts = adc.LaunchOptions(unsafe=True)
+    stream = torch.cuda.current_stream(dev)
+    out = {}
+    for name, dx, byt in (("dp_only", None, 8), ("with_dx", torch.zeros_like(x), 24)):
+        step = lambda: adc.launch_batch_shared_p("gaussnd_grad_0_1", x, p, 1.3, dx, dp, opts)  # noqa
+        for _ in range(warm):
+            step()
+        torch.cuda.synchronize()
+        evs = [event_time(step, stream) for _ in range(steps)]
+        torch.cuda.synchronize()
+        ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in evs)
+        out[name] = {"ms": ms, "pt_param_per_s": npts * dim * (2 if dx is not None else 1) /
+                     (ms * 1e-3), "hbm_gbs": byt * npts * dim / (ms * 1e-3) / 1e9,
+                     "bytes_per_element": byt}
+        del dx
+    return {"workload": f"gaussnd shared mean vector, dim={dim}, {npts} points (dp reduced in "
+                        "a fixed order)", **out}
+
+
 def bench_fig2b(local):
     """The paper's Fig. 2b (the reference's bench_scaling, fit.cpp:427-458) at
     B200 scale: gsum fits with K = 1, 2, 4, 8 Gaussians (3K parameters) over
@@ -553,6 +584,7 @@ def ours_arm(a, world, rank, local):
                      lambda: bench_points_small(local, "gauss1d"),
                      lambda: bench_points_small(local, "gaussnd1000"),
                      lambda: bench_jit(local),
+                     lambda: bench_shared_p(local),
                      lambda: bench_fig2b(local)]
         for job in jobs:
             try:

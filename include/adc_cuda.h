@@ -115,6 +115,16 @@ int adc_cuda_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, c
 /* Host-buffer variant (pinned memory recommended); synchronous, pipelined. */
 int adc_cuda_gaussnd_grad_host(int64_t n, int64_t dim, int64_t ld, const double* x,
                                const double* p, double sigma, double* dx, double* dp);
+/* Shared mean vector: every point i runs
+ * gaussnd_grad_0_1(x[:, i], p, sigma, dim, dx[:, i], dp) with ONE p[dim] and
+ * ONE shared slot dp[dim] — a shared-write hazard the reference refuses
+ * (launch.cpp:217-224, same message) unless `unsafe`.  Forced, dx[:, i]
+ * accumulates privately (dx may be NULL) and dp[d] += sum_i -_r6_{d,i} is
+ * reduced in a fixed order (no atomics; the same bits on every run and
+ * device).  Device pointers, stream-ordered. */
+int adc_cuda_gaussnd_grad_shared_p(int64_t n, int64_t dim, int64_t ld, const double* x,
+                                   const double* p, double sigma, double* dx, double* dp,
+                                   int32_t unsafe, void* stream);
 /* Kernel selection for experiments: 0 = auto, 1 = point-per-thread
  * (reference summation order), 2 = dims-over-warps tile. */
 int adc_cuda_gaussnd_set_variant(int32_t variant);

@@ -316,6 +316,43 @@ int cmd_launch_file(int argc, char** argv) {
   return 0;
 }
 
+// gaussnd-shared-p-in <dim> <n> <sigma> <in.bin> <out.bin>
+//   The shared-mean form: every point runs Program::eval("gaussnd_grad_0_1")
+//   with the same p vector and the same dp slot (ArgPack holds raw pointers,
+//   eval.hpp:36-61), points in order on one thread.  in = x (SoA dim x n),
+//   p (dim), dx0 (SoA), dp0 (dim); out = dx (SoA), dp (dim).
+int cmd_gaussnd_shared_p_in(int argc, char** argv) {
+  if (argc < 6) die("gaussnd-shared-p-in <dim> <n> <sigma> <in> <out>");
+  const int64_t dim = std::atoll(argv[1]);
+  const int64_t n = std::atoll(argv[2]);
+  const double sigma = std::atof(argv[3]);
+  const size_t tot = static_cast<size_t>(dim * n);
+  std::vector<double> all = read_f64(argv[4], 2 * tot + 2 * static_cast<size_t>(dim));
+  const double* X = all.data();
+  std::vector<double> p(all.begin() + tot, all.begin() + tot + dim);
+  std::vector<double> DX(all.begin() + tot + dim, all.begin() + 2 * tot + dim);
+  std::vector<double> dp(all.begin() + 2 * tot + dim, all.end());
+  Module m = load_named("gaussnd");
+  add_gradient(m, "gaussnd", {"x", "p"});
+  Program prog(std::move(m));
+  std::vector<double> x(dim), dx(dim);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t d = 0; d < dim; ++d) {
+      x[d] = X[d * n + i];
+      dx[d] = DX[d * n + i];
+    }
+    ArgPack a;
+    a.add_array(x).add_array(p).add_real(sigma).add_int(dim).add_array(dx).add_array(dp);
+    prog.eval("gaussnd_grad_0_1", a);
+    for (int64_t d = 0; d < dim; ++d) DX[d * n + i] = dx[d];
+  }
+  std::ofstream out(argv[5], std::ios::binary);
+  write_f64(out, DX);
+  write_f64(out, dp);
+  std::printf("{\"dim\": %lld, \"n\": %lld}\n", (long long)dim, (long long)n);
+  return 0;
+}
+
 // gaussnd-in <dim> <n> <sigma> <in.bin> <out.bin> [workers]
 //   in = x, p, dx0, dp0 in structure-of-arrays layout ([d*n + i]); each point
 //   is gathered into contiguous rows and run through
@@ -836,6 +873,7 @@ int main(int argc, char** argv) {
     if (cmd == "gauss1d") return cmd_gauss1d(argc - 1, argv + 1);
     if (cmd == "gauss1d-in") return cmd_gauss1d_in(argc - 1, argv + 1);
     if (cmd == "gaussnd-in") return cmd_gaussnd_in(argc - 1, argv + 1);
+    if (cmd == "gaussnd-shared-p-in") return cmd_gaussnd_shared_p_in(argc - 1, argv + 1);
     if (cmd == "gauss-shared-in") return cmd_gauss_shared_in(argc - 1, argv + 1);
     if (cmd == "launch-file") return cmd_launch_file(argc - 1, argv + 1);
     if (cmd == "chi2-in") return cmd_chi2_in(argc - 1, argv + 1);

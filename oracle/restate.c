@@ -139,12 +139,24 @@ void rs_gauss_shared_dsigma_compensated(const double* x, const double* p, double
  * forward loop pushes _t0,_t1,t; reverse loop pops them.  Only _t0 is read by
  * an adjoint rule, so the tape is replaced by the per-element recomputation
  * x[i]-p[i], which yields the identical bits. */
+static void gaussnd_grad_strided2(const double* x, int64_t xs, const double* p, int64_t ps,
+                                  double sigma, int64_t dim, double* _d_x, int64_t dxs,
+                                  double* _d_p, int64_t dps);
+
 static void gaussnd_grad_strided(const double* x, const double* p, double sigma, int64_t dim,
                                  int64_t stride, double* _d_x, double* _d_p) {
+  gaussnd_grad_strided2(x, stride, p, stride, sigma, dim, _d_x, stride, _d_p, stride);
+}
+
+/* x, p, _d_x, _d_p each with its own element stride (the shared-p form reads
+ * one p vector and accumulates into one dp vector for every point). */
+static void gaussnd_grad_strided2(const double* x, int64_t xs, const double* p, int64_t ps,
+                                  double sigma, int64_t dim, double* _d_x, int64_t dxs,
+                                  double* _d_p, int64_t dps) {
   double _d_t = 0, _d__t0 = 0, _d__t1 = 0, _d__t2 = 0, _d__t9 = 0, _d__t10 = 0;
   double t = 0;
   for (int64_t i = 0; i < dim; ++i) {
-    double _t0 = x[i * stride] - p[i * stride];
+    double _t0 = x[i * xs] - p[i * ps];
     double _t1 = _t0 * _t0;
     t = t + _t1;
   }
@@ -173,7 +185,7 @@ static void gaussnd_grad_strided(const double* x, const double* p, double sigma,
   _d_t += -_r3;
   for (int64_t j = 0; j < dim; ++j) {
     int64_t i = dim - 1 - j;
-    double _t0 = x[i * stride] - p[i * stride];
+    double _t0 = x[i * xs] - p[i * ps];
     double _r4 = _d_t;
     _d_t = 0;
     _d_t += _r4;
@@ -184,9 +196,46 @@ static void gaussnd_grad_strided(const double* x, const double* p, double sigma,
     _d__t0 += _t0 * _r5;
     double _r6 = _d__t0;
     _d__t0 = 0;
-    _d_x[i * stride] += _r6;
-    _d_p[i * stride] += -_r6;
+    _d_x[i * dxs] += _r6;
+    _d_p[i * dps] += -_r6;
   }
+}
+
+void rs_gaussnd_grad_shared_p(const double* x, const double* p, double sigma, int64_t dim,
+                              int64_t n, int64_t ld, double* dx, double* dp) {
+  for (int64_t g = 0; g < n; ++g) gaussnd_grad_strided2(x + g, ld, p, 1, sigma, dim, dx + g, ld, dp, 1);
+}
+
+void rs_gaussnd_shared_p_dp_compensated(const double* x, const double* p, double sigma, int64_t dim,
+                                        int64_t n, int64_t ld, double* total, double* abs_total) {
+  /* per point, the contributions -_r6_d land in a private row; sum them per d
+   * with Neumaier compensation (and their magnitudes) */
+  double* row = (double*)malloc((size_t)dim * sizeof(double));
+  double* dxr = (double*)malloc((size_t)dim * sizeof(double));
+  double* s = (double*)calloc((size_t)dim, sizeof(double));
+  double* c = (double*)calloc((size_t)dim, sizeof(double));
+  double* a = (double*)calloc((size_t)dim, sizeof(double));
+  for (int64_t g = 0; g < n; ++g) {
+    for (int64_t d = 0; d < dim; ++d) row[d] = 0.0, dxr[d] = 0.0;
+    gaussnd_grad_strided2(x + g, ld, p, 1, sigma, dim, dxr, 1, row, 1);
+    for (int64_t d = 0; d < dim; ++d) {
+      const double v = row[d];
+      const double t = s[d] + v;
+      if (fabs(s[d]) >= fabs(v)) c[d] += (s[d] - t) + v;
+      else c[d] += (v - t) + s[d];
+      s[d] = t;
+      a[d] += fabs(v);
+    }
+  }
+  for (int64_t d = 0; d < dim; ++d) {
+    total[d] = s[d] + c[d];
+    abs_total[d] = a[d];
+  }
+  free(row);
+  free(dxr);
+  free(s);
+  free(c);
+  free(a);
 }
 
 void rs_gaussnd_grad_0_1(const double* x, const double* p, double sigma, int64_t dim, double* dx,

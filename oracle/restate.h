@@ -49,6 +49,15 @@ void rs_gauss_shared_dsigma_compensated(const double* x, const double* p, double
 void rs_gaussnd_grad_batch(const double* x, const double* p, double sigma, int64_t dim, int64_t n,
                            int64_t ld, double* dx, double* dp);
 
+/* Shared mean vector: every point g runs gaussnd_grad_0_1(x[:, g], p, ...,
+ * dx[:, g], dp) with one p[dim] and one dp[dim], points in order (dx may not
+ * be NULL here).  And the compensated per-dim total of the dp contributions
+ * with the sum of their magnitudes (the tolerance scale). */
+void rs_gaussnd_grad_shared_p(const double* x, const double* p, double sigma, int64_t dim,
+                              int64_t n, int64_t ld, double* dx, double* dp);
+void rs_gaussnd_shared_p_dp_compensated(const double* x, const double* p, double sigma, int64_t dim,
+                                        int64_t n, int64_t ld, double* total, double* abs_total);
+
 /* One point, contiguous row of length dim (the layout Program::eval sees). */
 void rs_gaussnd_grad_0_1(const double* x, const double* p, double sigma, int64_t dim, double* dx,
                          double* dp);

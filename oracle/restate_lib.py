@@ -31,6 +31,8 @@ class Restate:
         lib.rs_gauss_grad_batch.argtypes = [_D, _D, d, _D, _D, i64]
         lib.rs_gauss_grad_shared_batch.argtypes = [_D, _D, d, _D, _D, _D, i64]
         lib.rs_gauss_shared_dsigma_compensated.argtypes = [_D, _D, d, i64, _D, _D]
+        lib.rs_gaussnd_grad_shared_p.argtypes = [_D, _D, d, i64, i64, i64, _D, _D]
+        lib.rs_gaussnd_shared_p_dp_compensated.argtypes = [_D, _D, d, i64, i64, i64, _D, _D]
         lib.rs_gaussnd_grad_batch.argtypes = [_D, _D, d, i64, i64, i64, _D, _D]
         lib.rs_model.argtypes = [i, d, _D, i64]
         lib.rs_model.restype = d
@@ -60,6 +62,18 @@ class Restate:
         t, a = np.zeros(1), np.zeros(1)
         self.lib.rs_gauss_shared_dsigma_compensated(_p(x), _p(p), sigma, x.size, _p(t), _p(a))
         return float(t[0]), float(a[0])
+
+    def gaussnd_grad_shared_p(self, x, p, sigma, dx, dp):
+        """x, dx (dim, n) SoA; p, dp (dim,): points in order, dp shared."""
+        dim, n = x.shape
+        self.lib.rs_gaussnd_grad_shared_p(_p(x), _p(p), sigma, dim, n, n, _p(dx), _p(dp))
+
+    def gaussnd_shared_p_dp_compensated(self, x, p, sigma):
+        dim, n = x.shape
+        tot, ab = np.zeros(dim), np.zeros(dim)
+        self.lib.rs_gaussnd_shared_p_dp_compensated(_p(x), _p(p), sigma, dim, n, n, _p(tot),
+                                                    _p(ab))
+        return tot, ab
 
     def gaussnd_grad(self, x, p, sigma, dx, dp):
         dim, n = x.shape

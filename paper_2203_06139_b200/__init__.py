@@ -7,7 +7,7 @@ built library raises: there is no CPU fallback.
 """
 from ._capi import AdcError, LIB_PATH, lib  # noqa: F401
 from .launch import (BufferSet, LaunchConfig, LaunchOptions, LaunchStats, launch,  # noqa: F401
-                     launch_batch, registry_find)
+                     launch_batch, launch_batch_shared_p, registry_find)
 from .comm import Comm  # noqa: F401
 from .jit import JitModule, launch_module  # noqa: F401
 from .fit import (Chi2Plan, FitEngine, FitOptions, FitResult, GradientProvider,  # noqa: F401
@@ -16,7 +16,7 @@ from .fit import (Chi2Plan, FitEngine, FitOptions, FitResult, GradientProvider, 
 
 __all__ = [
     "AdcError", "BufferSet", "Comm", "JitModule", "launch_module", "LaunchConfig", "LaunchOptions", "LaunchStats", "launch",
-    "launch_batch", "registry_find", "Chi2Plan", "FitEngine", "FitOptions", "FitResult",
+    "launch_batch", "launch_batch_shared_p", "registry_find", "Chi2Plan", "FitEngine", "FitOptions", "FitResult",
     "GradientProvider", "Histogram", "bench_csv", "bench_scaling", "chi2_layout",
     "default_truth", "perturbed_init", "sample_histogram", "finalize", "record_len",
 ]

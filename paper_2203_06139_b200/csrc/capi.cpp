@@ -16,6 +16,10 @@ int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, con
                         double sigma, double* dx, double* dp, cudaStream_t s);
 int gaussnd_set_variant(int v);
 int64_t gauss_shared_blocks(int64_t n);
+int64_t gaussnd_shared_p_blocks(int64_t n);
+int launch_gaussnd_shared_p(int64_t n, int64_t dim, int64_t ld, const double* x, const double* p,
+                            double sigma, double* dx, double* dp, double* partials,
+                            cudaStream_t s);
 int launch_gauss_shared(int64_t n, const double* x, const double* p, double sigma, double* dx,
                         double* dp, double* dsigma, double* partials, cudaStream_t stream);
 
@@ -365,6 +369,28 @@ extern "C" int adc_cuda_gaussnd_grad_host(int64_t n, int64_t dim, int64_t ld, co
   ADCB_CUDA(cudaStreamSynchronize(g_staging.stream[0]));
   ADCB_CUDA(cudaStreamSynchronize(g_staging.stream[1]));
   return ADC_OK;
+}
+
+extern "C" int adc_cuda_gaussnd_grad_shared_p(int64_t n, int64_t dim, int64_t ld,
+                                              const double* x, const double* p, double sigma,
+                                              double* dx, double* dp, int32_t unsafe,
+                                              void* stream) {
+  clear_error();
+  if (!unsafe)
+    return fail(ADC_E_LAUNCH,
+                "launch refused, hazardous parameter(s): dp (whole array shared with a writing "
+                "callee across threads); pass the unsafe flag to force");
+  if (n < 0 || dim < 0) return fail(ADC_E_LAUNCH, "gaussnd: negative size");
+  if (ld < n) return fail(ADC_E_LAUNCH, "gaussnd: leading dimension smaller than n");
+  if (n > 0 && dim > 0 && (!x || !p || !dp)) return fail(ADC_E_LAUNCH, "missing buffer");
+  if (int rc = require_device()) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (n == 0 || dim == 0) return launch_gaussnd_shared_p(n, dim, ld, x, p, sigma, dx, dp, nullptr, s);
+  double* ws = nullptr;
+  ADCB_CUDA(cudaMallocAsync(&ws, (size_t)(gaussnd_shared_p_blocks(n) + 1) * dim * sizeof(double), s));
+  const int rc = launch_gaussnd_shared_p(n, dim, ld, x, p, sigma, dx, dp, ws, s);
+  cudaFreeAsync(ws, s);
+  return rc;
 }
 
 extern "C" int adc_cuda_gaussnd_set_variant(int32_t v) {

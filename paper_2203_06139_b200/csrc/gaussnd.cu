@@ -18,8 +18,12 @@
 // With W = 1 the forward sum runs in exactly the reference order; with W > 1
 // the per-warp partial sums are combined in fixed warp order (deterministic,
 // <= W-term regrouping of t).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -301,6 +305,341 @@ int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, con
 int gaussnd_set_variant(int v) {
   if (v < 0 || v > 9) return fail(ADC_E_ARG, "gaussnd variant must be 0..9");
   g_variant = v;
+  return ADC_OK;
+}
+
+// ---- K2s: shared mean vector (SURVEY.md §8(e) "shared-p variant") -----------------
+// Every point i calls gaussnd_grad_0_1(x[:, i], p, sigma, dim, dx[:, i], dp)
+// with ONE mean vector p[dim] and ONE shared slot dp[dim] (the reference's
+// race_check would flag dp, launch.cpp:217-224): the per-point arithmetic is
+// K2's (same forward sum order, same scalar chain, same reverse order), dx is
+// private (optional), and dp_d = sum_i (-_r6_{d,i}) is reduced in a FIXED
+// order: per 32-point tile a fixed shuffle tree per dim, tiles in order per
+// CTA (a CTA walks tiles b, b + G, ... with G a function of n only), then the
+// CTA partials in order, then dp[d] += total.  No atomics; the same bits on
+// every run and device.
+constexpr int64_t kSharedPMaxBlocks = 1184;
+
+template <int U, int V>
+__global__ void __launch_bounds__(32) gaussnd_shared_p_kernel(
+    const double* __restrict__ x, const double* __restrict__ p, double* __restrict__ dx,
+    int64_t n, int dim, int64_t ld, double t4, double r1, int dstage,
+    double* __restrict__ partials) {
+  extern __shared__ double smem[];
+  double* dpart = smem;              // [dim]
+  double* stage = smem + dim;        // [dstage][32]
+  const int lane = threadIdx.x;
+  for (int d = lane; d < dim; d += 32) dpart[d] = 0.0;
+  __syncwarp();
+  const int64_t ntiles = (n + 31) / 32;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i = tile * 32 + lane;
+    const bool valid = i < n;
+    const double* xi = x + i;
+    // ---- forward: U rows in flight, the next U rows prefetched into L2
+    double t = 0.0;
+    if (valid) {
+      int d = 0;
+      for (; d + U <= dim; d += U) {
+        double xv[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) xv[k] = ld_stream(xi + (int64_t)(d + k) * ld);
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const int dn = d + U + k;
+          if (dn < dim) prefetch_l2(xi + (int64_t)dn * ld);
+          else if (dx != nullptr && dim - 1 - (dn - dim) >= 0)
+            prefetch_l2(dx + i + (int64_t)(dim - 1 - (dn - dim)) * ld);  // first reverse rows
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const double u = fsub(xv[k], __ldg(p + d + k));  // _t0 = x[i] - p[i]
+          if (d + k < dstage) stage[(d + k) * 32 + lane] = u;
+          t = fadd(t, fmul(u, u));                          // t = t + _t1
+        }
+      }
+      for (; d < dim; ++d) {
+        const double u = fsub(ld_stream(xi + (int64_t)d * ld), __ldg(p + d));
+        if (d < dstage) stage[d * 32 + lane] = u;
+        t = fadd(t, fmul(u, u));
+      }
+    }
+    const double tt = fdiv(-t, t4);
+    const double e = exp(tt);
+    const double r2 = fadd(0.0, fmul(r1, e));
+    const double r3 = fadd(0.0, fdiv(r2, t4));
+    const double c = fadd(0.0, -r3);
+    // ---- reverse (the generated loop order, d descending), V dims at a time
+    // so V shuffle trees and dx read-modify-writes overlap
+    int d = dim - 1;
+    for (; d - (V - 1) >= 0; d -= V) {
+      double v[V], a[V];
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const int dd = d - k;
+        v[k] = 0.0;
+        if (valid && dx != nullptr) a[k] = dx[i + (int64_t)dd * ld];
+        // the next tile's row dim-1-dd into L2 (ascending over the sweep)
+        const int64_t inext = i + (int64_t)gridDim.x * 32;
+        if (inext < n) prefetch_l2(x + inext + (int64_t)(dim - 1 - dd) * ld);
+      }
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const int dd = d - k;
+        if (valid) {
+          const double u = dd < dstage ? stage[dd * 32 + lane]
+                                       : fsub(ld_stream(xi + (int64_t)dd * ld), __ldg(p + dd));
+          const double r6 = fadd(fadd(0.0, fmul(c, u)), fmul(u, c));
+          if (dx != nullptr) dx[i + (int64_t)dd * ld] = fadd(a[k], r6);  // _d_x[_i0] += _r6
+          v[k] = -r6;                                                      // _d_p[_i0] += -_r6
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+        for (int k = 0; k < V; ++k) v[k] += __shfl_down_sync(0xffffffffu, v[k], off);
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < V; ++k) dpart[d - k] = fadd(dpart[d - k], v[k]);
+      }
+    }
+    for (; d >= 0; --d) {
+      double v = 0.0;
+      if (valid) {
+        const double u = d < dstage ? stage[d * 32 + lane]
+                                    : fsub(ld_stream(xi + (int64_t)d * ld), __ldg(p + d));
+        const double r6 = fadd(fadd(0.0, fmul(c, u)), fmul(u, c));
+        if (dx != nullptr) {
+          double* a = dx + i + (int64_t)d * ld;
+          *a = fadd(*a, r6);
+        }
+        v = -r6;
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+      if (lane == 0) dpart[d] = fadd(dpart[d], v);
+    }
+    __syncwarp();
+  }
+  __syncwarp();
+  for (int d = lane; d < dim; d += 32) partials[(int64_t)blockIdx.x * dim + d] = dpart[d];
+}
+
+// TMA-staged variant: one warp per CTA, two stage buffers; while a tile is
+// computed from one buffer, the next tile's dim rows (256 B each, one bulk
+// copy per row issued by the lanes) stream into the other, so every warp has
+// a whole tile of x in flight.  u = x - p is formed from the staged x in both
+// sweeps (the same bits as K2s).  The dp sum is transposed: lane l owns dims
+// l, l + 32, ... and adds the tile's 32 points' -_r6 for them in a fixed
+// rotated point order (l + s) % 32 (bank-conflict free), into registers — no
+// cross-lane reductions per element.  dx (optional) stays per point.  Full
+// 32-point tiles only; dim <= 32 * JMAX.
+template <int V, int JMAX>
+__global__ void __launch_bounds__(32) gaussnd_shared_p_tma_kernel(
+    const __grid_constant__ CUtensorMap tmap, const double* __restrict__ x,
+    const double* __restrict__ p, double* __restrict__ dx, int64_t ntiles, int dim, int64_t ld,
+    double t4, double r1, double* __restrict__ partials) {
+  extern __shared__ __align__(128) double smem[];
+  double* buf0 = smem;                       // [dim][32]
+  double* buf1 = smem + (size_t)dim * 32;    // [dim][32]
+  double* cbuf = smem + (size_t)dim * 64;    // [32]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(cbuf + 32);  // 2 mbarriers
+  const int lane = threadIdx.x;
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const uint32_t tile_bytes = (uint32_t)dim * 256u;
+  // one 2-D TMA load per tile: box {32 points, dim rows} -> buf[dim][32]
+  auto issue = [&](int64_t tile, int b) {
+    double* buf = b ? buf1 : buf0;
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bar[b], tile_bytes);
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+          "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(buf)),
+          "l"(reinterpret_cast<uint64_t>(&tmap)), "r"((int)(tile * 32)), "r"(0),
+          "r"(smem_u32(&bar[b]))
+          : "memory");
+    }
+  };
+  double acc[JMAX];
+  double pj[JMAX];
+#pragma unroll
+  for (int j = 0; j < JMAX; ++j) {
+    acc[j] = 0.0;
+    const int d = lane + 32 * j;
+    pj[j] = d < dim ? __ldg(p + d) : 0.0;
+  }
+  uint32_t phase[2] = {0u, 0u};
+  int64_t tile = blockIdx.x;
+  if (tile < ntiles) issue(tile, 0);
+  if (tile + gridDim.x < ntiles) issue(tile + gridDim.x, 1);
+  for (int k = 0; tile < ntiles; tile += gridDim.x, ++k) {
+    const int b = k & 1;
+    double* buf = b ? buf1 : buf0;
+    mbar_wait(&bar[b], phase[b]);
+    phase[b] ^= 1u;
+    const int64_t i = tile * 32 + lane;
+    double t = 0.0;
+    for (int d = 0; d < dim; ++d) {
+      const double u = fsub(buf[d * 32 + lane], __ldg(p + d));  // _t0 = x[i] - p[i]
+      t = fadd(t, fmul(u, u));                                 // t = t + _t1
+    }
+    const double tt = fdiv(-t, t4);
+    const double e = exp(tt);
+    const double r2 = fadd(0.0, fmul(r1, e));
+    const double r3 = fadd(0.0, fdiv(r2, t4));
+    const double c = fadd(0.0, -r3);
+    cbuf[lane] = c;
+    if (dx != nullptr) {  // _d_x[_i0] += _r6, the generated reverse order
+      int d = dim - 1;
+      for (; d - (V - 1) >= 0; d -= V) {
+        double a[V];
+#pragma unroll
+        for (int q = 0; q < V; ++q) a[q] = dx[i + (int64_t)(d - q) * ld];
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+          const int dd = d - q;
+          const double u = fsub(buf[dd * 32 + lane], __ldg(p + dd));
+          dx[i + (int64_t)dd * ld] = fadd(a[q], fadd(fadd(0.0, fmul(c, u)), fmul(u, c)));
+        }
+      }
+      for (; d >= 0; --d) {
+        const double u = fsub(buf[d * 32 + lane], __ldg(p + d));
+        double* a = dx + i + (int64_t)d * ld;
+        *a = fadd(*a, fadd(fadd(0.0, fmul(c, u)), fmul(u, c)));
+      }
+    }
+    __syncwarp();  // cbuf visible
+    // _d_p[d] += -_r6 of every point of the tile, lane l owning dims l + 32 j
+#pragma unroll
+    for (int j = 0; j < JMAX; ++j) {
+      const int d = lane + 32 * j;
+      if (j * 32 < dim && d < dim) {
+        const double* row = buf + d * 32;
+        double aj = acc[j];
+        for (int s = 0; s < 32; ++s) {
+          const int l = (lane + s) & 31;
+          const double cl = cbuf[l];
+          const double u = fsub(row[l], pj[j]);
+          aj = fadd(aj, -fadd(fadd(0.0, fmul(cl, u)), fmul(u, cl)));
+        }
+        acc[j] = aj;
+      }
+    }
+    __syncwarp();  // every lane is done reading buf / cbuf before they are refilled
+    if (tile + 2 * (int64_t)gridDim.x < ntiles) issue(tile + 2 * (int64_t)gridDim.x, b);
+  }
+#pragma unroll
+  for (int j = 0; j < JMAX; ++j) {
+    const int d = lane + 32 * j;
+    if (d < dim) partials[(int64_t)blockIdx.x * dim + d] = acc[j];
+  }
+}
+
+__global__ void gaussnd_shared_p_finish(const double* __restrict__ partials, int64_t nblocks,
+                                        int dim, double* __restrict__ dp) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= dim) return;
+  double acc = 0.0;
+  for (int64_t b = 0; b < nblocks; ++b) acc = fadd(acc, partials[b * dim + d]);
+  dp[d] = fadd(dp[d], acc);
+}
+
+// 2-D tensor map over the SoA rows: inner dimension = points (contiguous),
+// outer = dims (stride ld), box = {32 points, dim rows}.  The driver entry
+// point is fetched through the runtime (no link-time libcuda dependency).
+static int make_rows_tmap(CUtensorMap* m, const double* x, int64_t npts, int64_t dim, int64_t ld) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (encode == nullptr) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        fn == nullptr) {
+      cudaGetLastError();
+      return ADC_E_CUDA;
+    }
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t gdim[2] = {(cuuint64_t)npts, (cuuint64_t)dim};
+  const cuuint64_t gstride[1] = {(cuuint64_t)ld * sizeof(double)};
+  const cuuint32_t box[2] = {32u, (cuuint32_t)dim};
+  const cuuint32_t estride[2] = {1u, 1u};
+  const CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(x), gdim,
+                            gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? ADC_OK : ADC_E_CUDA;
+}
+
+int64_t gaussnd_shared_p_blocks(int64_t n) {
+  return std::max<int64_t>(1, std::min<int64_t>((n + 31) / 32, kSharedPMaxBlocks));
+}
+
+int launch_gaussnd_shared_p(int64_t n, int64_t dim, int64_t ld, const double* x, const double* p,
+                            double sigma, double* dx, double* dp, double* partials,
+                            cudaStream_t s) {
+  const double PI = 3.14159265358979323846;
+  const double t3 = 2 * sigma;
+  const double t4 = t3 * sigma;
+  if (n > 0 && t4 == 0.0) return fail(ADC_E_EVAL, "division by zero");
+  if (n == 0 || dim == 0) return ADC_OK;
+  if (dim > (1 << 20)) return fail(ADC_E_ARG, "gaussnd: dim too large");
+  double d_t9 = 0;
+  d_t9 += (std::pow(2 * PI, -0.5) * std::pow(sigma, -0.5)) * 1.0;
+  // stage as many dims of u as fit next to dp's partials (<= 26 KB: 8 CTAs/SM);
+  // ADC_SHAREDP_STAGE=0 re-reads x (L2) instead (experiment knob)
+  size_t budget = 26 * 1024 + 1024;
+  if (const char* e = getenv("ADC_SHAREDP_STAGE")) budget = (size_t)atoll(e);
+  const size_t fixed = (size_t)dim * sizeof(double);
+  int dstage = fixed >= budget ? 0 : (int)std::min<int64_t>(dim, (budget - fixed) / 256);
+  const size_t smem = fixed + (size_t)dstage * 256;
+  auto k = gaussnd_shared_p_kernel<32, 8>;  // measured best of U in {16, 32} x V in {4, 8}
+  if (smem > 48 * 1024)
+    ADCB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // Decomposition (a function of n only, so the bits do not depend on the
+  // path or the device): the full 32-point tiles over `blocks` CTAs, the last
+  // partial tile (if any) as one more block of partials, then a fixed-order
+  // total per dim.
+  const int64_t full = n / 32, rem = n % 32;
+  const int64_t blocks = full > 0 ? gaussnd_shared_p_blocks(full * 32) : 0;
+  const size_t tma_smem = (size_t)dim * 64 * sizeof(double) + 32 * sizeof(double) +
+                          2 * sizeof(uint64_t);
+  // The TMA kernel serves the dp-only form (x streamed by 2-D tensor loads,
+  // 4.5 TB/s at 10M x 100); with private dx slots the per-point RMW wants
+  // more warps in flight than its stage buffers allow, so K2s<32, 8> runs.
+  const bool tma = (getenv("ADC_SHAREDP_TMA") ? atoi(getenv("ADC_SHAREDP_TMA")) != 0 : true) &&
+                   dx == nullptr && ld % 2 == 0 && ((uintptr_t)x & 15) == 0 && dim <= 256 &&
+                   tma_smem <= 200 * 1024;
+  if (full > 0) {
+    CUtensorMap tmap;
+    if (tma && make_rows_tmap(&tmap, x, full * 32, dim, ld) == ADC_OK) {
+      auto kt = dim <= 128 ? gaussnd_shared_p_tma_kernel<8, 4> : gaussnd_shared_p_tma_kernel<8, 8>;
+      if (tma_smem > 48 * 1024)
+        ADCB_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)tma_smem));
+      kt<<<(unsigned)blocks, 32, tma_smem, s>>>(tmap, x, p, dx, full, (int)dim, ld, t4, d_t9,
+                                                partials);
+    } else {
+      k<<<(unsigned)blocks, 32, smem, s>>>(x, p, dx, full * 32, (int)dim, ld, t4, d_t9, dstage,
+                                           partials);
+    }
+    ADCB_CUDA(cudaGetLastError());
+  }
+  if (rem != 0) {
+    const int64_t off = full * 32;
+    k<<<1, 32, smem, s>>>(x + off, p, dx ? dx + off : nullptr, rem, (int)dim, ld, t4, d_t9, dstage,
+                          partials + blocks * dim);
+    ADCB_CUDA(cudaGetLastError());
+  }
+  gaussnd_shared_p_finish<<<(unsigned)((dim + 127) / 128), 128, 0, s>>>(
+      partials, blocks + (rem != 0 ? 1 : 0), (int)dim, dp);
+  ADCB_CUDA(cudaGetLastError());
   return ADC_OK;
 }
 

@@ -206,5 +206,27 @@ def launch_batch(grad_fn: str, x, p, sigma: float, dx, dp, ld: int | None = None
                                              dptr(dp)))
 
 
+def launch_batch_shared_p(grad_fn: str, x, p, sigma: float, dx, dp,
+                          opts: LaunchOptions | None = None, ld: int | None = None,
+                          callee_fingerprint: int | None = None):
+    """The shared-mean batched path: for every point i,
+    gaussnd_grad_0_1(x[:, i], p, sigma, dim, dx[:, i], dp) with ONE p (dim,)
+    and ONE shared slot dp (dim,) — refused as a shared-write hazard unless
+    opts.unsafe; forced, dp is reduced in a fixed order (deterministic).  dx
+    may be None.  Device (CUDA tensor) buffers."""
+    opts = opts or LaunchOptions()
+    if grad_fn != "gaussnd_grad_0_1":
+        raise AdcError("Launch", f"no B200 kernel registered for '{grad_fn}'")
+    fp = _fingerprints()[grad_fn] if callee_fingerprint is None else callee_fingerprint
+    registry_find(grad_fn, fp)
+    dim, n = x.shape
+    ld = n if ld is None else ld
+    if not _is_torch(x):
+        raise AdcError("Launch", "launch_batch_shared_p takes device (CUDA tensor) buffers")
+    check(lib.adc_cuda_gaussnd_grad_shared_p(n, dim, ld, dptr(x), dptr(p), float(sigma),
+                                             dptr(dx) if dx is not None else None, dptr(dp),
+                                             1 if opts.unsafe else 0, _stream_of(x)))
+
+
 def set_gaussnd_variant(v: int):
     check(lib.adc_cuda_gaussnd_set_variant(v))

@@ -187,6 +187,23 @@ def main():
                    f"{key}_dx": o[0], f"{key}_dp": o[1], f"{key}_sigma": sigma})
     np.savez(os.path.join(OUT, "gaussnd_cases.npz"), **nd)
 
+    # Shared mean vector: one p, one dp slot for every point (points in order).
+    sp = {}
+    for dim, n, seed in ((100, 64, 31), (37, 150, 32), (1, 40, 33), (300, 33, 34)):
+        x, _ = synth.points_nd(dim, n, seed=seed)
+        r = np.random.Generator(np.random.PCG64(seed + 200))
+        p = r.uniform(-2, 2, dim)
+        x = p[:, None] + 0.1 * r.standard_normal((dim, n))
+        dx0 = r.standard_normal((dim, n)) * 1e-3
+        dp0 = r.standard_normal(dim) * 1e-3
+        np.concatenate([x.ravel(), p, dx0.ravel(), dp0]).astype("<f8").tofile(ti)
+        run("gaussnd-shared-p-in", dim, n, 1.3, ti, to)
+        o = f64(to, dim * n + dim)
+        key = f"d{dim}_n{n}"
+        sp.update({f"{key}_x": x, f"{key}_p": p, f"{key}_dx0": dx0, f"{key}_dp0": dp0,
+                   f"{key}_dx": o[:dim * n].reshape(dim, n), f"{key}_dp": o[dim * n:]})
+    np.savez(os.path.join(OUT, "gaussnd_shared_p_cases.npz"), **sp)
+
     # chi2 value + gradient (fit.cpp:206-259) for gpoly and gsum K=1,2.
     ch = {}
     for key, model, bins, events, qtrue, q in (

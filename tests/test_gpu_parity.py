@@ -477,3 +477,46 @@ def test_bench_scaling_rows():
     assert all(r.grad_evals > 0 and r.median_wall_ns > 0 for r in rows)
     csv = adc.bench_csv(rows)
     assert csv.splitlines()[0].startswith("K,params,provider")
+
+
+# ---------------------------------------------------------------------------- shared mean vector
+@pytest.mark.parametrize("key", ["d100_n64", "d37_n150", "d1_n40", "d300_n33"])
+def test_gaussnd_shared_p_golden(restate, key):
+    """One p and one shared dp slot for every point: dx per point within 1e-12
+    (as K2); dp = dp0 + a fixed-order sum of every point's -_r6, within
+    1e-12 * sum|terms| of the compensated total, within the reference's 1e-9
+    (test_launch.cpp:165) of its sequential result, bitwise repeatable."""
+    g = golden("gaussnd_shared_p_cases.npz")
+    x, p = g[f"{key}_x"], g[f"{key}_p"]
+
+    def run():
+        dx, dp = t(g[f"{key}_dx0"]), t(g[f"{key}_dp0"])
+        adc.launch_batch_shared_p("gaussnd_grad_0_1", t(x), t(p), 1.3, dx, dp,
+                                  adc.LaunchOptions(unsafe=True))
+        return host(dx), host(dp)
+
+    dx, dp = run()
+    scale = np.maximum(np.abs(g[f"{key}_dx0"]), 0)
+    assert (np.abs(dx - g[f"{key}_dx"]) <= REL * np.maximum(
+        np.maximum(np.abs(dx), np.abs(g[f"{key}_dx"])), scale)).all()
+    tot, ab = restate.gaussnd_shared_p_dp_compensated(np.ascontiguousarray(x), p, 1.3)
+    dp0 = g[f"{key}_dp0"]
+    assert np.all(np.abs(dp - (dp0 + tot)) <= 1e-12 * (ab + np.abs(dp0)))
+    assert rel_err(dp, g[f"{key}_dp"]).max() <= 1e-9
+    dx2, dp2 = run()
+    assert dp2.tobytes() == dp.tobytes() and dx2.tobytes() == dx.tobytes()
+
+
+def test_gaussnd_shared_p_large_and_refusal(restate):
+    dim, n = 100, 200_003
+    x, _ = synth.points_nd(dim, n, seed=5)
+    p = np.linspace(-1, 1, dim)
+    x = p[:, None] + 0.1 * np.random.Generator(np.random.PCG64(6)).standard_normal((dim, n))
+    dp = t(np.zeros(dim))
+    with pytest.raises(adc.AdcError) as e:
+        adc.launch_batch_shared_p("gaussnd_grad_0_1", t(x), t(p), 1.3, None, dp)
+    assert e.value.kind == "Launch" and str(e.value).startswith("launch refused")
+    adc.launch_batch_shared_p("gaussnd_grad_0_1", t(x), t(p), 1.3, None, dp,
+                              adc.LaunchOptions(unsafe=True))
+    tot, ab = restate.gaussnd_shared_p_dp_compensated(np.ascontiguousarray(x), p, 1.3)
+    assert np.all(np.abs(host(dp) - tot) <= 1e-12 * ab)

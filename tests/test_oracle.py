@@ -102,3 +102,14 @@ def test_chi2_numeric_provider_bitexact(restate, key):
     # numeric and AD agree to finite-difference accuracy (test_fit.cpp:62-79: 1e-6)
     ad, _ = restate.chi2_gradient_compensated(model, counts, -5.0, 5.0, ev, q)
     assert np.all(np.abs(gc - ad) <= 1e-6 * scale)
+
+
+@pytest.mark.parametrize("key", ["d100_n64", "d37_n150", "d1_n40", "d300_n33"])
+def test_gaussnd_shared_p_bitexact(restate, key):
+    # one p and one dp slot for every point, points in order: the reference's
+    # Program::eval run sequentially (ref_tool gaussnd-shared-p-in)
+    g = golden("gaussnd_shared_p_cases.npz")
+    dx, dp = g[f"{key}_dx0"].copy(), g[f"{key}_dp0"].copy()
+    restate.gaussnd_grad_shared_p(np.ascontiguousarray(g[f"{key}_x"]), g[f"{key}_p"], 1.3, dx, dp)
+    assert dx.tobytes() == g[f"{key}_dx"].tobytes()
+    assert dp.tobytes() == g[f"{key}_dp"].tobytes()
