@@ -3,11 +3,15 @@
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,driver_version,clocks.sm,clocks.max.sm --format=csv,noheader > gpurun_out/gpu.txt
 lscpu | grep -E "Model name|^CPU\(s\)" >> gpurun_out/gpu.txt; ldd --version | head -1 >> gpurun_out/gpu.txt
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -2 gpurun_out/smoke.log
-timeout 900 python bench.py > gpurun_out/bench_ours.json 2> gpurun_out/bench_ours.err; tail -c 3500 gpurun_out/bench_ours.json; tail -3 gpurun_out/bench_ours.err
-timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; tail -c 600 gpurun_out/bench_ref.json
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/launches_bench.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:gaussnd -s 3 -c 1 -o gpurun_out/prof_gaussnd python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-secondary > gpurun_out/ncu1.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:chi2_tile -s 3 -c 1 -o gpurun_out/prof_chi2 python tools/probe_chi2.py 100000000 > gpurun_out/ncu2.log 2>&1
+timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
+./oracle/_ref/bridge_check gpu > gpurun_out/bridge_gpu.log 2>&1; tail -1 gpurun_out/bridge_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
+timeout 1200 python bench.py > gpurun_out/bench_ours.json 2> gpurun_out/bench_ours.err; tail -3 gpurun_out/bench_ours.err
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-secondary > gpurun_out/launches_bench.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gaussnd_tile -s 3 -c 1 -o gpurun_out/prof_gaussnd python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-secondary > gpurun_out/ncu1.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:chi2_tile -s 3 -c 1 -o gpurun_out/prof_chi2 python tools/probe_chi2.py 100000000 0 > gpurun_out/ncu2.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:adc_kernel -s 2 -c 1 -o gpurun_out/prof_jit python tools/probe_jit.py > gpurun_out/ncu3.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:shared_p_tma -s 2 -c 1 -o gpurun_out/prof_sharedp python tools/probe_shared_p.py > gpurun_out/ncu4.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:chi2_multi -s 20 -c 1 -o gpurun_out/prof_multi python tools/probe_fit_1e6.py > gpurun_out/ncu5.log 2>&1
 ls gpurun_out
