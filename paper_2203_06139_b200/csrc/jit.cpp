@@ -645,6 +645,10 @@ struct Emitter {
   std::ostringstream o;
   int tmp = 0;
 
+  // DSL identifiers get a prefix so they can never clash with C++/CUDA names
+  // or the emitter's own (tape, ctx, N, ...).
+  static std::string V(const std::string& n) { return "v_" + n; }
+
   static std::string dbl(double v) {
     char b[64];
     std::snprintf(b, sizeof b, "%.17g", v);
@@ -663,7 +667,8 @@ struct Emitter {
         if (e.name == "blockIdx") return "(long long)blockIdx.x";
         if (e.name == "blockDim") return "(long long)blockDim.x";
         if (e.name == "threadIdx") return "(long long)threadIdx.x";
-        return e.name;
+        if (e.name == "N") return "N";
+        return V(e.name);
       case Ex::Neg: return "(-" + ie(*e.a[0]) + ")";
       case Ex::Bin:
         return "(" + ie(*e.a[0]) + " " + std::string(1, e.op) + " " + ie(*e.a[1]) + ")";
@@ -676,7 +681,7 @@ struct Emitter {
     if (e.is_int) return "(double)" + ie(e);
     switch (e.k) {
       case Ex::Num: return dbl(e.v);
-      case Ex::Var: return e.name;
+      case Ex::Var: return V(e.name);
       case Ex::Neg: return "(-" + re(*e.a[0]) + ")";
       case Ex::Bin: {
         const std::string a = re(*e.a[0]), b = re(*e.a[1]);
@@ -696,7 +701,7 @@ struct Emitter {
         if (e.name == "pow") return "pow(" + a[0] + ", " + a[1] + ")";
         return e.name + "(" + a[0] + ")";
       }
-      case Ex::Index: return "adc_ld(" + e.name + ", " + ie_any(*e.a[0]) + ", ctx)";
+      case Ex::Index: return "adc_ld(" + V(e.name) + ", " + ie_any(*e.a[0]) + ", ctx)";
       default: return "0.0";
     }
   }
@@ -724,9 +729,9 @@ struct Emitter {
     switch (s.k) {
       case St::Decl:
         if (s.type == VT::Integer)
-          o << ind(d) << "long long " << s.target << " = " << ie_any(*s.expr) << ";\n";
+          o << ind(d) << "long long " << V(s.target) << " = " << ie_any(*s.expr) << ";\n";
         else
-          o << ind(d) << "double " << s.target << " = " << re(*s.expr) << ";\n";
+          o << ind(d) << "double " << V(s.target) << " = " << re(*s.expr) << ";\n";
         if (f.global && prefetch && is_thread_index_decl(s)) {
           // Every array the kernel touches at the thread index: start its DRAM
           // read now (L2 prefetch), so a thread's loads of x[i], ... and of
@@ -734,9 +739,9 @@ struct Emitter {
           std::set<std::string> seen;
           prefetch_scan(f.body, s.target, seen);
           for (const auto& a : seen)
-            o << ind(d) << "if (" << s.target << " >= 0 && " << s.target << " < " << a
-              << ".len) asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(" << a << ".p + "
-              << s.target << "));\n";
+            o << ind(d) << "if (" << V(s.target) << " >= 0 && " << V(s.target) << " < " << V(a)
+              << ".len) asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(" << V(a)
+              << ".p + " << V(s.target) << "));\n";
         }
         sc.add(s.target, s.type);
         break;
@@ -745,20 +750,20 @@ struct Emitter {
         if (s.indexed) {
           const std::string idx = ie_any(*s.index), v = re(*s.expr);
           if (s.compound)
-            o << ind(d) << (unsafe ? "adc_st_add_atomic(" : "adc_st_add(") << s.target << ", "
+            o << ind(d) << (unsafe ? "adc_st_add_atomic(" : "adc_st_add(") << V(s.target) << ", "
               << idx << ", " << v << ", ctx);\n";
           else
-            o << ind(d) << "adc_st(" << s.target << ", " << idx << ", " << v << ", ctx);\n";
+            o << ind(d) << "adc_st(" << V(s.target) << ", " << idx << ", " << v << ", ctx);\n";
         } else if (t == VT::Integer) {
           const std::string v = ie_any(*s.expr);
-          if (s.compound) o << ind(d) << s.target << " = " << s.target << " + " << v << ";\n";
-          else o << ind(d) << s.target << " = " << v << ";\n";
+          if (s.compound) o << ind(d) << V(s.target) << " = " << V(s.target) << " + " << v << ";\n";
+          else o << ind(d) << V(s.target) << " = " << v << ";\n";
         } else {
           const std::string v = re(*s.expr);
           if (s.compound)
-            o << ind(d) << s.target << " = __dadd_rn(" << s.target << ", " << v << ");\n";
+            o << ind(d) << V(s.target) << " = __dadd_rn(" << V(s.target) << ", " << v << ");\n";
           else
-            o << ind(d) << s.target << " = " << v << ";\n";
+            o << ind(d) << V(s.target) << " = " << v << ";\n";
         }
         break;
       case St::Return:
@@ -780,8 +785,8 @@ struct Emitter {
         o << ind(d) << "{\n";
         o << ind(d + 1) << "const long long _adc_lo" << k << " = " << ie_any(*s.lo) << ";\n";
         o << ind(d + 1) << "const long long _adc_hi" << k << " = " << ie_any(*s.hi) << ";\n";
-        o << ind(d + 1) << "for (long long " << s.loop_var << " = _adc_lo" << k << "; "
-          << s.loop_var << " < _adc_hi" << k << "; ++" << s.loop_var << ") {\n";
+        o << ind(d + 1) << "for (long long " << V(s.loop_var) << " = _adc_lo" << k << "; "
+          << V(s.loop_var) << " < _adc_hi" << k << "; ++" << V(s.loop_var) << ") {\n";
         sc.push();
         sc.add(s.loop_var, VT::Integer);
         block(s.then_b, f, sc, d + 2);
@@ -809,9 +814,9 @@ struct Emitter {
           const VT pt = c->params[a].type;
           if (a) o << ", ";
           if (pt == VT::RealArray) {
-            if (arg.k == Ex::Var) o << arg.name;  // whole array
-            else if (arg.k == Ex::Index)          // length-1 slice (eval.cpp:485-499)
-              o << "adc_slice(" << arg.name << ", " << ie_any(*arg.a[0]) << ", ctx)";
+            if (arg.k == Ex::Var) o << V(arg.name);  // whole array
+            else if (arg.k == Ex::Index)             // length-1 slice (eval.cpp:485-499)
+              o << "adc_slice(" << V(arg.name) << ", " << ie_any(*arg.a[0]) << ", ctx)";
             else throw ParseError{"argument of '" + s.callee + "' must be an array or slice"};
           } else if (pt == VT::Integer) {
             o << ie_any(arg);
@@ -923,18 +928,20 @@ __device__ __forceinline__ long long adc_pop_ctl(long long* t, int& cp, const Ad
       for (size_t i = 0; i < f.params.size(); ++i) {
         const Prm& p = f.params[i];
         if (i) o << ", ";
-        if (p.type == VT::RealArray) o << "double* " << p.name << "_p, long long " << p.name << "_n";
-        else o << ptype(p.type) << " " << p.name;
+        if (p.type == VT::RealArray)
+          o << "double* " << V(p.name) << "_p, long long " << V(p.name) << "_n";
+        else
+          o << ptype(p.type) << " " << V(p.name);
       }
       o << (f.params.empty() ? "" : ", ") << "long long N, AdcErr* adc_err) {\n";
       o << "  const AdcCtx ctx{adc_err, (long long)blockIdx.x * blockDim.x + threadIdx.x};\n";
       for (auto& p : f.params)
         if (p.type == VT::RealArray)
-          o << "  const AdcArr " << p.name << "{" << p.name << "_p, " << p.name << "_n};\n";
+          o << "  const AdcArr " << V(p.name) << "{" << V(p.name) << "_p, " << V(p.name) << "_n};\n";
     } else {
       o << "__device__ " << (f.returns_void ? "void" : "double") << " fn_" << f.name << "(";
       for (size_t i = 0; i < f.params.size(); ++i)
-        o << (i ? ", " : "") << ptype(f.params[i].type) << " " << f.params[i].name;
+        o << (i ? ", " : "") << ptype(f.params[i].type) << " " << V(f.params[i].name);
       o << (f.params.empty() ? "" : ", ") << "const AdcCtx& ctx) {\n";
     }
     if (f.uses_tape) o << "  double tape[ADC_TAPE]; int tp = 0;\n";
@@ -1022,7 +1029,7 @@ extern "C" int adc_jit_compile(const char* source, const char* kernel, int32_t u
                                std::string s;
                                for (size_t i = 0; i < f.params.size(); ++i)
                                  s += (i ? ", " : "") + Emitter::ptype(f.params[i].type) + " " +
-                                      f.params[i].name;
+                                      Emitter::V(f.params[i].name);
                                return s + (f.params.empty() ? "" : ", ") + "const AdcCtx& ctx);\n";
                              }();
     em.o << "\n";

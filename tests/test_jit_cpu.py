@@ -73,3 +73,25 @@ def test_launch_without_device_has_no_fallback():
     with pytest.raises(adc.AdcError) as e:
         m.launch(adc.LaunchConfig(1, 8, n), bufs)
     assert e.value.kind == "Cuda"
+
+
+def test_dsl_names_that_clash_with_cuda_or_emitter_names():
+    # DSL identifiers are prefixed in the emitted CUDA: names like tape, ctx,
+    # cp, double or threadIdx-lookalikes cannot collide with the emitter's own.
+    src = """device host void f_grad(real tape, real ctx, integer cp, real[] _d_tape, real[] double) {
+  real tp = 0;
+  __push(tp);
+  tp = tape * ctx;
+  _d_tape[0] += ctx;
+  double[0] += tape * cp;
+  tp = __pop();
+}
+global void k(real[] x, real[] y, real[] dx, real[] dy) {
+  integer i = blockIdx * blockDim + threadIdx;
+  if (i < N) {
+    f_grad(x[i], y[i], 3, dx[i], dy[i]);
+  }
+}
+"""
+    m = adc.JitModule(src, "k")
+    assert m.cubin_size > 0 and "v_double" in m.cuda_source
