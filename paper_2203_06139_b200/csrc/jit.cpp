@@ -642,6 +642,15 @@ struct Emitter {
   bool unsafe;
   int tape_cap;
   bool prefetch = true;
+  // Slot caching: a void function whose array parameters are only ever
+  // accessed at the literal index 0 (the length-1 slices of Listing-1 slots)
+  // gets a second variant fn_<name>_c that keeps each such slot in a
+  // register for the whole call (one load at entry, one store at exit if
+  // written) instead of a global read-modify-write per `+=` statement.  Used
+  // only where the call's array arguments are pairwise distinct kernel arrays
+  // (no aliasing; BufferSet arrays are distinct) and never when unsafe.
+  std::map<std::string, std::vector<int>> cacheable;  // fn -> per param: 0 no, 1 read, 2 written
+  const std::set<std::string>* cached = nullptr;      // params cached in the variant being emitted
   std::ostringstream o;
   int tmp = 0;
 
@@ -701,7 +710,9 @@ struct Emitter {
         if (e.name == "pow") return "pow(" + a[0] + ", " + a[1] + ")";
         return e.name + "(" + a[0] + ")";
       }
-      case Ex::Index: return "adc_ld(" + V(e.name) + ", " + ie_any(*e.a[0]) + ", ctx)";
+      case Ex::Index:
+        if (cached != nullptr && cached->count(e.name)) return "c_" + V(e.name);
+        return "adc_ld(" + V(e.name) + ", " + ie_any(*e.a[0]) + ", ctx)";
       default: return "0.0";
     }
   }
@@ -747,7 +758,12 @@ struct Emitter {
         break;
       case St::Assign:
         sc.find(s.target, t);
-        if (s.indexed) {
+        if (s.indexed && cached != nullptr && cached->count(s.target)) {
+          const std::string v = re(*s.expr);
+          const std::string c = "c_" + V(s.target);
+          if (s.compound) o << ind(d) << c << " = __dadd_rn(" << c << ", " << v << ");\n";
+          else o << ind(d) << c << " = " << v << ";\n";
+        } else if (s.indexed) {
           const std::string idx = ie_any(*s.index), v = re(*s.expr);
           if (s.compound)
             o << ind(d) << (unsafe ? "adc_st_add_atomic(" : "adc_st_add(") << V(s.target) << ", "
@@ -808,7 +824,17 @@ struct Emitter {
         if (c->global) throw ParseError{"a kernel cannot call a global function"};
         if (c->params.size() != s.args.size())
           throw ParseError{"wrong argument count calling '" + s.callee + "'"};
-        o << ind(d) << "fn_" << c->name << "(";
+        bool use_cached = false;
+        if (!unsafe && cacheable.count(c->name)) {
+          std::set<std::string> arrays_seen;
+          use_cached = true;
+          for (size_t a = 0; a < s.args.size() && a < c->params.size(); ++a) {
+            if (c->params[a].type != VT::RealArray) continue;
+            const Ex& arg = *s.args[a];
+            if (!arrays_seen.insert(arg.name).second) use_cached = false;  // aliasing
+          }
+        }
+        o << ind(d) << "fn_" << c->name << (use_cached ? "_c" : "") << "(";
         for (size_t a = 0; a < s.args.size(); ++a) {
           const Ex& arg = *s.args[a];
           const VT pt = c->params[a].type;
@@ -918,7 +944,82 @@ __device__ __forceinline__ long long adc_pop_ctl(long long* t, int& cp, const Ad
 )";
   }
 
+  // 0: not cacheable, 1: only read at [0], 2: read/written at [0] only
+  static void slot_uses(const Blk& b, const std::string& n, bool& ok, bool& written) {
+    std::function<void(const Ex&)> ex = [&](const Ex& e) {
+      if ((e.k == Ex::Index && e.name == n) &&
+          !(e.a[0]->k == Ex::Num && e.a[0]->int_lit && e.a[0]->v == 0.0))
+        ok = false;
+      if (e.k == Ex::Var && e.name == n) ok = false;  // whole-array use (a call argument)
+      for (auto& c : e.a) ex(*c);
+    };
+    for (auto& sp : b) {
+      const St& s = *sp;
+      if (s.k == St::Assign && s.indexed && s.target == n) {
+        written = true;
+        if (!(s.index->k == Ex::Num && s.index->int_lit && s.index->v == 0.0)) ok = false;
+      }
+      if (s.expr) ex(*s.expr);
+      if (s.index) ex(*s.index);
+      if (s.lo) ex(*s.lo);
+      if (s.hi) ex(*s.hi);
+      for (auto& a : s.args) {
+        if ((a->k == Ex::Var || a->k == Ex::Index) && a->name == n && s.callee != "__push")
+          ok = false;  // passed on to a callee
+        ex(*a);
+      }
+      slot_uses(s.then_b, n, ok, written);
+      slot_uses(s.else_b, n, ok, written);
+    }
+  }
+
+  void analyse_cacheable(const Fn& f) {
+    if (f.global || !f.returns_void) return;
+    std::vector<int> v(f.params.size(), 0);
+    bool any = false;
+    for (size_t i = 0; i < f.params.size(); ++i) {
+      if (f.params[i].type != VT::RealArray) continue;
+      bool ok = true, written = false;
+      slot_uses(f.body, f.params[i].name, ok, written);
+      if (ok) {
+        v[i] = written ? 2 : 1;
+        any = true;
+      }
+    }
+    if (any) cacheable[f.name] = v;
+  }
+
+  void function_cached(const Fn& f) {
+    const std::vector<int>& v = cacheable.at(f.name);
+    std::set<std::string> names;
+    o << "__device__ void fn_" << f.name << "_c(";
+    for (size_t i = 0; i < f.params.size(); ++i)
+      o << (i ? ", " : "") << ptype(f.params[i].type) << " " << V(f.params[i].name);
+    o << (f.params.empty() ? "" : ", ") << "const AdcCtx& ctx) {\n";
+    for (size_t i = 0; i < f.params.size(); ++i) {
+      if (!v[i]) continue;
+      const std::string n = V(f.params[i].name);
+      names.insert(f.params[i].name);
+      o << "  double c_" << n << " = adc_ok(" << n << ", 0, ctx) ? " << n << ".p[0] : 0.0;\n";
+    }
+    if (f.uses_tape) o << "  double tape[ADC_TAPE]; int tp = 0;\n";
+    if (f.uses_ctl) o << "  long long ctl[ADC_TAPE]; int cp = 0;\n";
+    Scope sc;
+    sc.push();
+    for (auto& p : f.params) sc.add(p.name, p.type);
+    cached = &names;
+    block(f.body, f, sc, 1);
+    cached = nullptr;
+    for (size_t i = 0; i < f.params.size(); ++i)
+      if (v[i] == 2) {
+        const std::string n = V(f.params[i].name);
+        o << "  if (" << n << ".len > 0) " << n << ".p[0] = c_" << n << ";\n";
+      }
+    o << "}\n\n";
+  }
+
   void function(const Fn& f) {
+    if (cacheable.count(f.name)) function_cached(f);
     Scope sc;
     sc.push();
     for (auto& p : f.params) sc.add(p.name, p.type);
@@ -1049,8 +1150,14 @@ extern "C" int adc_jit_compile(const char* source, const char* kernel, int32_t u
       }
     };
     for (size_t w = 0; w < work.size(); ++w) scan(work[w]->body);
+    if (!(getenv("ADC_JIT_SLOTCACHE") && atoi(getenv("ADC_JIT_SLOTCACHE")) == 0))
+      for (auto& f : m.fns)
+        if (reach.count(f.name)) em.analyse_cacheable(f);
+    // callees first, so a cached variant is declared before its call sites
     for (auto& f : m.fns)
-      if (reach.count(f.name)) em.function(f);
+      if (reach.count(f.name) && !f.global) em.function(f);
+    for (auto& f : m.fns)
+      if (reach.count(f.name) && f.global) em.function(f);
   } catch (const ParseError& e) {
     return fail(ADC_E_SEMANTIC, "jit: " + e.msg);
   }
