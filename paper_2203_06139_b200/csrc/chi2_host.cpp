@@ -133,6 +133,7 @@ struct adc_chi2_plan {
   // [kind][fast], kind 0 = value, 1 = AD gradient, 2 = numeric gradient
   cudaGraphExec_t graph[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
   bool warm[3][2] = {{false, false}, {false, false}, {false, false}};  // eager pass before capture
+  bool no_graph = false;  // the transport refused stream capture: enqueue directly
   // exchange / copy-back staging, sized once for the largest pass kind
   adc_comm* comm = nullptr;
   size_t xcount = 0;          // doubles per rank the staging holds
@@ -312,12 +313,23 @@ int run_pass(adc_chi2_plan* P, const double* q, int grad, const double** rec) {
   fill_qdev(P->model, P->np, q, P->h_q);
   if (int rc = ensure_lin(P, P->stream)) return rc;
   const int kind = grad ? 1 + numeric(P) : 0;
-  if (!P->warm[kind][P->fast]) {
+  if (!P->warm[kind][P->fast] || P->no_graph) {
     if (int rc = enqueue_pass(P, grad)) return rc;
     P->warm[kind][P->fast] = true;
   } else {
-    if (P->graph[kind][P->fast] == nullptr)
-      if (int rc = build_graph(P, grad)) return rc;
+    if (P->graph[kind][P->fast] == nullptr) {
+      if (int rc = build_graph(P, grad)) {
+        // A transport that cannot be captured (an older NCCL) keeps working
+        // with direct stream enqueues; anything else is an error.
+        if (P->comm == nullptr || P->comm->kind != ADC_COMM_NCCL) return rc;
+        cudaGetLastError();
+        clear_error();
+        P->no_graph = true;
+        if (int rc2 = enqueue_pass(P, grad)) return rc2;
+        ADCB_CUDA(cudaStreamSynchronize(P->stream));
+        return collect_finish(P, adc_chi2_record_len(P->np, grad), 1, rec);
+      }
+    }
     ADCB_CUDA(cudaGraphLaunch(P->graph[kind][P->fast], P->stream));
   }
   ADCB_CUDA(cudaStreamSynchronize(P->stream));
