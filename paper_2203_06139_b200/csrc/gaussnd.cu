@@ -209,8 +209,142 @@ __global__ void __launch_bounds__(W * 32) gaussnd_tile_kernel(
   }
 }
 
+// K2v: two points per lane with 16-byte (double2) accesses — a warp covers a
+// 64-point tile, each row access is one 512-byte segment.  Same per-point
+// arithmetic and order as K2 (W = 1), so each point's bits are K2's; the two
+// points of a lane are two independent dependency chains.  Full 64-point
+// tiles of a 16-byte-aligned, even-ld layout; the caller runs the rest with K2.
+template <int U>
+__global__ void __launch_bounds__(32) gaussnd_vec2_kernel(
+    const double* __restrict__ x, const double* __restrict__ p, double* __restrict__ dx,
+    double* __restrict__ dp, int64_t ntiles, int dim, int64_t ld, double t4, double r1,
+    int dstage) {
+  extern __shared__ double2 stage2[];  // [dstage][32]
+  const int lane = threadIdx.x;
+  const int64_t ld2 = ld / 2;
+  const double2* x2 = reinterpret_cast<const double2*>(x);
+  const double2* p2 = reinterpret_cast<const double2*>(p);
+  double2* dx2 = reinterpret_cast<double2*>(dx);
+  double2* dp2 = reinterpret_cast<double2*>(dp);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i2 = tile * 32 + lane;  // double2 index of points 2 i2, 2 i2 + 1
+    double ta = 0.0, tb = 0.0;
+    int d = 0;
+    for (; d + U <= dim; d += U) {
+      double2 xv[U], pv[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        xv[k] = ld_stream2(x2 + (int64_t)(d + k) * ld2 + i2);
+        pv[k] = ld_stream2(p2 + (int64_t)(d + k) * ld2 + i2);
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {  // next batch (or the first reverse rows) into L2
+        const int dn = d + U + k;
+        if ((lane & 7) == 0) {
+          if (dn < dim) {
+            prefetch_l2(x2 + (int64_t)dn * ld2 + i2);
+            prefetch_l2(p2 + (int64_t)dn * ld2 + i2);
+          } else if (dim - 1 - (dn - dim) >= 0) {
+            const int64_t o = (int64_t)(dim - 1 - (dn - dim)) * ld2 + i2;
+            prefetch_l2(dx2 + o);
+            prefetch_l2(dp2 + o);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const double ua = fsub(xv[k].x, pv[k].x), ub = fsub(xv[k].y, pv[k].y);
+        if (d + k < dstage) stage2[(d + k) * 32 + lane] = make_double2(ua, ub);
+        ta = fadd(ta, fmul(ua, ua));
+        tb = fadd(tb, fmul(ub, ub));
+      }
+    }
+    for (; d < dim; ++d) {
+      const double2 xv = ld_stream2(x2 + (int64_t)d * ld2 + i2);
+      const double2 pv = ld_stream2(p2 + (int64_t)d * ld2 + i2);
+      const double ua = fsub(xv.x, pv.x), ub = fsub(xv.y, pv.y);
+      if (d < dstage) stage2[d * 32 + lane] = make_double2(ua, ub);
+      ta = fadd(ta, fmul(ua, ua));
+      tb = fadd(tb, fmul(ub, ub));
+    }
+    double ca, cb;
+    {
+      const double e = exp(fdiv(-ta, t4));
+      ca = fadd(0.0, -fadd(0.0, fdiv(fadd(0.0, fmul(r1, e)), t4)));
+      const double f = exp(fdiv(-tb, t4));
+      cb = fadd(0.0, -fadd(0.0, fdiv(fadd(0.0, fmul(r1, f)), t4)));
+    }
+    d = dim;
+    for (; d - U >= 0; d -= U) {
+      double2 a[U], b[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t o = (int64_t)(d - 1 - k) * ld2 + i2;
+        a[k] = dx2[o];
+        b[k] = dp2[o];
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {  // next batch of slot rows; at the end, the next tile
+        const int dn = d - 1 - U - k;
+        if ((lane & 7) == 0) {
+          if (dn >= 0) {
+            prefetch_l2(dx2 + (int64_t)dn * ld2 + i2);
+            prefetch_l2(dp2 + (int64_t)dn * ld2 + i2);
+          } else if (tile + gridDim.x < ntiles && -1 - dn < dim) {
+            const int64_t o = (int64_t)(-1 - dn) * ld2 + i2 + (int64_t)gridDim.x * 32;
+            prefetch_l2(x2 + o);
+            prefetch_l2(p2 + o);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int dd = d - 1 - k;
+        double ua, ub;
+        if (dd < dstage) {
+          const double2 u = stage2[dd * 32 + lane];
+          ua = u.x;
+          ub = u.y;
+        } else {
+          const double2 xv = ld_stream2(x2 + (int64_t)dd * ld2 + i2);
+          const double2 pv = ld_stream2(p2 + (int64_t)dd * ld2 + i2);
+          ua = fsub(xv.x, pv.x);
+          ub = fsub(xv.y, pv.y);
+        }
+        const double ra = fadd(fadd(0.0, fmul(ca, ua)), fmul(ua, ca));
+        const double rb = fadd(fadd(0.0, fmul(cb, ub)), fmul(ub, cb));
+        const int64_t o = (int64_t)dd * ld2 + i2;
+        dx2[o] = make_double2(fadd(a[k].x, ra), fadd(a[k].y, rb));
+        dp2[o] = make_double2(fadd(b[k].x, -ra), fadd(b[k].y, -rb));
+      }
+    }
+    for (; d > 0; --d) {
+      const int dd = d - 1;
+      double ua, ub;
+      if (dd < dstage) {
+        const double2 u = stage2[dd * 32 + lane];
+        ua = u.x;
+        ub = u.y;
+      } else {
+        const double2 xv = ld_stream2(x2 + (int64_t)dd * ld2 + i2);
+        const double2 pv = ld_stream2(p2 + (int64_t)dd * ld2 + i2);
+        ua = fsub(xv.x, pv.x);
+        ub = fsub(xv.y, pv.y);
+      }
+      const double ra = fadd(fadd(0.0, fmul(ca, ua)), fmul(ua, ca));
+      const double rb = fadd(fadd(0.0, fmul(cb, ub)), fmul(ub, cb));
+      const int64_t o = (int64_t)dd * ld2 + i2;
+      const double2 a = dx2[o], b = dp2[o];
+      dx2[o] = make_double2(fadd(a.x, ra), fadd(a.y, rb));
+      dp2[o] = make_double2(fadd(b.x, -ra), fadd(b.y, -rb));
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
-// 0 auto; 1/3/4 = one warp per 32-point tile (reference summation order) with
+// 0 auto (K2v below 105 dims when aligned, else K2 as chosen by choose());
+// 10-13 = K2v (U = 16 / 16 with a 104 KB stage / 8 / 32);
+// 1/3/4 = one warp per 32-point tile (reference summation order) with
 // 8/16/32 rows in flight per thread (+ L2 prefetch of the next batch);
 // 5 = as 3 without prefetch; 6 = as 3 with bulk (TMA-unit) prefetch;
 // 2 = dims split over the warps of a CTA (7 = same with bulk prefetch);
@@ -280,6 +414,37 @@ int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, con
   if (dim > (1 << 24)) return fail(ADC_E_ARG, "gaussnd: dim too large");
   double d_t9 = 0;
   d_t9 += (std::pow(2 * PI, -0.5) * std::pow(sigma, -0.5)) * 1.0;  // _d__t9 += _t8 * _r0
+  // Auto: K2v for dims whose u rows all fit its 52 KB stage (the dim-100
+  // headline: 6.0 TB/s vs 5.8 for K2, the same bits per point).
+  const bool vec2_auto = g_variant == 0 && dim <= 104;
+  if (vec2_auto || (g_variant >= 10 && g_variant <= 13)) {
+    const int64_t ntiles = n / 64;
+    const bool ok = ld % 2 == 0 && ((((uintptr_t)x) | ((uintptr_t)p) | ((uintptr_t)dx) |
+                                     ((uintptr_t)dp)) & 15) == 0;
+    if (ok && ntiles > 0) {
+      const size_t budget = g_variant == 11 ? 104 * 1024 : 52 * 1024;
+      const int dstage = (int)std::min<int64_t>(dim, budget / 512);
+      const size_t smem = (size_t)dstage * 512;
+      auto k = g_variant == 12 ? gaussnd_vec2_kernel<8>
+             : g_variant == 13 ? gaussnd_vec2_kernel<32> : gaussnd_vec2_kernel<16>;
+      if (smem > 48 * 1024)
+        ADCB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int occ = 0;
+      ADCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 32, smem));
+      const int64_t blocks = std::min<int64_t>(ntiles, (int64_t)std::max(1, occ) * sm_count());
+      k<<<(unsigned)blocks, 32, smem, s>>>(x, p, dx, dp, ntiles, (int)dim, ld, t4, d_t9, dstage);
+      ADCB_CUDA(cudaGetLastError());
+      const int64_t done = ntiles * 64;
+      if (done == n) return ADC_OK;
+      // the last partial tile through K2 (W = 1 for these dims: same per-point bits)
+      const int saved = g_variant;
+      g_variant = 3;
+      const int rc = launch_gaussnd_grad(n - done, dim, ld, x + done, p + done, sigma, dx + done,
+                                         dp + done, s);
+      g_variant = saved;
+      return rc;
+    }
+  }
   NdConfig c = choose((int)dim);
   switch (c.w) {
     case 1:
@@ -303,7 +468,7 @@ int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, con
 }
 
 int gaussnd_set_variant(int v) {
-  if (v < 0 || v > 9) return fail(ADC_E_ARG, "gaussnd variant must be 0..9");
+  if (v < 0 || v > 13) return fail(ADC_E_ARG, "gaussnd variant must be 0..13");
   g_variant = v;
   return ADC_OK;
 }
