@@ -9,7 +9,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 1200 python bench.py > gpurun_out/bench_ours.json 2> gpurun_out/bench_ours.err; tail -3 gpurun_out/bench_ours.err
 timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-secondary > gpurun_out/launches_bench.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:gaussnd_tile -s 3 -c 1 -o gpurun_out/prof_gaussnd python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-secondary > gpurun_out/ncu1.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gaussnd_ -s 3 -c 1 -o gpurun_out/prof_gaussnd python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-secondary > gpurun_out/ncu1.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:chi2_tile -s 3 -c 1 -o gpurun_out/prof_chi2 python tools/probe_chi2.py 100000000 0 > gpurun_out/ncu2.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:adc_kernel -s 2 -c 1 -o gpurun_out/prof_jit python tools/probe_jit.py > gpurun_out/ncu3.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:shared_p_tma -s 2 -c 1 -o gpurun_out/prof_sharedp python tools/probe_shared_p.py > gpurun_out/ncu4.log 2>&1
