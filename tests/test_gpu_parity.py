@@ -114,7 +114,7 @@ def test_listing1_domain_error():
 ND_KEYS = ["d100_n64", "d1000_n8", "d1_n33", "d37_n70", "d128_n40", "d129_n5"]
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13])
 @pytest.mark.parametrize("key", ND_KEYS)
 def test_gaussnd_golden(key, variant):
     g = golden("gaussnd_cases.npz")
@@ -139,12 +139,14 @@ def test_gaussnd_host_path():
     assert acc_err(dp, g[f"{key}_dp"], g[f"{key}_dp0"]).max() <= REL
 
 
-@pytest.mark.parametrize("dim,n", [(100, 200_003), (1000, 20_011), (5, 77), (300, 1000)])
+@pytest.mark.parametrize("dim,n", [(100, 200_003), (100, 200_010), (64, 4096), (1000, 20_011),
+                                   (5, 77), (300, 1000)])
 def test_gaussnd_vs_oracle(restate, dim, n):
+    # variant 0 = auto (K2v with double2 for dim <= 104 on even ld, tail via K2)
     x, p = synth.points_nd(dim, n, seed=dim)
     ox, op = np.zeros((dim, n)), np.zeros((dim, n))
     restate.gaussnd_grad(x, p, 1.3, ox, op)
-    for variant in (1, 2, 6, 7):
+    for variant in (0, 1, 2, 6, 7, 10):
         set_gaussnd_variant(variant)
         try:
             dx = torch.zeros((dim, n), dtype=torch.float64, device=DEV)
