@@ -209,6 +209,86 @@ __global__ void __launch_bounds__(W * 32) gaussnd_tile_kernel(
   }
 }
 
+static int make_rows_tmap(CUtensorMap* m, const double* x, int64_t npts, int64_t dim, int64_t ld);
+
+// K2t: the TMA-streamed form.  One warp per CTA (one per SM: the stages take
+// ~205 KB of shared memory at dim 100).  Per 32-point tile, four 2-D tensor
+// loads (x, p, dx, dp; box {32 points, dim rows}) land in a stage; two stages
+// alternate, so the next tile's 4 x dim x 256 B are in flight while this one
+// is computed.  Forward and reverse read u = x - p from the staged x, p (the
+// same bits as K2), the reverse reads the staged dx, dp and writes the
+// updated rows with ordinary coalesced stores (fire and forget, so the stage
+// can be refilled at once).  Full tiles only; the caller runs the tail.
+// Measured (variant 14, 10M x 100): 8.71 ms = 5.5 TB/s, below K2v's 7.95 ms:
+// one warp per SM cannot issue the stores and the FP64 chain fast enough.
+// Kept as the experiment it is; K2v is the auto choice.
+__global__ void __launch_bounds__(32) gaussnd_tma_kernel(
+    const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tp,
+    const __grid_constant__ CUtensorMap tdx, const __grid_constant__ CUtensorMap tdp,
+    double* __restrict__ dx, double* __restrict__ dp, int64_t ntiles, int dim, int64_t ld,
+    double t4, double r1) {
+  extern __shared__ __align__(128) double smem[];
+  const size_t tile_d = (size_t)dim * 32;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 8 * tile_d);  // [2]
+  const int lane = threadIdx.x;
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const uint32_t tile_bytes = (uint32_t)dim * 256u;
+  auto issue = [&](int64_t tile, int st) {
+    if (lane == 0) {
+      double* base = smem + (size_t)st * 4 * tile_d;
+      mbar_arrive_expect_tx(&bar[st], 4 * tile_bytes);
+      const CUtensorMap* maps[4] = {&tx, &tp, &tdx, &tdp};
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+            "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(base + a * tile_d)),
+            "l"(reinterpret_cast<uint64_t>(maps[a])), "r"((int)(tile * 32)), "r"(0),
+            "r"(smem_u32(&bar[st]))
+            : "memory");
+    }
+  };
+  uint32_t phase[2] = {0u, 0u};
+  int64_t tile = blockIdx.x;
+  if (tile < ntiles) issue(tile, 0);
+  if (tile + gridDim.x < ntiles) issue(tile + gridDim.x, 1);
+  for (int k = 0; tile < ntiles; tile += gridDim.x, ++k) {
+    const int st = k & 1;
+    const double* bx = smem + (size_t)st * 4 * tile_d;
+    const double* bp = bx + tile_d;
+    const double* bdx = bp + tile_d;
+    const double* bdp = bdx + tile_d;
+    mbar_wait(&bar[st], phase[st]);
+    phase[st] ^= 1u;
+    double t = 0.0;
+    for (int d = 0; d < dim; ++d) {
+      const double u = fsub(bx[d * 32 + lane], bp[d * 32 + lane]);  // _t0 = x[i] - p[i]
+      t = fadd(t, fmul(u, u));                                     // t = t + _t1
+    }
+    const double tt = fdiv(-t, t4);
+    const double e = exp(tt);
+    const double r2 = fadd(0.0, fmul(r1, e));
+    const double r3 = fadd(0.0, fdiv(r2, t4));
+    const double c = fadd(0.0, -r3);
+    const int64_t i = tile * 32 + lane;
+#pragma unroll 4
+    for (int d = dim - 1; d >= 0; --d) {
+      const double u = fsub(bx[d * 32 + lane], bp[d * 32 + lane]);
+      const double r6 = fadd(fadd(0.0, fmul(c, u)), fmul(u, c));
+      const int64_t o = (int64_t)d * ld + i;
+      dx[o] = fadd(bdx[d * 32 + lane], r6);   // _d_x[_i0] += _r6
+      dp[o] = fadd(bdp[d * 32 + lane], -r6);  // _d_p[_i0] += -_r6
+    }
+    __syncwarp();  // every lane is done with the stage before it is refilled
+    if (tile + 2 * (int64_t)gridDim.x < ntiles) issue(tile + 2 * (int64_t)gridDim.x, st);
+  }
+}
+
 // K2v: two points per lane with 16-byte (double2) accesses — a warp covers a
 // 64-point tile, each row access is one 512-byte segment.  Same per-point
 // arithmetic and order as K2 (W = 1), so each point's bits are K2's; the two
@@ -414,6 +494,32 @@ int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, con
   if (dim > (1 << 24)) return fail(ADC_E_ARG, "gaussnd: dim too large");
   double d_t9 = 0;
   d_t9 += (std::pow(2 * PI, -0.5) * std::pow(sigma, -0.5)) * 1.0;  // _d__t9 += _t8 * _r0
+  if (g_variant == 14) {  // experiment: K2t (TMA-streamed tiles)
+    const int64_t ntiles = n / 32;
+    const size_t smem = (size_t)dim * 32 * 8 * sizeof(double) + 2 * sizeof(uint64_t);
+    const bool ok = ld % 2 == 0 && ((((uintptr_t)x) | ((uintptr_t)p) | ((uintptr_t)dx) |
+                                     ((uintptr_t)dp)) & 15) == 0 && dim <= 104 &&
+                    smem <= 227 * 1024;
+    CUtensorMap mx, mp, mdx, mdp;
+    if (ok && ntiles > 0 && make_rows_tmap(&mx, x, ntiles * 32, dim, ld) == ADC_OK &&
+        make_rows_tmap(&mp, p, ntiles * 32, dim, ld) == ADC_OK &&
+        make_rows_tmap(&mdx, dx, ntiles * 32, dim, ld) == ADC_OK &&
+        make_rows_tmap(&mdp, dp, ntiles * 32, dim, ld) == ADC_OK) {
+      ADCB_CUDA(cudaFuncSetAttribute(gaussnd_tma_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const int64_t blocks = std::min<int64_t>(ntiles, (int64_t)sm_count());
+      gaussnd_tma_kernel<<<(unsigned)blocks, 32, smem, s>>>(mx, mp, mdx, mdp, dx, dp, ntiles,
+                                                           (int)dim, ld, t4, d_t9);
+      ADCB_CUDA(cudaGetLastError());
+      const int64_t done = ntiles * 32;
+      if (done == n) return ADC_OK;
+      g_variant = 3;
+      const int rc = launch_gaussnd_grad(n - done, dim, ld, x + done, p + done, sigma, dx + done,
+                                         dp + done, s);
+      g_variant = 14;
+      return rc;
+    }
+  }
   // Auto: K2v for dims whose u rows all fit its 52 KB stage (the dim-100
   // headline: 6.0 TB/s vs 5.8 for K2, the same bits per point).
   const bool vec2_auto = g_variant == 0 && dim <= 104;
@@ -468,7 +574,7 @@ int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, con
 }
 
 int gaussnd_set_variant(int v) {
-  if (v < 0 || v > 13) return fail(ADC_E_ARG, "gaussnd variant must be 0..13");
+  if (v < 0 || v > 14) return fail(ADC_E_ARG, "gaussnd variant must be 0..14");
   g_variant = v;
   return ADC_OK;
 }
