@@ -374,8 +374,21 @@ def bench_chi2(world, rank, local, dist, bins=100_000_000, passes=20, warm=3):
     # transport over the process group for --dist-backend gloo).  The pass,
     # the record all-gather and the fixed-order finalize run inside
     # libadc_b200, captured in one CUDA graph per pass kind.
-    comm = adc.Comm.from_torch("nccl" if BACKEND == "nccl" else "host") if world > 1 else None
-    plan = adc.Chi2Plan("gpoly", 6, h, comm=comm)
+    comm, transport = None, "none"
+    if world > 1:
+        # peer memory first (GPU-to-GPU stores + flags in the pass graph, no
+        # NCCL on the pass path); the library's NCCL communicator otherwise
+        for transport in (("peer", "nccl") if BACKEND == "nccl" else ("peer", "host")):
+            try:
+                comm = adc.Comm.from_torch(transport)
+                plan = adc.Chi2Plan("gpoly", 6, h, comm=comm)
+                break
+            except Exception:  # noqa: BLE001
+                comm = None
+        if comm is None:
+            raise RuntimeError("no multi-GPU transport")
+    else:
+        plan = adc.Chi2Plan("gpoly", 6, h)
     L = plan.layout
     R = adc.record_len(6, True)
     loc = torch.zeros(max(1, L.chunk_end - L.chunk_begin) * R, dtype=torch.float64, device=dev)
@@ -411,8 +424,11 @@ def bench_chi2(world, rank, local, dist, bins=100_000_000, passes=20, warm=3):
            "device_ms_per_rank_pass": statistics.median(kt),
            "bins_per_s_device": (L.bin_end - L.bin_begin) / (statistics.median(kt) * 1e-3),
            "collective": ("all-gather of chunk records inside libadc_b200 ("
-                          + ("ncclAllGather in the pass graph" if BACKEND == "nccl"
-                             else "host transport over gloo") + ")") if world > 1 else "none",
+                          + {"peer": "GPU-to-GPU stores into IPC-shared buffers + flags, in the "
+                                     "pass graph",
+                             "nccl": "ncclAllGather in the pass graph",
+                             "host": "host transport over gloo"}[transport] + ")")
+                          if world > 1 else "none",
            "chi2": c2,
            "roofline": chi2_roofline(L.bin_end - L.bin_begin, statistics.median(kt)),
            "numeric_provider_device_ms_per_rank_pass": statistics.median(nt[1:]),

@@ -266,7 +266,7 @@ int adc_cuda_chi2_set_precision(adc_chi2_plan* plan, int32_t mode);
  * (adc_cuda_chi2, _gradient, _multi, _gradient_multi, adc_cuda_fit) works on
  * a sharded plan exactly as on a whole-histogram plan.
  *
- * Two transports:
+ * Three transports (the third, peer memory, is declared below):
  *  - NCCL (the product path on NVLink/NVSwitch): ncclAllGather enqueued on the
  *    plan's stream right after the chunk kernel, captured into the same CUDA
  *    graph as the pass.  Rank 0 calls adc_nccl_unique_id and the caller
@@ -278,7 +278,7 @@ int adc_cuda_chi2_set_precision(adc_chi2_plan* plan, int32_t mode);
  */
 typedef struct adc_comm adc_comm;
 typedef int (*adc_allgather_fn)(void* ctx, const void* send, void* recv, size_t bytes);
-enum { ADC_COMM_NCCL = 1, ADC_COMM_HOST = 2 };
+enum { ADC_COMM_NCCL = 1, ADC_COMM_HOST = 2, ADC_COMM_PEER = 3 };
 int adc_nccl_unique_id(unsigned char id[128]);
 /* Collective over the world: every rank calls it with the same id, on the
  * device it will run its plan on (the current device). */
@@ -286,6 +286,16 @@ int adc_cuda_comm_init_nccl(adc_comm** comm, const unsigned char id[128], int32_
                             int32_t rank);
 int adc_comm_init_host(adc_comm** comm, int32_t world, int32_t rank, adc_allgather_fn fn,
                        void* ctx);
+/* Peer memory (no NCCL on the pass path): each plan's receive buffer is
+ * exported with CUDA IPC and opened by every rank (the bootstrap all-gather
+ * `fn` exchanges the 64-byte handles once, when a plan attaches the comm).
+ * A pass then publishes its chunk records straight into every peer's buffer
+ * from the GPU (NVLink stores), raises a system-scope flag per peer and
+ * waits for every peer's flag — one small kernel after the chunk kernel,
+ * captured in the pass's CUDA graph.  All ranks must live on one node (on
+ * distinct GPUs, or sharing one). */
+int adc_cuda_comm_init_peer(adc_comm** comm, int32_t world, int32_t rank, adc_allgather_fn fn,
+                            void* ctx);
 int adc_comm_destroy(adc_comm* comm);
 int adc_comm_info(const adc_comm* comm, int32_t* world, int32_t* rank, int32_t* kind);
 /* Attaches comm (NULL detaches) to a plan created with the same world/rank.

@@ -233,6 +233,12 @@ class Comm {
     check(adc_comm_init_host(&c, world, rank, fn, ctx));
     return Comm(c);
   }
+  // peer memory: fn only bootstraps the CUDA IPC handles of each plan
+  static Comm peer(int world, int rank, adc_allgather_fn fn, void* ctx) {
+    adc_comm* c = nullptr;
+    check(adc_cuda_comm_init_peer(&c, world, rank, fn, ctx));
+    return Comm(c);
+  }
   Comm(Comm&& o) noexcept : c_(o.c_) { o.c_ = nullptr; }
   Comm& operator=(Comm&& o) noexcept {
     std::swap(c_, o.c_);

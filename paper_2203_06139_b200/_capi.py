@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(HERE, "libadc_b200.so")
 # adc_status codes; 1..5 mirror adc::ErrorKind (proj/include/adc/diag.hpp:17-23).
 ERROR_KINDS = {1: "Semantic", 2: "Transform", 3: "Eval", 4: "Launch", 5: "Io", 6: "Cuda", 7: "Arg",
                8: "Nccl"}
-COMM_NCCL, COMM_HOST = 1, 2
+COMM_NCCL, COMM_HOST, COMM_PEER = 1, 2, 3
 # int (*adc_allgather_fn)(void* ctx, const void* send, void* recv, size_t bytes)
 ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                 ctypes.c_size_t)
@@ -103,6 +103,7 @@ SIGNATURES = {
     "adc_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
     "adc_cuda_comm_init_nccl": (ctypes.c_int, [ctypes.POINTER(_VP), ctypes.c_char_p, _I32, _I32]),
     "adc_comm_init_host": (ctypes.c_int, [ctypes.POINTER(_VP), _I32, _I32, ALLGATHER_FN, _VP]),
+    "adc_cuda_comm_init_peer": (ctypes.c_int, [ctypes.POINTER(_VP), _I32, _I32, ALLGATHER_FN, _VP]),
     "adc_comm_destroy": (ctypes.c_int, [_VP]),
     "adc_comm_info": (ctypes.c_int, [_VP, ctypes.POINTER(_I32), ctypes.POINTER(_I32),
                                      ctypes.POINTER(_I32)]),

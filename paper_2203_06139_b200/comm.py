@@ -16,7 +16,7 @@ import ctypes
 
 import numpy as np
 
-from ._capi import ALLGATHER_FN, COMM_HOST, COMM_NCCL, check, lib
+from ._capi import ALLGATHER_FN, COMM_HOST, COMM_NCCL, COMM_PEER, check, lib
 
 
 class Comm:
@@ -43,10 +43,8 @@ class Comm:
         check(lib.adc_cuda_comm_init_nccl(ctypes.byref(p), uid, world, rank))
         return cls(p, world, rank, COMM_NCCL)
 
-    @classmethod
-    def host(cls, world: int, rank: int, allgather) -> "Comm":
-        """allgather(send: float64 ndarray[n]) -> float64 ndarray[world * n], rank-major."""
-
+    @staticmethod
+    def _callback(world, allgather):
         def _cb(_ctx, send, recv, nbytes):
             try:
                 n = nbytes // 8
@@ -59,17 +57,34 @@ class Comm:
             except Exception:  # noqa: BLE001 — reported to the C side as a status
                 return 1
 
-        cb = ALLGATHER_FN(_cb)
+        return ALLGATHER_FN(_cb)
+
+    @classmethod
+    def host(cls, world: int, rank: int, allgather) -> "Comm":
+        """allgather(send: float64 ndarray[n]) -> float64 ndarray[world * n], rank-major."""
+        cb = cls._callback(world, allgather)
         p = ctypes.c_void_p()
         check(lib.adc_comm_init_host(ctypes.byref(p), world, rank, cb, None))
         return cls(p, world, rank, COMM_HOST, keep=cb)
 
     @classmethod
+    def peer(cls, world: int, rank: int, allgather) -> "Comm":
+        """Peer-memory transport: `allgather` (as for host()) only bootstraps the
+        CUDA IPC handles when a plan attaches; every pass then exchanges its
+        records GPU to GPU (NVLink stores + system-scope flags), no NCCL."""
+        import torch  # noqa: F401
+        cb = cls._callback(world, allgather)
+        p = ctypes.c_void_p()
+        check(lib.adc_cuda_comm_init_peer(ctypes.byref(p), world, rank, cb, None))
+        return cls(p, world, rank, COMM_PEER, keep=cb)
+
+    @classmethod
     def from_torch(cls, transport: str = "nccl") -> "Comm":
         """Builds a communicator over the initialised torch.distributed group:
         transport "nccl" = the library's own NCCL communicator (unique id
-        broadcast over the group), "host" = gloo/NCCL all_gather of host
-        buffers through the process group."""
+        broadcast over the group), "peer" = GPU-to-GPU stores into IPC-shared
+        buffers (the group only bootstraps the handles), "host" = an all-gather
+        of host buffers through the process group."""
         import torch
         import torch.distributed as dist
         world, rank = dist.get_world_size(), dist.get_rank()
@@ -79,11 +94,12 @@ class Comm:
             return cls.nccl(world, rank, obj[0])
 
         def allgather(mine):
-            t = torch.from_numpy(mine)
-            parts = [torch.empty_like(t) for _ in range(world)]
-            dist.all_gather(parts, t)
-            return torch.cat(parts).numpy()
+            objs = [None] * world
+            dist.all_gather_object(objs, mine)  # works over gloo and NCCL groups
+            return np.concatenate(objs)
 
+        if transport == "peer":
+            return cls.peer(world, rank, allgather)
         return cls.host(world, rank, allgather)
 
     def info(self):

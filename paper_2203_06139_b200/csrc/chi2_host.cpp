@@ -136,6 +136,7 @@ struct adc_chi2_plan {
   bool no_graph = false;  // the transport refused stream capture: enqueue directly
   // exchange / copy-back staging, sized once for the largest pass kind
   adc_comm* comm = nullptr;
+  PeerExchange peer;          // ADC_COMM_PEER: IPC-shared receive buffers
   size_t xcount = 0;          // doubles per rank the staging holds
   double* gather = nullptr;   // device [world][xcount] (NCCL)
   double* h_send = nullptr;   // pinned [xcount]  (host transport / single device)
@@ -220,6 +221,11 @@ int collect_enqueue(adc_chi2_plan* P, const double* dev, int R, int nb, cudaStre
   if (P->comm != nullptr && P->comm->kind == ADC_COMM_NCCL) {
     if (int rc = comm_allgather_enqueue(P->comm, dev, P->gather, count, s)) return rc;
     ADCB_CUDA(cudaMemcpyAsync(P->h_gather, P->gather, count * P->world * sizeof(double),
+                              cudaMemcpyDeviceToHost, s));
+  } else if (P->comm != nullptr && P->comm->kind == ADC_COMM_PEER) {
+    // publish into every rank's buffer over peer memory, signal, wait: no NCCL
+    if (int rc = peer_exchange_enqueue(&P->peer, dev, count, s)) return rc;
+    ADCB_CUDA(cudaMemcpyAsync(P->h_gather, P->peer.out, count * P->world * sizeof(double),
                               cudaMemcpyDeviceToHost, s));
   } else {
     ADCB_CUDA(cudaMemcpyAsync(P->h_send, dev, count * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -347,6 +353,11 @@ int alloc_staging(adc_chi2_plan* P) {
   ADCB_CUDA(cudaMallocHost(&P->h_send, P->xcount * sizeof(double)));
   ADCB_CUDA(cudaMallocHost(&P->h_gather, P->xcount * P->world * sizeof(double)));
   if (nccl) ADCB_CUDA(cudaMalloc(&P->gather, P->xcount * P->world * sizeof(double)));
+  if (P->comm != nullptr && P->comm->kind == ADC_COMM_PEER) {
+    if (int rc = peer_setup(P->comm, P->xcount, &P->peer)) return rc;
+  } else {
+    peer_release(&P->peer);
+  }
   return ADC_OK;
 }
 
@@ -444,8 +455,9 @@ extern "C" int adc_cuda_chi2_plan_set_comm(adc_chi2_plan* P, adc_comm* comm) {
   if (P == nullptr) return fail(ADC_E_ARG, "null plan");
   if (comm != nullptr && (comm->world != P->world || comm->rank != P->rank))
     return fail(ADC_E_ARG, "communicator world/rank differ from the plan's");
-  if (comm != nullptr && comm->kind == ADC_COMM_NCCL && comm->device != P->device)
-    return fail(ADC_E_ARG, "NCCL communicator is on another device than the plan");
+  if (comm != nullptr && (comm->kind == ADC_COMM_NCCL || comm->kind == ADC_COMM_PEER) &&
+      comm->device != P->device)
+    return fail(ADC_E_ARG, "communicator is on another device than the plan");
   if (comm == nullptr && P->world > 1)
     return fail(ADC_E_ARG, "a sharded plan keeps its communicator");
   ADCB_CUDA(cudaSetDevice(P->device));
@@ -465,6 +477,7 @@ extern "C" int adc_cuda_chi2_plan_destroy(adc_chi2_plan* P) {
   if (P->h_send) cudaFreeHost(P->h_send);
   if (P->h_gather) cudaFreeHost(P->h_gather);
   if (P->gather) cudaFree(P->gather);
+  peer_release(&P->peer);
   if (P->qmulti) cudaFree(P->qmulti);
   if (P->h_qmulti) cudaFreeHost(P->h_qmulti);
   if (P->tile_ws_multi) cudaFree(P->tile_ws_multi);

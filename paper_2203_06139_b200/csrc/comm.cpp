@@ -116,6 +116,25 @@ extern "C" int adc_comm_init_host(adc_comm** out, int32_t world, int32_t rank,
   return ADC_OK;
 }
 
+extern "C" int adc_cuda_comm_init_peer(adc_comm** out, int32_t world, int32_t rank,
+                                       adc_allgather_fn fn, void* ctx) {
+  clear_error();
+  if (out == nullptr || fn == nullptr) return fail(ADC_E_ARG, "null argument");
+  *out = nullptr;
+  if (world <= 0 || rank < 0 || rank >= world) return fail(ADC_E_ARG, "bad rank/world");
+  if (!device_present()) return fail(ADC_E_CUDA, "no CUDA device: the B200 engine has no CPU fallback");
+  adc_comm* C = new (std::nothrow) adc_comm();
+  if (C == nullptr) return fail(ADC_E_ARG, "out of host memory");
+  C->kind = ADC_COMM_PEER;
+  C->world = world;
+  C->rank = rank;
+  C->fn = fn;
+  C->ctx = ctx;
+  cudaGetDevice(&C->device);
+  *out = C;
+  return ADC_OK;
+}
+
 extern "C" int adc_comm_destroy(adc_comm* C) {
   if (C == nullptr) return ADC_OK;
   if (C->nccl != nullptr) nccl()->comm_destroy(static_cast<ncclComm_t>(C->nccl));
@@ -139,6 +158,125 @@ int comm_allgather_enqueue(adc_comm* C, const double* send, double* recv, size_t
   ncclResult_t r =
       nccl()->all_gather(send, recv, count, ncclDouble, static_cast<ncclComm_t>(C->nccl), s);
   if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
+  return ADC_OK;
+}
+
+// ---- peer-memory exchange ------------------------------------------------------
+namespace {
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// One CTA: publish local[count] into every rank's slot [rank] of the pass's
+// parity, release a flag on every rank, wait for every rank's flag, then
+// compact the received slots into out[world][count].  The pass counter makes
+// the flags monotonic; the parity double-buffers the slots (a rank can only
+// run one pass ahead: its next pass needs every peer's publish of this one,
+// which each peer issues after it has read this pass's slots).
+__global__ void __launch_bounds__(256) peer_exchange_kernel(
+    const double* __restrict__ local, size_t count, double* const* peer_gather,
+    unsigned long long* const* peer_flags, double* own_gather, unsigned long long* own_flags,
+    unsigned long long* seq, int world, int rank, size_t xcount, double* __restrict__ out) {
+  __shared__ unsigned long long s_q;
+  if (threadIdx.x == 0) s_q = *seq + 1;
+  __syncthreads();
+  const unsigned long long q = s_q;
+  const size_t par = q & 1;
+  for (int r = 0; r < world; ++r) {
+    double* dst = peer_gather[r] + (par * world + rank) * xcount;
+    for (size_t k = threadIdx.x; k < count; k += blockDim.x) dst[k] = local[k];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x < world) st_release_sys(peer_flags[threadIdx.x] + rank, q);
+  if (threadIdx.x < world)
+    while (ld_acquire_sys(own_flags + threadIdx.x) < q) {
+    }
+  __syncthreads();
+  for (int r = 0; r < world; ++r) {
+    const double* src = own_gather + (par * world + r) * xcount;
+    for (size_t k = threadIdx.x; k < count; k += blockDim.x) out[(size_t)r * count + k] = src[k];
+  }
+  if (threadIdx.x == 0) *seq = q;
+}
+}  // namespace
+
+int peer_setup(adc_comm* C, size_t xcount, PeerExchange* X) {
+  peer_release(X);
+  X->world = C->world;
+  X->rank = C->rank;
+  X->xcount = xcount;
+  const int W = C->world;
+  ADCB_CUDA(cudaMalloc(&X->gather, 2 * (size_t)W * xcount * sizeof(double)));
+  ADCB_CUDA(cudaMalloc(&X->flags, (size_t)W * sizeof(unsigned long long)));
+  ADCB_CUDA(cudaMemset(X->flags, 0, (size_t)W * sizeof(unsigned long long)));
+  ADCB_CUDA(cudaMalloc(&X->seq, sizeof(unsigned long long)));
+  ADCB_CUDA(cudaMemset(X->seq, 0, sizeof(unsigned long long)));
+  ADCB_CUDA(cudaMalloc(&X->out, (size_t)W * xcount * sizeof(double)));
+  ADCB_CUDA(cudaMalloc(&X->peer_gather, (size_t)W * sizeof(double*)));
+  ADCB_CUDA(cudaMalloc(&X->peer_flags, (size_t)W * sizeof(unsigned long long*)));
+  ADCB_CUDA(cudaDeviceSynchronize());  // flags zeroed before any peer can write them
+  // bootstrap: every rank's two IPC handles
+  cudaIpcMemHandle_t mine[2];
+  ADCB_CUDA(cudaIpcGetMemHandle(&mine[0], X->gather));
+  ADCB_CUDA(cudaIpcGetMemHandle(&mine[1], X->flags));
+  std::vector<cudaIpcMemHandle_t> all(2 * (size_t)W);
+  const int rc = C->fn(C->ctx, mine, all.data(), sizeof(mine));
+  if (rc != 0) return fail(ADC_E_NCCL, "peer bootstrap all-gather failed (" + std::to_string(rc) + ")");
+  std::vector<double*> pg(W);
+  std::vector<unsigned long long*> pf(W);
+  for (int r = 0; r < W; ++r) {
+    if (r == C->rank) {
+      pg[r] = X->gather;
+      pf[r] = X->flags;
+      continue;
+    }
+    void* g = nullptr;
+    void* f = nullptr;
+    ADCB_CUDA(cudaIpcOpenMemHandle(&g, all[2 * r], cudaIpcMemLazyEnablePeerAccess));
+    X->opened.push_back(g);
+    ADCB_CUDA(cudaIpcOpenMemHandle(&f, all[2 * r + 1], cudaIpcMemLazyEnablePeerAccess));
+    X->opened.push_back(f);
+    pg[r] = static_cast<double*>(g);
+    pf[r] = static_cast<unsigned long long*>(f);
+  }
+  ADCB_CUDA(cudaMemcpy(X->peer_gather, pg.data(), (size_t)W * sizeof(double*),
+                       cudaMemcpyHostToDevice));
+  ADCB_CUDA(cudaMemcpy(X->peer_flags, pf.data(), (size_t)W * sizeof(unsigned long long*),
+                       cudaMemcpyHostToDevice));
+  // every rank has opened every buffer before any pass may write into it
+  double token = 0.0;
+  std::vector<double> tokens(W);
+  if (C->fn(C->ctx, &token, tokens.data(), sizeof(double)) != 0)
+    return fail(ADC_E_NCCL, "peer bootstrap barrier failed");
+  return ADC_OK;
+}
+
+void peer_release(PeerExchange* X) {
+  for (void* p : X->opened) cudaIpcCloseMemHandle(p);
+  X->opened.clear();
+  if (X->gather) cudaFree(X->gather);
+  if (X->flags) cudaFree(X->flags);
+  if (X->seq) cudaFree(X->seq);
+  if (X->out) cudaFree(X->out);
+  if (X->peer_gather) cudaFree(X->peer_gather);
+  if (X->peer_flags) cudaFree(X->peer_flags);
+  X->gather = X->out = nullptr;
+  X->flags = X->seq = nullptr;
+  X->peer_gather = nullptr;
+  X->peer_flags = nullptr;
+}
+
+int peer_exchange_enqueue(PeerExchange* X, const double* local, size_t count, cudaStream_t s) {
+  if (count > X->xcount) return fail(ADC_E_ARG, "peer exchange: record block too large");
+  peer_exchange_kernel<<<1, 256, 0, s>>>(local, count, X->peer_gather, X->peer_flags, X->gather,
+                                         X->flags, X->seq, X->world, X->rank, X->xcount, X->out);
+  ADCB_CUDA(cudaGetLastError());
   return ADC_OK;
 }
 

@@ -528,7 +528,8 @@ int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, con
     const bool ok = ld % 2 == 0 && ((((uintptr_t)x) | ((uintptr_t)p) | ((uintptr_t)dx) |
                                      ((uintptr_t)dp)) & 15) == 0;
     if (ok && ntiles > 0) {
-      const size_t budget = g_variant == 11 ? 104 * 1024 : 52 * 1024;
+      size_t budget = g_variant == 11 ? 104 * 1024 : 52 * 1024;
+      if (const char* e = getenv("ADC_K2V_STAGE_KB")) budget = (size_t)atoi(e) * 1024;  // experiment
       const int dstage = (int)std::min<int64_t>(dim, budget / 512);
       const size_t smem = (size_t)dstage * 512;
       auto k = g_variant == 12 ? gaussnd_vec2_kernel<8>

@@ -5,7 +5,8 @@ the fit loop are bitwise identical to the single-device plan on every rank.
 
 The box has one GPU: NCCL is exercised at world size 1 (same enqueue and
 graph-capture code as at N > 1), and world sizes 2 and 3 run as separate
-processes sharing the GPU over the host-callback transport (gloo)."""
+processes sharing the GPU over the host-callback transport (gloo) and over the
+peer-memory transport (CUDA IPC buffers, GPU-side publish + flags)."""
 import os
 import socket
 
@@ -71,6 +72,16 @@ def test_nccl_world1_bitwise_equals_single_device():
     comm.close()
 
 
+def test_peer_comm_world1_bitwise_equals_single_device():
+    counts, ev, q, qs = _problem(bins=900_001, seed=12)
+    ref = _single_device(counts, ev, q, qs)
+    comm = adc.Comm.peer(1, 0, lambda a: a.copy())
+    h = adc.Histogram(counts.size, -5.0, 5.0, ev, counts)
+    got = _results(adc.Chi2Plan("gpoly", 6, h, comm=comm), adc.FitEngine("gpoly", 6, comm=comm),
+                   h, q, qs)
+    assert got == ref
+
+
 def test_host_comm_world1_identity():
     counts, ev, q, qs = _problem(bins=700_001, seed=8)
     ref = _single_device(counts, ev, q, qs)
@@ -104,7 +115,7 @@ def test_failing_host_callback_is_reported():
     assert e.value.kind == "Nccl"
 
 
-def _worker(rank, world, port, out_q):
+def _worker(rank, world, port, out_q, transport="host"):
     import sys
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
@@ -115,7 +126,7 @@ def _worker(rank, world, port, out_q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         counts, ev, q, qs = _problem()
-        comm = adc_.Comm.from_torch("host")
+        comm = adc_.Comm.from_torch(transport)
         h = adc_.Histogram(counts.size, -5.0, 5.0, ev, counts)
         L = adc_.chi2_layout(counts.size, world, rank)
         shard = torch.from_numpy(counts[L.bin_begin:L.bin_end].copy()).cuda()
@@ -134,15 +145,20 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_ranks_share_gpu_host_comm_bitwise(world):
+@pytest.mark.parametrize("world,transport", [(2, "host"), (3, "host"), (2, "peer"), (3, "peer")])
+def test_ranks_share_gpu_bitwise(world, transport):
+    """Several ranks on the one GPU: the host transport (gloo all-gather) and
+    the peer transport (CUDA IPC buffers on the device, GPU-side publish and
+    flags — the multi-GPU path without NCCL) both give every rank the
+    single-device bits."""
     import torch.multiprocessing as mp
     counts, ev, q, qs = _problem()
     ref = _single_device(counts, ev, q, qs)
     ctx = mp.get_context("spawn")
     out_q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, out_q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, out_q, transport))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = [out_q.get(timeout=600) for _ in procs]
