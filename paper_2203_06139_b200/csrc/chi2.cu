@@ -28,6 +28,7 @@
 #include "chi2_internal.h"
 #include "common.cuh"
 #include "fastmath.cuh"
+#include "peer.cuh"
 
 namespace adcb {
 
@@ -567,12 +568,24 @@ struct LinMerge {
   int c0_pos = -1, g0_pos = -1, g1_pos = -1;
 };
 
+// pub (optional, the peer-memory transport): the kernel that reduces the
+// chunks also publishes them — each CTA stores its record straight into every
+// rank's receive slot as it is produced, and the last CTA to finish raises the
+// flags, waits for every rank and compacts (peer.cuh): the reduction and the
+// collective are one kernel.
 __global__ void __launch_bounds__(kChunkThreads) chi2_chunk_kernel(
     const double* __restrict__ tile_ws, int64_t ntiles, int R, int chunk_tiles,
-    double* __restrict__ records, LinMerge lm = LinMerge{}) {
+    double* __restrict__ records, LinMerge lm = LinMerge{}, PeerPublish pub = PeerPublish{}) {
   const int64_t chunk = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t t0 = chunk * chunk_tiles;
+  const bool publish = pub.peer_gather != nullptr;  // uniform over the grid
+  __shared__ unsigned long long s_q;
+  __shared__ bool s_last;
+  if (publish) {
+    if (threadIdx.x == 0) s_q = *pub.seq + 1;
+    __syncthreads();
+  }
   for (int v = warp; v < R; v += kChunkThreads / 32) {
     double part[4];
 #pragma unroll
@@ -590,7 +603,21 @@ __global__ void __launch_bounds__(kChunkThreads) chi2_chunk_kernel(
       else if (lm.g0_pos >= 0 && v >= lm.g0_pos && v < lm.g0_pos + L) a = a + l[v - lm.g0_pos];
       else if (lm.g1_pos >= 0 && v >= lm.g1_pos && v < lm.g1_pos + L) a = a + l[L + v - lm.g1_pos];
     }
-    if (lane == 0) records[chunk * R + v] = a;
+    if (lane == 0) {
+      records[chunk * R + v] = a;
+      if (publish)
+        for (int r = 0; r < pub.world; ++r) peer_slot(pub, r, s_q)[chunk * R + v] = a;
+    }
+  }
+  if (publish) {
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(pub.done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last) {
+      if (threadIdx.x == 0) *pub.done = 0u;
+      peer_signal_wait_compact(pub, s_q);
+    }
   }
 }
 
@@ -646,7 +673,7 @@ static void launch_tiles_m(const Chi2Pass& P, bool grad, bool fast, bool num, in
 
 int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast,
                  int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin,
-                 bool numeric) {
+                 bool numeric, const PeerPublish* pub) {
 
   const int64_t ntiles = P.tile_end - P.tile_begin;
   if (ntiles <= 0) return ADC_OK;
@@ -678,8 +705,8 @@ int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast,
     lm.g0_pos = 4 + lin0;
     lm.g1_pos = 4 + np + lin0;
   }
-  chi2_chunk_kernel<<<(unsigned)nchunks, kChunkThreads, 0, s>>>(P.tile_ws, ntiles, R,
-                                                               (int)chunk_tiles, records, lm);
+  chi2_chunk_kernel<<<(unsigned)nchunks, kChunkThreads, 0, s>>>(
+      P.tile_ws, ntiles, R, (int)chunk_tiles, records, lm, pub ? *pub : PeerPublish{});
   ADCB_CUDA(cudaGetLastError());
   return ADC_OK;
 }

@@ -215,7 +215,8 @@ int require_whole_or_comm(const adc_chi2_plan* P) {
 // stream s; after the stream is synchronised, collect_finish runs the host
 // transport (if any) and compacts to P->full = [nb][nchunks][R] in global
 // chunk order — the same bytes whatever the world size.
-int collect_enqueue(adc_chi2_plan* P, const double* dev, int R, int nb, cudaStream_t s) {
+int collect_enqueue(adc_chi2_plan* P, const double* dev, int R, int nb, cudaStream_t s,
+                    bool published = false) {
   const size_t count = (size_t)nb * P->maxc * R;
   if (count > P->xcount) return fail(ADC_E_ARG, "exchange staging too small");
   if (P->comm != nullptr && P->comm->kind == ADC_COMM_NCCL) {
@@ -224,7 +225,9 @@ int collect_enqueue(adc_chi2_plan* P, const double* dev, int R, int nb, cudaStre
                               cudaMemcpyDeviceToHost, s));
   } else if (P->comm != nullptr && P->comm->kind == ADC_COMM_PEER) {
     // publish into every rank's buffer over peer memory, signal, wait: no NCCL
-    if (int rc = peer_exchange_enqueue(&P->peer, dev, count, s)) return rc;
+    // (already done by the chunk kernel itself when `published`)
+    if (!published)
+      if (int rc = peer_exchange_enqueue(&P->peer, dev, count, s)) return rc;
     ADCB_CUDA(cudaMemcpyAsync(P->h_gather, P->peer.out, count * P->world * sizeof(double),
                               cudaMemcpyDeviceToHost, s));
   } else {
@@ -277,11 +280,17 @@ int ensure_lin(adc_chi2_plan* P, cudaStream_t s) {
 // q upload + tile/chunk kernels + exchange / copy back, on P->stream.
 int enqueue_pass(adc_chi2_plan* P, int grad) {
   ADCB_CUDA(cudaMemcpyAsync(P->qdev, P->h_q, qdev_bytes(), cudaMemcpyHostToDevice, P->stream));
+  const int R = adc_chi2_record_len(P->np, grad);
+  // peer transport: the chunk kernel publishes its records itself (fused
+  // reduction + collective); a rank without chunks uses the exchange kernel
+  const bool fuse = P->comm != nullptr && P->comm->kind == ADC_COMM_PEER && local_chunks(P) > 0;
+  PeerPublish pub;
+  if (fuse) pub = peer_publish_args(&P->peer, (size_t)P->maxc * R);
   if (int rc = chi2_enqueue(make_pass(P), P->model, P->np, grad != 0, P->fast != 0,
                             P->L.chunk_tiles, P->records, P->stream, P->lin,
-                            grad != 0 && numeric(P)))
+                            grad != 0 && numeric(P), fuse ? &pub : nullptr))
     return rc;
-  return collect_enqueue(P, P->records, adc_chi2_record_len(P->np, grad), 1, P->stream);
+  return collect_enqueue(P, P->records, R, 1, P->stream, fuse);
 }
 
 int build_graph(adc_chi2_plan* P, int grad) {

@@ -6,6 +6,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include "peer.cuh"
+
 namespace adcb {
 
 constexpr int kMaxNp = 24;
@@ -26,9 +28,10 @@ struct Chi2Pass {
 // lin: per-chunk q-independent basis sums from chi2_lin_enqueue (gradient
 // passes of models with linear parameters; nullptr otherwise).
 // numeric: GradientProvider::Numeric (central differences of the model).
+// pub: publish the chunk records over peer memory from the chunk kernel.
 int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast,
                  int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin,
-                 bool numeric = false);
+                 bool numeric = false, const PeerPublish* pub = nullptr);
 int chi2_lin_count(int model, int np);  // L: number of linear parameters
 // Once per plan: ic = [c > 0]/c into icounts_local (this rank's bins, indexed
 // from bin_begin), then [G0_lin[L], G1_lin[L], C0] per local chunk into

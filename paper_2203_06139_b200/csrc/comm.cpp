@@ -12,6 +12,7 @@
 
 #include "comm_internal.h"
 #include "common.cuh"
+#include "peer.cuh"
 
 using namespace adcb;
 
@@ -163,48 +164,42 @@ int comm_allgather_enqueue(adc_comm* C, const double* send, double* recv, size_t
 
 // ---- peer-memory exchange ------------------------------------------------------
 namespace {
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// One CTA: publish local[count] into every rank's slot [rank] of the pass's
-// parity, release a flag on every rank, wait for every rank's flag, then
-// compact the received slots into out[world][count].  The pass counter makes
-// the flags monotonic; the parity double-buffers the slots (a rank can only
-// run one pass ahead: its next pass needs every peer's publish of this one,
-// which each peer issues after it has read this pass's slots).
-__global__ void __launch_bounds__(256) peer_exchange_kernel(
-    const double* __restrict__ local, size_t count, double* const* peer_gather,
-    unsigned long long* const* peer_flags, double* own_gather, unsigned long long* own_flags,
-    unsigned long long* seq, int world, int rank, size_t xcount, double* __restrict__ out) {
+// One CTA: publish local[count] into every rank's slot, then signal / wait /
+// compact (peer.cuh).  The pass counter makes the flags monotonic; the parity
+// double-buffers the slots (a rank can only run one pass ahead: its next pass
+// needs every peer's publish of this one, which each peer issues after it has
+// read this pass's slots).
+__global__ void __launch_bounds__(256) peer_exchange_kernel(const double* __restrict__ local,
+                                                            PeerPublish pp) {
   __shared__ unsigned long long s_q;
-  if (threadIdx.x == 0) s_q = *seq + 1;
+  if (threadIdx.x == 0) s_q = *pp.seq + 1;
   __syncthreads();
   const unsigned long long q = s_q;
-  const size_t par = q & 1;
-  for (int r = 0; r < world; ++r) {
-    double* dst = peer_gather[r] + (par * world + rank) * xcount;
-    for (size_t k = threadIdx.x; k < count; k += blockDim.x) dst[k] = local[k];
+  for (int r = 0; r < pp.world; ++r) {
+    double* dst = peer_slot(pp, r, q);
+    for (size_t k = threadIdx.x; k < pp.count; k += blockDim.x) dst[k] = local[k];
   }
   __threadfence_system();
   __syncthreads();
-  if (threadIdx.x < world) st_release_sys(peer_flags[threadIdx.x] + rank, q);
-  if (threadIdx.x < world)
-    while (ld_acquire_sys(own_flags + threadIdx.x) < q) {
-    }
-  __syncthreads();
-  for (int r = 0; r < world; ++r) {
-    const double* src = own_gather + (par * world + r) * xcount;
-    for (size_t k = threadIdx.x; k < count; k += blockDim.x) out[(size_t)r * count + k] = src[k];
-  }
-  if (threadIdx.x == 0) *seq = q;
+  peer_signal_wait_compact(pp, q);
 }
 }  // namespace
+
+PeerPublish peer_publish_args(PeerExchange* X, size_t count) {
+  PeerPublish pp;
+  pp.peer_gather = X->peer_gather;
+  pp.peer_flags = X->peer_flags;
+  pp.own_gather = X->gather;
+  pp.own_flags = X->flags;
+  pp.seq = X->seq;
+  pp.done = X->done;
+  pp.out = X->out;
+  pp.world = X->world;
+  pp.rank = X->rank;
+  pp.xcount = X->xcount;
+  pp.count = count;
+  return pp;
+}
 
 int peer_setup(adc_comm* C, size_t xcount, PeerExchange* X) {
   peer_release(X);
@@ -217,6 +212,8 @@ int peer_setup(adc_comm* C, size_t xcount, PeerExchange* X) {
   ADCB_CUDA(cudaMemset(X->flags, 0, (size_t)W * sizeof(unsigned long long)));
   ADCB_CUDA(cudaMalloc(&X->seq, sizeof(unsigned long long)));
   ADCB_CUDA(cudaMemset(X->seq, 0, sizeof(unsigned long long)));
+  ADCB_CUDA(cudaMalloc(&X->done, sizeof(unsigned int)));
+  ADCB_CUDA(cudaMemset(X->done, 0, sizeof(unsigned int)));
   ADCB_CUDA(cudaMalloc(&X->out, (size_t)W * xcount * sizeof(double)));
   ADCB_CUDA(cudaMalloc(&X->peer_gather, (size_t)W * sizeof(double*)));
   ADCB_CUDA(cudaMalloc(&X->peer_flags, (size_t)W * sizeof(unsigned long long*)));
@@ -263,6 +260,8 @@ void peer_release(PeerExchange* X) {
   if (X->gather) cudaFree(X->gather);
   if (X->flags) cudaFree(X->flags);
   if (X->seq) cudaFree(X->seq);
+  if (X->done) cudaFree(X->done);
+  X->done = nullptr;
   if (X->out) cudaFree(X->out);
   if (X->peer_gather) cudaFree(X->peer_gather);
   if (X->peer_flags) cudaFree(X->peer_flags);
@@ -274,8 +273,7 @@ void peer_release(PeerExchange* X) {
 
 int peer_exchange_enqueue(PeerExchange* X, const double* local, size_t count, cudaStream_t s) {
   if (count > X->xcount) return fail(ADC_E_ARG, "peer exchange: record block too large");
-  peer_exchange_kernel<<<1, 256, 0, s>>>(local, count, X->peer_gather, X->peer_flags, X->gather,
-                                         X->flags, X->seq, X->world, X->rank, X->xcount, X->out);
+  peer_exchange_kernel<<<1, 256, 0, s>>>(local, peer_publish_args(X, count));
   ADCB_CUDA(cudaGetLastError());
   return ADC_OK;
 }

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "adc_cuda.h"
+#include "peer.cuh"
 
 struct adc_comm {
   int kind = 0;  // ADC_COMM_NCCL / ADC_COMM_HOST
@@ -27,12 +28,14 @@ struct PeerExchange {
   double* gather = nullptr;               // own [2][world][xcount] (IPC-exported)
   unsigned long long* flags = nullptr;    // own [world] (IPC-exported)
   unsigned long long* seq = nullptr;      // own pass counter
+  unsigned int* done = nullptr;           // CTA arrivals of a fused publish
   double* out = nullptr;                  // own [world][count] compacted result
   double** peer_gather = nullptr;         // device array [world] of peers' gather bases
   unsigned long long** peer_flags = nullptr;  // device array [world] of peers' flag bases
   std::vector<void*> opened;              // IPC mappings to close
 };
 int peer_setup(adc_comm* C, size_t xcount, PeerExchange* X);
+PeerPublish peer_publish_args(PeerExchange* X, size_t count);
 void peer_release(PeerExchange* X);
 // Publishes local[count] into every rank's slot [my rank], signals, waits for
 // every rank's signal, and leaves the [world][count] result in X->out.
