@@ -187,6 +187,30 @@ def launch(kernel: str, cfg: LaunchConfig, buffers: BufferSet,
     return LaunchStats(active=cfg.n, idle=cfg.grid_dim * cfg.block_dim - cfg.n)
 
 
+def _soa_ld(arrays, ld):
+    """Leading dimension (elements between dims) shared by the SoA buffers:
+    each must be (dim, n) float64 with unit point stride and the same row
+    stride (views with a row stride > n, e.g. x[:, a:b], are fine)."""
+    strides = set()
+    for a in arrays:
+        if a is None:
+            continue
+        if _is_torch(a):
+            if str(a.dtype) != "torch.float64" or a.dim() != 2 or (a.shape[1] > 1 and a.stride(1) != 1):
+                raise AdcError("Launch", "SoA buffers must be float64 (dim, n) with unit point stride")
+            strides.add(a.stride(0))
+        else:
+            if a.dtype != np.float64 or a.ndim != 2 or (a.shape[1] > 1 and a.strides[1] != 8):
+                raise AdcError("Launch", "SoA buffers must be float64 (dim, n) with unit point stride")
+            strides.add(a.strides[0] // 8)
+    if len(strides) != 1:
+        raise AdcError("Launch", "SoA buffers must share one row stride")
+    stride = strides.pop()
+    if ld is not None and ld != stride:
+        raise AdcError("Launch", f"ld {ld} differs from the buffers' row stride {stride}")
+    return stride
+
+
 def launch_batch(grad_fn: str, x, p, sigma: float, dx, dp, ld: int | None = None,
                  callee_fingerprint: int | None = None):
     """Batched per-point gradient over structure-of-arrays buffers of shape
@@ -197,7 +221,7 @@ def launch_batch(grad_fn: str, x, p, sigma: float, dx, dp, ld: int | None = None
     fp = _fingerprints()[grad_fn] if callee_fingerprint is None else callee_fingerprint
     registry_find(grad_fn, fp)
     dim, n = x.shape
-    ld = n if ld is None else ld
+    ld = _soa_ld((x, p, dx, dp), ld)
     if _is_torch(x):
         check(lib.adc_cuda_gaussnd_grad(n, dim, ld, dptr(x), dptr(p), float(sigma), dptr(dx),
                                         dptr(dp), _stream_of(x)))
@@ -220,9 +244,9 @@ def launch_batch_shared_p(grad_fn: str, x, p, sigma: float, dx, dp,
     fp = _fingerprints()[grad_fn] if callee_fingerprint is None else callee_fingerprint
     registry_find(grad_fn, fp)
     dim, n = x.shape
-    ld = n if ld is None else ld
     if not _is_torch(x):
         raise AdcError("Launch", "launch_batch_shared_p takes device (CUDA tensor) buffers")
+    ld = _soa_ld((x, dx), ld)
     check(lib.adc_cuda_gaussnd_grad_shared_p(n, dim, ld, dptr(x), dptr(p), float(sigma),
                                              dptr(dx) if dx is not None else None, dptr(dp),
                                              1 if opts.unsafe else 0, _stream_of(x)))

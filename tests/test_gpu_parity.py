@@ -522,3 +522,22 @@ def test_gaussnd_shared_p_large_and_refusal(restate):
                               adc.LaunchOptions(unsafe=True))
     tot, ab = restate.gaussnd_shared_p_dp_compensated(np.ascontiguousarray(x), p, 1.3)
     assert np.all(np.abs(host(dp) - tot) <= 1e-12 * ab)
+
+
+def test_gaussnd_strided_views(restate):
+    # a (dim, n) view of a wider SoA buffer: the row stride comes from the view
+    dim, n, big = 50, 3000, 3200
+    x, p = synth.points_nd(dim, big, seed=44)
+    X, P = t(x), t(p)
+    DX = torch.zeros_like(X)
+    DP = torch.zeros_like(X)
+    adc.launch_batch("gaussnd_grad_0_1", X[:, 64:64 + n], P[:, 64:64 + n], 1.3,
+                     DX[:, 64:64 + n], DP[:, 64:64 + n])
+    ox, op = np.zeros((dim, n)), np.zeros((dim, n))
+    restate.gaussnd_grad(np.ascontiguousarray(x[:, 64:64 + n]),
+                         np.ascontiguousarray(p[:, 64:64 + n]), 1.3, ox, op)
+    hx = host(DX)
+    assert rel_err(hx[:, 64:64 + n], ox).max() <= REL
+    assert np.all(hx[:, :64] == 0) and np.all(hx[:, 64 + n:] == 0)
+    with pytest.raises(adc.AdcError):
+        adc.launch_batch("gaussnd_grad_0_1", X[:, ::2], P[:, ::2], 1.3, DX[:, ::2], DP[:, ::2])
