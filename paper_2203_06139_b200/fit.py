@@ -124,6 +124,8 @@ class Chi2Plan:
         counts = h.counts if _shard is None else _shard
         if not hasattr(counts, "is_cuda"):
             counts = torch.from_numpy(np.ascontiguousarray(counts, dtype=np.float64)).cuda()
+        elif not counts.is_cuda or counts.dtype != torch.float64 or not counts.is_contiguous():
+            counts = counts.to(device="cuda", dtype=torch.float64).contiguous()
         self.counts = counts  # keep alive
         self._p = ctypes.c_void_p()
         stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
