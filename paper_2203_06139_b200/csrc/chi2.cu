@@ -400,6 +400,8 @@ __host__ __device__ constexpr int multi_ilp() {
 template <class M>
 __global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P, int ncand) {
   constexpr int G = kMultiGroup, CG = multi_ilp<M>();
+  if (P.ncand_dev != nullptr) ncand = *P.ncand_dev;  // set on the device (fit graph)
+  if ((int)blockIdx.y * G >= ncand) return;           // uniform over the CTA
   __shared__ QDev Q[G];
   __shared__ double red[kTileThreads / 32][3 * G + 1];
   __shared__ double tab[64];
@@ -575,7 +577,9 @@ struct LinMerge {
 // collective are one kernel.
 __global__ void __launch_bounds__(kChunkThreads) chi2_chunk_kernel(
     const double* __restrict__ tile_ws, int64_t ntiles, int R, int chunk_tiles,
-    double* __restrict__ records, LinMerge lm = LinMerge{}, PeerPublish pub = PeerPublish{}) {
+    double* __restrict__ records, LinMerge lm = LinMerge{}, PeerPublish pub = PeerPublish{},
+    const int* ncand_dev = nullptr) {
+  if (ncand_dev != nullptr) R = 1 + 3 * *ncand_dev;  // multi records sized on the device
   const int64_t chunk = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t t0 = chunk * chunk_tiles;
@@ -772,8 +776,8 @@ int chi2_multi_enqueue(const Chi2Pass& P, int model, int np, int ncand,
   lm.lin = lin;
   lm.L = chi2_lin_count(model, np);
   lm.c0_pos = 0;
-  chi2_chunk_kernel<<<(unsigned)nchunks, kChunkThreads, 0, s>>>(P.tile_ws, ntiles, R,
-                                                               (int)chunk_tiles, records, lm);
+  chi2_chunk_kernel<<<(unsigned)nchunks, kChunkThreads, 0, s>>>(
+      P.tile_ws, ntiles, R, (int)chunk_tiles, records, lm, PeerPublish{}, P.ncand_dev);
   ADCB_CUDA(cudaGetLastError());
   return ADC_OK;
 }

@@ -16,6 +16,7 @@
 
 #include "chi2_internal.h"
 #include "comm_internal.h"
+#include "fit_device.h"
 #include "common.cuh"
 
 using namespace adcb;
@@ -149,6 +150,14 @@ struct adc_chi2_plan {
   double* records_multi = nullptr;  // [maxc][1 + 3 kMultiMax]
   int64_t multi_passes = 0;
   double* grad_multi_records = nullptr;  // [kMultiMax][maxc][R] (adc_cuda_chi2_gradient_multi)
+  // device-resident fit iteration (fit_device.cu): one graph per iteration
+  FitDevState* fit_st = nullptr;   // device
+  FitDevState* h_fit_st = nullptr; // pinned
+  double* fit_scratch = nullptr;
+  int* ncand_dev = nullptr;
+  cudaGraphExec_t fit_graph = nullptr;
+  cudaEvent_t fit_ev[2] = {nullptr, nullptr};
+  FitDevConst fit_const{};
   // q-independent basis sums of the linear parameters (chi2_lin_enqueue)
   double* lin = nullptr;      // per local chunk [G0_lin[L], G1_lin[L], C0]
   double* icounts = nullptr;  // [c > 0]/c for this rank's bins (from bin_begin)
@@ -494,6 +503,13 @@ extern "C" int adc_cuda_chi2_plan_destroy(adc_chi2_plan* P) {
   if (P->lin) cudaFree(P->lin);
   if (P->icounts) cudaFree(P->icounts);
   if (P->grad_multi_records) cudaFree(P->grad_multi_records);
+  if (P->fit_graph) cudaGraphExecDestroy(P->fit_graph);
+  if (P->fit_st) cudaFree(P->fit_st);
+  if (P->h_fit_st) cudaFreeHost(P->h_fit_st);
+  if (P->fit_scratch) cudaFree(P->fit_scratch);
+  if (P->ncand_dev) cudaFree(P->ncand_dev);
+  for (auto& e : P->fit_ev)
+    if (e) cudaEventDestroy(e);
   if (P->stream) cudaStreamDestroy(P->stream);
   delete P;
   return ADC_OK;
@@ -758,6 +774,70 @@ bool damped_solve(std::vector<double> h, std::vector<double> g, double lambda, i
 }
 }  // namespace
 
+namespace {
+// Builds (once per plan and option set) the graph of one device-resident
+// steepest-descent iteration: QDev from the device parameters, the gradient
+// pass, finalize + trials, the multi-candidate pass, selection, copy-back.
+int build_fit_graph(adc_chi2_plan* P, const FitDevConst& c) {
+  const int64_t nchunks = P->L.nchunks;
+  const int Rmax = adc_chi2_record_len(P->np, 1);
+  if (P->fit_st == nullptr) {
+    ADCB_CUDA(cudaMalloc(&P->fit_st, sizeof(FitDevState)));
+    ADCB_CUDA(cudaMallocHost(&P->h_fit_st, sizeof(FitDevState)));
+    const size_t scratch = std::max<size_t>((size_t)nchunks * Rmax, (size_t)kMultiMax * nchunks * 4);
+    ADCB_CUDA(cudaMalloc(&P->fit_scratch, scratch * sizeof(double)));
+    ADCB_CUDA(cudaMalloc(&P->ncand_dev, sizeof(int)));
+    ADCB_CUDA(cudaEventCreate(&P->fit_ev[0]));
+    ADCB_CUDA(cudaEventCreate(&P->fit_ev[1]));
+  }
+  if (P->fit_graph != nullptr && std::memcmp(&P->fit_const, &c, sizeof(c)) == 0) return ADC_OK;
+  if (P->fit_graph) cudaGraphExecDestroy(P->fit_graph);
+  P->fit_graph = nullptr;
+  P->fit_const = c;
+  if (int rc = ensure_lin(P, P->stream)) return rc;
+  if (int rc = ensure_multi(P)) return rc;
+  cudaStream_t s = P->stream;
+  cudaGraph_t g = nullptr;
+  ADCB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  int rc = fit_device_enqueue_qdev(P->fit_st, P->model, P->np, P->qdev, s);
+  if (rc == ADC_OK) rc = cudaEventRecordWithFlags(P->fit_ev[0], s, cudaEventRecordExternal) == cudaSuccess ? ADC_OK : ADC_E_CUDA;
+  if (rc == ADC_OK)
+    rc = chi2_enqueue(make_pass(P), P->model, P->np, true, true, P->L.chunk_tiles, P->records, s,
+                      P->lin);
+  if (rc == ADC_OK) rc = cudaEventRecordWithFlags(P->fit_ev[1], s, cudaEventRecordExternal) == cudaSuccess ? ADC_OK : ADC_E_CUDA;
+  if (rc == ADC_OK)
+    rc = fit_device_enqueue_grad(P->fit_st, P->records, P->fit_scratch, nchunks, P->np, P->model,
+                                 P->events, c, P->qmulti, P->ncand_dev, s);
+  if (rc == ADC_OK) {
+    Chi2Pass pass = make_pass(P);
+    pass.qdev = P->qmulti;
+    pass.tile_ws = P->tile_ws_multi;
+    pass.ncand_dev = P->ncand_dev;
+    rc = chi2_multi_enqueue(pass, P->model, P->np, kMultiMax, P->L.chunk_tiles, P->records_multi,
+                            s, P->lin);
+  }
+  if (rc == ADC_OK)
+    rc = fit_device_enqueue_accept(P->fit_st, P->records_multi, P->fit_scratch, nchunks,
+                                   P->events, c, s);
+  if (rc == ADC_OK)
+    rc = cudaMemcpyAsync(P->h_fit_st, P->fit_st, sizeof(FitDevState), cudaMemcpyDeviceToHost, s) ==
+                 cudaSuccess
+             ? ADC_OK
+             : ADC_E_CUDA;
+  cudaError_t e = cudaStreamEndCapture(s, &g);
+  if (rc != ADC_OK) {
+    if (g) cudaGraphDestroy(g);
+    if (rc == ADC_E_CUDA) return fail(ADC_E_CUDA, "fit graph capture");
+    return rc;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture (fit)");
+  e = cudaGraphInstantiate(&P->fit_graph, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate (fit)");
+  return ADC_OK;
+}
+}  // namespace
+
 extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* clamp_idx,
                             int32_t nclamp, const adc_fit_options* opts, adc_fit_result* result,
                             double* iterates) {
@@ -793,7 +873,108 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
   if (opts->trace_iterates > 0) trace(q);
   std::vector<double> g(np), trial(np);
   int first_batch = 32;  // line-search batch size, adapted per iteration
+  // Device-resident iterations (fit_device.cu): steepest descent with the fast
+  // AD passes on one device.  ADC_FIT_DEVICE=0 keeps the host-driven loop
+  // (both give the same bits).
+  const char* fd_env = getenv("ADC_FIT_DEVICE");
+  const bool dev_mode = P->fast && !opts->use_hessian && !numeric(P) && P->comm == nullptr &&
+                        !sharded(P) && nclamp <= kMaxNp && !(fd_env && atoi(fd_env) == 0);
+  if (dev_mode) {
+    FitDevConst c{};
+    c.grad_tol = opts->grad_tol;
+    c.chi2_rel_tol = opts->chi2_rel_tol;
+    c.sigma_min = opts->sigma_min;
+    c.armijo_c1 = opts->armijo_c1;
+    c.nclamp = nclamp;
+    for (int k = 0; k < nclamp; ++k) c.clamp_idx[k] = clamp_idx[k];
+    if (int rc = build_fit_graph(P, c)) return rc;
+    std::memset(P->h_fit_st, 0, sizeof(FitDevState));
+    for (int i = 0; i < np; ++i) P->h_fit_st->q[i] = q[i];
+    P->h_fit_st->cur = cur;
+    P->h_fit_st->first_batch = first_batch;
+    ADCB_CUDA(cudaMemcpyAsync(P->fit_st, P->h_fit_st, sizeof(FitDevState), cudaMemcpyHostToDevice,
+                              P->stream));
+    ADCB_CUDA(cudaStreamSynchronize(P->stream));
+  }
   for (int iter = 0; iter < opts->budget; ++iter) {
+    if (dev_mode) {
+      // one graph = gradient pass + finalize + trials + multi pass + selection
+      ADCB_CUDA(cudaGraphLaunch(P->fit_graph, P->stream));
+      ADCB_CUDA(cudaStreamSynchronize(P->stream));
+      FitDevState& st = *P->h_fit_st;
+      float ms = 0.f;
+      ADCB_CUDA(cudaEventElapsedTime(&ms, P->fit_ev[0], P->fit_ev[1]));
+      res.gradient_ns += (uint64_t)(ms * 1e6);
+      ++res.gradient_evals;
+      if (st.status == kFitConvergedGrad) {
+        res.converged = 1;
+        break;
+      }
+      res.chi2_evals += (uint64_t)st.evals;
+      bool accepted = st.accepted_k >= 0;
+      double next = st.cur, rel_dec = st.rel_dec;
+      if (accepted) {
+        res.sigma_clamps += st.sigma_clamps;
+        for (int i = 0; i < np; ++i) q[i] = st.q[i];
+      } else if (st.status == kFitNeedHost) {
+        // the first batch held no acceptable step: continue the same search
+        // (t_next, t_next/2, ...) with host-driven batches, then hand the
+        // state back to the device
+        int tried = st.evals;
+        std::vector<double> trials, tvals, c2s(kMultiMax);
+        std::vector<int> cls;
+        double t = st.t_next;
+        while (t >= 1e-18 && !accepted) {
+          trials.clear();
+          tvals.clear();
+          cls.clear();
+          for (double tt = t; tt >= 1e-18 && (int)tvals.size() < kMultiMax; tt *= 0.5) {
+            trial = q;
+            for (int i = 0; i < np; ++i) trial[i] -= tt * st.g[i];
+            cls.push_back(clamp(trial));
+            trials.insert(trials.end(), trial.begin(), trial.end());
+            tvals.push_back(tt);
+          }
+          if (tvals.empty()) break;
+          if (int rc = adc_cuda_chi2_multi(P, trials.data(), (int32_t)tvals.size(), c2s.data()))
+            return rc;
+          for (size_t k = 0; k < tvals.size(); ++k) {
+            ++res.chi2_evals;
+            ++tried;
+            if (c2s[k] <= cur - opts->armijo_c1 * tvals[k] * st.gd) {
+              accepted = true;
+              next = c2s[k];
+              res.sigma_clamps += cls[k];
+              trial.assign(trials.begin() + k * np, trials.begin() + (k + 1) * np);
+              break;
+            }
+          }
+          t = tvals.back() * 0.5;
+        }
+        if (accepted) {
+          rel_dec = (cur - next) / std::max(1.0, std::fabs(cur));
+          q = trial;
+          for (int i = 0; i < np; ++i) st.q[i] = q[i];
+          st.cur = next;
+          st.first_batch = std::min(kMultiMax, std::max(8, (tried + 8 + 7) / 8 * 8));
+          ADCB_CUDA(cudaMemcpyAsync(P->fit_st, P->h_fit_st, sizeof(FitDevState),
+                                    cudaMemcpyHostToDevice, P->stream));
+          ADCB_CUDA(cudaStreamSynchronize(P->stream));
+        }
+      }
+      if (!accepted) {
+        res.converged = 1;
+        break;
+      }
+      cur = next;
+      ++res.iterations;
+      if (opts->trace_iterates > res.iterations) trace(q);
+      if (rel_dec <= opts->chi2_rel_tol) {
+        res.converged = 1;
+        break;
+      }
+      continue;
+    }
     auto t0 = clk::now();
     if (int rc = adc_cuda_chi2_gradient(P, q.data(), g.data(), nullptr)) return rc;
     res.gradient_ns += (uint64_t)std::chrono::nanoseconds(clk::now() - t0).count();

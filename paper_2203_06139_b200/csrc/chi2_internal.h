@@ -23,6 +23,7 @@ struct Chi2Pass {
   int64_t bin_end;       // one past the last bin this rank reads
   int bpt;               // bins per thread per tile (multiple of 4)
   int64_t tile_begin, tile_end;
+  const int* ncand_dev = nullptr;  // multi pass: candidate count read on the device (fit graph)
 };
 
 // lin: per-chunk q-independent basis sums from chi2_lin_enqueue (gradient
@@ -38,6 +39,8 @@ int chi2_lin_count(int model, int np);  // L: number of linear parameters
 // lin_records (2L + 1 doubles each); uses P.tile_ws.
 int chi2_lin_enqueue(const Chi2Pass& P, int model, int64_t chunk_tiles, double* lin_records,
                      double* icounts_local, cudaStream_t s);
+// ncand: candidates; with P.ncand_dev set, ncand is the upper bound (grid)
+// and the actual count is read on the device.
 int chi2_multi_enqueue(const Chi2Pass& P, int model, int np, int ncand,
                        int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin);
 void fill_qdev(int model, int np, const double* q, double* host_qdev);

@@ -1,0 +1,44 @@
+// Device-resident steepest-descent iteration (fit_device.cu) and its state.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "chi2_internal.h"
+
+namespace adcb {
+
+enum {
+  kFitRunning = 0,
+  kFitConvergedGrad = 1,    // gmax <= grad_tol (fit.cpp:340-344)
+  kFitConvergedRelDec = 2,  // relative decrease <= chi2_rel_tol
+  kFitConvergedNoStep = 3,  // no Armijo step down to t = 1e-18
+  kFitNeedHost = 4          // the first batch had no acceptable trial: continue on the host
+};
+
+// Lives in device memory; copied back (whole) once per iteration.
+struct FitDevState {
+  double q[kMaxNp];
+  double g[kMaxNp];
+  double cur, gd, gmax, rel_dec, t_next;
+  double tvals[kMultiMax];
+  double trials[kMultiMax * kMaxNp];
+  int cls[kMultiMax];
+  int ncand, first_batch, status, accepted_k, sigma_clamps, evals;
+};
+
+struct FitDevConst {
+  double grad_tol, chi2_rel_tol, sigma_min, armijo_c1;
+  int clamp_idx[kMaxNp];
+  int nclamp;
+};
+
+int fit_device_enqueue_qdev(FitDevState* st, int model, int np, double* qdev, cudaStream_t s);
+int fit_device_enqueue_grad(FitDevState* st, const double* records, double* scratch,
+                            int64_t nchunks, int np, int model, double events,
+                            const FitDevConst& c, double* qmulti, int* ncand_dev, cudaStream_t s);
+int fit_device_enqueue_accept(FitDevState* st, const double* records, double* scratch,
+                              int64_t nchunks, double events, const FitDevConst& c,
+                              cudaStream_t s);
+
+}  // namespace adcb

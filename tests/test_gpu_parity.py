@@ -541,3 +541,36 @@ def test_gaussnd_strided_views(restate):
     assert np.all(hx[:, :64] == 0) and np.all(hx[:, 64 + n:] == 0)
     with pytest.raises(adc.AdcError):
         adc.launch_batch("gaussnd_grad_0_1", X[:, ::2], P[:, ::2], 1.3, DX[:, ::2], DP[:, ::2])
+
+
+@pytest.mark.parametrize("case", ["gpoly_1e6", "gsum1", "gsum2", "gsum4"])
+def test_device_fit_loop_bitwise_equals_host_loop(case):
+    """The device-resident iteration (one CUDA graph per steepest-descent step:
+    gradient pass, finalize, Armijo trials, multi pass, selection) takes exactly
+    the host-driven loop's steps: same iterates, chi2 and counters, bit for bit."""
+    import os
+    if case == "gpoly_1e6":
+        counts, ev = synth.histogram(10**6, events=1e8, seed=11)
+        model, init, budget = "gpoly", list(synth.GPOLY_INIT), 400
+    else:
+        k = int(case[-1])
+        truth = adc.default_truth(k)
+        counts, ev = synth.histogram(20_000, -5.0, 5.0, 2e6, "gsum", truth, seed=k)
+        model, init, budget = "gsum", adc.perturbed_init(truth), 200
+    h = adc.Histogram(counts.size, -5.0, 5.0, ev, counts)
+    out = {}
+    for mode in ("0", "1"):
+        os.environ["ADC_FIT_DEVICE"] = mode
+        try:
+            r = adc.FitEngine(model, len(init)).fit(
+                h, init, adc.FitOptions(budget=budget, trace_iterates=budget + 1))
+        finally:
+            os.environ.pop("ADC_FIT_DEVICE", None)
+        out[mode] = r
+    a, b = out["0"], out["1"]
+    assert a.iterations == b.iterations and a.gradient_evals == b.gradient_evals
+    assert a.chi2_evals == b.chi2_evals and a.sigma_clamps == b.sigma_clamps
+    assert a.converged == b.converged
+    assert np.array(a.params).tobytes() == np.array(b.params).tobytes()
+    assert a.chi2 == b.chi2
+    assert np.array(a.iterates).tobytes() == np.array(b.iterates).tobytes()
