@@ -50,3 +50,13 @@ global void k_sumn(real[] x, integer n, real[] dx) {
     sumn_grad(x, n, dx);
   }
 }
+
+// Second order, forward-over-reverse (hessian.cpp:31): the tangent of the
+// generated gradient along x, per point — column x of each point's Hessian
+// lands in hx (d/dx dgauss/dx) and hp (d/dx dgauss/dp).
+global void k_hess(real[] x, real[] p, real sigma, real[] dx, real[] dp, real[] hx, real[] hp) {
+  integer i = blockIdx * blockDim + threadIdx;
+  if (i < N) {
+    gauss_grad_0_1_darg0(x[i], p[i], sigma, dx[i], dp[i], hx[i], hp[i]);
+  }
+}

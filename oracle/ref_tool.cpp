@@ -257,6 +257,18 @@ int cmd_gauss_shared_in(int argc, char** argv) {
   return refused ? 0 : 1;
 }
 
+// print-forward <module> <fn> <wrt>   — differentiate_forward(fn, wrt) text
+// (forward-over-reverse when fn is a generated gradient, hessian.cpp:31).
+int cmd_print_forward(int argc, char** argv) {
+  if (argc < 4) die("print-forward <module> <fn> <wrt>");
+  Module m = load_named(argv[1]);
+  const FunctionDef* f = m.find(argv[2]);
+  if (f == nullptr) die(std::string("no function ") + argv[2]);
+  TangentProgram t = differentiate_forward(*f, argv[3]);
+  std::cout << print(t.derived);
+  return 0;
+}
+
 // launch-file <module.dsl> <kernel> <n> <block> <in.bin> <out.bin> <module_out.txt> [unsafe]
 //   Any Listing-style kernel of a DSL module (the generic-lowering parity
 //   fixture): parse, ensure_called_derivatives (tooling.cpp:103-119), then
@@ -876,6 +888,7 @@ int main(int argc, char** argv) {
     if (cmd == "gaussnd-shared-p-in") return cmd_gaussnd_shared_p_in(argc - 1, argv + 1);
     if (cmd == "gauss-shared-in") return cmd_gauss_shared_in(argc - 1, argv + 1);
     if (cmd == "launch-file") return cmd_launch_file(argc - 1, argv + 1);
+    if (cmd == "print-forward") return cmd_print_forward(argc - 1, argv + 1);
     if (cmd == "chi2-in") return cmd_chi2_in(argc - 1, argv + 1);
     if (cmd == "fit-in") return cmd_fit_in(argc - 1, argv + 1);
     if (cmd == "gaussnd-bench") return cmd_gaussnd_bench(argc - 1, argv + 1);

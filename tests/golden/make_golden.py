@@ -127,6 +127,8 @@ def main():
         ("gsum", "k_gsum", 500, [r.uniform(-5, 5, 500), np.array([1.0, 0.0, 1.5, 0.5, 1.0, 0.7]),
                                  2, np.zeros(6)], "unsafe"),
         ("sumn", "k_sumn", 200, [r.uniform(-1, 1, 64), 64, np.zeros(64)], "unsafe"),
+        ("hess", "k_hess", n, [r.uniform(-3, 3, n), r.uniform(-2, 2, n), 1.3, np.zeros(n),
+                               np.zeros(n), np.zeros(n), np.zeros(n)], ""),
         ("gauss_div0", "k_gauss", 64, [np.ones(64), np.zeros(64), 0.0, np.zeros(64),
                                        np.zeros(64)], "sequential"),
     )

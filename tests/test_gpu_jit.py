@@ -51,7 +51,7 @@ def _run(key, device, **kw):
 
 
 @pytest.mark.parametrize("key", ["gauss", "rational", "branchy", "poly", "looped", "gsum",
-                                 "sumn"])
+                                 "sumn", "hess"])
 @pytest.mark.parametrize("device", [True, False])
 def test_corpus_gradient_matches_reference_launch(key, device):
     outs = _run(key, device)

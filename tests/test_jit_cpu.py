@@ -10,7 +10,7 @@ import paper_2203_06139_b200 as adc  # noqa: E402
 
 G = golden("jit_cases.npz")
 MODULE = str(G["module"])
-CASES = ["gauss", "rational", "branchy", "poly", "looped", "gsum", "sumn"]
+CASES = ["gauss", "rational", "branchy", "poly", "looped", "gsum", "sumn", "hess"]
 
 
 @pytest.mark.parametrize("key", CASES)
