@@ -813,6 +813,138 @@ __global__ void __launch_bounds__(32) gaussnd_shared_p_tma_kernel(
   }
 }
 
+// K2sv: the shared-mean form on K2v's layout — two points per lane with
+// double2 row accesses (64-point tiles, 512 B per row access, U rows in
+// flight, the next rows prefetched into L2), every dim's u staged for the
+// reverse sweep, dx per point (optional).  The reverse sweep overwrites each
+// staged u with the point's -_r6; dp is then summed transposed: lane l owns
+// dims l + 32 j and adds the tile's 64 staged -_r6 in the rotated point order
+// (l + s) % 64 (no bank conflicts, no shuffles), into registers.  A CTA walks
+// tiles b, b + G, ... (G = kSharedPVecBlocks, fixed): a fixed order that
+// depends on n only.  Full 64-point tiles of a 16-byte-aligned even-ld
+// layout, dim <= 32 * JMAX.
+constexpr int64_t kSharedPVecBlocks = 592;
+
+template <int UF, int U, int JMAX, bool DX>
+__global__ void __launch_bounds__(32) gaussnd_shared_p_vec2_kernel(
+    const double* __restrict__ x, const double* __restrict__ p, double* __restrict__ dx,
+    int64_t ntiles, int dim, int64_t ld, double t4, double r1, double* __restrict__ partials) {
+  extern __shared__ double2 stage2[];  // [dim][32]: u, then -_r6, of points 2 i2, 2 i2 + 1
+  const int lane = threadIdx.x;
+  const int64_t ld2 = ld / 2;
+  const double2* x2 = reinterpret_cast<const double2*>(x);
+  double2* dx2 = reinterpret_cast<double2*>(dx);
+  double acc[JMAX];
+#pragma unroll
+  for (int j = 0; j < JMAX; ++j) acc[j] = 0.0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i2 = tile * 32 + lane;
+    const bool more = tile + gridDim.x < ntiles;
+    double ta = 0.0, tb = 0.0;
+    int d = 0;
+    for (; d + UF <= dim; d += UF) {
+      double2 xv[UF];
+#pragma unroll
+      for (int k = 0; k < UF; ++k) xv[k] = ld_stream2(x2 + (int64_t)(d + k) * ld2 + i2);
+#pragma unroll
+      for (int k = 0; k < UF; ++k) {  // next batch (or the first reverse rows) into L2
+        const int dn = d + UF + k;
+        if ((lane & 7) == 0) {
+          if (dn < dim) prefetch_l2(x2 + (int64_t)dn * ld2 + i2);
+          else if (DX && dim - 1 - (dn - dim) >= 0)
+            prefetch_l2(dx2 + (int64_t)(dim - 1 - (dn - dim)) * ld2 + i2);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < UF; ++k) {
+        const double pd = __ldg(p + d + k);
+        const double ua = fsub(xv[k].x, pd), ub = fsub(xv[k].y, pd);  // _t0 = x[i] - p[i]
+        stage2[(d + k) * 32 + lane] = make_double2(ua, ub);
+        ta = fadd(ta, fmul(ua, ua));                                   // t = t + _t1
+        tb = fadd(tb, fmul(ub, ub));
+      }
+    }
+    for (; d < dim; ++d) {
+      const double2 xv = ld_stream2(x2 + (int64_t)d * ld2 + i2);
+      const double pd = __ldg(p + d);
+      const double ua = fsub(xv.x, pd), ub = fsub(xv.y, pd);
+      stage2[d * 32 + lane] = make_double2(ua, ub);
+      ta = fadd(ta, fmul(ua, ua));
+      tb = fadd(tb, fmul(ub, ub));
+    }
+    double ca, cb;
+    {
+      const double e = exp(fdiv(-ta, t4));
+      ca = fadd(0.0, -fadd(0.0, fdiv(fadd(0.0, fmul(r1, e)), t4)));
+      const double f = exp(fdiv(-tb, t4));
+      cb = fadd(0.0, -fadd(0.0, fdiv(fadd(0.0, fmul(r1, f)), t4)));
+    }
+    // reverse: _r6 per slot (each slot once, so the sweep order does not
+    // change bits); _d_x[_i0] += _r6 and the stage keeps -_r6 for _d_p
+    d = dim;
+    for (; d - U >= 0; d -= U) {
+      double2 a[U];
+      if (DX) {
+#pragma unroll
+        for (int k = 0; k < U; ++k) a[k] = dx2[(int64_t)(d - 1 - k) * ld2 + i2];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {  // next dx rows; at the end, the next tile's x
+          const int dn = d - 1 - U - k;
+          if ((lane & 7) == 0) {
+            if (dn >= 0) prefetch_l2(dx2 + (int64_t)dn * ld2 + i2);
+            else if (more && -1 - dn < dim)
+              prefetch_l2(x2 + (int64_t)(-1 - dn) * ld2 + i2 + (int64_t)gridDim.x * 32);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int dd = d - 1 - k;
+        const double2 u = stage2[dd * 32 + lane];
+        const double ra = fadd(fadd(0.0, fmul(ca, u.x)), fmul(u.x, ca));
+        const double rb = fadd(fadd(0.0, fmul(cb, u.y)), fmul(u.y, cb));
+        if (DX) dx2[(int64_t)dd * ld2 + i2] = make_double2(fadd(a[k].x, ra), fadd(a[k].y, rb));
+        stage2[dd * 32 + lane] = make_double2(-ra, -rb);
+      }
+    }
+    for (; d > 0; --d) {
+      const int dd = d - 1;
+      const double2 u = stage2[dd * 32 + lane];
+      const double ra = fadd(fadd(0.0, fmul(ca, u.x)), fmul(u.x, ca));
+      const double rb = fadd(fadd(0.0, fmul(cb, u.y)), fmul(u.y, cb));
+      if (DX) {
+        const int64_t o = (int64_t)dd * ld2 + i2;
+        const double2 a = dx2[o];
+        dx2[o] = make_double2(fadd(a.x, ra), fadd(a.y, rb));
+      }
+      stage2[dd * 32 + lane] = make_double2(-ra, -rb);
+    }
+    if (!DX && more && (lane & 7) == 0) {
+      for (int k = 0; k < U && k < dim; ++k)  // the next tile's first rows
+        prefetch_l2(x2 + (int64_t)k * ld2 + i2 + (int64_t)gridDim.x * 32);
+    }
+    __syncwarp();  // every lane's -_r6 visible
+    // _d_p[d] += -_r6 of the tile's 64 points, lane l owning dims l + 32 j
+#pragma unroll
+    for (int j = 0; j < JMAX; ++j) {
+      const int dd = lane + 32 * j;
+      if (j * 32 < dim && dd < dim) {
+        const double* row = reinterpret_cast<const double*>(stage2 + (size_t)dd * 32);
+        double aj = acc[j];
+#pragma unroll 16
+        for (int s = 0; s < 64; ++s) aj = fadd(aj, row[(lane + s) & 63]);
+        acc[j] = aj;
+      }
+    }
+    __syncwarp();  // the stage is rewritten by the next tile
+  }
+#pragma unroll
+  for (int j = 0; j < JMAX; ++j) {
+    const int dd = lane + 32 * j;
+    if (dd < dim) partials[(int64_t)blockIdx.x * dim + dd] = acc[j];
+  }
+}
+
 __global__ void gaussnd_shared_p_finish(const double* __restrict__ partials, int64_t nblocks,
                                         int dim, double* __restrict__ dp) {
   const int d = blockIdx.x * blockDim.x + threadIdx.x;
@@ -888,6 +1020,36 @@ int launch_gaussnd_shared_p(int64_t n, int64_t dim, int64_t ld, const double* x,
   const bool tma = (getenv("ADC_SHAREDP_TMA") ? atoi(getenv("ADC_SHAREDP_TMA")) != 0 : true) &&
                    dx == nullptr && ld % 2 == 0 && ((uintptr_t)x & 15) == 0 && dim <= 256 &&
                    tma_smem <= 200 * 1024;
+  // K2sv (double2 rows, 64-point tiles) when the layout allows it: the full
+  // 64-point tiles over kSharedPVecBlocks CTAs, the < 64 remaining points as
+  // one more block of partials (K2s), then the fixed-order total.
+  const bool vec = (getenv("ADC_SHAREDP_VEC") ? atoi(getenv("ADC_SHAREDP_VEC")) != 0 : dx != nullptr) &&
+                   ld % 2 == 0 && ((((uintptr_t)x) | ((uintptr_t)dx)) & 15) == 0 && dim <= 128 &&
+                   n >= 64;
+  if (vec) {
+    const int64_t full64 = n / 64, rem64 = n % 64;
+    const int64_t vblocks = std::min<int64_t>(full64, kSharedPVecBlocks);
+    const size_t vsmem = (size_t)dim * 512;
+    // U = 16 rows in flight: measured best of 16 / 24 / 32
+    auto kv = dx != nullptr ? gaussnd_shared_p_vec2_kernel<16, 16, 4, true>
+                            : gaussnd_shared_p_vec2_kernel<16, 16, 4, false>;
+    if (vsmem > 48 * 1024)
+      ADCB_CUDA(cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsmem));
+    ADCB_CUDA(cudaFuncSetAttribute(kv, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                   cudaSharedmemCarveoutMaxShared));
+    kv<<<(unsigned)vblocks, 32, vsmem, s>>>(x, p, dx, full64, (int)dim, ld, t4, d_t9, partials);
+    ADCB_CUDA(cudaGetLastError());
+    if (rem64 != 0) {
+      const int64_t off = full64 * 64;
+      k<<<1, 32, smem, s>>>(x + off, p, dx ? dx + off : nullptr, rem64, (int)dim, ld, t4, d_t9,
+                            dstage, partials + vblocks * dim);
+      ADCB_CUDA(cudaGetLastError());
+    }
+    gaussnd_shared_p_finish<<<(unsigned)((dim + 127) / 128), 128, 0, s>>>(
+        partials, vblocks + (rem64 != 0 ? 1 : 0), (int)dim, dp);
+    ADCB_CUDA(cudaGetLastError());
+    return ADC_OK;
+  }
   if (full > 0) {
     CUtensorMap tmap;
     if (tma && make_rows_tmap(&tmap, x, full * 32, dim, ld) == ADC_OK) {

@@ -524,6 +524,41 @@ def test_gaussnd_shared_p_large_and_refusal(restate):
     assert np.all(np.abs(host(dp) - tot) <= 1e-12 * ab)
 
 
+@pytest.mark.parametrize("dim,n", [(100, 200_006), (37, 64 * 700), (128, 5_000)])
+def test_gaussnd_shared_p_with_dx_paths(restate, dim, n):
+    """With private dx slots: the aligned layout runs K2sv (double2 rows,
+    64-point tiles, ragged tail through K2s), an odd-offset view of the same
+    points runs K2s.  dx per point within 1e-12 of the restatement in both;
+    dp within 1e-12 * sum|terms| of the compensated total in both (the two
+    paths sum in different fixed orders); each path bitwise repeatable."""
+    rng = np.random.Generator(np.random.PCG64(dim))
+    p = rng.uniform(-1, 1, dim)
+    x = p[:, None] + 0.1 * rng.standard_normal((dim, n))
+    dx0 = rng.standard_normal((dim, n))
+    dp0 = rng.standard_normal(dim)
+    rdx, rdp = dx0.copy(), dp0.copy()
+    restate.gaussnd_grad_shared_p(np.ascontiguousarray(x), p, 1.3, rdx, rdp)
+    tot, ab = restate.gaussnd_shared_p_dp_compensated(np.ascontiguousarray(x), p, 1.3)
+    o = adc.LaunchOptions(unsafe=True)
+    wide = np.zeros((dim, n + 1))
+    for offset in (0, 1):
+        X = t(np.ascontiguousarray(x)) if offset == 0 else t(wide)[:, 1:]
+        if offset:
+            X.copy_(t(x))
+        runs = []
+        for _ in range(2):
+            DX = t(dx0) if offset == 0 else t(np.zeros((dim, n + 1)))[:, 1:]
+            if offset:
+                DX.copy_(t(dx0))
+            DP = t(dp0)
+            adc.launch_batch_shared_p("gaussnd_grad_0_1", X, t(p), 1.3, DX, DP, o)
+            runs.append((host(DX), host(DP)))
+        (gdx, gdp), (gdx2, gdp2) = runs
+        assert gdx.tobytes() == gdx2.tobytes() and gdp.tobytes() == gdp2.tobytes()
+        assert acc_err(gdx, rdx, dx0).max() <= REL, offset
+        assert np.all(np.abs(gdp - (dp0 + tot)) <= 1e-12 * (ab + np.abs(dp0))), offset
+
+
 def test_gaussnd_strided_views(restate):
     # a (dim, n) view of a wider SoA buffer: the row stride comes from the view
     dim, n, big = 50, 3000, 3200
