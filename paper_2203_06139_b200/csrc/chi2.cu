@@ -63,6 +63,7 @@ static_assert(sizeof(QDev) + sizeof(QNum) == kQDoubles * sizeof(double), "QDev l
 // width parameter with multiplies by its host-computed reciprocal.
 struct GPoly {
   static constexpr int NP = 6;
+  static constexpr int NG = 1;  // Gaussian factors exp(-z^2/2), z = (x - mu) / sigma
   // q[3..5] enter linearly: dm/dq = (1, x, x^2) does not depend on q, so their
   // G0 and G1 sums are the same for every pass of a fit (precomputed once).
   static constexpr int LIN0 = 3;
@@ -89,15 +90,24 @@ struct GPoly {
     }
     return r;
   }
+  __device__ static __forceinline__ void gauss(const Reg& Q, int, double& mu, double& inv) {
+    mu = Q.q1;
+    inv = Q.inv2;
+  }
   template <bool GRAD, bool FAST>
   __device__ static __forceinline__ void eval(double x, const Reg& Q, const double* tab, double& m,
-                                              double* bg) {
+                                              double* bg, const double* erec = nullptr) {
     const double q0 = Q.q0, q1 = Q.q1, q2 = Q.q2, q3 = Q.q3, q4 = Q.q4, q5 = Q.q5;
     const double t0 = fsub(x, q1);                              // _t0 = x - q[1]
     const double z = FAST ? fmul(t0, Q.inv2) : fdiv(t0, q2);    // z = _t0 / q[2]
     const double t1 = fmul(-0.5, z);                            // _t1 = -0.5 * z
-    const double t2 = fmul(t1, z);                              // _t2 = _t1 * z
-    const double e = FAST ? exp_nonpos(t2, tab) : exp(t2);      // _t3 = exp(_t2)
+    double e;
+    if (erec != nullptr) {
+      e = erec[0];  // _t3 from the per-thread recurrence (tile_bins, REC)
+    } else {
+      const double t2 = fmul(t1, z);                            // _t2 = _t1 * z
+      e = FAST ? exp_nonpos(t2, tab) : exp(t2);                 // _t3 = exp(_t2)
+    }
     const double g = fmul(q0, e);                               // g = q[0] * _t3
     if (FAST)
       m = __fma_rn(q5 * x, x, __fma_rn(q4, x, g + q3));
@@ -124,6 +134,7 @@ struct GPoly {
 template <int K>
 struct GSum {
   static constexpr int NP = 3 * K;
+  static constexpr int NG = K;
   static constexpr int LIN0 = NP;  // no q-independent gradient components
   __device__ static __forceinline__ void lin_basis(double, double*) {}
   struct Reg {
@@ -143,9 +154,13 @@ struct GSum {
     if (i % 3 == 2) r.inv[i / 3] = inv;
     return r;
   }
+  __device__ static __forceinline__ void gauss(const Reg& Q, int j, double& mu, double& inv) {
+    mu = Q.q[3 * j + 1];
+    inv = Q.inv[j];
+  }
   template <bool GRAD, bool FAST>
   __device__ static __forceinline__ void eval(double x, const Reg& Q, const double* tab, double& m,
-                                              double* bg) {
+                                              double* bg, const double* erec = nullptr) {
     double acc = 0.0;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
@@ -153,8 +168,13 @@ struct GSum {
       const double t0 = fsub(x, mu);                                   // _t0 = x - mu
       const double z = FAST ? fmul(t0, Q.inv[j]) : fdiv(t0, sg);  // z = _t0 / sg
       const double t1 = fmul(-0.5, z);                                 // _t1 = -0.5 * z
-      const double t2 = fmul(t1, z);                                   // _t2 = _t1 * z
-      const double e = FAST ? exp_nonpos(t2, tab) : exp(t2);           // _t3 = exp(_t2)
+      double e;
+      if (erec != nullptr) {
+        e = erec[j];  // _t3 from the per-thread recurrence (tile_bins, REC)
+      } else {
+        const double t2 = fmul(t1, z);                                 // _t2 = _t1 * z
+        e = FAST ? exp_nonpos(t2, tab) : exp(t2);                      // _t3 = exp(_t2)
+      }
       acc = FAST ? __fma_rn(amp, e, acc) : fadd(acc, fmul(amp, e));    // acc = acc + amp*_t3
       if constexpr (GRAD) {
         const double r3 = fmul(amp, e);        // _r3 = (amp*_r1)*_q0
@@ -222,9 +242,10 @@ __device__ __forceinline__ void numeric_fold(double x, const typename M::Reg& QR
 template <class M, bool GRAD, bool FAST>
 __device__ __forceinline__ void bin_term(const Chi2Pass& P, const typename M::Reg& QR,
                                          const double* tab, double jh, double ic,
-                                         BinTerm<M, GRAD, FAST>& t) {
+                                         BinTerm<M, GRAD, FAST>& t,
+                                         const double* erec = nullptr) {
   const double x = fadd(P.lo, fmul(jh, P.width));  // Histogram::center: lo + (j + 0.5) * width
-  M::template eval<GRAD, FAST>(x, QR, tab, t.m, t.bg);
+  M::template eval<GRAD, FAST>(x, QR, tab, t.m, t.bg, erec);
   t.w = ic > 0.0 ? 1.0 : 0.0;
   t.mc = t.m * ic;
 }
@@ -252,10 +273,23 @@ __device__ __forceinline__ void bin_accumulate(const BinTerm<M, GRAD, FAST>& t, 
 // ILP evaluates that many independent bins before folding any, giving the
 // scheduler two dependency chains to interleave (the model's exp chain is
 // ~15 dependent FP64 ops deep).  The accumulation order is unchanged.
-template <class M, bool GRAD, bool FAST, bool CHECK, int ILP, bool NUM>
+// REC (gradient passes, precision mode 2): each thread's Gaussian factors
+// e_k = exp(-z_k^2 / 2) over its run of bins z_k = z_0 + k D (D = 256 width /
+// sigma, uniform) come from one anchor per tile instead of one exp per bin:
+//   e_k = (e_0 A^k) B_k,  e_0 = exp(-z_0^2 / 2),  A = exp(-z_0 D),
+//   B_k = exp(-(k D)^2 / 2)  (a per-pass table, uniform over threads),
+// i.e. two multiplies per bin; the product's rounding error grows by about
+// one ulp per bin (<= bpt + 2 ulp relative while e_0 is a normal number;
+// below that the absolute error is < 1e-290).  Used when |D| bpt <= 1 (a
+// run spans at most one sigma): then e_0 A^k = e_k / B_k <= e^(1/2), so the
+// product cannot overflow.
+constexpr int kRecMaxBpt = 192;
+
+template <class M, bool GRAD, bool FAST, bool CHECK, int ILP, bool NUM, bool REC = false>
 __device__ __forceinline__ void tile_bins(const Chi2Pass& P, const typename M::Reg& QR,
                                           const double* tab, int64_t base, double* acc,
-                                          const QNum* N) {
+                                          const QNum* N, const double* rtab = nullptr,
+                                          const double* rdl = nullptr) {
   constexpr int PD = kPD;  // P.bpt is a multiple of kPD (adc_chi2_make_layout)
   const int BPT = P.bpt;
   constexpr int STEP = ILP <= PD ? ILP : PD;
@@ -266,6 +300,18 @@ __device__ __forceinline__ void tile_bins(const Chi2Pass& P, const typename M::R
     ring[k] = (!CHECK || j < P.bin_end) ? ld_stream(P.icounts + j) : 0.0;
   }
   double jh = fadd((double)base, 0.5);  // advanced by 256.0 per bin: exact integers + 0.5
+  [[maybe_unused]] double rP[REC ? M::NG : 1], rA[REC ? M::NG : 1];
+  if constexpr (REC) {
+    const double x0 = fadd(P.lo, fmul(jh, P.width));
+#pragma unroll
+    for (int c = 0; c < M::NG; ++c) {
+      double mu, inv;
+      M::gauss(QR, c, mu, inv);
+      const double z0 = fmul(fsub(x0, mu), inv);  // the model's own z at bin 0
+      rP[c] = exp_nonpos(fmul(fmul(-0.5, z0), z0), tab);
+      rA[c] = exp(-fmul(z0, rdl[c]));
+    }
+  }
   for (int k0 = 0; k0 < BPT; k0 += PD) {
 #pragma unroll
     for (int kk = 0; kk < PD; kk += STEP) {
@@ -289,6 +335,16 @@ __device__ __forceinline__ void tile_bins(const Chi2Pass& P, const typename M::R
             bin_term<M, false, FAST>(P, QR, tab, jh, c, tv);
             bin_accumulate<M, false, FAST>(tv, acc);
             numeric_fold<M, FAST>(fadd(P.lo, fmul(jh, P.width)), QR, *N, tab, tv.w, tv.mc, acc);
+          }
+        } else if constexpr (REC) {
+          if (valid[u]) {
+            double e[M::NG];
+#pragma unroll
+            for (int g = 0; g < M::NG; ++g) {
+              e[g] = fmul(rP[g], rtab[g * kRecMaxBpt + k]);
+              rP[g] = fmul(rP[g], rA[g]);
+            }
+            bin_term<M, GRAD, FAST>(P, QR, tab, jh, c, t[u], e);
           }
         } else {
           if (valid[u]) bin_term<M, GRAD, FAST>(P, QR, tab, jh, c, t[u]);
@@ -314,7 +370,7 @@ __host__ __device__ constexpr bool pass_zero_entry(int v) {
 }
 
 template <class M, bool GRAD, bool FAST, int MINB = tile_min_blocks<M, GRAD>(),
-          int ILP = 1, bool NUM = false>
+          int ILP = 1, bool NUM = false, bool REC = false>
 __global__ void __launch_bounds__(kTileThreads, MINB) chi2_tile_kernel(Chi2Pass P) {
   constexpr int NP = M::NP;
   constexpr int R = GRAD ? 4 + 3 * NP : 4;
@@ -336,6 +392,30 @@ __global__ void __launch_bounds__(kTileThreads, MINB) chi2_tile_kernel(Chi2Pass 
   if (threadIdx.x < 64) tab[threadIdx.x] = exp2((double)threadIdx.x / 64.0);
   __syncthreads();
   const typename M::Reg QR = M::load(Q);
+  [[maybe_unused]] bool use_rec = false;
+  __shared__ double rtab[REC ? M::NG * kRecMaxBpt : 1];
+  __shared__ double rdl[REC ? M::NG : 1];
+  if constexpr (REC) {
+    // D per Gaussian factor and the B_k table (uniform; see tile_bins)
+    use_rec = P.bpt <= kRecMaxBpt;
+#pragma unroll
+    for (int c = 0; c < M::NG; ++c) {
+      double mu, inv;
+      M::gauss(QR, c, mu, inv);
+      const double dl = fmul((double)kTileThreads * P.width, inv);
+      use_rec = use_rec && fabs(dl) * P.bpt <= 1.0;
+      if (threadIdx.x == 0) rdl[c] = dl;
+    }
+    if (use_rec)
+      for (int v = threadIdx.x; v < M::NG * P.bpt; v += kTileThreads) {
+        const int c = v / P.bpt, k = v % P.bpt;
+        double mu, inv;
+        M::gauss(QR, c, mu, inv);
+        const double kd = fmul((double)k, fmul((double)kTileThreads * P.width, inv));
+        rtab[c * kRecMaxBpt + k] = exp(fmul(fmul(-0.5, kd), kd));
+      }
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int BPT = P.bpt;
   const int64_t TB = (int64_t)BPT * kTileThreads;
@@ -351,10 +431,15 @@ __global__ void __launch_bounds__(kTileThreads, MINB) chi2_tile_kernel(Chi2Pass 
     double acc[R];
 #pragma unroll
     for (int v = 0; v < R; ++v) acc[v] = 0.0;
-    if ((tile + 1) * TB <= P.bin_end)
+    const bool full = (tile + 1) * TB <= P.bin_end;
+    if (REC && use_rec) {
+      if (full) tile_bins<M, GRAD, FAST, false, ILP, NUM, REC>(P, QR, tab, base, acc, Np, rtab, rdl);
+      else tile_bins<M, GRAD, FAST, true, ILP, NUM, REC>(P, QR, tab, base, acc, Np, rtab, rdl);
+    } else if (full) {
       tile_bins<M, GRAD, FAST, false, ILP, NUM>(P, QR, tab, base, acc, Np);
-    else
+    } else {
       tile_bins<M, GRAD, FAST, true, ILP, NUM>(P, QR, tab, base, acc, Np);
+    }
     // fixed shuffle tree, then fixed cross-warp tree; entries a pass never
     // touches (C0 and the linear G0/G1: the K3l pre-pass supplies them) are
     // exact zeros and skip the tree
@@ -628,46 +713,55 @@ __global__ void __launch_bounds__(kChunkThreads) chi2_chunk_kernel(
 // ---- dispatch ----------------------------------------------------------------
 int g_chi2_tune = 0;  // experiment knob (ADC_CHI2_TUNE), see launch_tiles_t
 
-template <class M, bool GRAD, bool FAST>
+template <class M, bool GRAD, bool FAST, bool REC = false>
 static void launch_tiles_t(const Chi2Pass& P, int blocks, cudaStream_t s) {
   constexpr int MB = tile_min_blocks<M, GRAD>();
   if constexpr (std::is_same<M, GPoly>::value && FAST) {
     // experiments: 1 = one bin at a time; 3 = 2 bins, 3 CTAs/SM; 4 = 1 bin,
     // 3 CTAs/SM; 5 = 4 bins
     if (g_chi2_tune == 3) {
-      chi2_tile_kernel<M, GRAD, FAST, 3, 2><<<sm_count() * 3, kTileThreads, 0, s>>>(P);
+      chi2_tile_kernel<M, GRAD, FAST, 3, 2, false, REC><<<sm_count() * 3, kTileThreads, 0, s>>>(P);
       return;
     }
     if (g_chi2_tune == 4) {
-      chi2_tile_kernel<M, GRAD, FAST, 3, 1><<<sm_count() * 3, kTileThreads, 0, s>>>(P);
+      chi2_tile_kernel<M, GRAD, FAST, 3, 1, false, REC><<<sm_count() * 3, kTileThreads, 0, s>>>(P);
       return;
     }
     if (g_chi2_tune == 5) {
-      chi2_tile_kernel<M, GRAD, FAST, MB, 4><<<blocks, kTileThreads, 0, s>>>(P);
+      chi2_tile_kernel<M, GRAD, FAST, MB, 4, false, REC><<<blocks, kTileThreads, 0, s>>>(P);
       return;
     }
     if (g_chi2_tune == 1) {
-      chi2_tile_kernel<M, GRAD, FAST><<<blocks, kTileThreads, 0, s>>>(P);
+      chi2_tile_kernel<M, GRAD, FAST, MB, 1, false, REC><<<blocks, kTileThreads, 0, s>>>(P);
       return;
     }
-    // default: two bins evaluated before either is folded (measured 1.5% faster)
-    chi2_tile_kernel<M, GRAD, FAST, MB, 2><<<blocks, kTileThreads, 0, s>>>(P);
+    // default: two bins evaluated before either is folded (measured 1.5% faster);
+    // with REC one bin at a time (0.322 vs 0.366 ms at 1e8 bins: REC's two
+    // extra live doubles push the two-bin form into local memory)
+    if (REC) chi2_tile_kernel<M, GRAD, FAST, MB, 1, false, REC><<<blocks, kTileThreads, 0, s>>>(P);
+    else chi2_tile_kernel<M, GRAD, FAST, MB, 2, false, REC><<<blocks, kTileThreads, 0, s>>>(P);
     return;
   }
-  chi2_tile_kernel<M, GRAD, FAST><<<blocks, kTileThreads, 0, s>>>(P);
+  chi2_tile_kernel<M, GRAD, FAST, MB, 1, false, REC><<<blocks, kTileThreads, 0, s>>>(P);
 }
 
+// prec: 0 faithful, 1 fast, 2 fast + the Gaussian-factor recurrence in the
+// gradient pass (value passes are the same in modes 1 and 2)
 template <class M>
-static void launch_tiles_m(const Chi2Pass& P, bool grad, bool fast, bool num, int blocks,
+static void launch_tiles_m(const Chi2Pass& P, bool grad, int prec, bool num, int blocks,
                            cudaStream_t s) {
   constexpr int MB = tile_min_blocks<M, true>();
+  const bool fast = prec != 0;
   if (grad && num) {  // GradientProvider::Numeric
     if (fast) chi2_tile_kernel<M, true, true, MB, 1, true><<<blocks, kTileThreads, 0, s>>>(P);
     else chi2_tile_kernel<M, true, false, MB, 1, true><<<blocks, kTileThreads, 0, s>>>(P);
     return;
   }
   if (grad) {
-    if (fast) launch_tiles_t<M, true, true>(P, blocks, s);
+    // (REC holds two more doubles per Gaussian factor: models with <= 2
+    // factors only, larger gsum spills; they run mode 1)
+    if (prec == 2 && M::NG <= 2) launch_tiles_t<M, true, true, M::NG <= 2>(P, blocks, s);
+    else if (fast) launch_tiles_t<M, true, true>(P, blocks, s);
     else launch_tiles_t<M, true, false>(P, blocks, s);
   } else {
     if (fast) launch_tiles_t<M, false, true>(P, blocks, s);
@@ -675,7 +769,7 @@ static void launch_tiles_m(const Chi2Pass& P, bool grad, bool fast, bool num, in
   }
 }
 
-int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast,
+int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, int prec,
                  int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin,
                  bool numeric, const PeerPublish* pub) {
 
@@ -687,14 +781,14 @@ int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast,
   // models, see tile_min_blocks), tiles grid-strided.
   const int64_t blocks = std::min<int64_t>(ntiles, (int64_t)sm_count() * (np <= 6 ? 2 : 1));
   if (model == ADC_MODEL_GPOLY) {
-    launch_tiles_m<GPoly>(P, grad, fast, numeric, (int)blocks, s);
+    launch_tiles_m<GPoly>(P, grad, prec, numeric, (int)blocks, s);
   } else {
     switch (np / 3) {
-      case 1: launch_tiles_m<GSum<1>>(P, grad, fast, numeric, (int)blocks, s); break;
-      case 2: launch_tiles_m<GSum<2>>(P, grad, fast, numeric, (int)blocks, s); break;
-      case 3: launch_tiles_m<GSum<3>>(P, grad, fast, numeric, (int)blocks, s); break;
-      case 4: launch_tiles_m<GSum<4>>(P, grad, fast, numeric, (int)blocks, s); break;
-      case 8: launch_tiles_m<GSum<8>>(P, grad, fast, numeric, (int)blocks, s); break;
+      case 1: launch_tiles_m<GSum<1>>(P, grad, prec, numeric, (int)blocks, s); break;
+      case 2: launch_tiles_m<GSum<2>>(P, grad, prec, numeric, (int)blocks, s); break;
+      case 3: launch_tiles_m<GSum<3>>(P, grad, prec, numeric, (int)blocks, s); break;
+      case 4: launch_tiles_m<GSum<4>>(P, grad, prec, numeric, (int)blocks, s); break;
+      case 8: launch_tiles_m<GSum<8>>(P, grad, prec, numeric, (int)blocks, s); break;
       default: return fail(ADC_E_ARG, "gsum: unsupported component count");
     }
   }

@@ -122,7 +122,7 @@ struct adc_chi2_plan {
   int world = 1, rank = 0;
   int64_t maxc = 1;  // max chunks per rank: the padded per-rank record stride
   int bpt = 4;
-  int fast = 1;
+  int fast = 2;  // precision mode (adc_cuda_chi2_set_precision)
   int provider = ADC_PROVIDER_AD_REVERSE;  // of the gradient passes
   int device = 0;
   cudaStream_t stream = nullptr;       // plan-owned: graph replays
@@ -132,8 +132,8 @@ struct adc_chi2_plan {
   double* records = nullptr;  // [maxc][R] (gradient / value pass)
   double* h_q = nullptr;
   // [kind][fast], kind 0 = value, 1 = AD gradient, 2 = numeric gradient
-  cudaGraphExec_t graph[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
-  bool warm[3][2] = {{false, false}, {false, false}, {false, false}};  // eager pass before capture
+  cudaGraphExec_t graph[3][3] = {};  // [value, AD gradient, numeric gradient][precision mode]
+  bool warm[3][3] = {};              // eager pass before capture
   bool no_graph = false;  // the transport refused stream capture: enqueue directly
   // exchange / copy-back staging, sized once for the largest pass kind
   adc_comm* comm = nullptr;
@@ -295,7 +295,7 @@ int enqueue_pass(adc_chi2_plan* P, int grad) {
   const bool fuse = P->comm != nullptr && P->comm->kind == ADC_COMM_PEER && local_chunks(P) > 0;
   PeerPublish pub;
   if (fuse) pub = peer_publish_args(&P->peer, (size_t)P->maxc * R);
-  if (int rc = chi2_enqueue(make_pass(P), P->model, P->np, grad != 0, P->fast != 0,
+  if (int rc = chi2_enqueue(make_pass(P), P->model, P->np, grad != 0, P->fast,
                             P->L.chunk_tiles, P->records, P->stream, P->lin,
                             grad != 0 && numeric(P), fuse ? &pub : nullptr))
     return rc;
@@ -320,7 +320,7 @@ int build_graph(adc_chi2_plan* P, int grad) {
 
 void drop_graphs(adc_chi2_plan* P) {
   for (int g = 0; g < 3; ++g)
-    for (int f = 0; f < 2; ++f) {
+    for (int f = 0; f < 3; ++f) {
       if (P->graph[g][f]) cudaGraphExecDestroy(P->graph[g][f]);
       P->graph[g][f] = nullptr;
       P->warm[g][f] = false;
@@ -524,8 +524,12 @@ extern "C" int adc_cuda_chi2_plan_layout(const adc_chi2_plan* P, adc_chi2_layout
 
 extern "C" int adc_cuda_chi2_set_precision(adc_chi2_plan* P, int32_t mode) {
   clear_error();
-  if (P == nullptr || mode < 0 || mode > 1) return fail(ADC_E_ARG, "precision mode is 0 or 1");
+  if (P == nullptr || mode < 0 || mode > 2) return fail(ADC_E_ARG, "precision mode is 0, 1 or 2");
   P->fast = mode;
+  if (P->fit_graph) {  // the device fit iteration graph holds the gradient pass
+    cudaGraphExecDestroy(P->fit_graph);
+    P->fit_graph = nullptr;
+  }
   if (const char* t = getenv("ADC_CHI2_TUNE")) chi2_set_tune(atoi(t));
   return ADC_OK;
 }
@@ -564,7 +568,7 @@ extern "C" int adc_cuda_chi2_partials(adc_chi2_plan* P, const double* q, int32_t
   if (int rc = ensure_lin(P, s)) return rc;
   fill_qdev(P->model, P->np, q, P->h_q);
   ADCB_CUDA(cudaMemcpyAsync(P->qdev, P->h_q, qdev_bytes(), cudaMemcpyHostToDevice, s));
-  return chi2_enqueue(make_pass(P), P->model, P->np, want_grad != 0, P->fast != 0,
+  return chi2_enqueue(make_pass(P), P->model, P->np, want_grad != 0, P->fast,
                       P->L.chunk_tiles, records_dev ? records_dev : P->records, s, P->lin,
                       want_grad && numeric(P));
 }
@@ -674,7 +678,7 @@ extern "C" int adc_cuda_chi2_gradient_multi(adc_chi2_plan* P, const double* qs, 
   for (int k = 0; k < ncand; ++k) {
     Chi2Pass pass = make_pass(P);
     pass.qdev = reinterpret_cast<const double*>(reinterpret_cast<const char*>(P->qmulti) + k * qb);
-    if (int rc = chi2_enqueue(pass, P->model, P->np, true, P->fast != 0, P->L.chunk_tiles,
+    if (int rc = chi2_enqueue(pass, P->model, P->np, true, P->fast, P->L.chunk_tiles,
                               P->grad_multi_records + per * k, P->stream, P->lin, numeric(P)))
       return rc;
   }
@@ -802,8 +806,8 @@ int build_fit_graph(adc_chi2_plan* P, const FitDevConst& c) {
   int rc = fit_device_enqueue_qdev(P->fit_st, P->model, P->np, P->qdev, s);
   if (rc == ADC_OK) rc = cudaEventRecordWithFlags(P->fit_ev[0], s, cudaEventRecordExternal) == cudaSuccess ? ADC_OK : ADC_E_CUDA;
   if (rc == ADC_OK)
-    rc = chi2_enqueue(make_pass(P), P->model, P->np, true, true, P->L.chunk_tiles, P->records, s,
-                      P->lin);
+    rc = chi2_enqueue(make_pass(P), P->model, P->np, true, P->fast, P->L.chunk_tiles, P->records,
+                      s, P->lin);
   if (rc == ADC_OK) rc = cudaEventRecordWithFlags(P->fit_ev[1], s, cudaEventRecordExternal) == cudaSuccess ? ADC_OK : ADC_E_CUDA;
   if (rc == ADC_OK)
     rc = fit_device_enqueue_grad(P->fit_st, P->records, P->fit_scratch, nchunks, P->np, P->model,

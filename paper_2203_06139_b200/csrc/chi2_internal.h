@@ -30,7 +30,7 @@ struct Chi2Pass {
 // passes of models with linear parameters; nullptr otherwise).
 // numeric: GradientProvider::Numeric (central differences of the model).
 // pub: publish the chunk records over peer memory from the chunk kernel.
-int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, bool fast,
+int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, int prec,
                  int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin,
                  bool numeric = false, const PeerPublish* pub = nullptr);
 int chi2_lin_count(int model, int np);  // L: number of linear parameters

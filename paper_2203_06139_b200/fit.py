@@ -150,8 +150,12 @@ class Chi2Plan:
         chi2_layout(h.bins, comm.world, comm.rank); h.counts is not read."""
         return cls(model, np_, h, comm=comm, _shard=shard_counts)
 
-    def set_precision(self, fast: bool):
-        check(lib.adc_cuda_chi2_set_precision(self._p, 1 if fast else 0))
+    def set_precision(self, mode):
+        """0 / False: faithful IEEE divisions; 1: fast (reciprocal multiplies,
+        table exp); 2 / True (default): fast, and gradient passes take each
+        thread's Gaussian factors from an anchored product recurrence."""
+        mode = 2 if mode is True else 0 if mode is False else int(mode)
+        check(lib.adc_cuda_chi2_set_precision(self._p, mode))
 
     def refresh(self):
         """Recompute what depends on the counts alone (1/c, C0, linear sums)

@@ -176,7 +176,7 @@ def test_gaussnd_accumulates_twice():
 CHI2_KEYS = ["gpoly_b2000", "gsum1_b1000", "gsum2_b1500"]
 
 
-@pytest.mark.parametrize("fast", [False, True])
+@pytest.mark.parametrize("fast", [0, 1, 2])
 @pytest.mark.parametrize("key", CHI2_KEYS)
 def test_chi2_golden(restate, key, fast):
     g = golden("chi2_cases.npz")
