@@ -33,7 +33,7 @@
 namespace adcb {
 
 constexpr int kTileThreads = 256;
-constexpr int kChunkThreads = 256;
+constexpr int kChunkThreads = 1024;  // one warp per record entry: the grid is only nchunks CTAs
 
 // Uniform data for one pass, staged in device memory so CUDA-graph replays
 // pick up new parameters from a pinned host buffer.
@@ -282,7 +282,9 @@ __device__ __forceinline__ void bin_accumulate(const BinTerm<M, GRAD, FAST>& t, 
 // one ulp per bin (<= bpt + 2 ulp relative while e_0 is a normal number;
 // below that the absolute error is < 1e-290).  Used when |D| bpt <= 1 (a
 // run spans at most one sigma): then e_0 A^k = e_k / B_k <= e^(1/2), so the
-// product cannot overflow.
+// product cannot overflow; and when bpt >= 16 (shorter runs, e.g. the 4 bins
+// per thread below ~600K bins, pay more for the two anchor exps than they
+// save).
 constexpr int kRecMaxBpt = 192;
 
 template <class M, bool GRAD, bool FAST, bool CHECK, int ILP, bool NUM, bool REC = false>
@@ -397,7 +399,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) chi2_tile_kernel(Chi2Pass 
   __shared__ double rdl[REC ? M::NG : 1];
   if constexpr (REC) {
     // D per Gaussian factor and the B_k table (uniform; see tile_bins)
-    use_rec = P.bpt <= kRecMaxBpt;
+    use_rec = P.bpt >= 16 && P.bpt <= kRecMaxBpt;  // short runs: the anchors cost more
 #pragma unroll
     for (int c = 0; c < M::NG; ++c) {
       double mu, inv;

@@ -13,5 +13,13 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:gaus
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:chi2_tile -s 3 -c 1 -o gpurun_out/prof_chi2 python tools/probe_chi2.py 100000000 0 > gpurun_out/ncu2.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:adc_kernel -s 2 -c 1 -o gpurun_out/prof_jit python tools/probe_jit.py > gpurun_out/ncu3.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:shared_p_tma -s 2 -c 1 -o gpurun_out/prof_sharedp python tools/probe_shared_p.py > gpurun_out/ncu4.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:shared_p_vec2 -s 2 -c 1 -o gpurun_out/prof_spv python tools/probe_shared_p.py > gpurun_out/ncu6.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gaussnd_tile -c 1 -o gpurun_out/prof_nd1000 python tools/probe_gaussnd_variants.py 1000 1000000 0 > gpurun_out/ncu7.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:chi2_multi -s 20 -c 1 -o gpurun_out/prof_multi python tools/probe_fit_1e6.py > gpurun_out/ncu5.log 2>&1
 ls gpurun_out
+# summaries here (the box's ncu), then drop the big reports so gpurun_out/
+# stays under the 64 MiB copy-back limit (keep the two headline captures)
+python tools/ncu_summary.py gpurun_out/prof_*.ncu-rep > gpurun_out/ncu_summary.txt 2>&1
+python tools/ncu_fp64_per_unit.py gpurun_out/prof_chi2.ncu-rep 1e8 >> gpurun_out/ncu_summary.txt 2>&1
+for f in gpurun_out/prof_*.ncu-rep; do case "$f" in *prof_gaussnd.ncu-rep|*prof_chi2.ncu-rep) ;; *) rm -f "$f";; esac; done
+du -sh gpurun_out
