@@ -207,6 +207,48 @@ def test_chi2_config3_1e6(restate):
     assert abs(c2 - vref) <= 1e-12 * vscale
 
 
+@pytest.mark.parametrize("model,q", [
+    ("gpoly", synth.GPOLY_INIT),
+    ("gsum", (0.9, 0.1, 1.4)),
+    ("gsum", (0.7, -1.0, 1.2, 0.4, 1.5, 0.8)),
+])
+def test_chi2_gaussian_recurrence(restate, model, q):
+    """Precision mode 2 (default): gradient passes take each thread's Gaussian
+    factors from the anchored product recurrence (bpt >= 16 from ~1.2M bins
+    here 2M bins, 28 per thread).  Against the compensated oracle within the
+    reduction tolerance, within ~1e-13 of mode 1's per-bin table exp, and the
+    value pass is the same in both modes."""
+    bins = 2_000_000
+    q = np.array(q)
+    counts, ev = synth.histogram(bins, events=2e8, seed=21, model=model, q=q)
+    h = adc.Histogram(bins, -5.0, 5.0, ev, counts)
+    plan = adc.Chi2Plan(model, q.size, h)
+    assert plan.layout.tile_bins // 256 >= 16
+    g2, c2 = plan.gradient(q)
+    ref, scale = restate.chi2_gradient_compensated(model, counts, -5.0, 5.0, ev, q)
+    assert np.all(np.abs(g2 - ref) <= 1e-12 * scale)
+    v2 = plan.chi2(q)
+    plan.set_precision(1)
+    g1, c1 = plan.gradient(q)
+    assert np.all(np.abs(g2 - g1) <= 1e-13 * scale)
+    assert plan.chi2(q) == v2  # value passes do not use the recurrence
+    assert g2.tobytes() != g1.tobytes()  # ... and the gradient pass really did
+
+
+def test_chi2_recurrence_skipped_for_wide_runs():
+    """When a thread's run of bins spans more than one sigma (|D| bpt > 1) the
+    recurrence is not used: mode 2 is bitwise mode 1."""
+    bins = 2_000_000
+    q = np.array([1.0, 0.3, 0.004, 0.2, -0.01, 0.003])  # sigma = 0.004: D = 0.32, bpt 28
+    counts, ev = synth.histogram(bins, events=2e8, seed=23, model="gpoly", q=q)
+    h = adc.Histogram(bins, -5.0, 5.0, ev, counts)
+    plan = adc.Chi2Plan("gpoly", 6, h)
+    g2, _ = plan.gradient(q)
+    plan.set_precision(1)
+    g1, _ = plan.gradient(q)
+    assert g2.tobytes() == g1.tobytes()
+
+
 def test_chi2_sharding_bitwise_invariant():
     # Any split of whole chunks over ranks gives the same bits (fixed trees).
     counts, ev = synth.histogram(3_000_000, events=3e8, seed=9)
