@@ -253,11 +253,11 @@ enum { ADC_PROVIDER_AD_REVERSE = 0, ADC_PROVIDER_NUMERIC = 1 };
 int adc_cuda_chi2_set_provider(adc_chi2_plan* plan, int32_t provider);
 /* Selects per-bin arithmetic: 0 = faithful (IEEE divisions exactly as the
  * generated code), 1 = fast (reciprocal multiplies, table-driven exp; within
- * the reduction tolerance), 2 = fast, and gradient passes evaluate each
- * thread's run of Gaussian factors exp(-z^2/2) by an anchored product
- * recurrence (two multiplies per bin, <= bpt + 2 ulp; models with <= 2
- * Gaussian factors, when a thread's run spans at most one sigma).  Value
- * passes are identical in modes 1 and 2.  Default 2. */
+ * the reduction tolerance), 2 = fast, and every pass (gradient, value,
+ * batched line search) evaluates each thread's run of Gaussian factors
+ * exp(-z^2/2) by an anchored product recurrence (two multiplies per bin,
+ * <= bpt + 2 ulp; models with <= 2 Gaussian factors, runs of >= 16 bins that
+ * span at most one sigma).  Default 2. */
 int adc_cuda_chi2_set_precision(adc_chi2_plan* plan, int32_t mode);
 
 /* ---------------------------------------------------------------------------

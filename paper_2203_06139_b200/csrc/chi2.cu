@@ -484,7 +484,7 @@ __host__ __device__ constexpr int multi_ilp() {
   return M::NP <= 6 ? 4 : M::NP <= 12 ? 2 : 1;
 }
 
-template <class M>
+template <class M, bool REC = false>
 __global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P, int ncand) {
   constexpr int G = kMultiGroup, CG = multi_ilp<M>();
   if (P.ncand_dev != nullptr) ncand = *P.ncand_dev;  // set on the device (fit graph)
@@ -501,6 +501,34 @@ __global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P,
     Q[c].inv[i] = src[kMaxNp + i];
   }
   if (threadIdx.x < 64) tab[threadIdx.x] = exp2((double)threadIdx.x / 64.0);
+  // REC: per candidate the value pass's decision, D and B_k table (tile_bins)
+  __shared__ double rtab[REC ? G * M::NG * kRecMaxBpt : 1];
+  __shared__ double rdl[REC ? G * M::NG : 1];
+  __shared__ bool ruse[REC ? G : 1];
+  if constexpr (REC) {
+    __syncthreads();
+    if (threadIdx.x < G) {
+      const typename M::Reg QR = M::load(Q[threadIdx.x]);
+      bool use = P.bpt >= 16 && P.bpt <= kRecMaxBpt;
+#pragma unroll
+      for (int c = 0; c < M::NG; ++c) {
+        double mu, inv;
+        M::gauss(QR, c, mu, inv);
+        const double dl = fmul((double)kTileThreads * P.width, inv);
+        use = use && fabs(dl) * P.bpt <= 1.0;
+        rdl[threadIdx.x * M::NG + c] = dl;
+      }
+      ruse[threadIdx.x] = use;
+    }
+    __syncthreads();
+    for (int v = threadIdx.x; v < G * M::NG * P.bpt; v += kTileThreads) {
+      const int cg = v / P.bpt, k = v % P.bpt;  // cg = candidate * NG + factor
+      if (ruse[cg / M::NG]) {
+        const double kd = fmul((double)k, rdl[cg]);
+        rtab[cg * kRecMaxBpt + k] = exp(fmul(fmul(-0.5, kd), kd));
+      }
+    }
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int R = 1 + 3 * ncand;
@@ -524,6 +552,20 @@ __global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P,
 #pragma unroll
         for (int cc = 0; cc < CG; ++cc) a0[cc] = a1[cc] = a2[cc] = 0.0;
         double jh = fadd((double)base, 0.5);
+        [[maybe_unused]] double rP[REC ? CG * M::NG : 1], rA[REC ? CG * M::NG : 1];
+        if constexpr (REC) {  // the anchors of tile_bins, per candidate
+          const double x0 = fadd(P.lo, fmul(jh, P.width));
+#pragma unroll
+          for (int cc = 0; cc < CG; ++cc)
+#pragma unroll
+            for (int c = 0; c < M::NG; ++c) {
+              double mu, inv;
+              M::gauss(QR[cc], c, mu, inv);
+              const double z0 = fmul(fsub(x0, mu), inv);
+              rP[cc * M::NG + c] = exp_nonpos(fmul(fmul(-0.5, z0), z0), tab);
+              rA[cc * M::NG + c] = exp(-fmul(z0, rdl[(c0 + cc) * M::NG + c]));
+            }
+        }
         for (int k = 0; k < BPT; ++k) {
           const int64_t j = base + (int64_t)k * kTileThreads;
           if (j < P.bin_end) {
@@ -533,7 +575,17 @@ __global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P,
 #pragma unroll
             for (int cc = 0; cc < CG; ++cc) {
               double m, bg[1];
-              M::template eval<false, true>(x, QR[cc], tab, m, bg);
+              if (REC && ruse[c0 + cc]) {
+                double e[M::NG];
+#pragma unroll
+                for (int c = 0; c < M::NG; ++c) {
+                  e[c] = fmul(rP[cc * M::NG + c], rtab[((c0 + cc) * M::NG + c) * kRecMaxBpt + k]);
+                  rP[cc * M::NG + c] = fmul(rP[cc * M::NG + c], rA[cc * M::NG + c]);
+                }
+                M::template eval<false, true>(x, QR[cc], tab, m, bg, e);
+              } else {
+                M::template eval<false, true>(x, QR[cc], tab, m, bg);
+              }
               const double mc = m * ic;
               a0[cc] += m;
               a1[cc] = __fma_rn(w, m, a1[cc]);
@@ -747,8 +799,9 @@ static void launch_tiles_t(const Chi2Pass& P, int blocks, cudaStream_t s) {
   chi2_tile_kernel<M, GRAD, FAST, MB, 1, false, REC><<<blocks, kTileThreads, 0, s>>>(P);
 }
 
-// prec: 0 faithful, 1 fast, 2 fast + the Gaussian-factor recurrence in the
-// gradient pass (value passes are the same in modes 1 and 2)
+// prec: 0 faithful, 1 fast, 2 fast + the Gaussian-factor recurrence (every
+// pass: gradient, value and the multi-candidate pass, which repeats the value
+// pass's per-candidate decision and arithmetic)
 template <class M>
 static void launch_tiles_m(const Chi2Pass& P, bool grad, int prec, bool num, int blocks,
                            cudaStream_t s) {
@@ -766,7 +819,8 @@ static void launch_tiles_m(const Chi2Pass& P, bool grad, int prec, bool num, int
     else if (fast) launch_tiles_t<M, true, true>(P, blocks, s);
     else launch_tiles_t<M, true, false>(P, blocks, s);
   } else {
-    if (fast) launch_tiles_t<M, false, true>(P, blocks, s);
+    if (prec == 2 && M::NG <= 2) launch_tiles_t<M, false, true, M::NG <= 2>(P, blocks, s);
+    else if (fast) launch_tiles_t<M, false, true>(P, blocks, s);
     else launch_tiles_t<M, false, false>(P, blocks, s);
   }
 }
@@ -843,7 +897,8 @@ int chi2_lin_enqueue(const Chi2Pass& P, int model, int64_t chunk_tiles, double* 
 }
 
 int chi2_multi_enqueue(const Chi2Pass& P, int model, int np, int ncand,
-                       int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin) {
+                       int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin,
+                       int prec) {
   const int64_t ntiles = P.tile_end - P.tile_begin;
   if (ntiles <= 0) return ADC_OK;
   if (ncand < 1 || ncand > kMultiMax) return fail(ADC_E_ARG, "chi2 multi: bad candidate count");
@@ -851,6 +906,12 @@ int chi2_multi_enqueue(const Chi2Pass& P, int model, int np, int ncand,
                   (unsigned)((ncand + kMultiGroup - 1) / kMultiGroup));
   auto go = [&](auto model_tag) {
     using M = decltype(model_tag);
+    if constexpr (M::NG <= 2) {
+      if (prec == 2) {
+        chi2_multi_kernel<M, true><<<grid, kTileThreads, 0, s>>>(P, ncand);
+        return;
+      }
+    }
     chi2_multi_kernel<M><<<grid, kTileThreads, 0, s>>>(P, ncand);
   };
   if (model == ADC_MODEL_GPOLY) {

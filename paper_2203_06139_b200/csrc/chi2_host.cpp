@@ -626,7 +626,7 @@ extern "C" int adc_cuda_chi2_multi(adc_chi2_plan* P, const double* qs, int32_t n
   pass.qdev = P->qmulti;
   pass.tile_ws = P->tile_ws_multi;
   if (int rc = chi2_multi_enqueue(pass, P->model, P->np, ncand, P->L.chunk_tiles,
-                                  P->records_multi, P->stream, P->lin))
+                                  P->records_multi, P->stream, P->lin, P->fast))
     return rc;
   const int R = 1 + 3 * ncand;
   if (int rc = collect_enqueue(P, P->records_multi, R, 1, P->stream)) return rc;
@@ -818,7 +818,7 @@ int build_fit_graph(adc_chi2_plan* P, const FitDevConst& c) {
     pass.tile_ws = P->tile_ws_multi;
     pass.ncand_dev = P->ncand_dev;
     rc = chi2_multi_enqueue(pass, P->model, P->np, kMultiMax, P->L.chunk_tiles, P->records_multi,
-                            s, P->lin);
+                            s, P->lin, P->fast);
   }
   if (rc == ADC_OK)
     rc = fit_device_enqueue_accept(P->fit_st, P->records_multi, P->fit_scratch, nchunks,

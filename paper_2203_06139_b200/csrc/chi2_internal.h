@@ -42,7 +42,8 @@ int chi2_lin_enqueue(const Chi2Pass& P, int model, int64_t chunk_tiles, double* 
 // ncand: candidates; with P.ncand_dev set, ncand is the upper bound (grid)
 // and the actual count is read on the device.
 int chi2_multi_enqueue(const Chi2Pass& P, int model, int np, int ncand,
-                       int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin);
+                       int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin,
+                       int prec);
 void fill_qdev(int model, int np, const double* q, double* host_qdev);
 size_t qdev_bytes();
 int chi2_set_tune(int v);

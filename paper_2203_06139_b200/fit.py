@@ -152,7 +152,7 @@ class Chi2Plan:
 
     def set_precision(self, mode):
         """0 / False: faithful IEEE divisions; 1: fast (reciprocal multiplies,
-        table exp); 2 / True (default): fast, and gradient passes take each
+        table exp); 2 / True (default): fast, and every pass takes each
         thread's Gaussian factors from an anchored product recurrence."""
         mode = 2 if mode is True else 0 if mode is False else int(mode)
         check(lib.adc_cuda_chi2_set_precision(self._p, mode))

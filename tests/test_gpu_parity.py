@@ -216,8 +216,9 @@ def test_chi2_gaussian_recurrence(restate, model, q):
     """Precision mode 2 (default): gradient passes take each thread's Gaussian
     factors from the anchored product recurrence (bpt >= 16 from ~1.2M bins
     here 2M bins, 28 per thread).  Against the compensated oracle within the
-    reduction tolerance, within ~1e-13 of mode 1's per-bin table exp, and the
-    value pass is the same in both modes."""
+    reduction tolerance and within ~1e-13 of mode 1's per-bin table exp; the
+    same for the value pass, and the batched line-search pass repeats the
+    value pass bit for bit per candidate."""
     bins = 2_000_000
     q = np.array(q)
     counts, ev = synth.histogram(bins, events=2e8, seed=21, model=model, q=q)
@@ -228,11 +229,16 @@ def test_chi2_gaussian_recurrence(restate, model, q):
     ref, scale = restate.chi2_gradient_compensated(model, counts, -5.0, 5.0, ev, q)
     assert np.all(np.abs(g2 - ref) <= 1e-12 * scale)
     v2 = plan.chi2(q)
+    vref, vscale = restate.chi2_compensated(model, counts, -5.0, 5.0, ev, q)
+    assert abs(v2 - vref) <= 1e-12 * vscale
+    g = np.linspace(0.5, 1.5, q.size) * 1e-3 * np.abs(q)
+    qs = np.stack([q - 2.0 ** -k * g for k in range(9)])
+    assert plan.chi2_multi(qs).tobytes() == np.array([plan.chi2(qk) for qk in qs]).tobytes()
     plan.set_precision(1)
     g1, c1 = plan.gradient(q)
     assert np.all(np.abs(g2 - g1) <= 1e-13 * scale)
-    assert plan.chi2(q) == v2  # value passes do not use the recurrence
-    assert g2.tobytes() != g1.tobytes()  # ... and the gradient pass really did
+    assert abs(plan.chi2(q) - v2) <= 1e-13 * vscale
+    assert g2.tobytes() != g1.tobytes()  # the recurrence really ran
 
 
 def test_chi2_recurrence_skipped_for_wide_runs():
