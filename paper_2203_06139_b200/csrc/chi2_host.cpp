@@ -156,7 +156,8 @@ struct adc_chi2_plan {
   double* fit_scratch = nullptr;
   int* ncand_dev = nullptr;
   cudaGraphExec_t fit_graph = nullptr;
-  cudaEvent_t fit_ev[2] = {nullptr, nullptr};
+  double* fit_trace = nullptr;  // device iterate trace of the fit loop
+  int fit_trace_cap = 0;
   FitDevConst fit_const{};
   // q-independent basis sums of the linear parameters (chi2_lin_enqueue)
   double* lin = nullptr;      // per local chunk [G0_lin[L], G1_lin[L], C0]
@@ -508,8 +509,7 @@ extern "C" int adc_cuda_chi2_plan_destroy(adc_chi2_plan* P) {
   if (P->h_fit_st) cudaFreeHost(P->h_fit_st);
   if (P->fit_scratch) cudaFree(P->fit_scratch);
   if (P->ncand_dev) cudaFree(P->ncand_dev);
-  for (auto& e : P->fit_ev)
-    if (e) cudaEventDestroy(e);
+  if (P->fit_trace) cudaFree(P->fit_trace);
   if (P->stream) cudaStreamDestroy(P->stream);
   delete P;
   return ADC_OK;
@@ -779,9 +779,13 @@ bool damped_solve(std::vector<double> h, std::vector<double> g, double lambda, i
 }  // namespace
 
 namespace {
-// Builds (once per plan and option set) the graph of one device-resident
-// steepest-descent iteration: QDev from the device parameters, the gradient
-// pass, finalize + trials, the multi-candidate pass, selection, copy-back.
+// Builds (once per plan and option set) the device-resident fit loop: ONE
+// graph whose WHILE conditional node repeats the steepest-descent iteration
+// body — QDev from the device parameters, the gradient pass, finalize +
+// trials, the multi-candidate pass, selection, the loop bookkeeping — until
+// the loop-control kernel clears the condition (converged, budget spent, or
+// a line search that needs more trials than one batch).  No host round trip
+// between iterations.
 int build_fit_graph(adc_chi2_plan* P, const FitDevConst& c) {
   const int64_t nchunks = P->L.nchunks;
   const int Rmax = adc_chi2_record_len(P->np, 1);
@@ -791,8 +795,6 @@ int build_fit_graph(adc_chi2_plan* P, const FitDevConst& c) {
     const size_t scratch = std::max<size_t>((size_t)nchunks * Rmax, (size_t)kMultiMax * nchunks * 4);
     ADCB_CUDA(cudaMalloc(&P->fit_scratch, scratch * sizeof(double)));
     ADCB_CUDA(cudaMalloc(&P->ncand_dev, sizeof(int)));
-    ADCB_CUDA(cudaEventCreate(&P->fit_ev[0]));
-    ADCB_CUDA(cudaEventCreate(&P->fit_ev[1]));
   }
   if (P->fit_graph != nullptr && std::memcmp(&P->fit_const, &c, sizeof(c)) == 0) return ADC_OK;
   if (P->fit_graph) cudaGraphExecDestroy(P->fit_graph);
@@ -802,13 +804,30 @@ int build_fit_graph(adc_chi2_plan* P, const FitDevConst& c) {
   if (int rc = ensure_multi(P)) return rc;
   cudaStream_t s = P->stream;
   cudaGraph_t g = nullptr;
-  ADCB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  ADCB_CUDA(cudaGraphCreate(&g, 0));
+  auto fail_graph = [&](cudaError_t e, const char* what) {
+    cudaGraphDestroy(g);
+    return cuda_fail(e, what);
+  };
+  cudaGraphConditionalHandle h;
+  cudaError_t e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
+  if (e != cudaSuccess) return fail_graph(e, "cudaGraphConditionalHandleCreate");
+  cudaGraphNodeParams wp{};
+  wp.type = cudaGraphNodeTypeConditional;
+  wp.conditional.handle = h;
+  wp.conditional.type = cudaGraphCondTypeWhile;
+  wp.conditional.size = 1;
+  cudaGraphNode_t wnode;
+  e = cudaGraphAddNode(&wnode, g, nullptr, 0, &wp);
+  if (e != cudaSuccess) return fail_graph(e, "cudaGraphAddNode (while)");
+  cudaGraph_t body = wp.conditional.phGraph_out[0];
+  e = cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
+                                    cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return fail_graph(e, "cudaStreamBeginCaptureToGraph (fit body)");
   int rc = fit_device_enqueue_qdev(P->fit_st, P->model, P->np, P->qdev, s);
-  if (rc == ADC_OK) rc = cudaEventRecordWithFlags(P->fit_ev[0], s, cudaEventRecordExternal) == cudaSuccess ? ADC_OK : ADC_E_CUDA;
   if (rc == ADC_OK)
     rc = chi2_enqueue(make_pass(P), P->model, P->np, true, P->fast, P->L.chunk_tiles, P->records,
                       s, P->lin);
-  if (rc == ADC_OK) rc = cudaEventRecordWithFlags(P->fit_ev[1], s, cudaEventRecordExternal) == cudaSuccess ? ADC_OK : ADC_E_CUDA;
   if (rc == ADC_OK)
     rc = fit_device_enqueue_grad(P->fit_st, P->records, P->fit_scratch, nchunks, P->np, P->model,
                                  P->events, c, P->qmulti, P->ncand_dev, s);
@@ -823,21 +842,18 @@ int build_fit_graph(adc_chi2_plan* P, const FitDevConst& c) {
   if (rc == ADC_OK)
     rc = fit_device_enqueue_accept(P->fit_st, P->records_multi, P->fit_scratch, nchunks,
                                    P->events, c, s);
-  if (rc == ADC_OK)
-    rc = cudaMemcpyAsync(P->h_fit_st, P->fit_st, sizeof(FitDevState), cudaMemcpyDeviceToHost, s) ==
-                 cudaSuccess
-             ? ADC_OK
-             : ADC_E_CUDA;
-  cudaError_t e = cudaStreamEndCapture(s, &g);
+  if (rc == ADC_OK) rc = fit_device_enqueue_loop_ctl(P->fit_st, h, c, s);
+  cudaGraph_t captured = nullptr;
+  e = cudaStreamEndCapture(s, &captured);
   if (rc != ADC_OK) {
-    if (g) cudaGraphDestroy(g);
+    cudaGraphDestroy(g);
     if (rc == ADC_E_CUDA) return fail(ADC_E_CUDA, "fit graph capture");
     return rc;
   }
-  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture (fit)");
+  if (e != cudaSuccess) return fail_graph(e, "cudaStreamEndCapture (fit body)");
   e = cudaGraphInstantiate(&P->fit_graph, g, 0);
   cudaGraphDestroy(g);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate (fit)");
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate (fit loop)");
   return ADC_OK;
 }
 }  // namespace
@@ -891,94 +907,115 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
     c.armijo_c1 = opts->armijo_c1;
     c.nclamp = nclamp;
     for (int k = 0; k < nclamp; ++k) c.clamp_idx[k] = clamp_idx[k];
+    c.np = np;
+    if (iterates != nullptr && opts->trace_iterates > 1) {
+      if (P->fit_trace_cap < opts->trace_iterates) {
+        if (P->fit_trace) cudaFree(P->fit_trace);
+        P->fit_trace = nullptr;
+        P->fit_trace_cap = 0;
+        ADCB_CUDA(cudaMalloc(&P->fit_trace, (size_t)opts->trace_iterates * kMaxNp * sizeof(double)));
+        P->fit_trace_cap = opts->trace_iterates;
+      }
+      c.trace = P->fit_trace;
+      c.trace_cap = opts->trace_iterates;
+    }
     if (int rc = build_fit_graph(P, c)) return rc;
-    std::memset(P->h_fit_st, 0, sizeof(FitDevState));
-    for (int i = 0; i < np; ++i) P->h_fit_st->q[i] = q[i];
-    P->h_fit_st->cur = cur;
-    P->h_fit_st->first_batch = first_batch;
-    ADCB_CUDA(cudaMemcpyAsync(P->fit_st, P->h_fit_st, sizeof(FitDevState), cudaMemcpyHostToDevice,
-                              P->stream));
-    ADCB_CUDA(cudaStreamSynchronize(P->stream));
-  }
-  for (int iter = 0; iter < opts->budget; ++iter) {
-    if (dev_mode) {
-      // one graph = gradient pass + finalize + trials + multi pass + selection
+    FitDevState& st = *P->h_fit_st;
+    std::memset(&st, 0, sizeof(FitDevState));
+    for (int i = 0; i < np; ++i) st.q[i] = q[i];
+    st.cur = cur;
+    st.first_batch = first_batch;
+    st.budget = opts->budget;
+    const uint64_t chi2_evals0 = res.chi2_evals;
+    const int clamps0 = res.sigma_clamps;
+    while (st.passes < st.budget) {
+      // device loop: iterations until converged, budget spent or NeedHost
+      ADCB_CUDA(cudaMemcpyAsync(P->fit_st, &st, sizeof(FitDevState), cudaMemcpyHostToDevice,
+                                P->stream));
       ADCB_CUDA(cudaGraphLaunch(P->fit_graph, P->stream));
+      ADCB_CUDA(cudaMemcpyAsync(&st, P->fit_st, sizeof(FitDevState), cudaMemcpyDeviceToHost,
+                                P->stream));
       ADCB_CUDA(cudaStreamSynchronize(P->stream));
-      FitDevState& st = *P->h_fit_st;
-      float ms = 0.f;
-      ADCB_CUDA(cudaEventElapsedTime(&ms, P->fit_ev[0], P->fit_ev[1]));
-      res.gradient_ns += (uint64_t)(ms * 1e6);
-      ++res.gradient_evals;
-      if (st.status == kFitConvergedGrad) {
+      q.assign(st.q, st.q + np);
+      cur = st.cur;
+      if (st.status == kFitConvergedGrad || st.status == kFitConvergedRelDec ||
+          st.status == kFitConvergedNoStep) {
         res.converged = 1;
         break;
       }
-      res.chi2_evals += (uint64_t)st.evals;
-      bool accepted = st.accepted_k >= 0;
-      double next = st.cur, rel_dec = st.rel_dec;
-      if (accepted) {
-        res.sigma_clamps += st.sigma_clamps;
-        for (int i = 0; i < np; ++i) q[i] = st.q[i];
-      } else if (st.status == kFitNeedHost) {
-        // the first batch held no acceptable step: continue the same search
-        // (t_next, t_next/2, ...) with host-driven batches, then hand the
-        // state back to the device
-        int tried = st.evals;
-        std::vector<double> trials, tvals, c2s(kMultiMax);
-        std::vector<int> cls;
-        double t = st.t_next;
-        while (t >= 1e-18 && !accepted) {
-          trials.clear();
-          tvals.clear();
-          cls.clear();
-          for (double tt = t; tt >= 1e-18 && (int)tvals.size() < kMultiMax; tt *= 0.5) {
-            trial = q;
-            for (int i = 0; i < np; ++i) trial[i] -= tt * st.g[i];
-            cls.push_back(clamp(trial));
-            trials.insert(trials.end(), trial.begin(), trial.end());
-            tvals.push_back(tt);
-          }
-          if (tvals.empty()) break;
-          if (int rc = adc_cuda_chi2_multi(P, trials.data(), (int32_t)tvals.size(), c2s.data()))
-            return rc;
-          for (size_t k = 0; k < tvals.size(); ++k) {
-            ++res.chi2_evals;
-            ++tried;
-            if (c2s[k] <= cur - opts->armijo_c1 * tvals[k] * st.gd) {
-              accepted = true;
-              next = c2s[k];
-              res.sigma_clamps += cls[k];
-              trial.assign(trials.begin() + k * np, trials.begin() + (k + 1) * np);
-              break;
-            }
-          }
-          t = tvals.back() * 0.5;
+      if (st.status != kFitNeedHost) break;  // running: the budget is spent
+      // the first batch held no acceptable step: continue the same search
+      // (t_next, t_next/2, ...) with host-driven batches, then hand the state
+      // back to the device loop
+      bool accepted = false;
+      double next = cur;
+      int tried = st.evals;
+      std::vector<double> trials, tvals, c2s(kMultiMax);
+      std::vector<int> cls;
+      double t = st.t_next;
+      while (t >= 1e-18 && !accepted) {
+        trials.clear();
+        tvals.clear();
+        cls.clear();
+        for (double tt = t; tt >= 1e-18 && (int)tvals.size() < kMultiMax; tt *= 0.5) {
+          trial = q;
+          for (int i = 0; i < np; ++i) trial[i] -= tt * st.g[i];
+          cls.push_back(clamp(trial));
+          trials.insert(trials.end(), trial.begin(), trial.end());
+          tvals.push_back(tt);
         }
-        if (accepted) {
-          rel_dec = (cur - next) / std::max(1.0, std::fabs(cur));
-          q = trial;
-          for (int i = 0; i < np; ++i) st.q[i] = q[i];
-          st.cur = next;
-          st.first_batch = std::min(kMultiMax, std::max(8, (tried + 8 + 7) / 8 * 8));
-          ADCB_CUDA(cudaMemcpyAsync(P->fit_st, P->h_fit_st, sizeof(FitDevState),
-                                    cudaMemcpyHostToDevice, P->stream));
-          ADCB_CUDA(cudaStreamSynchronize(P->stream));
+        if (tvals.empty()) break;
+        if (int rc = adc_cuda_chi2_multi(P, trials.data(), (int32_t)tvals.size(), c2s.data()))
+          return rc;
+        for (size_t k = 0; k < tvals.size(); ++k) {
+          ++st.evals_total;
+          ++tried;
+          if (c2s[k] <= cur - opts->armijo_c1 * tvals[k] * st.gd) {
+            accepted = true;
+            next = c2s[k];
+            st.clamps_total += cls[k];
+            trial.assign(trials.begin() + k * np, trials.begin() + (k + 1) * np);
+            break;
+          }
         }
+        t = tvals.back() * 0.5;
       }
       if (!accepted) {
         res.converged = 1;
         break;
       }
+      const double rel_dec = (cur - next) / std::max(1.0, std::fabs(cur));
+      q = trial;
       cur = next;
-      ++res.iterations;
-      if (opts->trace_iterates > res.iterations) trace(q);
+      for (int i = 0; i < np; ++i) st.q[i] = q[i];
+      st.cur = next;
+      st.first_batch = std::min(kMultiMax, std::max(8, (tried + 8 + 7) / 8 * 8));
+      st.iters += 1;
+      if (c.trace != nullptr && c.trace_cap > st.iters)
+        ADCB_CUDA(cudaMemcpy(c.trace + (size_t)st.iters * np, q.data(), np * sizeof(double),
+                             cudaMemcpyHostToDevice));
       if (rel_dec <= opts->chi2_rel_tol) {
         res.converged = 1;
         break;
       }
-      continue;
     }
+    res.iterations = st.iters;
+    res.gradient_evals = st.n_grad;
+    res.gradient_ns = st.grad_ns;
+    res.chi2_evals = chi2_evals0 + (uint64_t)st.evals_total;
+    res.sigma_clamps = clamps0 + st.clamps_total;
+    if (c.trace != nullptr) {
+      const int rows = std::min(opts->trace_iterates, st.iters + 1);
+      if (rows > 1)
+        ADCB_CUDA(cudaMemcpy(iterates + np, c.trace + np, (size_t)(rows - 1) * np * sizeof(double),
+                             cudaMemcpyDeviceToHost));
+    }
+    std::memcpy(params, q.data(), np * sizeof(double));
+    res.chi2 = cur;
+    *result = res;
+    return ADC_OK;
+  }
+  for (int iter = 0; iter < opts->budget; ++iter) {
     auto t0 = clk::now();
     if (int rc = adc_cuda_chi2_gradient(P, q.data(), g.data(), nullptr)) return rc;
     res.gradient_ns += (uint64_t)std::chrono::nanoseconds(clk::now() - t0).count();

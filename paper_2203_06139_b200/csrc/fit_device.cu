@@ -31,8 +31,17 @@ __device__ void write_qdev(double* dst, int model, int np, const double* q) {
   }
 }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void fit_qdev_kernel(FitDevState* st, int model, int np, double* qdev) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) write_qdev(qdev, model, np, st->q);
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    write_qdev(qdev, model, np, st->q);
+    st->t0 = globaltimer();  // the gradient pass starts after this kernel
+  }
 }
 
 // adc_chi2_finalize's fixed pairwise tree, one record column per thread.
@@ -43,27 +52,37 @@ __device__ void column_tree(double* r, int64_t nchunks, int R, int v) {
 
 // Gradient finalize (adc_chi2_finalize), convergence test, direction = g,
 // gd, and the first batch of Armijo trials t = 1, 1/2, ... (fit.cpp:383-403)
-// written as QDev rows for the multi-candidate pass.
+// written as QDev rows for the multi-candidate pass.  Everything the serial
+// part reads is staged in shared memory first (the kernel is latency-bound:
+// each dependent global round trip is ~0.5 us).
 __global__ void __launch_bounds__(128) fit_grad_kernel(FitDevState* st, const double* records,
                                                        double* scratch, int64_t nchunks, int np,
                                                        int model, double events, FitDevConst c,
                                                        double* qmulti, int* ncand_dev) {
   const int R = 4 + 3 * np;
-  for (int64_t k = threadIdx.x; k < nchunks * R; k += blockDim.x) scratch[k] = records[k];
-  __syncthreads();
-  for (int v = threadIdx.x; v < R; v += blockDim.x) column_tree(scratch, nchunks, R, v);
-  __syncthreads();
+  if (threadIdx.x == 0) st->grad_ns += globaltimer() - st->t0;  // the pass just ended
+  __shared__ double s_g[kMaxNp], s_q[kMaxNp], s_col[4 + 3 * kMaxNp];
   __shared__ double s_gd;
-  __shared__ int s_stop;
+  __shared__ int s_stop, s_want;
+  for (int64_t k = threadIdx.x; k < nchunks * R; k += blockDim.x) scratch[k] = records[k];
+  if (threadIdx.x < kMaxNp) s_q[threadIdx.x] = st->q[threadIdx.x];
+  if (threadIdx.x == 0) s_want = st->first_batch;
+  __syncthreads();
+  for (int v = threadIdx.x; v < R; v += blockDim.x) {
+    column_tree(scratch, nchunks, R, v);
+    s_col[v] = scratch[v];
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    const double S = scratch[0], A1 = scratch[1], A2 = scratch[2];
+    const double S = s_col[0], A1 = s_col[1], A2 = s_col[2];
     const double a = fdiv(events, S);
     const double t_sum = fsub(fmul(2.0, A1), fmul(fmul(2.0, a), A2));
     const double s_coef = fmul(fdiv(events, fmul(S, S)), t_sum);
     double gmax = 0.0;
     for (int i = 0; i < np; ++i) {
-      const double G0 = scratch[4 + i], G1 = scratch[4 + np + i], G2 = scratch[4 + 2 * np + i];
+      const double G0 = s_col[4 + i], G1 = s_col[4 + np + i], G2 = s_col[4 + 2 * np + i];
       const double gi = fsub(fmul(s_coef, G0), fmul(fmul(2.0, a), fsub(G1, fmul(a, G2))));
+      s_g[i] = gi;
       st->g[i] = gi;
       gmax = fmax(gmax, fabs(gi));
     }
@@ -73,7 +92,7 @@ __global__ void __launch_bounds__(128) fit_grad_kernel(FitDevState* st, const do
     st->sigma_clamps = 0;  // per iteration
     s_stop = gmax <= c.grad_tol;  // fit.cpp:340-344
     double gd = 0.0;
-    for (int i = 0; i < np; ++i) gd = fadd(gd, fmul(st->g[i], st->g[i]));  // direction = g
+    for (int i = 0; i < np; ++i) gd = fadd(gd, fmul(s_g[i], s_g[i]));  // direction = g
     st->gd = gd;
     s_gd = gd;
   }
@@ -88,13 +107,13 @@ __global__ void __launch_bounds__(128) fit_grad_kernel(FitDevState* st, const do
   }
   // Trial n (one per thread): t = 1/2^n exactly (the host's repeated *= 0.5),
   // trial = q - t g, the sigma clamp, and its QDev row.
-  const int want = st->first_batch;
+  const int want = s_want;
   for (int n = threadIdx.x; n < want; n += blockDim.x) {
     const double tt = ldexp(1.0, -n);
     if (!(tt >= 1e-18)) continue;
-    double* trial = st->trials + (size_t)n * kMaxNp;
+    double trial[kMaxNp];
     int cl = 0;
-    for (int i = 0; i < np; ++i) trial[i] = fsub(st->q[i], fmul(tt, st->g[i]));
+    for (int i = 0; i < np; ++i) trial[i] = fsub(s_q[i], fmul(tt, s_g[i]));
     for (int k = 0; k < c.nclamp; ++k) {
       const int i = c.clamp_idx[k];
       if (i >= 0 && i < np && trial[i] < c.sigma_min) {
@@ -102,6 +121,8 @@ __global__ void __launch_bounds__(128) fit_grad_kernel(FitDevState* st, const do
         ++cl;
       }
     }
+    double* dst = st->trials + (size_t)n * kMaxNp;
+    for (int i = 0; i < np; ++i) dst[i] = trial[i];
     st->cls[n] = cl;
     st->tvals[n] = tt;
     write_qdev(qmulti + (size_t)n * kQDoubles, model, np, trial);
@@ -113,6 +134,7 @@ __global__ void __launch_bounds__(128) fit_grad_kernel(FitDevState* st, const do
     *ncand_dev = n;
     st->status = kFitRunning;
   }
+  (void)s_gd;
 }
 
 // Each candidate's value record -> chi2 (adc_chi2_finalize, value form), then
@@ -121,12 +143,13 @@ __global__ void __launch_bounds__(kMultiMax) fit_accept_kernel(FitDevState* st,
                                                                const double* records,
                                                                double* scratch, int64_t nchunks,
                                                                double events, FitDevConst c) {
-  __shared__ double c2[kMultiMax];
+  __shared__ double c2[kMultiMax], s_t[kMultiMax];
   const int n = st->ncand;
   if (n == 0) return;  // converged on the gradient
   const int R = 1 + 3 * n;
   const int k = threadIdx.x;
   if (k < n) {
+    s_t[k] = st->tvals[k];
     double* r = scratch + (size_t)k * nchunks * 4;
     for (int64_t ch = 0; ch < nchunks; ++ch) {
       const double* src = records + ch * R;
@@ -135,19 +158,24 @@ __global__ void __launch_bounds__(kMultiMax) fit_accept_kernel(FitDevState* st,
       r[ch * 4 + 2] = src[3 + 3 * k];
       r[ch * 4 + 3] = src[0];
     }
-    for (int v = 0; v < 4; ++v) column_tree(r, nchunks, 4, v);
-    const double S = r[0], A1 = r[1], A2 = r[2], C0 = r[3];
+    double S, A1, A2, C0;
+    if (nchunks == 1) {
+      S = r[0], A1 = r[1], A2 = r[2], C0 = r[3];
+    } else {
+      for (int v = 0; v < 4; ++v) column_tree(r, nchunks, 4, v);
+      S = r[0], A1 = r[1], A2 = r[2], C0 = r[3];
+    }
     const double a = fdiv(events, S);
     const double two_a = fmul(2.0, a);
     c2[k] = fadd(fsub(C0, fmul(two_a, A1)), fmul(fmul(a, a), A2));
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
-  const double cur = st->cur;
+  const double cur = st->cur, gd = st->gd;
   for (int j = 0; j < n; ++j) {
-    st->evals += 1;
-    if (c2[j] <= fsub(cur, fmul(fmul(c.armijo_c1, st->tvals[j]), st->gd))) {
+    if (c2[j] <= fsub(cur, fmul(fmul(c.armijo_c1, s_t[j]), gd))) {
       const double next = c2[j];
+      st->evals = j + 1;
       st->accepted_k = j;
       st->sigma_clamps = st->cls[j];
       const double rel_dec = fdiv(fsub(cur, next), fmax(1.0, fabs(cur)));
@@ -160,12 +188,43 @@ __global__ void __launch_bounds__(kMultiMax) fit_accept_kernel(FitDevState* st,
       return;
     }
   }
-  const double t_next = fmul(st->tvals[n - 1], 0.5);
+  st->evals = n;
+  const double t_next = fmul(s_t[n - 1], 0.5);
   st->t_next = t_next;
   st->status = t_next >= 1e-18 ? kFitNeedHost : kFitConvergedNoStep;
 }
 
+// The host loop's per-pass bookkeeping (chi2_host.cpp adc_cuda_fit), then the
+// loop condition: another pass while the search accepted a step, the fit has
+// not converged and the budget is not spent.  NeedHost / NoStep / converged
+// states end the device loop and the host takes over.
+__global__ void fit_loop_ctl_kernel(FitDevState* st, cudaGraphConditionalHandle h,
+                                    FitDevConst c) {
+  if (threadIdx.x != 0) return;
+  unsigned int cont = 0;
+  st->passes += 1;
+  st->n_grad += 1;
+  if (st->status != kFitConvergedGrad) {
+    st->evals_total += st->evals;
+    if (st->accepted_k >= 0) {
+      st->clamps_total += st->sigma_clamps;
+      st->iters += 1;
+      if (c.trace != nullptr && c.trace_cap > st->iters)
+        for (int i = 0; i < c.np; ++i) c.trace[(size_t)st->iters * c.np + i] = st->q[i];
+      cont = st->status == kFitRunning && st->passes < st->budget;
+    }
+  }
+  cudaGraphSetConditional(h, cont);
+}
+
 }  // namespace
+
+int fit_device_enqueue_loop_ctl(FitDevState* st, cudaGraphConditionalHandle h,
+                                const FitDevConst& c, cudaStream_t s) {
+  fit_loop_ctl_kernel<<<1, 32, 0, s>>>(st, h, c);
+  ADCB_CUDA(cudaGetLastError());
+  return ADC_OK;
+}
 
 int fit_device_enqueue_qdev(FitDevState* st, int model, int np, double* qdev, cudaStream_t s) {
   fit_qdev_kernel<<<1, 32, 0, s>>>(st, model, np, qdev);

@@ -25,12 +25,19 @@ struct FitDevState {
   double trials[kMultiMax * kMaxNp];
   int cls[kMultiMax];
   int ncand, first_batch, status, accepted_k, sigma_clamps, evals;
+  // device loop (WHILE node) bookkeeping, cumulative over one fit
+  int passes, budget, iters, clamps_total, n_grad;
+  long long evals_total;
+  unsigned long long grad_ns, t0;  // gradient-pass time from %globaltimer
 };
 
 struct FitDevConst {
   double grad_tol, chi2_rel_tol, sigma_min, armijo_c1;
   int clamp_idx[kMaxNp];
   int nclamp;
+  int np;
+  double* trace;  // [trace_cap][np] iterates (row 0 written by the host)
+  int trace_cap;
 };
 
 int fit_device_enqueue_qdev(FitDevState* st, int model, int np, double* qdev, cudaStream_t s);
@@ -40,5 +47,9 @@ int fit_device_enqueue_grad(FitDevState* st, const double* records, double* scra
 int fit_device_enqueue_accept(FitDevState* st, const double* records, double* scratch,
                               int64_t nchunks, double events, const FitDevConst& c,
                               cudaStream_t s);
+// End of a loop body: the host loop's bookkeeping for the pass just run, then
+// the WHILE node's condition (continue while running and within budget).
+int fit_device_enqueue_loop_ctl(FitDevState* st, cudaGraphConditionalHandle h,
+                                const FitDevConst& c, cudaStream_t s);
 
 }  // namespace adcb

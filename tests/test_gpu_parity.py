@@ -626,15 +626,19 @@ def test_gaussnd_strided_views(restate):
         adc.launch_batch("gaussnd_grad_0_1", X[:, ::2], P[:, ::2], 1.3, DX[:, ::2], DP[:, ::2])
 
 
-@pytest.mark.parametrize("case", ["gpoly_1e6", "gsum1", "gsum2", "gsum4"])
+@pytest.mark.parametrize("case", ["gpoly_1e6", "gpoly_1e6_b1", "gpoly_1e6_b3", "gsum1", "gsum2",
+                                  "gsum4"])
 def test_device_fit_loop_bitwise_equals_host_loop(case):
-    """The device-resident iteration (one CUDA graph per steepest-descent step:
-    gradient pass, finalize, Armijo trials, multi pass, selection) takes exactly
-    the host-driven loop's steps: same iterates, chi2 and counters, bit for bit."""
+    """The device-resident loop (one graph, a WHILE node around the
+    steepest-descent body: gradient pass, finalize, Armijo trials, multi pass,
+    selection, loop control; the host only continues searches longer than a
+    batch) takes exactly the host-driven loop's steps: same iterates, chi2 and
+    counters, bit for bit — also when the budget ends the loop early."""
     import os
-    if case == "gpoly_1e6":
+    if case.startswith("gpoly_1e6"):
         counts, ev = synth.histogram(10**6, events=1e8, seed=11)
-        model, init, budget = "gpoly", list(synth.GPOLY_INIT), 400
+        budget = {"gpoly_1e6": 400, "gpoly_1e6_b1": 1, "gpoly_1e6_b3": 3}[case]
+        model, init = "gpoly", list(synth.GPOLY_INIT)
     else:
         k = int(case[-1])
         truth = adc.default_truth(k)
