@@ -36,6 +36,7 @@ struct FitDevConst {
   int clamp_idx[kMaxNp];
   int nclamp;
   int np;
+  int margin;     // line-search batch margin (adc_cuda_fit)
   double* trace;  // [trace_cap][np] iterates (row 0 written by the host)
   int trace_cap;
 };
