@@ -62,7 +62,6 @@ __global__ void __launch_bounds__(128) fit_grad_kernel(FitDevState* st, const do
   const int R = 4 + 3 * np;
   if (threadIdx.x == 0) st->grad_ns += globaltimer() - st->t0;  // the pass just ended
   __shared__ double s_g[kMaxNp], s_q[kMaxNp], s_col[4 + 3 * kMaxNp];
-  __shared__ double s_gd;
   __shared__ int s_stop, s_want;
   for (int64_t k = threadIdx.x; k < nchunks * R; k += blockDim.x) scratch[k] = records[k];
   if (threadIdx.x < kMaxNp) s_q[threadIdx.x] = st->q[threadIdx.x];
@@ -94,7 +93,6 @@ __global__ void __launch_bounds__(128) fit_grad_kernel(FitDevState* st, const do
     double gd = 0.0;
     for (int i = 0; i < np; ++i) gd = fadd(gd, fmul(s_g[i], s_g[i]));  // direction = g
     st->gd = gd;
-    s_gd = gd;
   }
   __syncthreads();
   if (s_stop) {
@@ -134,7 +132,6 @@ __global__ void __launch_bounds__(128) fit_grad_kernel(FitDevState* st, const do
     *ncand_dev = n;
     st->status = kFitRunning;
   }
-  (void)s_gd;
 }
 
 // Each candidate's value record -> chi2 (adc_chi2_finalize, value form), then
