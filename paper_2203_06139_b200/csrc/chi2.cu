@@ -374,6 +374,9 @@ __host__ __device__ constexpr bool pass_zero_entry(int v) {
 template <class M, bool GRAD, bool FAST, int MINB = tile_min_blocks<M, GRAD>(),
           int ILP = 1, bool NUM = false, bool REC = false>
 __global__ void __launch_bounds__(kTileThreads, MINB) chi2_tile_kernel(Chi2Pass P) {
+  // batched passes (blockIdx.y = member): own parameters and tile records
+  P.qdev += blockIdx.y * P.q_stride;
+  P.tile_ws += blockIdx.y * P.ws_stride;
   constexpr int NP = M::NP;
   constexpr int R = GRAD ? 4 + 3 * NP : 4;
   __shared__ QDev Q;
@@ -717,8 +720,10 @@ struct LinMerge {
 __global__ void __launch_bounds__(kChunkThreads) chi2_chunk_kernel(
     const double* __restrict__ tile_ws, int64_t ntiles, int R, int chunk_tiles,
     double* __restrict__ records, LinMerge lm = LinMerge{}, PeerPublish pub = PeerPublish{},
-    const int* ncand_dev = nullptr) {
+    const int* ncand_dev = nullptr, int64_t ws_stride = 0, int64_t rec_stride = 0) {
   if (ncand_dev != nullptr) R = 1 + 3 * *ncand_dev;  // multi records sized on the device
+  tile_ws += blockIdx.y * ws_stride;  // batched passes (blockIdx.y = member)
+  records += blockIdx.y * rec_stride;
   const int64_t chunk = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t t0 = chunk * chunk_tiles;
@@ -768,17 +773,17 @@ __global__ void __launch_bounds__(kChunkThreads) chi2_chunk_kernel(
 int g_chi2_tune = 0;  // experiment knob (ADC_CHI2_TUNE), see launch_tiles_t
 
 template <class M, bool GRAD, bool FAST, bool REC = false>
-static void launch_tiles_t(const Chi2Pass& P, int blocks, cudaStream_t s) {
+static void launch_tiles_t(const Chi2Pass& P, dim3 blocks, cudaStream_t s) {
   constexpr int MB = tile_min_blocks<M, GRAD>();
   if constexpr (std::is_same<M, GPoly>::value && FAST) {
     // experiments: 1 = one bin at a time; 3 = 2 bins, 3 CTAs/SM; 4 = 1 bin,
     // 3 CTAs/SM; 5 = 4 bins
     if (g_chi2_tune == 3) {
-      chi2_tile_kernel<M, GRAD, FAST, 3, 2, false, REC><<<sm_count() * 3, kTileThreads, 0, s>>>(P);
+      chi2_tile_kernel<M, GRAD, FAST, 3, 2, false, REC><<<dim3(sm_count() * 3, blocks.y), kTileThreads, 0, s>>>(P);
       return;
     }
     if (g_chi2_tune == 4) {
-      chi2_tile_kernel<M, GRAD, FAST, 3, 1, false, REC><<<sm_count() * 3, kTileThreads, 0, s>>>(P);
+      chi2_tile_kernel<M, GRAD, FAST, 3, 1, false, REC><<<dim3(sm_count() * 3, blocks.y), kTileThreads, 0, s>>>(P);
       return;
     }
     if (g_chi2_tune == 5) {
@@ -803,7 +808,7 @@ static void launch_tiles_t(const Chi2Pass& P, int blocks, cudaStream_t s) {
 // pass: gradient, value and the multi-candidate pass, which repeats the value
 // pass's per-candidate decision and arithmetic)
 template <class M>
-static void launch_tiles_m(const Chi2Pass& P, bool grad, int prec, bool num, int blocks,
+static void launch_tiles_m(const Chi2Pass& P, bool grad, int prec, bool num, dim3 blocks,
                            cudaStream_t s) {
   constexpr int MB = tile_min_blocks<M, true>();
   const bool fast = prec != 0;
@@ -827,7 +832,7 @@ static void launch_tiles_m(const Chi2Pass& P, bool grad, int prec, bool num, int
 
 int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, int prec,
                  int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin,
-                 bool numeric, const PeerPublish* pub) {
+                 bool numeric, const PeerPublish* pub, int nbatch, int64_t rec_stride) {
 
   const int64_t ntiles = P.tile_end - P.tile_begin;
   if (ntiles <= 0) return ADC_OK;
@@ -836,15 +841,16 @@ int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, int prec,
   // Persistent grid: as many CTAs as are resident (2 per SM for the small
   // models, see tile_min_blocks), tiles grid-strided.
   const int64_t blocks = std::min<int64_t>(ntiles, (int64_t)sm_count() * (np <= 6 ? 2 : 1));
+  const dim3 grid((unsigned)blocks, (unsigned)nbatch);
   if (model == ADC_MODEL_GPOLY) {
-    launch_tiles_m<GPoly>(P, grad, prec, numeric, (int)blocks, s);
+    launch_tiles_m<GPoly>(P, grad, prec, numeric, grid, s);
   } else {
     switch (np / 3) {
-      case 1: launch_tiles_m<GSum<1>>(P, grad, prec, numeric, (int)blocks, s); break;
-      case 2: launch_tiles_m<GSum<2>>(P, grad, prec, numeric, (int)blocks, s); break;
-      case 3: launch_tiles_m<GSum<3>>(P, grad, prec, numeric, (int)blocks, s); break;
-      case 4: launch_tiles_m<GSum<4>>(P, grad, prec, numeric, (int)blocks, s); break;
-      case 8: launch_tiles_m<GSum<8>>(P, grad, prec, numeric, (int)blocks, s); break;
+      case 1: launch_tiles_m<GSum<1>>(P, grad, prec, numeric, grid, s); break;
+      case 2: launch_tiles_m<GSum<2>>(P, grad, prec, numeric, grid, s); break;
+      case 3: launch_tiles_m<GSum<3>>(P, grad, prec, numeric, grid, s); break;
+      case 4: launch_tiles_m<GSum<4>>(P, grad, prec, numeric, grid, s); break;
+      case 8: launch_tiles_m<GSum<8>>(P, grad, prec, numeric, grid, s); break;
       default: return fail(ADC_E_ARG, "gsum: unsupported component count");
     }
   }
@@ -859,8 +865,9 @@ int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, int prec,
     lm.g0_pos = 4 + lin0;
     lm.g1_pos = 4 + np + lin0;
   }
-  chi2_chunk_kernel<<<(unsigned)nchunks, kChunkThreads, 0, s>>>(
-      P.tile_ws, ntiles, R, (int)chunk_tiles, records, lm, pub ? *pub : PeerPublish{});
+  chi2_chunk_kernel<<<dim3((unsigned)nchunks, (unsigned)nbatch), kChunkThreads, 0, s>>>(
+      P.tile_ws, ntiles, R, (int)chunk_tiles, records, lm, pub ? *pub : PeerPublish{}, nullptr,
+      P.ws_stride, rec_stride);
   ADCB_CUDA(cudaGetLastError());
   return ADC_OK;
 }

@@ -150,6 +150,7 @@ struct adc_chi2_plan {
   double* records_multi = nullptr;  // [maxc][1 + 3 kMultiMax]
   int64_t multi_passes = 0;
   double* grad_multi_records = nullptr;  // [kMultiMax][maxc][R] (adc_cuda_chi2_gradient_multi)
+  double* batch_ws = nullptr;            // [kMultiMax][local tiles][R] tile records of a batch
   // device-resident fit iteration (fit_device.cu): one graph per iteration
   FitDevState* fit_st = nullptr;   // device
   FitDevState* h_fit_st = nullptr; // pinned
@@ -504,6 +505,7 @@ extern "C" int adc_cuda_chi2_plan_destroy(adc_chi2_plan* P) {
   if (P->lin) cudaFree(P->lin);
   if (P->icounts) cudaFree(P->icounts);
   if (P->grad_multi_records) cudaFree(P->grad_multi_records);
+  if (P->batch_ws) cudaFree(P->batch_ws);
   if (P->fit_graph) cudaGraphExecDestroy(P->fit_graph);
   if (P->fit_st) cudaFree(P->fit_st);
   if (P->h_fit_st) cudaFreeHost(P->h_fit_st);
@@ -604,6 +606,41 @@ int ensure_multi(adc_chi2_plan* P) {
   ADCB_CUDA(cudaMemset(P->records_multi, 0, (size_t)P->maxc * Rm * sizeof(double)));
   return ADC_OK;
 }
+
+int64_t local_tiles(const adc_chi2_plan* P) {
+  return std::max<int64_t>(
+      1, (P->L.bin_end + P->L.tile_bins - 1) / P->L.tile_bins - P->L.chunk_begin * P->L.chunk_tiles);
+}
+
+// Up to kMultiMax gradient passes as ONE batched launch (blockIdx.y = member):
+// member k reads the QDev row at qdev + k kQDoubles and leaves its chunk
+// records at grad_multi_records + k maxc R — each identical to a single
+// gradient pass (same tiles, same per-tile work, same trees).
+int ensure_grad_batch(adc_chi2_plan* P) {  // outside any stream capture
+  const int R = adc_chi2_record_len(P->np, 1);
+  const size_t per = (size_t)P->maxc * R;
+  if (P->grad_multi_records == nullptr) {
+    ADCB_CUDA(cudaMalloc(&P->grad_multi_records, per * kMultiMax * sizeof(double)));
+    ADCB_CUDA(cudaMemset(P->grad_multi_records, 0, per * kMultiMax * sizeof(double)));
+  }
+  if (P->batch_ws == nullptr)
+    ADCB_CUDA(cudaMalloc(&P->batch_ws, (size_t)kMultiMax * local_tiles(P) * R * sizeof(double)));
+  return ADC_OK;
+}
+
+int enqueue_grad_batch(adc_chi2_plan* P, const double* qdev, int nb, cudaStream_t s) {
+  const int R = adc_chi2_record_len(P->np, 1);
+  const size_t per = (size_t)P->maxc * R;
+  if (P->grad_multi_records == nullptr || P->batch_ws == nullptr)
+    return fail(ADC_E_ARG, "gradient batch buffers not allocated");
+  Chi2Pass pass = make_pass(P);
+  pass.qdev = qdev;
+  pass.q_stride = kQDoubles;
+  pass.tile_ws = P->batch_ws;
+  pass.ws_stride = local_tiles(P) * R;
+  return chi2_enqueue(pass, P->model, P->np, true, P->fast, P->L.chunk_tiles,
+                      P->grad_multi_records, s, P->lin, numeric(P), nullptr, nb, (int64_t)per);
+}
 }  // namespace
 
 extern "C" int adc_cuda_chi2_multi(adc_chi2_plan* P, const double* qs, int32_t ncand,
@@ -664,24 +701,14 @@ extern "C" int adc_cuda_chi2_gradient_multi(adc_chi2_plan* P, const double* qs, 
   if (int rc = ensure_multi(P)) return rc;
   const size_t qb = qdev_bytes();
   const int R = adc_chi2_record_len(P->np, 1);
-  const size_t per = (size_t)P->maxc * R;
-  if (P->grad_multi_records == nullptr) {
-    ADCB_CUDA(cudaMalloc(&P->grad_multi_records, per * kMultiMax * sizeof(double)));
-    ADCB_CUDA(cudaMemset(P->grad_multi_records, 0, per * kMultiMax * sizeof(double)));
-  }
   for (int k = 0; k < ncand; ++k)
     fill_qdev(P->model, P->np, qs + (size_t)k * P->np,
               reinterpret_cast<double*>(reinterpret_cast<char*>(P->h_qmulti) + k * qb));
   ADCB_CUDA(cudaMemcpyAsync(P->qmulti, P->h_qmulti, qb * ncand, cudaMemcpyHostToDevice, P->stream));
-  // ncand ordinary gradient passes back to back on one stream (each identical
-  // to adc_cuda_chi2_gradient), one exchange / copy back and one synchronisation.
-  for (int k = 0; k < ncand; ++k) {
-    Chi2Pass pass = make_pass(P);
-    pass.qdev = reinterpret_cast<const double*>(reinterpret_cast<const char*>(P->qmulti) + k * qb);
-    if (int rc = chi2_enqueue(pass, P->model, P->np, true, P->fast, P->L.chunk_tiles,
-                              P->grad_multi_records + per * k, P->stream, P->lin, numeric(P)))
-      return rc;
-  }
+  // ncand gradient passes as one batched launch (each member identical to
+  // adc_cuda_chi2_gradient), one exchange / copy back and one synchronisation.
+  if (int rc = ensure_grad_batch(P)) return rc;
+  if (int rc = enqueue_grad_batch(P, P->qmulti, ncand, P->stream)) return rc;
   if (int rc = collect_enqueue(P, P->grad_multi_records, R, ncand, P->stream)) return rc;
   ADCB_CUDA(cudaStreamSynchronize(P->stream));
   const double* rec = nullptr;
@@ -792,10 +819,15 @@ int build_fit_graph(adc_chi2_plan* P, const FitDevConst& c) {
   if (P->fit_st == nullptr) {
     ADCB_CUDA(cudaMalloc(&P->fit_st, sizeof(FitDevState)));
     ADCB_CUDA(cudaMallocHost(&P->h_fit_st, sizeof(FitDevState)));
-    const size_t scratch = std::max<size_t>((size_t)nchunks * Rmax, (size_t)kMultiMax * nchunks * 4);
+    // finalize trees of the gradient, the 2 np Newton probes, the candidates
+    const size_t scratch = std::max<size_t>((size_t)nchunks * Rmax * 2 * P->np,
+                                            (size_t)kMultiMax * nchunks * 4);
     ADCB_CUDA(cudaMalloc(&P->fit_scratch, scratch * sizeof(double)));
     ADCB_CUDA(cudaMalloc(&P->ncand_dev, sizeof(int)));
   }
+  const size_t per = (size_t)P->maxc * Rmax;
+  if (c.newton)
+    if (int rc = ensure_grad_batch(P)) return rc;
   if (P->fit_graph != nullptr && std::memcmp(&P->fit_const, &c, sizeof(c)) == 0) return ADC_OK;
   if (P->fit_graph) cudaGraphExecDestroy(P->fit_graph);
   P->fit_graph = nullptr;
@@ -831,6 +863,13 @@ int build_fit_graph(adc_chi2_plan* P, const FitDevConst& c) {
   if (rc == ADC_OK)
     rc = fit_device_enqueue_grad(P->fit_st, P->records, P->fit_scratch, nchunks, P->np, P->model,
                                  P->events, c, P->qmulti, P->ncand_dev, s);
+  if (c.newton) {  // the 2 np probe gradient passes (one batch), Hessian + solve + trials
+    if (rc == ADC_OK) rc = enqueue_grad_batch(P, P->qmulti, 2 * P->np, s);
+    if (rc == ADC_OK)
+      rc = fit_device_enqueue_newton(P->fit_st, P->grad_multi_records, per, P->fit_scratch,
+                                     nchunks, P->np, P->model, P->events, c, P->qmulti,
+                                     P->ncand_dev, s);
+  }
   if (rc == ADC_OK) {
     Chi2Pass pass = make_pass(P);
     pass.qdev = P->qmulti;
@@ -900,7 +939,7 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
   // AD passes on one device.  ADC_FIT_DEVICE=0 keeps the host-driven loop
   // (both give the same bits).
   const char* fd_env = getenv("ADC_FIT_DEVICE");
-  const bool dev_mode = P->fast && !opts->use_hessian && !numeric(P) && P->comm == nullptr &&
+  const bool dev_mode = P->fast && !numeric(P) && P->comm == nullptr &&
                         !sharded(P) && nclamp <= kMaxNp && !(fd_env && atoi(fd_env) == 0);
   if (dev_mode) {
     FitDevConst c{};
@@ -912,6 +951,8 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
     for (int k = 0; k < nclamp; ++k) c.clamp_idx[k] = clamp_idx[k];
     c.np = np;
     c.margin = margin;
+    c.newton = opts->use_hessian ? 1 : 0;
+    c.cbrt_eps = std::cbrt(2.220446049250313e-16);
     if (iterates != nullptr && opts->trace_iterates > 1) {
       if (P->fit_trace_cap < opts->trace_iterates) {
         if (P->fit_trace) cudaFree(P->fit_trace);
@@ -963,7 +1004,8 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
         cls.clear();
         for (double tt = t; tt >= 1e-18 && (int)tvals.size() < kMultiMax; tt *= 0.5) {
           trial = q;
-          for (int i = 0; i < np; ++i) trial[i] -= tt * st.g[i];
+          const double* dir = c.newton ? st.dir : st.g;
+          for (int i = 0; i < np; ++i) trial[i] -= tt * dir[i];
           cls.push_back(clamp(trial));
           trials.insert(trials.end(), trial.begin(), trial.end());
           tvals.push_back(tt);

@@ -24,6 +24,9 @@ struct Chi2Pass {
   int bpt;               // bins per thread per tile (multiple of 4)
   int64_t tile_begin, tile_end;
   const int* ncand_dev = nullptr;  // multi pass: candidate count read on the device (fit graph)
+  // batched passes (chi2_enqueue nbatch > 1): member b reads qdev + b q_stride
+  // and writes its tile records at tile_ws + b ws_stride (doubles)
+  int64_t q_stride = 0, ws_stride = 0;
 };
 
 // lin: per-chunk q-independent basis sums from chi2_lin_enqueue (gradient
@@ -32,7 +35,8 @@ struct Chi2Pass {
 // pub: publish the chunk records over peer memory from the chunk kernel.
 int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, int prec,
                  int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin,
-                 bool numeric = false, const PeerPublish* pub = nullptr);
+                 bool numeric = false, const PeerPublish* pub = nullptr, int nbatch = 1,
+                 int64_t rec_stride = 0);
 int chi2_lin_count(int model, int np);  // L: number of linear parameters
 // Once per plan: ic = [c > 0]/c into icounts_local (this rank's bins, indexed
 // from bin_begin), then [G0_lin[L], G1_lin[L], C0] per local chunk into

@@ -95,11 +95,33 @@ __global__ void __launch_bounds__(128) fit_grad_kernel(FitDevState* st, const do
     st->gd = gd;
   }
   __syncthreads();
+  if (c.newton) {
+    // the 2 np Hessian probes q +- h_c e_c, h_c = cbrt(eps) max(1, |q_c|)
+    // (fit.cpp:346-381; chi2_host.cpp builds the same rows), as QDev rows
+    // for the probe gradient passes that follow
+    for (int k = threadIdx.x; k < 2 * np; k += blockDim.x) {
+      const int col = k >> 1;
+      double probe[kMaxNp];
+      for (int i = 0; i < np; ++i) probe[i] = s_q[i];
+      const double x = s_q[col];
+      const double h = fmul(c.cbrt_eps, fmax(1.0, fabs(x)));
+      probe[col] = (k & 1) == 0 ? fadd(x, h) : fsub(x, h);
+      if ((k & 1) == 0) st->steps[col] = h;
+      write_qdev(qmulti + (size_t)k * kQDoubles, model, np, probe);
+    }
+  }
   if (s_stop) {
     if (threadIdx.x == 0) {
       st->status = kFitConvergedGrad;
       st->ncand = 0;
       *ncand_dev = 0;
+    }
+    return;
+  }
+  if (c.newton) {  // direction and trials after the probes (fit_newton_kernel)
+    if (threadIdx.x == 0) {
+      st->status = kFitRunning;
+      st->t1 = globaltimer();
     }
     return;
   }
@@ -131,6 +153,142 @@ __global__ void __launch_bounds__(128) fit_grad_kernel(FitDevState* st, const do
     st->ncand = n;
     *ncand_dev = n;
     st->status = kFitRunning;
+  }
+}
+
+// damped_solve (chi2_host.cpp): Gaussian elimination with partial pivoting on
+// H + lambda I, then back substitution — op for op, one thread.
+__device__ bool damped_solve_dev(const double* H, const double* g, double lambda, int n,
+                                 double* out) {
+  double h[kMaxNp * kMaxNp], gg[kMaxNp];
+  for (int i = 0; i < n * n; ++i) h[i] = H[i];
+  for (int i = 0; i < n; ++i) gg[i] = g[i];
+  for (int i = 0; i < n; ++i) h[i * n + i] = fadd(h[i * n + i], lambda);
+  for (int col = 0; col < n; ++col) {
+    int piv = col;
+    for (int r = col + 1; r < n; ++r)
+      if (fabs(h[r * n + col]) > fabs(h[piv * n + col])) piv = r;
+    if (fabs(h[piv * n + col]) < 1e-30) return false;
+    if (piv != col) {
+      for (int cc = 0; cc < n; ++cc) {
+        const double t = h[piv * n + cc];
+        h[piv * n + cc] = h[col * n + cc];
+        h[col * n + cc] = t;
+      }
+      const double t = gg[piv];
+      gg[piv] = gg[col];
+      gg[col] = t;
+    }
+    for (int r = col + 1; r < n; ++r) {
+      const double f = fdiv(h[r * n + col], h[col * n + col]);
+      for (int cc = col; cc < n; ++cc) h[r * n + cc] = fsub(h[r * n + cc], fmul(f, h[col * n + cc]));
+      gg[r] = fsub(gg[r], fmul(f, gg[col]));
+    }
+  }
+  for (int r = 0; r < n; ++r) out[r] = 0.0;
+  for (int r = n - 1; r >= 0; --r) {
+    double v = gg[r];
+    for (int cc = r + 1; cc < n; ++cc) v = fsub(v, fmul(h[r * n + cc], out[cc]));
+    out[r] = fdiv(v, h[r * n + r]);
+  }
+  return true;
+}
+
+// Newton option (fit.cpp:346-381 as adc_cuda_fit runs it): the 2 np probe
+// gradients (adc_chi2_finalize of each probe pass's records), the central-
+// difference Hessian, up to 10 damped solves (lambda 0, 1e-6, x10) until the
+// direction is a descent direction (else steepest descent), gd = g.d, then
+// the first batch of Armijo trials along the direction.
+__global__ void __launch_bounds__(256) fit_newton_kernel(FitDevState* st,
+                                                         const double* probe_records, size_t per,
+                                                         double* scratch, int64_t nchunks, int np,
+                                                         int model, double events, FitDevConst c,
+                                                         double* qmulti, int* ncand_dev) {
+  __shared__ double s_col[2 * kMaxNp][4 + 3 * kMaxNp];
+  __shared__ double s_pg[2 * kMaxNp][kMaxNp];
+  __shared__ double s_dir[kMaxNp], s_q[kMaxNp];
+  __shared__ int s_want;
+  if (st->status != kFitRunning) return;  // converged on the gradient
+  const int R = 4 + 3 * np, K = 2 * np;
+  if (threadIdx.x == 0) {
+    st->grad_ns += globaltimer() - st->t1;  // the probe passes just ended
+    s_want = st->first_batch;
+  }
+  if (threadIdx.x < kMaxNp) s_q[threadIdx.x] = st->q[threadIdx.x];
+  for (int idx = threadIdx.x; idx < K * R; idx += blockDim.x) {
+    const int k = idx / R, v = idx % R;
+    double* r = scratch + (size_t)k * nchunks * R;
+    const double* src = probe_records + (size_t)k * per;
+    for (int64_t ch = 0; ch < nchunks; ++ch) r[ch * R + v] = src[ch * R + v];
+    column_tree(r, nchunks, R, v);
+    s_col[k][v] = r[v];
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {  // adc_chi2_finalize per probe
+    const double S = s_col[k][0], A1 = s_col[k][1], A2 = s_col[k][2];
+    const double a = fdiv(events, S);
+    const double t_sum = fsub(fmul(2.0, A1), fmul(fmul(2.0, a), A2));
+    const double s_coef = fmul(fdiv(events, fmul(S, S)), t_sum);
+    for (int i = 0; i < np; ++i) {
+      const double G0 = s_col[k][4 + i], G1 = s_col[k][4 + np + i], G2 = s_col[k][4 + 2 * np + i];
+      s_pg[k][i] = fsub(fmul(s_coef, G0), fmul(fmul(2.0, a), fsub(G1, fmul(a, G2))));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double H[kMaxNp * kMaxNp], g[kMaxNp], dir[kMaxNp];
+    for (int i = 0; i < np; ++i) g[i] = dir[i] = st->g[i];
+    for (int col = 0; col < np; ++col)
+      for (int r = 0; r < np; ++r)
+        H[r * np + col] =
+            fdiv(fsub(s_pg[2 * col][r], s_pg[2 * col + 1][r]), fmul(2.0, st->steps[col]));
+    double lambda = 0.0;
+    bool ok = false;
+    for (int attempt = 0; attempt < 10 && !ok; ++attempt) {
+      ok = damped_solve_dev(H, g, lambda, np, dir);
+      if (ok) {
+        double descent = 0.0;
+        for (int i = 0; i < np; ++i) descent = fadd(descent, fmul(g[i], dir[i]));
+        ok = descent > 0.0;
+      }
+      lambda = lambda == 0.0 ? 1e-6 : fmul(lambda, 10.0);
+    }
+    if (!ok)
+      for (int i = 0; i < np; ++i) dir[i] = g[i];  // steepest descent
+    double gd = 0.0;
+    for (int i = 0; i < np; ++i) gd = fadd(gd, fmul(g[i], dir[i]));
+    st->gd = gd;
+    for (int i = 0; i < np; ++i) {
+      st->dir[i] = dir[i];
+      s_dir[i] = dir[i];
+    }
+  }
+  __syncthreads();
+  const int want = s_want;
+  for (int n = threadIdx.x; n < want; n += blockDim.x) {  // trials along the direction
+    const double tt = ldexp(1.0, -n);
+    if (!(tt >= 1e-18)) continue;
+    double trial[kMaxNp];
+    int cl = 0;
+    for (int i = 0; i < np; ++i) trial[i] = fsub(s_q[i], fmul(tt, s_dir[i]));
+    for (int k = 0; k < c.nclamp; ++k) {
+      const int i = c.clamp_idx[k];
+      if (i >= 0 && i < np && trial[i] < c.sigma_min) {
+        trial[i] = c.sigma_min;
+        ++cl;
+      }
+    }
+    double* dst = st->trials + (size_t)n * kMaxNp;
+    for (int i = 0; i < np; ++i) dst[i] = trial[i];
+    st->cls[n] = cl;
+    st->tvals[n] = tt;
+    write_qdev(qmulti + (size_t)n * kQDoubles, model, np, trial);
+  }
+  if (threadIdx.x == 0) {
+    int n = 0;
+    while (n < want && ldexp(1.0, -n) >= 1e-18) ++n;
+    st->ncand = n;
+    *ncand_dev = n;
   }
 }
 
@@ -202,6 +360,7 @@ __global__ void fit_loop_ctl_kernel(FitDevState* st, cudaGraphConditionalHandle 
   st->passes += 1;
   st->n_grad += 1;
   if (st->status != kFitConvergedGrad) {
+    if (c.newton) st->n_grad += 2 * c.np;  // the Hessian probes
     st->evals_total += st->evals;
     if (st->accepted_k >= 0) {
       st->clamps_total += st->sigma_clamps;
@@ -234,6 +393,16 @@ int fit_device_enqueue_grad(FitDevState* st, const double* records, double* scra
                             const FitDevConst& c, double* qmulti, int* ncand_dev, cudaStream_t s) {
   fit_grad_kernel<<<1, 128, 0, s>>>(st, records, scratch, nchunks, np, model, events, c, qmulti,
                                     ncand_dev);
+  ADCB_CUDA(cudaGetLastError());
+  return ADC_OK;
+}
+
+int fit_device_enqueue_newton(FitDevState* st, const double* probe_records, size_t per,
+                              double* scratch, int64_t nchunks, int np, int model, double events,
+                              const FitDevConst& c, double* qmulti, int* ncand_dev,
+                              cudaStream_t s) {
+  fit_newton_kernel<<<1, 256, 0, s>>>(st, probe_records, per, scratch, nchunks, np, model, events,
+                                      c, qmulti, ncand_dev);
   ADCB_CUDA(cudaGetLastError());
   return ADC_OK;
 }

@@ -28,7 +28,10 @@ struct FitDevState {
   // device loop (WHILE node) bookkeeping, cumulative over one fit
   int passes, budget, iters, clamps_total, n_grad;
   long long evals_total;
-  unsigned long long grad_ns, t0;  // gradient-pass time from %globaltimer
+  unsigned long long grad_ns, t0, t1;  // gradient-pass time from %globaltimer
+  // Newton option (fit.cpp:346-381): search direction and probe steps
+  double dir[kMaxNp];
+  double steps[kMaxNp];
 };
 
 struct FitDevConst {
@@ -37,6 +40,8 @@ struct FitDevConst {
   int nclamp;
   int np;
   int margin;     // line-search batch margin (adc_cuda_fit)
+  int newton;     // FitOptions::use_hessian: numeric-Hessian Newton direction
+  double cbrt_eps;  // std::cbrt(DBL_EPSILON) from the host libm
   double* trace;  // [trace_cap][np] iterates (row 0 written by the host)
   int trace_cap;
 };
@@ -45,6 +50,13 @@ int fit_device_enqueue_qdev(FitDevState* st, int model, int np, double* qdev, cu
 int fit_device_enqueue_grad(FitDevState* st, const double* records, double* scratch,
                             int64_t nchunks, int np, int model, double events,
                             const FitDevConst& c, double* qmulti, int* ncand_dev, cudaStream_t s);
+// Newton option: finalize the 2 np probe gradients (records [2np][nchunks][R]
+// at probe_records, stride per), central-difference Hessian, the damped
+// solve with its retries, and the Armijo trials along the direction.
+int fit_device_enqueue_newton(FitDevState* st, const double* probe_records, size_t per,
+                              double* scratch, int64_t nchunks, int np, int model, double events,
+                              const FitDevConst& c, double* qmulti, int* ncand_dev,
+                              cudaStream_t s);
 int fit_device_enqueue_accept(FitDevState* st, const double* records, double* scratch,
                               int64_t nchunks, double events, const FitDevConst& c,
                               cudaStream_t s);

@@ -241,6 +241,26 @@ def test_chi2_gaussian_recurrence(restate, model, q):
     assert g2.tobytes() != g1.tobytes()  # the recurrence really ran
 
 
+@pytest.mark.parametrize("bins,model,np_", [(100_003, "gpoly", 6), (2_000_000, "gpoly", 6),
+                                            (300_000, "gsum", 12)])
+def test_chi2_gradient_batch_bitwise_equals_single(bins, model, np_):
+    """adc_cuda_chi2_gradient_multi runs its members as ONE batched launch
+    (blockIdx.y = member); each member's gradient is bit-identical to a single
+    gradient pass."""
+    if model == "gpoly":
+        q = np.array(synth.GPOLY_INIT)
+    else:
+        q = np.array(adc.perturbed_init(adc.default_truth(np_ // 3)))
+    counts, ev = synth.histogram(bins, events=100.0 * bins, seed=31, model=model,
+                                 q=adc.default_truth(np_ // 3) if model == "gsum" else synth.GPOLY_TRUTH)
+    h = adc.Histogram(bins, -5.0, 5.0, ev, counts)
+    plan = adc.Chi2Plan(model, np_, h)
+    qs = np.stack([q * (1.0 + 1e-3 * k) for k in range(2 * np_)])
+    batch = plan.gradient_multi(qs)
+    single = np.stack([plan.gradient(qk)[0] for qk in qs])
+    assert batch.tobytes() == single.tobytes()
+
+
 def test_chi2_recurrence_skipped_for_wide_runs():
     """When a thread's run of bins spans more than one sigma (|D| bpt > 1) the
     recurrence is not used: mode 2 is bitwise mode 1."""
@@ -627,14 +647,17 @@ def test_gaussnd_strided_views(restate):
 
 
 @pytest.mark.parametrize("case", ["gpoly_1e6", "gpoly_1e6_b1", "gpoly_1e6_b3", "gsum1", "gsum2",
-                                  "gsum4"])
+                                  "gsum4", "gpoly_1e6_newton", "gsum2_newton", "gsum4_newton"])
 def test_device_fit_loop_bitwise_equals_host_loop(case):
     """The device-resident loop (one graph, a WHILE node around the
     steepest-descent body: gradient pass, finalize, Armijo trials, multi pass,
     selection, loop control; the host only continues searches longer than a
     batch) takes exactly the host-driven loop's steps: same iterates, chi2 and
-    counters, bit for bit — also when the budget ends the loop early."""
+    counters, bit for bit — also when the budget ends the loop early, and with
+    the Newton option (2 np probe gradient passes, Hessian, damped solve)."""
     import os
+    newton = case.endswith("_newton")
+    case = case.replace("_newton", "")
     if case.startswith("gpoly_1e6"):
         counts, ev = synth.histogram(10**6, events=1e8, seed=11)
         budget = {"gpoly_1e6": 400, "gpoly_1e6_b1": 1, "gpoly_1e6_b3": 3}[case]
@@ -650,7 +673,8 @@ def test_device_fit_loop_bitwise_equals_host_loop(case):
         os.environ["ADC_FIT_DEVICE"] = mode
         try:
             r = adc.FitEngine(model, len(init)).fit(
-                h, init, adc.FitOptions(budget=budget, trace_iterates=budget + 1))
+                h, init, adc.FitOptions(budget=budget, trace_iterates=budget + 1,
+                                        use_hessian=newton))
         finally:
             os.environ.pop("ADC_FIT_DEVICE", None)
         out[mode] = r
