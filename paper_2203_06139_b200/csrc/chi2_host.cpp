@@ -856,10 +856,11 @@ int build_fit_graph(adc_chi2_plan* P, const FitDevConst& c) {
   e = cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
                                     cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return fail_graph(e, "cudaStreamBeginCaptureToGraph (fit body)");
-  int rc = fit_device_enqueue_qdev(P->fit_st, P->model, P->np, P->qdev, s);
+  int rc = fit_device_enqueue_qdev(P->fit_st, P->model, P->np, P->qdev,
+                                   c.numeric ? c.cbrt_eps : 0.0, s);
   if (rc == ADC_OK)
     rc = chi2_enqueue(make_pass(P), P->model, P->np, true, P->fast, P->L.chunk_tiles, P->records,
-                      s, P->lin);
+                      s, P->lin, numeric(P));
   if (rc == ADC_OK)
     rc = fit_device_enqueue_grad(P->fit_st, P->records, P->fit_scratch, nchunks, P->np, P->model,
                                  P->events, c, P->qmulti, P->ncand_dev, s);
@@ -935,11 +936,11 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
   // next batch = the last search's trial count + margin, in groups of 8 (the
   // multi pass's candidate group); ADC_FIT_MARGIN is an experiment knob
   const int margin = getenv("ADC_FIT_MARGIN") ? atoi(getenv("ADC_FIT_MARGIN")) : 8;
-  // Device-resident iterations (fit_device.cu): steepest descent with the fast
-  // AD passes on one device.  ADC_FIT_DEVICE=0 keeps the host-driven loop
-  // (both give the same bits).
+  // Device-resident loop (fit_device.cu): the fast passes on one device,
+  // either gradient provider, steepest descent or the Newton option.
+  // ADC_FIT_DEVICE=0 keeps the host-driven loop (both give the same bits).
   const char* fd_env = getenv("ADC_FIT_DEVICE");
-  const bool dev_mode = P->fast && !numeric(P) && P->comm == nullptr &&
+  const bool dev_mode = P->fast && P->comm == nullptr &&
                         !sharded(P) && nclamp <= kMaxNp && !(fd_env && atoi(fd_env) == 0);
   if (dev_mode) {
     FitDevConst c{};
@@ -952,6 +953,7 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
     c.np = np;
     c.margin = margin;
     c.newton = opts->use_hessian ? 1 : 0;
+    c.numeric = numeric(P) ? 1 : 0;  // part of the graph's key: the provider picks the kernel
     c.cbrt_eps = std::cbrt(2.220446049250313e-16);
     if (iterates != nullptr && opts->trace_iterates > 1) {
       if (P->fit_trace_cap < opts->trace_iterates) {

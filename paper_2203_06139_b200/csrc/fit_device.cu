@@ -18,16 +18,46 @@ namespace adcb {
 namespace {
 
 // QDev of one parameter vector: q and, for the width parameters, 1/q
-// (fill_qdev, chi2.cu).  The AD passes read nothing else.
-__device__ void write_qdev(double* dst, int model, int np, const double* q) {
+// (fill_qdev, chi2.cu) — all the AD passes read.  With h0 = cbrt(eps) (the
+// numeric provider) also the QNum block the numeric pass reads: probes
+// q +- h, h = h0 max(1, |q|), their width reciprocals, 2h and 1/(2h), op for
+// op as fill_qdev computes them on the host.
+__device__ void write_qdev(double* dst, int model, int np, const double* q, double h0 = 0.0) {
   for (int i = 0; i < kMaxNp; ++i) {
     dst[i] = i < np ? q[i] : 0.0;
     dst[kMaxNp + i] = 0.0;
   }
+  double* qp = dst + 2 * kMaxNp;  // QNum: qp, qm, invp, invm, h2, rh2
+  double* qm = qp + kMaxNp;
+  double* invp = qm + kMaxNp;
+  double* invm = invp + kMaxNp;
+  double* h2 = invm + kMaxNp;
+  double* rh2 = h2 + kMaxNp;
+  if (h0 != 0.0) {
+    for (int i = 0; i < kMaxNp; ++i) {
+      if (i < np) {
+        const double h = fmul(h0, fmax(1.0, fabs(q[i])));
+        qp[i] = fadd(q[i], h);
+        qm[i] = fadd(q[i], -h);
+        h2[i] = fmul(2.0, h);
+        rh2[i] = fdiv(1.0, h2[i]);
+      } else {
+        qp[i] = qm[i] = h2[i] = rh2[i] = 0.0;
+      }
+      invp[i] = invm[i] = 0.0;
+    }
+  }
+  auto width = [&](int j) {
+    dst[kMaxNp + j] = fdiv(1.0, q[j]);
+    if (h0 != 0.0) {
+      invp[j] = fdiv(1.0, qp[j]);
+      invm[j] = fdiv(1.0, qm[j]);
+    }
+  };
   if (model == ADC_MODEL_GPOLY) {
-    dst[kMaxNp + 2] = fdiv(1.0, q[2]);
+    width(2);
   } else {
-    for (int j = 2; j < np; j += 3) dst[kMaxNp + j] = fdiv(1.0, q[j]);
+    for (int j = 2; j < np; j += 3) width(j);
   }
 }
 
@@ -37,9 +67,9 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-__global__ void fit_qdev_kernel(FitDevState* st, int model, int np, double* qdev) {
+__global__ void fit_qdev_kernel(FitDevState* st, int model, int np, double* qdev, double h0) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
-    write_qdev(qdev, model, np, st->q);
+    write_qdev(qdev, model, np, st->q, h0);
     st->t0 = globaltimer();  // the gradient pass starts after this kernel
   }
 }
@@ -107,7 +137,7 @@ __global__ void __launch_bounds__(128) fit_grad_kernel(FitDevState* st, const do
       const double h = fmul(c.cbrt_eps, fmax(1.0, fabs(x)));
       probe[col] = (k & 1) == 0 ? fadd(x, h) : fsub(x, h);
       if ((k & 1) == 0) st->steps[col] = h;
-      write_qdev(qmulti + (size_t)k * kQDoubles, model, np, probe);
+      write_qdev(qmulti + (size_t)k * kQDoubles, model, np, probe, c.numeric ? c.cbrt_eps : 0.0);
     }
   }
   if (s_stop) {
@@ -382,8 +412,9 @@ int fit_device_enqueue_loop_ctl(FitDevState* st, cudaGraphConditionalHandle h,
   return ADC_OK;
 }
 
-int fit_device_enqueue_qdev(FitDevState* st, int model, int np, double* qdev, cudaStream_t s) {
-  fit_qdev_kernel<<<1, 32, 0, s>>>(st, model, np, qdev);
+int fit_device_enqueue_qdev(FitDevState* st, int model, int np, double* qdev, double h0,
+                            cudaStream_t s) {
+  fit_qdev_kernel<<<1, 32, 0, s>>>(st, model, np, qdev, h0);
   ADCB_CUDA(cudaGetLastError());
   return ADC_OK;
 }

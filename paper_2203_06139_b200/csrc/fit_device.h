@@ -41,12 +41,15 @@ struct FitDevConst {
   int np;
   int margin;     // line-search batch margin (adc_cuda_fit)
   int newton;     // FitOptions::use_hessian: numeric-Hessian Newton direction
+  int numeric;    // GradientProvider::Numeric gradient passes
   double cbrt_eps;  // std::cbrt(DBL_EPSILON) from the host libm
   double* trace;  // [trace_cap][np] iterates (row 0 written by the host)
   int trace_cap;
 };
 
-int fit_device_enqueue_qdev(FitDevState* st, int model, int np, double* qdev, cudaStream_t s);
+// h0 = cbrt(eps) also writes the numeric provider's probe block (0: AD only).
+int fit_device_enqueue_qdev(FitDevState* st, int model, int np, double* qdev, double h0,
+                            cudaStream_t s);
 int fit_device_enqueue_grad(FitDevState* st, const double* records, double* scratch,
                             int64_t nchunks, int np, int model, double events,
                             const FitDevConst& c, double* qmulti, int* ncand_dev, cudaStream_t s);

@@ -647,17 +647,21 @@ def test_gaussnd_strided_views(restate):
 
 
 @pytest.mark.parametrize("case", ["gpoly_1e6", "gpoly_1e6_b1", "gpoly_1e6_b3", "gsum1", "gsum2",
-                                  "gsum4", "gpoly_1e6_newton", "gsum2_newton", "gsum4_newton"])
+                                  "gsum4", "gpoly_1e6_newton", "gsum2_newton", "gsum4_newton",
+                                  "gsum2_numeric", "gsum1_numeric_newton",
+                                  "gpoly_1e6_b3_numeric"])
 def test_device_fit_loop_bitwise_equals_host_loop(case):
     """The device-resident loop (one graph, a WHILE node around the
     steepest-descent body: gradient pass, finalize, Armijo trials, multi pass,
     selection, loop control; the host only continues searches longer than a
     batch) takes exactly the host-driven loop's steps: same iterates, chi2 and
-    counters, bit for bit — also when the budget ends the loop early, and with
-    the Newton option (2 np probe gradient passes, Hessian, damped solve)."""
+    counters, bit for bit — also when the budget ends the loop early, with the
+    Newton option (2 np probe gradient passes, Hessian, damped solve) and with
+    the numeric gradient provider."""
     import os
     newton = case.endswith("_newton")
-    case = case.replace("_newton", "")
+    numeric = "_numeric" in case
+    case = case.replace("_newton", "").replace("_numeric", "")
     if case.startswith("gpoly_1e6"):
         counts, ev = synth.histogram(10**6, events=1e8, seed=11)
         budget = {"gpoly_1e6": 400, "gpoly_1e6_b1": 1, "gpoly_1e6_b3": 3}[case]
@@ -674,7 +678,9 @@ def test_device_fit_loop_bitwise_equals_host_loop(case):
         try:
             r = adc.FitEngine(model, len(init)).fit(
                 h, init, adc.FitOptions(budget=budget, trace_iterates=budget + 1,
-                                        use_hessian=newton))
+                                        use_hessian=newton),
+                provider=adc.GradientProvider.Numeric if numeric else
+                adc.GradientProvider.AdReverse)
         finally:
             os.environ.pop("ADC_FIT_DEVICE", None)
         out[mode] = r
