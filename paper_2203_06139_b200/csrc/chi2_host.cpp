@@ -158,6 +158,8 @@ struct adc_chi2_plan {
   int* ncand_dev = nullptr;
   cudaGraphExec_t fit_graph = nullptr;
   double* fit_trace = nullptr;  // device iterate trace of the fit loop
+  double* fit_full = nullptr;    // compact all-rank records (sharded device loop)
+  int64_t* fit_rbegin = nullptr; // [world + 1] first chunk of each rank
   int fit_trace_cap = 0;
   FitDevConst fit_const{};
   // q-independent basis sums of the linear parameters (chi2_lin_enqueue)
@@ -512,6 +514,8 @@ extern "C" int adc_cuda_chi2_plan_destroy(adc_chi2_plan* P) {
   if (P->fit_scratch) cudaFree(P->fit_scratch);
   if (P->ncand_dev) cudaFree(P->ncand_dev);
   if (P->fit_trace) cudaFree(P->fit_trace);
+  if (P->fit_full) cudaFree(P->fit_full);
+  if (P->fit_rbegin) cudaFree(P->fit_rbegin);
   if (P->stream) cudaStreamDestroy(P->stream);
   delete P;
   return ADC_OK;
@@ -828,6 +832,34 @@ int build_fit_graph(adc_chi2_plan* P, const FitDevConst& c) {
   const size_t per = (size_t)P->maxc * Rmax;
   if (c.newton)
     if (int rc = ensure_grad_batch(P)) return rc;
+  // Sharded plan on the peer transport: every pass publishes its records to
+  // all ranks over peer memory inside the loop body, and a compaction kernel
+  // lays the exchanged blocks out as [nchunks][R] for the finalize kernels —
+  // every rank runs the same loop on the same bits, no host in between.
+  const bool peer = P->comm != nullptr && P->comm->kind == ADC_COMM_PEER;
+  const int Rm = 1 + 3 * kMultiMax;
+  if (peer && P->fit_full == nullptr) {
+    const size_t full = std::max<size_t>((size_t)nchunks * Rmax * 2 * P->np, (size_t)nchunks * Rm);
+    ADCB_CUDA(cudaMalloc(&P->fit_full, full * sizeof(double)));
+    std::vector<int64_t> rb(P->world + 1);
+    for (int r = 0; r < P->world; ++r) {
+      adc_chi2_layout Lr{};
+      adc_chi2_make_layout(P->bins, P->world, r, &Lr);
+      rb[r] = Lr.chunk_begin;
+    }
+    rb[P->world] = nchunks;
+    ADCB_CUDA(cudaMalloc(&P->fit_rbegin, rb.size() * sizeof(int64_t)));
+    ADCB_CUDA(cudaMemcpy(P->fit_rbegin, rb.data(), rb.size() * sizeof(int64_t),
+                         cudaMemcpyHostToDevice));
+  }
+  auto exchange = [&](const double* local, int nb, int R, bool published, const int* ndev,
+                      cudaStream_t st) -> int {
+    const size_t count = (size_t)nb * P->maxc * R;
+    if (!published)
+      if (int rc = peer_exchange_enqueue(&P->peer, local, count, st)) return rc;
+    return fit_device_enqueue_compact(P->peer.out, count, P->world, P->fit_rbegin, nchunks, nb,
+                                      P->maxc, R, ndev, P->fit_full, st);
+  };
   if (P->fit_graph != nullptr && std::memcmp(&P->fit_const, &c, sizeof(c)) == 0) return ADC_OK;
   if (P->fit_graph) cudaGraphExecDestroy(P->fit_graph);
   P->fit_graph = nullptr;
@@ -858,18 +890,25 @@ int build_fit_graph(adc_chi2_plan* P, const FitDevConst& c) {
   if (e != cudaSuccess) return fail_graph(e, "cudaStreamBeginCaptureToGraph (fit body)");
   int rc = fit_device_enqueue_qdev(P->fit_st, P->model, P->np, P->qdev,
                                    c.numeric ? c.cbrt_eps : 0.0, s);
-  if (rc == ADC_OK)
+  const bool fuse = peer && local_chunks(P) > 0;  // the chunk kernel publishes itself
+  const double* grad_rec = peer ? P->fit_full : P->records;
+  if (rc == ADC_OK) {
+    PeerPublish pub;
+    if (fuse) pub = peer_publish_args(&P->peer, (size_t)P->maxc * Rmax);
     rc = chi2_enqueue(make_pass(P), P->model, P->np, true, P->fast, P->L.chunk_tiles, P->records,
-                      s, P->lin, numeric(P));
+                      s, P->lin, numeric(P), fuse ? &pub : nullptr);
+  }
+  if (rc == ADC_OK && peer) rc = exchange(P->records, 1, Rmax, fuse, nullptr, s);
   if (rc == ADC_OK)
-    rc = fit_device_enqueue_grad(P->fit_st, P->records, P->fit_scratch, nchunks, P->np, P->model,
+    rc = fit_device_enqueue_grad(P->fit_st, grad_rec, P->fit_scratch, nchunks, P->np, P->model,
                                  P->events, c, P->qmulti, P->ncand_dev, s);
   if (c.newton) {  // the 2 np probe gradient passes (one batch), Hessian + solve + trials
     if (rc == ADC_OK) rc = enqueue_grad_batch(P, P->qmulti, 2 * P->np, s);
+    if (rc == ADC_OK && peer) rc = exchange(P->grad_multi_records, 2 * P->np, Rmax, false, nullptr, s);
     if (rc == ADC_OK)
-      rc = fit_device_enqueue_newton(P->fit_st, P->grad_multi_records, per, P->fit_scratch,
-                                     nchunks, P->np, P->model, P->events, c, P->qmulti,
-                                     P->ncand_dev, s);
+      rc = fit_device_enqueue_newton(P->fit_st, peer ? P->fit_full : P->grad_multi_records,
+                                     peer ? (size_t)nchunks * Rmax : per, P->fit_scratch, nchunks,
+                                     P->np, P->model, P->events, c, P->qmulti, P->ncand_dev, s);
   }
   if (rc == ADC_OK) {
     Chi2Pass pass = make_pass(P);
@@ -879,9 +918,18 @@ int build_fit_graph(adc_chi2_plan* P, const FitDevConst& c) {
     rc = chi2_multi_enqueue(pass, P->model, P->np, kMultiMax, P->L.chunk_tiles, P->records_multi,
                             s, P->lin, P->fast);
   }
+  if (rc == ADC_OK && peer) {
+    // the multi records' stride is the device candidate count: exchange the
+    // kMultiMax-sized block, compact with the device count
+    const size_t count = (size_t)P->maxc * Rm;
+    rc = peer_exchange_enqueue(&P->peer, P->records_multi, count, s);
+    if (rc == ADC_OK)
+      rc = fit_device_enqueue_compact(P->peer.out, count, P->world, P->fit_rbegin, nchunks, 1,
+                                      P->maxc, Rm, P->ncand_dev, P->fit_full, s);
+  }
   if (rc == ADC_OK)
-    rc = fit_device_enqueue_accept(P->fit_st, P->records_multi, P->fit_scratch, nchunks,
-                                   P->events, c, s);
+    rc = fit_device_enqueue_accept(P->fit_st, peer ? P->fit_full : P->records_multi,
+                                   P->fit_scratch, nchunks, P->events, c, s);
   if (rc == ADC_OK) rc = fit_device_enqueue_loop_ctl(P->fit_st, h, c, s);
   cudaGraph_t captured = nullptr;
   e = cudaStreamEndCapture(s, &captured);
@@ -940,8 +988,9 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
   // either gradient provider, steepest descent or the Newton option.
   // ADC_FIT_DEVICE=0 keeps the host-driven loop (both give the same bits).
   const char* fd_env = getenv("ADC_FIT_DEVICE");
-  const bool dev_mode = P->fast && P->comm == nullptr &&
-                        !sharded(P) && nclamp <= kMaxNp && !(fd_env && atoi(fd_env) == 0);
+  const bool peer = P->comm != nullptr && P->comm->kind == ADC_COMM_PEER;
+  const bool dev_mode = P->fast && (peer || (P->comm == nullptr && !sharded(P))) &&
+                        nclamp <= kMaxNp && !(fd_env && atoi(fd_env) == 0);
   if (dev_mode) {
     FitDevConst c{};
     c.grad_tol = opts->grad_tol;
@@ -958,6 +1007,8 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
     if (iterates != nullptr && opts->trace_iterates > 1) {
       if (P->fit_trace_cap < opts->trace_iterates) {
         if (P->fit_trace) cudaFree(P->fit_trace);
+  if (P->fit_full) cudaFree(P->fit_full);
+  if (P->fit_rbegin) cudaFree(P->fit_rbegin);
         P->fit_trace = nullptr;
         P->fit_trace_cap = 0;
         ADCB_CUDA(cudaMalloc(&P->fit_trace, (size_t)opts->trace_iterates * kMaxNp * sizeof(double)));

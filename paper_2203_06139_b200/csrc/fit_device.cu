@@ -403,7 +403,35 @@ __global__ void fit_loop_ctl_kernel(FitDevState* st, cudaGraphConditionalHandle 
   cudaGraphSetConditional(h, cont);
 }
 
+// Peer-transport exchange result [world][count] (each rank's block = its
+// local chunks' records, nb blocks of maxc * R) -> the compact
+// [nb][nchunks][R] layout the finalize kernels read (collect_finish's
+// compaction, on the device).  R from the device candidate count when given.
+__global__ void fit_compact_kernel(const double* __restrict__ out, size_t count, int world,
+                                   const int64_t* __restrict__ rbegin, int64_t nchunks, int nb,
+                                   int64_t maxc, int Rfix, const int* ncand_dev,
+                                   double* __restrict__ dst) {
+  const int R = ncand_dev != nullptr ? 1 + 3 * *ncand_dev : Rfix;
+  const int64_t total = (int64_t)nb * nchunks * R;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = idx % R, bc = idx / R, ch = bc % nchunks, b = bc / nchunks;
+    int r = 0;
+    while (r + 1 < world && rbegin[r + 1] <= ch) ++r;
+    dst[idx] = out[(size_t)r * count + (size_t)b * maxc * R + (size_t)(ch - rbegin[r]) * R + v];
+  }
+}
+
 }  // namespace
+
+int fit_device_enqueue_compact(const double* out, size_t count, int world, const int64_t* rbegin,
+                               int64_t nchunks, int nb, int64_t maxc, int Rfix,
+                               const int* ncand_dev, double* dst, cudaStream_t s) {
+  fit_compact_kernel<<<64, 256, 0, s>>>(out, count, world, rbegin, nchunks, nb, maxc, Rfix,
+                                        ncand_dev, dst);
+  ADCB_CUDA(cudaGetLastError());
+  return ADC_OK;
+}
 
 int fit_device_enqueue_loop_ctl(FitDevState* st, cudaGraphConditionalHandle h,
                                 const FitDevConst& c, cudaStream_t s) {

@@ -63,6 +63,10 @@ int fit_device_enqueue_newton(FitDevState* st, const double* probe_records, size
 int fit_device_enqueue_accept(FitDevState* st, const double* records, double* scratch,
                               int64_t nchunks, double events, const FitDevConst& c,
                               cudaStream_t s);
+// Sharded plans (peer transport): all ranks' exchanged records -> compact.
+int fit_device_enqueue_compact(const double* out, size_t count, int world, const int64_t* rbegin,
+                               int64_t nchunks, int nb, int64_t maxc, int Rfix,
+                               const int* ncand_dev, double* dst, cudaStream_t s);
 // End of a loop body: the host loop's bookkeeping for the pass just run, then
 // the WHILE node's condition (continue while running and within budget).
 int fit_device_enqueue_loop_ctl(FitDevState* st, cudaGraphConditionalHandle h,
