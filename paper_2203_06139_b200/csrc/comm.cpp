@@ -201,33 +201,56 @@ PeerPublish peer_publish_args(PeerExchange* X, size_t count) {
   return pp;
 }
 
+// Every rank reaches both all-gathers even when a local step failed (its
+// status travels with its handles / barrier token), so a failure anywhere is
+// a consistent error on every rank — callers can fall back to another
+// transport together instead of some ranks waiting on the others forever.
 int peer_setup(adc_comm* C, size_t xcount, PeerExchange* X) {
   peer_release(X);
   X->world = C->world;
   X->rank = C->rank;
   X->xcount = xcount;
   const int W = C->world;
-  ADCB_CUDA(cudaMalloc(&X->gather, 2 * (size_t)W * xcount * sizeof(double)));
-  ADCB_CUDA(cudaMalloc(&X->flags, (size_t)W * sizeof(unsigned long long)));
-  ADCB_CUDA(cudaMemset(X->flags, 0, (size_t)W * sizeof(unsigned long long)));
-  ADCB_CUDA(cudaMalloc(&X->seq, sizeof(unsigned long long)));
-  ADCB_CUDA(cudaMemset(X->seq, 0, sizeof(unsigned long long)));
-  ADCB_CUDA(cudaMalloc(&X->done, sizeof(unsigned int)));
-  ADCB_CUDA(cudaMemset(X->done, 0, sizeof(unsigned int)));
-  ADCB_CUDA(cudaMalloc(&X->out, (size_t)W * xcount * sizeof(double)));
-  ADCB_CUDA(cudaMalloc(&X->peer_gather, (size_t)W * sizeof(double*)));
-  ADCB_CUDA(cudaMalloc(&X->peer_flags, (size_t)W * sizeof(unsigned long long*)));
-  ADCB_CUDA(cudaDeviceSynchronize());  // flags zeroed before any peer can write them
-  // bootstrap: every rank's two IPC handles
-  cudaIpcMemHandle_t mine[2];
-  ADCB_CUDA(cudaIpcGetMemHandle(&mine[0], X->gather));
-  ADCB_CUDA(cudaIpcGetMemHandle(&mine[1], X->flags));
-  std::vector<cudaIpcMemHandle_t> all(2 * (size_t)W);
-  const int rc = C->fn(C->ctx, mine, all.data(), sizeof(mine));
-  if (rc != 0) return fail(ADC_E_NCCL, "peer bootstrap all-gather failed (" + std::to_string(rc) + ")");
+  std::string why;
+  auto step = [&](cudaError_t e, const char* what) {
+    if (e != cudaSuccess && why.empty()) {
+      why = std::string(what) + ": " + cudaGetErrorString(e);
+      cudaGetLastError();
+    }
+    return why.empty();
+  };
+  step(cudaMalloc(&X->gather, 2 * (size_t)W * xcount * sizeof(double)), "cudaMalloc") &&
+      step(cudaMalloc(&X->flags, (size_t)W * sizeof(unsigned long long)), "cudaMalloc") &&
+      step(cudaMemset(X->flags, 0, (size_t)W * sizeof(unsigned long long)), "cudaMemset") &&
+      step(cudaMalloc(&X->seq, sizeof(unsigned long long)), "cudaMalloc") &&
+      step(cudaMemset(X->seq, 0, sizeof(unsigned long long)), "cudaMemset") &&
+      step(cudaMalloc(&X->done, sizeof(unsigned int)), "cudaMalloc") &&
+      step(cudaMemset(X->done, 0, sizeof(unsigned int)), "cudaMemset") &&
+      step(cudaMalloc(&X->out, (size_t)W * xcount * sizeof(double)), "cudaMalloc") &&
+      step(cudaMalloc(&X->peer_gather, (size_t)W * sizeof(double*)), "cudaMalloc") &&
+      step(cudaMalloc(&X->peer_flags, (size_t)W * sizeof(unsigned long long*)), "cudaMalloc") &&
+      step(cudaDeviceSynchronize(), "cudaDeviceSynchronize");  // flags zeroed before peers write
+  // bootstrap: every rank's two IPC handles and its status so far
+  struct Boot {  // a whole number of doubles: the callbacks move float64 arrays
+    cudaIpcMemHandle_t h[2];
+    double ok;
+  };
+  static_assert(sizeof(Boot) % sizeof(double) == 0, "bootstrap record size");
+  Boot mine{};
+  if (why.empty())
+    step(cudaIpcGetMemHandle(&mine.h[0], X->gather), "cudaIpcGetMemHandle") &&
+        step(cudaIpcGetMemHandle(&mine.h[1], X->flags), "cudaIpcGetMemHandle");
+  mine.ok = why.empty() ? 1.0 : 0.0;
+  std::vector<Boot> all((size_t)W);
+  if (C->fn(C->ctx, &mine, all.data(), sizeof(Boot)) != 0) {
+    peer_release(X);
+    return fail(ADC_E_NCCL, "peer bootstrap all-gather failed");
+  }
+  for (int r = 0; r < W; ++r)
+    if (all[r].ok != 1.0 && why.empty()) why = "rank " + std::to_string(r) + " could not set up";
   std::vector<double*> pg(W);
   std::vector<unsigned long long*> pf(W);
-  for (int r = 0; r < W; ++r) {
+  for (int r = 0; r < W && why.empty(); ++r) {
     if (r == C->rank) {
       pg[r] = X->gather;
       pf[r] = X->flags;
@@ -235,22 +258,36 @@ int peer_setup(adc_comm* C, size_t xcount, PeerExchange* X) {
     }
     void* g = nullptr;
     void* f = nullptr;
-    ADCB_CUDA(cudaIpcOpenMemHandle(&g, all[2 * r], cudaIpcMemLazyEnablePeerAccess));
+    if (!step(cudaIpcOpenMemHandle(&g, all[r].h[0], cudaIpcMemLazyEnablePeerAccess),
+              "cudaIpcOpenMemHandle"))
+      break;
     X->opened.push_back(g);
-    ADCB_CUDA(cudaIpcOpenMemHandle(&f, all[2 * r + 1], cudaIpcMemLazyEnablePeerAccess));
+    if (!step(cudaIpcOpenMemHandle(&f, all[r].h[1], cudaIpcMemLazyEnablePeerAccess),
+              "cudaIpcOpenMemHandle"))
+      break;
     X->opened.push_back(f);
     pg[r] = static_cast<double*>(g);
     pf[r] = static_cast<unsigned long long*>(f);
   }
-  ADCB_CUDA(cudaMemcpy(X->peer_gather, pg.data(), (size_t)W * sizeof(double*),
-                       cudaMemcpyHostToDevice));
-  ADCB_CUDA(cudaMemcpy(X->peer_flags, pf.data(), (size_t)W * sizeof(unsigned long long*),
-                       cudaMemcpyHostToDevice));
-  // every rank has opened every buffer before any pass may write into it
-  double token = 0.0;
+  if (why.empty())
+    step(cudaMemcpy(X->peer_gather, pg.data(), (size_t)W * sizeof(double*),
+                    cudaMemcpyHostToDevice), "cudaMemcpy") &&
+        step(cudaMemcpy(X->peer_flags, pf.data(), (size_t)W * sizeof(unsigned long long*),
+                        cudaMemcpyHostToDevice), "cudaMemcpy");
+  // barrier + consensus: every rank has opened every buffer (or someone failed)
+  // before any pass may write into a peer's buffer
+  double token = why.empty() ? 0.0 : 1.0;
   std::vector<double> tokens(W);
-  if (C->fn(C->ctx, &token, tokens.data(), sizeof(double)) != 0)
+  if (C->fn(C->ctx, &token, tokens.data(), sizeof(double)) != 0) {
+    peer_release(X);
     return fail(ADC_E_NCCL, "peer bootstrap barrier failed");
+  }
+  for (int r = 0; r < W; ++r)
+    if (tokens[r] != 0.0 && why.empty()) why = "rank " + std::to_string(r) + " could not map a peer";
+  if (!why.empty()) {
+    peer_release(X);
+    return fail(ADC_E_CUDA, "peer transport unavailable (" + why + ")");
+  }
   return ADC_OK;
 }
 
