@@ -45,6 +45,9 @@ def _results(plan, eng, h, q, qs):
     out["fit_its"] = np.array(r.iterates)
     r = eng.fit(h, q, adc.FitOptions(budget=3, use_hessian=True))
     out["newton_params"] = np.array(r.params)
+    r = eng.fit(h, q, adc.FitOptions(budget=4, trace_iterates=5),
+                provider=adc.GradientProvider.Numeric)
+    out["numeric_its"] = np.array(r.iterates)
     return {k: np.asarray(v).tobytes() for k, v in out.items()}
 
 
