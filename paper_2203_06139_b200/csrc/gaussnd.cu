@@ -568,8 +568,10 @@ int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, con
       return launch_tile<1, 16>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
     case 8: return launch_tile<8, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
     case 16:
-      if (g_variant == 7) return launch_tile<16, 8, 2>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
-      return launch_tile<16, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+      // bulk (TMA-unit) L2 prefetch of the next rows: 2.4% faster at dim 1000
+      // (8.24 vs 8.45 ms, same bits); variant 2 keeps the per-lane prefetch
+      if (g_variant == 2) return launch_tile<16, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+      return launch_tile<16, 8, 2>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
   }
   return fail(ADC_E_ARG, "gaussnd: bad configuration");
 }

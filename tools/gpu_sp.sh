@@ -1,2 +1,6 @@
-mkdir -p gpurun_out
-timeout 900 python -m pytest tests -q -m gpu -k "fit or smoke or bridge or numeric or scaling" -x 2>&1 | grep -E "^E |passed|failed|Error" | head -20
+for dn in "150 6666666" "200 5000000" "300 3333334" "500 2000000"; do
+  for cfg in "8 2" "4 4" "4 3" "2 8" "2 6"; do
+    set -- $cfg
+    echo -n "dim/n $dn W=$1 cps=$2: "; ADC_GAUSSND_W=$1 ADC_GAUSSND_CPS=$2 timeout 120 python tools/probe_gaussnd_variants.py $dn 0 | grep variant
+  done
+done
