@@ -151,7 +151,7 @@ struct adc_chi2_plan {
   int64_t multi_passes = 0;
   double* grad_multi_records = nullptr;  // [kMultiMax][maxc][R] (adc_cuda_chi2_gradient_multi)
   double* batch_ws = nullptr;            // [kMultiMax][local tiles][R] tile records of a batch
-  // device-resident fit iteration (fit_device.cu): one graph per iteration
+  // device-resident fit loop (fit_device.cu): one graph, a WHILE node around the iteration
   FitDevState* fit_st = nullptr;   // device
   FitDevState* h_fit_st = nullptr; // pinned
   double* fit_scratch = nullptr;

@@ -1,12 +1,17 @@
-// Device-resident fit iteration: one CUDA graph per
-// steepest-descent iteration of FitEngine::fit (fit.cpp:315-425) —
+// Device-resident fit loop: the body of one
+// iteration of FitEngine::fit (fit.cpp:315-425) —
 //   parameters -> QDev, gradient pass (K3 + K4), gradient finalize +
-//   convergence test + Armijo trial construction, multi-candidate value pass
-//   (K3m + K4), trial finalize + first-accepted selection —
-// with no host work between the steps and one synchronisation per iteration.
+//   convergence test + Armijo trial construction (or, with the Newton
+//   option, the 2 np probe gradients as one batched pass, the Hessian and the
+//   damped solve first), multi-candidate value pass (K3m + K4), trial
+//   finalize + first-accepted selection, loop control —
+// captured once as the body of a CUDA graph WHILE node; the loop-control
+// kernel does the host loop's bookkeeping and sets the node's condition, so
+// iterations follow each other with no host work in between.
 // Every operation is the host loop's (chi2_host.cpp: adc_chi2_finalize, the
-// trial arithmetic, the Armijo test, the clamp), one IEEE op at a time in the
-// same order, so the iterates are bit-identical to the host-driven loop.
+// trial arithmetic, the Armijo test, the clamp, damped_solve), one IEEE op at
+// a time in the same order, so the iterates are bit-identical to the
+// host-driven loop.
 #include <cmath>
 
 #include "chi2_internal.h"
