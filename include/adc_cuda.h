@@ -167,6 +167,21 @@ int adc_cuda_jit_launch(adc_jit_module* module, int64_t grid_dim, int64_t block_
                         const adc_jit_arg* args, int32_t nargs, void* stream);
 int adc_cuda_jit_launch_host(adc_jit_module* module, int64_t grid_dim, int64_t block_dim,
                              int64_t n, const adc_jit_arg* args, int32_t nargs);
+/* The same launch with the reference's LaunchStats (launch.hpp:58-61): the
+ * counting variant of the kernel (built on first use) adds every operation
+ * the interpreter counts (eval.cpp: adds incl. unary minus and compound +=,
+ * muls, divs, intrinsics, if-comparisons, tape pushes and pops) into
+ * counts[7] = {adds, muls, divs, intrinsics, comparisons, tape_pushes,
+ * tape_pops} summed over all grid x block threads, and writes each thread's
+ * kernel-frame statement count to thread_statements[grid x block] (device
+ * memory for the device form, host memory for _host; may be NULL). */
+int adc_cuda_jit_launch_counted(adc_jit_module* module, int64_t grid_dim, int64_t block_dim,
+                                int64_t n, const adc_jit_arg* args, int32_t nargs, void* stream,
+                                uint64_t* counts, uint32_t* thread_statements);
+int adc_cuda_jit_launch_counted_host(adc_jit_module* module, int64_t grid_dim,
+                                     int64_t block_dim, int64_t n, const adc_jit_arg* args,
+                                     int32_t nargs, uint64_t* counts,
+                                     uint32_t* thread_statements);
 
 /* ---------------------------------------------------------------------------
  * chi2 histogram fit (FitEngine::chi2 / chi2_gradient, proj/src/fit.cpp:206-259)

@@ -147,10 +147,23 @@ LaunchStats launch_jit(const Program& p, const std::string& kernel, const Functi
       args[i].int_value = buffers.integers.at(prm.name);
     }
   }
+  // the counting variant: the reference's LaunchStats exactly (OpCounters
+  // summed over all threads, every thread's kernel-frame statements), for any
+  // kernel — data-dependent branches and loops included
   LaunchStats st;
-  analytic_counts(p, kernel, k, cfg, buffers, st);
-  check(adc_cuda_jit_launch_host(m, cfg.grid_dim, cfg.block_dim, cfg.n, args.data(),
-                                 static_cast<int32_t>(args.size())));
+  const int64_t total = cfg.grid_dim * cfg.block_dim;
+  st.thread_statements.assign(static_cast<size_t>(total), 0u);
+  uint64_t c[7] = {0, 0, 0, 0, 0, 0, 0};
+  check(adc_cuda_jit_launch_counted_host(m, cfg.grid_dim, cfg.block_dim, cfg.n, args.data(),
+                                         static_cast<int32_t>(args.size()), c,
+                                         st.thread_statements.data()));
+  st.counts.adds = c[0];
+  st.counts.muls = c[1];
+  st.counts.divs = c[2];
+  st.counts.intrinsics = c[3];
+  st.counts.comparisons = c[4];
+  st.counts.tape_pushes = c[5];
+  st.counts.tape_pops = c[6];
   return st;
 }
 

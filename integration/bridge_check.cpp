@@ -15,6 +15,7 @@
 #include "adc/parser.hpp"
 #include "adc/tooling.hpp"
 #include "adc_b200_bridge.hpp"
+#include "adc_cuda.h"
 #include "corpus_embed.inc"
 
 using namespace adc;
@@ -81,10 +82,16 @@ static void cpu_checks(const Program& p, bool gpu) {
   if (gpu)
     EXPECT(error_of([&] { b200_bridge::launch(p, "noop", {1, 1, 1}, b); }).empty(),
            "non-registered kernel (noop) runs through the JIT");
-  else
-    EXPECT(error_of([&] { b200_bridge::launch(p, "noop", {1, 1, 1}, b); }).find("no CUDA device") !=
-               std::string::npos,
-           "non-registered kernel goes to the JIT: no device -> Error, no interpreter fallback");
+  else {
+    int sms = 0, major = 0, minor = 0;
+    const bool have_device = adc_cuda_device_info(&sms, &major, &minor) == 0;
+    const std::string e = error_of([&] { b200_bridge::launch(p, "noop", {1, 1, 1}, b); });
+    if (have_device)  // `cpu` mode on a GPU machine: the JIT simply runs it
+      EXPECT(e.empty(), "non-registered kernel goes to the JIT (device present)");
+    else
+      EXPECT(e.find("no CUDA device") != std::string::npos,
+             "non-registered kernel goes to the JIT: no device -> Error, no interpreter fallback");
+  }
 }
 
 static void gpu_checks(const Program& p) {
@@ -195,6 +202,13 @@ static void gpu_checks(const Program& p) {
       std::printf("     JIT %s: worst rel %.3g\n", kern, worst);
       EXPECT(worst <= 1e-12, "bridged JIT launch matches adc::launch");
       EXPECT(rs.thread_statements == gs.thread_statements, "JIT LaunchStats.thread_statements");
+      std::printf("     JIT %s: counts adds %llu/%llu muls %llu/%llu divs %llu/%llu pushes %llu/%llu\n",
+                  kern, (unsigned long long)rs.counts.adds, (unsigned long long)gs.counts.adds,
+                  (unsigned long long)rs.counts.muls, (unsigned long long)gs.counts.muls,
+                  (unsigned long long)rs.counts.divs, (unsigned long long)gs.counts.divs,
+                  (unsigned long long)rs.counts.tape_pushes,
+                  (unsigned long long)gs.counts.tape_pushes);
+      EXPECT(rs.counts == gs.counts, "JIT LaunchStats.counts (exact, data-dependent kernels too)");
     }
   }
   // FitEngine::fit through the bridge vs the reference's own fit (both providers).

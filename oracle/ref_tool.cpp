@@ -314,8 +314,9 @@ int cmd_launch_file(int argc, char** argv) {
   if (mode == "unsafe") lo.unsafe = true;
   if (mode == "unsafe" || mode == "sequential") lo.sequential = true;
   std::string err;
+  LaunchStats st;
   try {
-    launch(prog, argv[2], LaunchConfig{n / block + 1, block, n}, b, lo);
+    st = launch(prog, argv[2], LaunchConfig{n / block + 1, block, n}, b, lo);
   } catch (const Error& e) {
     err = e.what();
   }
@@ -324,7 +325,18 @@ int cmd_launch_file(int argc, char** argv) {
     if (prm.type == ValType::RealArray) write_f64(out, b.arrays[prm.name]);
   std::ofstream mo(argv[7]);
   mo << text;
-  std::printf("{\"n\": %lld, \"error\": \"%s\"}\n", (long long)n, err.c_str());
+  // LaunchStats (launch.hpp:58-61): the OpCounters summed over all threads
+  // and every thread's kernel-frame statement count
+  const OpCounters& c = st.counts;
+  std::printf("{\"n\": %lld, \"error\": \"%s\", \"counts\": [%llu, %llu, %llu, %llu, %llu, "
+              "%llu, %llu], \"stm\": [",
+              (long long)n, err.c_str(), (unsigned long long)c.adds, (unsigned long long)c.muls,
+              (unsigned long long)c.divs, (unsigned long long)c.intrinsics,
+              (unsigned long long)c.comparisons, (unsigned long long)c.tape_pushes,
+              (unsigned long long)c.tape_pops);
+  for (size_t i = 0; i < st.thread_statements.size(); ++i)
+    std::printf("%s%u", i ? ", " : "", (unsigned)st.thread_statements[i]);
+  std::printf("]}\n");
   return 0;
 }
 

@@ -122,6 +122,12 @@ SIGNATURES = {
                                            _VP]),
     "adc_cuda_jit_launch_host": (ctypes.c_int, [_VP, _I64, _I64, _I64, ctypes.POINTER(JitArg),
                                                 _I32]),
+    "adc_cuda_jit_launch_counted": (ctypes.c_int, [_VP, _I64, _I64, _I64, ctypes.POINTER(JitArg),
+                                                   _I32, _VP, ctypes.POINTER(ctypes.c_uint64),
+                                                   _VP]),
+    "adc_cuda_jit_launch_counted_host": (ctypes.c_int, [_VP, _I64, _I64, _I64,
+                                                        ctypes.POINTER(JitArg), _I32,
+                                                        ctypes.POINTER(ctypes.c_uint64), _VP]),
     "adc_cuda_histogram_sample": (ctypes.c_int, [_I32, _I32, _D, _I64, _DBL, _DBL, _DBL,
                                                  ctypes.c_uint64, _I64, _VP, _D, _VP]),
     "adc_fit_default_options": (None, [ctypes.POINTER(FitOptions)]),

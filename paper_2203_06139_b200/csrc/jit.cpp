@@ -271,9 +271,16 @@ struct Parser {
   ExP unary() {
     if (is("-")) {
       expect("-");
+      ExP in = unary();
+      // a negated literal is a signed constant (parser.cpp:482-487; PI stays
+      // a negation) — no unary-minus op at run time, as in the interpreter
+      if (in->k == Ex::Num && !in->pi) {
+        in->v = -in->v;
+        return in;
+      }
       auto e = std::make_unique<Ex>();
       e->k = Ex::Neg;
-      e->a.push_back(unary());
+      e->a.push_back(std::move(in));
       return e;
     }
     return primary();
@@ -642,6 +649,17 @@ struct Emitter {
   bool unsafe;
   int tape_cap;
   bool prefetch = true;
+  // Counting variant (LaunchStats): every interpreter-counted operation of
+  // eval.cpp increments the thread's counter (adds: +, -, unary -, compound
+  // +=; muls; divs; intrinsics; comparisons: each if condition; tape pushes
+  // and pops) and every kernel-frame statement increments `st`.
+  bool count = false;
+  std::string C(const char* field, const std::string& e) const {
+    return count ? "(++ctx.cnt->" + std::string(field) + ", " + e + ")" : e;
+  }
+  void Cst(const char* field, int d) {
+    if (count) o << ind(d) << "++ctx.cnt->" << field << ";\n";
+  }
   // Slot caching: a void function whose array parameters are only ever
   // accessed at the literal index 0 (the length-1 slices of Listing-1 slots)
   // gets a second variant fn_<name>_c that keeps each such slot in a
@@ -678,10 +696,11 @@ struct Emitter {
         if (e.name == "threadIdx") return "(long long)threadIdx.x";
         if (e.name == "N") return "N";
         return V(e.name);
-      case Ex::Neg: return "(-" + ie(*e.a[0]) + ")";
+      case Ex::Neg: return C("a", "(-" + ie(*e.a[0]) + ")");
       case Ex::Bin:
-        return "(" + ie(*e.a[0]) + " " + std::string(1, e.op) + " " + ie(*e.a[1]) + ")";
-      case Ex::Call: return "adc_pop_ctl(ctl, cp, ctx)";
+        return C(e.op == '*' ? "m" : "a",
+                 "(" + ie(*e.a[0]) + " " + std::string(1, e.op) + " " + ie(*e.a[1]) + ")");
+      case Ex::Call: return C("po", "adc_pop_ctl(ctl, cp, ctx)");
       default: return "0";
     }
   }
@@ -691,24 +710,24 @@ struct Emitter {
     switch (e.k) {
       case Ex::Num: return dbl(e.v);
       case Ex::Var: return V(e.name);
-      case Ex::Neg: return "(-" + re(*e.a[0]) + ")";
+      case Ex::Neg: return C("a", "(-" + re(*e.a[0]) + ")");
       case Ex::Bin: {
         const std::string a = re(*e.a[0]), b = re(*e.a[1]);
         switch (e.op) {
-          case '+': return "__dadd_rn(" + a + ", " + b + ")";
-          case '-': return "__dsub_rn(" + a + ", " + b + ")";
-          case '*': return "__dmul_rn(" + a + ", " + b + ")";
-          default: return "adc_div(" + a + ", " + b + ", ctx)";
+          case '+': return C("a", "__dadd_rn(" + a + ", " + b + ")");
+          case '-': return C("a", "__dsub_rn(" + a + ", " + b + ")");
+          case '*': return C("m", "__dmul_rn(" + a + ", " + b + ")");
+          default: return C("d", "adc_div(" + a + ", " + b + ", ctx)");
         }
       }
       case Ex::Call: {
-        if (e.name == "__pop") return "adc_pop(tape, tp, ctx)";
+        if (e.name == "__pop") return C("po", "adc_pop(tape, tp, ctx)");
         std::vector<std::string> a;
         for (auto& c : e.a) a.push_back(re(*c));
-        if (e.name == "log") return "adc_log(" + a[0] + ", ctx)";
-        if (e.name == "sqrt") return "adc_sqrt(" + a[0] + ", ctx)";
-        if (e.name == "pow") return "pow(" + a[0] + ", " + a[1] + ")";
-        return e.name + "(" + a[0] + ")";
+        if (e.name == "log") return C("i", "adc_log(" + a[0] + ", ctx)");
+        if (e.name == "sqrt") return C("i", "adc_sqrt(" + a[0] + ", ctx)");
+        if (e.name == "pow") return C("i", "pow(" + a[0] + ", " + a[1] + ")");
+        return C("i", e.name + "(" + a[0] + ")");
       }
       case Ex::Index:
         if (cached != nullptr && cached->count(e.name)) return "c_" + V(e.name);
@@ -737,6 +756,10 @@ struct Emitter {
 
   void stmt(const St& s, const Fn& f, Scope& sc, int d) {
     VT t;
+    if (f.global) Cst("st", d);  // eval.cpp:402, the kernel frame's statements
+    if (s.k == St::Assign && s.compound) Cst("a", d);  // eval.cpp:420-447
+    if (s.k == St::If) Cst("c", d);                    // eval.cpp:647
+    if (s.k == St::Call && (s.callee == "__push" || s.callee == "__push_ctl")) Cst("pu", d);
     switch (s.k) {
       case St::Decl:
         if (s.type == VT::Integer)
@@ -880,7 +903,13 @@ struct Emitter {
     o << R"(// Generated by libadc_b200 (csrc/jit.cpp) from a DSL module; sm_100a, -fmad=false.
 struct AdcArr { double* p; long long len; };
 struct AdcErr { unsigned long long code; long long thread; long long aux; };
-struct AdcCtx { AdcErr* err; long long tid; };
+)";
+    if (count)
+      o << "struct AdcCnt { unsigned long long a, m, d, i, c, pu, po, st; };\n"
+           "struct AdcCtx { AdcErr* err; long long tid; AdcCnt* cnt; };\n";
+    else
+      o << "struct AdcCtx { AdcErr* err; long long tid; };\n";
+    o << R"(
 enum { ADC_JE_DIV0 = 1, ADC_JE_LOG = 2, ADC_JE_SQRT = 3, ADC_JE_INDEX = 4, ADC_JE_TAPE_FULL = 5,
        ADC_JE_TAPE_EMPTY = 6, ADC_JE_CTL_EMPTY = 7 };
 __device__ __noinline__ void adc_fail(const AdcCtx& c, unsigned code, long long aux) {
@@ -1034,8 +1063,14 @@ __device__ __forceinline__ long long adc_pop_ctl(long long* t, int& cp, const Ad
         else
           o << ptype(p.type) << " " << V(p.name);
       }
-      o << (f.params.empty() ? "" : ", ") << "long long N, AdcErr* adc_err) {\n";
-      o << "  const AdcCtx ctx{adc_err, (long long)blockIdx.x * blockDim.x + threadIdx.x};\n";
+      o << (f.params.empty() ? "" : ", ") << "long long N, AdcErr* adc_err"
+        << (count ? ", unsigned long long* adc_cnt_out, unsigned* adc_stm" : "") << ") {\n";
+      if (count)
+        o << "  AdcCnt adc_cnt{};\n"
+             "  const AdcCtx ctx{adc_err, (long long)blockIdx.x * blockDim.x + threadIdx.x, "
+             "&adc_cnt};\n";
+      else
+        o << "  const AdcCtx ctx{adc_err, (long long)blockIdx.x * blockDim.x + threadIdx.x};\n";
       for (auto& p : f.params)
         if (p.type == VT::RealArray)
           o << "  const AdcArr " << V(p.name) << "{" << V(p.name) << "_p, " << V(p.name) << "_n};\n";
@@ -1049,6 +1084,21 @@ __device__ __forceinline__ long long adc_pop_ctl(long long* t, int& cp, const Ad
     if (f.uses_ctl) o << "  long long ctl[ADC_TAPE]; int cp = 0;\n";
     block(f.body, f, sc, 1);
     if (!f.returns_void && !f.global) o << "  return __longlong_as_double(0x7ff8000000000000LL);\n";
+    if (f.global && count)  // per-block sums of the counters, one atomic per counter per block
+      o << R"(  __shared__ unsigned long long adc_bs[7];
+  if (threadIdx.x < 7) adc_bs[threadIdx.x] = 0ull;
+  __syncthreads();
+  atomicAdd(&adc_bs[0], adc_cnt.a);
+  atomicAdd(&adc_bs[1], adc_cnt.m);
+  atomicAdd(&adc_bs[2], adc_cnt.d);
+  atomicAdd(&adc_bs[3], adc_cnt.i);
+  atomicAdd(&adc_bs[4], adc_cnt.c);
+  atomicAdd(&adc_bs[5], adc_cnt.pu);
+  atomicAdd(&adc_bs[6], adc_cnt.po);
+  __syncthreads();
+  if (threadIdx.x < 7 && adc_bs[threadIdx.x] != 0ull) atomicAdd(adc_cnt_out + threadIdx.x, adc_bs[threadIdx.x]);
+  if (adc_stm != nullptr) adc_stm[ctx.tid] = (unsigned)adc_cnt.st;
+)";
     o << "}\n\n";
   }
 };
@@ -1071,6 +1121,16 @@ struct adc_jit_module {
   std::map<int, ErrWordT*> derr;  // per device, reset before every launch
   ErrWordT* herr = nullptr;       // pinned
   std::string kernel;
+  std::string source;  // the module text (the counting variant is built from it on demand)
+  bool unsafe = false;
+  int tape_capacity = 256;
+  // counting variant (adc_cuda_jit_launch_counted): built on first use
+  std::string cuda_counted;
+  std::vector<char> cubin_counted;
+  std::map<int, cudaLibrary_t> libs_counted;
+  std::map<int, cudaKernel_t> fns_counted;
+  unsigned long long* dcnt = nullptr;  // [7] device counters (the device of the last counted launch)
+  int dcnt_dev = -1;
   std::vector<int32_t> kinds;  // 0 real[], 1 real, 2 integer
   std::vector<std::string> names;
   std::string cuda;
@@ -1100,27 +1160,12 @@ int parse_module(const std::string& src, Module& m) {
 }
 }  // namespace
 
-extern "C" int adc_jit_compile(const char* source, const char* kernel, int32_t unsafe,
-                               int32_t tape_capacity, adc_jit_module** out) {
-  clear_error();
-  if (source == nullptr || kernel == nullptr || out == nullptr)
-    return fail(ADC_E_ARG, "null argument");
-  *out = nullptr;
-  if (tape_capacity <= 0) tape_capacity = 256;
-  Module m;
-  if (int rc = parse_module(source, m)) return rc;
-  const Fn* k = m.find(kernel);
-  if (k == nullptr) return fail(ADC_E_LAUNCH, std::string("unknown kernel '") + kernel + "'");
-  if (!k->global) return fail(ADC_E_LAUNCH, std::string("'") + kernel + "' is not a global kernel");
-  // race_check (launch.cpp:261-267): same refusal message
-  std::set<std::string> arrays;
-  for (auto& p : k->params)
-    if (p.type == VT::RealArray) arrays.insert(p.name);
-  std::map<std::string, std::string> haz;
-  std::string tvar;
-  kernel_hazards(m, k->body, "", arrays, haz, tvar);
-  if (!haz.empty() && !unsafe) return fail(ADC_E_LAUNCH, hazard_message(haz));
-  Emitter em{m, unsafe != 0, tape_capacity};
+namespace {
+// Emission (plain or counting variant) and NVRTC compilation of kernel k of m.
+int emit_and_compile(const Module& m, const Fn* k, const std::string& kernel, bool unsafe,
+                     int tape_capacity, bool count, std::string& cuda, std::vector<char>& cubin) {
+  Emitter em{m, unsafe, tape_capacity};
+  em.count = count;
   if (const char* e = getenv("ADC_JIT_PREFETCH")) em.prefetch = atoi(e) != 0;  // experiment knob
   try {
     em.prelude();
@@ -1163,20 +1208,10 @@ extern "C" int adc_jit_compile(const char* source, const char* kernel, int32_t u
   }
   const Nvrtc* N = nvrtc();
   if (N == nullptr) return fail(ADC_E_CUDA, "jit: libnvrtc.so.12 could not be loaded");
-  auto* J = new (std::nothrow) adc_jit_module();
-  if (J == nullptr) return fail(ADC_E_ARG, "out of host memory");
-  J->kernel = kernel;
-  for (auto& p : k->params) {
-    J->kinds.push_back(p.type == VT::RealArray ? 0 : p.type == VT::Real ? 1 : 2);
-    J->names.push_back(p.name);
-  }
-  J->cuda = em.o.str();
+  cuda = em.o.str();
   nvrtcProgram prog = nullptr;
-  nvrtcResult r = N->create(&prog, J->cuda.c_str(), "adc_jit.cu", 0, nullptr, nullptr);
-  if (r != NVRTC_SUCCESS) {
-    delete J;
-    return fail(ADC_E_CUDA, std::string("nvrtcCreateProgram: ") + N->error_string(r));
-  }
+  nvrtcResult r = N->create(&prog, cuda.c_str(), "adc_jit.cu", 0, nullptr, nullptr);
+  if (r != NVRTC_SUCCESS) return fail(ADC_E_CUDA, std::string("nvrtcCreateProgram: ") + N->error_string(r));
   const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "--std=c++17",
                         "-default-device", "--extra-device-vectorization"};
   r = N->compile(prog, 5, opts);
@@ -1186,14 +1221,52 @@ extern "C" int adc_jit_compile(const char* source, const char* kernel, int32_t u
     std::string log(n, '\0');
     if (n) N->log(prog, &log[0]);
     N->destroy(&prog);
-    delete J;
     return fail(ADC_E_CUDA, "jit: NVRTC failed: " + log);
   }
   size_t n = 0;
   N->cubin_size(prog, &n);
-  J->cubin.resize(n);
-  N->cubin(prog, J->cubin.data());
+  cubin.resize(n);
+  N->cubin(prog, cubin.data());
   N->destroy(&prog);
+  return ADC_OK;
+}
+}  // namespace
+
+extern "C" int adc_jit_compile(const char* source, const char* kernel, int32_t unsafe,
+                               int32_t tape_capacity, adc_jit_module** out) {
+  clear_error();
+  if (source == nullptr || kernel == nullptr || out == nullptr)
+    return fail(ADC_E_ARG, "null argument");
+  *out = nullptr;
+  if (tape_capacity <= 0) tape_capacity = 256;
+  Module m;
+  if (int rc = parse_module(source, m)) return rc;
+  const Fn* k = m.find(kernel);
+  if (k == nullptr) return fail(ADC_E_LAUNCH, std::string("unknown kernel '") + kernel + "'");
+  if (!k->global) return fail(ADC_E_LAUNCH, std::string("'") + kernel + "' is not a global kernel");
+  // race_check (launch.cpp:261-267): same refusal message
+  std::set<std::string> arrays;
+  for (auto& p : k->params)
+    if (p.type == VT::RealArray) arrays.insert(p.name);
+  std::map<std::string, std::string> haz;
+  std::string tvar;
+  kernel_hazards(m, k->body, "", arrays, haz, tvar);
+  if (!haz.empty() && !unsafe) return fail(ADC_E_LAUNCH, hazard_message(haz));
+  auto* J = new (std::nothrow) adc_jit_module();
+  if (J == nullptr) return fail(ADC_E_ARG, "out of host memory");
+  J->kernel = kernel;
+  J->source = source;
+  J->unsafe = unsafe != 0;
+  J->tape_capacity = tape_capacity;
+  for (auto& p : k->params) {
+    J->kinds.push_back(p.type == VT::RealArray ? 0 : p.type == VT::Real ? 1 : 2);
+    J->names.push_back(p.name);
+  }
+  if (int rc = emit_and_compile(m, k, kernel, unsafe != 0, tape_capacity, false, J->cuda,
+                                J->cubin)) {
+    delete J;
+    return rc;
+  }
   *out = J;
   return ADC_OK;
 }
@@ -1201,6 +1274,8 @@ extern "C" int adc_jit_compile(const char* source, const char* kernel, int32_t u
 extern "C" int adc_jit_destroy(adc_jit_module* J) {
   if (J == nullptr) return ADC_OK;
   for (auto& l : J->libs) cudaLibraryUnload(l.second);
+  for (auto& l : J->libs_counted) cudaLibraryUnload(l.second);
+  if (J->dcnt) cudaFree(J->dcnt);
   for (auto& e : J->derr) cudaFree(e.second);
   if (J->herr) cudaFreeHost(J->herr);
   delete J;
@@ -1242,9 +1317,12 @@ const char* jit_error_text(unsigned long long code) {
 
 }  // namespace
 
-extern "C" int adc_cuda_jit_launch(adc_jit_module* J, int64_t grid, int64_t block, int64_t n,
-                                   const adc_jit_arg* args, int32_t nargs, void* stream) {
-  clear_error();
+namespace {
+// counted: the counting variant (built on first use); counts[7] (host) gets
+// the OpCounters summed over all threads, stm (device, grid*block) every
+// thread's kernel-frame statement count when non-null.
+int jit_launch(adc_jit_module* J, int64_t grid, int64_t block, int64_t n, const adc_jit_arg* args,
+               int32_t nargs, void* stream, bool counted, uint64_t* counts, uint32_t* stm) {
   if (J == nullptr || (nargs > 0 && args == nullptr)) return fail(ADC_E_ARG, "null argument");
   if (grid <= 0 || block <= 0 || n <= 0)
     return fail(ADC_E_LAUNCH, "launch configuration must be positive (grid " +
@@ -1272,18 +1350,34 @@ extern "C" int adc_cuda_jit_launch(adc_jit_module* J, int64_t grid, int64_t bloc
       J->derr[dev] = d;
     }
     derr = J->derr[dev];
-    auto it = J->fns.find(dev);
-    if (it == J->fns.end()) {
+    if (counted && J->cubin_counted.empty()) {
+      Module m;
+      if (int rc = parse_module(J->source, m)) return rc;
+      if (int rc = emit_and_compile(m, m.find(J->kernel), J->kernel, J->unsafe, J->tape_capacity,
+                                    true, J->cuda_counted, J->cubin_counted))
+        return rc;
+    }
+    if (counted && (J->dcnt == nullptr || J->dcnt_dev != dev)) {
+      if (J->dcnt) cudaFree(J->dcnt);
+      J->dcnt = nullptr;
+      ADCB_CUDA(cudaMalloc(&J->dcnt, 7 * sizeof(unsigned long long)));
+      J->dcnt_dev = dev;
+    }
+    auto& fns = counted ? J->fns_counted : J->fns;
+    auto& libs = counted ? J->libs_counted : J->libs;
+    const std::vector<char>& cubin = counted ? J->cubin_counted : J->cubin;
+    auto it = fns.find(dev);
+    if (it == fns.end()) {
       cudaLibrary_t lib = nullptr;
-      ADCB_CUDA(cudaLibraryLoadData(&lib, J->cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+      ADCB_CUDA(cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
       const std::string name = "adc_kernel_" + J->kernel;
       cudaError_t e = cudaLibraryGetKernel(&fn, lib, name.c_str());
       if (e != cudaSuccess) {
         cudaLibraryUnload(lib);
         return cuda_fail(e, "cudaLibraryGetKernel");
       }
-      J->libs[dev] = lib;
-      J->fns[dev] = fn;
+      libs[dev] = lib;
+      fns[dev] = fn;
     } else {
       fn = it->second;
     }
@@ -1318,10 +1412,23 @@ extern "C" int adc_cuda_jit_launch(adc_jit_module* J, int64_t grid, int64_t bloc
   long long nn = n;
   kp.push_back(&nn);
   kp.push_back(&derr);
+  unsigned long long* dcnt = J->dcnt;
+  uint32_t* dstm = stm;
+  if (counted) {
+    ADCB_CUDA(cudaMemsetAsync(dcnt, 0, 7 * sizeof(unsigned long long), s));
+    kp.push_back(&dcnt);
+    kp.push_back(&dstm);
+  }
   cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void*>(fn), dim3((unsigned)grid),
                                    dim3((unsigned)block), kp.data(), 0, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel (jit)");
   ADCB_CUDA(cudaMemcpyAsync(J->herr, derr, sizeof(ErrWordT), cudaMemcpyDeviceToHost, s));
+  if (counted) {
+    unsigned long long h[7];
+    ADCB_CUDA(cudaMemcpyAsync(h, dcnt, sizeof h, cudaMemcpyDeviceToHost, s));
+    ADCB_CUDA(cudaStreamSynchronize(s));
+    for (int i = 0; i < 7; ++i) counts[i] = h[i];
+  }
   ADCB_CUDA(cudaStreamSynchronize(s));
   const ErrWordT herr = *J->herr;
   if (herr.code != 0) {
@@ -1331,10 +1438,27 @@ extern "C" int adc_cuda_jit_launch(adc_jit_module* J, int64_t grid, int64_t bloc
   }
   return ADC_OK;
 }
+}  // namespace
 
-extern "C" int adc_cuda_jit_launch_host(adc_jit_module* J, int64_t grid, int64_t block, int64_t n,
-                                        const adc_jit_arg* args, int32_t nargs) {
+extern "C" int adc_cuda_jit_launch(adc_jit_module* J, int64_t grid, int64_t block, int64_t n,
+                                   const adc_jit_arg* args, int32_t nargs, void* stream) {
   clear_error();
+  return jit_launch(J, grid, block, n, args, nargs, stream, false, nullptr, nullptr);
+}
+
+extern "C" int adc_cuda_jit_launch_counted(adc_jit_module* J, int64_t grid, int64_t block,
+                                           int64_t n, const adc_jit_arg* args, int32_t nargs,
+                                           void* stream, uint64_t* counts,
+                                           uint32_t* thread_statements) {
+  clear_error();
+  if (counts == nullptr) return fail(ADC_E_ARG, "null argument");
+  return jit_launch(J, grid, block, n, args, nargs, stream, true, counts, thread_statements);
+}
+
+namespace {
+int jit_launch_host(adc_jit_module* J, int64_t grid, int64_t block, int64_t n,
+                    const adc_jit_arg* args, int32_t nargs, bool counted, uint64_t* counts,
+                    uint32_t* thread_statements) {
   if (J == nullptr || (nargs > 0 && args == nullptr)) return fail(ADC_E_ARG, "null argument");
   if (nargs != (int32_t)J->kinds.size())
     return fail(ADC_E_LAUNCH, "kernel '" + J->kernel + "' takes " +
@@ -1358,7 +1482,21 @@ extern "C" int adc_cuda_jit_launch_host(adc_jit_module* J, int64_t grid, int64_t
     owned.push_back(d);
     dargs[i].ptr = d;
   }
-  const int rc = adc_cuda_jit_launch(J, grid, block, n, dargs.data(), nargs, nullptr);
+  uint32_t* dstm = nullptr;
+  const size_t total = grid > 0 && block > 0 ? (size_t)grid * (size_t)block : 0;
+  if (counted && thread_statements != nullptr && total > 0) {
+    cudaError_t e = cudaMalloc(&dstm, total * sizeof(uint32_t));
+    if (e != cudaSuccess) {
+      release();
+      return cuda_fail(e, "jit statement counts");
+    }
+  }
+  const int rc = jit_launch(J, grid, block, n, dargs.data(), nargs, nullptr, counted, counts, dstm);
+  if (dstm != nullptr) {
+    if (rc == ADC_OK)
+      cudaMemcpy(thread_statements, dstm, total * sizeof(uint32_t), cudaMemcpyDeviceToHost);
+    cudaFree(dstm);
+  }
   // buffers are written in place even when a thread reported an error, as in
   // the reference (a throwing launch leaves the other threads' writes)
   for (int32_t i = 0, k = 0; i < nargs; ++i) {
@@ -1369,4 +1507,19 @@ extern "C" int adc_cuda_jit_launch_host(adc_jit_module* J, int64_t grid, int64_t
   }
   release();
   return rc;
+}
+}  // namespace
+
+extern "C" int adc_cuda_jit_launch_host(adc_jit_module* J, int64_t grid, int64_t block, int64_t n,
+                                        const adc_jit_arg* args, int32_t nargs) {
+  clear_error();
+  return jit_launch_host(J, grid, block, n, args, nargs, false, nullptr, nullptr);
+}
+
+extern "C" int adc_cuda_jit_launch_counted_host(adc_jit_module* J, int64_t grid, int64_t block,
+                                                int64_t n, const adc_jit_arg* args, int32_t nargs,
+                                                uint64_t* counts, uint32_t* thread_statements) {
+  clear_error();
+  if (counts == nullptr) return fail(ADC_E_ARG, "null argument");
+  return jit_launch_host(J, grid, block, n, args, nargs, true, counts, thread_statements);
 }

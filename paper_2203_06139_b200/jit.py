@@ -45,7 +45,13 @@ class JitModule:
     def cubin_size(self) -> int:
         return lib.adc_jit_cubin_size(self._p)
 
-    def launch(self, cfg: LaunchConfig, buffers: BufferSet) -> LaunchStats:
+    COUNT_FIELDS = ("adds", "muls", "divs", "intrinsics", "comparisons", "tape_pushes",
+                    "tape_pops")
+
+    def launch(self, cfg: LaunchConfig, buffers: BufferSet, counts: bool = False) -> LaunchStats:
+        """adc::launch over this module's kernel.  counts=True runs the
+        counting variant and returns the reference's LaunchStats exactly
+        (OpCounters sums and every thread's kernel-frame statements)."""
         cfg.validate()
         args = (JitArg * max(1, len(self.params)))()
         device = None
@@ -76,6 +82,25 @@ class JitModule:
                 if name not in buffers.integers:
                     raise AdcError("Launch", f"missing integer value '{name}'")
                 args[i].int_value = int(buffers.integers[name])
+        total = cfg.grid_dim * cfg.block_dim
+        if counts:
+            c = (ctypes.c_uint64 * 7)()
+            if device:
+                import torch
+                stm = torch.zeros(total, dtype=torch.int32, device="cuda")
+                stream = torch.cuda.current_stream().cuda_stream
+                check(lib.adc_cuda_jit_launch_counted(
+                    self._p, cfg.grid_dim, cfg.block_dim, cfg.n, args, len(self.params),
+                    ctypes.c_void_p(stream), c, ctypes.c_void_p(stm.data_ptr())))
+                stm = stm.cpu().numpy().view(np.uint32)
+            else:
+                stm = np.zeros(total, dtype=np.uint32)
+                check(lib.adc_cuda_jit_launch_counted_host(
+                    self._p, cfg.grid_dim, cfg.block_dim, cfg.n, args, len(self.params), c,
+                    stm.ctypes.data_as(ctypes.c_void_p)))
+            return LaunchStats(active=cfg.n, idle=total - cfg.n,
+                               counts=dict(zip(self.COUNT_FIELDS, (int(v) for v in c))),
+                               statements=stm)
         if device:
             import torch
             stream = torch.cuda.current_stream().cuda_stream
@@ -84,7 +109,7 @@ class JitModule:
         else:
             check(lib.adc_cuda_jit_launch_host(self._p, cfg.grid_dim, cfg.block_dim, cfg.n, args,
                                                len(self.params)))
-        return LaunchStats(active=cfg.n, idle=cfg.grid_dim * cfg.block_dim - cfg.n)
+        return LaunchStats(active=cfg.n, idle=total - cfg.n)
 
     def close(self):
         if self._p:
@@ -102,13 +127,15 @@ _cache: Dict[Tuple[str, str, bool, int], JitModule] = {}
 
 
 def launch_module(module_source: str, kernel: str, cfg: LaunchConfig, buffers: BufferSet,
-                  opts: LaunchOptions | None = None, tape_capacity: int = 0) -> LaunchStats:
+                  opts: LaunchOptions | None = None, tape_capacity: int = 0,
+                  counts: bool = False) -> LaunchStats:
     """adc::launch(Program(module), kernel, cfg, buffers, opts) through the JIT;
-    compiled modules are cached per (source, kernel, unsafe, tape capacity)."""
+    compiled modules are cached per (source, kernel, unsafe, tape capacity).
+    counts=True returns the exact LaunchStats (see JitModule.launch)."""
     opts = opts or LaunchOptions()
     key = (module_source, kernel, bool(opts.unsafe), int(tape_capacity))
     mod = _cache.get(key)
     if mod is None:
         mod = JitModule(module_source, kernel, opts.unsafe, tape_capacity)
         _cache[key] = mod
-    return mod.launch(cfg, buffers)
+    return mod.launch(cfg, buffers, counts)

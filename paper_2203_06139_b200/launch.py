@@ -68,14 +68,21 @@ class LaunchOptions:
 
 @dataclass
 class LaunchStats:
-    """launch.hpp:58-61; thread_statements is derived analytically for the
-    Listing-1 shape: 3 kernel-frame statements for g < n, 2 for the padding
-    threads (test_launch.cpp:119-128).  Materialised on first access."""
+    """launch.hpp:58-61.  Registered (hand-written) kernels: thread_statements
+    is the Listing-1 shape's — 3 kernel-frame statements for g < n, 2 for the
+    padding threads (test_launch.cpp:119-128), materialised on first access.
+    JIT launches with counts=True carry the exact per-thread statements and
+    the OpCounters sums (`counts`: adds, muls, divs, intrinsics, comparisons,
+    tape_pushes, tape_pops) from the counting variant of the kernel."""
     active: int
     idle: int
+    counts: dict | None = None
+    statements: np.ndarray | None = None
 
     @property
     def thread_statements(self) -> np.ndarray:
+        if self.statements is not None:
+            return self.statements
         ts = np.full(self.active + self.idle, 2, dtype=np.uint32)
         ts[:self.active] = 3
         return ts
@@ -117,7 +124,7 @@ def _stream_of(a):
 
 def launch(kernel: str, cfg: LaunchConfig, buffers: BufferSet,
            opts: LaunchOptions | None = None, callee_fingerprint: int | None = None,
-           module: str | None = None) -> LaunchStats:
+           module: str | None = None, counts: bool = False) -> LaunchStats:
     """adc::launch (launch.cpp:252-346) for the Listing-1 kernels of kernels.dsl:
     `compute` (private slots) and `compute_shared` (the shared dsigma slot:
     refused unless opts.unsafe, then reduced in a fixed order, deterministic),
@@ -127,7 +134,7 @@ def launch(kernel: str, cfg: LaunchConfig, buffers: BufferSet,
     opts = opts or LaunchOptions()
     if module is not None and kernel not in ("compute", "compute_shared"):
         from .jit import launch_module
-        return launch_module(module, kernel, cfg, buffers, opts)
+        return launch_module(module, kernel, cfg, buffers, opts, counts=counts)
     cfg.validate()
     shared = kernel == "compute_shared"
     if shared:

@@ -155,6 +155,10 @@ def main():
         ji[f"{key}_n"] = nn
         ji[f"{key}_mode"] = mode
         ji[f"{key}_error"] = meta["error"]
+        # LaunchStats: OpCounters over all threads (adds, muls, divs, intrinsics,
+        # comparisons, tape_pushes, tape_pops) and per-thread statements
+        ji[f"{key}_counts"] = np.array(meta["counts"], dtype=np.int64)
+        ji[f"{key}_stm"] = np.array(meta["stm"], dtype=np.uint32)
         ji[f"{key}_nparams"] = len(params)
         for i, v in enumerate(params):
             ji[f"{key}_in{i}"] = np.asarray(v, dtype=np.float64)

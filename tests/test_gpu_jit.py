@@ -22,7 +22,7 @@ MODULE = str(G["module"])
 EXACT = {"rational", "poly", "looped"}
 
 
-def _run(key, device, **kw):
+def _run(key, device, counts=False, **kw):
     kern = str(G[f"{key}_kernel"])
     n = int(G[f"{key}_n"])
     unsafe = str(G[f"{key}_mode"]) == "unsafe"
@@ -41,13 +41,13 @@ def _run(key, device, **kw):
             bufs.scalars[name] = float(v)
         else:
             bufs.integers[name] = int(v)
-    st = m.launch(adc.LaunchConfig(n // 256 + 1, 256, n), bufs)
+    st = m.launch(adc.LaunchConfig(n // 256 + 1, 256, n), bufs, counts=counts)
     assert st.active == n
     outs = [bufs.arrays[a] for a in arrays]
     if device:
         torch.cuda.synchronize()
         outs = [o.cpu().numpy() for o in outs]
-    return outs
+    return (outs, st) if counts else outs
 
 
 @pytest.mark.parametrize("key", ["gauss", "rational", "branchy", "poly", "looped", "gsum",
@@ -65,6 +65,22 @@ def test_corpus_gradient_matches_reference_launch(key, device):
         else:
             scale = np.maximum(np.maximum(np.abs(got), np.abs(ref)), np.abs(ins[i]))
             assert (np.abs(got - ref) <= 1e-12 * np.maximum(scale, 1e-300)).all(), (key, i)
+
+
+@pytest.mark.parametrize("key", ["gauss", "rational", "branchy", "poly", "looped", "gsum",
+                                 "sumn", "hess"])
+@pytest.mark.parametrize("device", [True, False])
+def test_launch_stats_equal_reference(key, device):
+    """LaunchStats from the counting variant equal the reference launch's:
+    the OpCounters sums over all threads (data-dependent branches and loops:
+    branchy, looped, sumn) and every thread's kernel-frame statement count;
+    the results are those of the plain variant."""
+    outs, st = _run(key, device, counts=True)
+    assert tuple(st.counts.values()) == tuple(int(v) for v in G[f"{key}_counts"])
+    assert st.thread_statements.tobytes() == G[f"{key}_stm"].astype(np.uint32).tobytes()
+    if key in EXACT:
+        for i, got in enumerate(outs):
+            assert got.tobytes() == G[f"{key}_out{i}"].tobytes(), (key, i)
 
 
 def test_domain_error_is_eval():
