@@ -60,3 +60,13 @@ global void k_hess(real[] x, real[] p, real sigma, real[] dx, real[] dp, real[] 
     gauss_grad_0_1_darg0(x[i], p[i], sigma, dx[i], dp[i], hx[i], hp[i]);
   }
 }
+
+// Integer overflow (eval.cpp:601-628 raises "integer overflow"): the index
+// arithmetic of this kernel overflows int64 in every active thread.
+global void k_iovf(real[] x, integer big, real[] dx) {
+  integer i = blockIdx * blockDim + threadIdx;
+  if (i < N) {
+    integer k = big * big;
+    dx[i] += x[i] * k;
+  }
+}

@@ -696,10 +696,12 @@ struct Emitter {
         if (e.name == "threadIdx") return "(long long)threadIdx.x";
         if (e.name == "N") return "N";
         return V(e.name);
-      case Ex::Neg: return C("a", "(-" + ie(*e.a[0]) + ")");
+      // int64 arithmetic with the interpreter's overflow errors (eval.cpp:601-628)
+      case Ex::Neg: return C("a", "adc_ineg(" + ie(*e.a[0]) + ", ctx)");
       case Ex::Bin:
         return C(e.op == '*' ? "m" : "a",
-                 "(" + ie(*e.a[0]) + " " + std::string(1, e.op) + " " + ie(*e.a[1]) + ")");
+                 std::string(e.op == '+' ? "adc_iadd(" : e.op == '-' ? "adc_isub(" : "adc_imul(") +
+                     ie(*e.a[0]) + ", " + ie(*e.a[1]) + ", ctx)");
       case Ex::Call: return C("po", "adc_pop_ctl(ctl, cp, ctx)");
       default: return "0";
     }
@@ -795,7 +797,8 @@ struct Emitter {
             o << ind(d) << "adc_st(" << V(s.target) << ", " << idx << ", " << v << ", ctx);\n";
         } else if (t == VT::Integer) {
           const std::string v = ie_any(*s.expr);
-          if (s.compound) o << ind(d) << V(s.target) << " = " << V(s.target) << " + " << v << ";\n";
+          if (s.compound)
+            o << ind(d) << V(s.target) << " = adc_iadd(" << V(s.target) << ", " << v << ", ctx);\n";
           else o << ind(d) << V(s.target) << " = " << v << ";\n";
         } else {
           const std::string v = re(*s.expr);
@@ -911,7 +914,7 @@ struct AdcErr { unsigned long long code; long long thread; long long aux; };
       o << "struct AdcCtx { AdcErr* err; long long tid; };\n";
     o << R"(
 enum { ADC_JE_DIV0 = 1, ADC_JE_LOG = 2, ADC_JE_SQRT = 3, ADC_JE_INDEX = 4, ADC_JE_TAPE_FULL = 5,
-       ADC_JE_TAPE_EMPTY = 6, ADC_JE_CTL_EMPTY = 7 };
+       ADC_JE_TAPE_EMPTY = 6, ADC_JE_CTL_EMPTY = 7, ADC_JE_IOVF = 8 };
 __device__ __noinline__ void adc_fail(const AdcCtx& c, unsigned code, long long aux) {
   if (atomicCAS(&c.err->code, 0ull, (unsigned long long)code) == 0ull) {
     c.err->thread = c.tid;
@@ -929,6 +932,30 @@ __device__ __forceinline__ double adc_log(double a, const AdcCtx& c) {
 __device__ __forceinline__ double adc_sqrt(double a, const AdcCtx& c) {
   if (a < 0.0) adc_fail(c, ADC_JE_SQRT, 0);
   return __dsqrt_rn(a);
+}
+__device__ __forceinline__ long long adc_iadd(long long a, long long b, const AdcCtx& c) {
+  const long long r = (long long)((unsigned long long)a + (unsigned long long)b);
+  if (((a ^ r) & (b ^ r)) < 0) adc_fail(c, ADC_JE_IOVF, 0);
+  return r;
+}
+__device__ __forceinline__ long long adc_isub(long long a, long long b, const AdcCtx& c) {
+  const long long r = (long long)((unsigned long long)a - (unsigned long long)b);
+  if (((a ^ b) & (a ^ r)) < 0) adc_fail(c, ADC_JE_IOVF, 0);
+  return r;
+}
+__device__ __forceinline__ long long adc_imul(long long a, long long b, const AdcCtx& c) {
+  const long long r = (long long)((unsigned long long)a * (unsigned long long)b);
+  const long long mn = -9223372036854775807LL - 1;
+  bool ovf;
+  if (a == -1) ovf = b == mn;  // (r / a would itself overflow)
+  else if (b == -1) ovf = a == mn;
+  else ovf = a != 0 && r / a != b;
+  if (ovf) adc_fail(c, ADC_JE_IOVF, 0);
+  return r;
+}
+__device__ __forceinline__ long long adc_ineg(long long a, const AdcCtx& c) {
+  if (a == (-9223372036854775807LL - 1)) adc_fail(c, ADC_JE_IOVF, 0);
+  return (long long)(0ull - (unsigned long long)a);
 }
 __device__ __forceinline__ bool adc_ok(const AdcArr& a, long long i, const AdcCtx& c) {
   if (i < 0 || i >= a.len) { adc_fail(c, ADC_JE_INDEX, i); return false; }
@@ -1311,6 +1338,7 @@ const char* jit_error_text(unsigned long long code) {
     case 5: return "tape capacity exceeded (raise tape_capacity)";
     case 6: return "__pop on empty tape";
     case 7: return "__pop_ctl on empty control tape";
+    case 8: return "integer overflow";
     default: return "device error";
   }
 }

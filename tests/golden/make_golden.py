@@ -131,6 +131,7 @@ def main():
                                np.zeros(n), np.zeros(n), np.zeros(n)], ""),
         ("gauss_div0", "k_gauss", 64, [np.ones(64), np.zeros(64), 0.0, np.zeros(64),
                                        np.zeros(64)], "sequential"),
+        ("iovf", "k_iovf", 64, [np.ones(64), 3037000500, np.zeros(64)], "sequential"),
     )
     for key, kern, nn, params, mode in cases:
         flat = []

@@ -90,6 +90,14 @@ def test_domain_error_is_eval():
     assert "division by zero" in str(G["gauss_div0_error"])
 
 
+def test_integer_overflow_is_eval():
+    # int64 arithmetic raises like the interpreter (eval.cpp:601-628)
+    with pytest.raises(adc.AdcError) as e:
+        _run("iovf", True)
+    assert e.value.kind == "Eval" and "integer overflow" in str(e.value)
+    assert "integer overflow" in str(G["iovf_error"])
+
+
 def test_index_out_of_range_is_eval():
     m = adc.JitModule(MODULE, "k_sumn", unsafe=True)
     x = torch.zeros(64, dtype=torch.float64, device="cuda")
