@@ -1484,6 +1484,36 @@ extern "C" int adc_cuda_jit_launch_counted(adc_jit_module* J, int64_t grid, int6
 }
 
 namespace {
+// A larger tape: the module is re-emitted and recompiled with `cap` entries
+// per frame tape (both variants; the loaded images are dropped).
+int jit_grow_tape(adc_jit_module* J, int cap) {
+  std::lock_guard<std::mutex> lock(J->mu);
+  if (J->tape_capacity >= cap) return ADC_OK;
+  Module m;
+  if (int rc = parse_module(J->source, m)) return rc;
+  std::string cuda;
+  std::vector<char> cubin;
+  if (int rc = emit_and_compile(m, m.find(J->kernel), J->kernel, J->unsafe, cap, false, cuda, cubin))
+    return rc;
+  for (auto& l : J->libs) cudaLibraryUnload(l.second);
+  for (auto& l : J->libs_counted) cudaLibraryUnload(l.second);
+  J->libs.clear();
+  J->fns.clear();
+  J->libs_counted.clear();
+  J->fns_counted.clear();
+  J->cuda = std::move(cuda);
+  J->cubin = std::move(cubin);
+  J->cuda_counted.clear();
+  J->cubin_counted.clear();
+  J->tape_capacity = cap;
+  return ADC_OK;
+}
+
+// Host buffers stay untouched until the copy-back, so a launch that ran out
+// of tape (the reference's tapes are unbounded vectors) is redone from the
+// caller's data with a larger tape, up to kMaxTape entries per frame tape.
+constexpr int kMaxTape = 4096;
+
 int jit_launch_host(adc_jit_module* J, int64_t grid, int64_t block, int64_t n,
                     const adc_jit_arg* args, int32_t nargs, bool counted, uint64_t* counts,
                     uint32_t* thread_statements) {
@@ -1519,7 +1549,20 @@ int jit_launch_host(adc_jit_module* J, int64_t grid, int64_t block, int64_t n,
       return cuda_fail(e, "jit statement counts");
     }
   }
-  const int rc = jit_launch(J, grid, block, n, dargs.data(), nargs, nullptr, counted, counts, dstm);
+  int rc = jit_launch(J, grid, block, n, dargs.data(), nargs, nullptr, counted, counts, dstm);
+  while (rc == ADC_E_EVAL && J->herr != nullptr && J->herr->code == 5 &&
+         J->tape_capacity < kMaxTape) {  // tape capacity exceeded
+    if (int g = jit_grow_tape(J, std::min(kMaxTape, J->tape_capacity * 4))) {
+      rc = g;
+      break;
+    }
+    for (int32_t i = 0; i < nargs; ++i)  // the caller's data again
+      if (J->kinds[i] == 0 && args[i].len > 0)
+        cudaMemcpy(dargs[i].ptr, args[i].ptr, (size_t)args[i].len * sizeof(double),
+                   cudaMemcpyHostToDevice);
+    clear_error();
+    rc = jit_launch(J, grid, block, n, dargs.data(), nargs, nullptr, counted, counts, dstm);
+  }
   if (dstm != nullptr) {
     if (rc == ADC_OK)
       cudaMemcpy(thread_statements, dstm, total * sizeof(uint32_t), cudaMemcpyDeviceToHost);

@@ -132,6 +132,8 @@ def main():
         ("gauss_div0", "k_gauss", 64, [np.ones(64), np.zeros(64), 0.0, np.zeros(64),
                                        np.zeros(64)], "sequential"),
         ("iovf", "k_iovf", 64, [np.ones(64), 3037000500, np.zeros(64)], "sequential"),
+        # deeper than the JIT's default 256-entry tapes: the host path grows them
+        ("looped_deep", "k_looped", 300, [r.uniform(-2, 3, 300), 300, np.zeros(300)], ""),
     )
     for key, kern, nn, params, mode in cases:
         flat = []

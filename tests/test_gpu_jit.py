@@ -90,6 +90,22 @@ def test_domain_error_is_eval():
     assert "division by zero" in str(G["gauss_div0_error"])
 
 
+def test_tape_deeper_than_default_capacity():
+    """looped_grad with 300 iterations pushes more than the default 256 tape
+    entries per thread.  The reference's tapes are unbounded: the host-buffer
+    path redoes the launch from the caller's data with a larger tape (the same
+    bits as the reference); a device-buffer launch reports the overflow as an
+    Eval error naming the remedy."""
+    outs, st = _run("looped_deep", False, counts=True)
+    assert outs[-1].tobytes() == G["looped_deep_out1"].tobytes()
+    assert tuple(st.counts.values()) == tuple(int(v) for v in G["looped_deep_counts"])
+    with pytest.raises(adc.AdcError) as e:
+        _run("looped_deep", True)
+    assert e.value.kind == "Eval" and "tape capacity" in str(e.value)
+    outs = _run("looped_deep", True, tape_capacity=1024)
+    assert outs[-1].tobytes() == G["looped_deep_out1"].tobytes()
+
+
 def test_integer_overflow_is_eval():
     # int64 arithmetic raises like the interpreter (eval.cpp:601-628)
     with pytest.raises(adc.AdcError) as e:
