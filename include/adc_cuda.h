@@ -363,13 +363,21 @@ typedef struct adc_fit_result {
   int32_t sigma_clamps;
   uint64_t gradient_evals;
   uint64_t chi2_evals;
-  uint64_t gradient_ns; /* host wall clock around gradient passes (fit.cpp:332-336) */
+  uint64_t gradient_ns; /* time in gradient passes (fit.cpp:332-336): host wall clock in
+                           the host loop, the device's %globaltimer in the device loop */
 } adc_fit_result;
 
 void adc_fit_default_options(adc_fit_options* o);
 /* params: in = init (np), out = final.  iterates: trace_iterates * np doubles
  * (or NULL).  Single device, or every rank of a sharded plan with a
- * communicator attached (all ranks take the same steps). */
+ * communicator attached (all ranks take the same steps).  With the fast
+ * passes (precision mode >= 1) on one device or over the peer transport, the
+ * whole loop runs on the device: one CUDA graph whose WHILE node repeats the
+ * iteration (gradient pass, finalize, Newton probes and solve when
+ * use_hessian, batched Armijo trials, selection, bookkeeping); the host only
+ * continues a line search that needs more trials than one batch.  NCCL and
+ * host-callback plans, and mode 0, run the same passes from a host loop.
+ * Both loops give the same bits. */
 int adc_cuda_fit(adc_chi2_plan* plan, double* params, const int32_t* clamp_idx, int32_t nclamp,
                  const adc_fit_options* opts, adc_fit_result* result, double* iterates);
 
