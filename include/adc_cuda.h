@@ -125,6 +125,16 @@ int adc_cuda_gaussnd_grad_host(int64_t n, int64_t dim, int64_t ld, const double*
 int adc_cuda_gaussnd_grad_shared_p(int64_t n, int64_t dim, int64_t ld, const double* x,
                                    const double* p, double sigma, double* dx, double* dp,
                                    int32_t unsafe, void* stream);
+/* The same over the points of several ranks (the shared-p
+ * variant's one all-reduce of dp[dim]): each rank passes its own n points and
+ * the same p; every rank's dp partial (its points in the single-device fixed
+ * order) is all-gathered through `comm` (NCCL, or the host / peer transport's
+ * all-gather callback) and summed in rank order, so every rank ends with the
+ * same dp bits; at world 1 the result is the single-device one bit for bit. */
+typedef struct adc_comm adc_comm;
+int adc_cuda_gaussnd_grad_shared_p_comm(int64_t n, int64_t dim, int64_t ld, const double* x,
+                                        const double* p, double sigma, double* dx, double* dp,
+                                        int32_t unsafe, adc_comm* comm, void* stream);
 /* Kernel selection for experiments: 0 = auto, 1 = point-per-thread
  * (reference summation order), 2 = dims-over-warps tile. */
 int adc_cuda_gaussnd_set_variant(int32_t variant);
@@ -294,8 +304,8 @@ int adc_cuda_chi2_set_precision(adc_chi2_plan* plan, int32_t mode);
  *    gloo, ...): fn(ctx, send, recv, bytes) must place every rank's `bytes`
  *    bytes at recv + rank * bytes and return 0.  Used to run several ranks on
  *    one GPU in tests.
+ * (adc_comm is declared above, with adc_cuda_gaussnd_grad_shared_p_comm.)
  */
-typedef struct adc_comm adc_comm;
 typedef int (*adc_allgather_fn)(void* ctx, const void* send, void* recv, size_t bytes);
 enum { ADC_COMM_NCCL = 1, ADC_COMM_HOST = 2, ADC_COMM_PEER = 3 };
 int adc_nccl_unique_id(unsigned char id[128]);

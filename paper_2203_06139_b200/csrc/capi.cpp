@@ -5,10 +5,14 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
+#include "comm_internal.h"
 #include "common.cuh"
 
 namespace adcb {
+int gaussnd_shared_p_rank_sum_enqueue(const double* parts, int world, int64_t dim, double* dp,
+                                      cudaStream_t s);
 
 int launch_gauss_grad(int64_t n, const double* x, const double* p, double sigma, double* dx,
                       double* dp, cudaStream_t stream);
@@ -390,6 +394,58 @@ extern "C" int adc_cuda_gaussnd_grad_shared_p(int64_t n, int64_t dim, int64_t ld
   ADCB_CUDA(cudaMallocAsync(&ws, (size_t)(gaussnd_shared_p_blocks(n) + 1) * dim * sizeof(double), s));
   const int rc = launch_gaussnd_shared_p(n, dim, ld, x, p, sigma, dx, dp, ws, s);
   cudaFreeAsync(ws, s);
+  return rc;
+}
+
+extern "C" int adc_cuda_gaussnd_grad_shared_p_comm(int64_t n, int64_t dim, int64_t ld,
+                                                   const double* x, const double* p,
+                                                   double sigma, double* dx, double* dp,
+                                                   int32_t unsafe, adc_comm* comm, void* stream) {
+  clear_error();
+  if (comm == nullptr) return fail(ADC_E_ARG, "null communicator");
+  if (!unsafe)
+    return fail(ADC_E_LAUNCH,
+                "launch refused, hazardous parameter(s): dp (whole array shared with a writing "
+                "callee across threads); pass the unsafe flag to force");
+  if (n < 0 || dim < 0) return fail(ADC_E_LAUNCH, "gaussnd: negative size");
+  if (ld < n) return fail(ADC_E_LAUNCH, "gaussnd: leading dimension smaller than n");
+  if (n > 0 && dim > 0 && (!x || !p || !dp)) return fail(ADC_E_LAUNCH, "missing buffer");
+  if (dim > 0 && dp == nullptr) return fail(ADC_E_LAUNCH, "missing buffer");
+  if (int rc = require_device()) return rc;
+  if (dim == 0) return ADC_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int W = comm->world;
+  // this rank's partial (every rank takes part in the exchange, n = 0 too)
+  double *part = nullptr, *ws = nullptr, *parts = nullptr;
+  ADCB_CUDA(cudaMallocAsync(&part, (size_t)dim * sizeof(double), s));
+  ADCB_CUDA(cudaMallocAsync(&parts, (size_t)W * dim * sizeof(double), s));
+  ADCB_CUDA(cudaMemsetAsync(part, 0, (size_t)dim * sizeof(double), s));
+  int rc = ADC_OK;
+  if (n > 0) {
+    ADCB_CUDA(cudaMallocAsync(&ws, (size_t)(gaussnd_shared_p_blocks(n) + 1) * dim * sizeof(double), s));
+    rc = launch_gaussnd_shared_p(n, dim, ld, x, p, sigma, dx, part, ws, s);
+  }
+  if (rc == ADC_OK) {
+    if (comm->kind == ADC_COMM_NCCL) {
+      rc = comm_allgather_enqueue(comm, part, parts, (size_t)dim, s);
+    } else {  // host all-gather (the peer transport's bootstrap callback too)
+      std::vector<double> hs((size_t)dim), hr((size_t)W * dim);
+      cudaError_t e = cudaMemcpyAsync(hs.data(), part, hs.size() * sizeof(double),
+                                      cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) rc = cuda_fail(e, "shared-p partial");
+      if (rc == ADC_OK) rc = comm_allgather_host(comm, hs.data(), hr.data(), (size_t)dim);
+      if (rc == ADC_OK) {
+        e = cudaMemcpyAsync(parts, hr.data(), hr.size() * sizeof(double), cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // hr is a stack buffer
+        if (e != cudaSuccess) rc = cuda_fail(e, "shared-p partials");
+      }
+    }
+  }
+  if (rc == ADC_OK) rc = gaussnd_shared_p_rank_sum_enqueue(parts, W, dim, dp, s);
+  if (ws) cudaFreeAsync(ws, s);
+  cudaFreeAsync(part, s);
+  cudaFreeAsync(parts, s);
   return rc;
 }
 

@@ -983,6 +983,27 @@ static int make_rows_tmap(CUtensorMap* m, const double* x, int64_t npts, int64_t
   return r == CUDA_SUCCESS ? ADC_OK : ADC_E_CUDA;
 }
 
+// Multi-rank shared mean vector: every rank's dp partial [world][dim] (an
+// all-gather) is summed in rank order, dp[d] += (0 + part_0) + part_1 + ...,
+// the same bits on every rank.
+__global__ void gaussnd_shared_p_rank_sum(const double* __restrict__ parts, int world, int dim,
+                                          double* __restrict__ dp) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= dim) return;
+  double acc = 0.0;
+  for (int r = 0; r < world; ++r) acc = fadd(acc, parts[(size_t)r * dim + d]);
+  dp[d] = fadd(dp[d], acc);
+}
+
+int gaussnd_shared_p_rank_sum_enqueue(const double* parts, int world, int64_t dim, double* dp,
+                                      cudaStream_t s) {
+  if (dim == 0) return ADC_OK;
+  gaussnd_shared_p_rank_sum<<<(unsigned)((dim + 127) / 128), 128, 0, s>>>(parts, world, (int)dim,
+                                                                         dp);
+  ADCB_CUDA(cudaGetLastError());
+  return ADC_OK;
+}
+
 int64_t gaussnd_shared_p_blocks(int64_t n) {
   return std::max<int64_t>(1, std::min<int64_t>((n + 31) / 32, kSharedPMaxBlocks));
 }

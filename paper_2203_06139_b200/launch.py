@@ -239,12 +239,14 @@ def launch_batch(grad_fn: str, x, p, sigma: float, dx, dp, ld: int | None = None
 
 def launch_batch_shared_p(grad_fn: str, x, p, sigma: float, dx, dp,
                           opts: LaunchOptions | None = None, ld: int | None = None,
-                          callee_fingerprint: int | None = None):
+                          callee_fingerprint: int | None = None, comm=None):
     """The shared-mean batched path: for every point i,
     gaussnd_grad_0_1(x[:, i], p, sigma, dim, dx[:, i], dp) with ONE p (dim,)
     and ONE shared slot dp (dim,) — refused as a shared-write hazard unless
     opts.unsafe; forced, dp is reduced in a fixed order (deterministic).  dx
-    may be None.  Device (CUDA tensor) buffers."""
+    may be None.  Device (CUDA tensor) buffers.  With `comm` (a Comm), x / dx
+    hold this rank's points and every rank's dp partial is all-gathered and
+    summed in rank order: the same dp on every rank."""
     opts = opts or LaunchOptions()
     if grad_fn != "gaussnd_grad_0_1":
         raise AdcError("Launch", f"no B200 kernel registered for '{grad_fn}'")
@@ -254,6 +256,11 @@ def launch_batch_shared_p(grad_fn: str, x, p, sigma: float, dx, dp,
     if not _is_torch(x):
         raise AdcError("Launch", "launch_batch_shared_p takes device (CUDA tensor) buffers")
     ld = _soa_ld((x, dx), ld)
+    if comm is not None:
+        check(lib.adc_cuda_gaussnd_grad_shared_p_comm(
+            n, dim, ld, dptr(x), dptr(p), float(sigma), dptr(dx) if dx is not None else None,
+            dptr(dp), 1 if opts.unsafe else 0, comm._p, _stream_of(x)))
+        return
     check(lib.adc_cuda_gaussnd_grad_shared_p(n, dim, ld, dptr(x), dptr(p), float(sigma),
                                              dptr(dx) if dx is not None else None, dptr(dp),
                                              1 if opts.unsafe else 0, _stream_of(x)))

@@ -172,3 +172,88 @@ def test_ranks_share_gpu_bitwise(world, transport):
         assert err is None, (rank, err)
         for k in ref:
             assert got[k] == ref[k], (rank, k)
+
+
+# ---- shared mean vector over ranks (dp all-reduce) ---------------
+def _sp_problem(dim=100, n=50_003, seed=3):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    p = rng.uniform(-1, 1, dim)
+    x = p[:, None] + 0.1 * rng.standard_normal((dim, n))
+    dp0 = rng.standard_normal(dim)
+    return x, p, dp0
+
+
+def _sp_run(x, p, dp0, comm=None):
+    X = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    P = torch.from_numpy(p).cuda()
+    DX = torch.zeros_like(X)
+    DP = torch.from_numpy(dp0.copy()).cuda()
+    adc.launch_batch_shared_p("gaussnd_grad_0_1", X, P, 1.3, DX, DP,
+                              adc.LaunchOptions(unsafe=True), comm=comm)
+    torch.cuda.synchronize()
+    return DX.cpu().numpy(), DP.cpu().numpy()
+
+
+def test_shared_p_comm_world1_bitwise_equals_single_device():
+    x, p, dp0 = _sp_problem()
+    dx1, dp1 = _sp_run(x, p, dp0)
+    for comm in (adc.Comm.nccl(1, 0, adc.Comm.unique_id()), adc.Comm.host(1, 0, lambda a: a.copy()),
+                 adc.Comm.peer(1, 0, lambda a: a.copy())):
+        dx, dp = _sp_run(x, p, dp0, comm)
+        assert dx.tobytes() == dx1.tobytes() and dp.tobytes() == dp1.tobytes()
+        comm.close()
+
+
+def _sp_worker(rank, world, port, out_q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    import paper_2203_06139_b200 as adc_  # noqa: F401
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x, p, dp0 = _sp_problem()
+        n = x.shape[1]
+        lo, hi = n * rank // world, n * (rank + 1) // world
+        comm = adc_.Comm.from_torch("host")
+        runs = [_sp_run(x[:, lo:hi], p, dp0, comm) for _ in range(2)]
+        out_q.put((rank, runs[0][0].tobytes(), runs[0][1].tobytes(), runs[1][1].tobytes(), None))
+    except Exception as e:  # noqa: BLE001
+        out_q.put((rank, None, None, None, repr(e)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shared_p_ranks_share_gpu(restate, world):
+    """Each rank holds a contiguous slice of the points and the same p: its dx
+    rows are the single-device ones bit for bit, and every rank ends with the
+    same dp — within 1e-12 * sum|terms| of the compensated total, repeatable."""
+    import torch.multiprocessing as mp
+    x, p, dp0 = _sp_problem()
+    dx1, _ = _sp_run(x, p, dp0)
+    tot, ab = restate.gaussnd_shared_p_dp_compensated(np.ascontiguousarray(x), p, 1.3)
+    ctx = mp.get_context("spawn")
+    out_q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sp_worker, args=(r, world, port, out_q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted([out_q.get(timeout=600) for _ in procs])
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    n = x.shape[1]
+    dps = set()
+    for rank, dxb, dpb, dpb2, err in res:
+        assert err is None, (rank, err)
+        lo, hi = n * rank // world, n * (rank + 1) // world
+        dx = np.frombuffer(dxb).reshape(x.shape[0], hi - lo)
+        assert dx.tobytes() == np.ascontiguousarray(dx1[:, lo:hi]).tobytes()
+        assert dpb == dpb2
+        dps.add(dpb)
+    assert len(dps) == 1
+    dp = np.frombuffer(dps.pop())
+    assert np.all(np.abs(dp - (dp0 + tot)) <= 1e-12 * (ab + np.abs(dp0)))
