@@ -104,6 +104,14 @@ int adc_cuda_compute_gauss_shared(int64_t grid_dim, int64_t block_dim, int64_t n
 int adc_cuda_compute_gauss_shared_host(int64_t grid_dim, int64_t block_dim, int64_t n,
                                        const double* x, const double* p, double sigma, double* dx,
                                        double* dp, double* dsigma, int32_t unsafe);
+/* Over ranks: each rank launches over its own n points; every rank's dsigma
+ * partial is all-gathered through `comm` and added in rank order (the same
+ * dsigma bits on every rank; world 1 = the single-device result). */
+typedef struct adc_comm adc_comm;
+int adc_cuda_compute_gauss_shared_comm(int64_t grid_dim, int64_t block_dim, int64_t n,
+                                       const double* x, const double* p, double sigma, double* dx,
+                                       double* dp, double* dsigma, int32_t unsafe, adc_comm* comm,
+                                       void* stream);
 
 /* ---------------------------------------------------------------------------
  * Batched N-dim Gaussian gradient gaussnd_grad_0_1(x, p, sigma, dim, dx, dp)
@@ -131,7 +139,6 @@ int adc_cuda_gaussnd_grad_shared_p(int64_t n, int64_t dim, int64_t ld, const dou
  * order) is all-gathered through `comm` (NCCL, or the host / peer transport's
  * all-gather callback) and summed in rank order, so every rank ends with the
  * same dp bits; at world 1 the result is the single-device one bit for bit. */
-typedef struct adc_comm adc_comm;
 int adc_cuda_gaussnd_grad_shared_p_comm(int64_t n, int64_t dim, int64_t ld, const double* x,
                                         const double* p, double sigma, double* dx, double* dp,
                                         int32_t unsafe, adc_comm* comm, void* stream);

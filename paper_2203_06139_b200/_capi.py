@@ -86,6 +86,8 @@ SIGNATURES = {
                                                       _I32, _VP]),
     "adc_cuda_gaussnd_grad_shared_p_comm": (ctypes.c_int, [_I64, _I64, _I64, _VP, _VP, _DBL, _VP,
                                                            _VP, _I32, _VP, _VP]),
+    "adc_cuda_compute_gauss_shared_comm": (ctypes.c_int, [_I64, _I64, _I64, _VP, _VP, _DBL, _VP,
+                                                          _VP, _VP, _I32, _VP, _VP]),
     "adc_chi2_make_layout": (ctypes.c_int, [_I64, _I32, _I32, ctypes.POINTER(Chi2Layout)]),
     "adc_chi2_record_len": (_I32, [_I32, _I32]),
     "adc_chi2_finalize": (ctypes.c_int, [_I32, _DBL, _D, _I64, _I32, _D, _D]),

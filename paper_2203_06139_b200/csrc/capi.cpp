@@ -397,6 +397,38 @@ extern "C" int adc_cuda_gaussnd_grad_shared_p(int64_t n, int64_t dim, int64_t ld
   return rc;
 }
 
+namespace adcb {
+// dst[count] += sum over ranks of every rank's part[count] (device), in rank
+// order: the all-gather through the communicator (NCCL, or the host / peer
+// transport's callback), then one fixed-order add — the same bits on every rank.
+int rank_sum_into(adc_comm* comm, const double* part, int64_t count, double* dst,
+                  cudaStream_t s) {
+  if (count == 0) return ADC_OK;
+  const int W = comm->world;
+  double* parts = nullptr;
+  ADCB_CUDA(cudaMallocAsync(&parts, (size_t)W * count * sizeof(double), s));
+  int rc = ADC_OK;
+  if (comm->kind == ADC_COMM_NCCL) {
+    rc = comm_allgather_enqueue(comm, part, parts, (size_t)count, s);
+  } else {
+    std::vector<double> hs((size_t)count), hr((size_t)W * count);
+    cudaError_t e = cudaMemcpyAsync(hs.data(), part, hs.size() * sizeof(double),
+                                    cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = cuda_fail(e, "rank partial");
+    if (rc == ADC_OK) rc = comm_allgather_host(comm, hs.data(), hr.data(), (size_t)count);
+    if (rc == ADC_OK) {
+      e = cudaMemcpyAsync(parts, hr.data(), hr.size() * sizeof(double), cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // hr lives on this stack
+      if (e != cudaSuccess) rc = cuda_fail(e, "rank partials");
+    }
+  }
+  if (rc == ADC_OK) rc = gaussnd_shared_p_rank_sum_enqueue(parts, W, count, dst, s);
+  cudaFreeAsync(parts, s);
+  return rc;
+}
+}  // namespace adcb
+
 extern "C" int adc_cuda_gaussnd_grad_shared_p_comm(int64_t n, int64_t dim, int64_t ld,
                                                    const double* x, const double* p,
                                                    double sigma, double* dx, double* dp,
@@ -409,43 +441,45 @@ extern "C" int adc_cuda_gaussnd_grad_shared_p_comm(int64_t n, int64_t dim, int64
                 "callee across threads); pass the unsafe flag to force");
   if (n < 0 || dim < 0) return fail(ADC_E_LAUNCH, "gaussnd: negative size");
   if (ld < n) return fail(ADC_E_LAUNCH, "gaussnd: leading dimension smaller than n");
-  if (n > 0 && dim > 0 && (!x || !p || !dp)) return fail(ADC_E_LAUNCH, "missing buffer");
-  if (dim > 0 && dp == nullptr) return fail(ADC_E_LAUNCH, "missing buffer");
+  if ((n > 0 && dim > 0 && (!x || !p)) || (dim > 0 && dp == nullptr))
+    return fail(ADC_E_LAUNCH, "missing buffer");
   if (int rc = require_device()) return rc;
   if (dim == 0) return ADC_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int W = comm->world;
   // this rank's partial (every rank takes part in the exchange, n = 0 too)
-  double *part = nullptr, *ws = nullptr, *parts = nullptr;
+  double *part = nullptr, *ws = nullptr;
   ADCB_CUDA(cudaMallocAsync(&part, (size_t)dim * sizeof(double), s));
-  ADCB_CUDA(cudaMallocAsync(&parts, (size_t)W * dim * sizeof(double), s));
   ADCB_CUDA(cudaMemsetAsync(part, 0, (size_t)dim * sizeof(double), s));
   int rc = ADC_OK;
   if (n > 0) {
     ADCB_CUDA(cudaMallocAsync(&ws, (size_t)(gaussnd_shared_p_blocks(n) + 1) * dim * sizeof(double), s));
     rc = launch_gaussnd_shared_p(n, dim, ld, x, p, sigma, dx, part, ws, s);
   }
-  if (rc == ADC_OK) {
-    if (comm->kind == ADC_COMM_NCCL) {
-      rc = comm_allgather_enqueue(comm, part, parts, (size_t)dim, s);
-    } else {  // host all-gather (the peer transport's bootstrap callback too)
-      std::vector<double> hs((size_t)dim), hr((size_t)W * dim);
-      cudaError_t e = cudaMemcpyAsync(hs.data(), part, hs.size() * sizeof(double),
-                                      cudaMemcpyDeviceToHost, s);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-      if (e != cudaSuccess) rc = cuda_fail(e, "shared-p partial");
-      if (rc == ADC_OK) rc = comm_allgather_host(comm, hs.data(), hr.data(), (size_t)dim);
-      if (rc == ADC_OK) {
-        e = cudaMemcpyAsync(parts, hr.data(), hr.size() * sizeof(double), cudaMemcpyHostToDevice, s);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // hr is a stack buffer
-        if (e != cudaSuccess) rc = cuda_fail(e, "shared-p partials");
-      }
-    }
-  }
-  if (rc == ADC_OK) rc = gaussnd_shared_p_rank_sum_enqueue(parts, W, dim, dp, s);
+  if (rc == ADC_OK) rc = rank_sum_into(comm, part, dim, dp, s);
   if (ws) cudaFreeAsync(ws, s);
   cudaFreeAsync(part, s);
-  cudaFreeAsync(parts, s);
+  return rc;
+}
+
+extern "C" int adc_cuda_compute_gauss_shared_comm(int64_t grid, int64_t block, int64_t n,
+                                                  const double* x, const double* p, double sigma,
+                                                  double* dx, double* dp, double* dsigma,
+                                                  int32_t unsafe, adc_comm* comm, void* stream) {
+  clear_error();
+  if (comm == nullptr) return fail(ADC_E_ARG, "null communicator");
+  if (int rc = validate_config(grid, block, n)) return rc;
+  if (int rc = refuse_shared(unsafe)) return rc;
+  if (!x || !p || !dx || !dp || !dsigma) return fail(ADC_E_LAUNCH, "missing buffer");
+  if (int rc = require_device()) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double *part = nullptr, *ws = nullptr;
+  ADCB_CUDA(cudaMallocAsync(&part, sizeof(double), s));
+  ADCB_CUDA(cudaMemsetAsync(part, 0, sizeof(double), s));
+  ADCB_CUDA(cudaMallocAsync(&ws, (size_t)gauss_shared_blocks(n) * sizeof(double), s));
+  int rc = launch_gauss_shared(n, x, p, sigma, dx, dp, part, ws, s);
+  if (rc == ADC_OK) rc = rank_sum_into(comm, part, 1, dsigma, s);
+  cudaFreeAsync(ws, s);
+  cudaFreeAsync(part, s);
   return rc;
 }
 

@@ -124,13 +124,15 @@ def _stream_of(a):
 
 def launch(kernel: str, cfg: LaunchConfig, buffers: BufferSet,
            opts: LaunchOptions | None = None, callee_fingerprint: int | None = None,
-           module: str | None = None, counts: bool = False) -> LaunchStats:
+           module: str | None = None, counts: bool = False, comm=None) -> LaunchStats:
     """adc::launch (launch.cpp:252-346) for the Listing-1 kernels of kernels.dsl:
     `compute` (private slots) and `compute_shared` (the shared dsigma slot:
     refused unless opts.unsafe, then reduced in a fixed order, deterministic),
     on their hand-written kernels.  With `module` (the Program's text as
     adc::print emits it), any other global kernel goes through the generic
-    JIT (jit.py)."""
+    JIT (jit.py).  `compute_shared` with `comm` (device buffers): each rank
+    launches over its own points and the dsigma partials are summed over
+    ranks in rank order (the same dsigma on every rank)."""
     opts = opts or LaunchOptions()
     if module is not None and kernel not in ("compute", "compute_shared"):
         from .jit import launch_module
@@ -176,7 +178,13 @@ def launch(kernel: str, cfg: LaunchConfig, buffers: BufferSet,
         ds = buffers.arrays["dsigma"]
         if (ds.numel() if _is_torch(ds) else ds.size) < 1:
             raise AdcError("Launch", "buffer 'dsigma' is empty")
-        if _is_torch(x):
+        if comm is not None:
+            if not _is_torch(x):
+                raise AdcError("Launch", "compute_shared over ranks takes device buffers")
+            check(lib.adc_cuda_compute_gauss_shared_comm(
+                cfg.grid_dim, cfg.block_dim, cfg.n, dptr(x), dptr(p), sigma, dptr(dx), dptr(dp),
+                dptr(ds), 1, comm._p, _stream_of(x)))
+        elif _is_torch(x):
             check(lib.adc_cuda_compute_gauss_shared(cfg.grid_dim, cfg.block_dim, cfg.n, dptr(x),
                                                     dptr(p), sigma, dptr(dx), dptr(dp), dptr(ds),
                                                     1, _stream_of(x)))

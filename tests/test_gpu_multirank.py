@@ -257,3 +257,84 @@ def test_shared_p_ranks_share_gpu(restate, world):
     assert len(dps) == 1
     dp = np.frombuffer(dps.pop())
     assert np.all(np.abs(dp - (dp0 + tot)) <= 1e-12 * (ab + np.abs(dp0)))
+
+
+# ---- the forced compute_shared launch over ranks (the dsigma slot) ---------------
+def _cs_problem(n=200_003, seed=9):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return rng.uniform(-3, 3, n), rng.uniform(-2, 2, n)
+
+
+def _cs_run(x, p, comm=None):
+    n = x.size
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    X, P = t(x), t(p)
+    DX, DP = torch.zeros_like(X), torch.zeros_like(X)
+    DS = torch.full((1,), 0.25, dtype=torch.float64, device="cuda")
+    adc.launch("compute_shared", adc.LaunchConfig(n // 256 + 1, 256, n),
+               adc.BufferSet(arrays={"x": X, "p": P, "dx": DX, "dp": DP, "dsigma": DS},
+                             scalars={"sigma": 1.3}),
+               adc.LaunchOptions(unsafe=True), comm=comm)
+    torch.cuda.synchronize()
+    return DX.cpu().numpy(), DS.cpu().numpy()
+
+
+def test_compute_shared_comm_world1_bitwise_equals_single_device():
+    x, p = _cs_problem()
+    dx1, ds1 = _cs_run(x, p)
+    for comm in (adc.Comm.nccl(1, 0, adc.Comm.unique_id()), adc.Comm.host(1, 0, lambda a: a.copy())):
+        dx, ds = _cs_run(x, p, comm)
+        assert dx.tobytes() == dx1.tobytes() and ds.tobytes() == ds1.tobytes()
+        comm.close()
+
+
+def _cs_worker(rank, world, port, out_q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    import paper_2203_06139_b200 as adc_
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x, p = _cs_problem()
+        n = x.size
+        lo, hi = n * rank // world, n * (rank + 1) // world
+        comm = adc_.Comm.from_torch("peer")
+        dx, ds = _cs_run(x[lo:hi], p[lo:hi], comm)
+        out_q.put((rank, dx.tobytes(), ds.tobytes(), None))
+    except Exception as e:  # noqa: BLE001
+        out_q.put((rank, None, None, repr(e)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_compute_shared_ranks_share_gpu(restate):
+    """Two ranks (peer transport's callback), each with half the points: the
+    same dsigma on both, within 1e-12 * sum|terms| of the compensated total;
+    dx per point bit-identical to one device."""
+    import torch.multiprocessing as mp
+    x, p = _cs_problem()
+    dx1, _ = _cs_run(x, p)
+    tot, ab = restate.gauss_shared_dsigma_compensated(x, p, 1.3)
+    ctx = mp.get_context("spawn")
+    out_q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cs_worker, args=(r, 2, port, out_q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted([out_q.get(timeout=600) for _ in procs])
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    n = x.size
+    dss = set()
+    for rank, dxb, dsb, err in res:
+        assert err is None, (rank, err)
+        lo, hi = n * rank // 2, n * (rank + 1) // 2
+        assert np.frombuffer(dxb).tobytes() == dx1[lo:hi].tobytes()
+        dss.add(dsb)
+    assert len(dss) == 1
+    ds = np.frombuffer(dss.pop())[0]
+    assert abs(ds - (0.25 + tot)) <= 1e-12 * (ab + 0.25)
