@@ -981,9 +981,9 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
   if (opts->trace_iterates > 0) trace(q);
   std::vector<double> g(np), trial(np);
   int first_batch = 32;  // line-search batch size, adapted per iteration
-  // next batch = the last search's trial count + margin, in groups of 8 (the
+  // next batch = the last search's trial count + margin, in groups of 4 (the
   // multi pass's candidate group); ADC_FIT_MARGIN is an experiment knob
-  const int margin = getenv("ADC_FIT_MARGIN") ? atoi(getenv("ADC_FIT_MARGIN")) : 8;
+  const int margin = getenv("ADC_FIT_MARGIN") ? atoi(getenv("ADC_FIT_MARGIN")) : 4;
   // Device-resident loop (fit_device.cu): the fast passes on one device,
   // either gradient provider, steepest descent or the Newton option.
   // ADC_FIT_DEVICE=0 keeps the host-driven loop (both give the same bits).
@@ -1088,7 +1088,7 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
       cur = next;
       for (int i = 0; i < np; ++i) st.q[i] = q[i];
       st.cur = next;
-      st.first_batch = std::min(kMultiMax, std::max(8, (tried + margin + 7) / 8 * 8));
+      st.first_batch = std::min(kMultiMax, std::max(8, (tried + margin + 3) / 4 * 4));
       st.iters += 1;
       if (c.trace != nullptr && c.trace_cap > st.iters)
         ADCB_CUDA(cudaMemcpy(c.trace + (size_t)st.iters * np, q.data(), np * sizeof(double),
@@ -1210,7 +1210,7 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
         t = tvals.back() * 0.5;
         want = kMultiMax;
       }
-      if (accepted) first_batch = std::min(kMultiMax, std::max(8, (tried + margin + 7) / 8 * 8));
+      if (accepted) first_batch = std::min(kMultiMax, std::max(8, (tried + margin + 3) / 4 * 4));
     } else {
       while (t >= 1e-18) {
         trial = q;

@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(kMultiMax) fit_accept_kernel(FitDevState* st,
       st->cur = next;
       st->rel_dec = rel_dec;
       const int tried = j + 1;
-      st->first_batch = min(kMultiMax, max(8, (tried + c.margin + 7) / 8 * 8));
+      st->first_batch = min(kMultiMax, max(8, (tried + c.margin + 3) / 4 * 4));
       st->status = rel_dec <= c.chi2_rel_tol ? kFitConvergedRelDec : kFitRunning;
       return;
     }
