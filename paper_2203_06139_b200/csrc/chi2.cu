@@ -567,7 +567,7 @@ __host__ __device__ constexpr int multi_ilp() {
   return M::NP <= 6 ? 4 : M::NP <= 12 ? 2 : 1;
 }
 
-template <class M, bool REC = false>
+template <class M, bool REC = false, bool BULK = false>
 __global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P, int ncand) {
   constexpr int G = kMultiGroup, CG = multi_ilp<M>();
   if (P.ncand_dev != nullptr) ncand = *P.ncand_dev;  // set on the device (fit graph)
@@ -612,6 +612,15 @@ __global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P,
       }
     }
   }
+  __shared__ __align__(128) double sst[BULK ? kBulkStages * kBulkBlock : 1];
+  __shared__ __align__(8) uint64_t sbar[BULK ? kBulkStages : 1];
+  [[maybe_unused]] uint32_t phase = 0;
+  if constexpr (BULK) {
+    if (threadIdx.x == 0) {
+      for (int bb = 0; bb < kBulkStages; ++bb) mbar_init(&sbar[bb], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int R = 1 + 3 * ncand;
@@ -649,33 +658,62 @@ __global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P,
               rA[cc * M::NG + c] = exp(-fmul(z0, rdl[(c0 + cc) * M::NG + c]));
             }
         }
-        for (int k = 0; k < BPT; ++k) {
-          const int64_t j = base + (int64_t)k * kTileThreads;
-          if (j < P.bin_end) {
-            const double ic = ld_stream(P.icounts + j);
-            const double x = fadd(P.lo, fmul(jh, P.width));
-            const double w = ic > 0.0 ? 1.0 : 0.0;
+        auto bin = [&](int k, double ic) {
+          const double x = fadd(P.lo, fmul(jh, P.width));
+          const double w = ic > 0.0 ? 1.0 : 0.0;
 #pragma unroll
-            for (int cc = 0; cc < CG; ++cc) {
-              double m, bg[1];
-              if (REC && ruse[c0 + cc]) {
-                double e[M::NG];
+          for (int cc = 0; cc < CG; ++cc) {
+            double m, bg[1];
+            if (REC && ruse[c0 + cc]) {
+              double e[M::NG];
 #pragma unroll
-                for (int c = 0; c < M::NG; ++c) {
-                  e[c] = fmul(rP[cc * M::NG + c], rtab[((c0 + cc) * M::NG + c) * kRecMaxBpt + k]);
-                  rP[cc * M::NG + c] = fmul(rP[cc * M::NG + c], rA[cc * M::NG + c]);
-                }
-                M::template eval<false, true>(x, QR[cc], tab, m, bg, e);
-              } else {
-                M::template eval<false, true>(x, QR[cc], tab, m, bg);
+              for (int c = 0; c < M::NG; ++c) {
+                e[c] = fmul(rP[cc * M::NG + c], rtab[((c0 + cc) * M::NG + c) * kRecMaxBpt + k]);
+                rP[cc * M::NG + c] = fmul(rP[cc * M::NG + c], rA[cc * M::NG + c]);
               }
-              const double mc = m * ic;
-              a0[cc] += m;
-              a1[cc] = __fma_rn(w, m, a1[cc]);
-              a2[cc] = __fma_rn(m, mc, a2[cc]);
+              M::template eval<false, true>(x, QR[cc], tab, m, bg, e);
+            } else {
+              M::template eval<false, true>(x, QR[cc], tab, m, bg);
+            }
+            const double mc = m * ic;
+            a0[cc] += m;
+            a1[cc] = __fma_rn(w, m, a1[cc]);
+            a2[cc] = __fma_rn(m, mc, a2[cc]);
+          }
+        };
+        if (BULK && (tile + 1) * TB <= P.bin_end) {
+          // a full tile: 1/c in 8 KB blocks through shared memory (cp.async.bulk)
+          const int nblk = BPT / kPD;
+          const int64_t tb = tile * TB;
+          if (threadIdx.x == 0)
+            for (int bb = 0; bb < kBulkStages && bb < nblk; ++bb) {
+              mbar_arrive_expect_tx(&sbar[bb], kBulkBlock * sizeof(double));
+              bulk_g2s(sst + bb * kBulkBlock, P.icounts + tb + (int64_t)bb * kBulkBlock,
+                       kBulkBlock * sizeof(double), &sbar[bb]);
+            }
+          for (int bb = 0; bb < nblk; ++bb) {
+            const int st = bb % kBulkStages;
+            mbar_wait(&sbar[st], (phase >> st) & 1u);
+            phase ^= 1u << st;
+#pragma unroll
+            for (int kk = 0; kk < kPD; ++kk) {
+              bin(bb * kPD + kk, sst[st * kBulkBlock + kk * kTileThreads + threadIdx.x]);
+              jh = fadd(jh, (double)kTileThreads);
+            }
+            __syncthreads();  // every thread is done with this stage
+            if (threadIdx.x == 0 && bb + kBulkStages < nblk) {
+              mbar_arrive_expect_tx(&sbar[st], kBulkBlock * sizeof(double));
+              bulk_g2s(sst + st * kBulkBlock,
+                       P.icounts + tb + (int64_t)(bb + kBulkStages) * kBulkBlock,
+                       kBulkBlock * sizeof(double), &sbar[st]);
             }
           }
-          jh = fadd(jh, (double)kTileThreads);
+        } else {
+          for (int k = 0; k < BPT; ++k) {
+            const int64_t j = base + (int64_t)k * kTileThreads;
+            if (j < P.bin_end) bin(k, ld_stream(P.icounts + j));
+            jh = fadd(jh, (double)kTileThreads);
+          }
         }
         // this group's fixed shuffle trees
 #pragma unroll
@@ -1002,7 +1040,12 @@ int chi2_multi_enqueue(const Chi2Pass& P, int model, int np, int ncand,
     using M = decltype(model_tag);
     if constexpr (M::NG <= 2) {
       if (prec == 2) {
-        chi2_multi_kernel<M, true><<<grid, kTileThreads, 0, s>>>(P, ncand);
+        // bulk-staged 1/c for one-factor models (the two-factor tables leave
+        // no room for the stages in 48 KB); tune 6 = the direct-load form
+        if (M::NG == 1 && g_chi2_tune != 6)
+          chi2_multi_kernel<M, true, M::NG == 1><<<grid, kTileThreads, 0, s>>>(P, ncand);
+        else
+          chi2_multi_kernel<M, true><<<grid, kTileThreads, 0, s>>>(P, ncand);
         return;
       }
     }

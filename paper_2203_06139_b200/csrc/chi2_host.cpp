@@ -444,6 +444,7 @@ extern "C" int adc_cuda_chi2_plan_create(adc_chi2_plan** out, int32_t model, int
                                        sizeof(double))) != cudaSuccess)
     return cleanup(cuda_fail(e, "chi2 plan allocation"));
   if (int rc = alloc_staging(P)) return cleanup(rc);
+  if (const char* t = getenv("ADC_CHI2_TUNE")) chi2_set_tune(atoi(t));  // experiment knob
   *out = P;
   return ADC_OK;
 }
