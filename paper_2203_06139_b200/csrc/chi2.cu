@@ -398,6 +398,7 @@ __device__ __forceinline__ void tile_bins_bulk(const Chi2Pass& P, const typename
   for (int b = 0; b < nblk; ++b) {
     const int st = b % kBulkStages;
     mbar_wait(&sbar[st], (phase >> st) & 1u);
+    __syncwarp();  // the spin loop may leave the warp diverged
     phase ^= 1u << st;
     const double* blk = sst + st * kBulkBlock + threadIdx.x;
 #pragma unroll
@@ -419,6 +420,7 @@ __device__ __forceinline__ void tile_bins_bulk(const Chi2Pass& P, const typename
       bin_accumulate<M, GRAD, true>(t, acc);
       jh = fadd(jh, (double)kTileThreads);
     }
+    __syncwarp();
     __syncthreads();  // every thread is done with this stage
     if (threadIdx.x == 0 && b + kBulkStages < nblk) {
       mbar_arrive_expect_tx(&sbar[st], kBulkBlock * sizeof(double));
@@ -462,6 +464,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) chi2_tile_kernel(Chi2Pass 
     Q.inv[threadIdx.x] = P.qdev[kMaxNp + threadIdx.x];
   }
   if (threadIdx.x < 64) tab[threadIdx.x] = exp2((double)threadIdx.x / 64.0);
+  __syncwarp();  // reconverge (exp2's branches) before the CTA barrier (bar.sync is .aligned)
   __syncthreads();
   const typename M::Reg QR = M::load(Q);
   [[maybe_unused]] bool use_rec = false;
@@ -694,13 +697,15 @@ __global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P,
           for (int bb = 0; bb < nblk; ++bb) {
             const int st = bb % kBulkStages;
             mbar_wait(&sbar[st], (phase >> st) & 1u);
+            __syncwarp();  // the spin loop may leave the warp diverged
             phase ^= 1u << st;
 #pragma unroll
             for (int kk = 0; kk < kPD; ++kk) {
               bin(bb * kPD + kk, sst[st * kBulkBlock + kk * kTileThreads + threadIdx.x]);
               jh = fadd(jh, (double)kTileThreads);
             }
-            __syncthreads();  // every thread is done with this stage
+            __syncwarp();
+    __syncthreads();  // every thread is done with this stage
             if (threadIdx.x == 0 && bb + kBulkStages < nblk) {
               mbar_arrive_expect_tx(&sbar[st], kBulkBlock * sizeof(double));
               bulk_g2s(sst + st * kBulkBlock,
