@@ -400,13 +400,18 @@ extern "C" int adc_cuda_chi2_plan_create(adc_chi2_plan** out, int32_t model, int
     if (np % 3 != 0 || !(k == 1 || k == 2 || k == 3 || k == 4 || k == 8))
       return fail(ADC_E_ARG, "gsum: parameter count must be 3K with K in {1,2,3,4,8}");
   }
-  if (counts == nullptr) return fail(ADC_E_ARG, "plan: null counts");
   if (!(hi > lo)) return fail(ADC_E_EVAL, "degenerate histogram range");
   adc_chi2_plan* P = new (std::nothrow) adc_chi2_plan();
   if (P == nullptr) return fail(ADC_E_CUDA, "out of host memory");
   if (int rc = adc_chi2_make_layout(bins, world, rank, &P->L)) {
     delete P;
     return rc;
+  }
+  // A rank without bins (more ranks than chunks) never reads its counts: an
+  // empty shard may come with a null pointer.
+  if (counts == nullptr && P->L.bin_end > P->L.bin_begin) {
+    delete P;
+    return fail(ADC_E_ARG, "plan: null counts");
   }
   P->model = model;
   P->np = np;
@@ -457,11 +462,12 @@ extern "C" int adc_cuda_chi2_plan_create_sharded(adc_chi2_plan** out, int32_t mo
   if (out == nullptr) return fail(ADC_E_ARG, "plan: null output");
   *out = nullptr;
   if (comm == nullptr) return fail(ADC_E_ARG, "sharded plan: null communicator");
-  if (shard_counts == nullptr) return fail(ADC_E_ARG, "plan: null counts");
   adc_chi2_layout L{};
   if (int rc = adc_chi2_make_layout(bins, comm->world, comm->rank, &L)) return rc;
+  if (shard_counts == nullptr && L.bin_end > L.bin_begin)
+    return fail(ADC_E_ARG, "plan: null counts");
   // The kernels index counts by global bin number; the shard starts at bin_begin.
-  const double* base = shard_counts - L.bin_begin;
+  const double* base = shard_counts == nullptr ? nullptr : shard_counts - L.bin_begin;
   if (int rc = adc_cuda_chi2_plan_create(out, model, np, bins, lo, hi, events, base, comm->world,
                                          comm->rank, stream))
     return rc;

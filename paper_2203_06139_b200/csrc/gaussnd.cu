@@ -29,7 +29,7 @@
 
 namespace adcb {
 
-template <int W, int U, int PF, int PFD = 1>
+template <int W, int U, int PF, int PFD = 1, int CL = 1>
 __global__ void __launch_bounds__(W * 32) gaussnd_tile_kernel(
     const double* __restrict__ x, const double* __restrict__ p, double* __restrict__ dx,
     double* __restrict__ dp, int64_t n, int dim, int64_t ld, double t4, double r1, int dpw,
@@ -40,11 +40,16 @@ __global__ void __launch_bounds__(W * 32) gaussnd_tile_kernel(
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   double* my_stage = stage + (size_t)warp * dstage * 32 + lane;
-  const int d0 = warp * dpw;
+  // CL > 1: the CL CTAs of a cluster (CL SMs) share each tile, CTA r taking
+  // the dims of warps r*W .. r*W+W-1; the warp partials of t are combined
+  // over distributed shared memory in global warp order.
+  const int crank = CL > 1 ? (int)(blockIdx.x % CL) : 0;
+  const int d0 = (crank * W + warp) * dpw;
   const int d1 = min(dim, d0 + dpw);
   const int64_t ntiles = (n + 31) / 32;
+  const int64_t gstride = gridDim.x / CL;  // tiles in flight over the grid
 
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (int64_t tile = blockIdx.x / CL; tile < ntiles; tile += gstride) {
     const int64_t i = tile * 32 + lane;
     const bool valid = i < n;
     const double* xi = x + i;
@@ -104,7 +109,20 @@ __global__ void __launch_bounds__(W * 32) gaussnd_tile_kernel(
         t = fadd(t, fmul(u, u));
       }
     }
-    if (W > 1) {
+    if (CL > 1) {
+      tpart[warp * 32 + lane] = t;
+      cluster_sync();
+      t = 0.0;
+#pragma unroll 1
+      for (int r = 0; r < CL; ++r) {
+        const uint32_t rp = dsmem_map(tpart + lane, r);
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const double v = ld_dsmem(rp + (uint32_t)(w * 32 * sizeof(double)));
+          t = (r == 0 && w == 0) ? v : fadd(t, v);
+        }
+      }
+    } else if (W > 1) {
       tpart[warp * 32 + lane] = t;
       __syncthreads();
       t = tpart[lane];
@@ -161,7 +179,7 @@ __global__ void __launch_bounds__(W * 32) gaussnd_tile_kernel(
           const int l = lane % U;
           const bool second = lane >= U && lane < 2 * U;
           const int dn = d - 1 - U - l;
-          const int64_t tb = tile * 32, tn = tb + (int64_t)gridDim.x * 32;
+          const int64_t tb = tile * 32, tn = tb + gstride * 32;
           if (lane < 2 * U) {
             if (dn >= d0) {
               const unsigned seg = (unsigned)((n - tb < 32 ? n - tb : 32) * sizeof(double));
@@ -174,7 +192,7 @@ __global__ void __launch_bounds__(W * 32) gaussnd_tile_kernel(
         } else if (PF == 1) {
           // next batch of dx, dp rows (descending); in the last batch, the
           // first x, p rows of this warp's next tile
-          const int64_t inext = i + (int64_t)gridDim.x * 32;
+          const int64_t inext = i + gstride * 32;
 #pragma unroll
           for (int k = 0; k < U; ++k) {
             const int dn = d - 1 - U * PFD - k;
@@ -205,7 +223,8 @@ __global__ void __launch_bounds__(W * 32) gaussnd_tile_kernel(
         dpi[o] = fadd(dpi[o], -r6);
       }
     }
-    if (W > 1) __syncthreads();  // tpart is rewritten by the next tile
+    if (CL > 1) cluster_sync();  // peers have read tpart before the next tile rewrites it
+    else if (W > 1) __syncthreads();  // tpart is rewritten by the next tile
   }
 }
 
@@ -428,7 +447,8 @@ __global__ void __launch_bounds__(32) gaussnd_vec2_kernel(
 // 8/16/32 rows in flight per thread (+ L2 prefetch of the next batch);
 // 5 = as 3 without prefetch; 6 = as 3 with bulk (TMA-unit) prefetch;
 // 2 = dims split over the warps of a CTA (7 = same with bulk prefetch);
-// 8 = as 3 prefetching two batches ahead, 9 = U=8 prefetching three ahead.
+// 8 = as 3 prefetching two batches ahead, 9 = U=8 prefetching three ahead;
+// 15 = clusters of 2 CTAs x 16 warps sharing each tile (dims over 32 warps).
 static int g_variant = 0;
 
 struct NdConfig {
@@ -450,6 +470,35 @@ static int launch_tile(const NdConfig& c, int64_t n, int dim, int64_t ld, const 
   int64_t blocks = std::min<int64_t>(ntiles, (int64_t)occ * sm_count());
   k<<<(unsigned)blocks, W * 32, c.smem, s>>>(x, p, dx, dp, n, dim, ld, t4, r1, c.dpw, c.dstage);
   ADCB_CUDA(cudaGetLastError());
+  return ADC_OK;
+}
+
+// Cluster form: CL CTAs of W warps (one CTA per SM) share each 32-point tile,
+// so the whole u row of a tile is staged over CL SMs' shared memory.
+template <int W, int U, int PF, int CL>
+static int launch_tile_cluster(const NdConfig& c, int64_t n, int dim, int64_t ld, const double* x,
+                               const double* p, double* dx, double* dp, double t4, double r1,
+                               cudaStream_t s) {
+  auto k = gaussnd_tile_kernel<W, U, PF, 1, CL>;
+  ADCB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(W * 32);
+  cfg.dynamicSmemBytes = c.smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3((unsigned)(CL * sm_count()));
+  int clusters = 0;
+  ADCB_CUDA(cudaOccupancyMaxActiveClusters(&clusters, k, &cfg));
+  if (clusters < 1) return fail(ADC_E_LAUNCH, "gaussnd: cluster configuration does not fit");
+  const int64_t ntiles = (n + 31) / 32;
+  cfg.gridDim = dim3((unsigned)(CL * std::min<int64_t>(ntiles, clusters)));
+  ADCB_CUDA(cudaLaunchKernelEx(&cfg, k, x, p, dx, dp, n, dim, ld, t4, r1, c.dpw, c.dstage));
   return ADC_OK;
 }
 
@@ -552,6 +601,16 @@ int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, con
       return rc;
     }
   }
+  if (g_variant == 15) {  // cluster of 2 CTAs x 16 warps per tile
+    NdConfig c{};
+    c.w = 16;
+    c.u = 8;
+    c.dpw = (int)((dim + 31) / 32);
+    const size_t avail = kSmemPerSm - (size_t)c.w * 32 * 8 - 1024;
+    c.dstage = std::min<int>(c.dpw, (int)(avail / ((size_t)c.w * 256)));
+    c.smem = ((size_t)c.w * 32 + (size_t)c.w * c.dstage * 32) * sizeof(double);
+    return launch_tile_cluster<16, 8, 2, 2>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+  }
   NdConfig c = choose((int)dim);
   switch (c.w) {
     case 1:
@@ -577,7 +636,7 @@ int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, con
 }
 
 int gaussnd_set_variant(int v) {
-  if (v < 0 || v > 14) return fail(ADC_E_ARG, "gaussnd variant must be 0..14");
+  if (v < 0 || v > 15) return fail(ADC_E_ARG, "gaussnd variant must be 0..15");
   g_variant = v;
   return ADC_OK;
 }

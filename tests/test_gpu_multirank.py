@@ -118,7 +118,7 @@ def test_failing_host_callback_is_reported():
     assert e.value.kind == "Nccl"
 
 
-def _worker(rank, world, port, out_q, transport="host"):
+def _worker(rank, world, port, out_q, transport="host", bins=BINS):
     import sys
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
@@ -128,7 +128,7 @@ def _worker(rank, world, port, out_q, transport="host"):
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        counts, ev, q, qs = _problem()
+        counts, ev, q, qs = _problem(bins)
         comm = adc_.Comm.from_torch(transport)
         h = adc_.Histogram(counts.size, -5.0, 5.0, ev, counts)
         L = adc_.chi2_layout(counts.size, world, rank)
@@ -148,19 +148,22 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,transport", [(2, "host"), (3, "host"), (2, "peer"), (3, "peer")])
-def test_ranks_share_gpu_bitwise(world, transport):
+@pytest.mark.parametrize("world,transport,bins", [(2, "host", BINS), (3, "host", BINS),
+                                                  (2, "peer", BINS), (3, "peer", BINS),
+                                                  (3, "peer", 200_001)])
+def test_ranks_share_gpu_bitwise(world, transport, bins):
     """Several ranks on the one GPU: the host transport (gloo all-gather) and
     the peer transport (CUDA IPC buffers on the device, GPU-side publish and
     flags — the multi-GPU path without NCCL) both give every rank the
-    single-device bits."""
+    single-device bits; 200,001 bins over 3 ranks leaves a rank without
+    chunks (it only takes part in the exchanges)."""
     import torch.multiprocessing as mp
-    counts, ev, q, qs = _problem()
+    counts, ev, q, qs = _problem(bins)
     ref = _single_device(counts, ev, q, qs)
     ctx = mp.get_context("spawn")
     out_q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, out_q, transport))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, out_q, transport, bins))
              for r in range(world)]
     for p in procs:
         p.start()
