@@ -329,7 +329,10 @@ int adc_comm_init_host(adc_comm** comm, int32_t world, int32_t rank, adc_allgath
  * from the GPU (NVLink stores), raises a system-scope flag per peer and
  * waits for every peer's flag — one small kernel after the chunk kernel,
  * captured in the pass's CUDA graph.  All ranks must live on one node (on
- * distinct GPUs, or sharing one). */
+ * distinct GPUs, or sharing one).  The wait for the peers' flags is bounded:
+ * after ADC_PEER_TIMEOUT_S seconds (environment, default 120, 0 = unbounded)
+ * the kernel traps and the call fails with ADC_E_CUDA (the CUDA context of
+ * that process is lost) instead of spinning on the GPU forever. */
 int adc_cuda_comm_init_peer(adc_comm** comm, int32_t world, int32_t rank, adc_allgather_fn fn,
                             void* ctx);
 int adc_comm_destroy(adc_comm* comm);
@@ -339,7 +342,8 @@ int adc_comm_info(const adc_comm* comm, int32_t* world, int32_t* rank, int32_t* 
 int adc_cuda_chi2_plan_set_comm(adc_chi2_plan* plan, adc_comm* comm);
 /* One call for a rank that holds only its own shard: world/rank come from
  * comm, shard_counts is a DEVICE pointer to counts[bin_begin, bin_end) of the
- * layout adc_chi2_make_layout(bins, world, rank) gives, and comm is attached. */
+ * layout adc_chi2_make_layout(bins, world, rank) gives, and comm is attached.
+ * A rank the layout gives no bins (more ranks than chunks) may pass NULL. */
 int adc_cuda_chi2_plan_create_sharded(adc_chi2_plan** plan, int32_t model, int32_t np,
                                       int64_t bins, double lo, double hi, double events,
                                       const double* shard_counts, adc_comm* comm, void* stream);

@@ -185,6 +185,17 @@ __global__ void __launch_bounds__(256) peer_exchange_kernel(const double* __rest
 }
 }  // namespace
 
+// Bound on a rank's wait for its peers inside a pass: ADC_PEER_TIMEOUT_S
+// seconds (default 120; 0 = wait forever), read once per process.
+static unsigned long long peer_timeout_ns() {
+  static const unsigned long long ns = [] {
+    double sec = 120.0;
+    if (const char* e = getenv("ADC_PEER_TIMEOUT_S")) sec = atof(e);
+    return sec > 0 ? (unsigned long long)(sec * 1e9) : 0ull;
+  }();
+  return ns;
+}
+
 PeerPublish peer_publish_args(PeerExchange* X, size_t count) {
   PeerPublish pp;
   pp.peer_gather = X->peer_gather;
@@ -198,6 +209,7 @@ PeerPublish peer_publish_args(PeerExchange* X, size_t count) {
   pp.rank = X->rank;
   pp.xcount = X->xcount;
   pp.count = count;
+  pp.timeout_ns = peer_timeout_ns();
   return pp;
 }
 

@@ -20,6 +20,7 @@ struct PeerPublish {
   double* out = nullptr;               // [world][count] compacted result
   int world = 1, rank = 0;
   size_t xcount = 0, count = 0;
+  unsigned long long timeout_ns = 0;   // bound on the wait for the peers' flags
 };
 
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
@@ -29,6 +30,12 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   unsigned long long v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
+}
+
+__device__ __forceinline__ unsigned long long peer_clock_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
 // Slot of this rank in rank r's buffer for pass q.
@@ -42,9 +49,15 @@ __device__ __forceinline__ double* peer_slot(const PeerPublish& pp, int r, unsig
 __device__ __forceinline__ void peer_signal_wait_compact(const PeerPublish& pp,
                                                          unsigned long long q) {
   if ((int)threadIdx.x < pp.world) st_release_sys(pp.peer_flags[threadIdx.x] + pp.rank, q);
-  if ((int)threadIdx.x < pp.world)
+  // A peer that never arrives (its process died, or it failed before the
+  // pass) must not hang the GPU: past the bound the kernel traps, and the
+  // launch fails with a CUDA error on this rank instead of spinning forever.
+  if ((int)threadIdx.x < pp.world) {
+    const unsigned long long t0 = peer_clock_ns();
     while (ld_acquire_sys(pp.own_flags + threadIdx.x) < q) {
+      if (pp.timeout_ns != 0 && peer_clock_ns() - t0 > pp.timeout_ns) __trap();
     }
+  }
   __syncthreads();
   const size_t par = q & 1;
   for (int r = 0; r < pp.world; ++r) {

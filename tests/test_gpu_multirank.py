@@ -177,6 +177,58 @@ def test_ranks_share_gpu_bitwise(world, transport, bins):
             assert got[k] == ref[k], (rank, k)
 
 
+def _absent_peer_worker(rank, world, port, out_q):
+    import sys
+    import time
+    sys.path.insert(0, ROOT)
+    os.environ["ADC_PEER_TIMEOUT_S"] = "3"
+    import torch.distributed as dist
+    import paper_2203_06139_b200 as adc_
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    err = None
+    try:
+        counts, ev, q, _ = _problem(BINS)
+        comm = adc_.Comm.from_torch("peer")
+        h = adc_.Histogram(counts.size, -5.0, 5.0, ev, counts)
+        L = adc_.chi2_layout(counts.size, world, rank)
+        shard = torch.from_numpy(counts[L.bin_begin:L.bin_end].copy()).cuda()
+        plan = adc_.Chi2Plan.sharded("gpoly", 6, h, shard, comm)
+        if rank == 0:  # rank 1 never runs the pass
+            t0 = time.monotonic()
+            try:
+                plan.gradient(q)
+                torch.cuda.synchronize()
+            except Exception as e:  # noqa: BLE001
+                err = (e.kind if hasattr(e, "kind") else type(e).__name__, time.monotonic() - t0)
+        out_q.put((rank, err))
+    except Exception as e:  # noqa: BLE001
+        out_q.put((rank, ("setup", repr(e))))
+    dist.barrier()
+    os._exit(0)  # rank 0's CUDA context is gone after the trap
+
+
+def test_absent_peer_fails_instead_of_hanging():
+    """Peer transport: a rank whose peers never reach the pass gets an error
+    after ADC_PEER_TIMEOUT_S (the flag wait traps) — it does not spin on the
+    GPU forever."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    out_q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_absent_peer_worker, args=(r, 2, port, out_q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(out_q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+    assert res[1] is None
+    assert res[0] is not None and res[0][0] != "setup", res[0]
+    assert res[0][0] == "Cuda" and 2.5 < res[0][1] < 120, res[0]
+
+
 # ---- shared mean vector over ranks (SURVEY.md §8(e): dp all-reduce) ---------------
 def _sp_problem(dim=100, n=50_003, seed=3):
     rng = np.random.Generator(np.random.PCG64(seed))
