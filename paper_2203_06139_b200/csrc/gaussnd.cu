@@ -29,8 +29,8 @@
 
 namespace adcb {
 
-template <int W, int U, int PF, int PFD = 1, int CL = 1>
-__global__ void __launch_bounds__(W * 32) gaussnd_tile_kernel(
+template <int W, int U, int PF, int PFD = 1, int CL = 1, int TPC = 1>
+__global__ void __launch_bounds__(W * 32 * TPC) gaussnd_tile_kernel(
     const double* __restrict__ x, const double* __restrict__ p, double* __restrict__ dx,
     double* __restrict__ dp, int64_t n, int dim, int64_t ld, double t4, double r1, int dpw,
     int dstage) {
@@ -43,13 +43,18 @@ __global__ void __launch_bounds__(W * 32) gaussnd_tile_kernel(
   // CL > 1: the CL CTAs of a cluster (CL SMs) share each tile, CTA r taking
   // the dims of warps r*W .. r*W+W-1; the warp partials of t are combined
   // over distributed shared memory in global warp order.
+  // TPC > 1 (W = 1 only): the TPC warps of a CTA take TPC neighbouring
+  // tiles in step, so the 32-byte sectors two neighbouring tiles share in a
+  // row that is not sector-aligned are touched by one SM at about the same
+  // time (merged in L2) instead of by two SMs far apart.
   const int crank = CL > 1 ? (int)(blockIdx.x % CL) : 0;
-  const int d0 = (crank * W + warp) * dpw;
+  const int d0 = TPC > 1 ? 0 : (crank * W + warp) * dpw;
   const int d1 = min(dim, d0 + dpw);
   const int64_t ntiles = (n + 31) / 32;
-  const int64_t gstride = gridDim.x / CL;  // tiles in flight over the grid
+  const int64_t gstride = (int64_t)gridDim.x / CL * TPC;  // tiles in flight over the grid
 
-  for (int64_t tile = blockIdx.x / CL; tile < ntiles; tile += gstride) {
+  for (int64_t tile = blockIdx.x / CL * TPC + (TPC > 1 ? warp : 0); tile < ntiles;
+       tile += gstride) {
     const int64_t i = tile * 32 + lane;
     const bool valid = i < n;
     const double* xi = x + i;
@@ -441,14 +446,17 @@ __global__ void __launch_bounds__(32) gaussnd_vec2_kernel(
 }
 
 // ---------------------------------------------------------------------------
-// 0 auto (K2v below 105 dims when aligned, else K2 as chosen by choose());
+// 0 auto (K2v below 105 dims when aligned, else K2 as chosen by choose(),
+// with 8 tiles per CTA where W = 1 and the stages fit);
 // 10-13 = K2v (U = 16 / 16 with a 104 KB stage / 8 / 32);
 // 1/3/4 = one warp per 32-point tile (reference summation order) with
 // 8/16/32 rows in flight per thread (+ L2 prefetch of the next batch);
 // 5 = as 3 without prefetch; 6 = as 3 with bulk (TMA-unit) prefetch;
 // 2 = dims split over the warps of a CTA (7 = same with bulk prefetch);
 // 8 = as 3 prefetching two batches ahead, 9 = U=8 prefetching three ahead;
-// 15 = clusters of 2 CTAs x 16 warps sharing each tile (dims over 32 warps).
+// 15 = clusters of 2 CTAs x 16 warps sharing each tile (dims over 32 warps);
+// 16 / 17 = as 3 with 4 / 8 neighbouring tiles per CTA in step (one per warp),
+// 18 = as 1 (U = 8) with 8 tiles per CTA.
 static int g_variant = 0;
 
 struct NdConfig {
@@ -456,19 +464,21 @@ struct NdConfig {
   size_t smem;
 };
 
-template <int W, int U, int PF = 1, int PFD = 1>
+template <int W, int U, int PF = 1, int PFD = 1, int TPC = 1>
 static int launch_tile(const NdConfig& c, int64_t n, int dim, int64_t ld, const double* x,
                        const double* p, double* dx, double* dp, double t4, double r1,
                        cudaStream_t s) {
-  auto k = gaussnd_tile_kernel<W, U, PF, PFD>;
-  if (c.smem > 48 * 1024)
-    ADCB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem));
+  auto k = gaussnd_tile_kernel<W, U, PF, PFD, 1, TPC>;
+  const size_t smem = TPC > 1 ? ((size_t)TPC * 32 + (size_t)TPC * c.dstage * 32) * sizeof(double)
+                              : c.smem;
+  if (smem > 48 * 1024)
+    ADCB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
-  ADCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, W * 32, c.smem));
+  ADCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, W * 32 * TPC, smem));
   if (occ < 1) return fail(ADC_E_LAUNCH, "gaussnd: tile configuration does not fit an SM");
   const int64_t ntiles = (n + 31) / 32;
-  int64_t blocks = std::min<int64_t>(ntiles, (int64_t)occ * sm_count());
-  k<<<(unsigned)blocks, W * 32, c.smem, s>>>(x, p, dx, dp, n, dim, ld, t4, r1, c.dpw, c.dstage);
+  int64_t blocks = std::min<int64_t>((ntiles + TPC - 1) / TPC, (int64_t)occ * sm_count());
+  k<<<(unsigned)blocks, W * 32 * TPC, smem, s>>>(x, p, dx, dp, n, dim, ld, t4, r1, c.dpw, c.dstage);
   ADCB_CUDA(cudaGetLastError());
   return ADC_OK;
 }
@@ -511,7 +521,7 @@ static NdConfig choose(int dim) {
   // W = 1 keeps the reference's summation order; it needs the whole u row of
   // a point on chip: 256 B per dim per warp.  Use it while >= 8 warps fit.
   if (variant == 1 || variant == 3 || variant == 4 || variant == 5 || variant == 6 ||
-      variant == 8 || variant == 9 ||
+      variant == 8 || variant == 9 || variant == 16 || variant == 17 || variant == 18 ||
       (variant == 0 && (size_t)dim * 256 * 8 <= kSmemPerSm)) {
     c.w = 1;
     c.dpw = dim;
@@ -525,7 +535,7 @@ static NdConfig choose(int dim) {
     const size_t avail = per_cta - (size_t)c.w * 32 * 8 - 1024;
     c.dstage = std::min<int>(c.dpw, (int)(avail / ((size_t)c.w * 256)));
   }
-  c.u = (variant == 1 || variant == 9) ? 8 : variant == 4 ? 32 : 16;
+  c.u = (variant == 1 || variant == 9 || variant == 18) ? 8 : variant == 4 ? 32 : 16;
   if (c.w > 1) c.u = 8;
   c.smem = ((size_t)c.w * 32 + (size_t)c.w * c.dstage * 32) * sizeof(double);
   return c;
@@ -614,6 +624,17 @@ int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, con
   NdConfig c = choose((int)dim);
   switch (c.w) {
     case 1:
+      if (g_variant == 16)
+        return launch_tile<1, 16, 1, 1, 4>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+      // Auto: 8 neighbouring tiles per CTA for 32 <= dim <= 112 (the stages
+      // fit one CTA): same bits as one warp per CTA, 3-19% faster (10M x 100:
+      // 7.93 vs 8.29 ms aligned, 10.1 vs 12.0 ms with odd n); slower at dim 8.
+      if (g_variant == 17 ||
+          (g_variant == 0 && dim >= 32 &&
+           (size_t)8 * 32 * 8 + (size_t)8 * c.dstage * 256 <= 227 * 1024))
+        return launch_tile<1, 16, 1, 1, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+      if (g_variant == 18)
+        return launch_tile<1, 8, 1, 1, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
       if (c.u == 8) return launch_tile<1, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
       if (c.u == 32) return launch_tile<1, 32>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
       if (g_variant == 5)
@@ -636,7 +657,7 @@ int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, con
 }
 
 int gaussnd_set_variant(int v) {
-  if (v < 0 || v > 15) return fail(ADC_E_ARG, "gaussnd variant must be 0..15");
+  if (v < 0 || v > 18) return fail(ADC_E_ARG, "gaussnd variant must be 0..18");
   g_variant = v;
   return ADC_OK;
 }
