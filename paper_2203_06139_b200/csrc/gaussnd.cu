@@ -591,7 +591,10 @@ int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, con
       if (const char* e = getenv("ADC_K2V_STAGE_KB")) budget = (size_t)atoi(e) * 1024;  // experiment
       const int dstage = (int)std::min<int64_t>(dim, budget / 512);
       const size_t smem = (size_t)dstage * 512;
-      auto k = g_variant == 12 ? gaussnd_vec2_kernel<8>
+      // auto: the row batch no longer than the dims (U = 16 never batches below 16)
+      auto k = g_variant == 0 && dim < 4   ? gaussnd_vec2_kernel<2>
+             : g_variant == 0 && dim < 8   ? gaussnd_vec2_kernel<4>
+             : g_variant == 12 || (g_variant == 0 && dim < 16) ? gaussnd_vec2_kernel<8>
              : g_variant == 13 ? gaussnd_vec2_kernel<32> : gaussnd_vec2_kernel<16>;
       if (smem > 48 * 1024)
         ADCB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -626,15 +629,21 @@ int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, con
     case 1:
       if (g_variant == 16)
         return launch_tile<1, 16, 1, 1, 4>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
-      // Auto: 8 neighbouring tiles per CTA for 32 <= dim <= 112 (the stages
-      // fit one CTA): same bits as one warp per CTA, 3-19% faster (10M x 100:
-      // 7.93 vs 8.29 ms aligned, 10.1 vs 12.0 ms with odd n); slower at dim 8.
-      if (g_variant == 17 ||
-          (g_variant == 0 && dim >= 32 &&
-           (size_t)8 * 32 * 8 + (size_t)8 * c.dstage * 256 <= 227 * 1024))
-        return launch_tile<1, 16, 1, 1, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
-      if (g_variant == 18)
-        return launch_tile<1, 8, 1, 1, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+      // Auto: 8 neighbouring tiles per CTA for 8 <= dim <= 112 (the stages
+      // fit one CTA), with a row batch no longer than the dims: same bits as
+      // one warp per CTA, 3-19% faster (10M x 100: 7.93 vs 8.29 ms aligned,
+      // 10.1 vs 12.0 ms with odd n) and 2x at dim 8 (U = 16 never batches).
+      {
+        const bool fits = (size_t)8 * 32 * 8 + (size_t)8 * c.dstage * 256 <= 227 * 1024;
+        if (g_variant == 17 || (g_variant == 0 && dim >= 16 && fits))
+          return launch_tile<1, 16, 1, 1, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+        if (g_variant == 18 || (g_variant == 0 && dim >= 8 && fits))
+          return launch_tile<1, 8, 1, 1, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+        if (g_variant == 0 && dim >= 4 && fits)
+          return launch_tile<1, 4, 1, 1, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+        if (g_variant == 0 && dim >= 2 && fits)
+          return launch_tile<1, 2, 1, 1, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+      }
       if (c.u == 8) return launch_tile<1, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
       if (c.u == 32) return launch_tile<1, 32>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
       if (g_variant == 5)

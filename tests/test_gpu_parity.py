@@ -140,13 +140,16 @@ def test_gaussnd_host_path():
 
 
 @pytest.mark.parametrize("dim,n", [(100, 200_003), (100, 200_010), (64, 4096), (1000, 20_011),
-                                   (5, 77), (300, 1000)])
+                                   (5, 77), (300, 1000), (2, 4097), (3, 1000), (4, 2049),
+                                   (6, 640), (8, 1001), (12, 777), (16, 3000), (110, 513)])
 def test_gaussnd_vs_oracle(restate, dim, n):
-    # variant 0 = auto (K2v with double2 for dim <= 104 on even ld, tail via K2)
+    # variant 0 = auto (K2v with double2 for dim <= 104 on even ld, tail via K2;
+    # the row batch U follows the dims; K2 runs 8 neighbouring tiles per CTA),
+    # 15 = 2-CTA clusters, 17 / 18 = 8 tiles per CTA with U = 16 / 8
     x, p = synth.points_nd(dim, n, seed=dim)
     ox, op = np.zeros((dim, n)), np.zeros((dim, n))
     restate.gaussnd_grad(x, p, 1.3, ox, op)
-    for variant in (0, 1, 2, 6, 7, 10):
+    for variant in (0, 1, 2, 3, 6, 7, 10, 15) + ((17, 18) if dim <= 112 else ()):
         set_gaussnd_variant(variant)
         try:
             dx = torch.zeros((dim, n), dtype=torch.float64, device=DEV)
