@@ -1142,9 +1142,17 @@ int launch_gaussnd_shared_p(int64_t n, int64_t dim, int64_t ld, const double* x,
     const int64_t full64 = n / 64, rem64 = n % 64;
     const int64_t vblocks = std::min<int64_t>(full64, kSharedPVecBlocks);
     const size_t vsmem = (size_t)dim * 512;
-    // U = 16 rows in flight: measured best of 16 / 24 / 32
-    auto kv = dx != nullptr ? gaussnd_shared_p_vec2_kernel<16, 16, 4, true>
-                            : gaussnd_shared_p_vec2_kernel<16, 16, 4, false>;
+    // U = 16 rows in flight: measured best of 16 / 24 / 32; below 16 dims the
+    // batch follows the dims (U = 16 would never batch: one dependent row at
+    // a time).  Same bits for any U (t in row order, each slot once).
+    auto kv = dim >= 16 ? (dx != nullptr ? gaussnd_shared_p_vec2_kernel<16, 16, 4, true>
+                                         : gaussnd_shared_p_vec2_kernel<16, 16, 4, false>)
+            : dim >= 8  ? (dx != nullptr ? gaussnd_shared_p_vec2_kernel<8, 8, 4, true>
+                                         : gaussnd_shared_p_vec2_kernel<8, 8, 4, false>)
+            : dim >= 4  ? (dx != nullptr ? gaussnd_shared_p_vec2_kernel<4, 4, 4, true>
+                                         : gaussnd_shared_p_vec2_kernel<4, 4, 4, false>)
+                        : (dx != nullptr ? gaussnd_shared_p_vec2_kernel<2, 2, 4, true>
+                                         : gaussnd_shared_p_vec2_kernel<2, 2, 4, false>);
     if (vsmem > 48 * 1024)
       ADCB_CUDA(cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsmem));
     ADCB_CUDA(cudaFuncSetAttribute(kv, cudaFuncAttributePreferredSharedMemoryCarveout,

@@ -595,7 +595,8 @@ def test_gaussnd_shared_p_large_and_refusal(restate):
     assert np.all(np.abs(host(dp) - tot) <= 1e-12 * ab)
 
 
-@pytest.mark.parametrize("dim,n", [(100, 200_006), (37, 64 * 700), (128, 5_000)])
+@pytest.mark.parametrize("dim,n", [(100, 200_006), (37, 64 * 700), (128, 5_000), (2, 10_001),
+                                   (3, 6_400), (5, 4_099), (12, 3_000)])
 def test_gaussnd_shared_p_with_dx_paths(restate, dim, n):
     """With private dx slots: the aligned layout runs K2sv (double2 rows,
     64-point tiles, ragged tail through K2s), an odd-offset view of the same

@@ -9,8 +9,9 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2203_06139_b200 as adc  # noqa: E402
 
-dim, n = 100, 10_000_000
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 9
+dim = int(sys.argv[2]) if len(sys.argv) > 2 else 100
+n = int(sys.argv[3]) if len(sys.argv) > 3 else 10_000_000
 p = torch.rand(dim, dtype=torch.float64, device="cuda")
 x = p[:, None] + 0.1 * torch.randn((dim, n), dtype=torch.float64, device="cuda")
 dx = torch.zeros_like(x)
