@@ -1115,7 +1115,14 @@ int launch_gaussnd_shared_p(int64_t n, int64_t dim, int64_t ld, const double* x,
   const size_t fixed = (size_t)dim * sizeof(double);
   int dstage = fixed >= budget ? 0 : (int)std::min<int64_t>(dim, (budget - fixed) / 256);
   const size_t smem = fixed + (size_t)dstage * 256;
-  auto k = gaussnd_shared_p_kernel<32, 8>;  // measured best of U in {16, 32} x V in {4, 8}
+  // measured best of U in {16, 32} x V in {4, 8}; below 32 dims both follow
+  // the dims (a batch longer than the dims never runs).  Same bits for any
+  // U, V (t in row order; one fixed shuffle tree per dim).
+  auto k = dim >= 32 ? gaussnd_shared_p_kernel<32, 8>
+         : dim >= 16 ? gaussnd_shared_p_kernel<16, 8>
+         : dim >= 8  ? gaussnd_shared_p_kernel<8, 8>
+         : dim >= 4  ? gaussnd_shared_p_kernel<4, 4>
+                     : gaussnd_shared_p_kernel<2, 2>;
   if (smem > 48 * 1024)
     ADCB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   // Decomposition (a function of n only, so the bits do not depend on the
