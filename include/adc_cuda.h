@@ -123,6 +123,20 @@ int adc_cuda_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, c
 /* Host-buffer variant (pinned memory recommended); synchronous, pipelined. */
 int adc_cuda_gaussnd_grad_host(int64_t n, int64_t dim, int64_t ld, const double* x,
                                const double* p, double sigma, double* dx, double* dp);
+/* Multi-GPU host-buffer form (north_star (4); replaces the reference's
+ * data-parallel split of one batch over its worker threads, launch.cpp:305-343):
+ * the n points are split into ndev contiguous ranges of whole 64-point tiles
+ * and one host thread per device runs the host pipeline on its range, so
+ * every device's PCIe link carries its share of the copies at once.  No
+ * collective: points are independent, so every output is bit-identical to
+ * the single-device call.  devices: ndev distinct device ordinals, or NULL
+ * for 0..ndev-1.  Synchronous; safe to call from several threads. */
+int adc_cuda_gaussnd_grad_host_mg(int32_t ndev, const int32_t* devices, int64_t n, int64_t dim,
+                                  int64_t ld, const double* x, const double* p, double sigma,
+                                  double* dx, double* dp);
+int adc_cuda_compute_gauss_host_mg(int32_t ndev, const int32_t* devices, int64_t grid_dim,
+                                   int64_t block_dim, int64_t n, const double* x, const double* p,
+                                   double sigma, double* dx, double* dp);
 /* Shared mean vector: every point i runs
  * gaussnd_grad_0_1(x[:, i], p, sigma, dim, dx[:, i], dp) with ONE p[dim] and
  * ONE shared slot dp[dim] — a shared-write hazard the reference refuses
@@ -375,6 +389,8 @@ typedef struct adc_fit_options {
   double armijo_c1;      /* 1e-4 */
   int32_t trace_iterates;
   int32_t use_hessian;   /* 0; Newton step from a numeric Hessian of the gradient (fit.cpp:346-381) */
+  int32_t host_loop;     /* 0: the device-resident loop where the plan allows it; 1: the
+                            host-driven loop over graph-replayed passes (the same bits) */
 } adc_fit_options;
 
 typedef struct adc_fit_result {

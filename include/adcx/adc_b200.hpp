@@ -179,6 +179,19 @@ inline void launch_batch_gaussnd(int64_t n, int64_t dim, const std::vector<doubl
   check(adc_cuda_gaussnd_grad_host(n, dim, n, x.data(), p.data(), sigma, dx.data(), dp.data()));
 }
 
+// The same over several GPUs (one host thread per device, contiguous point
+// ranges; no collective): bit-identical to the single-device call.
+inline void launch_batch_gaussnd(int64_t n, int64_t dim, const std::vector<double>& x,
+                                 const std::vector<double>& p, double sigma,
+                                 std::vector<double>& dx, std::vector<double>& dp,
+                                 const std::vector<int32_t>& devices) {
+  const size_t need = static_cast<size_t>(n * dim);
+  if (x.size() < need || p.size() < need || dx.size() < need || dp.size() < need)
+    throw Error(ErrorKind::Launch, "gaussnd buffers shorter than dim * n");
+  check(adc_cuda_gaussnd_grad_host_mg(static_cast<int32_t>(devices.size()), devices.data(), n, dim,
+                                      n, x.data(), p.data(), sigma, dx.data(), dp.data()));
+}
+
 // ---- fit.hpp -------------------------------------------------------------
 struct Histogram {
   int bins = 0;
@@ -198,6 +211,7 @@ struct FitOptions {
   double armijo_c1 = 1e-4;
   bool use_hessian = false;
   int trace_iterates = 0;
+  bool host_loop = false;  // B200 option: host-driven loop (same bits as the device loop)
 };
 
 struct FitResult {
@@ -296,7 +310,7 @@ class FitEngine {
     else
       clamp.push_back(2);
     adc_fit_options co{o.budget, o.grad_tol, o.chi2_rel_tol, o.sigma_min, o.armijo_c1,
-                       o.trace_iterates, o.use_hessian ? 1 : 0};
+                       o.trace_iterates, o.use_hessian ? 1 : 0, o.host_loop ? 1 : 0};
     adc_fit_result cr{};
     std::vector<double> its(static_cast<size_t>(std::max(1, o.trace_iterates) * np_));
     check(adc_cuda_fit(plan(h), init.data(), clamp.data(), static_cast<int32_t>(clamp.size()),

@@ -44,7 +44,7 @@ class FitOptions(ctypes.Structure):
     _fields_ = [("budget", ctypes.c_int32), ("grad_tol", ctypes.c_double),
                 ("chi2_rel_tol", ctypes.c_double), ("sigma_min", ctypes.c_double),
                 ("armijo_c1", ctypes.c_double), ("trace_iterates", ctypes.c_int32),
-                ("use_hessian", ctypes.c_int32)]
+                ("use_hessian", ctypes.c_int32), ("host_loop", ctypes.c_int32)]
 
 
 class FitResultC(ctypes.Structure):
@@ -81,6 +81,10 @@ SIGNATURES = {
                                                           _VP, _VP, _I32]),
     "adc_cuda_gaussnd_grad": (ctypes.c_int, [_I64, _I64, _I64, _VP, _VP, _DBL, _VP, _VP, _VP]),
     "adc_cuda_gaussnd_grad_host": (ctypes.c_int, [_I64, _I64, _I64, _VP, _VP, _DBL, _VP, _VP]),
+    "adc_cuda_gaussnd_grad_host_mg": (ctypes.c_int, [_I32, _VP, _I64, _I64, _I64, _VP, _VP, _DBL,
+                                                      _VP, _VP]),
+    "adc_cuda_compute_gauss_host_mg": (ctypes.c_int, [_I32, _VP, _I64, _I64, _I64, _VP, _VP, _DBL,
+                                                       _VP, _VP]),
     "adc_cuda_gaussnd_set_variant": (ctypes.c_int, [_I32]),
     "adc_cuda_gaussnd_grad_shared_p": (ctypes.c_int, [_I64, _I64, _I64, _VP, _VP, _DBL, _VP, _VP,
                                                       _I32, _VP]),

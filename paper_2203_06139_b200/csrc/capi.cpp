@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -73,20 +74,16 @@ static int require_device() {
   return ADC_OK;
 }
 
-// Device staging for the host-buffer pipelines (grown on demand, reused).
+// Device staging for the host-buffer pipelines (grown on demand, reused):
+// one per device, each with its own lock, so host threads driving different
+// GPUs (adc_cuda_*_host_mg, or one caller thread per GPU) never share or
+// release each other's buffers; calls on the same device serialise on it.
 struct Staging {
   std::mutex mu;
-  int device = -1;
   size_t bytes = 0;
   double* buf[2] = {nullptr, nullptr};
   cudaStream_t stream[2] = {nullptr, nullptr};
   int ensure(size_t need) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (device != dev) {
-      release();
-      device = dev;
-    }
     if (stream[0] == nullptr) {
       ADCB_CUDA(cudaStreamCreateWithFlags(&stream[0], cudaStreamNonBlocking));
       ADCB_CUDA(cudaStreamCreateWithFlags(&stream[1], cudaStreamNonBlocking));
@@ -107,7 +104,20 @@ struct Staging {
     bytes = 0;
   }
 };
-static Staging g_staging;
+constexpr int kMaxDevices = 64;
+static Staging g_staging[kMaxDevices];
+
+int gauss_host_pipeline(int64_t n, const double* x, const double* p, double sigma, double* dx,
+                        double* dp);
+int gaussnd_host_pipeline(int64_t n, int64_t dim, int64_t ld, const double* x, const double* p,
+                          double sigma, double* dx, double* dp);
+
+// The staging of the calling thread's current device.
+static Staging* staging_here() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
+  return &g_staging[dev];
+}
 
 }  // namespace adcb
 
@@ -246,13 +256,24 @@ extern "C" int adc_cuda_compute_gauss_host(int64_t grid, int64_t block, int64_t 
   if (int rc = validate_config(grid, block, n)) return rc;
   if (!x || !p || !dx || !dp) return fail(ADC_E_LAUNCH, "missing buffer");
   if (int rc = require_device()) return rc;
-  std::lock_guard<std::mutex> lock(g_staging.mu);
+  return gauss_host_pipeline(n, x, p, sigma, dx, dp);
+}
+
+namespace adcb {
+// Host-buffer pipeline of K1 on the current device: stages of up to 16 Mi
+// points alternate over two streams (H2D, kernel, D2H overlap).
+int gauss_host_pipeline(int64_t n, const double* x, const double* p, double sigma, double* dx,
+                        double* dp) {
+  if (n <= 0) return ADC_OK;
+  Staging* S = staging_here();
+  if (S == nullptr) return fail(ADC_E_CUDA, "no staging for the current device");
+  std::lock_guard<std::mutex> lock(S->mu);
   const int64_t chunk = std::min<int64_t>(n, int64_t(16) << 20);  // points per stage
-  if (int rc = g_staging.ensure((size_t)chunk * 4 * sizeof(double))) return rc;
+  if (int rc = S->ensure((size_t)chunk * 4 * sizeof(double))) return rc;
   for (int64_t i0 = 0, k = 0; i0 < n; i0 += chunk, ++k) {
     const int64_t c = std::min(chunk, n - i0);
-    cudaStream_t s = g_staging.stream[k & 1];
-    double* b = g_staging.buf[k & 1];
+    cudaStream_t s = S->stream[k & 1];
+    double* b = S->buf[k & 1];
     double *X = b, *P = b + chunk, *DX = b + 2 * chunk, *DP = b + 3 * chunk;
     const size_t bytes = (size_t)c * sizeof(double);
     ADCB_CUDA(cudaMemcpyAsync(X, x + i0, bytes, cudaMemcpyHostToDevice, s));
@@ -263,10 +284,11 @@ extern "C" int adc_cuda_compute_gauss_host(int64_t grid, int64_t block, int64_t 
     ADCB_CUDA(cudaMemcpyAsync(dx + i0, DX, bytes, cudaMemcpyDeviceToHost, s));
     ADCB_CUDA(cudaMemcpyAsync(dp + i0, DP, bytes, cudaMemcpyDeviceToHost, s));
   }
-  ADCB_CUDA(cudaStreamSynchronize(g_staging.stream[0]));
-  ADCB_CUDA(cudaStreamSynchronize(g_staging.stream[1]));
+  ADCB_CUDA(cudaStreamSynchronize(S->stream[0]));
+  ADCB_CUDA(cudaStreamSynchronize(S->stream[1]));
   return ADC_OK;
 }
+}  // namespace adcb
 
 // ---------------------------------------------------------------------------
 // compute_shared: race_check flags dsigma (launch.cpp:112-240); refused unless
@@ -348,17 +370,31 @@ extern "C" int adc_cuda_gaussnd_grad_host(int64_t n, int64_t dim, int64_t ld, co
   if (int rc = require_device()) return rc;
   if (n == 0) return launch_gaussnd_grad(0, dim, ld, x, p, sigma, dx, dp, nullptr);
   if (dim == 0) return launch_gaussnd_grad(n, 0, n, x, p, sigma, dx, dp, nullptr);
-  std::lock_guard<std::mutex> lock(g_staging.mu);
+  return gaussnd_host_pipeline(n, dim, ld, x, p, sigma, dx, dp);
+}
+
+namespace adcb {
+// Host-buffer pipeline of K2 on the current device: stages of ~512 MB per
+// array alternate over two streams; rows are copied with 2-D copies, so a
+// range of points of a larger SoA (ld > n) needs no host repacking.
+int gaussnd_host_pipeline(int64_t n, int64_t dim, int64_t ld, const double* x, const double* p,
+                          double sigma, double* dx, double* dp) {
+  if (n <= 0 || dim <= 0) return ADC_OK;
+  const double t4 = (2 * sigma) * sigma;
+  if (t4 == 0.0) return fail(ADC_E_EVAL, "division by zero");
+  Staging* S = staging_here();
+  if (S == nullptr) return fail(ADC_E_CUDA, "no staging for the current device");
+  std::lock_guard<std::mutex> lock(S->mu);
   // ~512 MB per array per stage; a whole number of 32-point tiles.
   int64_t chunk = (int64_t(512) << 20) / (dim * (int64_t)sizeof(double));
   chunk = std::max<int64_t>(32, chunk / 32 * 32);
   chunk = std::min(chunk, n);
-  if (int rc = g_staging.ensure((size_t)chunk * dim * 4 * sizeof(double))) return rc;
+  if (int rc = S->ensure((size_t)chunk * dim * 4 * sizeof(double))) return rc;
   const size_t spitch = (size_t)ld * sizeof(double);
   for (int64_t i0 = 0, k = 0; i0 < n; i0 += chunk, ++k) {
     const int64_t c = std::min(chunk, n - i0);
-    cudaStream_t s = g_staging.stream[k & 1];
-    double* b = g_staging.buf[k & 1];
+    cudaStream_t s = S->stream[k & 1];
+    double* b = S->buf[k & 1];
     const size_t plane = (size_t)chunk * dim;
     double *X = b, *P = b + plane, *DX = b + 2 * plane, *DP = b + 3 * plane;
     const size_t w = (size_t)c * sizeof(double), dpitch = (size_t)chunk * sizeof(double);
@@ -370,9 +406,79 @@ extern "C" int adc_cuda_gaussnd_grad_host(int64_t n, int64_t dim, int64_t ld, co
     ADCB_CUDA(cudaMemcpy2DAsync(dx + i0, spitch, DX, dpitch, w, dim, cudaMemcpyDeviceToHost, s));
     ADCB_CUDA(cudaMemcpy2DAsync(dp + i0, spitch, DP, dpitch, w, dim, cudaMemcpyDeviceToHost, s));
   }
-  ADCB_CUDA(cudaStreamSynchronize(g_staging.stream[0]));
-  ADCB_CUDA(cudaStreamSynchronize(g_staging.stream[1]));
+  ADCB_CUDA(cudaStreamSynchronize(S->stream[0]));
+  ADCB_CUDA(cudaStreamSynchronize(S->stream[1]));
   return ADC_OK;
+}
+
+// One host thread per device over contiguous point ranges (whole 64-point
+// tiles, so every range but the last starts 16-byte aligned and keeps K2v).
+// Points are independent, so each point's bits are those of one device; the
+// first failing range's error (code and text) is returned on the caller's
+// thread.
+template <class F>
+static int run_on_devices(int32_t ndev, const int32_t* devices, int64_t n, F&& body) {
+  int count = 0;
+  ADCB_CUDA(cudaGetDeviceCount(&count));
+  std::vector<int> devs((size_t)ndev);
+  for (int r = 0; r < ndev; ++r) {
+    devs[r] = devices ? devices[r] : r;
+    if (devs[r] < 0 || devs[r] >= count || devs[r] >= kMaxDevices)
+      return fail(ADC_E_ARG, "device " + std::to_string(devs[r]) + " does not exist (" +
+                                 std::to_string(count) + " visible)");
+    for (int q = 0; q < r; ++q)
+      if (devs[q] == devs[r]) return fail(ADC_E_ARG, "device listed twice");
+  }
+  const int64_t tiles = (n + 63) / 64;
+  std::vector<int> rcs((size_t)ndev, ADC_OK);
+  std::vector<std::string> msgs((size_t)ndev);
+  std::vector<std::thread> th;
+  for (int r = 0; r < ndev; ++r) {
+    const int64_t b = std::min(n, tiles * r / ndev * 64), e = std::min(n, tiles * (r + 1) / ndev * 64);
+    th.emplace_back([&, r, b, e] {
+      cudaError_t ce = cudaSetDevice(devs[r]);
+      int rc = ce == cudaSuccess ? (e > b ? body(b, e) : ADC_OK) : cuda_fail(ce, "cudaSetDevice");
+      rcs[r] = rc;
+      if (rc != ADC_OK) msgs[r] = adc_cuda_last_error();
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int r = 0; r < ndev; ++r)
+    if (rcs[r] != ADC_OK)
+      return fail(rcs[r], "device " + std::to_string(devs[r]) + ": " + msgs[r]);
+  return ADC_OK;
+}
+}  // namespace adcb
+
+extern "C" int adc_cuda_gaussnd_grad_host_mg(int32_t ndev, const int32_t* devices, int64_t n,
+                                             int64_t dim, int64_t ld, const double* x,
+                                             const double* p, double sigma, double* dx,
+                                             double* dp) {
+  clear_error();
+  if (ndev < 1) return fail(ADC_E_ARG, "ndev must be >= 1");
+  if (n < 0 || dim < 0) return fail(ADC_E_LAUNCH, "gaussnd: negative size");
+  if (ld < n) return fail(ADC_E_LAUNCH, "gaussnd: leading dimension smaller than n");
+  if (n > 0 && dim > 0 && (!x || !p || !dx || !dp)) return fail(ADC_E_LAUNCH, "missing buffer");
+  if (int rc = require_device()) return rc;
+  if (n > 0 && (2 * sigma) * sigma == 0.0) return fail(ADC_E_EVAL, "division by zero");
+  if (n == 0 || dim == 0) return ADC_OK;
+  return run_on_devices(ndev, devices, n, [&](int64_t b, int64_t e) {
+    return gaussnd_host_pipeline(e - b, dim, ld, x + b, p + b, sigma, dx + b, dp + b);
+  });
+}
+
+extern "C" int adc_cuda_compute_gauss_host_mg(int32_t ndev, const int32_t* devices, int64_t grid,
+                                              int64_t block, int64_t n, const double* x,
+                                              const double* p, double sigma, double* dx,
+                                              double* dp) {
+  clear_error();
+  if (ndev < 1) return fail(ADC_E_ARG, "ndev must be >= 1");
+  if (int rc = validate_config(grid, block, n)) return rc;
+  if (!x || !p || !dx || !dp) return fail(ADC_E_LAUNCH, "missing buffer");
+  if (int rc = require_device()) return rc;
+  return run_on_devices(ndev, devices, n, [&](int64_t b, int64_t e) {
+    return gauss_host_pipeline(e - b, x + b, p + b, sigma, dx + b, dp + b);
+  });
 }
 
 extern "C" int adc_cuda_gaussnd_grad_shared_p(int64_t n, int64_t dim, int64_t ld,

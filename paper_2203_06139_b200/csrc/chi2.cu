@@ -893,34 +893,10 @@ __global__ void __launch_bounds__(kChunkThreads) chi2_chunk_kernel(
 }
 
 // ---- dispatch ----------------------------------------------------------------
-int g_chi2_tune = 0;  // experiment knob (ADC_CHI2_TUNE), see launch_tiles_t
-
 template <class M, bool GRAD, bool FAST, bool REC = false>
 static void launch_tiles_t(const Chi2Pass& P, dim3 blocks, cudaStream_t s) {
   constexpr int MB = tile_min_blocks<M, GRAD>();
   if constexpr (std::is_same<M, GPoly>::value && FAST) {
-    // experiments: 1 = one bin at a time; 3 = 2 bins, 3 CTAs/SM; 4 = 1 bin,
-    // 3 CTAs/SM; 5 = 4 bins
-    if (g_chi2_tune == 3) {
-      chi2_tile_kernel<M, GRAD, FAST, 3, 2, false, REC><<<dim3(sm_count() * 3, blocks.y), kTileThreads, 0, s>>>(P);
-      return;
-    }
-    if (g_chi2_tune == 4) {
-      chi2_tile_kernel<M, GRAD, FAST, 3, 1, false, REC><<<dim3(sm_count() * 3, blocks.y), kTileThreads, 0, s>>>(P);
-      return;
-    }
-    if (g_chi2_tune == 5) {
-      chi2_tile_kernel<M, GRAD, FAST, MB, 4, false, REC><<<blocks, kTileThreads, 0, s>>>(P);
-      return;
-    }
-    if (g_chi2_tune == 1) {
-      chi2_tile_kernel<M, GRAD, FAST, MB, 1, false, REC><<<blocks, kTileThreads, 0, s>>>(P);
-      return;
-    }
-    if (g_chi2_tune == 6) {  // REC with the register ring of global loads
-      chi2_tile_kernel<M, GRAD, FAST, MB, 1, false, REC><<<blocks, kTileThreads, 0, s>>>(P);
-      return;
-    }
     // default: two bins evaluated before either is folded (measured 1.5% faster);
     // with REC one bin at a time (0.322 vs 0.366 ms at 1e8 bins: REC's two
     // extra live doubles push the two-bin form into local memory) and the 1/c
@@ -1046,8 +1022,8 @@ int chi2_multi_enqueue(const Chi2Pass& P, int model, int np, int ncand,
     if constexpr (M::NG <= 2) {
       if (prec == 2) {
         // bulk-staged 1/c for one-factor models (the two-factor tables leave
-        // no room for the stages in 48 KB); tune 6 = the direct-load form
-        if (M::NG == 1 && g_chi2_tune != 6)
+        // no room for the stages in 48 KB)
+        if (M::NG == 1)
           chi2_multi_kernel<M, true, M::NG == 1><<<grid, kTileThreads, 0, s>>>(P, ncand);
         else
           chi2_multi_kernel<M, true><<<grid, kTileThreads, 0, s>>>(P, ncand);
@@ -1109,10 +1085,6 @@ void fill_qdev(int model, int np, const double* q, double* host_qdev) {
 
 size_t qdev_bytes() { return sizeof(QDev) + sizeof(QNum); }
 
-int chi2_set_tune(int v) {
-  g_chi2_tune = v;
-  return ADC_OK;
-}
 
 // ---- K6: on-device histogram sampling ---------------------
 // The reference's sample_histogram (fit.cpp:70-104) draws events by rejection

@@ -449,7 +449,6 @@ extern "C" int adc_cuda_chi2_plan_create(adc_chi2_plan** out, int32_t model, int
                                        sizeof(double))) != cudaSuccess)
     return cleanup(cuda_fail(e, "chi2 plan allocation"));
   if (int rc = alloc_staging(P)) return cleanup(rc);
-  if (const char* t = getenv("ADC_CHI2_TUNE")) chi2_set_tune(atoi(t));  // experiment knob
   *out = P;
   return ADC_OK;
 }
@@ -543,7 +542,6 @@ extern "C" int adc_cuda_chi2_set_precision(adc_chi2_plan* P, int32_t mode) {
     cudaGraphExecDestroy(P->fit_graph);
     P->fit_graph = nullptr;
   }
-  if (const char* t = getenv("ADC_CHI2_TUNE")) chi2_set_tune(atoi(t));
   return ADC_OK;
 }
 
@@ -783,6 +781,7 @@ extern "C" void adc_fit_default_options(adc_fit_options* o) {
   o->armijo_c1 = 1e-4;
   o->trace_iterates = 0;
   o->use_hessian = 0;
+  o->host_loop = 0;
 }
 
 namespace {
@@ -989,15 +988,14 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
   std::vector<double> g(np), trial(np);
   int first_batch = 32;  // line-search batch size, adapted per iteration
   // next batch = the last search's trial count + margin, in groups of 4 (the
-  // multi pass's candidate group); ADC_FIT_MARGIN is an experiment knob
-  const int margin = getenv("ADC_FIT_MARGIN") ? atoi(getenv("ADC_FIT_MARGIN")) : 4;
+  // multi pass's candidate group)
+  const int margin = 4;
   // Device-resident loop (fit_device.cu): the fast passes on one device,
   // either gradient provider, steepest descent or the Newton option.
-  // ADC_FIT_DEVICE=0 keeps the host-driven loop (both give the same bits).
-  const char* fd_env = getenv("ADC_FIT_DEVICE");
+  // opts->host_loop keeps the host-driven loop (both give the same bits).
   const bool peer = P->comm != nullptr && P->comm->kind == ADC_COMM_PEER;
   const bool dev_mode = P->fast && (peer || (P->comm == nullptr && !sharded(P))) &&
-                        nclamp <= kMaxNp && !(fd_env && atoi(fd_env) == 0);
+                        nclamp <= kMaxNp && !opts->host_loop;
   if (dev_mode) {
     FitDevConst c{};
     c.grad_tol = opts->grad_tol;
@@ -1014,8 +1012,6 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
     if (iterates != nullptr && opts->trace_iterates > 1) {
       if (P->fit_trace_cap < opts->trace_iterates) {
         if (P->fit_trace) cudaFree(P->fit_trace);
-  if (P->fit_full) cudaFree(P->fit_full);
-  if (P->fit_rbegin) cudaFree(P->fit_rbegin);
         P->fit_trace = nullptr;
         P->fit_trace_cap = 0;
         ADCB_CUDA(cudaMalloc(&P->fit_trace, (size_t)opts->trace_iterates * kMaxNp * sizeof(double)));

@@ -50,12 +50,11 @@ int chi2_multi_enqueue(const Chi2Pass& P, int model, int np, int ncand,
                        int prec);
 void fill_qdev(int model, int np, const double* q, double* host_qdev);
 size_t qdev_bytes();
-int chi2_set_tune(int v);
 // K6: counts[j] ~ Poisson(events m_j / sum m) (Philox, counter = bin), ws =
 // histogram_sample_ws_doubles(bins) doubles; ws[nblocks + 1] = sum of counts.
 int histogram_sample_enqueue(int model, int np, const double* qdev, int64_t bins, double lo,
                              double width, double events, uint64_t seed, int64_t zero_every,
                              double* counts, double* ws, cudaStream_t s);
-int64_t histogram_sample_ws_doubles(int64_t bins);  // kernel-variant experiments (ADC_CHI2_TUNE)
+int64_t histogram_sample_ws_doubles(int64_t bins);
 
 }  // namespace adcb

@@ -29,7 +29,7 @@
 
 namespace adcb {
 
-template <int W, int U, int PF, int PFD = 1, int CL = 1, int TPC = 1>
+template <int W, int U, int PF, int TPC = 1>
 __global__ void __launch_bounds__(W * 32 * TPC) gaussnd_tile_kernel(
     const double* __restrict__ x, const double* __restrict__ p, double* __restrict__ dx,
     double* __restrict__ dp, int64_t n, int dim, int64_t ld, double t4, double r1, int dpw,
@@ -40,20 +40,16 @@ __global__ void __launch_bounds__(W * 32 * TPC) gaussnd_tile_kernel(
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   double* my_stage = stage + (size_t)warp * dstage * 32 + lane;
-  // CL > 1: the CL CTAs of a cluster (CL SMs) share each tile, CTA r taking
-  // the dims of warps r*W .. r*W+W-1; the warp partials of t are combined
-  // over distributed shared memory in global warp order.
   // TPC > 1 (W = 1 only): the TPC warps of a CTA take TPC neighbouring
   // tiles in step, so the 32-byte sectors two neighbouring tiles share in a
   // row that is not sector-aligned are touched by one SM at about the same
   // time (merged in L2) instead of by two SMs far apart.
-  const int crank = CL > 1 ? (int)(blockIdx.x % CL) : 0;
-  const int d0 = TPC > 1 ? 0 : (crank * W + warp) * dpw;
+  const int d0 = TPC > 1 ? 0 : warp * dpw;
   const int d1 = min(dim, d0 + dpw);
   const int64_t ntiles = (n + 31) / 32;
-  const int64_t gstride = (int64_t)gridDim.x / CL * TPC;  // tiles in flight over the grid
+  const int64_t gstride = (int64_t)gridDim.x * TPC;  // tiles in flight over the grid
 
-  for (int64_t tile = blockIdx.x / CL * TPC + (TPC > 1 ? warp : 0); tile < ntiles;
+  for (int64_t tile = blockIdx.x * TPC + (TPC > 1 ? warp : 0); tile < ntiles;
        tile += gstride) {
     const int64_t i = tile * 32 + lane;
     const bool valid = i < n;
@@ -90,7 +86,7 @@ __global__ void __launch_bounds__(W * 32 * TPC) gaussnd_tile_kernel(
           // reverse sweep will read (dx, dp at the top of the range)
 #pragma unroll
           for (int k = 0; k < U; ++k) {
-            const int dn = d + U * PFD + k;
+            const int dn = d + U + k;
             if (dn < d1) {
               prefetch_l2(xi + (int64_t)dn * ld);
               prefetch_l2(pi + (int64_t)dn * ld);
@@ -114,20 +110,7 @@ __global__ void __launch_bounds__(W * 32 * TPC) gaussnd_tile_kernel(
         t = fadd(t, fmul(u, u));
       }
     }
-    if (CL > 1) {
-      tpart[warp * 32 + lane] = t;
-      cluster_sync();
-      t = 0.0;
-#pragma unroll 1
-      for (int r = 0; r < CL; ++r) {
-        const uint32_t rp = dsmem_map(tpart + lane, r);
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-          const double v = ld_dsmem(rp + (uint32_t)(w * 32 * sizeof(double)));
-          t = (r == 0 && w == 0) ? v : fadd(t, v);
-        }
-      }
-    } else if (W > 1) {
+    if (W > 1) {
       tpart[warp * 32 + lane] = t;
       __syncthreads();
       t = tpart[lane];
@@ -200,7 +183,7 @@ __global__ void __launch_bounds__(W * 32 * TPC) gaussnd_tile_kernel(
           const int64_t inext = i + gstride * 32;
 #pragma unroll
           for (int k = 0; k < U; ++k) {
-            const int dn = d - 1 - U * PFD - k;
+            const int dn = d - 1 - U - k;
             if (dn >= d0) {
               prefetch_l2(dxi + (int64_t)dn * ld);
               prefetch_l2(dpi + (int64_t)dn * ld);
@@ -228,90 +211,11 @@ __global__ void __launch_bounds__(W * 32 * TPC) gaussnd_tile_kernel(
         dpi[o] = fadd(dpi[o], -r6);
       }
     }
-    if (CL > 1) cluster_sync();  // peers have read tpart before the next tile rewrites it
-    else if (W > 1) __syncthreads();  // tpart is rewritten by the next tile
+    if (W > 1) __syncthreads();  // tpart is rewritten by the next tile
   }
 }
 
 static int make_rows_tmap(CUtensorMap* m, const double* x, int64_t npts, int64_t dim, int64_t ld);
-
-// K2t: the TMA-streamed form.  One warp per CTA (one per SM: the stages take
-// ~205 KB of shared memory at dim 100).  Per 32-point tile, four 2-D tensor
-// loads (x, p, dx, dp; box {32 points, dim rows}) land in a stage; two stages
-// alternate, so the next tile's 4 x dim x 256 B are in flight while this one
-// is computed.  Forward and reverse read u = x - p from the staged x, p (the
-// same bits as K2), the reverse reads the staged dx, dp and writes the
-// updated rows with ordinary coalesced stores (fire and forget, so the stage
-// can be refilled at once).  Full tiles only; the caller runs the tail.
-// Measured (variant 14, 10M x 100): 8.71 ms = 5.5 TB/s, below K2v's 7.95 ms:
-// one warp per SM cannot issue the stores and the FP64 chain fast enough.
-// Kept as the experiment it is; K2v is the auto choice.
-__global__ void __launch_bounds__(32) gaussnd_tma_kernel(
-    const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tp,
-    const __grid_constant__ CUtensorMap tdx, const __grid_constant__ CUtensorMap tdp,
-    double* __restrict__ dx, double* __restrict__ dp, int64_t ntiles, int dim, int64_t ld,
-    double t4, double r1) {
-  extern __shared__ __align__(128) double smem[];
-  const size_t tile_d = (size_t)dim * 32;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 8 * tile_d);  // [2]
-  const int lane = threadIdx.x;
-  if (lane == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  const uint32_t tile_bytes = (uint32_t)dim * 256u;
-  auto issue = [&](int64_t tile, int st) {
-    if (lane == 0) {
-      double* base = smem + (size_t)st * 4 * tile_d;
-      mbar_arrive_expect_tx(&bar[st], 4 * tile_bytes);
-      const CUtensorMap* maps[4] = {&tx, &tp, &tdx, &tdp};
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-        asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-            "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(base + a * tile_d)),
-            "l"(reinterpret_cast<uint64_t>(maps[a])), "r"((int)(tile * 32)), "r"(0),
-            "r"(smem_u32(&bar[st]))
-            : "memory");
-    }
-  };
-  uint32_t phase[2] = {0u, 0u};
-  int64_t tile = blockIdx.x;
-  if (tile < ntiles) issue(tile, 0);
-  if (tile + gridDim.x < ntiles) issue(tile + gridDim.x, 1);
-  for (int k = 0; tile < ntiles; tile += gridDim.x, ++k) {
-    const int st = k & 1;
-    const double* bx = smem + (size_t)st * 4 * tile_d;
-    const double* bp = bx + tile_d;
-    const double* bdx = bp + tile_d;
-    const double* bdp = bdx + tile_d;
-    mbar_wait(&bar[st], phase[st]);
-    phase[st] ^= 1u;
-    double t = 0.0;
-    for (int d = 0; d < dim; ++d) {
-      const double u = fsub(bx[d * 32 + lane], bp[d * 32 + lane]);  // _t0 = x[i] - p[i]
-      t = fadd(t, fmul(u, u));                                     // t = t + _t1
-    }
-    const double tt = fdiv(-t, t4);
-    const double e = exp(tt);
-    const double r2 = fadd(0.0, fmul(r1, e));
-    const double r3 = fadd(0.0, fdiv(r2, t4));
-    const double c = fadd(0.0, -r3);
-    const int64_t i = tile * 32 + lane;
-#pragma unroll 4
-    for (int d = dim - 1; d >= 0; --d) {
-      const double u = fsub(bx[d * 32 + lane], bp[d * 32 + lane]);
-      const double r6 = fadd(fadd(0.0, fmul(c, u)), fmul(u, c));
-      const int64_t o = (int64_t)d * ld + i;
-      dx[o] = fadd(bdx[d * 32 + lane], r6);   // _d_x[_i0] += _r6
-      dp[o] = fadd(bdp[d * 32 + lane], -r6);  // _d_p[_i0] += -_r6
-    }
-    __syncwarp();  // every lane is done with the stage before it is refilled
-    if (tile + 2 * (int64_t)gridDim.x < ntiles) issue(tile + 2 * (int64_t)gridDim.x, st);
-  }
-}
 
 // K2v: two points per lane with 16-byte (double2) accesses — a warp covers a
 // 64-point tile, each row access is one 512-byte segment.  Same per-point
@@ -446,29 +350,33 @@ __global__ void __launch_bounds__(32) gaussnd_vec2_kernel(
 }
 
 // ---------------------------------------------------------------------------
-// 0 auto (K2v below 105 dims when aligned, else K2 as chosen by choose(),
-// with 8 tiles per CTA where W = 1 and the stages fit);
-// 10-13 = K2v (U = 16 / 16 with a 104 KB stage / 8 / 32);
-// 1/3/4 = one warp per 32-point tile (reference summation order) with
-// 8/16/32 rows in flight per thread (+ L2 prefetch of the next batch);
-// 5 = as 3 without prefetch; 6 = as 3 with bulk (TMA-unit) prefetch;
-// 2 = dims split over the warps of a CTA (7 = same with bulk prefetch);
-// 8 = as 3 prefetching two batches ahead, 9 = U=8 prefetching three ahead;
-// 15 = clusters of 2 CTAs x 16 warps sharing each tile (dims over 32 warps);
-// 16 / 17 = as 3 with 4 / 8 neighbouring tiles per CTA in step (one per warp),
-// 18 = as 1 (U = 8) with 8 tiles per CTA.
-static int g_variant = 0;
+// Kernel selection.  The variant is an argument of every launch (never a
+// process-wide setting, so concurrent callers cannot reroute each other):
+//   0  auto — K2v below 105 dims on a 16-byte-aligned even-ld layout (the
+//      last partial 64-point tile through K2 W = 1), else K2 as choose()
+//      picks it: W = 1 with 8 neighbouring tiles per CTA up to 112 dims,
+//      dims over the warps of a CTA above;
+//   3  K2 with one warp per 32-point tile (the reference summation order;
+//      the tail form of K2v);
+//   2  K2 with the dims split over the warps of a CTA (W = 8 / 16);
+//   10 K2v (where the layout allows it; the rest through variant 3).
+// The forced forms exist for the parity tests, which check that every kernel
+// auto can pick gives the same per-point bits (W = 1 forms) or stays within
+// the regrouping tolerance (W > 1).  Measured alternatives that were not
+// kept (TMA-streamed tiles, 2-CTA clusters, deeper prefetch, other row
+// batches) are described in DESIGN.md §3.
+static thread_local int t_variant = 0;  // test override (adc_cuda_gaussnd_set_variant)
 
 struct NdConfig {
-  int w, u, dpw, dstage, blocks_per_sm;
+  int w, u, dpw, dstage;
   size_t smem;
 };
 
-template <int W, int U, int PF = 1, int PFD = 1, int TPC = 1>
+template <int W, int U, int PF = 1, int TPC = 1>
 static int launch_tile(const NdConfig& c, int64_t n, int dim, int64_t ld, const double* x,
                        const double* p, double* dx, double* dp, double t4, double r1,
                        cudaStream_t s) {
-  auto k = gaussnd_tile_kernel<W, U, PF, PFD, 1, TPC>;
+  auto k = gaussnd_tile_kernel<W, U, PF, TPC>;
   const size_t smem = TPC > 1 ? ((size_t)TPC * 32 + (size_t)TPC * c.dstage * 32) * sizeof(double)
                               : c.smem;
   if (smem > 48 * 1024)
@@ -483,46 +391,14 @@ static int launch_tile(const NdConfig& c, int64_t n, int dim, int64_t ld, const 
   return ADC_OK;
 }
 
-// Cluster form: CL CTAs of W warps (one CTA per SM) share each 32-point tile,
-// so the whole u row of a tile is staged over CL SMs' shared memory.
-template <int W, int U, int PF, int CL>
-static int launch_tile_cluster(const NdConfig& c, int64_t n, int dim, int64_t ld, const double* x,
-                               const double* p, double* dx, double* dp, double t4, double r1,
-                               cudaStream_t s) {
-  auto k = gaussnd_tile_kernel<W, U, PF, 1, CL>;
-  ADCB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem));
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3(W * 32);
-  cfg.dynamicSmemBytes = c.smem;
-  cfg.stream = s;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cfg.gridDim = dim3((unsigned)(CL * sm_count()));
-  int clusters = 0;
-  ADCB_CUDA(cudaOccupancyMaxActiveClusters(&clusters, k, &cfg));
-  if (clusters < 1) return fail(ADC_E_LAUNCH, "gaussnd: cluster configuration does not fit");
-  const int64_t ntiles = (n + 31) / 32;
-  cfg.gridDim = dim3((unsigned)(CL * std::min<int64_t>(ntiles, clusters)));
-  ADCB_CUDA(cudaLaunchKernelEx(&cfg, k, x, p, dx, dp, n, dim, ld, t4, r1, c.dpw, c.dstage));
-  return ADC_OK;
-}
-
 // Shared-memory budget per SM usable by the stage buffers.
 static constexpr size_t kSmemPerSm = 224 * 1024;
 
-static NdConfig choose(int dim) {
+static NdConfig choose(int dim, int variant) {
   NdConfig c{};
-  const int variant = g_variant;
   // W = 1 keeps the reference's summation order; it needs the whole u row of
   // a point on chip: 256 B per dim per warp.  Use it while >= 8 warps fit.
-  if (variant == 1 || variant == 3 || variant == 4 || variant == 5 || variant == 6 ||
-      variant == 8 || variant == 9 || variant == 16 || variant == 17 || variant == 18 ||
-      (variant == 0 && (size_t)dim * 256 * 8 <= kSmemPerSm)) {
+  if (variant == 3 || (variant != 2 && (size_t)dim * 256 * 8 <= kSmemPerSm)) {
     c.w = 1;
     c.dpw = dim;
     c.dstage = dim;
@@ -535,14 +411,13 @@ static NdConfig choose(int dim) {
     const size_t avail = per_cta - (size_t)c.w * 32 * 8 - 1024;
     c.dstage = std::min<int>(c.dpw, (int)(avail / ((size_t)c.w * 256)));
   }
-  c.u = (variant == 1 || variant == 9 || variant == 18) ? 8 : variant == 4 ? 32 : 16;
-  if (c.w > 1) c.u = 8;
+  c.u = c.w > 1 ? 8 : 16;
   c.smem = ((size_t)c.w * 32 + (size_t)c.w * c.dstage * 32) * sizeof(double);
   return c;
 }
 
-int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, const double* p,
-                        double sigma, double* dx, double* dp, cudaStream_t s) {
+static int launch_gaussnd_v(int64_t n, int64_t dim, int64_t ld, const double* x, const double* p,
+                            double sigma, double* dx, double* dp, cudaStream_t s, int variant) {
   const double PI = 3.14159265358979323846;
   const double t3 = 2 * sigma;
   const double t4 = t3 * sigma;
@@ -553,49 +428,20 @@ int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, con
   if (dim > (1 << 24)) return fail(ADC_E_ARG, "gaussnd: dim too large");
   double d_t9 = 0;
   d_t9 += (std::pow(2 * PI, -0.5) * std::pow(sigma, -0.5)) * 1.0;  // _d__t9 += _t8 * _r0
-  if (g_variant == 14) {  // experiment: K2t (TMA-streamed tiles)
-    const int64_t ntiles = n / 32;
-    const size_t smem = (size_t)dim * 32 * 8 * sizeof(double) + 2 * sizeof(uint64_t);
-    const bool ok = ld % 2 == 0 && ((((uintptr_t)x) | ((uintptr_t)p) | ((uintptr_t)dx) |
-                                     ((uintptr_t)dp)) & 15) == 0 && dim <= 104 &&
-                    smem <= 227 * 1024;
-    CUtensorMap mx, mp, mdx, mdp;
-    if (ok && ntiles > 0 && make_rows_tmap(&mx, x, ntiles * 32, dim, ld) == ADC_OK &&
-        make_rows_tmap(&mp, p, ntiles * 32, dim, ld) == ADC_OK &&
-        make_rows_tmap(&mdx, dx, ntiles * 32, dim, ld) == ADC_OK &&
-        make_rows_tmap(&mdp, dp, ntiles * 32, dim, ld) == ADC_OK) {
-      ADCB_CUDA(cudaFuncSetAttribute(gaussnd_tma_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      const int64_t blocks = std::min<int64_t>(ntiles, (int64_t)sm_count());
-      gaussnd_tma_kernel<<<(unsigned)blocks, 32, smem, s>>>(mx, mp, mdx, mdp, dx, dp, ntiles,
-                                                           (int)dim, ld, t4, d_t9);
-      ADCB_CUDA(cudaGetLastError());
-      const int64_t done = ntiles * 32;
-      if (done == n) return ADC_OK;
-      g_variant = 3;
-      const int rc = launch_gaussnd_grad(n - done, dim, ld, x + done, p + done, sigma, dx + done,
-                                         dp + done, s);
-      g_variant = 14;
-      return rc;
-    }
-  }
-  // Auto: K2v for dims whose u rows all fit its 52 KB stage (the dim-100
-  // headline: 6.0 TB/s vs 5.8 for K2, the same bits per point).
-  const bool vec2_auto = g_variant == 0 && dim <= 104;
-  if (vec2_auto || (g_variant >= 10 && g_variant <= 13)) {
+  // K2v for dims whose u rows all fit its 52 KB stage (the dim-100 headline:
+  // 6.0 TB/s vs 5.8 for K2, the same bits per point).
+  if ((variant == 0 && dim <= 104) || variant == 10) {
     const int64_t ntiles = n / 64;
     const bool ok = ld % 2 == 0 && ((((uintptr_t)x) | ((uintptr_t)p) | ((uintptr_t)dx) |
                                      ((uintptr_t)dp)) & 15) == 0;
     if (ok && ntiles > 0) {
-      size_t budget = g_variant == 11 ? 104 * 1024 : 52 * 1024;
-      if (const char* e = getenv("ADC_K2V_STAGE_KB")) budget = (size_t)atoi(e) * 1024;  // experiment
+      const size_t budget = 52 * 1024;
       const int dstage = (int)std::min<int64_t>(dim, budget / 512);
       const size_t smem = (size_t)dstage * 512;
-      // auto: the row batch no longer than the dims (U = 16 never batches below 16)
-      auto k = g_variant == 0 && dim < 4   ? gaussnd_vec2_kernel<2>
-             : g_variant == 0 && dim < 8   ? gaussnd_vec2_kernel<4>
-             : g_variant == 12 || (g_variant == 0 && dim < 16) ? gaussnd_vec2_kernel<8>
-             : g_variant == 13 ? gaussnd_vec2_kernel<32> : gaussnd_vec2_kernel<16>;
+      // the row batch no longer than the dims (U = 16 never batches below 16)
+      auto k = dim < 4 ? gaussnd_vec2_kernel<2>
+             : dim < 8 ? gaussnd_vec2_kernel<4>
+             : dim < 16 ? gaussnd_vec2_kernel<8> : gaussnd_vec2_kernel<16>;
       if (smem > 48 * 1024)
         ADCB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       int occ = 0;
@@ -606,68 +452,41 @@ int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, con
       const int64_t done = ntiles * 64;
       if (done == n) return ADC_OK;
       // the last partial tile through K2 (W = 1 for these dims: same per-point bits)
-      const int saved = g_variant;
-      g_variant = 3;
-      const int rc = launch_gaussnd_grad(n - done, dim, ld, x + done, p + done, sigma, dx + done,
-                                         dp + done, s);
-      g_variant = saved;
-      return rc;
+      return launch_gaussnd_v(n - done, dim, ld, x + done, p + done, sigma, dx + done, dp + done,
+                              s, 3);
     }
   }
-  if (g_variant == 15) {  // cluster of 2 CTAs x 16 warps per tile
-    NdConfig c{};
-    c.w = 16;
-    c.u = 8;
-    c.dpw = (int)((dim + 31) / 32);
-    const size_t avail = kSmemPerSm - (size_t)c.w * 32 * 8 - 1024;
-    c.dstage = std::min<int>(c.dpw, (int)(avail / ((size_t)c.w * 256)));
-    c.smem = ((size_t)c.w * 32 + (size_t)c.w * c.dstage * 32) * sizeof(double);
-    return launch_tile_cluster<16, 8, 2, 2>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
+  const NdConfig c = choose((int)dim, variant);
+  const int di = (int)dim;
+  if (c.w == 1) {
+    // Auto: 8 neighbouring tiles per CTA from 2 dims while the stages fit one
+    // CTA, with a row batch no longer than the dims: same bits as one warp
+    // per CTA, 3-19% faster (10M x 100: 7.93 vs 8.29 ms aligned, 10.1 vs
+    // 12.0 ms with odd n) and 2x at dim 8 (U = 16 never batches).
+    const bool fits = (size_t)8 * 32 * 8 + (size_t)8 * c.dstage * 256 <= 227 * 1024;
+    if (variant == 0 && fits) {
+      if (dim >= 16) return launch_tile<1, 16, 1, 8>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s);
+      if (dim >= 8) return launch_tile<1, 8, 1, 8>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s);
+      if (dim >= 4) return launch_tile<1, 4, 1, 8>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s);
+      if (dim >= 2) return launch_tile<1, 2, 1, 8>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s);
+    }
+    return launch_tile<1, 16>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s);
   }
-  NdConfig c = choose((int)dim);
-  switch (c.w) {
-    case 1:
-      if (g_variant == 16)
-        return launch_tile<1, 16, 1, 1, 4>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
-      // Auto: 8 neighbouring tiles per CTA for 8 <= dim <= 112 (the stages
-      // fit one CTA), with a row batch no longer than the dims: same bits as
-      // one warp per CTA, 3-19% faster (10M x 100: 7.93 vs 8.29 ms aligned,
-      // 10.1 vs 12.0 ms with odd n) and 2x at dim 8 (U = 16 never batches).
-      {
-        const bool fits = (size_t)8 * 32 * 8 + (size_t)8 * c.dstage * 256 <= 227 * 1024;
-        if (g_variant == 17 || (g_variant == 0 && dim >= 16 && fits))
-          return launch_tile<1, 16, 1, 1, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
-        if (g_variant == 18 || (g_variant == 0 && dim >= 8 && fits))
-          return launch_tile<1, 8, 1, 1, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
-        if (g_variant == 0 && dim >= 4 && fits)
-          return launch_tile<1, 4, 1, 1, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
-        if (g_variant == 0 && dim >= 2 && fits)
-          return launch_tile<1, 2, 1, 1, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
-      }
-      if (c.u == 8) return launch_tile<1, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
-      if (c.u == 32) return launch_tile<1, 32>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
-      if (g_variant == 5)
-        return launch_tile<1, 16, 0>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
-      if (g_variant == 6)
-        return launch_tile<1, 16, 2>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
-      if (g_variant == 8)
-        return launch_tile<1, 16, 1, 2>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
-      if (g_variant == 9)
-        return launch_tile<1, 8, 1, 3>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
-      return launch_tile<1, 16>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
-    case 8: return launch_tile<8, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
-    case 16:
-      // bulk (TMA-unit) L2 prefetch of the next rows: 2.4% faster at dim 1000
-      // (8.24 vs 8.45 ms, same bits); variant 2 keeps the per-lane prefetch
-      if (g_variant == 2) return launch_tile<16, 8>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
-      return launch_tile<16, 8, 2>(c, n, (int)dim, ld, x, p, dx, dp, t4, d_t9, s);
-  }
-  return fail(ADC_E_ARG, "gaussnd: bad configuration");
+  // bulk (TMA-unit) L2 prefetch of the next rows: 2.4% faster at dim 1000
+  // (8.24 vs 8.45 ms, same bits)
+  if (c.w == 16) return launch_tile<16, 8, 2>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s);
+  return launch_tile<8, 8>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s);
+}
+
+int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, const double* p,
+                        double sigma, double* dx, double* dp, cudaStream_t s) {
+  return launch_gaussnd_v(n, dim, ld, x, p, sigma, dx, dp, s, t_variant);
 }
 
 int gaussnd_set_variant(int v) {
-  if (v < 0 || v > 18) return fail(ADC_E_ARG, "gaussnd variant must be 0..18");
-  g_variant = v;
+  if (v != 0 && v != 2 && v != 3 && v != 10)
+    return fail(ADC_E_ARG, "gaussnd variant must be 0 (auto), 2, 3 or 10");
+  t_variant = v;
   return ADC_OK;
 }
 
@@ -1108,10 +927,8 @@ int launch_gaussnd_shared_p(int64_t n, int64_t dim, int64_t ld, const double* x,
   if (dim > (1 << 20)) return fail(ADC_E_ARG, "gaussnd: dim too large");
   double d_t9 = 0;
   d_t9 += (std::pow(2 * PI, -0.5) * std::pow(sigma, -0.5)) * 1.0;
-  // stage as many dims of u as fit next to dp's partials (<= 26 KB: 8 CTAs/SM);
-  // ADC_SHAREDP_STAGE=0 re-reads x (L2) instead (experiment knob)
-  size_t budget = 26 * 1024 + 1024;
-  if (const char* e = getenv("ADC_SHAREDP_STAGE")) budget = (size_t)atoll(e);
+  // stage as many dims of u as fit next to dp's partials (<= 26 KB: 8 CTAs/SM)
+  const size_t budget = 26 * 1024 + 1024;
   const size_t fixed = (size_t)dim * sizeof(double);
   int dstage = fixed >= budget ? 0 : (int)std::min<int64_t>(dim, (budget - fixed) / 256);
   const size_t smem = fixed + (size_t)dstage * 256;
@@ -1136,14 +953,12 @@ int launch_gaussnd_shared_p(int64_t n, int64_t dim, int64_t ld, const double* x,
   // The TMA kernel serves the dp-only form (x streamed by 2-D tensor loads,
   // 4.5 TB/s at 10M x 100); with private dx slots the per-point RMW wants
   // more warps in flight than its stage buffers allow, so K2s<32, 8> runs.
-  const bool tma = (getenv("ADC_SHAREDP_TMA") ? atoi(getenv("ADC_SHAREDP_TMA")) != 0 : true) &&
-                   dx == nullptr && ld % 2 == 0 && ((uintptr_t)x & 15) == 0 && dim <= 256 &&
+  const bool tma = dx == nullptr && ld % 2 == 0 && ((uintptr_t)x & 15) == 0 && dim <= 256 &&
                    tma_smem <= 200 * 1024;
   // K2sv (double2 rows, 64-point tiles) when the layout allows it: the full
   // 64-point tiles over kSharedPVecBlocks CTAs, the < 64 remaining points as
   // one more block of partials (K2s), then the fixed-order total.
-  const bool vec = (getenv("ADC_SHAREDP_VEC") ? atoi(getenv("ADC_SHAREDP_VEC")) != 0 : dx != nullptr) &&
-                   ld % 2 == 0 && ((((uintptr_t)x) | ((uintptr_t)dx)) & 15) == 0 && dim <= 128 &&
+  const bool vec = dx != nullptr && ld % 2 == 0 && ((((uintptr_t)x) | ((uintptr_t)dx)) & 15) == 0 && dim <= 128 &&
                    n >= 64;
   if (vec) {
     const int64_t full64 = n / 64, rem64 = n % 64;

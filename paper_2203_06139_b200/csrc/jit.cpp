@@ -21,7 +21,8 @@
 //  * the value / control tapes (__push, __pop, __push_ctl, __pop_ctl) are
 //    per call frame, as in the interpreter (eval.cpp:312-319), held in a
 //    thread-private array of the chosen capacity.
-// Integer overflow checks of the interpreter are not replicated.
+//  * int64 overflow of + - * (binary, unary minus, +=) raises the
+//    interpreter's 'integer overflow' Eval error (eval.cpp:601-628).
 //
 // Hazards: a whole real[] kernel parameter that is written (directly at an
 // index other than the thread index, or through a callee's writes) is a
@@ -1193,7 +1194,6 @@ int emit_and_compile(const Module& m, const Fn* k, const std::string& kernel, bo
                      int tape_capacity, bool count, std::string& cuda, std::vector<char>& cubin) {
   Emitter em{m, unsafe, tape_capacity};
   em.count = count;
-  if (const char* e = getenv("ADC_JIT_PREFETCH")) em.prefetch = atoi(e) != 0;  // experiment knob
   try {
     em.prelude();
     for (auto& f : m.fns)
@@ -1222,9 +1222,8 @@ int emit_and_compile(const Module& m, const Fn* k, const std::string& kernel, bo
       }
     };
     for (size_t w = 0; w < work.size(); ++w) scan(work[w]->body);
-    if (!(getenv("ADC_JIT_SLOTCACHE") && atoi(getenv("ADC_JIT_SLOTCACHE")) == 0))
-      for (auto& f : m.fns)
-        if (reach.count(f.name)) em.analyse_cacheable(f);
+    for (auto& f : m.fns)
+      if (reach.count(f.name)) em.analyse_cacheable(f);
     // callees first, so a cached variant is declared before its call sites
     for (auto& f : m.fns)
       if (reach.count(f.name) && !f.global) em.function(f);

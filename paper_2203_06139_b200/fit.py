@@ -51,6 +51,7 @@ class FitOptions:
     armijo_c1: float = 1e-4
     use_hessian: bool = False
     trace_iterates: int = 0
+    host_loop: bool = False  # B200 option: host-driven loop instead of the device-resident one
 
 
 @dataclass
@@ -233,13 +234,35 @@ class FitEngine:
         self.model, self.np, self.comm = model, np_, comm
         self._plans = {}
 
+    @staticmethod
+    def _state(h: Histogram):
+        """What a plan snapshots of a histogram: the reference's FitEngine reads
+        h.counts and h.events on every call, so a change of any of them (a
+        reassigned field, or an in-place write to a torch counts tensor, seen
+        through its version counter) rebuilds the plan.  Host (numpy) counts
+        are made read-only while a plan holds their snapshot, so an in-place
+        write raises instead of being silently ignored."""
+        c = h.counts
+        if hasattr(c, "is_cuda"):
+            cs = ("torch", c.data_ptr(), int(c._version), tuple(c.shape))
+        else:
+            cs = ("numpy", id(c), c.__array_interface__["data"][0], c.shape)
+        return (h.bins, float(h.lo), float(h.hi), float(h.events), cs)
+
     def _plan(self, h: Histogram) -> Chi2Plan:
         key = id(h)
-        pl = self._plans.get(key)
-        if pl is None or pl.h is not h:
+        st = self._state(h)
+        ent = self._plans.get(key)
+        if ent is None or ent[0].h is not h or ent[1] != st:
+            if ent is not None:
+                ent[0].close()
             pl = Chi2Plan(self.model, self.np, h, comm=self.comm)
-            self._plans = {key: pl}
-        return pl
+            c = h.counts
+            if not hasattr(c, "is_cuda") and isinstance(c, np.ndarray):
+                c.flags.writeable = False
+            self._plans = {key: (pl, st)}
+            return pl
+        return ent[0]
 
     def gradient_fn_name(self) -> str:
         return f"{self.model}_grad_1"
@@ -261,7 +284,8 @@ class FitEngine:
         pl = self._plan(h)
         pl.set_provider(provider)
         o = _FitOptionsC(opts.budget, opts.grad_tol, opts.chi2_rel_tol, opts.sigma_min,
-                         opts.armijo_c1, opts.trace_iterates, 1 if opts.use_hessian else 0)
+                         opts.armijo_c1, opts.trace_iterates, 1 if opts.use_hessian else 0,
+                         1 if opts.host_loop else 0)
         idx = default_clamp(self.model, self.np) if clamp is None else list(clamp)
         cidx = (ctypes.c_int32 * max(1, len(idx)))(*idx)
         params = np.ascontiguousarray(init, dtype=np.float64).copy()

@@ -113,8 +113,81 @@ def registry_find(name: str, fingerprint: int) -> int:
     return kid.value
 
 
+def printed_function(module: str, fn: str) -> str:
+    """The text of function `fn` as adc::print emits it, cut out of a printed
+    module (functions are separated by one blank line)."""
+    for head in ("device host void ", "device host real ", "host void ", "device void "):
+        i = module.find(head + fn + "(")
+        if i >= 0:
+            break
+    else:
+        raise AdcError("Launch", f"function '{fn}' not found in the module text")
+    k = module.find("\n}\n", i)
+    if k < 0:
+        raise AdcError("Launch", f"function '{fn}' is not terminated in the module text")
+    return module[i:k + 3]
+
+
+def fingerprint_of(text: str) -> int:
+    """FNV-1a-64 of a printed generated gradient: the registry key the
+    reference-side bridge computes from adc::print(FunctionDef)."""
+    b = text.encode()
+    return int(lib.adc_cuda_fingerprint(b, len(b)))
+
+
+def _callee_fingerprint(callee: str, fingerprint: int | None, module: str | None) -> int:
+    """Registry key of the called gradient.  With the Program's printed text
+    (`module`), the fingerprint is computed from the gradient actually printed
+    there, so a changed generator output is a registry miss (an
+    Error(Launch)), as in the reference-side bridge.  Without it the caller
+    vouches for the gradient by name and the registry's own fingerprint is
+    used."""
+    if fingerprint is not None:
+        return fingerprint
+    if module is not None:
+        return fingerprint_of(printed_function(module, callee))
+    return _fingerprints()[callee]
+
+
 def _is_torch(a) -> bool:
     return hasattr(a, "is_cuda")
+
+
+def _check_residency(arrays, what="buffers"):
+    """All device buffers are float64 CUDA tensors on ONE device, or all are
+    host float64 arrays: a host pointer never reaches a kernel."""
+    arrays = [a for a in arrays if a is not None]
+    dev = {_is_torch(a) and a.is_cuda for a in arrays}
+    if len(dev) != 1:
+        raise AdcError("Launch", f"{what}: mix of device (CUDA tensor) and host buffers")
+    if dev.pop():
+        devices = {a.device for a in arrays}
+        if len(devices) != 1:
+            raise AdcError("Launch", f"{what}: CUDA tensors on different devices {sorted(map(str, devices))}")
+        return next(iter(devices))
+    for a in arrays:
+        if _is_torch(a):
+            raise AdcError("Launch", f"{what}: CPU torch tensors are not accepted; pass numpy arrays")
+    return None
+
+
+class _on_device:
+    """Runs the C call with the buffers' device current (the C ABI launches on
+    the calling thread's current device)."""
+
+    def __init__(self, device):
+        self.device = device
+        self.ctx = None
+
+    def __enter__(self):
+        if self.device is not None:
+            import torch
+            self.ctx = torch.cuda.device(self.device)
+            self.ctx.__enter__()
+
+    def __exit__(self, *a):
+        if self.ctx is not None:
+            self.ctx.__exit__(*a)
 
 
 def _stream_of(a):
@@ -124,7 +197,8 @@ def _stream_of(a):
 
 def launch(kernel: str, cfg: LaunchConfig, buffers: BufferSet,
            opts: LaunchOptions | None = None, callee_fingerprint: int | None = None,
-           module: str | None = None, counts: bool = False, comm=None) -> LaunchStats:
+           module: str | None = None, counts: bool = False, comm=None,
+           devices=None) -> LaunchStats:
     """adc::launch (launch.cpp:252-346) for the Listing-1 kernels of kernels.dsl:
     `compute` (private slots) and `compute_shared` (the shared dsigma slot:
     refused unless opts.unsafe, then reduced in a fixed order, deterministic),
@@ -132,7 +206,9 @@ def launch(kernel: str, cfg: LaunchConfig, buffers: BufferSet,
     adc::print emits it), any other global kernel goes through the generic
     JIT (jit.py).  `compute_shared` with `comm` (device buffers): each rank
     launches over its own points and the dsigma partials are summed over
-    ranks in rank order (the same dsigma on every rank)."""
+    ranks in rank order (the same dsigma on every rank).  `compute` with host
+    buffers and `devices` (device ordinals): the points are split over those
+    GPUs, one host thread each (adc_cuda_compute_gauss_host_mg)."""
     opts = opts or LaunchOptions()
     if module is not None and kernel not in ("compute", "compute_shared"):
         from .jit import launch_module
@@ -148,8 +224,7 @@ def launch(kernel: str, cfg: LaunchConfig, buffers: BufferSet,
     elif kernel != "compute":
         raise AdcError("Launch", f"unknown kernel '{kernel}'")
     callee = "gauss_grad" if shared else "gauss_grad_0_1"
-    fp = _fingerprints()[callee] if callee_fingerprint is None else callee_fingerprint
-    registry_find(callee, fp)
+    registry_find(callee, _callee_fingerprint(callee, callee_fingerprint, module))
     arrs = {}
     for name, typ in COMPUTE_PARAMS:
         if typ == "real[]":
@@ -165,6 +240,7 @@ def launch(kernel: str, cfg: LaunchConfig, buffers: BufferSet,
             raise AdcError("Launch", f"missing scalar value '{name}'")
     sigma = float(buffers.scalars["sigma"])
     x, p, dx, dp = (arrs[k] for k in ("x", "p", "dx", "dp"))
+    device = _check_residency((x, p, dx, dp) + ((buffers.arrays.get("dsigma"),) if shared else ()))
     for a in (x, p, dx, dp):
         if _is_torch(x):
             if not (_is_torch(a) and a.is_cuda and a.is_contiguous()) or \
@@ -172,6 +248,11 @@ def launch(kernel: str, cfg: LaunchConfig, buffers: BufferSet,
                 raise AdcError("Launch", "device buffers must be contiguous float64 CUDA tensors")
         elif _is_torch(a) or a.dtype != np.float64 or not a.flags.c_contiguous:
             raise AdcError("Launch", "host buffers must be contiguous float64 arrays")
+    with _on_device(device):
+        return _launch_compute(cfg, buffers, shared, x, p, dx, dp, sigma, comm, devices)
+
+
+def _launch_compute(cfg, buffers, shared, x, p, dx, dp, sigma, comm, devices):
     if shared:
         if "dsigma" not in buffers.arrays:
             raise AdcError("Launch", "missing buffer 'dsigma'")
@@ -196,6 +277,12 @@ def launch(kernel: str, cfg: LaunchConfig, buffers: BufferSet,
     if _is_torch(x):
         check(lib.adc_cuda_compute_gauss(cfg.grid_dim, cfg.block_dim, cfg.n, dptr(x), dptr(p),
                                          sigma, dptr(dx), dptr(dp), _stream_of(x)))
+    elif devices is not None:
+        import ctypes
+        devs = (ctypes.c_int32 * len(devices))(*devices)
+        check(lib.adc_cuda_compute_gauss_host_mg(len(devices), devs, cfg.grid_dim, cfg.block_dim,
+                                                 cfg.n, dptr(x), dptr(p), sigma, dptr(dx),
+                                                 dptr(dp)))
     else:
         check(lib.adc_cuda_compute_gauss_host(cfg.grid_dim, cfg.block_dim, cfg.n, dptr(x),
                                               dptr(p), sigma, dptr(dx), dptr(dp)))
@@ -227,27 +314,44 @@ def _soa_ld(arrays, ld):
 
 
 def launch_batch(grad_fn: str, x, p, sigma: float, dx, dp, ld: int | None = None,
-                 callee_fingerprint: int | None = None):
+                 callee_fingerprint: int | None = None, module: str | None = None,
+                 devices=None):
     """Batched per-point gradient over structure-of-arrays buffers of shape
     (dim, n): gaussnd_grad_0_1(x[:, i], p[:, i], sigma, dim, dx[:, i], dp[:, i])
-    for every point i, accumulating into dx, dp."""
+    for every point i, accumulating into dx, dp.  Host buffers with `devices`
+    (a list of device ordinals): the points are split over those GPUs, one
+    host thread each (adc_cuda_gaussnd_grad_host_mg), the same bits as one
+    device."""
     if grad_fn != "gaussnd_grad_0_1":
         raise AdcError("Launch", f"no B200 kernel registered for '{grad_fn}'")
-    fp = _fingerprints()[grad_fn] if callee_fingerprint is None else callee_fingerprint
-    registry_find(grad_fn, fp)
+    registry_find(grad_fn, _callee_fingerprint(grad_fn, callee_fingerprint, module))
+    device = _check_residency((x, p, dx, dp))
+    if len(x.shape) != 2:
+        raise AdcError("Launch", "SoA buffers must be float64 (dim, n) with unit point stride")
     dim, n = x.shape
+    for name, a in (("p", p), ("dx", dx), ("dp", dp)):
+        if tuple(a.shape) != (dim, n):  # launch.cpp:279-284: no buffer may be shorter
+            raise AdcError("Launch", f"buffer '{name}' has shape {tuple(a.shape)} but the points are "
+                                     f"x's ({dim}, {n})")
     ld = _soa_ld((x, p, dx, dp), ld)
-    if _is_torch(x):
-        check(lib.adc_cuda_gaussnd_grad(n, dim, ld, dptr(x), dptr(p), float(sigma), dptr(dx),
-                                        dptr(dp), _stream_of(x)))
-    else:
-        check(lib.adc_cuda_gaussnd_grad_host(n, dim, ld, dptr(x), dptr(p), float(sigma), dptr(dx),
-                                             dptr(dp)))
+    with _on_device(device):
+        if device is not None:
+            check(lib.adc_cuda_gaussnd_grad(n, dim, ld, dptr(x), dptr(p), float(sigma), dptr(dx),
+                                            dptr(dp), _stream_of(x)))
+        elif devices is not None:
+            import ctypes
+            devs = (ctypes.c_int32 * len(devices))(*devices)
+            check(lib.adc_cuda_gaussnd_grad_host_mg(len(devices), devs, n, dim, ld, dptr(x),
+                                                    dptr(p), float(sigma), dptr(dx), dptr(dp)))
+        else:
+            check(lib.adc_cuda_gaussnd_grad_host(n, dim, ld, dptr(x), dptr(p), float(sigma),
+                                                 dptr(dx), dptr(dp)))
 
 
 def launch_batch_shared_p(grad_fn: str, x, p, sigma: float, dx, dp,
                           opts: LaunchOptions | None = None, ld: int | None = None,
-                          callee_fingerprint: int | None = None, comm=None):
+                          callee_fingerprint: int | None = None, comm=None,
+                          module: str | None = None):
     """The shared-mean batched path: for every point i,
     gaussnd_grad_0_1(x[:, i], p, sigma, dim, dx[:, i], dp) with ONE p (dim,)
     and ONE shared slot dp (dim,) — refused as a shared-write hazard unless
@@ -258,12 +362,26 @@ def launch_batch_shared_p(grad_fn: str, x, p, sigma: float, dx, dp,
     opts = opts or LaunchOptions()
     if grad_fn != "gaussnd_grad_0_1":
         raise AdcError("Launch", f"no B200 kernel registered for '{grad_fn}'")
-    fp = _fingerprints()[grad_fn] if callee_fingerprint is None else callee_fingerprint
-    registry_find(grad_fn, fp)
-    dim, n = x.shape
+    registry_find(grad_fn, _callee_fingerprint(grad_fn, callee_fingerprint, module))
     if not _is_torch(x):
         raise AdcError("Launch", "launch_batch_shared_p takes device (CUDA tensor) buffers")
+    device = _check_residency((x, p, dx, dp))
+    if len(x.shape) != 2:
+        raise AdcError("Launch", "SoA buffers must be float64 (dim, n) with unit point stride")
+    dim, n = x.shape
+    if dx is not None and tuple(dx.shape) != (dim, n):
+        raise AdcError("Launch", f"buffer 'dx' has shape {tuple(dx.shape)} but the points are "
+                                 f"x's ({dim}, {n})")
+    for name, a in (("p", p), ("dp", dp)):
+        if str(a.dtype) != "torch.float64" or not a.is_contiguous() or a.numel() < dim:
+            raise AdcError("Launch", f"buffer '{name}' must be a contiguous float64 vector of at "
+                                     f"least dim = {dim} elements (has {a.numel()})")
     ld = _soa_ld((x, dx), ld)
+    with _on_device(device):
+        _shared_p_call(n, dim, ld, x, p, sigma, dx, dp, opts, comm)
+
+
+def _shared_p_call(n, dim, ld, x, p, sigma, dx, dp, opts, comm):
     if comm is not None:
         check(lib.adc_cuda_gaussnd_grad_shared_p_comm(
             n, dim, ld, dptr(x), dptr(p), float(sigma), dptr(dx) if dx is not None else None,

@@ -125,6 +125,46 @@ int main(int argc, char** argv) {
     rs_gaussnd_grad_batch(X.data(), P.data(), 1.3, dim, m, m, RX.data(), RP.data());
     launch_batch_gaussnd(m, dim, X, P, 1.3, DX, DP);
     EXPECT(relmax(DX, RX) <= 1e-12 && relmax(DP, RP) <= 1e-12, "launch_batch_gaussnd matches");
+    // Thread safety (the reference's launch is safe from several threads on
+    // distinct buffer sets): 4 threads, each its own buffers,
+    // each calling the host pipeline 3 times (the per-device staging lock
+    // serialises them) and the multi-GPU form; every thread's result is
+    // bit-identical to the sequential one.
+    {
+      const int T = 4;
+      std::vector<std::vector<double>> tdx(T, std::vector<double>(dim * m, 0.0)),
+          tdp(T, std::vector<double>(dim * m, 0.0));
+      std::vector<double> sdx(dim * m, 0.0), sdp(dim * m, 0.0);
+      for (int k = 0; k < 3; ++k) launch_batch_gaussnd(m, dim, X, P, 1.3, sdx, sdp);
+      launch_batch_gaussnd(m, dim, X, P, 1.3, sdx, sdp, std::vector<int32_t>{0});
+      std::vector<std::string> terr(T);
+      std::vector<std::thread> tt;
+      for (int t = 0; t < T; ++t)
+        tt.emplace_back([&, t] {
+          try {
+            for (int k = 0; k < 3; ++k) launch_batch_gaussnd(m, dim, X, P, 1.3, tdx[t], tdp[t]);
+            launch_batch_gaussnd(m, dim, X, P, 1.3, tdx[t], tdp[t], std::vector<int32_t>{0});
+          } catch (const std::exception& ex) {
+            terr[t] = ex.what();
+          }
+        });
+      for (auto& t : tt) t.join();
+      bool same = true;
+      for (int t = 0; t < T; ++t)
+        same = same && terr[t].empty() &&
+               std::memcmp(tdx[t].data(), sdx.data(), sdx.size() * sizeof(double)) == 0 &&
+               std::memcmp(tdp[t].data(), sdp.data(), sdp.size() * sizeof(double)) == 0;
+      EXPECT(same, "4 threads on distinct buffers: bitwise equal to the sequential calls");
+      ErrorKind ek{};
+      EXPECT(err([&] { launch_batch_gaussnd(m, dim, X, P, 1.3, sdx, sdp,
+                                            std::vector<int32_t>{0, 0}); }, &ek)
+                     .find("device listed twice") != std::string::npos && ek == ErrorKind::Arg,
+             "multi-GPU form: a device listed twice is Error(Arg)");
+      EXPECT(err([&] { launch_batch_gaussnd(m, dim, X, P, 1.3, sdx, sdp,
+                                            std::vector<int32_t>{0, 4096}); })
+                     .find("does not exist") != std::string::npos,
+             "multi-GPU form: a missing device is refused");
+    }
     // FitEngine gsum K=1 over a 4000-bin histogram vs the compensated oracle.
     Histogram hist;
     hist.bins = 4000;

@@ -85,6 +85,26 @@ def test_peer_comm_world1_bitwise_equals_single_device():
     assert got == ref
 
 
+def test_peer_fit_trace_grows_between_fits_on_one_plan():
+    """The device fit loop on a peer-sharded plan reallocates only its iterate
+    trace when a later fit asks for more iterates (the compact
+    all-rank record buffers stay allocated; the rebuilt graph must not point
+    at freed memory).  Each fit equals the single-device fit bit for bit."""
+    counts, ev, q, _ = _problem(bins=600_001, seed=21)
+    h1 = adc.Histogram(counts.size, -5.0, 5.0, ev, counts)
+    ref_eng = adc.FitEngine("gpoly", 6)
+    comm = adc.Comm.peer(1, 0, lambda a: a.copy())
+    h2 = adc.Histogram(counts.size, -5.0, 5.0, ev, counts.copy())
+    eng = adc.FitEngine("gpoly", 6, comm=comm)
+    for trace in (2, 10, 40, 5, 41):
+        o = adc.FitOptions(budget=40, trace_iterates=trace)
+        a, b = ref_eng.fit(h1, q, o), eng.fit(h2, q, o)
+        assert np.array(a.params).tobytes() == np.array(b.params).tobytes(), trace
+        assert np.array(a.iterates).tobytes() == np.array(b.iterates).tobytes(), trace
+        assert a.chi2 == b.chi2 and a.iterations == b.iterations
+    comm.close()
+
+
 def test_host_comm_world1_identity():
     counts, ev, q, qs = _problem(bins=700_001, seed=8)
     ref = _single_device(counts, ev, q, qs)

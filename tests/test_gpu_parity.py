@@ -114,7 +114,7 @@ def test_listing1_domain_error():
 ND_KEYS = ["d100_n64", "d1000_n8", "d1_n33", "d37_n70", "d128_n40", "d129_n5"]
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13])
+@pytest.mark.parametrize("variant", [0, 2, 3, 10])
 @pytest.mark.parametrize("key", ND_KEYS)
 def test_gaussnd_golden(key, variant):
     g = golden("gaussnd_cases.npz")
@@ -144,12 +144,13 @@ def test_gaussnd_host_path():
                                    (6, 640), (8, 1001), (12, 777), (16, 3000), (110, 513)])
 def test_gaussnd_vs_oracle(restate, dim, n):
     # variant 0 = auto (K2v with double2 for dim <= 104 on even ld, tail via K2;
-    # the row batch U follows the dims; K2 runs 8 neighbouring tiles per CTA),
-    # 15 = 2-CTA clusters, 17 / 18 = 8 tiles per CTA with U = 16 / 8
+    # the row batch U follows the dims; K2 runs 8 neighbouring tiles per CTA
+    # up to 112 dims), 3 = K2 one warp per 32-point tile, 2 = K2 with the
+    # dims over the warps of a CTA, 10 = K2v forced
     x, p = synth.points_nd(dim, n, seed=dim)
     ox, op = np.zeros((dim, n)), np.zeros((dim, n))
     restate.gaussnd_grad(x, p, 1.3, ox, op)
-    for variant in (0, 1, 2, 3, 6, 7, 10, 15) + ((17, 18) if dim <= 112 else ()):
+    for variant in (0, 2, 3, 10):
         set_gaussnd_variant(variant)
         try:
             dx = torch.zeros((dim, n), dtype=torch.float64, device=DEV)
@@ -678,15 +679,11 @@ def test_device_fit_loop_bitwise_equals_host_loop(case):
     h = adc.Histogram(counts.size, -5.0, 5.0, ev, counts)
     out = {}
     for mode in ("0", "1"):
-        os.environ["ADC_FIT_DEVICE"] = mode
-        try:
-            r = adc.FitEngine(model, len(init)).fit(
-                h, init, adc.FitOptions(budget=budget, trace_iterates=budget + 1,
-                                        use_hessian=newton),
-                provider=adc.GradientProvider.Numeric if numeric else
-                adc.GradientProvider.AdReverse)
-        finally:
-            os.environ.pop("ADC_FIT_DEVICE", None)
+        r = adc.FitEngine(model, len(init)).fit(
+            h, init, adc.FitOptions(budget=budget, trace_iterates=budget + 1,
+                                    use_hessian=newton, host_loop=mode == "0"),
+            provider=adc.GradientProvider.Numeric if numeric else
+            adc.GradientProvider.AdReverse)
         out[mode] = r
     a, b = out["0"], out["1"]
     assert a.iterations == b.iterations and a.gradient_evals == b.gradient_evals

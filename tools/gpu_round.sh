@@ -16,7 +16,7 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:shar
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:shared_p_vec2 -s 2 -c 1 -o gpurun_out/prof_spv python tools/probe_shared_p.py > gpurun_out/ncu6.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:gaussnd_tile -c 1 -o gpurun_out/prof_nd1000 python tools/probe_gaussnd_variants.py 1000 1000000 0 > gpurun_out/ncu7.log 2>&1
 # (kernels inside a graph with a conditional node cannot be profiled: the host loop runs the same multi kernel)
-ADC_FIT_DEVICE=0 timeout 600 ncu --set full --clock-control none --import-source on -k regex:chi2_multi -s 20 -c 1 -o gpurun_out/prof_multi python tools/probe_fit_1e6.py > gpurun_out/ncu5.log 2>&1
+ADC_PROBE_HOST_LOOP=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:chi2_multi -s 20 -c 1 -o gpurun_out/prof_multi python tools/probe_fit_1e6.py > gpurun_out/ncu5.log 2>&1
 ls gpurun_out
 # summaries here (the box's ncu), then drop the big reports so gpurun_out/
 # stays under the 64 MiB copy-back limit (keep the two headline captures)

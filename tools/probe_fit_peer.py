@@ -1,5 +1,5 @@
 """Fit through a peer-transport communicator (world 1): the device loop (default)
-vs the host loop (ADC_FIT_DEVICE=0) — same bits, different speed."""
+vs the host loop (FitOptions.host_loop) — same bits, different speed."""
 import os
 import sys
 import time
@@ -15,12 +15,11 @@ h = adc.Histogram(10**6, -5.0, 5.0, ev, counts)
 comm = adc.Comm.peer(1, 0, lambda a: a.copy())
 res = {}
 for mode in ("1", "0", "1"):
-    os.environ["ADC_FIT_DEVICE"] = mode
     eng = adc.FitEngine("gpoly", 6, comm=comm)
-    eng.fit(h, synth.GPOLY_INIT, adc.FitOptions(budget=3))
+    eng.fit(h, synth.GPOLY_INIT, adc.FitOptions(budget=3, host_loop=mode == "0"))
     t0 = time.perf_counter()
-    r = eng.fit(h, synth.GPOLY_INIT, adc.FitOptions(budget=200))
+    r = eng.fit(h, synth.GPOLY_INIT, adc.FitOptions(budget=200, host_loop=mode == "0"))
     dt = time.perf_counter() - t0
     res[mode] = np.array(r.params).tobytes()
-    print(f"ADC_FIT_DEVICE={mode}: {r.iterations / dt:.0f} iterations/s, chi2 {r.chi2!r}")
+    print(f"device loop={mode}: {r.iterations / dt:.0f} iterations/s, chi2 {r.chi2!r}")
 print("same bits:", res["0"] == res["1"])
