@@ -772,6 +772,41 @@ def bench_fit(local):
     return rec
 
 
+def bench_jit(local, npts=100_000_000, steps=10, warm=3):
+    """Generic lowering (DSL -> CUDA -> NVRTC sm_100a):
+    the reference corpus gradients rational_grad (no tape) and looped_grad
+    (n = 10: tape entries in registers, the static-tape variant) called from
+    Listing-style kernels over 1e8 points; 48 / 24 B per point."""
+    import numpy as np
+    import torch
+    import paper_2203_06139_b200 as adc
+    module = str(np.load(os.path.join(ROOT, "tests", "golden", "jit_cases.npz"))["module"])
+    dev = torch.device("cuda", local)
+    g = torch.Generator(device=dev)
+    g.manual_seed(5)
+    x = torch.rand(npts, dtype=torch.float64, device=dev, generator=g) * 4 - 2
+    y = torch.rand(npts, dtype=torch.float64, device=dev, generator=g) * 4 - 2
+    dx, dy = torch.zeros_like(x), torch.zeros_like(x)
+    cfg = adc.LaunchConfig(npts // 256 + 1, 256, npts)
+    stream = torch.cuda.current_stream(dev)
+    rec = {"workload": "generic JIT: corpus gradients over 1e8 points (launch incl. the per-launch "
+                       "error-word check)"}
+    for kern, bufs, bytes_pt, ints in (
+            ("k_rational", adc.BufferSet(arrays={"x": x, "y": y, "dx": dx, "dy": dy}), 48, []),
+            ("k_looped", adc.BufferSet(arrays={"x": x, "dx": dx}, integers={"n": 10}), 24, [10])):
+        mod = adc.JitModule(module, kern)
+        step = lambda: mod.launch(cfg, bufs)  # noqa: E731
+        for _ in range(warm):
+            step()
+        torch.cuda.synchronize()
+        evs = [event_time(step, stream) for _ in range(steps)]
+        torch.cuda.synchronize()
+        ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in evs)
+        rec[kern] = {"ms_per_launch": ms, "static_tape": mod.static_source(ints) is not None,
+                     "roofline": hbm_roofline(bytes_pt * npts, ms, "jit_" + kern)}
+    return rec
+
+
 # ---------------------------------------------------------------------------- our arm
 def ours_arm(a, world, rank, local):
     import torch
@@ -809,6 +844,7 @@ def points_headline(a, world, rank, local, dist):
             jobs = [("cfg1_gauss1d_1M", lambda: config_points("gauss1d", local)),
                     ("cfg3_fit_1e6", lambda: bench_fit(local)),
                     ("cfg4_gaussnd1000_1M", lambda: config_points("gaussnd1000", local))] + jobs
+            jobs.append(("jit_corpus", lambda: bench_jit(local)))
         for name, job in jobs:
             try:
                 configs[name] = job()

@@ -191,6 +191,17 @@ int adc_jit_kernel_params(const adc_jit_module* module, int32_t* nparams, int32_
                           int32_t cap);
 const char* adc_jit_kernel_param_name(const adc_jit_module* module, int32_t index);
 const char* adc_jit_cuda_source(const adc_jit_module* module);
+/* Tape elimination: where every tape push/pop sits
+ * at a compile-time depth, launches run a static-tape variant whose entries
+ * are locals (registers) instead of the per-frame tape arrays — for kernels
+ * with integer parameters specialised per tuple of integer arguments (loops
+ * with those trip counts unrolled), built by NVRTC on first use.  Same
+ * operations in the same order: the same bits.  This returns the CUDA source
+ * of the variant a launch with these integer arguments (kernel parameter
+ * order, integers only) uses, or *cuda_source = NULL when it runs the
+ * dynamic-tape kernel (adc_jit_cuda_source). */
+int adc_jit_static_variant(adc_jit_module* module, const int64_t* int_args, int32_t nint,
+                           const char** cuda_source);
 size_t adc_jit_cubin_size(const adc_jit_module* module);
 /* LaunchConfig semantics (launch.cpp:9-19): grid x block threads, the
  * kernel's own `i < N` guard idles the padding.  Synchronous on `stream`. */

@@ -125,6 +125,8 @@ SIGNATURES = {
                                              _I32]),
     "adc_jit_kernel_param_name": (ctypes.c_char_p, [_VP, _I32]),
     "adc_jit_cuda_source": (ctypes.c_char_p, [_VP]),
+    "adc_jit_static_variant": (ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_int64), ctypes.c_int32,
+                                              ctypes.POINTER(ctypes.c_char_p)]),
     "adc_jit_cubin_size": (ctypes.c_size_t, [_VP]),
     "adc_cuda_jit_launch": (ctypes.c_int, [_VP, _I64, _I64, _I64, ctypes.POINTER(JitArg), _I32,
                                            _VP]),

@@ -166,6 +166,13 @@ struct adc_chi2_plan {
   double* lin = nullptr;      // per local chunk [G0_lin[L], G1_lin[L], C0]
   double* icounts = nullptr;  // [c > 0]/c for this rank's bins (from bin_begin)
   bool lin_ready = false;
+  // the empty bins of this rank's chunks (CSR by local chunk) and the side
+  // pass's per-chunk sums over them (chi2.cu K3z)
+  int64_t* empty_idx = nullptr;
+  int64_t empty_cap = 0;
+  int64_t* empty_off = nullptr;  // [local chunks + 1]
+  int64_t* empty_cnt = nullptr;  // [local chunks]
+  double* zws = nullptr;         // [kMultiMax][maxc][1 + kMaxNp]
 };
 
 namespace {
@@ -204,6 +211,9 @@ Chi2Pass make_pass(const adc_chi2_plan* P) {
   pass.tile_begin = P->L.chunk_begin * P->L.chunk_tiles;
   pass.tile_end = (P->L.bin_end + P->L.tile_bins - 1) / P->L.tile_bins;
   if (pass.tile_end < pass.tile_begin) pass.tile_end = pass.tile_begin;
+  pass.empty_idx = P->empty_idx;
+  pass.empty_off = P->empty_off;
+  pass.zws = P->zws;
   return pass;
 }
 
@@ -277,6 +287,8 @@ int collect_finish(adc_chi2_plan* P, int R, int nb, const double** out) {
 // Once per plan (and after adc_cuda_chi2_plan_refresh): everything that
 // depends on the counts alone — ic = [c > 0]/c per bin, C0 and the linear
 // parameters' G0/G1 per chunk.
+void drop_graphs(adc_chi2_plan* P);
+
 int ensure_lin(adc_chi2_plan* P, cudaStream_t s) {
   if (P->lin_ready) return ADC_OK;
   const int L = chi2_lin_count(P->model, P->np);
@@ -285,6 +297,41 @@ int ensure_lin(adc_chi2_plan* P, cudaStream_t s) {
     ADCB_CUDA(cudaMalloc(&P->lin, (size_t)nrec * (2 * L + 1) * sizeof(double)));
   if (int rc = chi2_lin_enqueue(make_pass(P), P->model, P->L.chunk_tiles, P->lin, P->icounts, s))
     return rc;
+  // the empty-bin lists (ascending per chunk) for the passes' side pass
+  if (P->empty_off == nullptr) {
+    ADCB_CUDA(cudaMalloc(&P->empty_off, (size_t)(nrec + 1) * sizeof(int64_t)));
+    ADCB_CUDA(cudaMalloc(&P->empty_cnt, (size_t)nrec * sizeof(int64_t)));
+    ADCB_CUDA(cudaMalloc(&P->zws, (size_t)kMultiMax * P->maxc * (1 + kMaxNp) * sizeof(double)));
+  }
+  const int64_t nloc = local_chunks(P);
+  std::vector<int64_t> off((size_t)nloc + 1, 0);
+  if (nloc > 0) {
+    if (int rc = chi2_empty_count_enqueue(make_pass(P), P->L.chunk_tiles, P->empty_cnt, s))
+      return rc;
+    ADCB_CUDA(cudaMemcpyAsync(off.data() + 1, P->empty_cnt, (size_t)nloc * sizeof(int64_t),
+                              cudaMemcpyDeviceToHost, s));
+    ADCB_CUDA(cudaStreamSynchronize(s));
+    for (int64_t c = 0; c < nloc; ++c) off[c + 1] += off[c];
+  }
+  const int64_t total = std::max<int64_t>(1, off[nloc]);
+  if (total > P->empty_cap) {  // (a refreshed histogram with more empty bins)
+    if (P->empty_idx) {
+      ADCB_CUDA(cudaStreamSynchronize(s));
+      cudaFree(P->empty_idx);
+      drop_graphs(P);  // captured passes hold the old list
+      if (P->fit_graph) cudaGraphExecDestroy(P->fit_graph);
+      P->fit_graph = nullptr;
+    }
+    P->empty_idx = nullptr;
+    ADCB_CUDA(cudaMalloc(&P->empty_idx, (size_t)total * sizeof(int64_t)));
+    P->empty_cap = total;
+  }
+  ADCB_CUDA(cudaMemcpyAsync(P->empty_off, off.data(), (size_t)(nloc + 1) * sizeof(int64_t),
+                            cudaMemcpyHostToDevice, s));
+  if (nloc > 0)
+    if (int rc = chi2_empty_fill_enqueue(make_pass(P), P->L.chunk_tiles, P->empty_off,
+                                         P->empty_idx, s))
+      return rc;
   ADCB_CUDA(cudaStreamSynchronize(s));
   P->lin_ready = true;
   return ADC_OK;
@@ -512,6 +559,10 @@ extern "C" int adc_cuda_chi2_plan_destroy(adc_chi2_plan* P) {
   if (P->records_multi) cudaFree(P->records_multi);
   if (P->lin) cudaFree(P->lin);
   if (P->icounts) cudaFree(P->icounts);
+  if (P->empty_idx) cudaFree(P->empty_idx);
+  if (P->empty_off) cudaFree(P->empty_off);
+  if (P->empty_cnt) cudaFree(P->empty_cnt);
+  if (P->zws) cudaFree(P->zws);
   if (P->grad_multi_records) cudaFree(P->grad_multi_records);
   if (P->batch_ws) cudaFree(P->batch_ws);
   if (P->fit_graph) cudaGraphExecDestroy(P->fit_graph);

@@ -27,6 +27,12 @@ struct Chi2Pass {
   // batched passes (chi2_enqueue nbatch > 1): member b reads qdev + b q_stride
   // and writes its tile records at tile_ws + b ws_stride (doubles)
   int64_t q_stride = 0, ws_stride = 0;
+  // the empty bins (c <= 0) of this rank's chunks, ascending, CSR by local
+  // chunk (chi2_empty_*_enqueue); zws: their per-chunk model sums
+  // (chi2_enqueue / chi2_multi_enqueue), kMultiMax x local chunks x (1 + kMaxNp)
+  const int64_t* empty_idx = nullptr;
+  const int64_t* empty_off = nullptr;
+  double* zws = nullptr;
 };
 
 // lin: per-chunk q-independent basis sums from chi2_lin_enqueue (gradient
@@ -48,6 +54,13 @@ int chi2_lin_enqueue(const Chi2Pass& P, int model, int64_t chunk_tiles, double* 
 int chi2_multi_enqueue(const Chi2Pass& P, int model, int np, int ncand,
                        int64_t chunk_tiles, double* records, cudaStream_t s, const double* lin,
                        int prec);
+// The empty-bin lists (once per plan, after chi2_lin_enqueue has written ic):
+// per local chunk the number of bins with ic == +0 into counts[nchunks]; then,
+// with off[nchunks + 1] its exclusive scan, their indices in ascending order.
+int chi2_empty_count_enqueue(const Chi2Pass& P, int64_t chunk_tiles, int64_t* counts,
+                             cudaStream_t s);
+int chi2_empty_fill_enqueue(const Chi2Pass& P, int64_t chunk_tiles, const int64_t* off,
+                            int64_t* idx, cudaStream_t s);
 void fill_qdev(int model, int np, const double* q, double* host_qdev);
 size_t qdev_bytes();
 // K6: counts[j] ~ Poisson(events m_j / sum m) (Philox, counter = bin), ws =

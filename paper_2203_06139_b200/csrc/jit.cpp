@@ -645,11 +645,51 @@ void kernel_hazards(const Module& m, const Blk& b, const std::string& tid,
 }
 
 // ---- CUDA emission ---------------------------------------------------------------
+// Static tape (tape elimination by SSA renaming).  The
+// value / control tapes of the generated code (reverse.cpp:335-382 pushes in
+// the forward sweep, 432-466 pops in the reversed loops) are LIFO per call
+// frame, so wherever the tape depth at a push or pop is a compile-time
+// constant, the entry is a plain local variable: push at depth d writes
+// _tv<d>, the matching pop reads it back — registers instead of a
+// thread-private array in local memory.  The depth is static through
+//  * straight-line code;
+//  * if/else whose branches move the depth by different amounts: forward
+//    branches (net pushes) all start at the same depth and the depth after the
+//    statement is padded to the largest branch; reverse branches (net pops)
+//    start where their forward branch ended (depth - max + own), so each
+//    reverse branch reads back exactly the slots its forward branch wrote;
+//  * loops whose body leaves both depths unchanged (slots reused every
+//    iteration);
+//  * loops with a compile-time trip count (integer kernel arguments are
+//    specialised per launch, integer locals, loop variables and control-tape
+//    entries folded), fully unrolled;
+// otherwise (data-dependent trip counts that push, deep unrolling) the
+// function keeps the dynamic tape.  Pops and pushes happen at the same points
+// in the same order with the same values, so results are the same bits.
+struct Dynamic {};
+
 struct Emitter {
   const Module& m;
   bool unsafe;
   int tape_cap;
   bool prefetch = true;
+  // static-tape state of the function frame being emitted
+  struct Frame {
+    bool stat = false;
+    int dv = 0, dc = 0, maxv = 0, maxc = 0;
+    std::map<std::string, long long> ienv;  // integer variables holding a known constant
+    std::map<int, long long> ctlval;        // control-tape slots holding a known constant
+  };
+  Frame fr;
+  long long unrolled_stmts = 0;  // emission budget of the unrolled code (per module)
+  static constexpr long long kUnrollBudget = 20000;
+  static constexpr long long kMaxTrip = 512;
+  // specialisations: key (function, cached, integer constants) -> emitted name
+  std::map<std::string, std::string> spec;
+  std::set<std::string> spec_active;
+  bool all_static = true;  // every callee specialisation got a static tape
+  std::ostringstream spec_decls, spec_defs;
+  int spec_count = 0;
   // Counting variant (LaunchStats): every interpreter-counted operation of
   // eval.cpp increments the thread's counter (adds: +, -, unary -, compound
   // +=; muls; divs; intrinsics; comparisons: each if condition; tape pushes
@@ -687,6 +727,56 @@ struct Emitter {
   }
   std::string ind(int d) { return std::string(2 * d, ' '); }
 
+  // Compile-time value of an integer expression in the current frame (static
+  // tape mode), or nothing; overflow is left to the run-time check.
+  bool fold(const Ex& e, long long& v) const {
+    if (!fr.stat || !e.is_int) return false;
+    long long a, b;
+    switch (e.k) {
+      case Ex::Num: v = (long long)e.v; return true;
+      case Ex::Var: {
+        auto it = fr.ienv.find(e.name);
+        if (it == fr.ienv.end()) return false;
+        v = it->second;
+        return true;
+      }
+      case Ex::Neg:
+        if (!fold(*e.a[0], a) || a == (-9223372036854775807LL - 1)) return false;
+        v = -a;
+        return true;
+      case Ex::Bin:
+        if (!fold(*e.a[0], a) || !fold(*e.a[1], b)) return false;
+        if (e.op == '+') return !__builtin_add_overflow(a, b, &v);
+        if (e.op == '-') return !__builtin_sub_overflow(a, b, &v);
+        if (e.op == '*') return !__builtin_mul_overflow(a, b, &v);
+        return false;
+      case Ex::Call: {
+        if (e.name != "__pop_ctl" || fr.dc <= 0) return false;
+        auto it = fr.ctlval.find(fr.dc - 1);
+        if (it == fr.ctlval.end()) return false;
+        v = it->second;
+        return true;
+      }
+      default: return false;
+    }
+  }
+  static int count_pops(const Ex& e) {
+    int n = e.k == Ex::Call && (e.name == "__pop" || e.name == "__pop_ctl");
+    for (auto& c : e.a) n += count_pops(*c);
+    return n;
+  }
+  // beyond this many live entries per frame the registers would spill to
+  // local memory anyway: keep the dynamic tape
+  static constexpr int kMaxStaticSlots = 64;
+  void note_push_v() {
+    fr.maxv = std::max(fr.maxv, ++fr.dv);
+    if (fr.maxv > kMaxStaticSlots) throw Dynamic{};
+  }
+  void note_push_c() {
+    fr.maxc = std::max(fr.maxc, ++fr.dc);
+    if (fr.maxc > kMaxStaticSlots) throw Dynamic{};
+  }
+
   // integer-valued expression (only called when e.is_int)
   std::string ie(const Ex& e) {
     switch (e.k) {
@@ -696,6 +786,8 @@ struct Emitter {
         if (e.name == "blockDim") return "(long long)blockDim.x";
         if (e.name == "threadIdx") return "(long long)threadIdx.x";
         if (e.name == "N") return "N";
+        if (fr.stat && fr.ienv.count(e.name))
+          return "(long long)" + std::to_string(fr.ienv.at(e.name)) + "LL";
         return V(e.name);
       // int64 arithmetic with the interpreter's overflow errors (eval.cpp:601-628)
       case Ex::Neg: return C("a", "adc_ineg(" + ie(*e.a[0]) + ", ctx)");
@@ -703,7 +795,12 @@ struct Emitter {
         return C(e.op == '*' ? "m" : "a",
                  std::string(e.op == '+' ? "adc_iadd(" : e.op == '-' ? "adc_isub(" : "adc_imul(") +
                      ie(*e.a[0]) + ", " + ie(*e.a[1]) + ", ctx)");
-      case Ex::Call: return C("po", "adc_pop_ctl(ctl, cp, ctx)");
+      case Ex::Call:
+        if (fr.stat) {
+          if (fr.dc <= 0) throw Dynamic{};  // underflow: the dynamic tape reports it
+          return "_tc" + std::to_string(--fr.dc);
+        }
+        return C("po", "adc_pop_ctl(ctl, cp, ctx)");
       default: return "0";
     }
   }
@@ -720,11 +817,26 @@ struct Emitter {
           case '+': return C("a", "__dadd_rn(" + a + ", " + b + ")");
           case '-': return C("a", "__dsub_rn(" + a + ", " + b + ")");
           case '*': return C("m", "__dmul_rn(" + a + ", " + b + ")");
-          default: return C("d", "adc_div(" + a + ", " + b + ", ctx)");
+          default: {
+            // x / 2^k == x * 2^-k exactly (both are the correctly rounded
+            // quotient, subnormals included), and the divisor is not 0
+            const Ex& d = *e.a[1];
+            int ex = 0;
+            if (d.k == Ex::Num && !d.pi && d.v != 0.0 && std::isfinite(d.v) &&
+                std::fabs(std::frexp(d.v, &ex)) == 0.5 && ex >= -1020 && ex <= 1020)
+              return C("d", "__dmul_rn(" + a + ", " + dbl(1.0 / d.v) + ")");
+            return C("d", "adc_div(" + a + ", " + b + ", ctx)");
+          }
         }
       }
       case Ex::Call: {
-        if (e.name == "__pop") return C("po", "adc_pop(tape, tp, ctx)");
+        if (e.name == "__pop") {
+          if (fr.stat) {
+            if (fr.dv <= 0) throw Dynamic{};
+            return "_tv" + std::to_string(--fr.dv);
+          }
+          return C("po", "adc_pop(tape, tp, ctx)");
+        }
         std::vector<std::string> a;
         for (auto& c : e.a) a.push_back(re(*c));
         if (e.name == "log") return C("i", "adc_log(" + a[0] + ", ctx)");
@@ -757,14 +869,80 @@ struct Emitter {
     sc.pop();
   }
 
+  // Integer variables a block may assign (their constants are forgotten
+  // around code that may run a data-dependent number of times).
+  static void assigned_ints(const Blk& b, std::set<std::string>& out) {
+    for (auto& sp : b) {
+      const St& s = *sp;
+      if ((s.k == St::Decl || (s.k == St::Assign && !s.indexed)) && !s.target.empty())
+        out.insert(s.target);
+      if (s.k == St::For) out.insert(s.loop_var);
+      assigned_ints(s.then_b, out);
+      assigned_ints(s.else_b, out);
+    }
+  }
+
+  // Emits `b` into a scratch stream and returns the frame state after it (the
+  // emitter's own state is restored): the depth a block leaves behind.
+  Frame dry_block(const Blk& b, const Fn& f, Scope& sc, int d) {
+    const Frame saved = fr;
+    const int saved_tmp = tmp;
+    const long long saved_budget = unrolled_stmts;
+    std::ostringstream scratch;
+    std::swap(o, scratch);
+    Frame out;
+    try {
+      block(b, f, sc, d);
+      out = fr;
+    } catch (...) {
+      std::swap(o, scratch);
+      fr = saved;
+      tmp = saved_tmp;
+      unrolled_stmts = saved_budget;
+      throw;
+    }
+    std::swap(o, scratch);
+    fr = saved;
+    tmp = saved_tmp;
+    unrolled_stmts = saved_budget;
+    return out;
+  }
+
+  // Start depth of each branch of an if (static tape; see the Dynamic note).
+  static void branch_starts(int d0, int e1, int e2, int& s1, int& s2, int& after) {
+    const int a = e1 - d0, b = e2 - d0;
+    if (a == b) {
+      s1 = s2 = d0;
+      after = e1;
+    } else if (a >= 0 && b >= 0) {  // forward: pad to the larger branch
+      s1 = s2 = d0;
+      after = d0 + std::max(a, b);
+    } else if (a <= 0 && b <= 0) {  // reverse: each branch reads its forward branch's slots
+      const int mn = std::min(a, b);
+      s1 = d0 + mn - a;
+      s2 = d0 + mn - b;
+      after = d0 + mn;
+    } else {
+      throw Dynamic{};
+    }
+  }
+
   void stmt(const St& s, const Fn& f, Scope& sc, int d) {
     VT t;
     if (f.global) Cst("st", d);  // eval.cpp:402, the kernel frame's statements
     if (s.k == St::Assign && s.compound) Cst("a", d);  // eval.cpp:420-447
     if (s.k == St::If) Cst("c", d);                    // eval.cpp:647
     if (s.k == St::Call && (s.callee == "__push" || s.callee == "__push_ctl")) Cst("pu", d);
+    if (fr.stat) {
+      int pops = (s.expr ? count_pops(*s.expr) : 0) + (s.index ? count_pops(*s.index) : 0);
+      for (auto& a : s.args) pops += count_pops(*a);
+      if (pops > 1) throw Dynamic{};  // several pops in one statement: keep the dynamic tape
+      if (++unrolled_stmts > kUnrollBudget) throw Dynamic{};
+    }
     switch (s.k) {
-      case St::Decl:
+      case St::Decl: {
+        long long cv = 0;
+        const bool known = s.type == VT::Integer && fold(*s.expr, cv);
         if (s.type == VT::Integer)
           o << ind(d) << "long long " << V(s.target) << " = " << ie_any(*s.expr) << ";\n";
         else
@@ -781,7 +959,10 @@ struct Emitter {
               << ".p + " << V(s.target) << "));\n";
         }
         sc.add(s.target, s.type);
+        if (known) fr.ienv[s.target] = cv;
+        else fr.ienv.erase(s.target);
         break;
+      }
       case St::Assign:
         sc.find(s.target, t);
         if (s.indexed && cached != nullptr && cached->count(s.target)) {
@@ -797,10 +978,20 @@ struct Emitter {
           else
             o << ind(d) << "adc_st(" << V(s.target) << ", " << idx << ", " << v << ", ctx);\n";
         } else if (t == VT::Integer) {
+          long long cv = 0, ev = 0;
+          bool known = fold(*s.expr, ev);
+          if (known && s.compound) {
+            auto it = fr.ienv.find(s.target);
+            known = it != fr.ienv.end() && !__builtin_add_overflow(it->second, ev, &cv);
+          } else {
+            cv = ev;
+          }
           const std::string v = ie_any(*s.expr);
           if (s.compound)
             o << ind(d) << V(s.target) << " = adc_iadd(" << V(s.target) << ", " << v << ", ctx);\n";
           else o << ind(d) << V(s.target) << " = " << v << ";\n";
+          if (known) fr.ienv[s.target] = cv;
+          else fr.ienv.erase(s.target);
         } else {
           const std::string v = re(*s.expr);
           if (s.compound)
@@ -812,18 +1003,105 @@ struct Emitter {
       case St::Return:
         o << ind(d) << "return " << re(*s.expr) << ";\n";
         break;
-      case St::If:
-        o << ind(d) << "if " << cond(*s.expr) << " {\n";
-        block(s.then_b, f, sc, d + 1);
-        o << ind(d) << "}";
-        if (!s.else_b.empty()) {
-          o << " else {\n";
-          block(s.else_b, f, sc, d + 1);
+      case St::If: {
+        if (!fr.stat) {
+          o << ind(d) << "if " << cond(*s.expr) << " {\n";
+          block(s.then_b, f, sc, d + 1);
           o << ind(d) << "}";
+          if (!s.else_b.empty()) {
+            o << " else {\n";
+            block(s.else_b, f, sc, d + 1);
+            o << ind(d) << "}";
+          }
+          o << "\n";
+          break;
         }
-        o << "\n";
+        o << ind(d) << "if " << cond(*s.expr) << " {\n";  // (a condition never pops)
+        const Frame f1 = dry_block(s.then_b, f, sc, d + 1);
+        const Frame f2 = dry_block(s.else_b, f, sc, d + 1);
+        int v1, v2, va, c1, c2, ca;
+        branch_starts(fr.dv, f1.dv, f2.dv, v1, v2, va);
+        branch_starts(fr.dc, f1.dc, f2.dc, c1, c2, ca);
+        const Frame base = fr;
+        fr.dv = v1;
+        fr.dc = c1;
+        block(s.then_b, f, sc, d + 1);
+        const Frame t1 = fr;
+        fr = base;
+        fr.maxv = std::max(fr.maxv, t1.maxv);
+        fr.maxc = std::max(fr.maxc, t1.maxc);
+        fr.dv = v2;
+        fr.dc = c2;
+        o << ind(d) << "} else {\n";
+        block(s.else_b, f, sc, d + 1);
+        o << ind(d) << "}\n";
+        const Frame t2 = fr;
+        fr = base;
+        fr.maxv = std::max({fr.maxv, t1.maxv, t2.maxv, va});
+        fr.maxc = std::max({fr.maxc, t1.maxc, t2.maxc, ca});
+        if (fr.maxv > kMaxStaticSlots || fr.maxc > kMaxStaticSlots) throw Dynamic{};
+        fr.dv = va;
+        fr.dc = ca;
+        // constants that both branches agree on survive the statement
+        fr.ienv.clear();
+        for (auto& kv : t1.ienv) {
+          auto it = t2.ienv.find(kv.first);
+          if (it != t2.ienv.end() && it->second == kv.second) fr.ienv.insert(kv);
+        }
+        // control slots written in a branch hold a data-dependent value
+        for (int k = std::min(base.dc, ca); k < std::max({base.dc, t1.maxc, t2.maxc, ca}); ++k)
+          fr.ctlval.erase(k);
+        for (auto& kv : t1.ctlval) {
+          auto it = t2.ctlval.find(kv.first);
+          if (kv.first < std::min(base.dc, ca) && it != t2.ctlval.end() && it->second == kv.second)
+            fr.ctlval[kv.first] = kv.second;
+        }
         break;
+      }
       case St::For: {
+        long long lo = 0, hi = 0;
+        const bool const_trip = fold(*s.lo, lo) && fold(*s.hi, hi);
+        if (fr.stat) {
+          // does the body move the tape depths?
+          std::set<std::string> asg;
+          assigned_ints(s.then_b, asg);
+          Frame probe_base = fr;
+          for (auto& v : asg) fr.ienv.erase(v);
+          fr.ctlval.clear();
+          bool balanced = false;
+          sc.push();
+          sc.add(s.loop_var, VT::Integer);
+          try {
+            const Frame body_end = dry_block(s.then_b, f, sc, d + 2);
+            balanced = body_end.dv == fr.dv && body_end.dc == fr.dc;
+          } catch (Dynamic&) {
+            balanced = false;  // e.g. an inner trip count that needs this loop's variable
+          }
+          sc.pop();
+          fr = probe_base;
+          if (!balanced) {
+            if (!const_trip || hi - lo > kMaxTrip) throw Dynamic{};
+            // unrolled: one copy of the body per iteration, the loop variable a constant
+            const int k = tmp++;
+            o << ind(d) << "{  // unrolled: " << std::max(0LL, hi - lo) << " iterations\n";
+            (void)k;
+            for (long long it = lo; it < hi; ++it) {
+              o << ind(d + 1) << "{\n";
+              o << ind(d + 2) << "const long long " << V(s.loop_var) << " = " << it << "LL;\n";
+              sc.push();
+              sc.add(s.loop_var, VT::Integer);
+              fr.ienv[s.loop_var] = it;
+              block(s.then_b, f, sc, d + 2);
+              fr.ienv.erase(s.loop_var);
+              sc.pop();
+              o << ind(d + 1) << "}\n";
+            }
+            o << ind(d) << "}\n";
+            break;
+          }
+          for (auto& v : asg) fr.ienv.erase(v);
+          fr.ctlval.clear();  // a body may pop and re-push slots below its start depth
+        }
         const int k = tmp++;
         o << ind(d) << "{\n";
         o << ind(d + 1) << "const long long _adc_lo" << k << " = " << ie_any(*s.lo) << ";\n";
@@ -832,18 +1110,40 @@ struct Emitter {
           << V(s.loop_var) << " < _adc_hi" << k << "; ++" << V(s.loop_var) << ") {\n";
         sc.push();
         sc.add(s.loop_var, VT::Integer);
+        const int cbase = fr.dc;
         block(s.then_b, f, sc, d + 2);
         sc.pop();
         o << ind(d + 1) << "}\n" << ind(d) << "}\n";
+        if (fr.stat) {
+          std::set<std::string> asg;
+          assigned_ints(s.then_b, asg);
+          for (auto& v : asg) fr.ienv.erase(v);
+          fr.ctlval.clear();
+          (void)cbase;
+        }
         break;
       }
       case St::Call: {
         if (s.callee == "__push") {
-          o << ind(d) << "adc_push(tape, tp, " << re(*s.args[0]) << ", ctx);\n";
+          if (fr.stat) {
+            o << ind(d) << "_tv" << fr.dv << " = " << re(*s.args[0]) << ";\n";
+            note_push_v();
+          } else {
+            o << ind(d) << "adc_push(tape, tp, " << re(*s.args[0]) << ", ctx);\n";
+          }
           break;
         }
         if (s.callee == "__push_ctl") {
-          o << ind(d) << "adc_push_ctl(ctl, cp, " << ie_any(*s.args[0]) << ", ctx);\n";
+          if (fr.stat) {
+            long long cv = 0;
+            const bool known = fold(*s.args[0], cv);
+            o << ind(d) << "_tc" << fr.dc << " = " << ie_any(*s.args[0]) << ";\n";
+            if (known) fr.ctlval[fr.dc] = cv;
+            else fr.ctlval.erase(fr.dc);
+            note_push_c();
+          } else {
+            o << ind(d) << "adc_push_ctl(ctl, cp, " << ie_any(*s.args[0]) << ", ctx);\n";
+          }
           break;
         }
         const Fn* c = m.find(s.callee);
@@ -861,7 +1161,9 @@ struct Emitter {
             if (!arrays_seen.insert(arg.name).second) use_cached = false;  // aliasing
           }
         }
-        o << ind(d) << "fn_" << c->name << (use_cached ? "_c" : "") << "(";
+        std::string callee = "fn_" + c->name + (use_cached ? "_c" : "");
+        if (fr.stat) callee = specialised(*c, s, use_cached, callee);
+        o << ind(d) << callee << "(";
         for (size_t a = 0; a < s.args.size(); ++a) {
           const Ex& arg = *s.args[a];
           const VT pt = c->params[a].type;
@@ -881,6 +1183,41 @@ struct Emitter {
         break;
       }
     }
+  }
+
+  // The static-tape definition of callee c for this call's integer constants
+  // (emitted once per distinct key into spec_defs); the generic name when the
+  // callee needs the dynamic tape or is already being specialised (recursion).
+  std::string specialised(const Fn& c, const St& call, bool cached_variant,
+                          const std::string& generic) {
+    std::map<std::string, long long> consts;
+    std::string key = c.name + (cached_variant ? "|c" : "|g");
+    for (size_t a = 0; a < call.args.size() && a < c.params.size(); ++a) {
+      long long v = 0;
+      if (c.params[a].type == VT::Integer && fold(*call.args[a], v)) {
+        consts[c.params[a].name] = v;
+        key += "|" + c.params[a].name + "=" + std::to_string(v);
+      }
+    }
+    auto it = spec.find(key);
+    if (it != spec.end()) return it->second;
+    if (spec_active.count(key)) {
+      all_static = false;
+      return generic;
+    }
+    spec_active.insert(key);
+    const std::string name = "fn_" + c.name + "_s" + std::to_string(spec_count++);
+    std::string text;
+    const bool ok = function_text(c, name, cached_variant, &consts, text);
+    spec_active.erase(key);
+    const std::string use = ok ? name : generic;
+    if (!ok) all_static = false;
+    spec[key] = use;
+    if (ok) {
+      spec_decls << signature(c, name) << ";\n";
+      spec_defs << text;
+    }
+    return use;
   }
 
   // arrays of the kernel indexed exactly by the thread-index variable
@@ -1046,73 +1383,137 @@ __device__ __forceinline__ long long adc_pop_ctl(long long* t, int& cp, const Ad
     if (any) cacheable[f.name] = v;
   }
 
-  void function_cached(const Fn& f) {
-    const std::vector<int>& v = cacheable.at(f.name);
-    std::set<std::string> names;
-    o << "__device__ void fn_" << f.name << "_c(";
+  std::string signature(const Fn& f, const std::string& name) const {
+    std::string sig = std::string("__device__ ") + (f.returns_void ? "void " : "double ") + name + "(";
     for (size_t i = 0; i < f.params.size(); ++i)
-      o << (i ? ", " : "") << ptype(f.params[i].type) << " " << V(f.params[i].name);
-    o << (f.params.empty() ? "" : ", ") << "const AdcCtx& ctx) {\n";
-    for (size_t i = 0; i < f.params.size(); ++i) {
-      if (!v[i]) continue;
-      const std::string n = V(f.params[i].name);
-      names.insert(f.params[i].name);
-      o << "  double c_" << n << " = adc_ok(" << n << ", 0, ctx) ? " << n << ".p[0] : 0.0;\n";
-    }
-    if (f.uses_tape) o << "  double tape[ADC_TAPE]; int tp = 0;\n";
-    if (f.uses_ctl) o << "  long long ctl[ADC_TAPE]; int cp = 0;\n";
-    Scope sc;
-    sc.push();
-    for (auto& p : f.params) sc.add(p.name, p.type);
-    cached = &names;
-    block(f.body, f, sc, 1);
-    cached = nullptr;
-    for (size_t i = 0; i < f.params.size(); ++i)
-      if (v[i] == 2) {
-        const std::string n = V(f.params[i].name);
-        o << "  if (" << n << ".len > 0) " << n << ".p[0] = c_" << n << ";\n";
-      }
-    o << "}\n\n";
+      sig += (i ? ", " : "") + ptype(f.params[i].type) + " " + V(f.params[i].name);
+    return sig + (f.params.empty() ? "" : ", ") + "const AdcCtx& ctx)";
   }
 
+  // The definition of a device function under `name`: slot-cached or not;
+  // with `consts` (static tape) its integer parameters bound to constants.
+  // Returns false (and no text) when the static tape is not possible.
+  bool function_text(const Fn& f, const std::string& name, bool cached_variant,
+                     const std::map<std::string, long long>* consts, std::string& text) {
+    const Frame saved_fr = fr;
+    const std::set<std::string>* saved_cached = cached;
+    std::ostringstream body;
+    std::swap(o, body);
+    std::set<std::string> names;
+    const std::vector<int>* v = cached_variant ? &cacheable.at(f.name) : nullptr;
+    fr = Frame{};
+    fr.stat = consts != nullptr;
+    if (consts) fr.ienv = *consts;
+    bool ok = true;
+    try {
+      if (v)
+        for (size_t i = 0; i < f.params.size(); ++i) {
+          if (!(*v)[i]) continue;
+          const std::string n = V(f.params[i].name);
+          names.insert(f.params[i].name);
+          o << "  double c_" << n << " = adc_ok(" << n << ", 0, ctx) ? " << n << ".p[0] : 0.0;\n";
+        }
+      Scope sc;
+      sc.push();
+      for (auto& p : f.params) sc.add(p.name, p.type);
+      cached = v ? &names : nullptr;
+      block(f.body, f, sc, 1);
+      cached = saved_cached;
+      if (v)
+        for (size_t i = 0; i < f.params.size(); ++i)
+          if ((*v)[i] == 2) {
+            const std::string n = V(f.params[i].name);
+            o << "  if (" << n << ".len > 0) " << n << ".p[0] = c_" << n << ";\n";
+          }
+      if (!f.returns_void) o << "  return __longlong_as_double(0x7ff8000000000000LL);\n";
+    } catch (Dynamic&) {
+      ok = false;
+    } catch (...) {
+      std::swap(o, body);
+      fr = saved_fr;
+      cached = saved_cached;
+      throw;
+    }
+    std::swap(o, body);
+    const Frame done = fr;
+    fr = saved_fr;
+    cached = saved_cached;
+    if (!ok) return false;
+    std::ostringstream t;
+    t << signature(f, name) << " {\n";
+    if (done.stat) {
+      for (int k = 0; k < done.maxv; ++k) t << "  double _tv" << k << " = 0.0;\n";
+      for (int k = 0; k < done.maxc; ++k) t << "  long long _tc" << k << " = 0;\n";
+    } else {
+      if (f.uses_tape) t << "  double tape[ADC_TAPE]; int tp = 0;\n";
+      if (f.uses_ctl) t << "  long long ctl[ADC_TAPE]; int cp = 0;\n";
+    }
+    t << body.str() << "}\n\n";
+    text = t.str();
+    return true;
+  }
+
+  // Generic (dynamic-tape) definitions of a device function: fn_<f> and,
+  // when cacheable, fn_<f>_c.
   void function(const Fn& f) {
-    if (cacheable.count(f.name)) function_cached(f);
+    std::string text;
+    if (cacheable.count(f.name)) {
+      function_text(f, "fn_" + f.name + "_c", true, nullptr, text);
+      o << text;
+    }
+    function_text(f, "fn_" + f.name, false, nullptr, text);
+    o << text;
+  }
+
+  // The kernel.  kconst: integer kernel parameters bound to constants (the
+  // static tape specialisation; nullptr = the generic dynamic-tape kernel).
+  // Throws Dynamic if the kernel frame itself cannot use a static tape.
+  void kernel(const Fn& f, const std::map<std::string, long long>* kconst) {
     Scope sc;
     sc.push();
+    sc.global = true;
     for (auto& p : f.params) sc.add(p.name, p.type);
-    if (f.global) {
-      sc.global = true;
-      o << "extern \"C\" __global__ void adc_kernel_" << f.name << "(";
-      for (size_t i = 0; i < f.params.size(); ++i) {
-        const Prm& p = f.params[i];
-        if (i) o << ", ";
-        if (p.type == VT::RealArray)
-          o << "double* " << V(p.name) << "_p, long long " << V(p.name) << "_n";
-        else
-          o << ptype(p.type) << " " << V(p.name);
-      }
-      o << (f.params.empty() ? "" : ", ") << "long long N, AdcErr* adc_err"
-        << (count ? ", unsigned long long* adc_cnt_out, unsigned* adc_stm" : "") << ") {\n";
-      if (count)
-        o << "  AdcCnt adc_cnt{};\n"
-             "  const AdcCtx ctx{adc_err, (long long)blockIdx.x * blockDim.x + threadIdx.x, "
-             "&adc_cnt};\n";
+    o << "extern \"C\" __global__ void adc_kernel_" << f.name << "(";
+    for (size_t i = 0; i < f.params.size(); ++i) {
+      const Prm& p = f.params[i];
+      if (i) o << ", ";
+      if (p.type == VT::RealArray)
+        o << "double* " << V(p.name) << "_p, long long " << V(p.name) << "_n";
       else
-        o << "  const AdcCtx ctx{adc_err, (long long)blockIdx.x * blockDim.x + threadIdx.x};\n";
-      for (auto& p : f.params)
-        if (p.type == VT::RealArray)
-          o << "  const AdcArr " << V(p.name) << "{" << V(p.name) << "_p, " << V(p.name) << "_n};\n";
-    } else {
-      o << "__device__ " << (f.returns_void ? "void" : "double") << " fn_" << f.name << "(";
-      for (size_t i = 0; i < f.params.size(); ++i)
-        o << (i ? ", " : "") << ptype(f.params[i].type) << " " << V(f.params[i].name);
-      o << (f.params.empty() ? "" : ", ") << "const AdcCtx& ctx) {\n";
+        o << ptype(p.type) << " " << V(p.name);
     }
-    if (f.uses_tape) o << "  double tape[ADC_TAPE]; int tp = 0;\n";
-    if (f.uses_ctl) o << "  long long ctl[ADC_TAPE]; int cp = 0;\n";
-    block(f.body, f, sc, 1);
-    if (!f.returns_void && !f.global) o << "  return __longlong_as_double(0x7ff8000000000000LL);\n";
-    if (f.global && count)  // per-block sums of the counters, one atomic per counter per block
+    o << (f.params.empty() ? "" : ", ") << "long long N, AdcErr* adc_err"
+      << (count ? ", unsigned long long* adc_cnt_out, unsigned* adc_stm" : "") << ") {\n";
+    if (count)
+      o << "  AdcCnt adc_cnt{};\n"
+           "  const AdcCtx ctx{adc_err, (long long)blockIdx.x * blockDim.x + threadIdx.x, "
+           "&adc_cnt};\n";
+    else
+      o << "  const AdcCtx ctx{adc_err, (long long)blockIdx.x * blockDim.x + threadIdx.x};\n";
+    for (auto& p : f.params)
+      if (p.type == VT::RealArray)
+        o << "  const AdcArr " << V(p.name) << "{" << V(p.name) << "_p, " << V(p.name) << "_n};\n";
+    fr = Frame{};
+    fr.stat = kconst != nullptr;
+    if (kconst) fr.ienv = *kconst;
+    std::ostringstream body;
+    std::swap(o, body);
+    try {
+      block(f.body, f, sc, 1);
+    } catch (...) {
+      std::swap(o, body);
+      throw;
+    }
+    std::swap(o, body);
+    if (fr.stat) {
+      for (int k = 0; k < fr.maxv; ++k) o << "  double _tv" << k << " = 0.0;\n";
+      for (int k = 0; k < fr.maxc; ++k) o << "  long long _tc" << k << " = 0;\n";
+    } else {
+      if (f.uses_tape) o << "  double tape[ADC_TAPE]; int tp = 0;\n";
+      if (f.uses_ctl) o << "  long long ctl[ADC_TAPE]; int cp = 0;\n";
+    }
+    o << body.str();
+    if (count)  // per-block sums of the counters, one atomic per counter per block
       o << R"(  __shared__ unsigned long long adc_bs[7];
   if (threadIdx.x < 7) adc_bs[threadIdx.x] = 0ull;
   __syncthreads();
@@ -1165,6 +1566,18 @@ struct adc_jit_module {
   std::vector<char> cubin;
   std::map<int, cudaLibrary_t> libs;  // per device
   std::map<int, cudaKernel_t> fns;
+  // static-tape variants (jit.cpp, "Static tape"): one for every launch when
+  // the kernel needs no integer constants (key "*"), else one per tuple of
+  // integer kernel arguments (built on first use, at most kMaxStaticVariants)
+  struct Variant {
+    bool ok = false;  // false: this key runs the dynamic-tape kernel
+    std::string cuda;
+    std::vector<char> cubin;
+    std::map<int, cudaLibrary_t> libs;
+    std::map<int, cudaKernel_t> fns;
+  };
+  std::map<std::string, Variant> statics;
+  bool static_any = false;  // statics["*"] serves every launch
   std::mutex mu;
 };
 
@@ -1190,8 +1603,15 @@ int parse_module(const std::string& src, Module& m) {
 
 namespace {
 // Emission (plain or counting variant) and NVRTC compilation of kernel k of m.
+// kconst != nullptr: the static-tape variant with the kernel's integer
+// parameters bound as given (possibly none); returns kStaticImpossible when it
+// cannot be built (the caller keeps the dynamic-tape kernel).
+constexpr int kStaticImpossible = -1000;
+
 int emit_and_compile(const Module& m, const Fn* k, const std::string& kernel, bool unsafe,
-                     int tape_capacity, bool count, std::string& cuda, std::vector<char>& cubin) {
+                     int tape_capacity, bool count, std::string& cuda, std::vector<char>& cubin,
+                     const std::map<std::string, long long>* kconst = nullptr,
+                     bool* fully_static = nullptr) {
   Emitter em{m, unsafe, tape_capacity};
   em.count = count;
   try {
@@ -1227,8 +1647,20 @@ int emit_and_compile(const Module& m, const Fn* k, const std::string& kernel, bo
     // callees first, so a cached variant is declared before its call sites
     for (auto& f : m.fns)
       if (reach.count(f.name) && !f.global) em.function(f);
-    for (auto& f : m.fns)
-      if (reach.count(f.name) && f.global) em.function(f);
+    // the kernel (its static-tape specialisations of the callees before it)
+    std::ostringstream ko;
+    std::swap(em.o, ko);
+    try {
+      em.kernel(*k, kconst);
+    } catch (Dynamic&) {
+      return kStaticImpossible;
+    } catch (...) {
+      std::swap(em.o, ko);
+      throw;
+    }
+    std::swap(em.o, ko);
+    em.o << em.spec_decls.str() << "\n" << em.spec_defs.str() << ko.str();
+    if (fully_static) *fully_static = em.all_static;
   } catch (const ParseError& e) {
     return fail(ADC_E_SEMANTIC, "jit: " + e.msg);
   }
@@ -1293,6 +1725,24 @@ extern "C" int adc_jit_compile(const char* source, const char* kernel, int32_t u
     delete J;
     return rc;
   }
+  // the static-tape kernel that needs no integer constants, when there is one
+  {
+    const std::map<std::string, long long> none;
+    adc_jit_module::Variant v;
+    bool full = false;
+    const int rc = emit_and_compile(m, k, kernel, unsafe != 0, tape_capacity, false, v.cuda,
+                                    v.cubin, &none, &full);
+    bool has_ints = false;
+    for (auto& p : k->params) has_ints = has_ints || p.type == VT::Integer;
+    if (rc == ADC_OK && (full || !has_ints)) {
+      v.ok = true;
+      J->statics["*"] = std::move(v);
+      J->static_any = true;
+    } else if (rc != ADC_OK && rc != kStaticImpossible) {
+      delete J;
+      return rc;
+    }
+  }
   *out = J;
   return ADC_OK;
 }
@@ -1301,6 +1751,8 @@ extern "C" int adc_jit_destroy(adc_jit_module* J) {
   if (J == nullptr) return ADC_OK;
   for (auto& l : J->libs) cudaLibraryUnload(l.second);
   for (auto& l : J->libs_counted) cudaLibraryUnload(l.second);
+  for (auto& v : J->statics)
+    for (auto& l : v.second.libs) cudaLibraryUnload(l.second);
   if (J->dcnt) cudaFree(J->dcnt);
   for (auto& e : J->derr) cudaFree(e.second);
   if (J->herr) cudaFreeHost(J->herr);
@@ -1323,6 +1775,58 @@ extern "C" const char* adc_jit_kernel_param_name(const adc_jit_module* J, int32_
 
 extern "C" const char* adc_jit_cuda_source(const adc_jit_module* J) {
   return J ? J->cuda.c_str() : nullptr;
+}
+
+namespace {
+constexpr size_t kMaxStaticVariants = 32;
+
+// The static-tape variant a launch with these arguments uses (built on first
+// use); nullptr = the dynamic-tape kernel.  Caller holds J->mu.
+adc_jit_module::Variant* static_variant(adc_jit_module* J, const adc_jit_arg* args, int& rc) {
+  rc = ADC_OK;
+  if (J->static_any) return &J->statics["*"];
+  std::map<std::string, long long> consts;
+  std::string key;
+  for (size_t i = 0; i < J->kinds.size(); ++i)
+    if (J->kinds[i] == 2) {
+      consts[J->names[i]] = args[i].int_value;
+      key += std::to_string(args[i].int_value) + ",";
+    }
+  if (consts.empty()) return nullptr;  // no constants to specialise on
+  auto it = J->statics.find(key);
+  if (it != J->statics.end()) return it->second.ok ? &it->second : nullptr;
+  if (J->statics.size() >= kMaxStaticVariants) return nullptr;
+  Module m;
+  if ((rc = parse_module(J->source, m))) return nullptr;
+  adc_jit_module::Variant v;
+  bool full = false;
+  rc = emit_and_compile(m, m.find(J->kernel), J->kernel, J->unsafe, J->tape_capacity, false,
+                        v.cuda, v.cubin, &consts, &full);
+  if (rc == kStaticImpossible) rc = ADC_OK;
+  else if (rc != ADC_OK) return nullptr;
+  else v.ok = full;  // a partly static variant buys nothing over the dynamic kernel
+  auto& slot = J->statics[key] = std::move(v);
+  return slot.ok ? &slot : nullptr;
+}
+}  // namespace
+
+extern "C" int adc_jit_static_variant(adc_jit_module* J, const int64_t* int_args, int32_t nint,
+                                      const char** cuda_source) {
+  clear_error();
+  if (J == nullptr || cuda_source == nullptr) return fail(ADC_E_ARG, "null argument");
+  std::vector<adc_jit_arg> args(J->kinds.size());
+  int32_t k = 0;
+  for (size_t i = 0; i < J->kinds.size(); ++i)
+    if (J->kinds[i] == 2) {
+      if (k >= nint || int_args == nullptr) return fail(ADC_E_ARG, "missing integer argument");
+      args[i].int_value = int_args[k++];
+    }
+  std::lock_guard<std::mutex> lock(J->mu);
+  int rc = ADC_OK;
+  adc_jit_module::Variant* v = static_variant(J, args.data(), rc);
+  if (rc != ADC_OK) return rc;
+  *cuda_source = v ? v->cuda.c_str() : nullptr;
+  return ADC_OK;
 }
 
 extern "C" size_t adc_jit_cubin_size(const adc_jit_module* J) { return J ? J->cubin.size() : 0; }
@@ -1390,9 +1894,15 @@ int jit_launch(adc_jit_module* J, int64_t grid, int64_t block, int64_t n, const 
       ADCB_CUDA(cudaMalloc(&J->dcnt, 7 * sizeof(unsigned long long)));
       J->dcnt_dev = dev;
     }
-    auto& fns = counted ? J->fns_counted : J->fns;
-    auto& libs = counted ? J->libs_counted : J->libs;
-    const std::vector<char>& cubin = counted ? J->cubin_counted : J->cubin;
+    adc_jit_module::Variant* sv = nullptr;
+    if (!counted) {
+      int rc = ADC_OK;
+      sv = static_variant(J, args, rc);
+      if (rc != ADC_OK) return rc;
+    }
+    auto& fns = sv ? sv->fns : counted ? J->fns_counted : J->fns;
+    auto& libs = sv ? sv->libs : counted ? J->libs_counted : J->libs;
+    const std::vector<char>& cubin = sv ? sv->cubin : counted ? J->cubin_counted : J->cubin;
     auto it = fns.find(dev);
     if (it == fns.end()) {
       cudaLibrary_t lib = nullptr;

@@ -41,6 +41,15 @@ class JitModule:
     def cuda_source(self) -> str:
         return lib.adc_jit_cuda_source(self._p).decode()
 
+    def static_source(self, integers=()):
+        """CUDA source of the static-tape variant a launch with these integer
+        arguments (kernel parameter order) runs, or None when it runs the
+        dynamic-tape kernel (tape entries in thread-private arrays)."""
+        vals = (ctypes.c_int64 * max(1, len(integers)))(*[int(v) for v in integers])
+        out = ctypes.c_char_p()
+        check(lib.adc_jit_static_variant(self._p, vals, len(integers), ctypes.byref(out)))
+        return out.value.decode() if out.value is not None else None
+
     @property
     def cubin_size(self) -> int:
         return lib.adc_jit_cubin_size(self._p)

@@ -242,7 +242,16 @@ def test_chi2_gaussian_recurrence(restate, model, q):
     g1, c1 = plan.gradient(q)
     assert np.all(np.abs(g2 - g1) <= 1e-13 * scale)
     assert abs(plan.chi2(q) - v2) <= 1e-13 * vscale
-    assert g2.tobytes() != g1.tobytes()  # the recurrence really ran
+    # the recurrence really ran: the chunk records (before the final rounding
+    # of the closed form) are not mode 1's
+    R = adc.record_len(q.size, True)
+    recs = []
+    for mode in (2, 1):
+        plan.set_precision(mode)
+        r = torch.zeros(plan.layout.nchunks * R, dtype=torch.float64, device="cuda")
+        plan.partials(list(q), True, r)
+        recs.append(host(r))
+    assert recs[0].tobytes() != recs[1].tobytes()
 
 
 @pytest.mark.parametrize("bins,model,np_", [(100_003, "gpoly", 6), (2_000_000, "gpoly", 6),

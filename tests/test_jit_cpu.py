@@ -95,3 +95,52 @@ global void k(real[] x, real[] y, real[] dx, real[] dy) {
 """
     m = adc.JitModule(src, "k")
     assert m.cubin_size > 0 and "v_double" in m.cuda_source
+
+
+def _fn_body(src, prefix):
+    """The definition text of the first device function whose name starts with prefix."""
+    i = src.index("__device__ void " + prefix)
+    i = src.index("{", src.index(")", i))
+    j = src.index("\n}\n", i)
+    return src[i:j]
+
+
+def test_static_tape_straight_line_and_branches():
+    """Tape elimination: branchy_grad's value and control
+    tapes sit at compile-time depths (both branches push one of each), so the
+    launch variant keeps them in locals — no per-frame tape arrays."""
+    m = adc.JitModule(MODULE, "k_branchy")
+    src = m.static_source()
+    assert src is not None
+    body = _fn_body(src, "fn_branchy_grad_s")
+    assert "_tv0 = v__ret0;" in body and "v__ret0 = _tv0;" in body
+    assert "_tc0 = (long long)1;" in body and "long long v__c0 = _tc0;" in body
+    assert "adc_push" not in body and "adc_pop" not in body and "tape[" not in body
+
+
+def test_static_tape_unrolls_constant_trip_counts():
+    """looped_grad pushes a data-dependent 1 or 2 values per iteration; with
+    the trip count n a specialised integer argument the loop is unrolled and
+    every push gets its own slot (2 per iteration, the branches padded), the
+    reverse loop reads them back in mirrored order.  Division by the literal 2
+    is the exact multiply by 0.5."""
+    m = adc.JitModule(MODULE, "k_looped")
+    body = _fn_body(m.static_source([10]), "fn_looped_grad_s")
+    assert "adc_push" not in body and "adc_pop" not in body and "tape[" not in body
+    assert body.count("_tc") and "double _tv19 = 0.0;" in body and "_tv20" not in body
+    assert "__dmul_rn(v_s, 0.5)" in body and "adc_div(v_s" not in body
+    # beyond the static slot bound (300 iterations) the dynamic tape stays
+    assert m.static_source([300]) is None
+    # kernels without integer parameters need no specialisation
+    assert adc.JitModule(MODULE, "k_rational").static_source() is not None
+
+
+def test_static_tape_falls_back_on_pop_underflow():
+    src = ("device host void f(real x, real[] _d_x) {\n  real a = __pop();\n  _d_x[0] += a;\n}\n"
+           "global void k(real[] x, real[] dx) {\n  integer i = blockIdx * blockDim + threadIdx;\n"
+           "  if (i < N) {\n    f(x[i], dx[i]);\n  }\n}\n")
+    m = adc.JitModule(src, "k")
+    s = m.static_source()
+    # the kernel frame is static, the callee keeps the dynamic tape (its run-time
+    # underflow error is the interpreter's)
+    assert s is not None and "adc_pop(tape, tp, ctx)" in s
