@@ -94,6 +94,22 @@ struct GPoly {
     mu = Q.q1;
     inv = Q.inv2;
   }
+  // Fast mode with the run recurrence (tile_bins REC): x, z and the Gaussian
+  // factor e come from the thread's run (x = x0 + k Dx, z = z0 + k Dz with one
+  // rounding each, e from the anchored product); the rest is eval's fast form.
+  template <bool GRAD>
+  __device__ static __forceinline__ void eval_rec(double x, const double* z, const double* e,
+                                                  const Reg& Q, double& m, double* bg) {
+    m = __fma_rn(Q.q0, e[0], __fma_rn(__fma_rn(Q.q5, x, Q.q4), x, Q.q3));
+    if constexpr (GRAD) {
+      bg[0] = e[0];
+      bg[1] = fmul(e[0], z[0]);  // without the factor q[0] / q[2] (Derive)
+      bg[2] = fmul(bg[1], z[0]);
+      bg[3] = 1.0;
+      bg[4] = x;
+      bg[5] = fmul(x, x);
+    }
+  }
   template <bool GRAD, bool FAST>
   __device__ static __forceinline__ void eval(double x, const Reg& Q, const double* tab, double& m,
                                               double* bg, const double* erec = nullptr) {
@@ -107,11 +123,12 @@ struct GPoly {
       const double z = fmul(fsub(x, q1), Q.inv2);                 // z = (x - q[1]) / q[2]
       const double e = erec != nullptr ? erec[0]                  // _t3 (recurrence)
                                        : exp_nonpos(fmul(fmul(-0.5, z), z), tab);
-      const double g = fmul(q0, e);
-      m = fadd(__fma_rn(__fma_rn(q5, x, q4), x, q3), g);
+      m = __fma_rn(q0, e, __fma_rn(__fma_rn(q5, x, q4), x, q3));
       if constexpr (GRAD) {
+        // _d_q[1], _d_q[2] without their common factor q[0] / q[2] (the
+        // chunk kernel multiplies the sums: Derive)
         bg[0] = e;
-        bg[1] = fmul(fmul(g, z), Q.inv2);
+        bg[1] = fmul(e, z);
         bg[2] = fmul(bg[1], z);
         bg[3] = 1.0;
         bg[4] = x;
@@ -176,6 +193,23 @@ struct GSum {
     mu = Q.q[3 * j + 1];
     inv = Q.inv[j];
   }
+  template <bool GRAD>
+  __device__ static __forceinline__ void eval_rec(double x, const double* z, const double* e,
+                                                  const Reg& Q, double& m, double* bg) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const double amp = Q.q[3 * j];
+      acc = __fma_rn(amp, e[j], acc);
+      if constexpr (GRAD) {  // without the factor amp / sg (Derive)
+        const double b1 = fmul(e[j], z[j]);
+        bg[3 * j + 2] = fmul(b1, z[j]);
+        bg[3 * j + 1] = b1;
+        bg[3 * j] = e[j];
+      }
+    }
+    m = acc;
+  }
   template <bool GRAD, bool FAST>
   __device__ static __forceinline__ void eval(double x, const Reg& Q, const double* tab, double& m,
                                               double* bg, const double* erec = nullptr) {
@@ -195,10 +229,11 @@ struct GSum {
       }
       acc = FAST ? __fma_rn(amp, e, acc) : fadd(acc, fmul(amp, e));    // acc = acc + amp*_t3
       if constexpr (GRAD && FAST) {
-        // _d_z = _t1 _r3 - 0.5 (_r3 z) = -(_r3 z) exactly (see GPoly::eval)
-        const double b1 = fmul(fmul(fmul(amp, e), z), Q.inv[j]);
-        bg[3 * j + 2] = fmul(b1, z);           // -(_r5 _q1 / sg)
-        bg[3 * j + 1] = b1;                    // _d_mu += -_r6
+        // _d_z = _t1 _r3 - 0.5 (_r3 z) = -(_r3 z) exactly (see GPoly::eval);
+        // the mu / sigma entries without their factor amp / sg (Derive)
+        const double b1 = fmul(e, z);
+        bg[3 * j + 2] = fmul(b1, z);           // -(_r5 _q1 / sg) * sg
+        bg[3 * j + 1] = b1;                    // _d_mu += -_r6, * sg
         bg[3 * j] = e;                         // _d_amp += _r1*_t3
       } else if constexpr (GRAD) {
         const double r3 = fmul(amp, e);        // _r3 = (amp*_r1)*_q0
@@ -224,6 +259,7 @@ struct GSum {
 // (C0 and the linear parameters' G0/G1 come from the once-per-plan K3l pass).
 // Full tiles skip the per-bin bounds test.
 constexpr int kPD = 4;
+constexpr int kPrefetchRows = 16;  // L2 prefetch distance of the tile passes, in bin rows
 
 // CTAs per SM the register budget is tuned for (spill-free at these counts).
 // (measured on B200: 2 x 256 threads with 128 registers beats 3 x 256 with 80
@@ -285,12 +321,19 @@ __device__ __forceinline__ void bin_term(const Chi2Pass& P, const typename M::Re
 // list of them (c = 0 is rare: 1% of the bins in the BASELINE histograms).
 // The tile records carry copies (copy_source) and the chunk kernel subtracts
 // the empty-bin sums (ZMerge).  No per-bin [c > 0] test, select or multiply.
+// Fast AD gradient passes (DER) do not accumulate S and A2 at all: the models
+// are sums of terms each linear in exactly one parameter of the set L (gpoly:
+// q0 e + q3 + q4 x + q5 x^2; gsum: sum_k amp_k e_k), so
+//   S = sum_{i in L} q_i G0_i,   A2 = sum_{i in L} q_i G2_i
+// exactly (Euler's identity for m); the chunk kernel derives them (Derive).
 template <class M, bool GRAD, bool FAST>
 __device__ __forceinline__ void bin_accumulate(const BinTerm<M, GRAD, FAST>& t, double* acc) {
   constexpr int NP = M::NP;
   constexpr int LIN0 = M::LIN0;
-  acc[0] += t.m;
-  acc[2] = __fma_rn(t.m, t.mc, acc[2]);
+  if constexpr (!(GRAD && FAST)) {
+    acc[0] += t.m;
+    acc[2] = __fma_rn(t.m, t.mc, acc[2]);
+  }
   // acc[3] (C0) comes from the K3l pre-pass
   if constexpr (GRAD) {
 #pragma unroll
@@ -337,26 +380,98 @@ __device__ __forceinline__ void tile_bins(const Chi2Pass& P, const typename M::R
   const int BPT = P.bpt;
   constexpr int STEP = ILP <= PD ? ILP : PD;
   static_assert(PD % 4 == 0 && 4 % STEP == 0, "ring depth / step");
+  double jh = fadd((double)base, 0.5);  // advanced by 256.0 per bin: exact integers + 0.5
+  [[maybe_unused]] double rP[REC ? M::NG : 1], rA[REC ? M::NG : 1], rz0[REC ? M::NG : 1];
+  [[maybe_unused]] double x0 = 0.0, kd = 0.0;
+  if constexpr (REC) {
+    x0 = fadd(P.lo, fmul(jh, P.width));
+#pragma unroll
+    for (int c = 0; c < M::NG; ++c) {
+      double mu, inv;
+      M::gauss(QR, c, mu, inv);
+      rz0[c] = fmul(fsub(x0, mu), inv);  // the model's own z at bin 0
+      rP[c] = exp_nonpos(fmul(fmul(-0.5, rz0[c]), rz0[c]), tab);
+      rA[c] = exp(-fmul(rz0[c], rdl[c]));
+    }
+  }
+  if constexpr (REC && !CHECK && !NUM && PD == 4) {
+    // A full tile with the run recurrence (the default gradient and value
+    // passes): the same bins and arithmetic as the general loop below, with
+    // the index work hoisted.  Two register sets of 1/c values (blocks of 4
+    // rows) alternate, so a block's loads land directly in the registers that
+    // consume them (no ring copies); thread 0 keeps the CTA's rows 16 ahead
+    // coming into L2 with one bulk prefetch (TMA unit) per 8 KB block, into
+    // the CTA's next tile past this one's end.
+    const int nblk = BPT / 4;
+    const double* pn = P.icounts + base;
+    const double dx = fmul(256.0, P.width);
+    const int64_t tile_base = base - threadIdx.x;
+    const double* pf = P.icounts + tile_base + (int64_t)kPrefetchRows * kTileThreads;
+    const double* pf_end = P.icounts + tile_base + (int64_t)BPT * kTileThreads;
+    const int64_t pf_shift = (int64_t)(gridDim.x - 1) * BPT * kTileThreads;
+    const double* bin_end = P.icounts + P.bin_end;
+    double ra[4], rb[4];
+    auto load = [&](double* r, int blk) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) r[u] = ld_stream(pn + ((int64_t)blk * 4 + u) * kTileThreads);
+    };
+    auto block = [&](const double* r, int blk) {
+      if (threadIdx.x == 0) {
+        if (pf >= pf_end && pf < pf_end + 4 * kTileThreads) pf += pf_shift;
+        if (pf + 4 * kTileThreads <= bin_end) bulk_prefetch_l2(pf, 4 * kTileThreads * 8);
+        pf += 4 * kTileThreads;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = 4 * blk + u;
+        BinTerm<M, GRAD, FAST> t;
+        double e[M::NG], z[M::NG];
+        const double x = __fma_rn(kd, dx, x0);
+#pragma unroll
+        for (int g = 0; g < M::NG; ++g) {
+          e[g] = fmul(rP[g], rtab[g * kRecMaxBpt + k]);
+          rP[g] = fmul(rP[g], rA[g]);
+          z[g] = __fma_rn(kd, rdl[g], rz0[g]);
+        }
+        M::template eval_rec<GRAD>(x, z, e, QR, t.m, t.bg);
+        t.mc = t.m * r[u];
+        bin_accumulate<M, GRAD, FAST>(t, acc);
+        kd = fadd(kd, 1.0);
+      }
+    };
+    load(ra, 0);
+    if (nblk > 1) load(rb, 1);
+    for (int b = 0; b < nblk; b += 2) {
+      block(ra, b);
+      if (b + 2 < nblk) load(ra, b + 2);
+      if (b + 1 < nblk) {
+        block(rb, b + 1);
+        if (b + 3 < nblk) load(rb, b + 3);
+      }
+    }
+    return;
+  }
   double ring[PD];
 #pragma unroll
   for (int k = 0; k < PD; ++k) {
     const int64_t j = base + (int64_t)k * kTileThreads;
     ring[k] = (k < BPT && (!CHECK || j < P.bin_end)) ? ld_stream(P.icounts + j) : 0.0;
   }
-  double jh = fadd((double)base, 0.5);  // advanced by 256.0 per bin: exact integers + 0.5
-  [[maybe_unused]] double rP[REC ? M::NG : 1], rA[REC ? M::NG : 1];
-  if constexpr (REC) {
-    const double x0 = fadd(P.lo, fmul(jh, P.width));
-#pragma unroll
-    for (int c = 0; c < M::NG; ++c) {
-      double mu, inv;
-      M::gauss(QR, c, mu, inv);
-      const double z0 = fmul(fsub(x0, mu), inv);  // the model's own z at bin 0
-      rP[c] = exp_nonpos(fmul(fmul(-0.5, z0), z0), tab);
-      rA[c] = exp(-fmul(z0, rdl[c]));
-    }
-  }
+  // L2 prefetch kPrefetchRows bin rows ahead of the register ring: lanes 0-7
+  // each take one 128-byte line of this warp's 4 x 256 bytes of that block
+  // (past the tile's end: the same rows of the CTA's next tile), so the
+  // ring's loads hit L2 instead of waiting on HBM.
+  const int64_t tile_base = base - threadIdx.x;
+  const int64_t next_base = tile_base + (int64_t)gridDim.x * BPT * kTileThreads;
+  const int pl = threadIdx.x & 31;
+  const int64_t poff = (int64_t)(pl >> 1) * kTileThreads + (threadIdx.x & ~31) + (pl & 1) * 16;
   for (int k0 = 0; k0 < BPT; k0 += PD) {
+    if (pl < 8) {
+      const int kp = k0 + kPrefetchRows;
+      const int64_t pa = (kp < BPT ? tile_base + (int64_t)kp * kTileThreads
+                                   : next_base + (int64_t)(kp - BPT) * kTileThreads) + poff;
+      if (pa < P.bin_end) prefetch_l2(P.icounts + pa);
+    }
 #pragma unroll
     for (int kk = 0; kk < PD; kk += STEP) {
       if (PD > 4 && kk >= 4 && k0 + kk >= BPT) break;  // BPT % 4 == 0 (uniform)
@@ -384,14 +499,20 @@ __device__ __forceinline__ void tile_bins(const Chi2Pass& P, const typename M::R
           }
         } else if constexpr (REC) {
           if (valid[u]) {
-            double e[M::NG];
+            // bin k of the run: x = x0 + k (256 width), z = z0 + k D (one
+            // rounding each; D = 256 width / sigma = rdl)
+            double e[M::NG], z[M::NG];
+            const double x = __fma_rn(kd, fmul(256.0, P.width), x0);
 #pragma unroll
             for (int g = 0; g < M::NG; ++g) {
               e[g] = fmul(rP[g], rtab[g * kRecMaxBpt + k]);
               rP[g] = fmul(rP[g], rA[g]);
+              z[g] = __fma_rn(kd, rdl[g], rz0[g]);
             }
-            bin_term<M, GRAD, FAST>(P, QR, tab, jh, c, t[u], e);
+            M::template eval_rec<GRAD>(x, z, e, QR, t[u].m, t[u].bg);
+            t[u].mc = t[u].m * c;
           }
+          kd = fadd(kd, 1.0);
         } else {
           if (valid[u]) bin_term<M, GRAD, FAST>(P, QR, tab, jh, c, t[u]);
         }
@@ -408,11 +529,12 @@ __device__ __forceinline__ void tile_bins(const Chi2Pass& P, const typename M::R
 
 // Record entries a tile pass leaves at zero: C0 (always) and, for the AD
 // gradient, the linear parameters' G0/G1 (all merged from the K3l pre-pass).
-template <class M, bool GRAD, bool NUM>
+template <class M, bool GRAD, bool NUM, bool FAST>
 __host__ __device__ constexpr bool pass_zero_entry(int v) {
   constexpr int NP = M::NP, L0 = M::LIN0;
-  return v == 3 || (GRAD && !NUM &&
-                    ((v >= 4 + L0 && v < 4 + NP) || (v >= 4 + NP + L0 && v < 4 + 2 * NP)));
+  return v == 3 || (GRAD && FAST && !NUM && v <= 2) ||  // S, A1, A2 derived (DER)
+         (GRAD && !NUM &&
+          ((v >= 4 + L0 && v < 4 + NP) || (v >= 4 + NP + L0 && v < 4 + 2 * NP)));
 }
 
 template <class M, bool GRAD, bool FAST, int MINB = tile_min_blocks<M, GRAD>(),
@@ -471,12 +593,14 @@ __global__ void __launch_bounds__(kTileThreads, MINB) chi2_tile_kernel(Chi2Pass 
   const int64_t TB = (int64_t)BPT * kTileThreads;
   for (int64_t tile = P.tile_begin + blockIdx.x; tile < P.tile_end; tile += gridDim.x) {
     const int64_t base = tile * TB + threadIdx.x;
-    {  // the next tile of this CTA into L2 while this one computes
-      const int64_t nb = base + (int64_t)gridDim.x * TB;
-#pragma unroll 4
-      for (int k = 0; k < BPT; k += 4)
-        if (nb + (int64_t)k * kTileThreads < P.bin_end)
-          prefetch_l2(P.icounts + nb + (int64_t)k * kTileThreads);
+    if (tile == P.tile_begin + blockIdx.x) {  // the first rows of the CTA's first tile
+      const int pl = threadIdx.x & 31;
+      if (pl < 8)
+        for (int k = (pl >> 1); k < min(kPrefetchRows, BPT); k += 4) {
+          const int64_t pa = tile * TB + (int64_t)k * kTileThreads + (threadIdx.x & ~31) +
+                             (pl & 1) * 16;
+          if (pa < P.bin_end) prefetch_l2(P.icounts + pa);
+        }
     }
     double acc[R];
 #pragma unroll
@@ -495,7 +619,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) chi2_tile_kernel(Chi2Pass 
     // exact zeros and skip the tree
 #pragma unroll
     for (int v = 0; v < R; ++v) {
-      if (!pass_zero_entry<M, GRAD, NUM>(v) && copy_source<M, GRAD, NUM>(v) < 0) {
+      if (!pass_zero_entry<M, GRAD, NUM, FAST>(v) && copy_source<M, GRAD, NUM>(v) < 0) {
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1)
           acc[v] += __shfl_down_sync(0xffffffffu, acc[v], off);
@@ -503,7 +627,8 @@ __global__ void __launch_bounds__(kTileThreads, MINB) chi2_tile_kernel(Chi2Pass 
     }
     if (lane == 0) {
 #pragma unroll
-      for (int v = 0; v < R; ++v) red[warp][v] = pass_zero_entry<M, GRAD, NUM>(v) ? 0.0 : acc[v];
+      for (int v = 0; v < R; ++v)
+        red[warp][v] = pass_zero_entry<M, GRAD, NUM, FAST>(v) ? 0.0 : acc[v];
     }
     __syncthreads();
     for (int v = threadIdx.x; v < R; v += kTileThreads) {
@@ -602,9 +727,11 @@ __global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P,
 #pragma unroll
         for (int cc = 0; cc < CG; ++cc) a0[cc] = a2[cc] = 0.0;
         double jh = fadd((double)base, 0.5);
-        [[maybe_unused]] double rP[REC ? CG * M::NG : 1], rA[REC ? CG * M::NG : 1];
+        [[maybe_unused]] double rP[REC ? CG * M::NG : 1], rA[REC ? CG * M::NG : 1],
+            rz0[REC ? CG * M::NG : 1];
+        [[maybe_unused]] double x0 = 0.0, kd = 0.0;
         if constexpr (REC) {  // the anchors of tile_bins, per candidate
-          const double x0 = fadd(P.lo, fmul(jh, P.width));
+          x0 = fadd(P.lo, fmul(jh, P.width));
 #pragma unroll
           for (int cc = 0; cc < CG; ++cc)
 #pragma unroll
@@ -612,23 +739,26 @@ __global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P,
               double mu, inv;
               M::gauss(QR[cc], c, mu, inv);
               const double z0 = fmul(fsub(x0, mu), inv);
+              rz0[cc * M::NG + c] = z0;
               rP[cc * M::NG + c] = exp_nonpos(fmul(fmul(-0.5, z0), z0), tab);
               rA[cc * M::NG + c] = exp(-fmul(z0, rdl[(c0 + cc) * M::NG + c]));
             }
         }
         auto bin = [&](int k, double ic) {
           const double x = fadd(P.lo, fmul(jh, P.width));
+          [[maybe_unused]] const double xr = REC ? __fma_rn(kd, fmul(256.0, P.width), x0) : 0.0;
 #pragma unroll
           for (int cc = 0; cc < CG; ++cc) {
             double m, bg[1];
-            if (REC && ruse[c0 + cc]) {
-              double e[M::NG];
+            if (REC && ruse[c0 + cc]) {  // tile_bins' REC arithmetic, per candidate
+              double e[M::NG], z[M::NG];
 #pragma unroll
               for (int c = 0; c < M::NG; ++c) {
                 e[c] = fmul(rP[cc * M::NG + c], rtab[((c0 + cc) * M::NG + c) * kRecMaxBpt + k]);
                 rP[cc * M::NG + c] = fmul(rP[cc * M::NG + c], rA[cc * M::NG + c]);
+                z[c] = __fma_rn(kd, rdl[(c0 + cc) * M::NG + c], rz0[cc * M::NG + c]);
               }
-              M::template eval<false, true>(x, QR[cc], tab, m, bg, e);
+              M::template eval_rec<false>(xr, z, e, QR[cc], m, bg);
             } else {
               M::template eval<false, true>(x, QR[cc], tab, m, bg);
             }
@@ -641,6 +771,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) chi2_multi_kernel(Chi2Pass P,
           const int64_t j = base + (int64_t)k * kTileThreads;
           if (j < P.bin_end) bin(k, ld_stream(P.icounts + j));
           jh = fadd(jh, (double)kTileThreads);
+          if constexpr (REC) kd = fadd(kd, 1.0);
         }
         // this group's fixed shuffle trees (A1 is a copy of S: copy_source)
 #pragma unroll
@@ -803,13 +934,15 @@ __global__ void __launch_bounds__(kEmptyThreads) chi2_empty_fill_kernel(Chi2Pass
 }
 
 // ---- K3z: the model (and nonlinear gradient) sums over a chunk's empty bins -----
-// One CTA per (local chunk, batch member / candidate); fixed per-thread order,
-// shuffle tree and cross-warp tree.  zws[y][chunk][ZL]: [sum m, sum dm_i (i < ZL-1)].
+// One CTA per (local chunk, segment of its list, batch member / candidate);
+// fixed per-thread order, shuffle tree and cross-warp tree.
+// zws[y][chunk][seg][ZL]: [sum m, sum dm_i (i < ZL-1)]; the chunk kernel adds
+// the segments in order (ZMerge).
 // multi: blockIdx.y is a line-search candidate (q at qdev + y kQDoubles);
 // otherwise a batch member (qdev + y q_stride).
 template <class M, bool GRAD, bool FAST>
 __global__ void __launch_bounds__(kTileThreads) chi2_empty_kernel(Chi2Pass P, int64_t nchunks,
-                                                                  bool multi) {
+                                                                  int nseg, bool multi) {
   constexpr int ZL = GRAD ? 1 + M::LIN0 : 1;
   const int y = blockIdx.y;
   if (multi && P.ncand_dev != nullptr && y >= *P.ncand_dev) return;  // uniform over the CTA
@@ -828,7 +961,9 @@ __global__ void __launch_bounds__(kTileThreads) chi2_empty_kernel(Chi2Pass P, in
   double acc[ZL];
 #pragma unroll
   for (int v = 0; v < ZL; ++v) acc[v] = 0.0;
-  const int64_t o0 = P.empty_off[blockIdx.x], o1 = P.empty_off[blockIdx.x + 1];
+  const int64_t chunk = blockIdx.x / nseg, seg = blockIdx.x % nseg;
+  const int64_t c0 = P.empty_off[chunk], c1 = P.empty_off[chunk + 1];
+  const int64_t o0 = c0 + (c1 - c0) * seg / nseg, o1 = c0 + (c1 - c0) * (seg + 1) / nseg;
   for (int64_t t = o0 + threadIdx.x; t < o1; t += kTileThreads) {
     const double jh = fadd((double)P.empty_idx[t], 0.5);
     const double x = fadd(P.lo, fmul(jh, P.width));  // Histogram::center, as bin_term
@@ -852,8 +987,42 @@ __global__ void __launch_bounds__(kTileThreads) chi2_empty_kernel(Chi2Pass P, in
     const int v = threadIdx.x;
     const double s01 = red[0][v] + red[1][v], s23 = red[2][v] + red[3][v];
     const double s45 = red[4][v] + red[5][v], s67 = red[6][v] + red[7][v];
-    P.zws[((int64_t)y * nchunks + blockIdx.x) * ZL + v] = (s01 + s23) + (s45 + s67);
+    P.zws[(((int64_t)y * nchunks + chunk) * nseg + seg) * ZL + v] = (s01 + s23) + (s45 + s67);
   }
+}
+
+// Fast AD gradient passes: what the chunk kernel derives from the chunk's sums
+// (bin_accumulate): the width-derivative entries (G0/G1/G2 of the parameters
+// in `sc`) times 1/q[sinv] (the eval leaves that common factor out), then
+// S = sum_{i in lin} q_i G0_i, A2 = sum_{i in lin} q_i G2_i, A1 = S - Z.
+struct Derive {
+  const double* qdev = nullptr;  // QDev of batch member blockIdx.y at qdev + y q_stride
+  int64_t q_stride = 0;
+  int np = 0, nl = 0, ns = 0;
+  signed char lin[kMaxNp];
+  signed char sc[kMaxNp], sq[kMaxNp], sinv[kMaxNp];  // entry sc times q[sq] / q[sinv]
+};
+
+template <class M>
+Derive make_derive(const Chi2Pass& P) {
+  Derive d;
+  d.qdev = P.qdev;
+  d.q_stride = P.q_stride;
+  d.np = M::NP;
+  if constexpr (std::is_same<M, GPoly>::value) {
+    const signed char lin[] = {0, 3, 4, 5};
+    for (signed char i : lin) d.lin[d.nl++] = i;
+    d.sc[d.ns] = 1, d.sq[d.ns] = 0, d.sinv[d.ns++] = 2;
+    d.sc[d.ns] = 2, d.sq[d.ns] = 0, d.sinv[d.ns++] = 2;
+  } else {
+    for (int j = 0; j < M::NG; ++j) {
+      const signed char a = (signed char)(3 * j), w = (signed char)(3 * j + 2);
+      d.lin[d.nl++] = a;
+      d.sc[d.ns] = (signed char)(3 * j + 1), d.sq[d.ns] = a, d.sinv[d.ns++] = w;
+      d.sc[d.ns] = w, d.sq[d.ns] = a, d.sinv[d.ns++] = w;
+    }
+  }
+  return d;
 }
 
 // The chunk kernel's subtraction of the empty-bin sums (copy_source entries):
@@ -861,20 +1030,28 @@ __global__ void __launch_bounds__(kTileThreads) chi2_empty_kernel(Chi2Pass P, in
 // multi records [C0, (S, A1, A2) x ncand]: candidate c's A1 -= z[c][chunk][0].
 struct ZMerge {
   const double* z = nullptr;
-  int zl = 0, np = 0;
+  int zl = 0, np = 0, nseg = 1;
   bool multi = false;
   int64_t nchunks = 0;
 };
 
+// the empty-bin sum of entry k of member y: its segments added in order
+__device__ __forceinline__ double zsum(const ZMerge& zm, int64_t y, int64_t chunk, int k) {
+  const double* z = zm.z + ((y * zm.nchunks + chunk) * zm.nseg) * zm.zl + k;
+  double s = z[0];
+  for (int g = 1; g < zm.nseg; ++g) s = s + z[(int64_t)g * zm.zl];
+  return s;
+}
+
 __device__ __forceinline__ double zmerge(const ZMerge& zm, int64_t chunk, int v, double a) {
   if (zm.z == nullptr) return a;
   if (zm.multi) {
-    if (v >= 1 && (v - 1) % 3 == 1) return a - zm.z[((v - 1) / 3) * zm.nchunks + chunk];
+    if (v >= 1 && (v - 1) % 3 == 1) return a - zsum(zm, (v - 1) / 3, chunk, 0);
     return a;
   }
-  const double* z = zm.z + (blockIdx.y * zm.nchunks + chunk) * zm.zl;
-  if (v == 1) return a - z[0];
-  if (v >= 4 + zm.np && v < 4 + zm.np + zm.zl - 1) return a - z[1 + v - 4 - zm.np];
+  if (v == 1) return a - zsum(zm, blockIdx.y, chunk, 0);
+  if (v >= 4 + zm.np && v < 4 + zm.np + zm.zl - 1)
+    return a - zsum(zm, blockIdx.y, chunk, 1 + v - 4 - zm.np);
   return a;
 }
 
@@ -900,7 +1077,7 @@ __global__ void __launch_bounds__(kChunkThreads) chi2_chunk_kernel(
     const double* __restrict__ tile_ws, int64_t ntiles, int R, int chunk_tiles,
     double* __restrict__ records, LinMerge lm = LinMerge{}, PeerPublish pub = PeerPublish{},
     const int* ncand_dev = nullptr, int64_t ws_stride = 0, int64_t rec_stride = 0,
-    ZMerge zm = ZMerge{}) {
+    ZMerge zm = ZMerge{}, Derive dv = Derive{}) {
   if (ncand_dev != nullptr) R = 1 + 3 * *ncand_dev;  // multi records sized on the device
   tile_ws += blockIdx.y * ws_stride;  // batched passes (blockIdx.y = member)
   records += blockIdx.y * rec_stride;
@@ -910,6 +1087,7 @@ __global__ void __launch_bounds__(kChunkThreads) chi2_chunk_kernel(
   const bool publish = pub.peer_gather != nullptr;  // uniform over the grid
   __shared__ unsigned long long s_q;
   __shared__ bool s_last;
+  __shared__ double srec[4 + 3 * kMaxNp];  // Derive: the chunk's record, staged
   if (publish) {
     if (threadIdx.x == 0) s_q = *pub.seq + 1;
     __syncthreads();
@@ -933,9 +1111,42 @@ __global__ void __launch_bounds__(kChunkThreads) chi2_chunk_kernel(
     }
     if (lane == 0) {
       a = zmerge(zm, chunk, v, a);
-      records[chunk * R + v] = a;
+      if (dv.nl > 0) {
+        srec[v] = a;
+      } else {
+        records[chunk * R + v] = a;
+        if (publish)
+          for (int r = 0; r < pub.world; ++r) peer_slot(pub, r, s_q)[chunk * R + v] = a;
+      }
+    }
+  }
+  if (dv.nl > 0) {  // uniform over the grid
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double* q = dv.qdev + blockIdx.y * dv.q_stride;  // QDev: q[kMaxNp], inv[kMaxNp]
+      const int np = dv.np;
+      for (int k = 0; k < dv.ns; ++k) {
+        const double inv = q[dv.sq[k]] * q[kMaxNp + dv.sinv[k]];
+        const int i = dv.sc[k];
+        srec[4 + i] = srec[4 + i] * inv;
+        srec[4 + np + i] = srec[4 + np + i] * inv;
+        srec[4 + 2 * np + i] = srec[4 + 2 * np + i] * inv;
+      }
+      double S = 0.0, A2 = 0.0;
+      for (int k = 0; k < dv.nl; ++k) {
+        const int i = dv.lin[k];
+        S = __fma_rn(q[i], srec[4 + i], S);
+        A2 = __fma_rn(q[i], srec[4 + 2 * np + i], A2);
+      }
+      srec[0] = S;
+      srec[1] = S + srec[1];  // the tile records' A1 is 0: minus the empty-bin sum
+      srec[2] = A2;
+    }
+    __syncthreads();
+    for (int v = threadIdx.x; v < R; v += kChunkThreads) {
+      records[chunk * R + v] = srec[v];
       if (publish)
-        for (int r = 0; r < pub.world; ++r) peer_slot(pub, r, s_q)[chunk * R + v] = a;
+        for (int r = 0; r < pub.world; ++r) peer_slot(pub, r, s_q)[chunk * R + v] = srec[v];
     }
   }
   if (publish) {
@@ -998,15 +1209,19 @@ static void launch_tiles_m(const Chi2Pass& P, bool grad, int prec, bool num, dim
 
 // K3z for a pass: grid (local chunks, ny).  Returns the ZMerge for its chunk kernel.
 template <class M>
-static void launch_empty_m(const Chi2Pass& P, bool grad, bool fast, int64_t nchunks, int ny,
-                           bool multi, cudaStream_t s) {
-  const dim3 grid((unsigned)nchunks, (unsigned)ny);
+static void launch_empty_m(const Chi2Pass& P, bool grad, bool fast, int64_t nchunks, int nseg,
+                           int ny, bool multi, cudaStream_t s) {
+  const dim3 grid((unsigned)(nchunks * nseg), (unsigned)ny);
   if (grad) {
-    if (fast) chi2_empty_kernel<M, true, true><<<grid, kTileThreads, 0, s>>>(P, nchunks, multi);
-    else chi2_empty_kernel<M, true, false><<<grid, kTileThreads, 0, s>>>(P, nchunks, multi);
+    if (fast)
+      chi2_empty_kernel<M, true, true><<<grid, kTileThreads, 0, s>>>(P, nchunks, nseg, multi);
+    else
+      chi2_empty_kernel<M, true, false><<<grid, kTileThreads, 0, s>>>(P, nchunks, nseg, multi);
   } else {
-    if (fast) chi2_empty_kernel<M, false, true><<<grid, kTileThreads, 0, s>>>(P, nchunks, multi);
-    else chi2_empty_kernel<M, false, false><<<grid, kTileThreads, 0, s>>>(P, nchunks, multi);
+    if (fast)
+      chi2_empty_kernel<M, false, true><<<grid, kTileThreads, 0, s>>>(P, nchunks, nseg, multi);
+    else
+      chi2_empty_kernel<M, false, false><<<grid, kTileThreads, 0, s>>>(P, nchunks, nseg, multi);
   }
 }
 
@@ -1014,16 +1229,20 @@ static int launch_empty(const Chi2Pass& P, int model, int np, bool grad, bool fa
                         int64_t nchunks, int ny, bool multi, cudaStream_t s, ZMerge& zm) {
   if (P.empty_off == nullptr || P.zws == nullptr)
     return fail(ADC_E_ARG, "chi2 pass: the plan's empty-bin lists are not built");
+  // a fixed number of segments per chunk list (not a function of the device
+  // or the split, so the same sums on every rank and world size)
+  const int nseg = kEmptySegs;
+  zm.nseg = nseg;
   if (model == ADC_MODEL_GPOLY) {
-    launch_empty_m<GPoly>(P, grad, fast, nchunks, ny, multi, s);
+    launch_empty_m<GPoly>(P, grad, fast, nchunks, nseg, ny, multi, s);
     zm.zl = grad ? 1 + GPoly::LIN0 : 1;
   } else {
     switch (np / 3) {
-      case 1: launch_empty_m<GSum<1>>(P, grad, fast, nchunks, ny, multi, s); break;
-      case 2: launch_empty_m<GSum<2>>(P, grad, fast, nchunks, ny, multi, s); break;
-      case 3: launch_empty_m<GSum<3>>(P, grad, fast, nchunks, ny, multi, s); break;
-      case 4: launch_empty_m<GSum<4>>(P, grad, fast, nchunks, ny, multi, s); break;
-      case 8: launch_empty_m<GSum<8>>(P, grad, fast, nchunks, ny, multi, s); break;
+      case 1: launch_empty_m<GSum<1>>(P, grad, fast, nchunks, nseg, ny, multi, s); break;
+      case 2: launch_empty_m<GSum<2>>(P, grad, fast, nchunks, nseg, ny, multi, s); break;
+      case 3: launch_empty_m<GSum<3>>(P, grad, fast, nchunks, nseg, ny, multi, s); break;
+      case 4: launch_empty_m<GSum<4>>(P, grad, fast, nchunks, nseg, ny, multi, s); break;
+      case 8: launch_empty_m<GSum<8>>(P, grad, fast, nchunks, nseg, ny, multi, s); break;
       default: return fail(ADC_E_ARG, "gsum: unsupported component count");
     }
     zm.zl = grad ? 1 + np : 1;
@@ -1075,9 +1294,24 @@ int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, int prec,
   if (int rc = launch_empty(P, model, np, grad && !numeric, prec != 0, nchunks, nbatch, false, s,
                             zm))
     return rc;
+  Derive dv;
+  if (grad && !numeric && prec != 0) {
+    if (model == ADC_MODEL_GPOLY) {
+      dv = make_derive<GPoly>(P);
+    } else {
+      switch (np / 3) {
+        case 1: dv = make_derive<GSum<1>>(P); break;
+        case 2: dv = make_derive<GSum<2>>(P); break;
+        case 3: dv = make_derive<GSum<3>>(P); break;
+        case 4: dv = make_derive<GSum<4>>(P); break;
+        case 8: dv = make_derive<GSum<8>>(P); break;
+        default: return fail(ADC_E_ARG, "gsum: unsupported component count");
+      }
+    }
+  }
   chi2_chunk_kernel<<<dim3((unsigned)nchunks, (unsigned)nbatch), kChunkThreads, 0, s>>>(
       P.tile_ws, ntiles, R, (int)chunk_tiles, records, lm, pub ? *pub : PeerPublish{}, nullptr,
-      P.ws_stride, rec_stride, zm);
+      P.ws_stride, rec_stride, zm, dv);
   ADCB_CUDA(cudaGetLastError());
   return ADC_OK;
 }

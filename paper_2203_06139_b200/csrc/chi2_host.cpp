@@ -172,7 +172,7 @@ struct adc_chi2_plan {
   int64_t empty_cap = 0;
   int64_t* empty_off = nullptr;  // [local chunks + 1]
   int64_t* empty_cnt = nullptr;  // [local chunks]
-  double* zws = nullptr;         // [kMultiMax][maxc][1 + kMaxNp]
+  double* zws = nullptr;         // [kMultiMax][maxc][kEmptySegs][1 + kMaxNp]
 };
 
 namespace {
@@ -301,7 +301,8 @@ int ensure_lin(adc_chi2_plan* P, cudaStream_t s) {
   if (P->empty_off == nullptr) {
     ADCB_CUDA(cudaMalloc(&P->empty_off, (size_t)(nrec + 1) * sizeof(int64_t)));
     ADCB_CUDA(cudaMalloc(&P->empty_cnt, (size_t)nrec * sizeof(int64_t)));
-    ADCB_CUDA(cudaMalloc(&P->zws, (size_t)kMultiMax * P->maxc * (1 + kMaxNp) * sizeof(double)));
+    ADCB_CUDA(cudaMalloc(&P->zws, (size_t)kMultiMax * P->maxc * kEmptySegs * (1 + kMaxNp) *
+                                      sizeof(double)));
   }
   const int64_t nloc = local_chunks(P);
   std::vector<int64_t> off((size_t)nloc + 1, 0);

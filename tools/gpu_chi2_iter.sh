@@ -9,9 +9,11 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:chi2
 python tools/ncu_summary.py $O/prof_chi2.ncu-rep > $O/ncu_summary.txt 2>&1
 python tools/ncu_fp64_per_unit.py $O/prof_chi2.ncu-rep 1e8 >> $O/ncu_summary.txt 2>&1
 timeout 600 python tools/probe_jit.py > $O/probe_jit.log 2>&1; tail -6 $O/probe_jit.log
-if [ -f tools/alt.sed ]; then
+for alt in tools/alt_*.sed; do
+  [ -f "$alt" ] || continue
+  name=$(basename $alt .sed)
   rm -rf /tmp/alt && mkdir /tmp/alt && cp -r paper_2203_06139_b200 include tools oracle /tmp/alt/ && cd /tmp/alt
-  sed -i -f tools/alt.sed paper_2203_06139_b200/csrc/chi2.cu && make -s -j8 -C paper_2203_06139_b200/csrc > /tmp/alt_build.log 2>&1
-  timeout 300 python tools/probe_chi2.py 100000000 20 > $GRAFT_REPO_ROOT/$O/probe_chi2_alt.log 2>&1; tail -3 $GRAFT_REPO_ROOT/$O/probe_chi2_alt.log
+  sed -i -f $alt paper_2203_06139_b200/csrc/chi2.cu && make -s -j8 -C paper_2203_06139_b200/csrc > /tmp/alt_build.log 2>&1
+  timeout 300 python tools/probe_chi2.py 100000000 20 > $GRAFT_REPO_ROOT/$O/probe_chi2_$name.log 2>&1; echo "$name: $(tail -1 $GRAFT_REPO_ROOT/$O/probe_chi2_$name.log)"
   cd $GRAFT_REPO_ROOT
-fi
+done
