@@ -449,8 +449,7 @@ __device__ __forceinline__ void tile_bins(const Chi2Pass& P, const typename M::R
         if (b + 3 < nblk) load(rb, b + 3);
       }
     }
-    return;
-  }
+  } else {
   double ring[PD];
 #pragma unroll
   for (int k = 0; k < PD; ++k) {
@@ -525,6 +524,7 @@ __device__ __forceinline__ void tile_bins(const Chi2Pass& P, const typename M::R
       }
     }
   }
+  }  // the general loop
 }
 
 // Record entries a tile pass leaves at zero: C0 (always) and, for the AD
@@ -1267,6 +1267,15 @@ int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, int prec,
   // models, see tile_min_blocks), tiles grid-strided.
   const int64_t blocks = std::min<int64_t>(ntiles, (int64_t)sm_count() * (np <= 6 ? 2 : 1));
   const dim3 grid((unsigned)blocks, (unsigned)nbatch);
+  // The empty-bin side pass (K3z) does not depend on the tile kernel: with the
+  // plan's low-priority side stream it runs beside it (the block scheduler
+  // places its CTAs as the tile kernel's retire in the last partial wave),
+  // joined before the chunk kernel.
+  const bool fork = P.side_stream != nullptr;
+  if (fork) {
+    ADCB_CUDA(cudaEventRecord(P.ev_fork, s));
+    ADCB_CUDA(cudaStreamWaitEvent(P.side_stream, P.ev_fork, 0));
+  }
   if (model == ADC_MODEL_GPOLY) {
     launch_tiles_m<GPoly>(P, grad, prec, numeric, grid, s);
   } else {
@@ -1291,9 +1300,13 @@ int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, int prec,
     lm.g1_pos = 4 + np + lin0;
   }
   ZMerge zm;
-  if (int rc = launch_empty(P, model, np, grad && !numeric, prec != 0, nchunks, nbatch, false, s,
-                            zm))
+  if (int rc = launch_empty(P, model, np, grad && !numeric, prec != 0, nchunks, nbatch, false,
+                            fork ? P.side_stream : s, zm))
     return rc;
+  if (fork) {
+    ADCB_CUDA(cudaEventRecord(P.ev_join, P.side_stream));
+    ADCB_CUDA(cudaStreamWaitEvent(s, P.ev_join, 0));
+  }
   Derive dv;
   if (grad && !numeric && prec != 0) {
     if (model == ADC_MODEL_GPOLY) {

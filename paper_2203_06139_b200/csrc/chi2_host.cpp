@@ -126,6 +126,8 @@ struct adc_chi2_plan {
   int provider = ADC_PROVIDER_AD_REVERSE;  // of the gradient passes
   int device = 0;
   cudaStream_t stream = nullptr;       // plan-owned: graph replays
+  cudaStream_t side = nullptr;         // plan-owned, lowest priority: the empty-bin side pass
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t user_stream = nullptr;  // caller's (0 = legacy default): adc_cuda_chi2_partials
   double* qdev = nullptr;
   double* tile_ws = nullptr;
@@ -214,6 +216,9 @@ Chi2Pass make_pass(const adc_chi2_plan* P) {
   pass.empty_idx = P->empty_idx;
   pass.empty_off = P->empty_off;
   pass.zws = P->zws;
+  pass.side_stream = P->side;
+  pass.ev_fork = P->ev_fork;
+  pass.ev_join = P->ev_join;
   return pass;
 }
 
@@ -487,7 +492,15 @@ extern "C" int adc_cuda_chi2_plan_create(adc_chi2_plan** out, int32_t model, int
       1, (P->L.bin_end + P->L.tile_bins - 1) / P->L.tile_bins - P->L.chunk_begin * P->L.chunk_tiles);
   const int Rmax = adc_chi2_record_len(np, 1);
   cudaError_t e;
-  if ((e = cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking)) != cudaSuccess ||
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  // the pass stream at the highest priority, the side pass below it, so the
+  // block scheduler fills SMs with tile CTAs first
+  if ((e = cudaStreamCreateWithPriority(&P->stream, cudaStreamNonBlocking, prio_hi)) !=
+          cudaSuccess ||
+      (e = cudaStreamCreateWithPriority(&P->side, cudaStreamNonBlocking, prio_lo)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming)) != cudaSuccess ||
       (e = cudaMalloc(&P->qdev, qdev_bytes())) != cudaSuccess ||
       (e = cudaMalloc(&P->tile_ws, (size_t)ntiles_local * Rmax * sizeof(double))) != cudaSuccess ||
       (e = cudaMalloc(&P->records, (size_t)P->maxc * Rmax * sizeof(double))) != cudaSuccess ||
@@ -575,6 +588,9 @@ extern "C" int adc_cuda_chi2_plan_destroy(adc_chi2_plan* P) {
   if (P->fit_full) cudaFree(P->fit_full);
   if (P->fit_rbegin) cudaFree(P->fit_rbegin);
   if (P->stream) cudaStreamDestroy(P->stream);
+  if (P->side) cudaStreamDestroy(P->side);
+  if (P->ev_fork) cudaEventDestroy(P->ev_fork);
+  if (P->ev_join) cudaEventDestroy(P->ev_join);
   delete P;
   return ADC_OK;
 }

@@ -34,6 +34,10 @@ struct Chi2Pass {
   const int64_t* empty_idx = nullptr;
   const int64_t* empty_off = nullptr;
   double* zws = nullptr;
+  // optional: a low-priority stream (and fork / join events) the side pass
+  // runs on beside the tile kernel (chi2_enqueue)
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 // lin: per-chunk q-independent basis sums from chi2_lin_enqueue (gradient
