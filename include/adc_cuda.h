@@ -280,6 +280,11 @@ int adc_cuda_chi2_plan_layout(const adc_chi2_plan* plan, adc_chi2_layout* out);
  * written to records_dev + (chunk - chunk_begin) * record_len (device
  * pointer; NULL = the plan's own buffer, readable via
  * adc_cuda_chi2_plan_records).  Stream-ordered, asynchronous. */
+/* Measurement hook: with timing on, adc_cuda_chi2_partials records CUDA
+ * events around the pass's tile kernel (the dominant one) on its stream;
+ * adc_cuda_chi2_kernel_ms waits for and returns the last such duration. */
+int adc_cuda_chi2_set_kernel_timing(adc_chi2_plan* plan, int32_t on);
+int adc_cuda_chi2_kernel_ms(adc_chi2_plan* plan, float* ms);
 int adc_cuda_chi2_partials(adc_chi2_plan* plan, const double* q, int32_t want_grad,
                            double* records_dev);
 double* adc_cuda_chi2_plan_records(adc_chi2_plan* plan);

@@ -101,6 +101,8 @@ SIGNATURES = {
     "adc_cuda_chi2_plan_refresh": (ctypes.c_int, [_VP]),
     "adc_cuda_chi2_plan_layout": (ctypes.c_int, [_VP, ctypes.POINTER(Chi2Layout)]),
     "adc_cuda_chi2_partials": (ctypes.c_int, [_VP, _D, _I32, _VP]),
+    "adc_cuda_chi2_set_kernel_timing": (ctypes.c_int, [_VP, _I32]),
+    "adc_cuda_chi2_kernel_ms": (ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_float)]),
     "adc_cuda_chi2_plan_records": (_VP, [_VP]),
     "adc_cuda_chi2_gradient": (ctypes.c_int, [_VP, _D, _D, _D]),
     "adc_cuda_chi2": (ctypes.c_int, [_VP, _D, _D]),

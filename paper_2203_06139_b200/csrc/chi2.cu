@@ -1276,6 +1276,7 @@ int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, int prec,
     ADCB_CUDA(cudaEventRecord(P.ev_fork, s));
     ADCB_CUDA(cudaStreamWaitEvent(P.side_stream, P.ev_fork, 0));
   }
+  if (P.tk0) ADCB_CUDA(cudaEventRecord(P.tk0, s));
   if (model == ADC_MODEL_GPOLY) {
     launch_tiles_m<GPoly>(P, grad, prec, numeric, grid, s);
   } else {
@@ -1289,6 +1290,7 @@ int chi2_enqueue(const Chi2Pass& P, int model, int np, bool grad, int prec,
     }
   }
   ADCB_CUDA(cudaGetLastError());
+  if (P.tk1) ADCB_CUDA(cudaEventRecord(P.tk1, s));
   const int64_t nchunks = (ntiles + chunk_tiles - 1) / chunk_tiles;
   const int lin0 = model == ADC_MODEL_GPOLY ? GPoly::LIN0 : np;
   LinMerge lm;

@@ -128,6 +128,7 @@ struct adc_chi2_plan {
   cudaStream_t stream = nullptr;       // plan-owned: graph replays
   cudaStream_t side = nullptr;         // plan-owned, lowest priority: the empty-bin side pass
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t tk0 = nullptr, tk1 = nullptr;  // adc_cuda_chi2_set_kernel_timing
   cudaStream_t user_stream = nullptr;  // caller's (0 = legacy default): adc_cuda_chi2_partials
   double* qdev = nullptr;
   double* tile_ws = nullptr;
@@ -591,6 +592,8 @@ extern "C" int adc_cuda_chi2_plan_destroy(adc_chi2_plan* P) {
   if (P->side) cudaStreamDestroy(P->side);
   if (P->ev_fork) cudaEventDestroy(P->ev_fork);
   if (P->ev_join) cudaEventDestroy(P->ev_join);
+  if (P->tk0) cudaEventDestroy(P->tk0);
+  if (P->tk1) cudaEventDestroy(P->tk1);
   delete P;
   return ADC_OK;
 }
@@ -647,9 +650,37 @@ extern "C" int adc_cuda_chi2_partials(adc_chi2_plan* P, const double* q, int32_t
   if (int rc = ensure_lin(P, s)) return rc;
   fill_qdev(P->model, P->np, q, P->h_q);
   ADCB_CUDA(cudaMemcpyAsync(P->qdev, P->h_q, qdev_bytes(), cudaMemcpyHostToDevice, s));
-  return chi2_enqueue(make_pass(P), P->model, P->np, want_grad != 0, P->fast,
+  Chi2Pass pass = make_pass(P);
+  pass.tk0 = P->tk0;
+  pass.tk1 = P->tk1;
+  return chi2_enqueue(pass, P->model, P->np, want_grad != 0, P->fast,
                       P->L.chunk_tiles, records_dev ? records_dev : P->records, s, P->lin,
                       want_grad && numeric(P));
+}
+
+extern "C" int adc_cuda_chi2_set_kernel_timing(adc_chi2_plan* P, int32_t on) {
+  clear_error();
+  if (P == nullptr) return fail(ADC_E_ARG, "null plan");
+  ADCB_CUDA(cudaSetDevice(P->device));
+  if (on && P->tk0 == nullptr) {
+    ADCB_CUDA(cudaEventCreate(&P->tk0));
+    ADCB_CUDA(cudaEventCreate(&P->tk1));
+  } else if (!on && P->tk0 != nullptr) {
+    cudaEventDestroy(P->tk0);
+    cudaEventDestroy(P->tk1);
+    P->tk0 = P->tk1 = nullptr;
+  }
+  return ADC_OK;
+}
+
+extern "C" int adc_cuda_chi2_kernel_ms(adc_chi2_plan* P, float* ms) {
+  clear_error();
+  if (P == nullptr || ms == nullptr) return fail(ADC_E_ARG, "null argument");
+  if (P->tk0 == nullptr) return fail(ADC_E_ARG, "kernel timing is off");
+  ADCB_CUDA(cudaSetDevice(P->device));
+  ADCB_CUDA(cudaEventSynchronize(P->tk1));
+  ADCB_CUDA(cudaEventElapsedTime(ms, P->tk0, P->tk1));
+  return ADC_OK;
 }
 
 extern "C" int adc_cuda_chi2_gradient(adc_chi2_plan* P, const double* q, double* grad,

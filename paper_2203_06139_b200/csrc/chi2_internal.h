@@ -38,6 +38,9 @@ struct Chi2Pass {
   // runs on beside the tile kernel (chi2_enqueue)
   cudaStream_t side_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // optional (adc_cuda_chi2_partials with kernel timing on): recorded around
+  // the tile kernel on the pass stream
+  cudaEvent_t tk0 = nullptr, tk1 = nullptr;
 };
 
 // lin: per-chunk q-independent basis sums from chi2_lin_enqueue (gradient

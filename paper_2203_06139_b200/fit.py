@@ -203,6 +203,16 @@ class Chi2Plan:
         check(lib.adc_cuda_chi2_partials(self._p, dbl_array(q), 1 if want_grad else 0,
                                          dptr(records_dev) if records_dev is not None else None))
 
+    def tile_kernel_ms(self, q, want_grad: bool = True, records_dev=None) -> float:
+        """One pass (partials) with CUDA events around its tile kernel (the
+        dominant kernel); returns that kernel's duration in ms."""
+        check(lib.adc_cuda_chi2_set_kernel_timing(self._p, 1))
+        self.partials(q, want_grad, records_dev)
+        ms = ctypes.c_float()
+        check(lib.adc_cuda_chi2_kernel_ms(self._p, ctypes.byref(ms)))
+        check(lib.adc_cuda_chi2_set_kernel_timing(self._p, 0))
+        return ms.value
+
     @property
     def stream_ptr(self):
         return None
