@@ -816,6 +816,24 @@ def bench_jit(local, npts=100_000_000, steps=10, warm=3):
     return rec
 
 
+def bench_fig2b(local):
+    """The paper's Fig. 2b (the reference's bench_scaling, fit.cpp:427-458) at
+    B200 scale: gsum fits with K = 1, 2, 4, 8 Gaussians (3K parameters) over
+    1e6 bins with each gradient provider; per gradient evaluation (wall,
+    host included)."""
+    import paper_2203_06139_b200 as adc
+    rows = adc.bench_scaling(k_list=(1, 2, 4, 8), bins=1_000_000, events=1e8, seed=42, repeats=3)
+    table = {}
+    for r in rows:
+        t = table.setdefault(str(r.params), {})
+        t[r.provider] = round(r.median_wall_ns / 1e6 / max(1, r.grad_evals), 5)
+    for t in table.values():
+        if "ad-reverse" in t and "numeric" in t:
+            t["numeric_over_ad"] = round(t["numeric"] / t["ad-reverse"], 3)
+    return {"workload": "Fig. 2b analog: bench_scaling gsum K=1,2,4,8 over 1e6 bins, ms per "
+                        "gradient evaluation by provider (keys: parameter count)", "params": table}
+
+
 # ---------------------------------------------------------------------------- our arm
 def ours_arm(a, world, rank, local):
     import torch
@@ -854,6 +872,7 @@ def points_headline(a, world, rank, local, dist):
                     ("cfg3_fit_1e6", lambda: bench_fit(local)),
                     ("cfg4_gaussnd1000_1M", lambda: config_points("gaussnd1000", local))] + jobs
             jobs.append(("jit_corpus", lambda: bench_jit(local)))
+            jobs.append(("fig2b_bench_scaling", lambda: bench_fig2b(local)))
         for name, job in jobs:
             try:
                 configs[name] = job()
