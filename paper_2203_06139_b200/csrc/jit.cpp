@@ -679,6 +679,7 @@ struct Emitter {
     int dv = 0, dc = 0, maxv = 0, maxc = 0;
     std::map<std::string, long long> ienv;  // integer variables holding a known constant
     std::map<int, long long> ctlval;        // control-tape slots holding a known constant
+    std::set<int> wide;  // control slots that may hold a value beyond int32 (others: int)
   };
   Frame fr;
   long long unrolled_stmts = 0;  // emission budget of the unrolled code (per module)
@@ -1030,6 +1031,7 @@ struct Emitter {
         fr = base;
         fr.maxv = std::max(fr.maxv, t1.maxv);
         fr.maxc = std::max(fr.maxc, t1.maxc);
+        fr.wide = t1.wide;
         fr.dv = v2;
         fr.dc = c2;
         o << ind(d) << "} else {\n";
@@ -1037,6 +1039,7 @@ struct Emitter {
         o << ind(d) << "}\n";
         const Frame t2 = fr;
         fr = base;
+        fr.wide = t2.wide;  // (t2 started from t1's: the union)
         fr.maxv = std::max({fr.maxv, t1.maxv, t2.maxv, va});
         fr.maxc = std::max({fr.maxc, t1.maxc, t2.maxc, ca});
         if (fr.maxv > kMaxStaticSlots || fr.maxc > kMaxStaticSlots) throw Dynamic{};
@@ -1140,6 +1143,7 @@ struct Emitter {
             o << ind(d) << "_tc" << fr.dc << " = " << ie_any(*s.args[0]) << ";\n";
             if (known) fr.ctlval[fr.dc] = cv;
             else fr.ctlval.erase(fr.dc);
+            if (!known || cv != (long long)(int)cv) fr.wide.insert(fr.dc);
             note_push_c();
           } else {
             o << ind(d) << "adc_push_ctl(ctl, cp, " << ie_any(*s.args[0]) << ", ctx);\n";
@@ -1383,6 +1387,18 @@ __device__ __forceinline__ long long adc_pop_ctl(long long* t, int& cp, const Ad
     if (any) cacheable[f.name] = v;
   }
 
+  // The register-slot form (vector kernels): every slot parameter is the
+  // caller's register, by reference.
+  std::string signature_ref(const Fn& f, const std::string& name,
+                            const std::vector<int>& v) const {
+    std::string sig = std::string("__device__ ") + (f.returns_void ? "void " : "double ") + name + "(";
+    for (size_t i = 0; i < f.params.size(); ++i)
+      sig += (i ? ", " : "") +
+             (v[i] ? "double& c_" + V(f.params[i].name)
+                   : ptype(f.params[i].type) + " " + V(f.params[i].name));
+    return sig + (f.params.empty() ? "" : ", ") + "const AdcCtx& ctx)";
+  }
+
   std::string signature(const Fn& f, const std::string& name) const {
     std::string sig = std::string("__device__ ") + (f.returns_void ? "void " : "double ") + name + "(";
     for (size_t i = 0; i < f.params.size(); ++i)
@@ -1394,7 +1410,8 @@ __device__ __forceinline__ long long adc_pop_ctl(long long* t, int& cp, const Ad
   // with `consts` (static tape) its integer parameters bound to constants.
   // Returns false (and no text) when the static tape is not possible.
   bool function_text(const Fn& f, const std::string& name, bool cached_variant,
-                     const std::map<std::string, long long>* consts, std::string& text) {
+                     const std::map<std::string, long long>* consts, std::string& text,
+                     bool ref = false) {
     const Frame saved_fr = fr;
     const std::set<std::string>* saved_cached = cached;
     std::ostringstream body;
@@ -1411,7 +1428,8 @@ __device__ __forceinline__ long long adc_pop_ctl(long long* t, int& cp, const Ad
           if (!(*v)[i]) continue;
           const std::string n = V(f.params[i].name);
           names.insert(f.params[i].name);
-          o << "  double c_" << n << " = adc_ok(" << n << ", 0, ctx) ? " << n << ".p[0] : 0.0;\n";
+          if (!ref)
+            o << "  double c_" << n << " = adc_ok(" << n << ", 0, ctx) ? " << n << ".p[0] : 0.0;\n";
         }
       Scope sc;
       sc.push();
@@ -1419,7 +1437,7 @@ __device__ __forceinline__ long long adc_pop_ctl(long long* t, int& cp, const Ad
       cached = v ? &names : nullptr;
       block(f.body, f, sc, 1);
       cached = saved_cached;
-      if (v)
+      if (v && !ref)
         for (size_t i = 0; i < f.params.size(); ++i)
           if ((*v)[i] == 2) {
             const std::string n = V(f.params[i].name);
@@ -1440,10 +1458,11 @@ __device__ __forceinline__ long long adc_pop_ctl(long long* t, int& cp, const Ad
     cached = saved_cached;
     if (!ok) return false;
     std::ostringstream t;
-    t << signature(f, name) << " {\n";
+    t << (ref ? signature_ref(f, name, *v) : signature(f, name)) << " {\n";
     if (done.stat) {
       for (int k = 0; k < done.maxv; ++k) t << "  double _tv" << k << " = 0.0;\n";
-      for (int k = 0; k < done.maxc; ++k) t << "  long long _tc" << k << " = 0;\n";
+      for (int k = 0; k < done.maxc; ++k)
+        t << (done.wide.count(k) ? "  long long _tc" : "  int _tc") << k << " = 0;\n";
     } else {
       if (f.uses_tape) t << "  double tape[ADC_TAPE]; int tp = 0;\n";
       if (f.uses_ctl) t << "  long long ctl[ADC_TAPE]; int cp = 0;\n";
@@ -1463,6 +1482,126 @@ __device__ __forceinline__ long long adc_pop_ctl(long long* t, int& cp, const Ad
     }
     function_text(f, "fn_" + f.name, false, nullptr, text);
     o << text;
+  }
+
+  // Vector form of a Listing-1 kernel (static-tape variants only): when the
+  // kernel is exactly `integer i = blockIdx*blockDim+threadIdx; if (i < N) {
+  // f(..) }` with every argument of f a slice a[i] of a kernel array (the
+  // slots; pairwise distinct), a by-value a[i], a kernel scalar or a literal,
+  // and f's array parameters all length-1 slots, `adc_kernel_<k>_v2` runs
+  // points 2t and 2t+1 on thread t with 16-byte loads and stores, through a
+  // register-slot variant of f (the same statements in the same order per
+  // point, so the same bits).  The launch picks it when every array is
+  // 16-byte aligned and covers N (no index error can occur), never for the
+  // counting variant or forced (unsafe) launches.
+  bool kernel_v2(const Fn& f, const std::map<std::string, long long>& kconst) {
+    if (unsafe || count || f.body.size() != 2) return false;
+    const St& d = *f.body[0];
+    const St& g = *f.body[1];
+    if (!is_thread_index_decl(d) || g.k != St::If || !g.else_b.empty() || g.then_b.size() != 1)
+      return false;
+    const std::string iv = d.target;
+    const Ex& ce = *g.expr;
+    if (ce.k != Ex::Cmp || ce.cmp != "<" || ce.a[0]->k != Ex::Var || ce.a[0]->name != iv ||
+        ce.a[1]->k != Ex::Var || ce.a[1]->name != "N")
+      return false;
+    const St& call = *g.then_b[0];
+    if (call.k != St::Call) return false;
+    const Fn* c = m.find(call.callee);
+    if (c == nullptr || c->global || c->params.size() != call.args.size() ||
+        !cacheable.count(c->name))
+      return false;
+    const std::vector<int>& cv = cacheable.at(c->name);
+    std::map<std::string, VT> kp;
+    for (auto& p : f.params) kp[p.name] = p.type;
+    std::set<std::string> slots, loads;
+    std::map<std::string, long long> consts;
+    std::string key = c->name + "|r";
+    for (size_t a = 0; a < call.args.size(); ++a) {
+      const Ex& e = *call.args[a];
+      const VT pt = c->params[a].type;
+      const bool at_i = e.k == Ex::Index && e.a[0]->k == Ex::Var && e.a[0]->name == iv &&
+                        kp.count(e.name) && kp[e.name] == VT::RealArray;
+      if (pt == VT::RealArray) {
+        if (!at_i || !cv[a] || !slots.insert(e.name).second) return false;
+      } else if (pt == VT::Real) {
+        if (at_i) loads.insert(e.name);
+        else if (!(e.k == Ex::Num || (e.k == Ex::Var && kp.count(e.name) && kp[e.name] != VT::RealArray)))
+          return false;
+      } else {
+        if (e.k == Ex::Var && kconst.count(e.name)) {
+          consts[c->params[a].name] = kconst.at(e.name);
+          key += "|" + c->params[a].name + "=" + std::to_string(kconst.at(e.name));
+        } else if (e.k == Ex::Num && e.int_lit) {
+          consts[c->params[a].name] = (long long)e.v;
+          key += "|" + c->params[a].name + "=" + std::to_string((long long)e.v);
+        } else {
+          return false;
+        }
+      }
+    }
+    for (auto& l : loads)
+      if (slots.count(l)) return false;  // read by value and written through a slot
+    std::string name;
+    auto it = spec.find(key);
+    if (it != spec.end()) {
+      name = it->second;
+    } else {
+      name = "fn_" + c->name + "_r" + std::to_string(spec_count++);
+      std::string text;
+      if (!function_text(*c, name, true, &consts, text, true)) return false;
+      spec[key] = name;
+      spec_decls << signature_ref(*c, name, cv) << ";\n";
+      spec_defs << text;
+    }
+    // the kernel
+    o << "extern \"C\" __global__ void adc_kernel_" << f.name << "_v2(";
+    for (size_t i = 0; i < f.params.size(); ++i) {
+      const Prm& p = f.params[i];
+      if (i) o << ", ";
+      if (p.type == VT::RealArray)
+        o << "double* " << V(p.name) << "_p, long long " << V(p.name) << "_n";
+      else
+        o << ptype(p.type) << " " << V(p.name);
+    }
+    o << (f.params.empty() ? "" : ", ") << "long long N, AdcErr* adc_err) {\n";
+    o << "  const long long i0 = 2 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);\n";
+    o << "  if (i0 >= N) return;\n";
+    auto arg_expr = [&](const Ex& e, int lane) -> std::string {
+      if (e.k == Ex::Index) return "L_" + V(e.name) + (lane ? ".y" : ".x");
+      if (e.k == Ex::Num) return dbl(e.v);
+      return V(e.name);
+    };
+    auto emit_call = [&](int lane, bool pair) {
+      o << "    {\n      const AdcCtx ctx{adc_err, i0 + " << lane << "};\n      " << name << "(";
+      for (size_t a = 0; a < call.args.size(); ++a) {
+        const Ex& e = *call.args[a];
+        const VT pt = c->params[a].type;
+        if (a) o << ", ";
+        if (pt == VT::RealArray) o << "S_" << V(e.name) << (pair ? (lane ? ".y" : ".x") : "");
+        else if (pt == VT::Integer) o << "(long long)" << consts[c->params[a].name] << "LL";
+        else if (e.k == Ex::Index) o << (pair ? arg_expr(e, lane) : V(e.name) + "_p[i0]");
+        else o << arg_expr(e, lane);
+      }
+      o << ", ctx);\n    }\n";
+    };
+    o << "  if (i0 + 1 < N) {\n";
+    for (auto& l : loads)
+      o << "    const double2 L_" << V(l) << " = __ldcs(reinterpret_cast<const double2*>(" << V(l)
+        << "_p + i0));\n";
+    for (auto& sl : slots)
+      o << "    double2 S_" << V(sl) << " = __ldcs(reinterpret_cast<const double2*>(" << V(sl)
+        << "_p + i0));\n";
+    emit_call(0, true);
+    emit_call(1, true);
+    for (auto& sl : slots)
+      o << "    __stcs(reinterpret_cast<double2*>(" << V(sl) << "_p + i0), S_" << V(sl) << ");\n";
+    o << "  } else {\n";
+    for (auto& sl : slots) o << "    double S_" << V(sl) << " = " << V(sl) << "_p[i0];\n";
+    emit_call(0, false);
+    for (auto& sl : slots) o << "    " << V(sl) << "_p[i0] = S_" << V(sl) << ";\n";
+    o << "  }\n}\n\n";
+    return true;
   }
 
   // The kernel.  kconst: integer kernel parameters bound to constants (the
@@ -1507,7 +1646,8 @@ __device__ __forceinline__ long long adc_pop_ctl(long long* t, int& cp, const Ad
     std::swap(o, body);
     if (fr.stat) {
       for (int k = 0; k < fr.maxv; ++k) o << "  double _tv" << k << " = 0.0;\n";
-      for (int k = 0; k < fr.maxc; ++k) o << "  long long _tc" << k << " = 0;\n";
+      for (int k = 0; k < fr.maxc; ++k)
+        o << (fr.wide.count(k) ? "  long long _tc" : "  int _tc") << k << " = 0;\n";
     } else {
       if (f.uses_tape) o << "  double tape[ADC_TAPE]; int tp = 0;\n";
       if (f.uses_ctl) o << "  long long ctl[ADC_TAPE]; int cp = 0;\n";
@@ -1571,10 +1711,12 @@ struct adc_jit_module {
   // integer kernel arguments (built on first use, at most kMaxStaticVariants)
   struct Variant {
     bool ok = false;  // false: this key runs the dynamic-tape kernel
+    bool has_v2 = false;  // the vector Listing-1 kernel adc_kernel_<k>_v2 is in the image
     std::string cuda;
     std::vector<char> cubin;
     std::map<int, cudaLibrary_t> libs;
     std::map<int, cudaKernel_t> fns;
+    std::map<int, cudaKernel_t> fns_v2;
   };
   std::map<std::string, Variant> statics;
   bool static_any = false;  // statics["*"] serves every launch
@@ -1611,7 +1753,7 @@ constexpr int kStaticImpossible = -1000;
 int emit_and_compile(const Module& m, const Fn* k, const std::string& kernel, bool unsafe,
                      int tape_capacity, bool count, std::string& cuda, std::vector<char>& cubin,
                      const std::map<std::string, long long>* kconst = nullptr,
-                     bool* fully_static = nullptr) {
+                     bool* fully_static = nullptr, bool* has_v2 = nullptr) {
   Emitter em{m, unsafe, tape_capacity};
   em.count = count;
   try {
@@ -1652,6 +1794,7 @@ int emit_and_compile(const Module& m, const Fn* k, const std::string& kernel, bo
     std::swap(em.o, ko);
     try {
       em.kernel(*k, kconst);
+      if (kconst != nullptr && has_v2 != nullptr) *has_v2 = em.kernel_v2(*k, *kconst);
     } catch (Dynamic&) {
       return kStaticImpossible;
     } catch (...) {
@@ -1731,7 +1874,7 @@ extern "C" int adc_jit_compile(const char* source, const char* kernel, int32_t u
     adc_jit_module::Variant v;
     bool full = false;
     const int rc = emit_and_compile(m, k, kernel, unsafe != 0, tape_capacity, false, v.cuda,
-                                    v.cubin, &none, &full);
+                                    v.cubin, &none, &full, &v.has_v2);
     bool has_ints = false;
     for (auto& p : k->params) has_ints = has_ints || p.type == VT::Integer;
     if (rc == ADC_OK && (full || !has_ints)) {
@@ -1801,7 +1944,7 @@ adc_jit_module::Variant* static_variant(adc_jit_module* J, const adc_jit_arg* ar
   adc_jit_module::Variant v;
   bool full = false;
   rc = emit_and_compile(m, m.find(J->kernel), J->kernel, J->unsafe, J->tape_capacity, false,
-                        v.cuda, v.cubin, &consts, &full);
+                        v.cuda, v.cubin, &consts, &full, &v.has_v2);
   if (rc == kStaticImpossible) rc = ADC_OK;
   else if (rc != ADC_OK) return nullptr;
   else v.ok = full;  // a partly static variant buys nothing over the dynamic kernel
@@ -1909,6 +2052,11 @@ int jit_launch(adc_jit_module* J, int64_t grid, int64_t block, int64_t n, const 
       ADCB_CUDA(cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
       const std::string name = "adc_kernel_" + J->kernel;
       cudaError_t e = cudaLibraryGetKernel(&fn, lib, name.c_str());
+      if (e == cudaSuccess && sv && sv->has_v2) {
+        cudaKernel_t f2 = nullptr;
+        e = cudaLibraryGetKernel(&f2, lib, (name + "_v2").c_str());
+        sv->fns_v2[dev] = f2;
+      }
       if (e != cudaSuccess) {
         cudaLibraryUnload(lib);
         return cuda_fail(e, "cudaLibraryGetKernel");
@@ -1917,6 +2065,18 @@ int jit_launch(adc_jit_module* J, int64_t grid, int64_t block, int64_t n, const 
       fns[dev] = fn;
     } else {
       fn = it->second;
+    }
+    // the vector form: every array 16-byte aligned and covering N
+    if (sv && sv->has_v2) {
+      bool ok = true;
+      for (int32_t i = 0; i < nargs && ok; ++i)
+        if (J->kinds[i] == 0)
+          ok = (reinterpret_cast<uintptr_t>(args[i].ptr) & 15) == 0 && args[i].len >= n;
+      if (ok) {
+        fn = sv->fns_v2[dev];
+        block = 256;
+        grid = ((n + 1) / 2 + block - 1) / block;
+      }
     }
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -144,3 +144,17 @@ def test_static_tape_falls_back_on_pop_underflow():
     # the kernel frame is static, the callee keeps the dynamic tape (its run-time
     # underflow error is the interpreter's)
     assert s is not None and "adc_pop(tape, tp, ctx)" in s
+
+
+def test_vector_listing1_kernel_is_emitted():
+    """Listing-1 kernels (one call of a slot-only gradient at the thread
+    index) get a vector form — two points per thread, 16-byte accesses —
+    through a register-slot variant of the gradient; the others do not."""
+    m = adc.JitModule(MODULE, "k_rational")
+    src = m.static_source()
+    assert "adc_kernel_k_rational_v2" in src and "double& c_v__d_x" in src
+    looped = adc.JitModule(MODULE, "k_looped").static_source([10])
+    assert "adc_kernel_k_looped_v2" in looped
+    # a whole-array slot (sumn_grad(x, n, dx)) is not a Listing-1 slot call
+    sumn = adc.JitModule(MODULE, "k_sumn", unsafe=True).static_source([64])
+    assert sumn is None or "k_sumn_v2" not in sumn
