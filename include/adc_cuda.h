@@ -280,6 +280,16 @@ int adc_cuda_chi2_plan_layout(const adc_chi2_plan* plan, adc_chi2_layout* out);
  * written to records_dev + (chunk - chunk_begin) * record_len (device
  * pointer; NULL = the plan's own buffer, readable via
  * adc_cuda_chi2_plan_records).  Stream-ordered, asynchronous. */
+/* chi2 values of high-count histograms.  The single pass forms chi2 as
+ * C0 - 2a A1 + a^2 A2 from sums of magnitude E (events), so its relative
+ * rounding error is ~5 eps kappa, kappa = C0 / non-empty bins (the counts
+ * per bin).  A whole-histogram plan with kappa > 256 computes every chi2
+ * VALUE it returns (adc_cuda_chi2, _multi, the gradient's chi2 output, the
+ * fit's line search) as sum (c - a m)^2 / c directly in a second pass (K3r)
+ * with a = E/S from the first; its passes then run precision mode 1 (the
+ * residual pass and the S it uses see the same m) and the fit runs its host
+ * loop.  *residual = 1 in that mode; *kappa = C0 / non-empty bins. */
+int adc_cuda_chi2_value_mode(adc_chi2_plan* plan, int32_t* residual, double* kappa);
 /* Measurement hook: with timing on, adc_cuda_chi2_partials records CUDA
  * events around the pass's tile kernel (the dominant one) on its stream;
  * adc_cuda_chi2_kernel_ms waits for and returns the last such duration. */

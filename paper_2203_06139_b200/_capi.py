@@ -102,6 +102,8 @@ SIGNATURES = {
     "adc_cuda_chi2_plan_layout": (ctypes.c_int, [_VP, ctypes.POINTER(Chi2Layout)]),
     "adc_cuda_chi2_partials": (ctypes.c_int, [_VP, _D, _I32, _VP]),
     "adc_cuda_chi2_set_kernel_timing": (ctypes.c_int, [_VP, _I32]),
+    "adc_cuda_chi2_value_mode": (ctypes.c_int, [_VP, ctypes.POINTER(_I32),
+                                                ctypes.POINTER(ctypes.c_double)]),
     "adc_cuda_chi2_kernel_ms": (ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_float)]),
     "adc_cuda_chi2_plan_records": (_VP, [_VP]),
     "adc_cuda_chi2_gradient": (ctypes.c_int, [_VP, _D, _D, _D]),

@@ -1055,6 +1055,84 @@ __device__ __forceinline__ double zmerge(const ZMerge& zm, int64_t chunk, int v,
   return a;
 }
 
+// ---- K3r: the residual chi2 value (high-count histograms) -------------------------
+// chi2 = sum_{c>0} (c - a m)^2 / c with a = E/S known from a first pass: the
+// residual r is formed per bin, so nothing of magnitude E cancels (the single
+// pass's C0 - 2a A1 + a^2 A2 loses ~eps * E).  Same bins, centres and fast /
+// faithful model arithmetic as the value pass without the run recurrence, so
+// S and the residuals see the same m.  One CTA per (local chunk, segment,
+// candidate y); fixed per-thread order, shuffle tree and cross-warp tree into
+// out[y][chunk][seg].
+template <class M, bool FAST>
+__global__ void __launch_bounds__(kTileThreads) chi2_resid_kernel(Chi2Pass P, int64_t chunk_bins,
+                                                                  int64_t nchunks,
+                                                                  const double* a_dev,
+                                                                  bool multi, double* out) {
+  const int y = blockIdx.y;
+  const double* qd = P.qdev + (multi ? (int64_t)y * kQDoubles : y * P.q_stride);
+  __shared__ QDev Q;
+  __shared__ double tab[64];
+  __shared__ double red[kTileThreads / 32];
+  if (threadIdx.x < kMaxNp) {
+    Q.q[threadIdx.x] = qd[threadIdx.x];
+    Q.inv[threadIdx.x] = qd[kMaxNp + threadIdx.x];
+  }
+  if (threadIdx.x < 64) tab[threadIdx.x] = exp2((double)threadIdx.x / 64.0);
+  __syncwarp();
+  __syncthreads();
+  const typename M::Reg QR = M::load(Q);
+  const double a = a_dev[y];
+  const int64_t chunk = blockIdx.x / kResidSegs, seg = blockIdx.x % kResidSegs;
+  const int64_t begin = P.tile_begin * (int64_t)P.bpt * kTileThreads;
+  const int64_t c0 = begin + chunk * chunk_bins, c1 = min(c0 + chunk_bins, P.bin_end);
+  const int64_t o0 = c0 + (c1 - c0) * seg / kResidSegs, o1 = c0 + (c1 - c0) * (seg + 1) / kResidSegs;
+  double acc = 0.0;
+  for (int64_t j = o0 + threadIdx.x; j < o1; j += kTileThreads) {
+    const double x = fadd(P.lo, fmul(fadd((double)j, 0.5), P.width));
+    double m, bg[1];
+    M::template eval<false, FAST>(x, QR, tab, m, bg);
+    const double r = P.counts[j] - a * m;  // [c > 0] via ic = 0 below
+    acc += (r * r) * P.icounts[j];
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    out[((int64_t)y * nchunks + chunk) * kResidSegs + seg] =
+        ((red[0] + red[1]) + (red[2] + red[3])) + ((red[4] + red[5]) + (red[6] + red[7]));
+}
+
+int chi2_resid_enqueue(const Chi2Pass& P, int model, int np, int prec, int64_t chunk_tiles,
+                       const double* a_dev, int ny, bool multi, double* out, cudaStream_t s) {
+  const int64_t ntiles = P.tile_end - P.tile_begin;
+  if (ntiles <= 0) return ADC_OK;
+  const int64_t nchunks = (ntiles + chunk_tiles - 1) / chunk_tiles;
+  const int64_t chunk_bins = chunk_tiles * (int64_t)P.bpt * kTileThreads;
+  const dim3 grid((unsigned)(nchunks * kResidSegs), (unsigned)ny);
+  auto go = [&](auto tag) {
+    using M = decltype(tag);
+    if (prec != 0)
+      chi2_resid_kernel<M, true><<<grid, kTileThreads, 0, s>>>(P, chunk_bins, nchunks, a_dev, multi, out);
+    else
+      chi2_resid_kernel<M, false><<<grid, kTileThreads, 0, s>>>(P, chunk_bins, nchunks, a_dev, multi, out);
+  };
+  if (model == ADC_MODEL_GPOLY) {
+    go(GPoly{});
+  } else {
+    switch (np / 3) {
+      case 1: go(GSum<1>{}); break;
+      case 2: go(GSum<2>{}); break;
+      case 3: go(GSum<3>{}); break;
+      case 4: go(GSum<4>{}); break;
+      case 8: go(GSum<8>{}); break;
+      default: return fail(ADC_E_ARG, "gsum: unsupported component count");
+    }
+  }
+  ADCB_CUDA(cudaGetLastError());
+  return ADC_OK;
+}
+
 // ---- K4: chunk reduce (fixed tree over the chunk's tiles) ---------------------
 // One CTA per chunk; warp w owns record entries v = w, w+8, ...; lane l sums
 // tiles l, l+32, l+64, l+96 pairwise, then a fixed shuffle tree.

@@ -24,6 +24,9 @@ using namespace adcb;
 namespace {
 
 constexpr int64_t kTileThreads = 256;
+// counts per non-empty bin above which chi2 values take the residual pass:
+// the single pass's relative error is ~5 eps kappa (K3)
+constexpr double kResidKappa = 256.0;
 constexpr int64_t kChunkBins = int64_t(1) << 20;  // large histograms: 1 Mi-bin chunks
 
 // Bins per thread per tile.  Large histograms amortise the per-tile
@@ -169,6 +172,14 @@ struct adc_chi2_plan {
   double* lin = nullptr;      // per local chunk [G0_lin[L], G1_lin[L], C0]
   double* icounts = nullptr;  // [c > 0]/c for this rank's bins (from bin_begin)
   bool lin_ready = false;
+  // high counts per bin (kappa = C0 / non-empty bins > kResidKappa, whole
+  // histogram on one device): chi2 VALUES come from the residual pass (K3r)
+  bool resid = false;
+  double kappa = 0.0;
+  double* resid_a = nullptr;    // device [kMultiMax]: E / S per candidate
+  double* h_resid_a = nullptr;  // pinned
+  double* resid_out = nullptr;  // device [kMultiMax][local chunks][kResidSegs]
+  double* h_resid_out = nullptr;
   // the empty bins of this rank's chunks (CSR by local chunk) and the side
   // pass's per-chunk sums over them (chi2.cu K3z)
   int64_t* empty_idx = nullptr;
@@ -340,7 +351,73 @@ int ensure_lin(adc_chi2_plan* P, cudaStream_t s) {
                                          P->empty_idx, s))
       return rc;
   ADCB_CUDA(cudaStreamSynchronize(s));
+  // counts per non-empty bin: C0 over this rank's chunks / non-empty bins
+  if (!sharded(P) && nloc > 0) {
+    std::vector<double> lin((size_t)nrec * (2 * L + 1));
+    ADCB_CUDA(cudaMemcpy(lin.data(), P->lin, lin.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    double c0 = 0.0;
+    for (int64_t c = 0; c < nloc; ++c) c0 += lin[(size_t)c * (2 * L + 1) + 2 * L];
+    const double nonempty = (double)(P->L.bin_end - P->L.bin_begin) - (double)off[nloc];
+    P->kappa = nonempty > 0 ? c0 / nonempty : 0.0;
+    const bool resid = P->comm == nullptr && P->kappa > kResidKappa;
+    if (resid && P->resid_a == nullptr) {
+      ADCB_CUDA(cudaMalloc(&P->resid_a, kMultiMax * sizeof(double)));
+      ADCB_CUDA(cudaMallocHost(&P->h_resid_a, kMultiMax * sizeof(double)));
+      const size_t cnt = (size_t)kMultiMax * P->L.nchunks * kResidSegs;
+      ADCB_CUDA(cudaMalloc(&P->resid_out, cnt * sizeof(double)));
+      ADCB_CUDA(cudaMallocHost(&P->h_resid_out, cnt * sizeof(double)));
+    }
+    if (resid != P->resid) {
+      P->resid = resid;
+      drop_graphs(P);
+      if (P->fit_graph) cudaGraphExecDestroy(P->fit_graph);
+      P->fit_graph = nullptr;
+    }
+    // the residual pass evaluates m without the run recurrence: so do the
+    // passes whose S it uses
+    if (P->resid && P->fast == 2) P->fast = 1;
+  }
   P->lin_ready = true;
+  return ADC_OK;
+}
+
+// The sum over chunks of record entry v in adc_chi2_finalize's fixed
+// pairwise tree (the same bits as the finalize's S when v = 0).
+double chunk_tree_sum(const double* rec, int64_t nchunks, int R, int v) {
+  std::vector<double> t((size_t)nchunks);
+  for (int64_t c = 0; c < nchunks; ++c) t[c] = rec[c * R + v];
+  for (int64_t s = 1; s < nchunks; s *= 2)
+    for (int64_t i = 0; i + s < nchunks; i += 2 * s) t[i] = t[i] + t[i + s];
+  return t[0];
+}
+
+// Residual chi2 values (K3r) of ncand parameter vectors already on the device
+// (P->qdev for one, P->qmulti for a multi pass) given their S: sum (c-am)^2/c
+// with a = E/S, reduced in fixed order (segments, then the chunk tree).
+int resid_values(adc_chi2_plan* P, int ncand, const double* S, bool multi, double* chi2) {
+  const int64_t nch = P->L.nchunks;  // whole-histogram plans only (resid)
+  for (int k = 0; k < ncand; ++k) P->h_resid_a[k] = P->events / S[k];
+  ADCB_CUDA(cudaMemcpyAsync(P->resid_a, P->h_resid_a, ncand * sizeof(double),
+                            cudaMemcpyHostToDevice, P->stream));
+  Chi2Pass pass = make_pass(P);
+  if (multi) pass.qdev = P->qmulti;
+  if (int rc = chi2_resid_enqueue(pass, P->model, P->np, P->fast, P->L.chunk_tiles, P->resid_a,
+                                  ncand, multi, P->resid_out, P->stream))
+    return rc;
+  const size_t cnt = (size_t)ncand * nch * kResidSegs;
+  ADCB_CUDA(cudaMemcpyAsync(P->h_resid_out, P->resid_out, cnt * sizeof(double),
+                            cudaMemcpyDeviceToHost, P->stream));
+  ADCB_CUDA(cudaStreamSynchronize(P->stream));
+  std::vector<double> per((size_t)nch);
+  for (int k = 0; k < ncand; ++k) {
+    for (int64_t c = 0; c < nch; ++c) {
+      const double* o = P->h_resid_out + ((size_t)k * nch + c) * kResidSegs;
+      double v = o[0];
+      for (int g = 1; g < kResidSegs; ++g) v = v + o[g];
+      per[c] = v;
+    }
+    chi2[k] = chunk_tree_sum(per.data(), nch, 1, 0);
+  }
   return ADC_OK;
 }
 
@@ -574,6 +651,10 @@ extern "C" int adc_cuda_chi2_plan_destroy(adc_chi2_plan* P) {
   if (P->records_multi) cudaFree(P->records_multi);
   if (P->lin) cudaFree(P->lin);
   if (P->icounts) cudaFree(P->icounts);
+  if (P->resid_a) cudaFree(P->resid_a);
+  if (P->h_resid_a) cudaFreeHost(P->h_resid_a);
+  if (P->resid_out) cudaFree(P->resid_out);
+  if (P->h_resid_out) cudaFreeHost(P->h_resid_out);
   if (P->empty_idx) cudaFree(P->empty_idx);
   if (P->empty_off) cudaFree(P->empty_off);
   if (P->empty_cnt) cudaFree(P->empty_cnt);
@@ -608,7 +689,7 @@ extern "C" int adc_cuda_chi2_plan_layout(const adc_chi2_plan* P, adc_chi2_layout
 extern "C" int adc_cuda_chi2_set_precision(adc_chi2_plan* P, int32_t mode) {
   clear_error();
   if (P == nullptr || mode < 0 || mode > 2) return fail(ADC_E_ARG, "precision mode is 0, 1 or 2");
-  P->fast = mode;
+  P->fast = P->resid && mode == 2 ? 1 : mode;  // (residual-value plans: no run recurrence)
   if (P->fit_graph) {  // the device fit iteration graph holds the gradient pass
     cudaGraphExecDestroy(P->fit_graph);
     P->fit_graph = nullptr;
@@ -658,6 +739,16 @@ extern "C" int adc_cuda_chi2_partials(adc_chi2_plan* P, const double* q, int32_t
                       want_grad && numeric(P));
 }
 
+extern "C" int adc_cuda_chi2_value_mode(adc_chi2_plan* P, int32_t* residual, double* kappa) {
+  clear_error();
+  if (P == nullptr || residual == nullptr || kappa == nullptr) return fail(ADC_E_ARG, "null argument");
+  ADCB_CUDA(cudaSetDevice(P->device));
+  if (int rc = ensure_lin(P, P->stream)) return rc;
+  *residual = P->resid ? 1 : 0;
+  *kappa = P->kappa;
+  return ADC_OK;
+}
+
 extern "C" int adc_cuda_chi2_set_kernel_timing(adc_chi2_plan* P, int32_t on) {
   clear_error();
   if (P == nullptr) return fail(ADC_E_ARG, "null plan");
@@ -689,7 +780,12 @@ extern "C" int adc_cuda_chi2_gradient(adc_chi2_plan* P, const double* q, double*
   if (P == nullptr || q == nullptr || grad == nullptr) return fail(ADC_E_ARG, "null argument");
   const double* rec = nullptr;
   if (int rc = run_pass(P, q, 1, &rec)) return rc;
-  return adc_chi2_finalize(P->np, P->events, rec, P->L.nchunks, 1, grad, chi2);
+  if (int rc = adc_chi2_finalize(P->np, P->events, rec, P->L.nchunks, 1, grad, chi2)) return rc;
+  if (P->resid && chi2 != nullptr) {
+    const double S = chunk_tree_sum(rec, P->L.nchunks, adc_chi2_record_len(P->np, 1), 0);
+    return resid_values(P, 1, &S, false, chi2);
+  }
+  return ADC_OK;
 }
 
 extern "C" int adc_cuda_chi2(adc_chi2_plan* P, const double* q, double* chi2) {
@@ -697,7 +793,12 @@ extern "C" int adc_cuda_chi2(adc_chi2_plan* P, const double* q, double* chi2) {
   if (P == nullptr || q == nullptr || chi2 == nullptr) return fail(ADC_E_ARG, "null argument");
   const double* rec = nullptr;
   if (int rc = run_pass(P, q, 0, &rec)) return rc;
-  return adc_chi2_finalize(P->np, P->events, rec, P->L.nchunks, 0, nullptr, chi2);
+  if (int rc = adc_chi2_finalize(P->np, P->events, rec, P->L.nchunks, 0, nullptr, chi2)) return rc;
+  if (P->resid) {
+    const double S = chunk_tree_sum(rec, P->L.nchunks, 4, 0);
+    return resid_values(P, 1, &S, false, chi2);
+  }
+  return ADC_OK;
 }
 
 namespace {
@@ -792,6 +893,11 @@ extern "C" int adc_cuda_chi2_multi(adc_chi2_plan* P, const double* qs, int32_t n
     if (int rc = adc_chi2_finalize(P->np, P->events, rec4.data(), P->L.nchunks, 0, nullptr,
                                    chi2s + k))
       return rc;
+  }
+  if (P->resid) {
+    std::vector<double> S((size_t)ncand);
+    for (int k = 0; k < ncand; ++k) S[k] = chunk_tree_sum(rec, P->L.nchunks, R, 1 + 3 * k);
+    return resid_values(P, ncand, S.data(), true, chi2s);
   }
   return ADC_OK;
 }
@@ -1093,8 +1199,9 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
   // either gradient provider, steepest descent or the Newton option.
   // opts->host_loop keeps the host-driven loop (both give the same bits).
   const bool peer = P->comm != nullptr && P->comm->kind == ADC_COMM_PEER;
+  // (residual-value plans keep the host loop: its value passes add K3r)
   const bool dev_mode = P->fast && (peer || (P->comm == nullptr && !sharded(P))) &&
-                        nclamp <= kMaxNp && !opts->host_loop;
+                        nclamp <= kMaxNp && !opts->host_loop && !P->resid;
   if (dev_mode) {
     FitDevConst c{};
     c.grad_tol = opts->grad_tol;

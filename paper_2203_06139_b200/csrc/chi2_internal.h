@@ -69,6 +69,12 @@ int chi2_empty_count_enqueue(const Chi2Pass& P, int64_t chunk_tiles, int64_t* co
                              cudaStream_t s);
 int chi2_empty_fill_enqueue(const Chi2Pass& P, int64_t chunk_tiles, const int64_t* off,
                             int64_t* idx, cudaStream_t s);
+// K3r: the residual chi2 value of ny parameter vectors (qdev + y q_stride, or
+// candidate y of a multi pass) with a_dev[y] = E / S_y: partial sums
+// out[y][local chunk][kResidSegs] (fixed order).
+constexpr int kResidSegs = 8;
+int chi2_resid_enqueue(const Chi2Pass& P, int model, int np, int prec, int64_t chunk_tiles,
+                       const double* a_dev, int ny, bool multi, double* out, cudaStream_t s);
 void fill_qdev(int model, int np, const double* q, double* host_qdev);
 size_t qdev_bytes();
 // K6: counts[j] ~ Poisson(events m_j / sum m) (Philox, counter = bin), ws =

@@ -203,6 +203,13 @@ class Chi2Plan:
         check(lib.adc_cuda_chi2_partials(self._p, dbl_array(q), 1 if want_grad else 0,
                                          dptr(records_dev) if records_dev is not None else None))
 
+    def value_mode(self):
+        """(residual, kappa): whether chi2 values take the residual pass
+        (high counts per bin, include/adc_cuda.h) and C0 / non-empty bins."""
+        r, k = ctypes.c_int32(), ctypes.c_double()
+        check(lib.adc_cuda_chi2_value_mode(self._p, ctypes.byref(r), ctypes.byref(k)))
+        return bool(r.value), k.value
+
     def tile_kernel_ms(self, q, want_grad: bool = True, records_dev=None) -> float:
         """One pass (partials) with CUDA events around its tile kernel (the
         dominant kernel); returns that kernel's duration in ms."""

@@ -80,7 +80,10 @@ static int thread_allgather(void* ctx, const void* send, void* recv, size_t byte
 }
 
 int main(int argc, char** argv) {
-  const bool gpu = argc > 1 && std::string(argv[1]) == "gpu";
+  // "gpu-launch": the launch paths only (for compute-sanitizer's racecheck /
+  // synccheck, which do not follow the fit's device-side graph loop)
+  const bool launch_only = argc > 1 && std::string(argv[1]) == "gpu-launch";
+  const bool gpu = argc > 1 && (std::string(argv[1]) == "gpu" || launch_only);
   BufferSet b;
   b.arrays["x"] = std::vector<double>(512, 0.5);
   b.arrays["p"] = std::vector<double>(512, 0.0);
@@ -164,6 +167,10 @@ int main(int argc, char** argv) {
                                             std::vector<int32_t>{0, 4096}); })
                      .find("does not exist") != std::string::npos,
              "multi-GPU form: a missing device is refused");
+    }
+    if (launch_only) {
+      std::printf("%d failure(s)\n", failures);
+      return failures ? 1 : 0;
     }
     // FitEngine gsum K=1 over a 4000-bin histogram vs the compensated oracle.
     Histogram hist;

@@ -701,3 +701,43 @@ def test_device_fit_loop_bitwise_equals_host_loop(case):
     assert np.array(a.params).tobytes() == np.array(b.params).tobytes()
     assert a.chi2 == b.chi2
     assert np.array(a.iterates).tobytes() == np.array(b.iterates).tobytes()
+
+
+# ---------------------------------------------------------------------------- high counts per bin
+@pytest.mark.parametrize("bins,events", [(1000, 1e8), (100, 1e11), (20_000, 1e9)])
+def test_chi2_value_high_counts_residual(restate, bins, events):
+    """the single pass's chi2 = C0 - 2a A1 + a^2 A2 loses ~eps * E
+    (relative ~5 eps kappa, kappa = counts per bin).  Plans with kappa > 256
+    compute chi2 values as sum (c - a m)^2 / c directly (K3r).  Checked
+    against the compensated oracle RELATIVE TO chi2 itself (not the ~4E sum of
+    the expanded terms), through every value entry point, and the batched
+    line search still equals the single value pass bit for bit."""
+    counts, ev = synth.histogram(bins, events=events, seed=bins)
+    h = adc.Histogram(bins, -5.0, 5.0, ev, counts)
+    plan = adc.Chi2Plan("gpoly", 6, h)
+    resid, kappa = plan.value_mode()
+    assert resid and kappa > 256
+    q = np.array(synth.GPOLY_INIT)
+    cref, _ = restate.chi2_compensated("gpoly", counts, -5.0, 5.0, ev, q)
+    v = plan.chi2(q)
+    assert abs(v - cref) <= 1e-12 * abs(cref), (v, cref, abs(v - cref) / cref)
+    g, c2 = plan.gradient(q)
+    assert abs(c2 - cref) <= 1e-12 * abs(cref)  # (its S is the gradient pass's: other bits)
+    ref, scale = restate.chi2_gradient_compensated("gpoly", counts, -5.0, 5.0, ev, q)
+    assert np.all(np.abs(g - ref) <= 1e-12 * scale)
+    qs = np.stack([q, q * (1 + 1e-4), q * (1 - 1e-4)])
+    vm = plan.chi2_multi(qs)
+    assert vm[0] == v
+    for k in range(3):
+        ck, _ = restate.chi2_compensated("gpoly", counts, -5.0, 5.0, ev, qs[k])
+        assert abs(vm[k] - ck) <= 1e-12 * abs(ck)
+    # the fit runs (host loop in this mode) and agrees with the reference's bound
+    r = adc.FitEngine("gpoly", 6).fit(h, synth.GPOLY_INIT, adc.FitOptions(budget=60, use_hessian=True))
+    assert np.isfinite(r.chi2) and r.chi2 <= v
+
+
+def test_chi2_value_mode_baseline_histograms_stay_single_pass():
+    counts, ev = synth.histogram(1_000_000, events=1e8, seed=11)  # configs[2]: ~100 per bin
+    plan = adc.Chi2Plan("gpoly", 6, adc.Histogram(1_000_000, -5.0, 5.0, ev, counts))
+    resid, kappa = plan.value_mode()
+    assert not resid and 50 < kappa < 256
