@@ -13,7 +13,7 @@ for alt in tools/alt_*.sed; do
   [ -f "$alt" ] || continue
   name=$(basename $alt .sed)
   rm -rf /tmp/alt && mkdir /tmp/alt && cp -r paper_2203_06139_b200 include tools oracle /tmp/alt/ && cd /tmp/alt
-  sed -i -f $alt paper_2203_06139_b200/csrc/chi2.cu && make -s -j8 -C paper_2203_06139_b200/csrc > /tmp/alt_build.log 2>&1
+  sed -i -f $alt paper_2203_06139_b200/csrc/chi2.cu paper_2203_06139_b200/csrc/chi2_host.cpp && make -s -j8 -C paper_2203_06139_b200/csrc > /tmp/alt_build.log 2>&1
   timeout 300 python tools/probe_chi2.py 100000000 20 > $GRAFT_REPO_ROOT/$O/probe_chi2_$name.log 2>&1; echo "$name: $(tail -1 $GRAFT_REPO_ROOT/$O/probe_chi2_$name.log)"
   cd $GRAFT_REPO_ROOT
 done
