@@ -400,6 +400,21 @@ int adc_cuda_histogram_sample(int32_t model, int32_t np, const double* q, int64_
                               double hi, double events, uint64_t seed, int64_t zero_every,
                               double* counts_dev, double* total, void* stream);
 
+/* Histogram ingest format (the reference's Histogram, fit.hpp:23-34, on
+ * disk; shared with the oracle's readers): little-endian
+ *   char magic[8] = "ADCHIST1"; int64 bins; double lo, hi, events;
+ *   double counts[bins].
+ * adc_histogram_write takes host or device counts (copied through a pinned
+ * bounce buffer in 64 MiB pieces); adc_histogram_read_header fills the
+ * scalars; adc_histogram_read_counts reads the counts into host or device
+ * memory (device: pinned pieces, H2D overlapped with the file reads).
+ * Errors: ADC_E_ARG (bad magic, short file, bins mismatch). */
+int adc_histogram_write(const char* path, int64_t bins, double lo, double hi, double events,
+                        const double* counts);
+int adc_histogram_read_header(const char* path, int64_t* bins, double* lo, double* hi,
+                              double* events);
+int adc_histogram_read_counts(const char* path, int64_t bins, double* counts);
+
 /* ---------------------------------------------------------------------------
  * Fit loop (FitEngine::fit, proj/src/fit.cpp:315-425: steepest descent or the
  * optional damped Newton step from a central-difference Hessian of the

@@ -726,6 +726,45 @@ int cmd_chi2_in(int argc, char** argv) {
   return engine_match ? 0 : 1;
 }
 
+// chi2-file <model> <hist.adchist> <out.bin> q...  — the reference's chi2 and
+// chi2_gradient (the FitEngine formula over the reference Program) of a
+// histogram in the engine's ingest format (include/adc_cuda.h "ADCHIST1"),
+// read here independently of the product.  out = [chi2, grad[np]].
+int cmd_chi2_file(int argc, char** argv) {
+  if (argc < 4) die("chi2-file <model> <hist.adchist> <out> q...");
+  std::string model = argv[1];
+  std::ifstream in(argv[2], std::ios::binary);
+  if (!in) die(std::string("cannot open ") + argv[2]);
+  char magic[8];
+  int64_t bins = 0;
+  double lo = 0, hi = 0, events = 0;
+  in.read(magic, 8);
+  in.read(reinterpret_cast<char*>(&bins), 8);
+  in.read(reinterpret_cast<char*>(&lo), 8);
+  in.read(reinterpret_cast<char*>(&hi), 8);
+  in.read(reinterpret_cast<char*>(&events), 8);
+  if (!in || std::memcmp(magic, "ADCHIST1", 8) != 0 || bins <= 0) die("not an ADCHIST1 file");
+  Histogram h;
+  h.bins = static_cast<int>(bins);
+  h.lo = lo;
+  h.hi = hi;
+  h.events = static_cast<uint64_t>(events);
+  h.counts.resize(bins);
+  in.read(reinterpret_cast<char*>(h.counts.data()), bins * 8);
+  if (!in) die("short histogram file");
+  std::vector<double> q;
+  for (int i = 4; i < argc; ++i) q.push_back(std::atof(argv[i]));
+  ModelEngine eng = make_engine(model);
+  std::vector<double> g;
+  eng.chi2_gradient(h, q, g);
+  std::vector<double> res{eng.chi2(h, q)};
+  res.insert(res.end(), g.begin(), g.end());
+  std::ofstream out(argv[3], std::ios::binary);
+  write_f64(out, res);
+  std::printf("{\"bins\": %lld, \"events\": %.17g}\n", (long long)bins, events);
+  return 0;
+}
+
 // fit-in <model> <bins> <lo> <hi> <counts.bin> <out.bin> <trace> <budget[:hess]> q...
 //   out = [chi2, iterations, gradient_evals, converged, sigma_clamps,
 //          params[np], iterates[trace x np] (zero padded)].
@@ -906,6 +945,7 @@ int main(int argc, char** argv) {
     if (cmd == "gaussnd-bench") return cmd_gaussnd_bench(argc - 1, argv + 1);
     if (cmd == "gauss1d-bench") return cmd_gauss1d_bench(argc - 1, argv + 1);
     if (cmd == "chi2-bench") return cmd_chi2_bench(argc - 1, argv + 1);
+    if (cmd == "chi2-file") return cmd_chi2_file(argc - 1, argv + 1);
   } catch (const Error& e) {
     std::fprintf(stderr, "ref_tool: adc::Error(kind=%d): %s\n", static_cast<int>(e.kind()),
                  e.what());

@@ -152,3 +152,18 @@ def load() -> Restate:
             build()
         _lib = Restate(ctypes.CDLL(SO))
     return _lib
+
+
+def read_histogram(path):
+    """The histogram ingest format (include/adc_cuda.h), read independently of
+    the product: "ADCHIST1", int64 bins, double lo, hi, events, double
+    counts[bins] (little-endian).  Returns (bins, lo, hi, events, counts)."""
+    with open(path, "rb") as f:
+        if f.read(8) != b"ADCHIST1":
+            raise ValueError(f"{path}: not an ADCHIST1 histogram file")
+        bins = int(np.frombuffer(f.read(8), dtype="<i8")[0])
+        lo, hi, events = (float(v) for v in np.frombuffer(f.read(24), dtype="<f8"))
+        counts = np.frombuffer(f.read(8 * bins), dtype="<f8").copy()
+    if counts.size != bins:
+        raise ValueError(f"{path}: short file")
+    return bins, lo, hi, events, counts

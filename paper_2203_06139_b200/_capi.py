@@ -102,6 +102,11 @@ SIGNATURES = {
     "adc_cuda_chi2_plan_layout": (ctypes.c_int, [_VP, ctypes.POINTER(Chi2Layout)]),
     "adc_cuda_chi2_partials": (ctypes.c_int, [_VP, _D, _I32, _VP]),
     "adc_cuda_chi2_set_kernel_timing": (ctypes.c_int, [_VP, _I32]),
+    "adc_histogram_write": (ctypes.c_int, [ctypes.c_char_p, _I64, _DBL, _DBL, _DBL, _VP]),
+    "adc_histogram_read_header": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_I64),
+                                                 ctypes.POINTER(_DBL), ctypes.POINTER(_DBL),
+                                                 ctypes.POINTER(_DBL)]),
+    "adc_histogram_read_counts": (ctypes.c_int, [ctypes.c_char_p, _I64, _VP]),
     "adc_cuda_chi2_value_mode": (ctypes.c_int, [_VP, ctypes.POINTER(_I32),
                                                 ctypes.POINTER(ctypes.c_double)]),
     "adc_cuda_chi2_kernel_ms": (ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_float)]),

@@ -9,6 +9,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <new>
 #include <string>
@@ -1455,4 +1456,115 @@ extern "C" int adc_cuda_fit(adc_chi2_plan* P, double* params, const int32_t* cla
   res.chi2 = cur;
   *result = res;
   return ADC_OK;
+}
+
+// ---- histogram ingest format (include/adc_cuda.h) ---------------------------------
+namespace {
+constexpr char kHistMagic[8] = {'A', 'D', 'C', 'H', 'I', 'S', 'T', '1'};
+constexpr size_t kHistHeader = 8 + 8 + 3 * 8;
+constexpr size_t kHistPiece = size_t(64) << 20;  // bytes per bounce-buffer piece
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+}  // namespace
+
+extern "C" int adc_histogram_write(const char* path, int64_t bins, double lo, double hi,
+                                   double events, const double* counts) {
+  clear_error();
+  if (path == nullptr || counts == nullptr || bins <= 0) return fail(ADC_E_ARG, "histogram write: bad argument");
+  FILE* f = std::fopen(path, "wb");
+  if (f == nullptr) return fail(ADC_E_ARG, std::string("histogram write: cannot open ") + path);
+  bool ok = std::fwrite(kHistMagic, 1, 8, f) == 8 && std::fwrite(&bins, 8, 1, f) == 1 &&
+            std::fwrite(&lo, 8, 1, f) == 1 && std::fwrite(&hi, 8, 1, f) == 1 &&
+            std::fwrite(&events, 8, 1, f) == 1;
+  if (ok && !is_device_ptr(counts)) {
+    ok = std::fwrite(counts, 8, (size_t)bins, f) == (size_t)bins;
+  } else if (ok) {
+    double* bounce = nullptr;
+    if (cudaMallocHost(&bounce, kHistPiece) != cudaSuccess) {
+      std::fclose(f);
+      return cuda_fail(cudaGetLastError(), "histogram write: pinned buffer");
+    }
+    const size_t per = kHistPiece / 8;
+    for (int64_t o = 0; ok && o < bins; o += (int64_t)per) {
+      const size_t n = (size_t)std::min<int64_t>((int64_t)per, bins - o);
+      ok = cudaMemcpy(bounce, counts + o, n * 8, cudaMemcpyDeviceToHost) == cudaSuccess &&
+           std::fwrite(bounce, 8, n, f) == n;
+    }
+    cudaFreeHost(bounce);
+  }
+  ok = std::fclose(f) == 0 && ok;
+  return ok ? ADC_OK : fail(ADC_E_ARG, std::string("histogram write failed: ") + path);
+}
+
+extern "C" int adc_histogram_read_header(const char* path, int64_t* bins, double* lo, double* hi,
+                                         double* events) {
+  clear_error();
+  if (path == nullptr || bins == nullptr || lo == nullptr || hi == nullptr || events == nullptr)
+    return fail(ADC_E_ARG, "null argument");
+  FILE* f = std::fopen(path, "rb");
+  if (f == nullptr) return fail(ADC_E_ARG, std::string("histogram read: cannot open ") + path);
+  char magic[8];
+  const bool ok = std::fread(magic, 1, 8, f) == 8 && std::memcmp(magic, kHistMagic, 8) == 0 &&
+                  std::fread(bins, 8, 1, f) == 1 && std::fread(lo, 8, 1, f) == 1 &&
+                  std::fread(hi, 8, 1, f) == 1 && std::fread(events, 8, 1, f) == 1 && *bins > 0;
+  std::fclose(f);
+  return ok ? ADC_OK : fail(ADC_E_ARG, std::string("not an ADCHIST1 histogram file: ") + path);
+}
+
+extern "C" int adc_histogram_read_counts(const char* path, int64_t bins, double* counts) {
+  clear_error();
+  if (counts == nullptr) return fail(ADC_E_ARG, "null argument");
+  int64_t fb = 0;
+  double lo, hi, ev;
+  if (int rc = adc_histogram_read_header(path, &fb, &lo, &hi, &ev)) return rc;
+  if (fb != bins)
+    return fail(ADC_E_ARG, "histogram read: file has " + std::to_string(fb) + " bins, not " +
+                               std::to_string(bins));
+  FILE* f = std::fopen(path, "rb");
+  if (f == nullptr || std::fseek(f, (long)kHistHeader, SEEK_SET) != 0) {
+    if (f) std::fclose(f);
+    return fail(ADC_E_ARG, std::string("histogram read: cannot open ") + path);
+  }
+  bool ok = true;
+  if (!is_device_ptr(counts)) {
+    ok = std::fread(counts, 8, (size_t)bins, f) == (size_t)bins;
+  } else {
+    // two pinned pieces: the file read of one overlaps the H2D copy of the other
+    double* bounce[2] = {nullptr, nullptr};
+    cudaStream_t s = nullptr;
+    if (cudaMallocHost(&bounce[0], kHistPiece) != cudaSuccess ||
+        cudaMallocHost(&bounce[1], kHistPiece) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+      if (bounce[0]) cudaFreeHost(bounce[0]);
+      if (bounce[1]) cudaFreeHost(bounce[1]);
+      std::fclose(f);
+      return cuda_fail(cudaGetLastError(), "histogram read: pinned buffers");
+    }
+    cudaEvent_t done[2];
+    cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming);
+    const size_t per = kHistPiece / 8;
+    int k = 0;
+    for (int64_t o = 0; ok && o < bins; o += (int64_t)per, k ^= 1) {
+      const size_t n = (size_t)std::min<int64_t>((int64_t)per, bins - o);
+      ok = cudaEventSynchronize(done[k]) == cudaSuccess && std::fread(bounce[k], 8, n, f) == n &&
+           cudaMemcpyAsync(counts + o, bounce[k], n * 8, cudaMemcpyHostToDevice, s) == cudaSuccess &&
+           cudaEventRecord(done[k], s) == cudaSuccess;
+    }
+    ok = cudaStreamSynchronize(s) == cudaSuccess && ok;
+    cudaEventDestroy(done[0]);
+    cudaEventDestroy(done[1]);
+    cudaStreamDestroy(s);
+    cudaFreeHost(bounce[0]);
+    cudaFreeHost(bounce[1]);
+  }
+  std::fclose(f);
+  return ok ? ADC_OK : fail(ADC_E_ARG, std::string("histogram read: short or unreadable file ") + path);
 }

@@ -37,6 +37,36 @@ class Histogram:
     def width(self) -> float:
         return (self.hi - self.lo) / self.bins
 
+    def save(self, path: str) -> None:
+        """The ingest format (include/adc_cuda.h: "ADCHIST1", bins, lo, hi,
+        events, counts); counts from host (numpy) or device (CUDA tensor)."""
+        c = self.counts
+        if hasattr(c, "is_cuda"):
+            c = c.contiguous()
+            ptr = c.data_ptr()
+        else:
+            c = np.ascontiguousarray(c, dtype=np.float64)
+            ptr = c.ctypes.data
+        check(lib.adc_histogram_write(path.encode(), int(self.bins), float(self.lo), float(self.hi),
+                                      float(self.events), ctypes.c_void_p(ptr)))
+
+    @classmethod
+    def load(cls, path: str, device=None) -> "Histogram":
+        """Read a histogram file; device != None puts the counts in a CUDA
+        tensor on that device (pinned pieces, H2D overlapped with the reads)."""
+        b, lo, hi, ev = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        check(lib.adc_histogram_read_header(path.encode(), ctypes.byref(b), ctypes.byref(lo),
+                                            ctypes.byref(hi), ctypes.byref(ev)))
+        if device is None:
+            counts = np.empty(b.value, dtype=np.float64)
+            ptr = counts.ctypes.data
+        else:
+            import torch
+            counts = torch.empty(b.value, dtype=torch.float64, device=device)
+            ptr = counts.data_ptr()
+        check(lib.adc_histogram_read_counts(path.encode(), b.value, ctypes.c_void_p(ptr)))
+        return cls(b.value, lo.value, hi.value, ev.value, counts)
+
     def center(self, i: int) -> float:
         return self.lo + (i + 0.5) * self.width()
 
