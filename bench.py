@@ -545,30 +545,45 @@ def config_points(workload, local, steps=20, warm=3):
     kms = ms
     if workload == "gauss1d":
         # 48 MB fits in L2 and the API call's host work (validation, race
-        # check, registry lookup) is longer than the kernel: time the kernel
-        # alone from a CUDA graph of the same call, with a 512 MB write
-        # between replays so every replay starts from HBM.
-        flush = torch.empty(64 << 20, dtype=torch.float64, device=dev)
+        # check, registry lookup) is longer than the kernel: the kernel alone
+        # from CUDA graphs of K x [L2 flush, the call] minus K x [L2 flush]
+        # (no graph-launch latency in the difference).  The flush writes
+        # 512 MB and then reads another 256 MB, so every replay starts from
+        # HBM with clean L2 lines (a write-only flush leaves dirty lines whose
+        # write-backs would compete with the kernel).
+        K = 10
+        flush_w = torch.empty(64 << 20, dtype=torch.float64, device=dev)
+        flush_r = torch.ones(32 << 20, dtype=torch.float64, device=dev)
         side = torch.cuda.Stream(dev)
         side.wait_stream(stream)
         with torch.cuda.stream(side):
             step()
+            flush_w.fill_(1.0)
+            flush_r.sum()
         torch.cuda.synchronize()
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=side):
-            step()
+        graphs = {}
+        for with_call in (True, False):
+            g_ = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_, stream=side):
+                for _ in range(K):
+                    flush_w.fill_(1.0)
+                    flush_r.sum()
+                    if with_call:
+                        step()
+            graphs[with_call] = g_
         torch.cuda.synchronize()
-        kl = []
+        tt = {True: [], False: []}
         for _ in range(steps):
-            flush.fill_(1.0)
-            e0, e1 = event_time(graph.replay, stream)
-            torch.cuda.synchronize()
-            kl.append(e0.elapsed_time(e1))
-        kms = statistics.median(kl)
+            for with_call in (True, False):
+                e0, e1 = event_time(graphs[with_call].replay, stream)
+                torch.cuda.synchronize()
+                tt[with_call].append(e0.elapsed_time(e1))
+        kms = (statistics.median(tt[True]) - statistics.median(tt[False])) / K
         rec.update({"value": units / (kms * 1e-3), "api_value": units / (ms * 1e-3),
-                    "note": "value: CUDA-graph replay of the same call, L2 flushed (512 MB write) "
-                            "before each replay; api_*: CUDA events around each public-API call"})
-        del flush, graph
+                    "note": "value: the kernel alone, from CUDA graphs of 10 x [L2 flush (512 MB "
+                            "write + 256 MB read), the call] minus the same without the call; "
+                            "api_*: CUDA events around each public-API call"})
+        del flush_w, flush_r, graphs
     else:
         rec["note"] = f"device-resident, CUDA events around each public-API call; inputs " \
                       f"{32 * npts * dim / 1e9:.0f} GB >> L2"
