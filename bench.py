@@ -747,6 +747,26 @@ def bench_fit(local):
     pass_s = (time.perf_counter() - t0) / reps
     rec = {"workload": WORKLOADS["fit"][2], "value": 1.0 / pass_s, "unit": "gradient passes/s",
            "ms_per_pass": pass_s * 1e3}
+    # the pass's dominant kernel alone (CUDA events inside the library around
+    # the tile kernel), against SURVEY.md §8(d)'s W = 62 per bin (the
+    # exp-per-bin algorithm; this kernel runs 16 bins per thread per tile, one
+    # wave of 245 tiles: latency- and tail-bound, not throughput-bound)
+    plan = eng._plan(h)
+    tk = [plan.tile_kernel_ms(q0) for _ in range(9)]
+    tms = statistics.median(tk[1:])
+    pk = fp64_peak(local)
+    achieved = 62.0 * FIT_BINS / (tms * 1e-3) / 1e12
+    rec["tile_kernel_ms"] = tms
+    rec["roofline"] = {"bound": "fp64", "achieved": achieved, "peak": pk["tinstr_s"],
+                       "unit": "T FP64 instr/s", "frac": achieved / pk["tinstr_s"],
+                       "hbm_frac": 8.0 * FIT_BINS / (tms * 1e-3) / 1e9 / peaks()["hbm_gbs"],
+                       "traffic": None, "work_per_bin": "62 FP64 instr (SURVEY.md §8(d), the "
+                       "exp-per-bin algorithm)", "bins_per_thread": plan.layout.tile_bins // 256,
+                       "peak_source": pk.get("source"),
+                       "kernel_ms": tms,
+                       "note": "1e6 bins = 8 MB: a few-microsecond kernel, launch- and "
+                               "tail-bound; the pass itself (graph replay, 21-double copy back, "
+                               "host finalize) is ms_per_pass"}
     for name, hess in (("newton_numeric_hessian", True), ("gd_armijo", False)):
         ts = []
         for _ in range(3):
