@@ -156,8 +156,11 @@ int adc_cuda_gaussnd_grad_shared_p(int64_t n, int64_t dim, int64_t ld, const dou
 int adc_cuda_gaussnd_grad_shared_p_comm(int64_t n, int64_t dim, int64_t ld, const double* x,
                                         const double* p, double sigma, double* dx, double* dp,
                                         int32_t unsafe, adc_comm* comm, void* stream);
-/* Kernel selection for experiments: 0 = auto, 1 = point-per-thread
- * (reference summation order), 2 = dims-over-warps tile. */
+/* Kernel selection for the calling thread (parity tests): 0 = auto,
+ * 2 = dims over the warps of a 32-point tile, 3 = one warp per 32-point tile
+ * (reference summation order), 10 = two points per lane (double2); + 100 runs
+ * the same kernel on the static grid-stride schedule instead of claimed
+ * spans (same bits). */
 int adc_cuda_gaussnd_set_variant(int32_t variant);
 
 /* ---------------------------------------------------------------------------

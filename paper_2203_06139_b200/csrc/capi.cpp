@@ -2,6 +2,7 @@
 // argument validation mirroring the reference's launch contract, and the
 // host-buffer pipelines (H2D / kernel / D2H overlapped over two streams).
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <mutex>
 #include <thread>
@@ -52,6 +53,45 @@ int sm_count() {
     g_sm_count[dev] = v > 0 ? v : 148;
   }
   return g_sm_count[dev];
+}
+
+// The claim ring: kClaimSlots pairs per device, handed out round-robin, so
+// concurrent launches (other streams, other host threads) use distinct pairs.
+static constexpr uint32_t kClaimSlots = 4096;
+static std::mutex g_claim_mu;
+static unsigned long long* g_claim[64] = {nullptr};
+static std::atomic<uint32_t> g_claim_next[64];
+
+unsigned long long* claim_slot() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_claim_mu);
+    if (!g_claim[dev]) {
+      // relaxed capture mode for this thread: the one-time allocation may
+      // happen while some stream is being captured into a graph; the zero
+      // fill runs on a private non-blocking stream
+      cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+      cudaThreadExchangeStreamCaptureMode(&mode);
+      unsigned long long* ptr = nullptr;
+      cudaStream_t st = nullptr;
+      const size_t bytes = kClaimSlots * 2 * sizeof(unsigned long long);
+      bool ok = cudaMalloc(&ptr, bytes) == cudaSuccess &&
+                cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
+                cudaMemsetAsync(ptr, 0, bytes, st) == cudaSuccess &&
+                cudaStreamSynchronize(st) == cudaSuccess;
+      if (st) cudaStreamDestroy(st);
+      cudaThreadExchangeStreamCaptureMode(&mode);
+      if (!ok) {
+        cudaGetLastError();
+        if (ptr) cudaFree(ptr);
+        return nullptr;
+      }
+      g_claim[dev] = ptr;
+    }
+  }
+  const uint32_t k = g_claim_next[dev].fetch_add(1, std::memory_order_relaxed) % kClaimSlots;
+  return g_claim[dev] + 2 * (size_t)k;
 }
 
 bool device_present() {

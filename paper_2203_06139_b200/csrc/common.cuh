@@ -113,4 +113,25 @@ int cuda_fail(cudaError_t e, const char* what);
 int sm_count();  // cached per device
 bool device_present();
 
+// Dynamic span claiming (K2).  A launch takes a {next span, CTAs done} pair
+// from a per-device ring (zero between launches); each CTA claims spans in
+// order with one atomic, so the spans in flight at any moment are neighbours
+// and the row lines they share are read once, while the data is in L2.  The
+// last CTA out resets the pair, so a launch needs no memset and replays in a
+// CUDA graph.  nullptr (the ring could not be allocated, e.g. first use
+// inside a stream capture) selects the static grid-stride schedule: same
+// per-point arithmetic, same bits.
+unsigned long long* claim_slot();
+
+__device__ __forceinline__ int64_t claim_next(unsigned long long* c) {
+  return (int64_t)atomicAdd(c, 1ull);
+}
+// One thread per CTA, after its last claim (the one past the end).
+__device__ __forceinline__ void claim_done(unsigned long long* c) {
+  if (atomicAdd(c + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
+    atomicExch(c, 0ull);
+    atomicExch(c + 1, 0ull);
+  }
+}
+
 }  // namespace adcb

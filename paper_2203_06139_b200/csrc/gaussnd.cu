@@ -33,8 +33,9 @@ template <int W, int U, int PF, int TPC = 1>
 __global__ void __launch_bounds__(W * 32 * TPC) gaussnd_tile_kernel(
     const double* __restrict__ x, const double* __restrict__ p, double* __restrict__ dx,
     double* __restrict__ dp, int64_t n, int dim, int64_t ld, double t4, double r1, int dpw,
-    int dstage) {
+    int dstage, unsigned long long* claim) {
   extern __shared__ double smem[];
+  __shared__ int64_t s_claim[2];           // claimed span, double-buffered
   double* tpart = smem;                    // [W][32]
   double* stage = smem + W * 32;           // [W][dstage][32]
   const int lane = threadIdx.x & 31;
@@ -49,8 +50,18 @@ __global__ void __launch_bounds__(W * 32 * TPC) gaussnd_tile_kernel(
   const int64_t ntiles = (n + 31) / 32;
   const int64_t gstride = (int64_t)gridDim.x * TPC;  // tiles in flight over the grid
 
-  for (int64_t tile = blockIdx.x * TPC + (TPC > 1 ? warp : 0); tile < ntiles;
-       tile += gstride) {
+  // a span = the TPC tiles of a CTA (one tile when TPC = 1); claimed in
+  // order (claim != nullptr) or grid-stride
+  const int64_t nspans = (ntiles + TPC - 1) / TPC;
+  int64_t span = blockIdx.x;
+  int it = 0;
+  if (claim) {
+    if (threadIdx.x == 0) s_claim[0] = claim_next(claim);
+    __syncthreads();
+    span = s_claim[0];
+  }
+  while (span < nspans) {
+    const int64_t tile = span * TPC + (TPC > 1 ? warp : 0);
     const int64_t i = tile * 32 + lane;
     const bool valid = i < n;
     const double* xi = x + i;
@@ -212,7 +223,16 @@ __global__ void __launch_bounds__(W * 32 * TPC) gaussnd_tile_kernel(
       }
     }
     if (W > 1) __syncthreads();  // tpart is rewritten by the next tile
+    if (claim) {
+      ++it;
+      if (threadIdx.x == 0) s_claim[it & 1] = claim_next(claim);
+      __syncthreads();
+      span = s_claim[it & 1];
+    } else {
+      span += gridDim.x;
+    }
   }
+  if (claim && threadIdx.x == 0) claim_done(claim);
 }
 
 static int make_rows_tmap(CUtensorMap* m, const double* x, int64_t npts, int64_t dim, int64_t ld);
@@ -226,7 +246,7 @@ template <int U>
 __global__ void __launch_bounds__(32) gaussnd_vec2_kernel(
     const double* __restrict__ x, const double* __restrict__ p, double* __restrict__ dx,
     double* __restrict__ dp, int64_t ntiles, int dim, int64_t ld, double t4, double r1,
-    int dstage) {
+    int dstage, unsigned long long* claim) {
   extern __shared__ double2 stage2[];  // [dstage][32]
   const int lane = threadIdx.x;
   const int64_t ld2 = ld / 2;
@@ -234,7 +254,9 @@ __global__ void __launch_bounds__(32) gaussnd_vec2_kernel(
   const double2* p2 = reinterpret_cast<const double2*>(p);
   double2* dx2 = reinterpret_cast<double2*>(dx);
   double2* dp2 = reinterpret_cast<double2*>(dp);
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  int64_t tile = blockIdx.x;
+  if (claim) tile = __shfl_sync(0xffffffffu, lane == 0 ? claim_next(claim) : 0, 0);
+  while (tile < ntiles) {
     const int64_t i2 = tile * 32 + lane;  // double2 index of points 2 i2, 2 i2 + 1
     double ta = 0.0, tb = 0.0;
     int d = 0;
@@ -346,20 +368,27 @@ __global__ void __launch_bounds__(32) gaussnd_vec2_kernel(
       dx2[o] = make_double2(fadd(a.x, ra), fadd(a.y, rb));
       dp2[o] = make_double2(fadd(b.x, -ra), fadd(b.y, -rb));
     }
+    if (claim) {
+      tile = __shfl_sync(0xffffffffu, lane == 0 ? claim_next(claim) : 0, 0);
+    } else {
+      tile += gridDim.x;
+    }
   }
+  if (claim && lane == 0) claim_done(claim);
 }
 
 // ---------------------------------------------------------------------------
 // Kernel selection.  The variant is an argument of every launch (never a
 // process-wide setting, so concurrent callers cannot reroute each other):
-//   0  auto — K2v below 105 dims on a 16-byte-aligned even-ld layout (the
-//      last partial 64-point tile through K2 W = 1), else K2 as choose()
-//      picks it: W = 1 with 8 neighbouring tiles per CTA up to 112 dims,
-//      dims over the warps of a CTA above;
+//   0  auto — K2 as choose() picks it: W = 1 with 8 neighbouring tiles per
+//      CTA up to 112 dims, dims over the warps of a CTA above;
 //   3  K2 with one warp per 32-point tile (the reference summation order;
 //      the tail form of K2v);
 //   2  K2 with the dims split over the warps of a CTA (W = 8 / 16);
-//   10 K2v (where the layout allows it; the rest through variant 3).
+//   10 K2v (where the layout allows it; the rest through variant 3);
+//   + 100  the same kernel on the static grid-stride schedule instead of
+//      claimed spans (claim_slot in common.cuh; also what runs when the
+//      claim ring is unavailable).  Same bits either way.
 // The forced forms exist for the parity tests, which check that every kernel
 // auto can pick gives the same per-point bits (W = 1 forms) or stays within
 // the regrouping tolerance (W > 1).  Measured alternatives that were not
@@ -375,7 +404,7 @@ struct NdConfig {
 template <int W, int U, int PF = 1, int TPC = 1>
 static int launch_tile(const NdConfig& c, int64_t n, int dim, int64_t ld, const double* x,
                        const double* p, double* dx, double* dp, double t4, double r1,
-                       cudaStream_t s) {
+                       cudaStream_t s, bool dyn) {
   auto k = gaussnd_tile_kernel<W, U, PF, TPC>;
   const size_t smem = TPC > 1 ? ((size_t)TPC * 32 + (size_t)TPC * c.dstage * 32) * sizeof(double)
                               : c.smem;
@@ -386,7 +415,9 @@ static int launch_tile(const NdConfig& c, int64_t n, int dim, int64_t ld, const 
   if (occ < 1) return fail(ADC_E_LAUNCH, "gaussnd: tile configuration does not fit an SM");
   const int64_t ntiles = (n + 31) / 32;
   int64_t blocks = std::min<int64_t>((ntiles + TPC - 1) / TPC, (int64_t)occ * sm_count());
-  k<<<(unsigned)blocks, W * 32 * TPC, smem, s>>>(x, p, dx, dp, n, dim, ld, t4, r1, c.dpw, c.dstage);
+  unsigned long long* claim = dyn && blocks < (ntiles + TPC - 1) / TPC ? claim_slot() : nullptr;
+  k<<<(unsigned)blocks, W * 32 * TPC, smem, s>>>(x, p, dx, dp, n, dim, ld, t4, r1, c.dpw, c.dstage,
+                                                  claim);
   ADCB_CUDA(cudaGetLastError());
   return ADC_OK;
 }
@@ -426,11 +457,15 @@ static int launch_gaussnd_v(int64_t n, int64_t dim, int64_t ld, const double* x,
   if (n > 0 && t4 == 0.0) return fail(ADC_E_EVAL, "division by zero");
   if (n == 0) return ADC_OK;
   if (dim > (1 << 24)) return fail(ADC_E_ARG, "gaussnd: dim too large");
+  // + 100: the static grid-stride schedule (parity tests of that path)
+  const bool dyn = variant < 100;
+  variant %= 100;
   double d_t9 = 0;
   d_t9 += (std::pow(2 * PI, -0.5) * std::pow(sigma, -0.5)) * 1.0;  // _d__t9 += _t8 * _r0
-  // K2v for dims whose u rows all fit its 52 KB stage (the dim-100 headline:
-  // 6.0 TB/s vs 5.8 for K2, the same bits per point).
-  if ((variant == 0 && dim <= 104) || variant == 10) {
+  // K2v (forced only): two points per lane.  It was the dim-100 headline
+  // kernel (7.94 ms) until the claimed spans made K2 faster (7.53 ms); with
+  // claiming its 64-point tiles need 4x K2's claims (dim 2: 13.3 ms).
+  if (variant == 10) {
     const int64_t ntiles = n / 64;
     const bool ok = ld % 2 == 0 && ((((uintptr_t)x) | ((uintptr_t)p) | ((uintptr_t)dx) |
                                      ((uintptr_t)dp)) & 15) == 0;
@@ -447,13 +482,15 @@ static int launch_gaussnd_v(int64_t n, int64_t dim, int64_t ld, const double* x,
       int occ = 0;
       ADCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 32, smem));
       const int64_t blocks = std::min<int64_t>(ntiles, (int64_t)std::max(1, occ) * sm_count());
-      k<<<(unsigned)blocks, 32, smem, s>>>(x, p, dx, dp, ntiles, (int)dim, ld, t4, d_t9, dstage);
+      unsigned long long* claim = dyn && blocks < ntiles ? claim_slot() : nullptr;
+      k<<<(unsigned)blocks, 32, smem, s>>>(x, p, dx, dp, ntiles, (int)dim, ld, t4, d_t9, dstage,
+                                           claim);
       ADCB_CUDA(cudaGetLastError());
       const int64_t done = ntiles * 64;
       if (done == n) return ADC_OK;
       // the last partial tile through K2 (W = 1 for these dims: same per-point bits)
       return launch_gaussnd_v(n - done, dim, ld, x + done, p + done, sigma, dx + done, dp + done,
-                              s, 3);
+                              s, dyn ? 3 : 103);
     }
   }
   const NdConfig c = choose((int)dim, variant);
@@ -461,21 +498,23 @@ static int launch_gaussnd_v(int64_t n, int64_t dim, int64_t ld, const double* x,
   if (c.w == 1) {
     // Auto: 8 neighbouring tiles per CTA from 2 dims while the stages fit one
     // CTA, with a row batch no longer than the dims: same bits as one warp
-    // per CTA, 3-19% faster (10M x 100: 7.93 vs 8.29 ms aligned, 10.1 vs
-    // 12.0 ms with odd n) and 2x at dim 8 (U = 16 never batches).
+    // per CTA.  Static schedule: 3-19% faster than one tile per CTA (10M x
+    // 100: 7.93 vs 8.29 ms aligned, 10.1 vs 12.0 ms with odd n); claimed
+    // spans: 7.53 ms aligned, 9.67 odd.  Deeper row batches
+    // (U = 24 / 32) spill and were slower.
     const bool fits = (size_t)8 * 32 * 8 + (size_t)8 * c.dstage * 256 <= 227 * 1024;
     if (variant == 0 && fits) {
-      if (dim >= 16) return launch_tile<1, 16, 1, 8>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s);
-      if (dim >= 8) return launch_tile<1, 8, 1, 8>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s);
-      if (dim >= 4) return launch_tile<1, 4, 1, 8>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s);
-      if (dim >= 2) return launch_tile<1, 2, 1, 8>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s);
+      if (dim >= 16) return launch_tile<1, 16, 1, 8>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s, dyn);
+      if (dim >= 8) return launch_tile<1, 8, 1, 8>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s, dyn);
+      if (dim >= 4) return launch_tile<1, 4, 1, 8>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s, dyn);
+      if (dim >= 2) return launch_tile<1, 2, 1, 8>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s, dyn);
     }
-    return launch_tile<1, 16>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s);
+    return launch_tile<1, 16>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s, dyn);
   }
   // bulk (TMA-unit) L2 prefetch of the next rows: 2.4% faster at dim 1000
   // (8.24 vs 8.45 ms, same bits)
-  if (c.w == 16) return launch_tile<16, 8, 2>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s);
-  return launch_tile<8, 8>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s);
+  if (c.w == 16) return launch_tile<16, 8, 2>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s, dyn);
+  return launch_tile<8, 8>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s, dyn);
 }
 
 int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, const double* p,
@@ -484,8 +523,9 @@ int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, con
 }
 
 int gaussnd_set_variant(int v) {
-  if (v != 0 && v != 2 && v != 3 && v != 10)
-    return fail(ADC_E_ARG, "gaussnd variant must be 0 (auto), 2, 3 or 10");
+  const int k = v % 100;
+  if (v < 0 || v >= 200 || (k != 0 && k != 2 && k != 3 && k != 10))
+    return fail(ADC_E_ARG, "gaussnd variant must be 0 (auto), 2, 3 or 10, + 100 for the static schedule");
   t_variant = v;
   return ADC_OK;
 }

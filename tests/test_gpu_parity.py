@@ -114,7 +114,7 @@ def test_listing1_domain_error():
 ND_KEYS = ["d100_n64", "d1000_n8", "d1_n33", "d37_n70", "d128_n40", "d129_n5"]
 
 
-@pytest.mark.parametrize("variant", [0, 2, 3, 10])
+@pytest.mark.parametrize("variant", [0, 2, 3, 10, 100, 102])
 @pytest.mark.parametrize("key", ND_KEYS)
 def test_gaussnd_golden(key, variant):
     g = golden("gaussnd_cases.npz")
@@ -143,14 +143,15 @@ def test_gaussnd_host_path():
                                    (5, 77), (300, 1000), (2, 4097), (3, 1000), (4, 2049),
                                    (6, 640), (8, 1001), (12, 777), (16, 3000), (110, 513)])
 def test_gaussnd_vs_oracle(restate, dim, n):
-    # variant 0 = auto (K2v with double2 for dim <= 104 on even ld, tail via K2;
-    # the row batch U follows the dims; K2 runs 8 neighbouring tiles per CTA
-    # up to 112 dims), 3 = K2 one warp per 32-point tile, 2 = K2 with the
-    # dims over the warps of a CTA, 10 = K2v forced
+    # variant 0 = auto (K2: 8 neighbouring tiles per CTA up to 112 dims, the
+    # row batch U following the dims; dims over the warps of a CTA above;
+    # spans claimed in order), 3 = K2 one warp per 32-point tile, 2 = K2 with
+    # the dims over the warps of a CTA, 10 = K2v (double2) forced; + 100 =
+    # the static grid-stride schedule
     x, p = synth.points_nd(dim, n, seed=dim)
     ox, op = np.zeros((dim, n)), np.zeros((dim, n))
     restate.gaussnd_grad(x, p, 1.3, ox, op)
-    for variant in (0, 2, 3, 10):
+    for variant in (0, 2, 3, 10, 100, 102, 103):
         set_gaussnd_variant(variant)
         try:
             dx = torch.zeros((dim, n), dtype=torch.float64, device=DEV)
@@ -174,6 +175,65 @@ def test_gaussnd_accumulates_twice():
     once = host(dx).copy()
     adc.launch_batch("gaussnd_grad_0_1", X, P, 0.9, dx, dp)
     assert np.array_equal(host(dx), 2 * once)
+
+
+def _nd_repeat(variant, X, P, launches, sigma=1.1):
+    set_gaussnd_variant(variant)
+    try:
+        dx = torch.zeros_like(X)
+        dp = torch.zeros_like(X)
+        for _ in range(launches):
+            adc.launch_batch("gaussnd_grad_0_1", X, P, sigma, dx, dp)
+        return host(dx), host(dp)
+    finally:
+        set_gaussnd_variant(0)
+
+
+@pytest.mark.parametrize("dim,n", [(2, 400_003), (37, 200_001), (300, 30_011)])
+def test_gaussnd_claimed_spans_match_static(dim, n):
+    # Claimed spans (auto) and the static grid-stride schedule (+100) run the
+    # same per-point arithmetic: bit-identical, with more spans than CTAs so
+    # claiming engages (dim 2: ~1.5k spans of 256 points).
+    x, p = synth.points_nd(dim, n, seed=dim + 1)
+    X, P = t(x), t(p)
+    a = _nd_repeat(0, X, P, 1)
+    b = _nd_repeat(100, X, P, 1)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_gaussnd_claim_ring_wraps():
+    # 4100 launches walk every pair of the 4096-slot claim ring and reuse some:
+    # each launch's last CTA must leave its pair at zero, or a reused pair
+    # would skip spans.  The accumulated slots equal the static schedule's.
+    x, p = synth.points_nd(2, 400_003, seed=11)
+    X, P = t(x), t(p)
+    a = _nd_repeat(0, X, P, 4100)
+    b = _nd_repeat(100, X, P, 4100)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_gaussnd_claimed_spans_in_cuda_graph():
+    # a captured launch keeps one claim pair; the kernel resets it, so graph
+    # replays accumulate exactly like eager launches
+    x, p = synth.points_nd(37, 200_001, seed=4)
+    X, P = t(x), t(p)
+    eager = _nd_repeat(0, X, P, 3)
+    dx = torch.zeros_like(X)
+    dp = torch.zeros_like(X)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        adc.launch_batch("gaussnd_grad_0_1", X, P, 1.1, dx, dp)  # warm-up outside capture
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    dx.zero_()
+    dp.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        adc.launch_batch("gaussnd_grad_0_1", X, P, 1.1, dx, dp)
+    for _ in range(3):
+        g.replay()
+    assert np.array_equal(host(dx), eager[0]) and np.array_equal(host(dp), eager[1])
 
 
 # ---------------------------------------------------------------------------- chi2
