@@ -29,6 +29,11 @@
 
 namespace adcb {
 
+// x and p rows are read through L1 (ld.global.nc, allocating): at rows that
+// are not 128 B aligned, the line two neighbouring warps of a CTA share is
+// then one L2 request, not two.  Measured against no-allocate loads (ms):
+// 10M x 100 odd n 8.94 vs 9.73, 1M x 1000 7.90 vs 8.10 (odd 9.72 vs 10.73),
+// 5M x 200 odd 7.56 vs 8.04, 3,333,334 x 300 7.77 vs 8.50.
 template <int W, int U, int PF, int TPC = 1>
 __global__ void __launch_bounds__(W * 32 * TPC) gaussnd_tile_kernel(
     const double* __restrict__ x, const double* __restrict__ p, double* __restrict__ dx,
@@ -74,8 +79,8 @@ __global__ void __launch_bounds__(W * 32 * TPC) gaussnd_tile_kernel(
         double xv[U], pv[U];
 #pragma unroll
         for (int k = 0; k < U; ++k) {
-          xv[k] = ld_stream(xi + (int64_t)(d + k) * ld);
-          pv[k] = ld_stream(pi + (int64_t)(d + k) * ld);
+          xv[k] = __ldg(xi + (int64_t)(d + k) * ld);
+          pv[k] = __ldg(pi + (int64_t)(d + k) * ld);
         }
         if (PF == 2) {
           // lane l < U: x row d+U+l, lane U+l: p row d+U+l (one 256 B segment
@@ -116,7 +121,7 @@ __global__ void __launch_bounds__(W * 32 * TPC) gaussnd_tile_kernel(
         }
       }
       for (; d < d1; ++d) {
-        const double u = fsub(ld_stream(xi + (int64_t)d * ld), ld_stream(pi + (int64_t)d * ld));
+        const double u = fsub(__ldg(xi + (int64_t)d * ld), __ldg(pi + (int64_t)d * ld));
         if (d - d0 < dstage) my_stage[(d - d0) * 32] = u;
         t = fadd(t, fmul(u, u));
       }
@@ -145,8 +150,8 @@ __global__ void __launch_bounds__(W * 32 * TPC) gaussnd_tile_kernel(
 #pragma unroll
         for (int k = 0; k < U; ++k) {
           const int64_t o = (int64_t)(d - 1 - k) * ld;
-          xv[k] = ld_stream(xi + o);
-          pv[k] = ld_stream(pi + o);
+          xv[k] = __ldg(xi + o);
+          pv[k] = __ldg(pi + o);
           a[k] = dxi[o];
           b[k] = dpi[o];
         }
@@ -161,7 +166,7 @@ __global__ void __launch_bounds__(W * 32 * TPC) gaussnd_tile_kernel(
       }
       for (; d > dre; --d) {
         const int64_t o = (int64_t)(d - 1) * ld;
-        const double u = fsub(ld_stream(xi + o), ld_stream(pi + o));
+        const double u = fsub(__ldg(xi + o), __ldg(pi + o));
         const double r6 = fadd(fadd(0.0, fmul(c, u)), fmul(u, c));
         dxi[o] = fadd(dxi[o], r6);
         dpi[o] = fadd(dpi[o], -r6);
