@@ -94,6 +94,43 @@ unsigned long long* claim_slot() {
   return g_claim[dev] + 2 * (size_t)k;
 }
 
+// Stream-ordered workspaces come from a private per-device pool that keeps
+// its memory (release threshold = max): with the default pool's threshold 0,
+// every synchronize handed the pages back and the next call re-mapped them
+// inside the timed stream work (shared-mean launches varied 1.7 - 20 ms).
+static cudaMemPool_t g_pool[64] = {nullptr};
+
+cudaError_t ws_alloc(void** ptr, size_t bytes, cudaStream_t s) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaMallocAsync(ptr, bytes, s);
+  {
+    std::lock_guard<std::mutex> lk(g_claim_mu);
+    if (!g_pool[dev]) {
+      cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+      cudaThreadExchangeStreamCaptureMode(&mode);
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      cudaMemPool_t pool = nullptr;
+      e = cudaMemPoolCreate(&pool, &props);
+      if (e == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      cudaThreadExchangeStreamCaptureMode(&mode);
+      if (e != cudaSuccess) {
+        if (pool) cudaMemPoolDestroy(pool);
+        return e;
+      }
+      g_pool[dev] = pool;
+    }
+  }
+  return cudaMallocFromPoolAsync(ptr, bytes, g_pool[dev], s);
+}
+
 bool device_present() {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) {
@@ -352,7 +389,7 @@ extern "C" int adc_cuda_compute_gauss_shared(int64_t grid, int64_t block, int64_
   // CTA partials of the dsigma reduction: stream-ordered scratch.
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   double* ws = nullptr;
-  ADCB_CUDA(cudaMallocAsync(&ws, (size_t)gauss_shared_blocks(n) * sizeof(double), s));
+  ADCB_CUDA(ws_alloc((void**)&ws, (size_t)gauss_shared_blocks(n) * sizeof(double), s));
   const int rc = launch_gauss_shared(n, x, p, sigma, dx, dp, dsigma, ws, s);
   cudaFreeAsync(ws, s);
   return rc;
@@ -537,7 +574,7 @@ extern "C" int adc_cuda_gaussnd_grad_shared_p(int64_t n, int64_t dim, int64_t ld
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (n == 0 || dim == 0) return launch_gaussnd_shared_p(n, dim, ld, x, p, sigma, dx, dp, nullptr, s);
   double* ws = nullptr;
-  ADCB_CUDA(cudaMallocAsync(&ws, (size_t)(gaussnd_shared_p_blocks(n) + 1) * dim * sizeof(double), s));
+  ADCB_CUDA(ws_alloc((void**)&ws, (size_t)(gaussnd_shared_p_blocks(n) + 1) * dim * sizeof(double), s));
   const int rc = launch_gaussnd_shared_p(n, dim, ld, x, p, sigma, dx, dp, ws, s);
   cudaFreeAsync(ws, s);
   return rc;
@@ -552,7 +589,7 @@ int rank_sum_into(adc_comm* comm, const double* part, int64_t count, double* dst
   if (count == 0) return ADC_OK;
   const int W = comm->world;
   double* parts = nullptr;
-  ADCB_CUDA(cudaMallocAsync(&parts, (size_t)W * count * sizeof(double), s));
+  ADCB_CUDA(ws_alloc((void**)&parts, (size_t)W * count * sizeof(double), s));
   int rc = ADC_OK;
   if (comm->kind == ADC_COMM_NCCL) {
     rc = comm_allgather_enqueue(comm, part, parts, (size_t)count, s);
@@ -594,11 +631,11 @@ extern "C" int adc_cuda_gaussnd_grad_shared_p_comm(int64_t n, int64_t dim, int64
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // this rank's partial (every rank takes part in the exchange, n = 0 too)
   double *part = nullptr, *ws = nullptr;
-  ADCB_CUDA(cudaMallocAsync(&part, (size_t)dim * sizeof(double), s));
+  ADCB_CUDA(ws_alloc((void**)&part, (size_t)dim * sizeof(double), s));
   ADCB_CUDA(cudaMemsetAsync(part, 0, (size_t)dim * sizeof(double), s));
   int rc = ADC_OK;
   if (n > 0) {
-    ADCB_CUDA(cudaMallocAsync(&ws, (size_t)(gaussnd_shared_p_blocks(n) + 1) * dim * sizeof(double), s));
+    ADCB_CUDA(ws_alloc((void**)&ws, (size_t)(gaussnd_shared_p_blocks(n) + 1) * dim * sizeof(double), s));
     rc = launch_gaussnd_shared_p(n, dim, ld, x, p, sigma, dx, part, ws, s);
   }
   if (rc == ADC_OK) rc = rank_sum_into(comm, part, dim, dp, s);
@@ -619,9 +656,9 @@ extern "C" int adc_cuda_compute_gauss_shared_comm(int64_t grid, int64_t block, i
   if (int rc = require_device()) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   double *part = nullptr, *ws = nullptr;
-  ADCB_CUDA(cudaMallocAsync(&part, sizeof(double), s));
+  ADCB_CUDA(ws_alloc((void**)&part, sizeof(double), s));
   ADCB_CUDA(cudaMemsetAsync(part, 0, sizeof(double), s));
-  ADCB_CUDA(cudaMallocAsync(&ws, (size_t)gauss_shared_blocks(n) * sizeof(double), s));
+  ADCB_CUDA(ws_alloc((void**)&ws, (size_t)gauss_shared_blocks(n) * sizeof(double), s));
   int rc = launch_gauss_shared(n, x, p, sigma, dx, dp, part, ws, s);
   if (rc == ADC_OK) rc = rank_sum_into(comm, part, 1, dsigma, s);
   cudaFreeAsync(ws, s);

@@ -955,8 +955,8 @@ extern "C" int adc_cuda_histogram_sample(int32_t model, int32_t np, const double
   double* qd = nullptr;
   double* ws = nullptr;
   const int64_t wsn = histogram_sample_ws_doubles(bins);
-  ADCB_CUDA(cudaMallocAsync(&qd, qdev_bytes(), s));
-  ADCB_CUDA(cudaMallocAsync(&ws, (size_t)wsn * sizeof(double), s));
+  ADCB_CUDA(ws_alloc((void**)&qd, qdev_bytes(), s));
+  ADCB_CUDA(ws_alloc((void**)&ws, (size_t)wsn * sizeof(double), s));
   ADCB_CUDA(cudaMemcpyAsync(qd, hq.data(), qdev_bytes(), cudaMemcpyHostToDevice, s));
   int rc = histogram_sample_enqueue(model, np, qd, bins, lo, (hi - lo) / (double)bins, events,
                                     seed, zero_every, counts, ws, s);

@@ -111,6 +111,9 @@ int cuda_fail(cudaError_t e, const char* what);
   } while (0)
 
 int sm_count();  // cached per device
+// Stream-ordered workspace from the device's private pool (free with
+// cudaFreeAsync on the same stream).
+cudaError_t ws_alloc(void** ptr, size_t bytes, cudaStream_t s);
 bool device_present();
 
 // Dynamic span claiming (K2).  A launch takes a {next span, CTAs done} pair

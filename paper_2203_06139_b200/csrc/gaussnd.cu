@@ -546,12 +546,16 @@ int gaussnd_set_variant(int v) {
 // CTA partials in order, then dp[d] += total.  No atomics; the same bits on
 // every run and device.
 constexpr int64_t kSharedPMaxBlocks = 1184;
+constexpr int64_t kSharedPRowsMaxDim = 24;  // K2sr below, the staged-tile forms above
 
 template <int U, int V>
 __global__ void __launch_bounds__(32) gaussnd_shared_p_kernel(
     const double* __restrict__ x, const double* __restrict__ p, double* __restrict__ dx,
     int64_t n, int dim, int64_t ld, double t4, double r1, int dstage,
-    double* __restrict__ partials) {
+    double* __restrict__ partials, int dq) {
+  // dq: the forward sum runs in chunks of dq dims combined in order, the
+  // grouping of the TMA form's warps, so a point's bits do not depend on
+  // which of the two forms its layout selects (dq >= dim: one chunk)
   extern __shared__ double smem[];
   double* dpart = smem;              // [dim]
   double* stage = smem + dim;        // [dstage][32]
@@ -564,7 +568,18 @@ __global__ void __launch_bounds__(32) gaussnd_shared_p_kernel(
     const bool valid = i < n;
     const double* xi = x + i;
     // ---- forward: U rows in flight, the next U rows prefetched into L2
-    double t = 0.0;
+    double t = 0.0, tc = 0.0;
+    int left = dq;
+    bool first = true;
+    auto add = [&](double u) {
+      tc = fadd(tc, fmul(u, u));  // t = t + _t1 (this chunk)
+      if (--left == 0) {
+        t = first ? tc : fadd(t, tc);
+        first = false;
+        tc = 0.0;
+        left = dq;
+      }
+    };
     if (valid) {
       int d = 0;
       for (; d + U <= dim; d += U) {
@@ -582,14 +597,15 @@ __global__ void __launch_bounds__(32) gaussnd_shared_p_kernel(
         for (int k = 0; k < U; ++k) {
           const double u = fsub(xv[k], __ldg(p + d + k));  // _t0 = x[i] - p[i]
           if (d + k < dstage) stage[(d + k) * 32 + lane] = u;
-          t = fadd(t, fmul(u, u));                          // t = t + _t1
+          add(u);
         }
       }
       for (; d < dim; ++d) {
         const double u = fsub(ld_stream(xi + (int64_t)d * ld), __ldg(p + d));
         if (d < dstage) stage[d * 32 + lane] = u;
-        t = fadd(t, fmul(u, u));
+        add(u);
       }
+      if (left != dq) t = first ? tc : fadd(t, tc);  // the last, partial chunk
     }
     const double tt = fdiv(-t, t4);
     const double e = exp(tt);
@@ -662,28 +678,36 @@ __global__ void __launch_bounds__(32) gaussnd_shared_p_kernel(
 // rotated point order (l + s) % 32 (bank-conflict free), into registers — no
 // cross-lane reductions per element.  dx (optional) stays per point.  Full
 // 32-point tiles only; dim <= 32 * JMAX.
-template <int V, int JMAX>
-__global__ void __launch_bounds__(32) gaussnd_shared_p_tma_kernel(
+template <int V, int JMAX, int NW>
+__global__ void __launch_bounds__(32 * NW) gaussnd_shared_p_tma_kernel(
     const __grid_constant__ CUtensorMap tmap, const double* __restrict__ x,
     const double* __restrict__ p, double* __restrict__ dx, int64_t ntiles, int dim, int64_t ld,
     double t4, double r1, double* __restrict__ partials) {
+  // NW warps share each staged tile: warp w sums the forward t over dims
+  // [w dq, (w+1) dq) (the NW partials combined in warp order), does the dx
+  // read-modify-write of those dims, and owns dims w 32 + lane + 32 NW j of
+  // the transposed dp sum.  With one warp per SM sub-partition the tile's
+  // dependent FP64 chains (100 adds of t, 32 of each dp owner) left the warp
+  // waiting on fixed latency (ncu: issue active 38%, stall "wait" dominant).
   extern __shared__ __align__(128) double smem[];
-  double* buf0 = smem;                       // [dim][32]
-  double* buf1 = smem + (size_t)dim * 32;    // [dim][32]
-  double* cbuf = smem + (size_t)dim * 64;    // [32]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(cbuf + 32);  // 2 mbarriers
-  const int lane = threadIdx.x;
-  if (lane == 0) {
+  double* buf0 = smem;                              // [dim][32]
+  double* buf1 = smem + (size_t)dim * 32;           // [dim][32]
+  double* cbuf = smem + (size_t)dim * 64;           // [NW][32]: each warp's copy of c
+  double* tpart = cbuf + 32 * NW;                   // [NW][32]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tpart + 32 * NW);  // 2 mbarriers
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncwarp();
+  __syncthreads();
   const uint32_t tile_bytes = (uint32_t)dim * 256u;
   // one 2-D TMA load per tile: box {32 points, dim rows} -> buf[dim][32]
   auto issue = [&](int64_t tile, int b) {
     double* buf = b ? buf1 : buf0;
-    if (lane == 0) {
+    if (threadIdx.x == 0) {
       mbar_arrive_expect_tx(&bar[b], tile_bytes);
       asm volatile(
           "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
@@ -693,14 +717,17 @@ __global__ void __launch_bounds__(32) gaussnd_shared_p_tma_kernel(
           : "memory");
     }
   };
+  const int dq = (dim + NW - 1) / NW;
+  const int f0 = min(dim, warp * dq), f1 = min(dim, f0 + dq);  // this warp's forward dims
   double acc[JMAX];
   double pj[JMAX];
 #pragma unroll
   for (int j = 0; j < JMAX; ++j) {
     acc[j] = 0.0;
-    const int d = lane + 32 * j;
+    const int d = warp * 32 + lane + 32 * NW * j;
     pj[j] = d < dim ? __ldg(p + d) : 0.0;
   }
+  double* my_c = cbuf + warp * 32;
   uint32_t phase[2] = {0u, 0u};
   int64_t tile = blockIdx.x;
   if (tile < ntiles) issue(tile, 0);
@@ -712,19 +739,26 @@ __global__ void __launch_bounds__(32) gaussnd_shared_p_tma_kernel(
     phase[b] ^= 1u;
     const int64_t i = tile * 32 + lane;
     double t = 0.0;
-    for (int d = 0; d < dim; ++d) {
+    for (int d = f0; d < f1; ++d) {
       const double u = fsub(buf[d * 32 + lane], __ldg(p + d));  // _t0 = x[i] - p[i]
       t = fadd(t, fmul(u, u));                                 // t = t + _t1
+    }
+    if (NW > 1) {
+      tpart[warp * 32 + lane] = t;
+      __syncthreads();
+      t = tpart[lane];
+#pragma unroll
+      for (int w = 1; w < NW; ++w) t = fadd(t, tpart[w * 32 + lane]);
     }
     const double tt = fdiv(-t, t4);
     const double e = exp(tt);
     const double r2 = fadd(0.0, fmul(r1, e));
     const double r3 = fadd(0.0, fdiv(r2, t4));
     const double c = fadd(0.0, -r3);
-    cbuf[lane] = c;
-    if (dx != nullptr) {  // _d_x[_i0] += _r6, the generated reverse order
-      int d = dim - 1;
-      for (; d - (V - 1) >= 0; d -= V) {
+    my_c[lane] = c;
+    if (dx != nullptr) {  // _d_x[_i0] += _r6 over this warp's dims (each slot once)
+      int d = f1 - 1;
+      for (; d - (V - 1) >= f0; d -= V) {
         double a[V];
 #pragma unroll
         for (int q = 0; q < V; ++q) a[q] = dx[i + (int64_t)(d - q) * ld];
@@ -735,168 +769,127 @@ __global__ void __launch_bounds__(32) gaussnd_shared_p_tma_kernel(
           dx[i + (int64_t)dd * ld] = fadd(a[q], fadd(fadd(0.0, fmul(c, u)), fmul(u, c)));
         }
       }
-      for (; d >= 0; --d) {
+      for (; d >= f0; --d) {
         const double u = fsub(buf[d * 32 + lane], __ldg(p + d));
         double* a = dx + i + (int64_t)d * ld;
         *a = fadd(*a, fadd(fadd(0.0, fmul(c, u)), fmul(u, c)));
       }
     }
-    __syncwarp();  // cbuf visible
-    // _d_p[d] += -_r6 of every point of the tile, lane l owning dims l + 32 j
+    __syncwarp();  // my_c visible to the warp
+    // _d_p[d] += -_r6 of every point of the tile
 #pragma unroll
     for (int j = 0; j < JMAX; ++j) {
-      const int d = lane + 32 * j;
-      if (j * 32 < dim && d < dim) {
+      const int d = warp * 32 + lane + 32 * NW * j;
+      if (32 * NW * j < dim && d < dim) {
         const double* row = buf + d * 32;
         double aj = acc[j];
         for (int s = 0; s < 32; ++s) {
           const int l = (lane + s) & 31;
-          const double cl = cbuf[l];
+          const double cl = my_c[l];
           const double u = fsub(row[l], pj[j]);
           aj = fadd(aj, -fadd(fadd(0.0, fmul(cl, u)), fmul(u, cl)));
         }
         acc[j] = aj;
       }
     }
-    __syncwarp();  // every lane is done reading buf / cbuf before they are refilled
+    // every warp is done reading buf / its c / tpart before they are refilled
+    if (NW > 1) __syncthreads(); else __syncwarp();
     if (tile + 2 * (int64_t)gridDim.x < ntiles) issue(tile + 2 * (int64_t)gridDim.x, b);
   }
 #pragma unroll
   for (int j = 0; j < JMAX; ++j) {
-    const int d = lane + 32 * j;
+    const int d = warp * 32 + lane + 32 * NW * j;
     if (d < dim) partials[(int64_t)blockIdx.x * dim + d] = acc[j];
   }
 }
 
-// K2sv: the shared-mean form on K2v's layout — two points per lane with
-// double2 row accesses (64-point tiles, 512 B per row access, U rows in
-// flight, the next rows prefetched into L2), every dim's u staged for the
-// reverse sweep, dx per point (optional).  The reverse sweep overwrites each
-// staged u with the point's -_r6; dp is then summed transposed: lane l owns
-// dims l + 32 j and adds the tile's 64 staged -_r6 in the rotated point order
-// (l + s) % 64 (no bank conflicts, no shuffles), into registers.  A CTA walks
-// tiles b, b + G, ... (G = kSharedPVecBlocks, fixed): a fixed order that
-// depends on n only.  Full 64-point tiles of a 16-byte-aligned even-ld
-// layout, dim <= 32 * JMAX.
-constexpr int64_t kSharedPVecBlocks = 592;
-
-template <int UF, int U, int JMAX, bool DX>
-__global__ void __launch_bounds__(32) gaussnd_shared_p_vec2_kernel(
+// K2sr: the shared-mean form for dims <= 24 (DIM at compile time).  A
+// 32-point tile of so few rows is too little work per staged tile (the TMA
+// form ran dim 8 at 1.7 TB/s), so here a thread owns single points: PPT
+// points in flight per thread (PPT x DIM loads, each warp row access one
+// 256 B segment), the forward sum and scalar chain per point as K2, dx per
+// point (optional), and the point's -_r6 added to the thread's DIM
+// accumulators.  Thread g walks points g, g + T, ... (T = grid threads, the
+// grid a function of n only); the CTA combines its threads per dim with a
+// fixed xor tree and then its 8 warps in order: deterministic.
+template <int DIM, int PPT, bool DX>
+__global__ void __launch_bounds__(256) gaussnd_shared_p_rows_kernel(
     const double* __restrict__ x, const double* __restrict__ p, double* __restrict__ dx,
-    int64_t ntiles, int dim, int64_t ld, double t4, double r1, double* __restrict__ partials) {
-  extern __shared__ double2 stage2[];  // [dim][32]: u, then -_r6, of points 2 i2, 2 i2 + 1
-  const int lane = threadIdx.x;
-  const int64_t ld2 = ld / 2;
-  const double2* x2 = reinterpret_cast<const double2*>(x);
-  double2* dx2 = reinterpret_cast<double2*>(dx);
-  double acc[JMAX];
+    int64_t n, int64_t ld, double t4, double r1, double* __restrict__ partials) {
+  __shared__ double wsum[8][DIM];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int64_t T = (int64_t)gridDim.x * 256;
+  double pv[DIM], acc[DIM];
 #pragma unroll
-  for (int j = 0; j < JMAX; ++j) acc[j] = 0.0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t i2 = tile * 32 + lane;
-    const bool more = tile + gridDim.x < ntiles;
-    double ta = 0.0, tb = 0.0;
-    int d = 0;
-    for (; d + UF <= dim; d += UF) {
-      double2 xv[UF];
+  for (int d = 0; d < DIM; ++d) {
+    pv[d] = __ldg(p + d);
+    acc[d] = 0.0;
+  }
+  for (int64_t i0 = (int64_t)blockIdx.x * 256 + threadIdx.x; i0 < n; i0 += T * PPT) {
+    double xv[PPT][DIM];
 #pragma unroll
-      for (int k = 0; k < UF; ++k) xv[k] = ld_stream2(x2 + (int64_t)(d + k) * ld2 + i2);
+    for (int q = 0; q < PPT; ++q) {
+      const int64_t i = i0 + q * T;
+      if (i < n) {
 #pragma unroll
-      for (int k = 0; k < UF; ++k) {  // next batch (or the first reverse rows) into L2
-        const int dn = d + UF + k;
-        if ((lane & 7) == 0) {
-          if (dn < dim) prefetch_l2(x2 + (int64_t)dn * ld2 + i2);
-          else if (DX && dim - 1 - (dn - dim) >= 0)
-            prefetch_l2(dx2 + (int64_t)(dim - 1 - (dn - dim)) * ld2 + i2);
+        for (int d = 0; d < DIM; ++d) xv[q][d] = __ldg(x + i + d * ld);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      const int64_t i = i0 + q * T;
+      if (i < n) {
+        double t = 0.0;
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) {
+          xv[q][d] = fsub(xv[q][d], pv[d]);                // _t0 = x[i] - p[i]
+          t = fadd(t, fmul(xv[q][d], xv[q][d]));           // t = t + _t1
+        }
+        const double e = exp(fdiv(-t, t4));
+        const double c = fadd(0.0, -fadd(0.0, fdiv(fadd(0.0, fmul(r1, e)), t4)));
+        double a[DIM];
+        if (DX) {
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) a[d] = dx[i + d * ld];
+        }
+#pragma unroll
+        for (int d = DIM - 1; d >= 0; --d) {
+          const double u = xv[q][d];
+          const double r6 = fadd(fadd(0.0, fmul(c, u)), fmul(u, c));
+          if (DX) dx[i + d * ld] = fadd(a[d], r6);          // _d_x[_i0] += _r6
+          acc[d] = fadd(acc[d], -r6);                         // _d_p[_i0] += -_r6
         }
       }
-#pragma unroll
-      for (int k = 0; k < UF; ++k) {
-        const double pd = __ldg(p + d + k);
-        const double ua = fsub(xv[k].x, pd), ub = fsub(xv[k].y, pd);  // _t0 = x[i] - p[i]
-        stage2[(d + k) * 32 + lane] = make_double2(ua, ub);
-        ta = fadd(ta, fmul(ua, ua));                                   // t = t + _t1
-        tb = fadd(tb, fmul(ub, ub));
-      }
     }
-    for (; d < dim; ++d) {
-      const double2 xv = ld_stream2(x2 + (int64_t)d * ld2 + i2);
-      const double pd = __ldg(p + d);
-      const double ua = fsub(xv.x, pd), ub = fsub(xv.y, pd);
-      stage2[d * 32 + lane] = make_double2(ua, ub);
-      ta = fadd(ta, fmul(ua, ua));
-      tb = fadd(tb, fmul(ub, ub));
-    }
-    double ca, cb;
-    {
-      const double e = exp(fdiv(-ta, t4));
-      ca = fadd(0.0, -fadd(0.0, fdiv(fadd(0.0, fmul(r1, e)), t4)));
-      const double f = exp(fdiv(-tb, t4));
-      cb = fadd(0.0, -fadd(0.0, fdiv(fadd(0.0, fmul(r1, f)), t4)));
-    }
-    // reverse: _r6 per slot (each slot once, so the sweep order does not
-    // change bits); _d_x[_i0] += _r6 and the stage keeps -_r6 for _d_p
-    d = dim;
-    for (; d - U >= 0; d -= U) {
-      double2 a[U];
-      if (DX) {
-#pragma unroll
-        for (int k = 0; k < U; ++k) a[k] = dx2[(int64_t)(d - 1 - k) * ld2 + i2];
-#pragma unroll
-        for (int k = 0; k < U; ++k) {  // next dx rows; at the end, the next tile's x
-          const int dn = d - 1 - U - k;
-          if ((lane & 7) == 0) {
-            if (dn >= 0) prefetch_l2(dx2 + (int64_t)dn * ld2 + i2);
-            else if (more && -1 - dn < dim)
-              prefetch_l2(x2 + (int64_t)(-1 - dn) * ld2 + i2 + (int64_t)gridDim.x * 32);
-          }
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const int dd = d - 1 - k;
-        const double2 u = stage2[dd * 32 + lane];
-        const double ra = fadd(fadd(0.0, fmul(ca, u.x)), fmul(u.x, ca));
-        const double rb = fadd(fadd(0.0, fmul(cb, u.y)), fmul(u.y, cb));
-        if (DX) dx2[(int64_t)dd * ld2 + i2] = make_double2(fadd(a[k].x, ra), fadd(a[k].y, rb));
-        stage2[dd * 32 + lane] = make_double2(-ra, -rb);
-      }
-    }
-    for (; d > 0; --d) {
-      const int dd = d - 1;
-      const double2 u = stage2[dd * 32 + lane];
-      const double ra = fadd(fadd(0.0, fmul(ca, u.x)), fmul(u.x, ca));
-      const double rb = fadd(fadd(0.0, fmul(cb, u.y)), fmul(u.y, cb));
-      if (DX) {
-        const int64_t o = (int64_t)dd * ld2 + i2;
-        const double2 a = dx2[o];
-        dx2[o] = make_double2(fadd(a.x, ra), fadd(a.y, rb));
-      }
-      stage2[dd * 32 + lane] = make_double2(-ra, -rb);
-    }
-    if (!DX && more && (lane & 7) == 0) {
-      for (int k = 0; k < U && k < dim; ++k)  // the next tile's first rows
-        prefetch_l2(x2 + (int64_t)k * ld2 + i2 + (int64_t)gridDim.x * 32);
-    }
-    __syncwarp();  // every lane's -_r6 visible
-    // _d_p[d] += -_r6 of the tile's 64 points, lane l owning dims l + 32 j
-#pragma unroll
-    for (int j = 0; j < JMAX; ++j) {
-      const int dd = lane + 32 * j;
-      if (j * 32 < dim && dd < dim) {
-        const double* row = reinterpret_cast<const double*>(stage2 + (size_t)dd * 32);
-        double aj = acc[j];
-#pragma unroll 16
-        for (int s = 0; s < 64; ++s) aj = fadd(aj, row[(lane + s) & 63]);
-        acc[j] = aj;
-      }
-    }
-    __syncwarp();  // the stage is rewritten by the next tile
   }
 #pragma unroll
-  for (int j = 0; j < JMAX; ++j) {
-    const int dd = lane + 32 * j;
-    if (dd < dim) partials[(int64_t)blockIdx.x * dim + dd] = acc[j];
+  for (int d = 0; d < DIM; ++d) {
+    double v = acc[d];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = fadd(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (lane == 0) wsum[warp][d] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < DIM) {
+    double v = wsum[0][threadIdx.x];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) v = fadd(v, wsum[w][threadIdx.x]);
+    partials[(int64_t)blockIdx.x * DIM + threadIdx.x] = v;
+  }
+}
+
+template <bool DX>
+static void* shared_p_rows_fn(int dim) {
+  switch (dim) {
+#define ADCB_ROWS(D) \
+    case D: return (void*)gaussnd_shared_p_rows_kernel<D, (32 / D > 16 ? 16 : (32 / D < 2 ? 2 : 32 / D)), DX>;
+    ADCB_ROWS(1) ADCB_ROWS(2) ADCB_ROWS(3) ADCB_ROWS(4) ADCB_ROWS(5) ADCB_ROWS(6) ADCB_ROWS(7)
+    ADCB_ROWS(8) ADCB_ROWS(9) ADCB_ROWS(10) ADCB_ROWS(11) ADCB_ROWS(12) ADCB_ROWS(13)
+    ADCB_ROWS(14) ADCB_ROWS(15) ADCB_ROWS(16) ADCB_ROWS(17) ADCB_ROWS(18) ADCB_ROWS(19)
+    ADCB_ROWS(20) ADCB_ROWS(21) ADCB_ROWS(22) ADCB_ROWS(23) ADCB_ROWS(24)
+#undef ADCB_ROWS
+    default: return nullptr;
   }
 }
 
@@ -972,6 +965,20 @@ int launch_gaussnd_shared_p(int64_t n, int64_t dim, int64_t ld, const double* x,
   if (dim > (1 << 20)) return fail(ADC_E_ARG, "gaussnd: dim too large");
   double d_t9 = 0;
   d_t9 += (std::pow(2 * PI, -0.5) * std::pow(sigma, -0.5)) * 1.0;
+  // K2sr up to 24 dims (measured against the staged-tile forms, ms, dp only /
+  // with dx: 1.2e8 x 8 1.28 / 4.83 vs 4.48 / 8.39; 6e7 x 16 1.22 / 3.99 vs
+  // 2.50 / 6.78; 4e7 x 24 1.32 / 4.21 vs 2.35 / 5.74; at 32 dims its
+  // registers spill and the TMA form wins with dx, 4.81 vs 3.84)
+  if (dim <= kSharedPRowsMaxDim) {
+    const int64_t blocks = gaussnd_shared_p_blocks(n);
+    void* fn = dx ? shared_p_rows_fn<true>((int)dim) : shared_p_rows_fn<false>((int)dim);
+    void* args[] = {(void*)&x, (void*)&p, (void*)&dx, (void*)&n, (void*)&ld, (void*)&t4,
+                    (void*)&d_t9, (void*)&partials};
+    ADCB_CUDA(cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(256), args, 0, s));
+    gaussnd_shared_p_finish<<<1, 128, 0, s>>>(partials, blocks, (int)dim, dp);
+    ADCB_CUDA(cudaGetLastError());
+    return ADC_OK;
+  }
   // stage as many dims of u as fit next to dp's partials (<= 26 KB: 8 CTAs/SM)
   const size_t budget = 26 * 1024 + 1024;
   const size_t fixed = (size_t)dim * sizeof(double);
@@ -993,69 +1000,40 @@ int launch_gaussnd_shared_p(int64_t n, int64_t dim, int64_t ld, const double* x,
   // total per dim.
   const int64_t full = n / 32, rem = n % 32;
   const int64_t blocks = full > 0 ? gaussnd_shared_p_blocks(full * 32) : 0;
-  const size_t tma_smem = (size_t)dim * 64 * sizeof(double) + 32 * sizeof(double) +
+  // warps per staged tile of the TMA form by the dims (measured, ms, dp only
+  // 10M x 100: 2.03 / 1.50 / 1.51 / 1.73 with 1 / 2 / 4 / 8 warps; 5M x 200
+  // 2.99 / 1.99 / 1.52 / 1.53; with dx 10M x 100 7.48 / 5.10 / 4.75 with
+  // 2 / 4 / 8, 27M x 37 5.50 / 4.72 / 6.93, 5M x 200 12.5 / 7.64 / 5.14).
+  // K2s sums in the same chunks wherever the TMA form could run (dim <= 256).
+  const int nw = dx ? (dim >= 64 ? 8 : 4) : (dim >= 128 ? 4 : 2);
+  const int dq = dim <= 256 ? (int)((dim + nw - 1) / nw) : (int)dim;
+  const size_t tma_smem = (size_t)dim * 64 * sizeof(double) + 64 * 8 * sizeof(double) +
                           2 * sizeof(uint64_t);
-  // The TMA kernel serves the dp-only form (x streamed by 2-D tensor loads,
-  // 4.5 TB/s at 10M x 100); with private dx slots the per-point RMW wants
-  // more warps in flight than its stage buffers allow, so K2s<32, 8> runs.
-  const bool tma = dx == nullptr && ld % 2 == 0 && ((uintptr_t)x & 15) == 0 && dim <= 256 &&
+  // The TMA form: x streamed by 2-D tensor loads, NW warps per staged tile,
+  // dx (optional) per point.  Other layouts run K2s.
+  const bool tma = ld % 2 == 0 && ((uintptr_t)x & 15) == 0 && dim <= 256 &&
                    tma_smem <= 200 * 1024;
-  // K2sv (double2 rows, 64-point tiles) when the layout allows it: the full
-  // 64-point tiles over kSharedPVecBlocks CTAs, the < 64 remaining points as
-  // one more block of partials (K2s), then the fixed-order total.
-  const bool vec = dx != nullptr && ld % 2 == 0 && ((((uintptr_t)x) | ((uintptr_t)dx)) & 15) == 0 && dim <= 128 &&
-                   n >= 64;
-  if (vec) {
-    const int64_t full64 = n / 64, rem64 = n % 64;
-    const int64_t vblocks = std::min<int64_t>(full64, kSharedPVecBlocks);
-    const size_t vsmem = (size_t)dim * 512;
-    // U = 16 rows in flight: measured best of 16 / 24 / 32; below 16 dims the
-    // batch follows the dims (U = 16 would never batch: one dependent row at
-    // a time).  Same bits for any U (t in row order, each slot once).
-    auto kv = dim >= 16 ? (dx != nullptr ? gaussnd_shared_p_vec2_kernel<16, 16, 4, true>
-                                         : gaussnd_shared_p_vec2_kernel<16, 16, 4, false>)
-            : dim >= 8  ? (dx != nullptr ? gaussnd_shared_p_vec2_kernel<8, 8, 4, true>
-                                         : gaussnd_shared_p_vec2_kernel<8, 8, 4, false>)
-            : dim >= 4  ? (dx != nullptr ? gaussnd_shared_p_vec2_kernel<4, 4, 4, true>
-                                         : gaussnd_shared_p_vec2_kernel<4, 4, 4, false>)
-                        : (dx != nullptr ? gaussnd_shared_p_vec2_kernel<2, 2, 4, true>
-                                         : gaussnd_shared_p_vec2_kernel<2, 2, 4, false>);
-    if (vsmem > 48 * 1024)
-      ADCB_CUDA(cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsmem));
-    ADCB_CUDA(cudaFuncSetAttribute(kv, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                   cudaSharedmemCarveoutMaxShared));
-    kv<<<(unsigned)vblocks, 32, vsmem, s>>>(x, p, dx, full64, (int)dim, ld, t4, d_t9, partials);
-    ADCB_CUDA(cudaGetLastError());
-    if (rem64 != 0) {
-      const int64_t off = full64 * 64;
-      k<<<1, 32, smem, s>>>(x + off, p, dx ? dx + off : nullptr, rem64, (int)dim, ld, t4, d_t9,
-                            dstage, partials + vblocks * dim);
-      ADCB_CUDA(cudaGetLastError());
-    }
-    gaussnd_shared_p_finish<<<(unsigned)((dim + 127) / 128), 128, 0, s>>>(
-        partials, vblocks + (rem64 != 0 ? 1 : 0), (int)dim, dp);
-    ADCB_CUDA(cudaGetLastError());
-    return ADC_OK;
-  }
   if (full > 0) {
     CUtensorMap tmap;
     if (tma && make_rows_tmap(&tmap, x, full * 32, dim, ld) == ADC_OK) {
-      auto kt = dim <= 128 ? gaussnd_shared_p_tma_kernel<8, 4> : gaussnd_shared_p_tma_kernel<8, 8>;
+      auto kt = nw == 8 ? gaussnd_shared_p_tma_kernel<8, 1, 8>
+              : nw == 4 ? gaussnd_shared_p_tma_kernel<8, 2, 4>
+                        : gaussnd_shared_p_tma_kernel<8, 2, 2>;
       if (tma_smem > 48 * 1024)
         ADCB_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)tma_smem));
-      kt<<<(unsigned)blocks, 32, tma_smem, s>>>(tmap, x, p, dx, full, (int)dim, ld, t4, d_t9,
+      kt<<<(unsigned)blocks, 32 * nw, tma_smem, s>>>(tmap, x, p, dx, full, (int)dim, ld, t4, d_t9,
                                                 partials);
     } else {
       k<<<(unsigned)blocks, 32, smem, s>>>(x, p, dx, full * 32, (int)dim, ld, t4, d_t9, dstage,
-                                           partials);
+                                           partials, dq);
     }
     ADCB_CUDA(cudaGetLastError());
   }
   if (rem != 0) {
     const int64_t off = full * 32;
     k<<<1, 32, smem, s>>>(x + off, p, dx ? dx + off : nullptr, rem, (int)dim, ld, t4, d_t9, dstage,
-                          partials + blocks * dim);
+                          partials + blocks * dim, dq);
     ADCB_CUDA(cudaGetLastError());
   }
   gaussnd_shared_p_finish<<<(unsigned)((dim + 127) / 128), 128, 0, s>>>(

@@ -666,13 +666,16 @@ def test_gaussnd_shared_p_large_and_refusal(restate):
 
 
 @pytest.mark.parametrize("dim,n", [(100, 200_006), (37, 64 * 700), (128, 5_000), (2, 10_001),
-                                   (3, 6_400), (5, 4_099), (12, 3_000)])
+                                   (3, 6_400), (5, 4_099), (12, 3_000), (24, 7_001), (25, 3_333),
+                                   (256, 1_100), (257, 650)])
 def test_gaussnd_shared_p_with_dx_paths(restate, dim, n):
-    """With private dx slots: the aligned layout runs K2sv (double2 rows,
-    64-point tiles, ragged tail through K2s), an odd-offset view of the same
-    points runs K2s.  dx per point within 1e-12 of the restatement in both;
-    dp within 1e-12 * sum|terms| of the compensated total in both (the two
-    paths sum in different fixed orders); each path bitwise repeatable."""
+    """With private dx slots: up to 24 dims K2sr (a thread per point, any
+    layout); above, the aligned layout runs the TMA form (2-D tensor loads of
+    32-point tiles, 4 or 8 warps per tile, ragged tail through K2s, dim <=
+    256) and an odd-offset view of the same points runs K2s.  dx per point
+    within 1e-12 of the restatement in both; dp within 1e-12 * sum|terms| of
+    the compensated total in both (the paths sum in different fixed orders);
+    each path bitwise repeatable."""
     rng = np.random.Generator(np.random.PCG64(dim))
     p = rng.uniform(-1, 1, dim)
     x = p[:, None] + 0.1 * rng.standard_normal((dim, n))
@@ -683,6 +686,7 @@ def test_gaussnd_shared_p_with_dx_paths(restate, dim, n):
     tot, ab = restate.gaussnd_shared_p_dp_compensated(np.ascontiguousarray(x), p, 1.3)
     o = adc.LaunchOptions(unsafe=True)
     wide = np.zeros((dim, n + 1))
+    per_offset = []
     for offset in (0, 1):
         X = t(np.ascontiguousarray(x)) if offset == 0 else t(wide)[:, 1:]
         if offset:
@@ -699,6 +703,10 @@ def test_gaussnd_shared_p_with_dx_paths(restate, dim, n):
         assert gdx.tobytes() == gdx2.tobytes() and gdp.tobytes() == gdp2.tobytes()
         assert acc_err(gdx, rdx, dx0).max() <= REL, offset
         assert np.all(np.abs(gdp - (dp0 + tot)) <= 1e-12 * (ab + np.abs(dp0))), offset
+        per_offset.append(gdx)
+    # a point's dx bits do not depend on which form its layout selected (K2s
+    # sums the forward in the TMA form's warp chunks)
+    assert per_offset[0].tobytes() == per_offset[1].tobytes()
 
 
 def test_gaussnd_strided_views(restate):
