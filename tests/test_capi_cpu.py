@@ -21,7 +21,7 @@ HEADER = os.path.join(ROOT, "include", "adc_cuda.h")
 def declared_symbols():
     text = open(HEADER).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(adc_(?:cuda|chi2|fit|nccl|comm|jit)_\w+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(adc_(?:cuda|chi2|fit|nccl|comm|jit|histogram)_\w+)\s*\(", text)))
 
 
 def test_every_declared_symbol_is_exported_and_bound():
