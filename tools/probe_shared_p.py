@@ -1,4 +1,4 @@
-"""Shared-mean gaussnd (K2s / K2sv / TMA) throughput at 10M points x 100 dims:
+"""Shared-mean gaussnd (K2sr / TMA form / K2s) throughput at 10M points x 100 dims:
 per-launch CUDA events, median and min of `reps` launches."""
 import os
 import sys
