@@ -846,8 +846,24 @@ def bench_jit(local, npts=100_000_000, steps=10, warm=3):
         evs = [event_time(step, stream) for _ in range(steps)]
         torch.cuda.synchronize()
         ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in evs)
+        roof = hbm_roofline(bytes_pt * npts, ms, "jit_" + kern)
+        slots = traffic_for("jit_k_looped_fp64_warp_instr_per_pt") if kern == "k_looped" else None
+        if slots:
+            # k_looped is bound by the FP64 pipe, not HBM (ncu: pipe active 91%,
+            # HBM 60%): 10 data-dependent branches per point leave part of each
+            # warp's lanes predicated off, so the pipe's work is counted in
+            # lane slots (warp instructions x 32), not executed thread-instructions
+            pk = fp64_peak(local)
+            lanes = slots * 32 * npts / (ms * 1e-3) / 1e12
+            roof = {"bound": "fp64", "achieved": lanes, "peak": pk["tinstr_s"],
+                    "unit": "T FP64 lane-slots/s", "frac": lanes / pk["tinstr_s"],
+                    "hbm_frac": roof["frac"], "traffic": roof["traffic"],
+                    "work_per_point": f"{slots:g} FP64 warp instructions x 32 lanes; "
+                                      f"{traffic_for('jit_k_looped_fp64_thread_instr_per_pt'):g} "
+                                      "executed thread-instructions (ncu, profiles/traffic.json)",
+                    "kernel_ms": ms, "peak_source": pk["source"]}
         rec[kern] = {"ms_per_launch": ms, "static_tape": mod.static_source(ints) is not None,
-                     "roofline": hbm_roofline(bytes_pt * npts, ms, "jit_" + kern)}
+                     "roofline": roof}
     return rec
 
 

@@ -6,7 +6,7 @@
 mkdir -p gpurun_out
 # torch must not pool allocations, or memcheck only sees its 2 MB segments
 export PYTORCH_NO_CUDA_MEMORY_CACHING=1
-SEL="golden or listing1_cases or domain_error or shared_p_golden or multi_bitwise or numeric_provider_probe or accumulates_twice or sample_histogram_zero or compute_shared_forced or chi2_gradient_batch or corpus_gradient or high_counts"
+SEL="claimed_spans_match or claimed_spans_in_cuda_graph or shared_p_with_dx or golden or listing1_cases or domain_error or shared_p_golden or multi_bitwise or numeric_provider_probe or accumulates_twice or sample_histogram_zero or compute_shared_forced or chi2_gradient_batch or corpus_gradient or high_counts"
 # racecheck / synccheck cannot follow the fit's device-side loop (a CUDA graph
 # WHILE node): they run the kernels without the device-loop fits (the fits'
 # kernels are the same chi2 / multi kernels the other cases launch)
