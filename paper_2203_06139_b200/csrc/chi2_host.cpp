@@ -186,7 +186,7 @@ struct adc_chi2_plan {
   int64_t* empty_idx = nullptr;
   int64_t empty_cap = 0;
   int64_t* empty_off = nullptr;  // [local chunks + 1]
-  int64_t* empty_cnt = nullptr;  // [local chunks]
+  int64_t* empty_cnt = nullptr;  // [local chunks x kEmptySections + 1]: counts, then bases
   double* zws = nullptr;         // [kMultiMax][maxc][kEmptySegs][1 + kMaxNp]
 };
 
@@ -318,19 +318,24 @@ int ensure_lin(adc_chi2_plan* P, cudaStream_t s) {
   // the empty-bin lists (ascending per chunk) for the passes' side pass
   if (P->empty_off == nullptr) {
     ADCB_CUDA(cudaMalloc(&P->empty_off, (size_t)(nrec + 1) * sizeof(int64_t)));
-    ADCB_CUDA(cudaMalloc(&P->empty_cnt, (size_t)nrec * sizeof(int64_t)));
+    ADCB_CUDA(cudaMalloc(&P->empty_cnt, ((size_t)nrec * kEmptySections + 1) * sizeof(int64_t)));
     ADCB_CUDA(cudaMalloc(&P->zws, (size_t)kMultiMax * P->maxc * kEmptySegs * (1 + kMaxNp) *
                                       sizeof(double)));
   }
   const int64_t nloc = local_chunks(P);
+  // per (chunk, section) counts -> their exclusive prefix (the fill kernel's
+  // bases, uploaded into empty_cnt) and the per-chunk offsets (empty_off)
   std::vector<int64_t> off((size_t)nloc + 1, 0);
+  std::vector<int64_t> sec((size_t)nloc * kEmptySections + 1, 0);
   if (nloc > 0) {
     if (int rc = chi2_empty_count_enqueue(make_pass(P), P->L.chunk_tiles, P->empty_cnt, s))
       return rc;
-    ADCB_CUDA(cudaMemcpyAsync(off.data() + 1, P->empty_cnt, (size_t)nloc * sizeof(int64_t),
+    ADCB_CUDA(cudaMemcpyAsync(sec.data() + 1, P->empty_cnt,
+                              (size_t)nloc * kEmptySections * sizeof(int64_t),
                               cudaMemcpyDeviceToHost, s));
     ADCB_CUDA(cudaStreamSynchronize(s));
-    for (int64_t c = 0; c < nloc; ++c) off[c + 1] += off[c];
+    for (size_t k = 1; k < sec.size(); ++k) sec[k] += sec[k - 1];
+    for (int64_t c = 0; c <= nloc; ++c) off[c] = sec[(size_t)c * kEmptySections];
   }
   const int64_t total = std::max<int64_t>(1, off[nloc]);
   if (total > P->empty_cap) {  // (a refreshed histogram with more empty bins)
@@ -347,10 +352,13 @@ int ensure_lin(adc_chi2_plan* P, cudaStream_t s) {
   }
   ADCB_CUDA(cudaMemcpyAsync(P->empty_off, off.data(), (size_t)(nloc + 1) * sizeof(int64_t),
                             cudaMemcpyHostToDevice, s));
-  if (nloc > 0)
-    if (int rc = chi2_empty_fill_enqueue(make_pass(P), P->L.chunk_tiles, P->empty_off,
+  if (nloc > 0) {
+    ADCB_CUDA(cudaMemcpyAsync(P->empty_cnt, sec.data(), sec.size() * sizeof(int64_t),
+                              cudaMemcpyHostToDevice, s));
+    if (int rc = chi2_empty_fill_enqueue(make_pass(P), P->L.chunk_tiles, P->empty_cnt,
                                          P->empty_idx, s))
       return rc;
+  }
   ADCB_CUDA(cudaStreamSynchronize(s));
   // counts per non-empty bin: C0 over this rank's chunks / non-empty bins
   if (!sharded(P) && nloc > 0) {

@@ -14,6 +14,7 @@ constexpr int kMaxNp = 24;
 constexpr int kQDoubles = 8 * kMaxNp;  // QDev (q, 1/q) + QNum (numeric probes), chi2.cu
 constexpr int kMultiMax = 64;  // line-search candidates (or gradients) per multi pass
 constexpr int kEmptySegs = 8;  // segments of each chunk's empty-bin list (side pass CTAs)
+constexpr int kEmptySections = 64;  // CTAs building each chunk's list (once per plan)
 
 struct Chi2Pass {
   const double* counts;   // full histogram, device (read by the once-per-plan passes)

@@ -1,6 +1,6 @@
 # Per-kernel device times of the chi2 gradient pass (ncu launch list).
 O=gpurun_out; mkdir -p $O
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_chi2.csv python tools/probe_chi2.py 100000000 3 > /dev/null 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_chi2.csv python tools/probe_chi2.py ${CHI2_BINS:-100000000} 3 > /dev/null 2>&1
 python - <<'PY'
 import csv, collections
 rows = list(csv.reader(open("gpurun_out/launches_chi2.csv")))
