@@ -56,39 +56,64 @@ int sm_count() {
 }
 
 // The claim ring: kClaimSlots pairs per device, handed out round-robin, so
-// concurrent launches (other streams, other host threads) use distinct pairs.
+// concurrent eager launches (other streams, other host threads) use distinct
+// pairs.  A launch being captured into a CUDA graph keeps its pair for the
+// graph's lifetime, so it takes one from a separate arena that is never
+// handed out again (16 bytes per captured launch, in blocks of kClaimSlots):
+// a ring pair could otherwise be reused by an eager launch running beside a
+// replay of the graph.
 static constexpr uint32_t kClaimSlots = 4096;
 static std::mutex g_claim_mu;
 static unsigned long long* g_claim[64] = {nullptr};
 static std::atomic<uint32_t> g_claim_next[64];
+static std::vector<unsigned long long*> g_claim_arena[64];
+static uint32_t g_claim_arena_used[64] = {0};
 
-unsigned long long* claim_slot() {
+// kClaimSlots zeroed pairs; relaxed capture mode for this thread (the
+// allocation may happen while a stream is being captured), the zero fill on
+// a private non-blocking stream.
+static unsigned long long* claim_block() {
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  unsigned long long* ptr = nullptr;
+  cudaStream_t st = nullptr;
+  const size_t bytes = kClaimSlots * 2 * sizeof(unsigned long long);
+  bool ok = cudaMalloc(&ptr, bytes) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaMemsetAsync(ptr, 0, bytes, st) == cudaSuccess &&
+            cudaStreamSynchronize(st) == cudaSuccess;
+  if (st) cudaStreamDestroy(st);
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  if (!ok) {
+    cudaGetLastError();
+    if (ptr) cudaFree(ptr);
+    return nullptr;
+  }
+  return ptr;
+}
+
+unsigned long long* claim_slot(cudaStream_t s) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  {
-    std::lock_guard<std::mutex> lk(g_claim_mu);
-    if (!g_claim[dev]) {
-      // relaxed capture mode for this thread: the one-time allocation may
-      // happen while some stream is being captured into a graph; the zero
-      // fill runs on a private non-blocking stream
-      cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
-      cudaThreadExchangeStreamCaptureMode(&mode);
-      unsigned long long* ptr = nullptr;
-      cudaStream_t st = nullptr;
-      const size_t bytes = kClaimSlots * 2 * sizeof(unsigned long long);
-      bool ok = cudaMalloc(&ptr, bytes) == cudaSuccess &&
-                cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
-                cudaMemsetAsync(ptr, 0, bytes, st) == cudaSuccess &&
-                cudaStreamSynchronize(st) == cudaSuccess;
-      if (st) cudaStreamDestroy(st);
-      cudaThreadExchangeStreamCaptureMode(&mode);
-      if (!ok) {
-        cudaGetLastError();
-        if (ptr) cudaFree(ptr);
-        return nullptr;
-      }
-      g_claim[dev] = ptr;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(g_claim_mu);
+  if (cs == cudaStreamCaptureStatusActive) {
+    auto& arena = g_claim_arena[dev];
+    if (arena.empty() || g_claim_arena_used[dev] == kClaimSlots) {
+      unsigned long long* blk = claim_block();
+      if (blk == nullptr) return nullptr;
+      arena.push_back(blk);
+      g_claim_arena_used[dev] = 0;
     }
+    return arena.back() + 2 * (size_t)g_claim_arena_used[dev]++;
+  }
+  if (!g_claim[dev]) {
+    g_claim[dev] = claim_block();
+    if (!g_claim[dev]) return nullptr;
   }
   const uint32_t k = g_claim_next[dev].fetch_add(1, std::memory_order_relaxed) % kClaimSlots;
   return g_claim[dev] + 2 * (size_t)k;

@@ -117,14 +117,15 @@ cudaError_t ws_alloc(void** ptr, size_t bytes, cudaStream_t s);
 bool device_present();
 
 // Dynamic span claiming (K2).  A launch takes a {next span, CTAs done} pair
-// from a per-device ring (zero between launches); each CTA claims spans in
-// order with one atomic, so the spans in flight at any moment are neighbours
-// and the row lines they share are read once, while the data is in L2.  The
-// last CTA out resets the pair, so a launch needs no memset and replays in a
-// CUDA graph.  nullptr (the ring could not be allocated, e.g. first use
-// inside a stream capture) selects the static grid-stride schedule: same
+// (zero between launches); each CTA claims spans in order with one atomic,
+// so the spans in flight at any moment are neighbours and the row lines they
+// share are read once, while the data is in L2.  The last CTA out resets the
+// pair, so a launch needs no memset and replays in a CUDA graph.  Eager
+// launches take pairs from a per-device ring; a launch on a capturing stream
+// gets a pair of its own for the graph's lifetime (capi.cpp).  nullptr (no
+// memory for the pairs) selects the static grid-stride schedule: same
 // per-point arithmetic, same bits.
-unsigned long long* claim_slot();
+unsigned long long* claim_slot(cudaStream_t s);
 
 __device__ __forceinline__ int64_t claim_next(unsigned long long* c) {
   return (int64_t)atomicAdd(c, 1ull);

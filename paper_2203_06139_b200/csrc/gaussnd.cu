@@ -420,7 +420,7 @@ static int launch_tile(const NdConfig& c, int64_t n, int dim, int64_t ld, const 
   if (occ < 1) return fail(ADC_E_LAUNCH, "gaussnd: tile configuration does not fit an SM");
   const int64_t ntiles = (n + 31) / 32;
   int64_t blocks = std::min<int64_t>((ntiles + TPC - 1) / TPC, (int64_t)occ * sm_count());
-  unsigned long long* claim = dyn && blocks < (ntiles + TPC - 1) / TPC ? claim_slot() : nullptr;
+  unsigned long long* claim = dyn && blocks < (ntiles + TPC - 1) / TPC ? claim_slot(s) : nullptr;
   k<<<(unsigned)blocks, W * 32 * TPC, smem, s>>>(x, p, dx, dp, n, dim, ld, t4, r1, c.dpw, c.dstage,
                                                   claim);
   ADCB_CUDA(cudaGetLastError());
@@ -487,7 +487,7 @@ static int launch_gaussnd_v(int64_t n, int64_t dim, int64_t ld, const double* x,
       int occ = 0;
       ADCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 32, smem));
       const int64_t blocks = std::min<int64_t>(ntiles, (int64_t)std::max(1, occ) * sm_count());
-      unsigned long long* claim = dyn && blocks < ntiles ? claim_slot() : nullptr;
+      unsigned long long* claim = dyn && blocks < ntiles ? claim_slot(s) : nullptr;
       k<<<(unsigned)blocks, 32, smem, s>>>(x, p, dx, dp, ntiles, (int)dim, ld, t4, d_t9, dstage,
                                            claim);
       ADCB_CUDA(cudaGetLastError());
