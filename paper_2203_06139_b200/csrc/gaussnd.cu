@@ -29,6 +29,48 @@
 
 namespace adcb {
 
+// Row batches of K for the last rows of a sweep: the remainder after the
+// U-row batches goes through batches of 8, 4, 2, 1 (all loads of a batch in
+// flight together), not row at a time: a remainder of 12 rows was 12 memory
+// round trips (dim 28 at 11.0 ms vs 6.9 with U = 8).  Same order, same bits.
+template <int K>
+__device__ __forceinline__ void fwd_rows(const double* xi, const double* pi, int64_t ld, int d,
+                                         int d0, int dstage, double* my_stage, double& t) {
+  double xv[K], pv[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    xv[k] = __ldg(xi + (int64_t)(d + k) * ld);
+    pv[k] = __ldg(pi + (int64_t)(d + k) * ld);
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const double u = fsub(xv[k], pv[k]);  // _t0 = x[i] - p[i]
+    if (d + k - d0 < dstage) my_stage[(d + k - d0) * 32] = u;
+    t = fadd(t, fmul(u, u));              // _t1 = _t0*_t0; t = t + _t1
+  }
+}
+
+// Staged rows d - K .. d - 1 (descending) of the reverse sweep.
+template <int K>
+__device__ __forceinline__ void rev_rows(double* dxi, double* dpi, int64_t ld, int d, int d0,
+                                         const double* my_stage, double c) {
+  double a[K], b[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int64_t o = (int64_t)(d - 1 - k) * ld;
+    a[k] = dxi[o];
+    b[k] = dpi[o];
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const double u = my_stage[(d - 1 - k - d0) * 32];
+    const double r6 = fadd(fadd(0.0, fmul(c, u)), fmul(u, c));
+    const int64_t o = (int64_t)(d - 1 - k) * ld;
+    dxi[o] = fadd(a[k], r6);
+    dpi[o] = fadd(b[k], -r6);
+  }
+}
+
 // x and p rows are read through L1 (ld.global.nc, allocating): at rows that
 // are not 128 B aligned, the line two neighbouring warps of a CTA share is
 // then one L2 request, not two.  Measured against no-allocate loads (ms):
@@ -120,11 +162,10 @@ __global__ void __launch_bounds__(W * 32 * TPC) gaussnd_tile_kernel(
           t = fadd(t, fmul(u, u));              // _t1 = _t0*_t0; t = t + _t1
         }
       }
-      for (; d < d1; ++d) {
-        const double u = fsub(__ldg(xi + (int64_t)d * ld), __ldg(pi + (int64_t)d * ld));
-        if (d - d0 < dstage) my_stage[(d - d0) * 32] = u;
-        t = fadd(t, fmul(u, u));
-      }
+      if (U > 8 && d + 8 <= d1) { fwd_rows<8>(xi, pi, ld, d, d0, dstage, my_stage, t); d += 8; }
+      if (U > 4 && d + 4 <= d1) { fwd_rows<4>(xi, pi, ld, d, d0, dstage, my_stage, t); d += 4; }
+      if (U > 2 && d + 2 <= d1) { fwd_rows<2>(xi, pi, ld, d, d0, dstage, my_stage, t); d += 2; }
+      if (d < d1) { fwd_rows<1>(xi, pi, ld, d, d0, dstage, my_stage, t); d += 1; }
     }
     if (W > 1) {
       tpart[warp * 32 + lane] = t;
@@ -219,13 +260,10 @@ __global__ void __launch_bounds__(W * 32 * TPC) gaussnd_tile_kernel(
           dpi[o] = fadd(b[k], -r6);
         }
       }
-      for (; d > d0; --d) {
-        const int64_t o = (int64_t)(d - 1) * ld;
-        const double u = my_stage[(d - 1 - d0) * 32];
-        const double r6 = fadd(fadd(0.0, fmul(c, u)), fmul(u, c));
-        dxi[o] = fadd(dxi[o], r6);
-        dpi[o] = fadd(dpi[o], -r6);
-      }
+      if (U > 8 && d - 8 >= d0) { rev_rows<8>(dxi, dpi, ld, d, d0, my_stage, c); d -= 8; }
+      if (U > 4 && d - 4 >= d0) { rev_rows<4>(dxi, dpi, ld, d, d0, my_stage, c); d -= 4; }
+      if (U > 2 && d - 2 >= d0) { rev_rows<2>(dxi, dpi, ld, d, d0, my_stage, c); d -= 2; }
+      if (d > d0) { rev_rows<1>(dxi, dpi, ld, d, d0, my_stage, c); d -= 1; }
     }
     if (W > 1) __syncthreads();  // tpart is rewritten by the next tile
     if (claim) {
@@ -509,7 +547,11 @@ static int launch_gaussnd_v(int64_t n, int64_t dim, int64_t ld, const double* x,
     // (U = 24 / 32) spill and were slower.
     const bool fits = (size_t)8 * 32 * 8 + (size_t)8 * c.dstage * 256 <= 227 * 1024;
     if (variant == 0 && fits) {
-      if (dim >= 16) return launch_tile<1, 16, 1, 8>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s, dyn);
+      // U = 16 from 48 dims, 8 below (measured with the batched remainders,
+      // ms, aligned / odd n: dim 20 6.65 / 6.83 vs 7.24 / 7.89 with U = 16,
+      // dim 28 7.00 / 6.97 vs 7.16 / 7.95; dim 100 7.01 / 8.32 vs 7.26 / 8.57
+      // with U = 8)
+      if (dim >= 48) return launch_tile<1, 16, 1, 8>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s, dyn);
       if (dim >= 8) return launch_tile<1, 8, 1, 8>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s, dyn);
       if (dim >= 4) return launch_tile<1, 4, 1, 8>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s, dyn);
       if (dim >= 2) return launch_tile<1, 2, 1, 8>(c, n, di, ld, x, p, dx, dp, t4, d_t9, s, dyn);
