@@ -24,6 +24,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -642,11 +644,26 @@ __global__ void __launch_bounds__(32) gaussnd_shared_p_kernel(
           add(u);
         }
       }
-      for (; d < dim; ++d) {
-        const double u = fsub(ld_stream(xi + (int64_t)d * ld), __ldg(p + d));
-        if (d < dstage) stage[d * 32 + lane] = u;
-        add(u);
-      }
+      // the remainder in batches of 16, 8, 4, 2, 1 (row at a time: a round
+      // trip each)
+      auto frows = [&](auto kc) {
+        constexpr int K = decltype(kc)::value;
+        double xv[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) xv[k] = ld_stream(xi + (int64_t)(d + k) * ld);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const double u = fsub(xv[k], __ldg(p + d + k));
+          if (d + k < dstage) stage[(d + k) * 32 + lane] = u;
+          add(u);
+        }
+        d += K;
+      };
+      if (U > 16 && d + 16 <= dim) frows(std::integral_constant<int, 16>{});
+      if (U > 8 && d + 8 <= dim) frows(std::integral_constant<int, 8>{});
+      if (U > 4 && d + 4 <= dim) frows(std::integral_constant<int, 4>{});
+      if (U > 2 && d + 2 <= dim) frows(std::integral_constant<int, 2>{});
+      if (d < dim) frows(std::integral_constant<int, 1>{});
       if (left != dq) t = first ? tc : fadd(t, tc);  // the last, partial chunk
     }
     const double tt = fdiv(-t, t4);
@@ -655,12 +672,13 @@ __global__ void __launch_bounds__(32) gaussnd_shared_p_kernel(
     const double r3 = fadd(0.0, fdiv(r2, t4));
     const double c = fadd(0.0, -r3);
     // ---- reverse (the generated loop order, d descending), V dims at a time
-    // so V shuffle trees and dx read-modify-writes overlap
-    int d = dim - 1;
-    for (; d - (V - 1) >= 0; d -= V) {
-      double v[V], a[V];
+    // so V shuffle trees and dx read-modify-writes overlap; the remainder in
+    // batches of 4, 2, 1
+    auto rrows = [&](auto kc, int d) {
+      constexpr int K = decltype(kc)::value;
+      double v[K], a[K];
 #pragma unroll
-      for (int k = 0; k < V; ++k) {
+      for (int k = 0; k < K; ++k) {
         const int dd = d - k;
         v[k] = 0.0;
         if (valid && dx != nullptr) a[k] = dx[i + (int64_t)dd * ld];
@@ -669,7 +687,7 @@ __global__ void __launch_bounds__(32) gaussnd_shared_p_kernel(
         if (inext < n) prefetch_l2(x + inext + (int64_t)(dim - 1 - dd) * ld);
       }
 #pragma unroll
-      for (int k = 0; k < V; ++k) {
+      for (int k = 0; k < K; ++k) {
         const int dd = d - k;
         if (valid) {
           const double u = dd < dstage ? stage[dd * 32 + lane]
@@ -682,29 +700,18 @@ __global__ void __launch_bounds__(32) gaussnd_shared_p_kernel(
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
 #pragma unroll
-        for (int k = 0; k < V; ++k) v[k] += __shfl_down_sync(0xffffffffu, v[k], off);
+        for (int k = 0; k < K; ++k) v[k] += __shfl_down_sync(0xffffffffu, v[k], off);
       }
       if (lane == 0) {
 #pragma unroll
-        for (int k = 0; k < V; ++k) dpart[d - k] = fadd(dpart[d - k], v[k]);
+        for (int k = 0; k < K; ++k) dpart[d - k] = fadd(dpart[d - k], v[k]);
       }
-    }
-    for (; d >= 0; --d) {
-      double v = 0.0;
-      if (valid) {
-        const double u = d < dstage ? stage[d * 32 + lane]
-                                    : fsub(ld_stream(xi + (int64_t)d * ld), __ldg(p + d));
-        const double r6 = fadd(fadd(0.0, fmul(c, u)), fmul(u, c));
-        if (dx != nullptr) {
-          double* a = dx + i + (int64_t)d * ld;
-          *a = fadd(*a, r6);
-        }
-        v = -r6;
-      }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
-      if (lane == 0) dpart[d] = fadd(dpart[d], v);
-    }
+    };
+    int d = dim - 1;
+    for (; d - (V - 1) >= 0; d -= V) rrows(std::integral_constant<int, V>{}, d);
+    if (V > 4 && d - 3 >= 0) { rrows(std::integral_constant<int, 4>{}, d); d -= 4; }
+    if (V > 2 && d - 1 >= 0) { rrows(std::integral_constant<int, 2>{}, d); d -= 2; }
+    if (d >= 0) rrows(std::integral_constant<int, 1>{}, d);
     __syncwarp();
   }
   __syncwarp();
@@ -720,7 +727,16 @@ __global__ void __launch_bounds__(32) gaussnd_shared_p_kernel(
 // rotated point order (l + s) % 32 (bank-conflict free), into registers — no
 // cross-lane reductions per element.  dx (optional) stays per point.  Full
 // 32-point tiles only; dim <= 32 * JMAX.
-template <int V, int JMAX, int NW>
+// ASYNC: the same kernel for layouts a tensor map cannot describe (odd ld,
+// x not 16-byte aligned): each thread copies its rows' elements into the
+// stage with 8-byte cp.async (LDGSTS), one commit group per tile, double
+// buffered like the TMA form.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+
+template <int V, int JMAX, int NW, bool ASYNC = false>
 __global__ void __launch_bounds__(32 * NW) gaussnd_shared_p_tma_kernel(
     const __grid_constant__ CUtensorMap tmap, const double* __restrict__ x,
     const double* __restrict__ p, double* __restrict__ dx, int64_t ntiles, int dim, int64_t ld,
@@ -747,8 +763,19 @@ __global__ void __launch_bounds__(32 * NW) gaussnd_shared_p_tma_kernel(
   __syncthreads();
   const uint32_t tile_bytes = (uint32_t)dim * 256u;
   // one 2-D TMA load per tile: box {32 points, dim rows} -> buf[dim][32]
+  // (ASYNC: every thread's 8-byte copies, one commit group per call, empty
+  // past the last tile so the wait below always counts the same groups)
   auto issue = [&](int64_t tile, int b) {
     double* buf = b ? buf1 : buf0;
+    if (ASYNC) {
+      if (tile < ntiles) {
+        const double* src = x + tile * 32 + lane;
+        for (int r = warp; r < dim; r += NW) cp_async8(buf + r * 32 + lane, src + (int64_t)r * ld);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      return;
+    }
+    if (tile >= ntiles) return;
     if (threadIdx.x == 0) {
       mbar_arrive_expect_tx(&bar[b], tile_bytes);
       asm volatile(
@@ -772,13 +799,18 @@ __global__ void __launch_bounds__(32 * NW) gaussnd_shared_p_tma_kernel(
   double* my_c = cbuf + warp * 32;
   uint32_t phase[2] = {0u, 0u};
   int64_t tile = blockIdx.x;
-  if (tile < ntiles) issue(tile, 0);
-  if (tile + gridDim.x < ntiles) issue(tile + gridDim.x, 1);
+  issue(tile, 0);
+  issue(tile + gridDim.x, 1);
   for (int k = 0; tile < ntiles; tile += gridDim.x, ++k) {
     const int b = k & 1;
     double* buf = b ? buf1 : buf0;
-    mbar_wait(&bar[b], phase[b]);
-    phase[b] ^= 1u;
+    if (ASYNC) {
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // this tile's group
+      __syncthreads();                                       // every thread's copies
+    } else {
+      mbar_wait(&bar[b], phase[b]);
+      phase[b] ^= 1u;
+    }
     const int64_t i = tile * 32 + lane;
     double t = 0.0;
     for (int d = f0; d < f1; ++d) {
@@ -799,23 +831,25 @@ __global__ void __launch_bounds__(32 * NW) gaussnd_shared_p_tma_kernel(
     const double c = fadd(0.0, -r3);
     my_c[lane] = c;
     if (dx != nullptr) {  // _d_x[_i0] += _r6 over this warp's dims (each slot once)
-      int d = f1 - 1;
-      for (; d - (V - 1) >= f0; d -= V) {
-        double a[V];
+      // rows d, d-1, ..., d-K+1: K read-modify-writes in flight together
+      auto rows = [&](auto kc, int d) {
+        constexpr int K = decltype(kc)::value;
+        double a[K];
 #pragma unroll
-        for (int q = 0; q < V; ++q) a[q] = dx[i + (int64_t)(d - q) * ld];
+        for (int q = 0; q < K; ++q) a[q] = dx[i + (int64_t)(d - q) * ld];
 #pragma unroll
-        for (int q = 0; q < V; ++q) {
+        for (int q = 0; q < K; ++q) {
           const int dd = d - q;
           const double u = fsub(buf[dd * 32 + lane], __ldg(p + dd));
           dx[i + (int64_t)dd * ld] = fadd(a[q], fadd(fadd(0.0, fmul(c, u)), fmul(u, c)));
         }
-      }
-      for (; d >= f0; --d) {
-        const double u = fsub(buf[d * 32 + lane], __ldg(p + d));
-        double* a = dx + i + (int64_t)d * ld;
-        *a = fadd(*a, fadd(fadd(0.0, fmul(c, u)), fmul(u, c)));
-      }
+      };
+      int d = f1 - 1;
+      for (; d - (V - 1) >= f0; d -= V) rows(std::integral_constant<int, V>{}, d);
+      // the remainder in batches of 4, 2, 1 (row at a time: a round trip each)
+      if (V > 4 && d - 3 >= f0) { rows(std::integral_constant<int, 4>{}, d); d -= 4; }
+      if (V > 2 && d - 1 >= f0) { rows(std::integral_constant<int, 2>{}, d); d -= 2; }
+      if (d >= f0) rows(std::integral_constant<int, 1>{}, d);
     }
     __syncwarp();  // my_c visible to the warp
     // _d_p[d] += -_r6 of every point of the tile
@@ -836,8 +870,9 @@ __global__ void __launch_bounds__(32 * NW) gaussnd_shared_p_tma_kernel(
     }
     // every warp is done reading buf / its c / tpart before they are refilled
     if (NW > 1) __syncthreads(); else __syncwarp();
-    if (tile + 2 * (int64_t)gridDim.x < ntiles) issue(tile + 2 * (int64_t)gridDim.x, b);
+    issue(tile + 2 * (int64_t)gridDim.x, b);
   }
+  if (ASYNC) asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll
   for (int j = 0; j < JMAX; ++j) {
     const int d = warp * 32 + lane + 32 * NW * j;
@@ -1047,20 +1082,32 @@ int launch_gaussnd_shared_p(int64_t n, int64_t dim, int64_t ld, const double* x,
   // 2.99 / 1.99 / 1.52 / 1.53; with dx 10M x 100 7.48 / 5.10 / 4.75 with
   // 2 / 4 / 8, 27M x 37 5.50 / 4.72 / 6.93, 5M x 200 12.5 / 7.64 / 5.14).
   // K2s sums in the same chunks wherever the TMA form could run (dim <= 256).
-  const int nw = dx ? (dim >= 64 ? 8 : 4) : (dim >= 128 ? 4 : 2);
+  // With dx the chunking is the same in every form (the dx bits do not
+  // depend on the layout); dp only, the cp.async form takes more warps
+  // (measured at odd ld, ms: dim 100 3.56 / 2.84 / 2.99 with 2 / 4 / 8 warps,
+  // dim 200 8.70 / 7.11 / 6.11).
+  const bool aligned = ld % 2 == 0 && ((uintptr_t)x & 15) == 0;
+  const int nw = dx ? (dim >= 64 ? 8 : 4)
+                    : aligned ? (dim >= 128 ? 4 : 2) : (dim >= 128 ? 8 : 4);
   const int dq = dim <= 256 ? (int)((dim + nw - 1) / nw) : (int)dim;
   const size_t tma_smem = (size_t)dim * 64 * sizeof(double) + 64 * 8 * sizeof(double) +
                           2 * sizeof(uint64_t);
-  // The TMA form: x streamed by 2-D tensor loads, NW warps per staged tile,
-  // dx (optional) per point.  Other layouts run K2s.
-  const bool tma = ld % 2 == 0 && ((uintptr_t)x & 15) == 0 && dim <= 256 &&
-                   tma_smem <= 200 * 1024;
+  // The staged-tile form: x streamed by 2-D tensor loads (TMA), or by 8-byte
+  // cp.async copies where a tensor map cannot describe the layout (odd ld, x
+  // not 16-byte aligned), NW warps per staged tile, dx (optional) per point.
+  // Above 256 dims K2s.
+  const bool tma = aligned && dim <= 256 && tma_smem <= 200 * 1024;
   if (full > 0) {
     CUtensorMap tmap;
-    if (tma && make_rows_tmap(&tmap, x, full * 32, dim, ld) == ADC_OK) {
-      auto kt = nw == 8 ? gaussnd_shared_p_tma_kernel<8, 1, 8>
-              : nw == 4 ? gaussnd_shared_p_tma_kernel<8, 2, 4>
-                        : gaussnd_shared_p_tma_kernel<8, 2, 2>;
+    std::memset(&tmap, 0, sizeof(tmap));
+    const bool tmap_ok = tma && make_rows_tmap(&tmap, x, full * 32, dim, ld) == ADC_OK;
+    if (tmap_ok || (dim <= 256 && tma_smem <= 200 * 1024)) {
+      auto kt = nw == 8 ? (tmap_ok ? gaussnd_shared_p_tma_kernel<8, 1, 8>
+                                   : gaussnd_shared_p_tma_kernel<8, 1, 8, true>)
+              : nw == 4 ? (tmap_ok ? gaussnd_shared_p_tma_kernel<8, 2, 4>
+                                   : gaussnd_shared_p_tma_kernel<8, 2, 4, true>)
+                        : (tmap_ok ? gaussnd_shared_p_tma_kernel<8, 2, 2>
+                                   : gaussnd_shared_p_tma_kernel<8, 2, 2, true>);
       if (tma_smem > 48 * 1024)
         ADCB_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)tma_smem));

@@ -670,9 +670,9 @@ def test_gaussnd_shared_p_large_and_refusal(restate):
                                    (256, 1_100), (257, 650)])
 def test_gaussnd_shared_p_with_dx_paths(restate, dim, n):
     """With private dx slots: up to 24 dims K2sr (a thread per point, any
-    layout); above, the aligned layout runs the TMA form (2-D tensor loads of
-    32-point tiles, 4 or 8 warps per tile, ragged tail through K2s, dim <=
-    256) and an odd-offset view of the same points runs K2s.  dx per point
+    layout); up to 256 dims the staged-tile form (4 or 8 warps per 32-point
+    tile, ragged tail through K2s) — the aligned layout with 2-D tensor
+    loads, an odd-offset view with cp.async copies; K2s above.  dx per point
     within 1e-12 of the restatement in both; dp within 1e-12 * sum|terms| of
     the compensated total in both (the paths sum in different fixed orders);
     each path bitwise repeatable."""
