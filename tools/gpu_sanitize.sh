@@ -19,7 +19,7 @@ for tool in ${TOOLS:-memcheck racecheck synccheck initcheck}; do
     python -m pytest tests/test_gpu_parity.py tests/test_gpu_jit.py -q -x -m gpu -k "$sel" -p no:cacheprovider \
     > gpurun_out/sanitize_${tool}_pytest.log 2>&1
   echo "$tool rc=$? $(tail -1 gpurun_out/sanitize_${tool}_pytest.log)"
-  grep -E "ERROR SUMMARY|Invalid|Race|Uninitialized" gpurun_out/sanitize_${tool}.log | sort | uniq -c | head -8
+  grep -E "ERROR SUMMARY|RACECHECK SUMMARY|Invalid|Race|Uninitialized" gpurun_out/sanitize_${tool}.log | sort | uniq -c | head -8
 done
 # the fit's kernels through the host loop
 for tool in racecheck synccheck; do
