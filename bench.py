@@ -746,7 +746,7 @@ def bench_fit(local):
         g = eng.chi2_gradient(h, q0)
     pass_s = (time.perf_counter() - t0) / reps
     rec = {"workload": WORKLOADS["fit"][2], "value": 1.0 / pass_s, "unit": "gradient passes/s",
-           "ms_per_pass": pass_s * 1e3}
+           "ms_per_pass": pass_s * 1e3, "timed_passes": reps}
     # the pass's dominant kernel alone (CUDA events inside the library around
     # the tile kernel), against SURVEY.md §8(d)'s W = 62 per bin (the
     # exp-per-bin algorithm; this kernel runs 16 bins per thread per tile, one
@@ -757,6 +757,7 @@ def bench_fit(local):
     pk = fp64_peak(local)
     achieved = 62.0 * FIT_BINS / (tms * 1e-3) / 1e12
     rec["tile_kernel_ms"] = tms
+    rec["d2h_bytes_per_pass"] = 8 * (4 + 3 * 6) * plan.layout.nchunks  # the chunk records
     rec["roofline"] = {"bound": "fp64", "achieved": achieved, "peak": pk["tinstr_s"],
                        "unit": "T FP64 instr/s", "frac": achieved / pk["tinstr_s"],
                        "hbm_frac": 8.0 * FIT_BINS / (tms * 1e-3) / 1e9 / peaks()["hbm_gbs"],
@@ -961,16 +962,24 @@ def chi2_headline(a, world, rank, local, dist):
     """--workload chi2 / fit: the chi2 pass is the line."""
     import torch
     if a.workload == "fit":
-        rec = bench_fit(local) if rank == 0 else None
+        with ClockSampler(local) as clocks:
+            rec = bench_fit(local) if rank == 0 else None
         if rank != 0:
             return None
         line = common_line(a, world, rec["value"], "gradient passes/s", rec["ms_per_pass"],
                            "weak")
         line.update({"data": "synthetic (numpy Poisson histogram at the gpoly truth, every 100th "
                              "bin 0)", "config": {"workload": rec["workload"], "bins": FIT_BINS},
+                     "roofline": rec.get("roofline"),
                      "cpu_baseline": rec.get("cpu_baseline"), "parity": rec.get("parity"),
                      "fit": {k: rec[k] for k in ("newton_numeric_hessian", "gd_armijo")},
-                     "gpu_launches": None})
+                     "e2e": {"value": rec["value"], "unit": "gradient passes/s",
+                             "h2d_bytes_per_step": 6 * 8,
+                             "d2h_bytes_per_step": rec["d2h_bytes_per_pass"],
+                             "path": "FitEngine.chi2_gradient(h, q): q H2D, graph replay, "
+                                     "gradient + chi2 D2H, host wall clock"},
+                     # per pass: the tile kernel, the empty-bin side pass, the chunk kernel
+                     "gpu_launches": 3 * rec["timed_passes"], "clocks": clocks.summary()})
         return line
     with ClockSampler(local) as clocks:
         rec = bench_chi2(a, world, rank, local, dist, passes=max(a.steps, 1),
@@ -991,7 +1000,8 @@ def chi2_headline(a, world, rank, local, dist):
                 "d2h_bytes_per_step": rec["d2h_bytes_per_pass"],
                 "path": "Chi2Plan.gradient(q): q H2D, graph replay, gradient + chi2 D2H, host "
                         "wall clock (the histogram is resident: it is the plan's state)"},
-        "gpu_launches": 2 * max(a.steps, 1), "clocks": clocks.summary(), "chi2_detail": rec})
+        # per pass: the tile kernel, the empty-bin side pass, the chunk kernel
+        "gpu_launches": 3 * max(a.steps, 1), "clocks": clocks.summary(), "chi2_detail": rec})
     _ = torch
     return line
 
