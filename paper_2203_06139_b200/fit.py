@@ -195,18 +195,28 @@ class Chi2Plan:
 
     def set_provider(self, provider: int):
         """GradientProvider.AdReverse (default) or GradientProvider.Numeric."""
-        check(lib.adc_cuda_chi2_set_provider(self._p, int(provider)))
+        provider = int(provider)
+        if provider != getattr(self, "_provider", None):  # one C call per change
+            check(lib.adc_cuda_chi2_set_provider(self._p, provider))
+            self._provider = provider
+
+    def _params(self, q):
+        # a ctypes array of exactly np doubles (cheaper per call than numpy +
+        # data_as on this per-pass path)
+        if len(q) != self.np:
+            raise AdcError("Arg", f"expected {self.np} parameters, got {len(q)}")
+        return (ctypes.c_double * self.np)(*map(float, q))
 
     def gradient(self, q):
-        g = np.zeros(self.np)
+        qa = self._params(q)
+        g = (ctypes.c_double * self.np)()
         c2 = ctypes.c_double()
-        check(lib.adc_cuda_chi2_gradient(self._p, dbl_array(q), g.ctypes.data_as(
-            ctypes.POINTER(ctypes.c_double)), ctypes.byref(c2)))
-        return g, c2.value
+        check(lib.adc_cuda_chi2_gradient(self._p, qa, g, ctypes.byref(c2)))
+        return np.frombuffer(g, dtype=np.float64).copy(), c2.value
 
     def chi2(self, q) -> float:
         c2 = ctypes.c_double()
-        check(lib.adc_cuda_chi2(self._p, dbl_array(q), ctypes.byref(c2)))
+        check(lib.adc_cuda_chi2(self._p, self._params(q), ctypes.byref(c2)))
         return c2.value
 
     def chi2_multi(self, qs) -> np.ndarray:
