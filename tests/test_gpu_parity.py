@@ -212,6 +212,39 @@ def test_gaussnd_claim_ring_wraps():
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
+def test_gaussnd_claimed_spans_concurrent_threads():
+    # four host threads, each on its own stream with its own buffers, launch
+    # at the same time: each launch takes its own claim pair from the ring, so
+    # every thread's slots equal the single-thread result bit for bit
+    import threading
+    x, p = synth.points_nd(37, 200_001, seed=8)
+    X, P = t(x), t(p)
+    ref = _nd_repeat(0, X, P, 5)
+    out, errs = {}, []
+
+    def work(k):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                dx = torch.zeros_like(X)
+                dp = torch.zeros_like(X)
+                for _ in range(5):
+                    adc.launch_batch("gaussnd_grad_0_1", X, P, 1.1, dx, dp)
+            s.synchronize()
+            out[k] = (host(dx), host(dp))
+        except Exception as e:  # noqa: BLE001
+            errs.append(repr(e))
+
+    ths = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    assert not errs, errs
+    for k in range(4):
+        assert np.array_equal(out[k][0], ref[0]) and np.array_equal(out[k][1], ref[1]), k
+
+
 def test_gaussnd_claimed_spans_in_cuda_graph():
     # a captured launch keeps one claim pair; the kernel resets it, so graph
     # replays accumulate exactly like eager launches
