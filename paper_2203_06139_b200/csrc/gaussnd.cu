@@ -585,10 +585,15 @@ int gaussnd_set_variant(int v) {
 // race_check would flag dp, launch.cpp:217-224): the per-point arithmetic is
 // K2's (same forward sum order, same scalar chain, same reverse order), dx is
 // private (optional), and dp_d = sum_i (-_r6_{d,i}) is reduced in a FIXED
-// order: per 32-point tile a fixed shuffle tree per dim, tiles in order per
-// CTA (a CTA walks tiles b, b + G, ... with G a function of n only), then the
-// CTA partials in order, then dp[d] += total.  No atomics; the same bits on
-// every run and device.
+// order: per thread / tile a fixed order, tiles in order per CTA (a CTA walks
+// tiles b, b + G, ... with G a function of n only), then the CTA partials in
+// order, then dp[d] += total.  No atomics; the same bits on every run and
+// device.  Three forms, by dims and layout (launch_gaussnd_shared_p): K2sr
+// (<= 24 dims, a thread per point), the staged-tile form (<= 256 dims: 2-D
+// TMA tile loads, or cp.async copies where a tensor map cannot describe the
+// layout; 2-8 warps per tile), and K2s below (one warp per tile, LSU loads;
+// above 256 dims and for the < 32-point tail).  With dx, all forms sum a
+// point's forward in the same dim chunks, so dx does not depend on the form.
 constexpr int64_t kSharedPMaxBlocks = 1184;
 constexpr int64_t kSharedPRowsMaxDim = 24;  // K2sr below, the staged-tile forms above
 
@@ -598,8 +603,8 @@ __global__ void __launch_bounds__(32) gaussnd_shared_p_kernel(
     int64_t n, int dim, int64_t ld, double t4, double r1, int dstage,
     double* __restrict__ partials, int dq) {
   // dq: the forward sum runs in chunks of dq dims combined in order, the
-  // grouping of the TMA form's warps, so a point's bits do not depend on
-  // which of the two forms its layout selects (dq >= dim: one chunk)
+  // grouping of the staged-tile form's warps, so a point's bits do not
+  // depend on which form its layout selects (dq >= dim: one chunk)
   extern __shared__ double smem[];
   double* dpart = smem;              // [dim]
   double* stage = smem + dim;        // [dstage][32]
