@@ -267,11 +267,12 @@ __global__ void __launch_bounds__(W * 32 * TPC) gaussnd_tile_kernel(
       if (U > 2 && d - 2 >= d0) { rev_rows<2>(dxi, dpi, ld, d, d0, my_stage, c); d -= 2; }
       if (d > d0) { rev_rows<1>(dxi, dpi, ld, d, d0, my_stage, c); d -= 1; }
     }
-    if (W > 1) __syncthreads();  // tpart is rewritten by the next tile
+    // the next span: one barrier publishes it (and, W > 1, guards tpart,
+    // which the next tile rewrites)
+    if (claim && threadIdx.x == 0) s_claim[(it + 1) & 1] = claim_next(claim);
+    if (W > 1 || claim) __syncthreads();
     if (claim) {
       ++it;
-      if (threadIdx.x == 0) s_claim[it & 1] = claim_next(claim);
-      __syncthreads();
       span = s_claim[it & 1];
     } else {
       span += gridDim.x;
