@@ -1,4 +1,6 @@
-timeout 600 python -m pytest tests -q -m gpu -x -k "shared_p or multirank" 2>&1 | tail -2
-for cfg in "100 10000000" "8 120000000" "16 60000000" "37 27000000" "200 5000000" "2 480000000"; do
-echo "dim/n=$cfg: $(python tools/probe_shared_p.py 5 $cfg 2>&1 | cut -c1-50 | tr '\n' '|')"
-done
+# ncu of the shared-mean staged-tile kernel (dp only and with dx, 10M x 100)
+mkdir -p gpurun_out
+O=gpurun_out
+timeout 600 ncu --set full --clock-control none -k regex:shared_p_tma -s 2 -c 1 -o $O/prof_sp_tma_dx python tools/probe_shared_p.py 3 100 10000000 > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none -k regex:shared_p_tma -s 5 -c 1 -o $O/prof_sp_tma_dp python tools/probe_shared_p.py 3 100 10000000 > /dev/null 2>&1
+python tools/ncu_summary.py $O/prof_sp_tma_*.ncu-rep
