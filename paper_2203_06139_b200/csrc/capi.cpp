@@ -23,6 +23,7 @@ int launch_gaussnd_grad(int64_t n, int64_t dim, int64_t ld, const double* x, con
 int gaussnd_set_variant(int v);
 int64_t gauss_shared_blocks(int64_t n);
 int64_t gaussnd_shared_p_blocks(int64_t n);
+int64_t gaussnd_shared_p_ws_doubles(int64_t n, int64_t dim);
 int launch_gaussnd_shared_p(int64_t n, int64_t dim, int64_t ld, const double* x, const double* p,
                             double sigma, double* dx, double* dp, double* partials,
                             cudaStream_t s);
@@ -599,7 +600,7 @@ extern "C" int adc_cuda_gaussnd_grad_shared_p(int64_t n, int64_t dim, int64_t ld
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (n == 0 || dim == 0) return launch_gaussnd_shared_p(n, dim, ld, x, p, sigma, dx, dp, nullptr, s);
   double* ws = nullptr;
-  ADCB_CUDA(ws_alloc((void**)&ws, (size_t)(gaussnd_shared_p_blocks(n) + 1) * dim * sizeof(double), s));
+  ADCB_CUDA(ws_alloc((void**)&ws, (size_t)gaussnd_shared_p_ws_doubles(n, dim) * sizeof(double), s));
   const int rc = launch_gaussnd_shared_p(n, dim, ld, x, p, sigma, dx, dp, ws, s);
   cudaFreeAsync(ws, s);
   return rc;
@@ -660,7 +661,7 @@ extern "C" int adc_cuda_gaussnd_grad_shared_p_comm(int64_t n, int64_t dim, int64
   ADCB_CUDA(cudaMemsetAsync(part, 0, (size_t)dim * sizeof(double), s));
   int rc = ADC_OK;
   if (n > 0) {
-    ADCB_CUDA(ws_alloc((void**)&ws, (size_t)(gaussnd_shared_p_blocks(n) + 1) * dim * sizeof(double), s));
+    ADCB_CUDA(ws_alloc((void**)&ws, (size_t)gaussnd_shared_p_ws_doubles(n, dim) * sizeof(double), s));
     rc = launch_gaussnd_shared_p(n, dim, ld, x, p, sigma, dx, part, ws, s);
   }
   if (rc == ADC_OK) rc = rank_sum_into(comm, part, dim, dp, s);

@@ -596,6 +596,7 @@ int gaussnd_set_variant(int v) {
 // above 256 dims and for the < 32-point tail).  With dx, all forms sum a
 // point's forward in the same dim chunks, so dx does not depend on the form.
 constexpr int64_t kSharedPMaxBlocks = 1184;
+constexpr int64_t kSharedPSpan = 8;  // tiles per dp partial row (staged-tile form)
 constexpr int64_t kSharedPRowsMaxDim = 24;  // K2sr below, the staged-tile forms above
 
 template <int U, int V>
@@ -746,7 +747,7 @@ template <int V, int JMAX, int NW, bool ASYNC = false>
 __global__ void __launch_bounds__(32 * NW) gaussnd_shared_p_tma_kernel(
     const __grid_constant__ CUtensorMap tmap, const double* __restrict__ x,
     const double* __restrict__ p, double* __restrict__ dx, int64_t ntiles, int dim, int64_t ld,
-    double t4, double r1, double* __restrict__ partials) {
+    double t4, double r1, double* __restrict__ partials, unsigned long long* claim) {
   // NW warps share each staged tile: warp w sums the forward t over dims
   // [w dq, (w+1) dq) (the NW partials combined in warp order), does the dx
   // read-modify-write of those dims, and owns dims w 32 + lane + 32 NW j of
@@ -754,6 +755,7 @@ __global__ void __launch_bounds__(32 * NW) gaussnd_shared_p_tma_kernel(
   // dependent FP64 chains (100 adds of t, 32 of each dp owner) left the warp
   // waiting on fixed latency (ncu: issue active 38%, stall "wait" dominant).
   extern __shared__ __align__(128) double smem[];
+  __shared__ int64_t s_span[2];
   double* buf0 = smem;                              // [dim][32]
   double* buf1 = smem + (size_t)dim * 32;           // [dim][32]
   double* cbuf = smem + (size_t)dim * 64;           // [NW][32]: each warp's copy of c
@@ -804,10 +806,56 @@ __global__ void __launch_bounds__(32 * NW) gaussnd_shared_p_tma_kernel(
   }
   double* my_c = cbuf + warp * 32;
   uint32_t phase[2] = {0u, 0u};
-  int64_t tile = blockIdx.x;
-  issue(tile, 0);
-  issue(tile + gridDim.x, 1);
-  for (int k = 0; tile < ntiles; tile += gridDim.x, ++k) {
+  // Spans of kSharedPSpan consecutive tiles, each summed into its own dp
+  // partial row partials[span] (the grouping is a function of n only, so the
+  // bits do not depend on which CTA takes a span or when).  A CTA takes
+  // spans in order from the claim counter (claim != nullptr: the spans in
+  // flight stay neighbours) or grid-stride; s_span holds its current and
+  // next span, refilled by thread 0 when it moves on (the barriers of the
+  // tiles in between publish it).
+  // SPANS (the cp.async form; measured: odd ld, 5M x 100 with dx 3.14 ->
+  // 2.45 ms, dp only 1.48 -> 1.41): spans of consecutive tiles claimed in
+  // order.  The TMA form keeps one row per CTA over tiles b, b + G, ...
+  // (at any moment the CTAs' tiles are contiguous; with spans of 8
+  // consecutive tiles per CTA its dx path measured slower: 10M x 100
+  // 4.16 -> 5.25 ms).
+  constexpr bool SPANS = ASYNC;
+  const int64_t nspans = (ntiles + kSharedPSpan - 1) / kSharedPSpan;
+  int64_t taken = 0;  // thread 0: spans taken so far (the grid-stride schedule)
+  auto take = [&]() -> int64_t {
+    return claim ? claim_next(claim) : (int64_t)blockIdx.x + (taken++) * gridDim.x;
+  };
+  if (SPANS && threadIdx.x == 0) {
+    s_span[0] = take();
+    s_span[1] = take();
+  }
+  __syncthreads();
+  // tile of a (slot, index) position; past the last tile: ntiles (none).  A
+  // position moves to the other slot only after all kSharedPSpan of this
+  // one (the last, short span runs out into "none"), so the issue position,
+  // two tiles ahead, enters a slot only after thread 0 refilled it.
+  auto tile_of = [&](int slot, int idx) -> int64_t {
+    if (!SPANS) {
+      const int64_t t = (int64_t)blockIdx.x + (int64_t)idx * gridDim.x;
+      return t < ntiles ? t : ntiles;
+    }
+    const int64_t t = s_span[slot] * kSharedPSpan + idx;
+    return s_span[slot] < nspans && t < ntiles ? t : ntiles;
+  };
+  auto advance = [&](int& slot, int& idx) {
+    if (++idx == kSharedPSpan && SPANS) {
+      slot ^= 1;
+      idx = 0;
+    }
+  };
+  int pslot = 0, pidx = 0;  // the tile being computed
+  int islot = 0, iidx = 0;  // the next tile to issue
+  issue(tile_of(islot, iidx), 0);
+  advance(islot, iidx);
+  issue(tile_of(islot, iidx), 1);
+  advance(islot, iidx);
+  int64_t tile = tile_of(pslot, pidx);
+  for (int k = 0; tile < ntiles; ++k) {
     const int b = k & 1;
     double* buf = b ? buf1 : buf0;
     if (ASYNC) {
@@ -884,16 +932,36 @@ __global__ void __launch_bounds__(32 * NW) gaussnd_shared_p_tma_kernel(
         acc[j] = aj;
       }
     }
-    // every warp is done reading buf / its c / tpart before they are refilled
-    if (NW > 1) __syncthreads(); else __syncwarp();
-    issue(tile + 2 * (int64_t)gridDim.x, b);
+    const int64_t span = SPANS ? s_span[pslot] : 0;
+    const bool span_end = SPANS && (pidx == kSharedPSpan - 1 || tile == ntiles - 1);
+    if (span_end) {  // the span's dp partial row; the next span starts from zero
+#pragma unroll
+      for (int j = 0; j < JMAX; ++j) {
+        const int d = warp * 32 + lane + 32 * NW * j;
+        if (d < dim) partials[span * dim + d] = acc[j];
+        acc[j] = 0.0;
+      }
+    }
+    const int old_slot = pslot;
+    advance(pslot, pidx);
+    // every warp is done reading buf / its c / tpart (and this span's slot)
+    // before they are refilled
+    __syncthreads();
+    if (span_end && threadIdx.x == 0 && pslot != old_slot)
+      s_span[old_slot] = take();  // the span after next
+    issue(tile_of(islot, iidx), b);
+    advance(islot, iidx);
+    tile = tile_of(pslot, pidx);
   }
   if (ASYNC) asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if (!SPANS) {  // the CTA's dp partial row
 #pragma unroll
-  for (int j = 0; j < JMAX; ++j) {
-    const int d = warp * 32 + lane + 32 * NW * j;
-    if (d < dim) partials[(int64_t)blockIdx.x * dim + d] = acc[j];
+    for (int j = 0; j < JMAX; ++j) {
+      const int d = warp * 32 + lane + 32 * NW * j;
+      if (d < dim) partials[(int64_t)blockIdx.x * dim + d] = acc[j];
+    }
   }
+  if (claim && threadIdx.x == 0) claim_done(claim);
 }
 
 // K2sr: the shared-mean form for dims <= 24 (DIM at compile time).  A
@@ -995,6 +1063,37 @@ __global__ void gaussnd_shared_p_finish(const double* __restrict__ partials, int
   dp[d] = fadd(dp[d], acc);
 }
 
+// The partial rows in groups of kFinishGroup, each summed in row order into
+// w1[group] (many groups in parallel), then the groups in order into dp.
+constexpr int64_t kFinishGroup = 64;
+
+__global__ void gaussnd_shared_p_finish_groups(const double* __restrict__ partials, int64_t rows,
+                                               int dim, double* __restrict__ w1) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= dim) return;
+  const int64_t groups = (rows + kFinishGroup - 1) / kFinishGroup;
+  for (int64_t g = blockIdx.y; g < groups; g += gridDim.y) {
+    const int64_t r1 = min(rows, (g + 1) * kFinishGroup);
+    double acc = 0.0;
+    for (int64_t r = g * kFinishGroup; r < r1; ++r) acc = fadd(acc, partials[r * dim + d]);
+    w1[g * dim + d] = acc;
+  }
+}
+
+// dp[d] += the fixed two-level sum of rows partial rows; the workspace past
+// the rows (gaussnd_shared_p_ws_doubles) holds the group sums.
+static int shared_p_finish(double* partials, int64_t rows, int64_t dim, double* dp,
+                           cudaStream_t s) {
+  const int64_t groups = (rows + kFinishGroup - 1) / kFinishGroup;
+  double* w1 = partials + rows * dim;
+  const unsigned gx = (unsigned)((dim + 127) / 128);
+  const unsigned gy = (unsigned)std::min<int64_t>(groups, 65535);
+  gaussnd_shared_p_finish_groups<<<dim3(gx, gy), 128, 0, s>>>(partials, rows, (int)dim, w1);
+  gaussnd_shared_p_finish<<<gx, 128, 0, s>>>(w1, groups, (int)dim, dp);
+  ADCB_CUDA(cudaGetLastError());
+  return ADC_OK;
+}
+
 // 2-D tensor map over the SoA rows: inner dimension = points (contiguous),
 // outer = dims (stride ld), box = {32 points, dim rows}.  The driver entry
 // point is fetched through the runtime (no link-time libcuda dependency).
@@ -1047,6 +1146,15 @@ int64_t gaussnd_shared_p_blocks(int64_t n) {
   return std::max<int64_t>(1, std::min<int64_t>((n + 31) / 32, kSharedPMaxBlocks));
 }
 
+// Workspace (doubles) of launch_gaussnd_shared_p: the dp partial rows of any
+// form (CTA rows, or one per span of tiles) plus the tail's row, then the
+// finish's group sums.
+int64_t gaussnd_shared_p_ws_doubles(int64_t n, int64_t dim) {
+  const int64_t spans = (n / 32 + kSharedPSpan - 1) / kSharedPSpan;
+  const int64_t rows = std::max(gaussnd_shared_p_blocks(n), spans) + 1;
+  return (rows + (rows + kFinishGroup - 1) / kFinishGroup) * std::max<int64_t>(dim, 1);
+}
+
 int launch_gaussnd_shared_p(int64_t n, int64_t dim, int64_t ld, const double* x, const double* p,
                             double sigma, double* dx, double* dp, double* partials,
                             cudaStream_t s) {
@@ -1068,9 +1176,7 @@ int launch_gaussnd_shared_p(int64_t n, int64_t dim, int64_t ld, const double* x,
     void* args[] = {(void*)&x, (void*)&p, (void*)&dx, (void*)&n, (void*)&ld, (void*)&t4,
                     (void*)&d_t9, (void*)&partials};
     ADCB_CUDA(cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(256), args, 0, s));
-    gaussnd_shared_p_finish<<<1, 128, 0, s>>>(partials, blocks, (int)dim, dp);
-    ADCB_CUDA(cudaGetLastError());
-    return ADC_OK;
+    return shared_p_finish(partials, blocks, dim, dp, s);
   }
   // stage as many dims of u as fit next to dp's partials (<= 26 KB: 8 CTAs/SM)
   const size_t budget = 26 * 1024 + 1024;
@@ -1113,6 +1219,7 @@ int launch_gaussnd_shared_p(int64_t n, int64_t dim, int64_t ld, const double* x,
   // not 16-byte aligned), NW warps per staged tile, dx (optional) per point.
   // Above 256 dims K2s.
   const bool tma = aligned && dim <= 256 && tma_smem <= 200 * 1024;
+  int64_t rows = blocks;  // dp partial rows before the tail's
   if (full > 0) {
     CUtensorMap tmap;
     std::memset(&tmap, 0, sizeof(tmap));
@@ -1127,8 +1234,20 @@ int launch_gaussnd_shared_p(int64_t n, int64_t dim, int64_t ld, const double* x,
       if (tma_smem > 48 * 1024)
         ADCB_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)tma_smem));
-      kt<<<(unsigned)blocks, 32 * nw, tma_smem, s>>>(tmap, x, p, dx, full, (int)dim, ld, t4, d_t9,
-                                                partials);
+      // TMA form: one dp partial row per CTA (blocks, a function of n only);
+      // cp.async form: one per span of kSharedPSpan tiles, claimed in order
+      int64_t grid = blocks;
+      unsigned long long* claim = nullptr;
+      if (!tmap_ok) {
+        const int64_t nspans = (full + kSharedPSpan - 1) / kSharedPSpan;
+        int occ = 0;
+        ADCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kt, 32 * nw, tma_smem));
+        grid = std::min<int64_t>(nspans, (int64_t)std::max(1, occ) * sm_count());
+        claim = grid < nspans ? claim_slot(s) : nullptr;
+        rows = nspans;
+      }
+      kt<<<(unsigned)grid, 32 * nw, tma_smem, s>>>(tmap, x, p, dx, full, (int)dim, ld, t4, d_t9,
+                                                  partials, claim);
     } else {
       k<<<(unsigned)blocks, 32, smem, s>>>(x, p, dx, full * 32, (int)dim, ld, t4, d_t9, dstage,
                                            partials, dq);
@@ -1138,13 +1257,10 @@ int launch_gaussnd_shared_p(int64_t n, int64_t dim, int64_t ld, const double* x,
   if (rem != 0) {
     const int64_t off = full * 32;
     k<<<1, 32, smem, s>>>(x + off, p, dx ? dx + off : nullptr, rem, (int)dim, ld, t4, d_t9, dstage,
-                          partials + blocks * dim, dq);
+                          partials + rows * dim, dq);
     ADCB_CUDA(cudaGetLastError());
   }
-  gaussnd_shared_p_finish<<<(unsigned)((dim + 127) / 128), 128, 0, s>>>(
-      partials, blocks + (rem != 0 ? 1 : 0), (int)dim, dp);
-  ADCB_CUDA(cudaGetLastError());
-  return ADC_OK;
+  return shared_p_finish(partials, rows + (rem != 0 ? 1 : 0), dim, dp, s);
 }
 
 }  // namespace adcb
